@@ -1,0 +1,54 @@
+"""Plain finite-trace semantics of LTLf, used only to re-check a witness.
+
+``synthesize`` re-validates the formula it returns against this definition
+before handing it to the caller, exactly as the reference does through
+``oracle.separates_by_sat`` (reference ``engine.py:502``, ``oracle.py:27-63``).
+It shares nothing with the CUDA kernels: a position-by-position evaluation
+with the quantifiers of F and U written out.  It runs once per synthesis on a
+single formula and is never part of enumeration.
+"""
+
+from __future__ import annotations
+
+from .formulas import And, Atom, Formula, Future, Next, Not, Or, Until
+from .traces import Specification, Trace
+
+
+def _truth_table(trace: Trace, f: Formula) -> list[bool]:
+    """Truth value of ``f`` at every position of ``trace``."""
+    n = trace.length
+    if isinstance(f, Atom):
+        return [f.index in step for step in trace.steps]
+    if isinstance(f, Not):
+        return [not v for v in _truth_table(trace, f.child)]
+    if isinstance(f, Next):
+        inner = _truth_table(trace, f.child)
+        return [inner[i + 1] if i + 1 < n else False for i in range(n)]
+    if isinstance(f, Future):
+        inner = _truth_table(trace, f.child)
+        return [any(inner[i:]) for i in range(n)]
+    if isinstance(f, (And, Or, Until)):
+        lhs, rhs = _truth_table(trace, f.left), _truth_table(trace, f.right)
+        if isinstance(f, And):
+            return [a and b for a, b in zip(lhs, rhs)]
+        if isinstance(f, Or):
+            return [a or b for a, b in zip(lhs, rhs)]
+        return [any(rhs[k] and all(lhs[i:k]) for k in range(i, n)) for i in range(n)]
+    raise TypeError(f"not a formula node: {f!r}")
+
+
+def sat(trace: Trace, i: int, f: Formula) -> bool:
+    """Does ``f`` hold at position ``i`` of ``trace``?"""
+    if i < 0 or i >= trace.length:
+        raise ValueError(f"position {i} out of range for trace of length {trace.length}")
+    return _truth_table(trace, f)[i]
+
+
+def separates_by_sat(spec: Specification, f: Formula) -> bool:
+    for trace in spec.positives:
+        if not sat(trace, 0, f):
+            return False
+    for trace in spec.negatives:
+        if sat(trace, 0, f):
+            return False
+    return True

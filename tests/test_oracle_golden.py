@@ -1,0 +1,54 @@
+"""Pins the CPU oracle (oracle/ltl_oracle.c) to the unmodified reference.
+
+Every JSON under tests/golden was produced by tests/golden/make_golden.py from
+the reference itself; the oracle must reproduce each level's arrays (sha256 of
+the numpy byte image), counters, separator ids and witness text.
+"""
+
+import pytest
+
+import oracle
+from helpers import assert_level_matches_golden, golden_names, load_golden
+from paper_2504_18943_b200 import to_text, workloads
+
+SLOW = {"spec2_found", "c5_s0_exh10", "c3_s0_exh12"}
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if n not in SLOW])
+def test_oracle_reproduces_reference_levels(name):
+    _check(name)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", sorted(SLOW & set(golden_names())))
+def test_oracle_reproduces_reference_levels_slow(name):
+    _check(name)
+
+
+def _check(name):
+    gold = load_golden(name)
+    spec = workloads.named_workload(gold["workload"], gold["seed"])
+    store = oracle.OracleStore(spec)
+    assert store.trace_count == gold["trace_count"]
+    assert store.dtype.itemsize * 8 == gold["lane_bits"]
+    constructed, found = 0, None
+    for gl in gold["levels"]:
+        n_new, sep, delta, failure = store.expand_level(
+            gl["cost"], gold["operators"], gold["exhaustive"], gold["batch_size"], memory_budget_mb=1 << 20
+        )
+        assert failure is None
+        constructed += delta
+        where = f"{name} cost {gl['cost']}"
+        assert n_new == gl["n"], where
+        assert delta == gl["constructed"], where
+        assert sep == gl["sep_gid"], where
+        assert_level_matches_golden(store.level(gl["cost"]), gl, where)
+        if sep is not None and found is None:
+            found = (sep, gl["cost"])
+    assert constructed == gold["constructed"]
+    assert store.total == gold["unique"]
+    if gold["formula"] is None:
+        assert found is None
+    else:
+        assert found == (gold["found_gid"], gold["found_cost"])
+        assert to_text(oracle.reconstruct(store, found[0]), spec.alphabet) == gold["formula"]
