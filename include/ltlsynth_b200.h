@@ -1,0 +1,150 @@
+/*
+ * ltlsynth_b200.h -- C ABI of the B200 enumeration engine.
+ *
+ * The reference (ltlsynth 0.1.0, pure Python + numpy) has no FFI of its own: its
+ * seam is the Python API of pkg/src/ltlsynth/engine.py.  Each entry point below
+ * states the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/ltlsynth).  INTEGRATION.md shows the ctypes binding a
+ * reference maintainer would add; paper_2504_18943_b200/_native.py is that
+ * binding as shipped here.
+ *
+ * Plain C types only.  All host pointers are caller-owned.  The engine owns all
+ * device memory behind the handle (language cache, hash set, scratch) until
+ * ltlb200_destroy.  One handle is used by one host thread at a time.  There is
+ * no CPU fallback: every entry point fails (NULL / negative status) when no
+ * sm_100 device is usable, and ltlb200_last_error() says why.
+ *
+ * Vocabulary: a CM (characteristic matrix) is T lanes of `lane_bits` bits, one
+ * lane per example trace, bit j of lane t = "the formula holds at position j of
+ * trace t".  Row byte image = the T lanes little-endian, back to back, exactly
+ * numpy's `cms.tobytes()` for the reference's lane dtype.
+ */
+#ifndef LTLSYNTH_B200_H
+#define LTLSYNTH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTLB200_ABI_VERSION 1
+
+/* operator tags == reference engine.py:42 (OP_ATOM..OP_OR) */
+enum {
+    LTLB200_OP_ATOM = 0,
+    LTLB200_OP_NOT = 1,
+    LTLB200_OP_NEXT = 2,
+    LTLB200_OP_FUTURE = 3,
+    LTLB200_OP_AND = 4,
+    LTLB200_OP_UNTIL = 5,
+    LTLB200_OP_OR = 6
+};
+
+/* status of ltlb200_expand_level; 1 and 2 are the reference's two _BudgetExceeded
+ * messages (engine.py:416-417, 443-444), which are outcomes, not errors */
+enum {
+    LTLB200_OK = 0,
+    LTLB200_TIME_BUDGET = 1,
+    LTLB200_MEMORY_BUDGET = 2,
+    LTLB200_ERR_ARGUMENT = -1,
+    LTLB200_ERR_CUDA = -2,
+    LTLB200_ERR_UNSUPPORTED = -3
+};
+
+typedef struct ltlb200_engine ltlb200_engine;
+
+/* counters of one handle since creation */
+typedef struct ltlb200_stats {
+    uint64_t constructed;        /* candidates built, pre-dedup (RunStats.constructed, engine.py:85) */
+    uint64_t unique;             /* stored CMs (RunStats.unique, engine.py:86) */
+    uint64_t kernel_launches;    /* CUDA kernels launched by this handle */
+    double enumerate_ms;         /* device time of the construction+dedup kernels (CUDA events) */
+    double finalize_ms;          /* device time of the per-level compaction kernels */
+    uint64_t enumerate_launches; /* launches of the construction+dedup kernel */
+    uint64_t enumerate_candidates; /* candidates covered by those launches */
+    uint64_t table_slots;        /* hash-set capacity now */
+    uint64_t table_rebuilds;     /* times the hash set was regrown */
+    uint64_t device_bytes;       /* device memory held now */
+    uint64_t h2d_bytes;          /* bytes copied host->device since creation */
+    uint64_t d2h_bytes;          /* bytes copied device->host since creation */
+    uint32_t row_bytes;          /* CM bytes (T * lane_bits / 8) */
+    uint32_t key_bytes;          /* CM bytes as stored in HBM (row_bytes padded to 16) */
+} ltlb200_stats;
+
+/* ABI version of the loaded library (== LTLB200_ABI_VERSION it was built with). */
+int ltlb200_abi_version(void);
+
+/* Last error message of the calling thread ("" when none). */
+const char *ltlb200_last_error(void);
+
+/* Number of usable sm_100 devices; 0 (and an error message) when there is none. */
+int ltlb200_device_count(void);
+
+/*
+ * Replaces CandidateStore.__init__ (engine.py:121-131).
+ *   trace_count, lane_bits (8/16/32/64 = smallest_lane_dtype, traces.py:168)
+ *   masks[T], target[T]   = Layout.masks / Layout.target as uint64 (traces.py:196-199)
+ *   atoms[n_atoms*T]      = atom_bitvectors as uint64, row-major (traces.py:217-230)
+ *   device                = CUDA device ordinal
+ *   hbm_budget_bytes      = cap on device memory held by the handle (0 = 90% of what is free now)
+ *   cuda_stream           = cudaStream_t to launch on, or NULL for an engine-owned stream
+ * Returns NULL on failure.
+ */
+ltlb200_engine *ltlb200_create(int32_t trace_count, int32_t lane_bits, const uint64_t *masks,
+                               const uint64_t *target, const uint64_t *atoms, int32_t n_atoms,
+                               int32_t device, uint64_t hbm_budget_bytes, void *cuda_stream);
+
+/* Frees every device allocation of the handle. */
+void ltlb200_destroy(ltlb200_engine *e);
+
+/*
+ * Replaces expand_level (engine.py:367-451) together with _tasks_for_level (:219-266),
+ * _build_chunk (:269-350) and _first_occurrence_indices (:185-205): builds every
+ * candidate of cost `cost` on the device, keeps the canonical-order-first constructor
+ * of each CM not seen before, appends them as level `cost`.
+ *   cost              must be (number of levels built so far) + 1
+ *   op_mask           bit k set <=> operator tag k enabled (normalize_operators, :52-58)
+ *   exhaustive        EngineConfig.exhaustive (:69)
+ *   batch_size        EngineConfig.batch_size (:67); only the `constructed` counter of the
+ *                     level that holds the separator depends on it
+ *   memory_budget_bytes  EngineConfig.memory_budget_mb << 20, applied to the reference's own
+ *                     estimate (rows + n*(key_words*8+80), :442-444); 0 = unlimited
+ *   deadline_s        absolute CLOCK_MONOTONIC seconds (see ltlb200_now), < 0 = none (:416)
+ * Outputs: *n_new entries appended, *sep_gid id of the level's first fresh separating
+ * entry or -1, *constructed_delta the reference's `stats.constructed` increment.
+ * A level is appended on every status >= 0 (the reference's `finally: flush()`).
+ */
+int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive,
+                         int64_t batch_size, uint64_t memory_budget_bytes, double deadline_s,
+                         int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
+
+/* CLOCK_MONOTONIC now, in seconds (time base of deadline_s). */
+double ltlb200_now(void);
+
+/* _Level.n / _Level.base (engine.py:101-111).  cost is 1-based. */
+int ltlb200_level_info(const ltlb200_engine *e, int32_t cost, int64_t *n, int64_t *base);
+
+/* Number of levels built (len(store.levels)). */
+int32_t ltlb200_num_levels(const ltlb200_engine *e);
+
+/*
+ * Copies _Level.cms / .op / .left / .right (engine.py:103-106) of one level to host
+ * buffers: cms = n * row_bytes bytes (numpy byte image), op = n bytes, left/right = n
+ * int64 each.  Any output pointer may be NULL.  `first`/`count` select a row range.
+ */
+int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t count, uint8_t *cms,
+                       uint8_t *op, int64_t *left, int64_t *right);
+
+/* CandidateStore.entry (engine.py:140-145): provenance of one global id. */
+int ltlb200_entry(ltlb200_engine *e, int64_t gid, int32_t *op, int64_t *left, int64_t *right);
+
+/* approx_bytes of the reference's accounting (engine.py:131,442). */
+uint64_t ltlb200_approx_bytes(const ltlb200_engine *e);
+
+int ltlb200_get_stats(ltlb200_engine *e, ltlb200_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LTLSYNTH_B200_H */

@@ -1,0 +1,119 @@
+"""ctypes binding of the C ABI in ``include/ltlsynth_b200.h``.
+
+This is the binding INTEGRATION.md describes for a reference maintainer: plain
+pointers and sizes, no torch types.  Loading fails loudly -- there is no CPU
+fallback behind it, and the in-tree shared library must have been built with
+``python -c "import __graft_entry__ as g; g.build()"`` (nvcc, sm_100a).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libltlsynth_b200.so"
+
+OK, TIME_BUDGET, MEMORY_BUDGET = 0, 1, 2
+ERR_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED = -1, -2, -3
+ABI_VERSION = 1
+
+# every symbol include/ltlsynth_b200.h declares
+EXPORTED_SYMBOLS = (
+    "ltlb200_abi_version",
+    "ltlb200_last_error",
+    "ltlb200_device_count",
+    "ltlb200_create",
+    "ltlb200_destroy",
+    "ltlb200_expand_level",
+    "ltlb200_now",
+    "ltlb200_level_info",
+    "ltlb200_num_levels",
+    "ltlb200_level_copy",
+    "ltlb200_entry",
+    "ltlb200_approx_bytes",
+    "ltlb200_get_stats",
+)
+
+
+class NativeEngineError(RuntimeError):
+    """The CUDA engine is missing, unusable, or reported an error."""
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("constructed", ctypes.c_uint64),
+        ("unique", ctypes.c_uint64),
+        ("kernel_launches", ctypes.c_uint64),
+        ("enumerate_ms", ctypes.c_double),
+        ("finalize_ms", ctypes.c_double),
+        ("enumerate_launches", ctypes.c_uint64),
+        ("enumerate_candidates", ctypes.c_uint64),
+        ("table_slots", ctypes.c_uint64),
+        ("table_rebuilds", ctypes.c_uint64),
+        ("device_bytes", ctypes.c_uint64),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
+        ("row_bytes", ctypes.c_uint32),
+        ("key_bytes", ctypes.c_uint32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+
+def load():
+    """Load the shared library and declare its prototypes (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeEngineError(
+            f"{LIB_PATH} is missing: build the CUDA engine first (__graft_entry__.build()); "
+            "this package has no CPU fallback"
+        )
+    try:
+        L = ctypes.CDLL(str(LIB_PATH))
+    except OSError as err:
+        raise NativeEngineError(f"cannot load {LIB_PATH}: {err}") from err
+    i32, i64, u32, u64, p, dbl = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64,
+                                  ctypes.c_void_p, ctypes.c_double)
+    L.ltlb200_abi_version.restype = ctypes.c_int
+    L.ltlb200_last_error.restype = ctypes.c_char_p
+    L.ltlb200_device_count.restype = ctypes.c_int
+    L.ltlb200_create.restype = p
+    L.ltlb200_create.argtypes = [i32, i32, p, p, p, i32, i32, u64, p]
+    L.ltlb200_destroy.argtypes = [p]
+    L.ltlb200_destroy.restype = None
+    L.ltlb200_expand_level.restype = ctypes.c_int
+    L.ltlb200_expand_level.argtypes = [p, i32, u32, i32, i64, u64, dbl,
+                                       ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.ltlb200_now.restype = dbl
+    L.ltlb200_level_info.restype = ctypes.c_int
+    L.ltlb200_level_info.argtypes = [p, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.ltlb200_num_levels.restype = i32
+    L.ltlb200_num_levels.argtypes = [p]
+    L.ltlb200_level_copy.restype = ctypes.c_int
+    L.ltlb200_level_copy.argtypes = [p, i32, i64, i64, p, p, p, p]
+    L.ltlb200_entry.restype = ctypes.c_int
+    L.ltlb200_entry.argtypes = [p, i64, ctypes.POINTER(i32), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.ltlb200_approx_bytes.restype = u64
+    L.ltlb200_approx_bytes.argtypes = [p]
+    L.ltlb200_get_stats.restype = ctypes.c_int
+    L.ltlb200_get_stats.argtypes = [p, ctypes.POINTER(Stats)]
+    if L.ltlb200_abi_version() != ABI_VERSION:
+        raise NativeEngineError("libltlsynth_b200.so was built from a different header version; rebuild it")
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().ltlb200_last_error().decode("utf-8", "replace")
+
+
+def check(status: int, what: str) -> int:
+    if status < 0:
+        raise NativeEngineError(f"{what} failed (status {status}): {last_error()}")
+    return status

@@ -1,0 +1,814 @@
+// engine.cu -- host side of the B200 enumeration engine and its C ABI (include/ltlsynth_b200.h).
+//
+// Owns the HBM-resident language cache (all finalised CMs by global id + the ordinal
+// each entry won with), the dedup hash set and the per-level scratch, and drives one
+// cost level per ltlb200_expand_level call:
+//
+//   plan      canonical block list of the level (reference _tasks_for_level,
+//             engine.py:219-266, minus its batch chunking) -> ordinal offsets, tiles
+//   enumerate one persistent launch of the construction+dedup kernel (narrow.cuh / wide.cuh)
+//   finalise  bitmap-rank compaction: winners ordered by ordinal, appended to the cache
+//   account   `constructed` as the reference counts it, including its chunk rounding on
+//             the level that holds the separator (engine.py:418,445-446)
+//
+// No CPU fallback exists: without a usable sm_100 device every entry point fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <ctime>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ltlsynth_b200.h"
+#include "narrow.cuh"
+
+namespace ltlb200 {
+
+static thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct MemoryBudget : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CUDA_CHECK(expr)                                                                              \
+    do {                                                                                              \
+        cudaError_t err__ = (expr);                                                                   \
+        if (err__ != cudaSuccess)                                                                     \
+            throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(err__) + " (" __FILE__ ":" + \
+                            std::to_string(__LINE__) + ")");                                          \
+    } while (0)
+
+static double monotonic_s() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+static u64 next_pow2(u64 x) {
+    u64 p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// ---- small device kernels shared by both key widths --------------------------------
+
+// exclusive scan of per-superblock popcounts, 1024 values per CTA; block totals go to `sums`
+__global__ void __launch_bounds__(1024) sb_scan_kernel(const uint32_t *bitmap, u64 n_words, const uint32_t *in,
+                                                      uint32_t *out, u64 n, uint32_t *sums) {
+    __shared__ uint32_t warp_tot[32];
+    const u64 i = (u64)blockIdx.x * 1024 + threadIdx.x;
+    uint32_t v = 0;
+    if (i < n) {
+        if (bitmap) {  // first level: popcount of the 32 words of superblock i
+            const u64 w0 = i << 5;
+#pragma unroll 4
+            for (int k = 0; k < 32; ++k)
+                if (w0 + k < n_words) v += __popc(bitmap[w0 + k]);
+        } else {
+            v = in[i];
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = warp_tot[lane], wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+            if (lane >= d) wi += t;
+        }
+        warp_tot[lane] = wi - w;  // exclusive prefix of warp totals
+        if (lane == 31 && sums) sums[blockIdx.x] = wi;
+    }
+    __syncthreads();
+    if (i < n) out[i] = warp_tot[warp] + incl - v;
+}
+
+__global__ void __launch_bounds__(1024) sb_add_kernel(uint32_t *out, u64 n, const uint32_t *block_prefix) {
+    const u64 i = (u64)blockIdx.x * 1024 + threadIdx.x;
+    if (i < n) out[i] += block_prefix[blockIdx.x];
+}
+
+// counters[5] = number of winners, counters[6] = rank of the separator's ordinal
+__global__ void level_summary_kernel(const uint32_t *bitmap, const uint32_t *sb_rank, u64 n_bits, u64 sep_ord,
+                                     u64 *counters) {
+    counters[5] = n_bits ? ordinal_rank(bitmap, sb_rank, n_bits - 1) + ((bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u) : 0;
+    counters[6] = sep_ord < n_bits ? ordinal_rank(bitmap, sb_rank, sep_ord) : ~0ull;
+}
+
+// ---- host-side level bookkeeping ------------------------------------------------------
+
+struct LevelMeta {
+    u64 n = 0, base = 0;
+    std::vector<BlockDesc> blocks;
+};
+
+template <typename T>
+struct DeviceArray {
+    T *ptr = nullptr;
+    u64 cap = 0;  // elements
+};
+
+class Engine {
+public:
+    Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *target, const uint64_t *atoms, int n_atoms,
+           int device, u64 budget, void *stream);
+    ~Engine();
+
+    int expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
+                     int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
+    int level_info(int cost, int64_t *n, int64_t *base) const;
+    int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
+    int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
+    void get_stats(ltlb200_stats *out);
+    int num_levels() const { return (int)levels_.size(); }
+    u64 approx_bytes() const { return approx_bytes_; }
+
+private:
+    // geometry
+    int T_, lw_, row_bytes_, key_words_, n_atoms_;
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    bool own_stream_ = false;
+    u64 budget_ = 0, held_ = 0;
+    uint4 valid_{}, target_{};
+    bool special_possible_ = false;
+
+    // device state
+    uint4 *d_atoms_ = nullptr;
+    DeviceArray<uint4> store_;
+    DeviceArray<u64> ords_;
+    DeviceArray<Slot16> slots_;
+    DeviceArray<uint32_t> new_list_;
+    DeviceArray<uint32_t> bitmap_;
+    DeviceArray<uint32_t> sb_rank_;
+    DeviceArray<uint32_t> scan_tmp_;
+    u64 *d_counters_ = nullptr;
+    BlockDesc *d_blocks_ = nullptr;
+    static constexpr int kMaxBlocks = 512;
+    u64 *h_counters_ = nullptr;  // pinned
+    cudaEvent_t ev_[4] = {};
+    bool table_dirty_ = false;
+
+    std::vector<LevelMeta> levels_;
+    u64 total_ = 0, approx_bytes_ = 0, last_constructed_ = 0;
+    int occupancy_ = 2;
+    ltlb200_stats st_{};
+    int sm_count_ = 148;
+
+    template <typename T>
+    void reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems = 0);
+    template <typename T>
+    void release(DeviceArray<T> &a);
+    void plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &constructed, u64 &n_tiles);
+    void rebuild_table(u64 slots);
+    void read_counters();
+    void decode(const LevelMeta &lv, u64 ord, int32_t *op, int64_t *left, int64_t *right) const;
+    u64 constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) const;
+    void launch_enumerate(const NarrowParams &P, int grid);
+};
+
+template <typename T>
+void Engine::release(DeviceArray<T> &a) {
+    if (a.ptr) {
+        cudaFree(a.ptr);
+        held_ -= a.cap * sizeof(T);
+    }
+    a.ptr = nullptr;
+    a.cap = 0;
+}
+
+// grow `a` to at least `want` elements; with keep, the first keep_elems survive
+template <typename T>
+void Engine::reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems) {
+    if (want <= a.cap) return;
+    u64 cap = keep ? std::max(want, a.cap + a.cap / 2) : want;
+    u64 extra_needed = cap * sizeof(T) - (keep ? 0 : a.cap * sizeof(T));
+    if (held_ + extra_needed > budget_) {
+        cap = want;  // retry without head-room
+        extra_needed = cap * sizeof(T) - (keep ? 0 : a.cap * sizeof(T));
+        if (held_ + extra_needed > budget_) throw MemoryBudget("device memory budget exhausted");
+    }
+    if (!keep) release(a);
+    T *p = nullptr;
+    cudaError_t err = cudaMalloc(&p, cap * sizeof(T));
+    if (err != cudaSuccess) {
+        cudaGetLastError();
+        throw MemoryBudget(std::string("cudaMalloc failed: ") + cudaGetErrorString(err));
+    }
+    held_ += cap * sizeof(T);
+    if (keep && a.ptr) {
+        if (keep_elems) CUDA_CHECK(cudaMemcpyAsync(p, a.ptr, keep_elems * sizeof(T), cudaMemcpyDeviceToDevice, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        cudaFree(a.ptr);
+        held_ -= a.cap * sizeof(T);
+    }
+    a.ptr = p;
+    a.cap = cap;
+}
+
+static uint4 pack_lanes16(const uint64_t *lanes, int T, int lane_bits) {
+    uint8_t bytes[16] = {0};
+    const int lb = lane_bits / 8;
+    for (int t = 0; t < T; ++t) memcpy(bytes + t * lb, &lanes[t], lb);
+    uint4 v;
+    memcpy(&v, bytes, 16);
+    return v;
+}
+
+Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *target, const uint64_t *atoms, int n_atoms,
+               int device, u64 budget, void *stream)
+    : T_(T), lw_(lane_bits), row_bytes_(T * lane_bits / 8), key_words_((T * lane_bits / 8 + 7) / 8), n_atoms_(n_atoms),
+      device_(device) {
+    CUDA_CHECK(cudaSetDevice(device_));
+    cudaDeviceProp prop;
+    CUDA_CHECK(cudaGetDeviceProperties(&prop, device_));
+    if (prop.major != 10) throw CudaError("device is not sm_100 (Blackwell B200); this library has no other code path");
+    sm_count_ = prop.multiProcessorCount;
+    if (row_bytes_ > 16) throw std::invalid_argument("CMs wider than 16 bytes are not supported by this build");
+    if (stream) stream_ = (cudaStream_t)stream;
+    else {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        own_stream_ = true;
+    }
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    budget_ = budget ? budget : (u64)(free_b * 0.9);
+    valid_ = pack_lanes16(masks, T, lane_bits);
+    target_ = pack_lanes16(target, T, lane_bits);
+    // the all-ones vector doubles as the empty-slot marker; it is a legal CM only when
+    // the row fills the vector and every lane is fully valid
+    special_possible_ = (valid_.x & valid_.y & valid_.z & valid_.w) == 0xFFFFFFFFu;
+
+    std::vector<uint4> h_atoms(std::max(n_atoms, 1));
+    for (int p = 0; p < n_atoms; ++p) h_atoms[p] = pack_lanes16(atoms + (size_t)p * T, T, lane_bits);
+    CUDA_CHECK(cudaMalloc(&d_atoms_, h_atoms.size() * sizeof(uint4)));
+    CUDA_CHECK(cudaMemcpyAsync(d_atoms_, h_atoms.data(), h_atoms.size() * sizeof(uint4), cudaMemcpyHostToDevice, stream_));
+    st_.h2d_bytes += h_atoms.size() * sizeof(uint4);
+    CUDA_CHECK(cudaMalloc(&d_counters_, CTR_COUNT * sizeof(u64)));
+    CUDA_CHECK(cudaMalloc(&d_blocks_, kMaxBlocks * sizeof(BlockDesc)));
+    CUDA_CHECK(cudaMallocHost(&h_counters_, CTR_COUNT * sizeof(u64)));
+    for (auto &e : ev_) CUDA_CHECK(cudaEventCreate(&e));
+    u64 init[CTR_COUNT];
+    for (auto &c : init) c = 0;
+    init[CTR_SPECIAL] = VAL_EMPTY;
+    CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    held_ += h_atoms.size() * sizeof(uint4) + CTR_COUNT * sizeof(u64) + kMaxBlocks * sizeof(BlockDesc);
+    {
+        int occ = 0;
+        cudaError_t err = cudaSuccess;
+        switch (lw_) {
+            case 8: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<8>, CTA_THREADS, 0); break;
+            case 16: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<16>, CTA_THREADS, 0); break;
+            case 32: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<32>, CTA_THREADS, 0); break;
+            default: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<64>, CTA_THREADS, 0); break;
+        }
+        CUDA_CHECK(err);
+        occupancy_ = std::max(occ, 1);
+    }
+    rebuild_table(1 << 12);
+    st_.row_bytes = row_bytes_;
+    st_.key_bytes = 16;
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    release(store_);
+    release(ords_);
+    release(slots_);
+    release(new_list_);
+    release(bitmap_);
+    release(sb_rank_);
+    release(scan_tmp_);
+    cudaFree(d_atoms_);
+    cudaFree(d_counters_);
+    cudaFree(d_blocks_);
+    cudaFreeHost(h_counters_);
+    for (auto &e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+// Fresh table of `slots` entries holding every finalised CM (val = global id).
+void Engine::rebuild_table(u64 slots) {
+    slots = std::max<u64>(next_pow2(slots), 1 << 12);
+    if (slots > (1ull << 32) - 2) throw MemoryBudget("hash set would exceed 2^32 slots");
+    if (slots != slots_.cap) {
+        release(slots_);
+        reserve(slots_, slots, false);
+    }
+    CUDA_CHECK(cudaMemsetAsync(slots_.ptr, 0xFF, slots_.cap * sizeof(Slot16), stream_));
+    u64 special = VAL_EMPTY;
+    CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SPECIAL, &special, sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    if (total_) {
+        int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
+        narrow_rebuild_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, store_.ptr, 0, total_, d_counters_);
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+    }
+    table_dirty_ = false;
+    st_.table_rebuilds++;
+}
+
+void Engine::read_counters() {
+    CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += CTR_COUNT * sizeof(u64);
+}
+
+// Canonical block order of one level (reference engine.py:219-266 without the chunking).
+void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &constructed, u64 &n_tiles) {
+    constructed = 0;
+    n_tiles = 0;
+    auto push = [&](BlockDesc b) {
+        if (b.size == 0) return;
+        b.ord0 = constructed;
+        b.tile0 = n_tiles;
+        constructed += b.size;
+        n_tiles += b.tiles_v * b.tiles_s;
+        lv.blocks.push_back(b);
+    };
+    auto ceil_div = [](u64 a, u64 b) { return (a + b - 1) / b; };
+    if (cost == 1) {
+        BlockDesc b{};
+        b.op = OP_ATOM;
+        b.kind = BK_UNARY;
+        b.from_atoms = 1;
+        b.na = (u64)n_atoms_;
+        b.size = b.na;
+        b.tiles_v = ceil_div(b.na, (u64)CTA_THREADS * UNARY_ITEMS);
+        b.tiles_s = 1;
+        push(b);
+        return;
+    }
+    const LevelMeta &prev = levels_[cost - 2];
+    static const int unary_tags[3] = {OP_NOT, OP_NEXT, OP_FUTURE};
+    static const int binary_tags[3] = {OP_AND, OP_UNTIL, OP_OR};
+    for (int tag : unary_tags) {
+        if (!(op_mask >> tag & 1u) || prev.n == 0) continue;
+        BlockDesc b{};
+        b.op = (uint32_t)tag;
+        b.kind = BK_UNARY;
+        b.a_off = prev.base;
+        b.na = prev.n;
+        b.size = prev.n;
+        b.tiles_v = ceil_div(b.na, (u64)CTA_THREADS * UNARY_ITEMS);
+        b.tiles_s = 1;
+        push(b);
+    }
+    for (int tag : binary_tags) {
+        if (!(op_mask >> tag & 1u)) continue;
+        const bool commutative = tag == OP_AND || tag == OP_OR;
+        for (int c1 = 1; c1 < cost - 1; ++c1) {
+            const int c2 = cost - 1 - c1;
+            if (commutative && c1 > c2) break;
+            const LevelMeta &la = levels_[c1 - 1], &lb = levels_[c2 - 1];
+            if (la.n == 0 || lb.n == 0) continue;
+            BlockDesc b{};
+            b.op = (uint32_t)tag;
+            b.a_off = la.base;
+            b.na = la.n;
+            b.b_off = lb.base;
+            b.nb = lb.n;
+            if (commutative && c1 == c2) {
+                b.kind = BK_TRI;
+                b.vec_is_b = 1;
+                b.size = la.n * (la.n + 1) / 2;
+            } else {
+                b.kind = BK_RECT;
+                b.vec_is_b = lb.n >= la.n;
+                b.size = la.n * lb.n;
+            }
+            const u64 n_vec = b.vec_is_b ? b.nb : b.na, n_sc = b.vec_is_b ? b.na : b.nb;
+            b.tiles_v = ceil_div(n_vec, CTA_THREADS);
+            b.tiles_s = ceil_div(n_sc, TILE_S);
+            push(b);
+        }
+    }
+    if ((int)lv.blocks.size() > kMaxBlocks) throw std::invalid_argument("too many operand blocks in one level");
+}
+
+// ordinal (within a triangle block over n rows) of the first pair of row i: sum of the row lengths n, n-1, ...
+static u64 tri_row_start(u64 n, u64 i) { return i * n - (i ? (i * (i - 1)) / 2 : 0); }
+
+// provenance of an entry from the ordinal it won with (engine.py:274-327)
+void Engine::decode(const LevelMeta &lv, u64 ord, int32_t *op, int64_t *left, int64_t *right) const {
+    size_t bi = 0;
+    while (bi + 1 < lv.blocks.size() && ord >= lv.blocks[bi + 1].ord0) ++bi;
+    const BlockDesc &b = lv.blocks[bi];
+    const u64 k = ord - b.ord0;
+    *op = (int32_t)b.op;
+    if (b.kind == BK_UNARY) {
+        *left = (int64_t)(b.from_atoms ? k : b.a_off + k);
+        *right = -1;
+    } else if (b.kind == BK_RECT) {
+        *left = (int64_t)(b.a_off + k / b.nb);
+        *right = (int64_t)(b.b_off + k % b.nb);
+    } else {
+        // row i of the triangle starts at i*n - i(i-1)/2; invert with a float guess + exact fix-up
+        const u64 n = b.na;
+        long double fn = (long double)(2 * n + 1);
+        long double disc = fn * fn - 8.0L * (long double)k;
+        u64 i = (u64)((fn - sqrtl(disc > 0 ? disc : 0)) / 2.0L);
+        if (i >= n) i = n - 1;
+        while (i > 0 && tri_row_start(n, i) > k) --i;
+        while (i + 1 < n && tri_row_start(n, i + 1) <= k) ++i;
+        const u64 j = i + (k - tri_row_start(n, i));
+        *left = (int64_t)(b.a_off + i);
+        *right = (int64_t)(b.a_off + j);
+    }
+}
+
+// `stats.constructed` increment of a level cut short at the separator: the reference
+// adds whole chunks (engine.py:418) and stops after the separator's chunk (:445-446),
+// so the count is "everything up to the end of the chunk that holds sep_ord" under the
+// chunk schedule of _tasks_for_level (:219-266) for this batch size.
+u64 Engine::constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) const {
+    size_t bi = 0;
+    while (bi + 1 < lv.blocks.size() && sep_ord >= lv.blocks[bi + 1].ord0) ++bi;
+    const BlockDesc &b = lv.blocks[bi];
+    const u64 k = sep_ord - b.ord0;
+    u64 end;  // candidates of this block covered by chunks up to the separator's
+    if (b.kind == BK_UNARY) {
+        end = b.from_atoms ? b.size : std::min(b.size, (k / batch + 1) * batch);
+    } else if (b.kind == BK_RECT) {
+        const u64 rows = batch / b.nb, i = k / b.nb, j = k % b.nb;
+        if (rows >= 1) end = std::min(b.na, (i / rows + 1) * rows) * b.nb;
+        else end = i * b.nb + std::min(b.nb, (j / batch + 1) * batch);
+    } else {
+        const u64 n = b.na;
+        int32_t op;
+        int64_t l, r;
+        decode(lv, sep_ord, &op, &l, &r);
+        const u64 i = (u64)l - b.a_off, j = (u64)r - b.a_off;
+        if (n - i > batch) {  // a long row is split over j on its own (trij chunks)
+            end = tri_row_start(n, i) + std::min(n - i, ((j - i) / batch + 1) * batch);
+        } else {  // greedy groups of whole rows with at most `batch` pairs
+            u64 i0 = n > batch ? n - batch : 0;
+            for (;;) {
+                u64 pairs = 0, i1 = i0;
+                while (i1 < n && pairs + (n - i1) <= batch) {
+                    pairs += n - i1;
+                    ++i1;
+                }
+                if (i < i1) {
+                    end = i1 < n ? tri_row_start(n, i1) : b.size;
+                    break;
+                }
+                i0 = i1;
+            }
+        }
+    }
+    return b.ord0 + end;
+}
+
+void Engine::launch_enumerate(const NarrowParams &P, int grid) {
+    switch (lw_) {
+        case 8: narrow_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+        case 16: narrow_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+        case 32: narrow_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+        default: narrow_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+    }
+    CUDA_CHECK(cudaGetLastError());
+    st_.kernel_launches++;
+    st_.enumerate_launches++;
+}
+
+int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
+                         int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
+    if (cost != (int)levels_.size() + 1 || batch < 1) throw std::invalid_argument("cost must be the next unbuilt level and batch_size >= 1");
+    CUDA_CHECK(cudaSetDevice(device_));
+    *n_new = 0;
+    *sep_gid = -1;
+    *constructed_delta = 0;
+    LevelMeta lv;
+    lv.base = total_;
+    if (deadline >= 0 && monotonic_s() > deadline) {  // engine.py:416-417, before the first chunk
+        levels_.push_back(lv);
+        return LTLB200_TIME_BUDGET;
+    }
+    u64 constructed = 0, n_tiles = 0;
+    plan_level(cost, op_mask, lv, constructed, n_tiles);
+    if (constructed == 0) {
+        levels_.push_back(lv);
+        return LTLB200_OK;
+    }
+    u64 n_claimed = 0, sep_ord = VAL_EMPTY;
+    try {
+        if (table_dirty_) rebuild_table(slots_.cap);
+        CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
+        st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
+
+        // expected number of new CMs: everything for small levels, else the previous level's
+        // uniqueness with head-room; a wrong guess trips the overflow flag and the level is redone
+        const u64 kExact = 1ull << 22, kSlack = 1ull << 21;
+        u64 est = constructed;
+        if (constructed > kExact) {
+            double u = 1.0;
+            if (levels_.size() >= 2 && last_constructed_ > 0) u = std::min(1.0, 1.5 * (double)levels_.back().n / (double)last_constructed_ + 0.02);
+            est = std::min(constructed, std::max(kExact, (u64)(u * (double)constructed)));
+        }
+        for (int attempt = 0;; ++attempt) {
+            const bool exact = est >= constructed;
+            const u64 want_slots = next_pow2(2 * (total_ + est + (exact ? 0 : kSlack)));
+            if (want_slots > slots_.cap) rebuild_table(want_slots);
+            reserve(new_list_, est + (exact ? 64 : kSlack), false);
+            u64 init[CTR_COUNT] = {0, 0, VAL_EMPTY, 0, 0, 0, 0, 0};
+            // the special-key register (CTR_SPECIAL) persists across levels
+            CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, 3 * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+            CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_OVERFLOW, init + CTR_OVERFLOW, 4 * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+            NarrowParams P{};
+            P.store = store_.ptr;
+            P.atoms = d_atoms_;
+            P.slots = slots_.ptr;
+            P.slot_mask = slots_.cap - 1;
+            P.new_list = new_list_.ptr;
+            P.new_list_cap = new_list_.cap;
+            P.counters = d_counters_;
+            P.blocks = d_blocks_;
+            P.n_blocks = (int)lv.blocks.size();
+            P.n_tiles = n_tiles;
+            P.valid = valid_;
+            P.target = target_;
+            P.prune_after_sep = exhaustive ? 0 : 1;
+            P.special_possible = special_possible_ ? 1 : 0;
+            P.claim_limit = exact ? ~0ull : est;
+            const int grid = (int)std::min<u64>(n_tiles, (u64)sm_count_ * occupancy_);
+            CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+            launch_enumerate(P, grid);
+            CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+            read_counters();
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+            st_.enumerate_ms += ms;
+            st_.enumerate_candidates += constructed;
+            if (h_counters_[CTR_OVERFLOW] == 0) break;
+            if (exact || attempt > 8) throw CudaError("hash set overflow on an exactly sized table");
+            est = std::min(constructed, est * 4);
+            rebuild_table(next_pow2(2 * (total_ + est + kSlack)));  // drops this attempt's claims
+        }
+        n_claimed = h_counters_[CTR_CLAIMED];
+        sep_ord = h_counters_[CTR_SEP];
+
+        // ---- finalise: rank winners by ordinal, append to the cache
+        const bool cut = !exhaustive && sep_ord != VAL_EMPTY;
+        const u64 n_bits = cut ? sep_ord + 1 : constructed;
+        const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
+        reserve(bitmap_, n_words + 1, false);
+        reserve(sb_rank_, n_sb + 1, false);
+        reserve(store_, total_ + n_claimed, true, total_);
+        reserve(ords_, total_ + n_claimed, true, total_);
+        CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
+        CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+        FinalizeParams F{};
+        F.slots = slots_.ptr;
+        F.new_list = new_list_.ptr;
+        F.n_claimed = n_claimed;
+        F.counters = d_counters_;
+        F.bitmap = bitmap_.ptr;
+        F.sb_rank = sb_rank_.ptr;
+        F.ord_limit = cut ? sep_ord : VAL_EMPTY - 1;
+        F.store = store_.ptr;
+        F.ords = ords_.ptr;
+        F.base = total_;
+        const int fgrid = (int)std::max<u64>(1, std::min<u64>((n_claimed + 255) / 256, (u64)sm_count_ * 16));
+        narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        CUDA_CHECK(cudaGetLastError());
+        // popcount prefix per superblock: up to three scan levels of 1024
+        {
+            const u64 nb1 = (n_sb + 1023) / 1024;
+            reserve(scan_tmp_, 2 * (nb1 + 1024) + 2048, false);
+            uint32_t *sums1 = scan_tmp_.ptr, *pre1 = sums1 + nb1 + 8;
+            sb_scan_kernel<<<(unsigned)nb1, 1024, 0, stream_>>>(bitmap_.ptr, n_words, nullptr, sb_rank_.ptr, n_sb, sums1);
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+            if (nb1 > 1) {
+                const u64 nb2 = (nb1 + 1023) / 1024;
+                uint32_t *sums2 = pre1 + nb1 + 8, *pre2 = sums2 + nb2 + 8;
+                sb_scan_kernel<<<(unsigned)nb2, 1024, 0, stream_>>>(nullptr, 0, sums1, pre1, nb1, sums2);
+                if (nb2 > 1) {
+                    if (nb2 > 1024) throw std::invalid_argument("level too large for the rank scan");
+                    sb_scan_kernel<<<1, 1024, 0, stream_>>>(nullptr, 0, sums2, pre2, nb2, nullptr);
+                    sb_add_kernel<<<(unsigned)nb2, 1024, 0, stream_>>>(pre1, nb1, pre2);
+                    st_.kernel_launches += 2;
+                }
+                sb_add_kernel<<<(unsigned)nb1, 1024, 0, stream_>>>(sb_rank_.ptr, n_sb, pre1);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches += 2;
+            }
+        }
+        level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, sep_ord, d_counters_);
+        narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        CUDA_CHECK(cudaGetLastError());
+        CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
+        st_.kernel_launches += 3;
+        read_counters();
+        float fms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&fms, ev_[2], ev_[3]));
+        st_.finalize_ms += fms;
+        lv.n = h_counters_[5];
+        if (sep_ord != VAL_EMPTY) *sep_gid = (int64_t)(total_ + h_counters_[6]);
+        if (cut) table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
+    } catch (const MemoryBudget &e) {
+        g_last_error = e.what();
+        table_dirty_ = true;
+        levels_.push_back(LevelMeta{0, total_, {}});
+        return LTLB200_MEMORY_BUDGET;
+    }
+    const bool found_cut = !exhaustive && sep_ord != VAL_EMPTY;
+    *constructed_delta = (int64_t)(found_cut ? constructed_through(lv, sep_ord, (u64)batch) : constructed);
+    last_constructed_ = constructed;
+    *n_new = (int64_t)lv.n;
+    total_ += lv.n;
+    st_.constructed += (u64)*constructed_delta;
+    st_.unique = total_;
+    approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
+    levels_.push_back(std::move(lv));
+    if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
+    return LTLB200_OK;
+}
+
+int Engine::level_info(int cost, int64_t *n, int64_t *base) const {
+    if (cost < 1 || cost > (int)levels_.size()) return LTLB200_ERR_ARGUMENT;
+    *n = (int64_t)levels_[cost - 1].n;
+    *base = (int64_t)levels_[cost - 1].base;
+    return LTLB200_OK;
+}
+
+int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right) {
+    if (cost < 1 || cost > (int)levels_.size()) return LTLB200_ERR_ARGUMENT;
+    const LevelMeta &lv = levels_[cost - 1];
+    if (first < 0 || count < 0 || (u64)(first + count) > lv.n) return LTLB200_ERR_ARGUMENT;
+    if (count == 0) return LTLB200_OK;
+    CUDA_CHECK(cudaSetDevice(device_));
+    const u64 g0 = lv.base + (u64)first;
+    if (cms) {
+        std::vector<uint4> rows((size_t)count);
+        CUDA_CHECK(cudaMemcpyAsync(rows.data(), store_.ptr + g0, (size_t)count * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        st_.d2h_bytes += (u64)count * sizeof(uint4);
+        for (int64_t k = 0; k < count; ++k) memcpy(cms + (size_t)k * row_bytes_, &rows[(size_t)k], (size_t)row_bytes_);
+    }
+    if (op || left || right) {
+        std::vector<u64> ords((size_t)count);
+        CUDA_CHECK(cudaMemcpyAsync(ords.data(), ords_.ptr + g0, (size_t)count * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        st_.d2h_bytes += (u64)count * sizeof(u64);
+        for (int64_t k = 0; k < count; ++k) {
+            int32_t o;
+            int64_t l, r;
+            decode(lv, ords[(size_t)k], &o, &l, &r);
+            if (op) op[k] = (uint8_t)o;
+            if (left) left[k] = l;
+            if (right) right[k] = r;
+        }
+    }
+    return LTLB200_OK;
+}
+
+int Engine::entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
+    if (gid < 0 || (u64)gid >= total_) return LTLB200_ERR_ARGUMENT;
+    size_t li = 0;
+    while (li + 1 < levels_.size() && (u64)gid >= levels_[li + 1].base) ++li;
+    while (levels_[li].n == 0 || (u64)gid < levels_[li].base) --li;
+    CUDA_CHECK(cudaSetDevice(device_));
+    u64 ord = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&ord, ords_.ptr + gid, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += sizeof(u64);
+    decode(levels_[li], ord, op, left, right);
+    return LTLB200_OK;
+}
+
+void Engine::get_stats(ltlb200_stats *out) {
+    st_.table_slots = slots_.cap;
+    st_.device_bytes = held_;
+    *out = st_;
+}
+
+}  // namespace ltlb200
+
+// ---- C ABI -----------------------------------------------------------------------------
+using ltlb200::Engine;
+using ltlb200::g_last_error;
+
+struct ltlb200_engine {
+    Engine *impl;
+};
+
+template <typename Fn>
+static int guarded(Fn &&fn) {
+    try {
+        g_last_error.clear();
+        return fn();
+    } catch (const ltlb200::CudaError &e) {
+        g_last_error = e.what();
+        return LTLB200_ERR_CUDA;
+    } catch (const std::invalid_argument &e) {
+        g_last_error = e.what();
+        return LTLB200_ERR_ARGUMENT;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return LTLB200_ERR_CUDA;
+    }
+}
+
+extern "C" {
+
+int ltlb200_abi_version(void) { return LTLB200_ABI_VERSION; }
+
+const char *ltlb200_last_error(void) { return g_last_error.c_str(); }
+
+int ltlb200_device_count(void) {
+    int n = 0;
+    cudaError_t err = cudaGetDeviceCount(&n);
+    if (err != cudaSuccess) {
+        g_last_error = std::string("cudaGetDeviceCount: ") + cudaGetErrorString(err);
+        cudaGetLastError();
+        return 0;
+    }
+    int usable = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++usable;
+    }
+    if (!usable) g_last_error = "no sm_100 (B200) device visible";
+    return usable;
+}
+
+ltlb200_engine *ltlb200_create(int32_t trace_count, int32_t lane_bits, const uint64_t *masks, const uint64_t *target,
+                               const uint64_t *atoms, int32_t n_atoms, int32_t device, uint64_t hbm_budget_bytes,
+                               void *cuda_stream) {
+    ltlb200_engine *h = nullptr;
+    int rc = guarded([&] {
+        if (trace_count < 1 || n_atoms < 1 || !masks || !target || !atoms ||
+            (lane_bits != 8 && lane_bits != 16 && lane_bits != 32 && lane_bits != 64))
+            throw std::invalid_argument("bad specification geometry");
+        Engine *impl = new Engine(trace_count, lane_bits, masks, target, atoms, n_atoms, device, hbm_budget_bytes, cuda_stream);
+        h = new ltlb200_engine{impl};
+        return 0;
+    });
+    return rc == 0 ? h : nullptr;
+}
+
+void ltlb200_destroy(ltlb200_engine *e) {
+    if (!e) return;
+    delete e->impl;
+    delete e;
+}
+
+int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, int64_t batch_size,
+                         uint64_t memory_budget_bytes, double deadline_s, int64_t *n_new, int64_t *sep_gid,
+                         int64_t *constructed_delta) {
+    if (!e || !n_new || !sep_gid || !constructed_delta) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        return e->impl->expand_level(cost, op_mask, exhaustive != 0, batch_size, memory_budget_bytes, deadline_s, n_new,
+                                     sep_gid, constructed_delta);
+    });
+}
+
+double ltlb200_now(void) { return ltlb200::monotonic_s(); }
+
+int ltlb200_level_info(const ltlb200_engine *e, int32_t cost, int64_t *n, int64_t *base) {
+    if (!e || !n || !base) return LTLB200_ERR_ARGUMENT;
+    return e->impl->level_info(cost, n, base);
+}
+
+int32_t ltlb200_num_levels(const ltlb200_engine *e) { return e ? e->impl->num_levels() : 0; }
+
+int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op,
+                       int64_t *left, int64_t *right) {
+    if (!e) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] { return e->impl->level_copy(cost, first, count, cms, op, left, right); });
+}
+
+int ltlb200_entry(ltlb200_engine *e, int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
+    if (!e || !op || !left || !right) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] { return e->impl->entry(gid, op, left, right); });
+}
+
+uint64_t ltlb200_approx_bytes(const ltlb200_engine *e) { return e ? e->impl->approx_bytes() : 0; }
+
+int ltlb200_get_stats(ltlb200_engine *e, ltlb200_stats *out) {
+    if (!e || !out) return LTLB200_ERR_ARGUMENT;
+    e->impl->get_stats(out);
+    return LTLB200_OK;
+}
+
+}  // extern "C"

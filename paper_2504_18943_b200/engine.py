@@ -1,0 +1,292 @@
+"""Drop-in replacement for the reference's enumeration engine, running on a B200.
+
+Same entry points, argument meaning, results and error behaviour as the
+reference's ``pkg/src/ltlsynth/engine.py``:
+
+=====================  ======================================================
+here                   reference
+=====================  ======================================================
+``EngineConfig``       ``engine.py:61-80``
+``RunStats``           ``engine.py:83-88``
+``SynthesisResult``    ``engine.py:91-98``
+``CandidateStore``     ``engine.py:114-167`` (the language cache; here in HBM)
+``expand_level``       ``engine.py:367-451``
+``synthesize``         ``engine.py:454-506``
+``reconstruct``        ``engine.py:170-182``
+``normalize_operators````engine.py:52-58``
+=====================  ======================================================
+
+The level loop, witness reconstruction and the final semantic re-check stay in
+Python as in the reference; everything inside a level (candidate construction,
+separation check, observational-equivalence dedup, ordering, append) is one call
+into the CUDA library through the C ABI of ``include/ltlsynth_b200.h``.  There is
+no CPU path: constructing a ``CandidateStore`` without the built library or
+without a B200 raises ``NativeEngineError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, semantics
+from .formulas import (
+    DEFAULT_OPERATORS,
+    OPERATOR_NAMES,
+    And,
+    Atom,
+    Formula,
+    Future,
+    Next,
+    Not,
+    Or,
+    Until,
+)
+from .traces import Layout, Specification, atom_bitvectors, smallest_lane_dtype, validate_feasible
+
+OP_ATOM, OP_NOT, OP_NEXT, OP_FUTURE, OP_AND, OP_UNTIL, OP_OR = range(7)
+_TAG_OF = {"not": OP_NOT, "next": OP_NEXT, "future": OP_FUTURE, "and": OP_AND, "until": OP_UNTIL, "or": OP_OR}
+_UNARY_NODE = {OP_NOT: Not, OP_NEXT: Next, OP_FUTURE: Future}
+_BINARY_NODE = {OP_AND: And, OP_UNTIL: Until, OP_OR: Or}
+
+OUTCOME_FOUND = "found"
+OUTCOME_EXHAUSTED = "exhausted"
+_FAILURE_TEXT = {_native.TIME_BUDGET: "time budget exhausted", _native.MEMORY_BUDGET: "memory budget exhausted"}
+
+
+def normalize_operators(operators) -> tuple[str, ...]:
+    wanted = set(operators)
+    bad = wanted.difference(OPERATOR_NAMES)
+    if bad:
+        raise ValueError(f"unknown operators: {sorted(bad)}")
+    return tuple(name for name in OPERATOR_NAMES if name in wanted)
+
+
+def operator_mask(operators) -> int:
+    """Bit k set <=> operator tag k enabled (``op_mask`` of the C ABI)."""
+    return sum(1 << _TAG_OF[name] for name in normalize_operators(operators))
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    operators: tuple[str, ...] = DEFAULT_OPERATORS
+    max_cost: int = 20
+    time_budget_s: float = 300.0
+    memory_budget_mb: int = 8192  # the reference's host-side estimate, see CandidateStore.approx_bytes
+    batch_size: int = 1 << 16  # only shapes the `constructed` counter on the level that ends the run
+    threads: int | None = None  # accepted for compatibility; the device schedules its own parallelism
+    exhaustive: bool = False
+    dnc_threshold: int = 8
+    device: int = 0  # extension: CUDA device ordinal
+    hbm_budget_mb: int = 0  # extension: cap on device memory (0 = 90% of free HBM)
+
+    def __post_init__(self):
+        if self.max_cost < 1:
+            raise ValueError("max_cost must be >= 1")
+        if self.time_budget_s < 0 or self.memory_budget_mb <= 0:
+            raise ValueError("budgets must be positive")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.threads is not None and self.threads < 1:
+            raise ValueError("threads must be >= 1")
+
+
+@dataclass
+class RunStats:
+    constructed: int = 0
+    unique: int = 0
+    elapsed_s: float = 0.0
+    max_cost_reached: int = 0
+
+
+@dataclass
+class SynthesisResult:
+    formula: Formula | None
+    cost: int | None
+    minimal: bool
+    outcome: str
+    stats: RunStats
+    failure: str | None = None
+
+
+class _Level:
+    """One cost level of the cache; arrays are fetched from HBM on first use."""
+
+    def __init__(self, store: "CandidateStore", cost: int, n: int, base: int):
+        self._store, self._cost, self.n, self.base = store, cost, n, base
+        self._arrays = None
+
+    def _fetch(self):
+        if self._arrays is None:
+            self._arrays = self._store._copy_level(self._cost, self.n)
+        return self._arrays
+
+    cms = property(lambda self: self._fetch()[0])
+    op = property(lambda self: self._fetch()[1])
+    left = property(lambda self: self._fetch()[2])
+    right = property(lambda self: self._fetch()[3])
+
+
+class CandidateStore:
+    """Cost-indexed cache of unique CMs with provenance, resident on the GPU."""
+
+    def __init__(self, spec: Specification, dtype=None, device: int = 0, hbm_budget_mb: int = 0, stream=None):
+        self.spec = spec
+        self.dtype = np.dtype(dtype) if dtype is not None else smallest_lane_dtype(spec.max_length)
+        self.layout = Layout.from_specification(spec, self.dtype)
+        self.atoms = atom_bitvectors(spec, self.dtype)
+        self.trace_count = spec.trace_count
+        self.key_words = -(-(self.trace_count * self.dtype.itemsize) // 8)
+        self.levels: list[_Level] = []
+        lib = _native.load()
+        if lib.ltlb200_device_count() < 1:
+            raise _native.NativeEngineError("no usable B200: " + _native.last_error())
+        as_u64 = lambda a: np.ascontiguousarray(a, dtype=np.uint64)
+        masks, target, atoms = as_u64(self.layout.masks), as_u64(self.layout.target), as_u64(self.atoms)
+        self._handle = lib.ltlb200_create(
+            self.trace_count, self.dtype.itemsize * 8, masks.ctypes.data, target.ctypes.data, atoms.ctypes.data,
+            spec.alphabet.n, int(device), int(hbm_budget_mb) << 20, ctypes.c_void_p(stream or 0),
+        )
+        if not self._handle:
+            raise _native.NativeEngineError("ltlb200_create failed: " + _native.last_error())
+
+    def close(self):
+        handle, self._handle = getattr(self, "_handle", None), None
+        if handle:
+            _native.load().ltlb200_destroy(handle)
+
+    __del__ = close
+
+    # -- reference-shaped accessors -------------------------------------------------
+    @property
+    def total(self) -> int:
+        return sum(level.n for level in self.levels)
+
+    @property
+    def approx_bytes(self) -> int:
+        return int(_native.load().ltlb200_approx_bytes(self._handle))
+
+    def level(self, cost: int) -> _Level:
+        return self.levels[cost - 1]
+
+    def entry(self, gid: int) -> tuple[int, int, int]:
+        op, left, right = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _native.check(
+            _native.load().ltlb200_entry(self._handle, int(gid), ctypes.byref(op), ctypes.byref(left), ctypes.byref(right)),
+            f"entry({gid})",
+        )
+        return op.value, left.value, right.value
+
+    def all_cms(self) -> np.ndarray:
+        parts = [level.cms for level in self.levels]
+        if not parts:
+            return np.empty((0, self.trace_count), dtype=self.dtype)
+        return np.concatenate(parts, axis=0)
+
+    def device_stats(self) -> dict:
+        st = _native.Stats()
+        _native.check(_native.load().ltlb200_get_stats(self._handle, ctypes.byref(st)), "get_stats")
+        return st.as_dict()
+
+    # -- plumbing ---------------------------------------------------------------------
+    def _expand(self, cost, op_mask, exhaustive, batch_size, memory_budget_bytes, deadline):
+        n_new, sep, delta = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        status = _native.check(
+            _native.load().ltlb200_expand_level(
+                self._handle, cost, op_mask, int(exhaustive), int(batch_size), int(memory_budget_bytes),
+                -1.0 if deadline is None else float(deadline),
+                ctypes.byref(n_new), ctypes.byref(sep), ctypes.byref(delta)),
+            f"expand_level({cost})",
+        )
+        base = self.total
+        self.levels.append(_Level(self, cost, n_new.value, base))
+        return status, n_new.value, (None if sep.value < 0 else sep.value), delta.value
+
+    def _copy_level(self, cost: int, n: int):
+        cms = np.empty((n, self.trace_count), dtype=self.dtype)
+        op = np.empty(n, dtype=np.uint8)
+        left = np.empty(n, dtype=np.int64)
+        right = np.empty(n, dtype=np.int64)
+        if n:
+            _native.check(
+                _native.load().ltlb200_level_copy(self._handle, cost, 0, n, cms.ctypes.data, op.ctypes.data,
+                                                  left.ctypes.data, right.ctypes.data),
+                f"level_copy({cost})",
+            )
+        return cms, op, left, right
+
+
+def reconstruct(store, gid: int) -> Formula:
+    """Witness formula from (operator, child ids) provenance."""
+    tag, left, right = store.entry(gid)
+    if tag == OP_ATOM:
+        return Atom(left)
+    if tag in _UNARY_NODE:
+        return _UNARY_NODE[tag](reconstruct(store, left))
+    return _BINARY_NODE[tag](reconstruct(store, left), reconstruct(store, right))
+
+
+class _BudgetExceeded(Exception):
+    pass
+
+
+def _monotonic() -> float:
+    return float(_native.load().ltlb200_now())
+
+
+def expand_level(store: CandidateStore, cost: int, ops=DEFAULT_OPERATORS, config: EngineConfig | None = None,
+                 stats: RunStats | None = None, deadline: float | None = None, executor=None):
+    """Build level ``cost``; returns ``(new entries, separator id or None)``.
+
+    ``deadline`` is on the clock of ``time.perf_counter()`` as in the reference;
+    ``executor`` is accepted and ignored (the device needs no worker threads).
+    """
+    config = config or EngineConfig()
+    stats = stats if stats is not None else RunStats()
+    mask = operator_mask(ops)
+    native_deadline = None
+    if deadline is not None:
+        native_deadline = _monotonic() + (deadline - time.perf_counter())
+    status, n_new, sep_gid, delta = store._expand(
+        cost, mask, config.exhaustive, config.batch_size, config.memory_budget_mb << 20, native_deadline
+    )
+    stats.constructed += delta
+    stats.unique = store.total
+    if status in _FAILURE_TEXT:
+        raise _BudgetExceeded(_FAILURE_TEXT[status])
+    return n_new, sep_gid
+
+
+def synthesize(spec: Specification, config: EngineConfig = EngineConfig()) -> SynthesisResult:
+    """Minimum-cost separating formula by level-wise enumeration on the GPU."""
+    validate_feasible(spec)
+    ops = normalize_operators(config.operators)
+    t0 = time.perf_counter()
+    store = CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb)
+    try:
+        stats = RunStats()
+        deadline = t0 + config.time_budget_s
+        found, failure = None, None
+        for cost in range(1, config.max_cost + 1):
+            stats.max_cost_reached = cost
+            try:
+                _, sep_gid = expand_level(store, cost, ops, config=config, stats=stats, deadline=deadline)
+            except _BudgetExceeded as stop:
+                failure = str(stop)
+                break
+            if sep_gid is not None and found is None:
+                found = (sep_gid, cost)
+                if not config.exhaustive:
+                    break
+        stats.elapsed_s = time.perf_counter() - t0
+        if found is None:
+            return SynthesisResult(None, None, False, OUTCOME_EXHAUSTED, stats, failure)
+        formula = reconstruct(store, found[0])
+    finally:
+        store.close()
+    if not semantics.separates_by_sat(spec, formula):
+        raise RuntimeError("internal error: synthesized formula fails the reference semantics")
+    return SynthesisResult(formula, found[1], True, OUTCOME_FOUND, stats)

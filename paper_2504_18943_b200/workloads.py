@@ -78,6 +78,8 @@ _SYNTHETIC = {
     "c5": (4, 32, 32, 16, True),  # 64 x 16 bit = 128 B
     "w32": (2, 3, 3, 20, False),  # 32-bit lanes
     "w64": (2, 2, 3, 40, False),  # 64-bit lanes
+    "w32n": (2, 2, 2, 20, False),  # 4 x 32 bit = 16 B (one uint4)
+    "w64n": (3, 1, 1, 40, False),  # 2 x 64 bit = 16 B (one uint4)
 }
 
 

@@ -69,6 +69,12 @@ CASES = [
     dict(name="w32_s1_found", workload="w32", seed=1, max_cost=12, exhaustive=False),
     dict(name="w64_s0_exh8", workload="w64", seed=0, max_cost=8, exhaustive=True),
     dict(name="w64_s1_found", workload="w64", seed=1, max_cost=12, exhaustive=False),
+    dict(name="w32n_s0_exh9", workload="w32n", seed=0, max_cost=9, exhaustive=True),
+    dict(name="w32n_s2_found", workload="w32n", seed=2, max_cost=12, exhaustive=False),
+    dict(name="w64n_s0_exh9", workload="w64n", seed=0, max_cost=9, exhaustive=True),
+    dict(name="w64n_s3_found", workload="w64n", seed=3, max_cost=12, exhaustive=False),
+    dict(name="c3_s1_found", workload="c3", seed=1, max_cost=12, exhaustive=False),
+    dict(name="c3_s0_b1000_found", workload="c3", seed=2, max_cost=12, exhaustive=False, batch_size=1000),
 ]
 SLOW_CASES = [
     # the paper's 7+7 example to its cost-16 solution (about a minute of reference time)
