@@ -40,18 +40,20 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > built for p in deps)
 
 
-def build_native(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    if not force and not _stale():
+def build_native(force: bool = False, verbose: bool = False, defines=(), out: pathlib.Path | None = None) -> pathlib.Path:
+    """``defines``/``out`` build a tuning variant (e.g. ("LTLB200_PROBE_BATCH=2",)) beside the default library."""
+    target = pathlib.Path(out) if out else LIB_PATH
+    if not force and out is None and not _stale():
         return LIB_PATH
     LIB_DIR.mkdir(exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
-           "-o", str(LIB_PATH), *[str(CSRC / s) for s in SOURCES]]
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
+           "-o", str(target), *[str(CSRC / s) for s in SOURCES]]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + proc.stdout + proc.stderr)
     if verbose:
         print(proc.stdout + proc.stderr)
-    return LIB_PATH
+    return target
 
 
 if __name__ == "__main__":

@@ -9,9 +9,11 @@ fallback behind it, and the in-tree shared library must have been built with
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libltlsynth_b200.so"
+# LTLB200_LIB selects a tuning variant built by _build.build_native(defines=..., out=...)
+LIB_PATH = pathlib.Path(os.environ.get("LTLB200_LIB") or pathlib.Path(__file__).resolve().parent / "_lib" / "libltlsynth_b200.so")
 
 OK, TIME_BUDGET, MEMORY_BUDGET = 0, 1, 2
 ERR_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED = -1, -2, -3

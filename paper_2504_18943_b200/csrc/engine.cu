@@ -103,11 +103,19 @@ __global__ void __launch_bounds__(1024) sb_add_kernel(uint32_t *out, u64 n, cons
     if (i < n) out[i] += block_prefix[blockIdx.x];
 }
 
-// counters[5] = number of winners, counters[6] = rank of the separator's ordinal
-__global__ void level_summary_kernel(const uint32_t *bitmap, const uint32_t *sb_rank, u64 n_bits, u64 sep_ord,
-                                     u64 *counters) {
-    counters[5] = n_bits ? ordinal_rank(bitmap, sb_rank, n_bits - 1) + ((bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u) : 0;
-    counters[6] = sep_ord < n_bits ? ordinal_rank(bitmap, sb_rank, sep_ord) : ~0ull;
+// number of winners and rank of the separator's ordinal (the separator is counters[CTR_SEP])
+__global__ void level_summary_kernel(const uint32_t *bitmap, const uint32_t *sb_rank, u64 n_bits, u64 *counters) {
+    const u64 sep_ord = counters[CTR_SEP];
+    counters[CTR_WINNERS] = n_bits ? ordinal_rank(bitmap, sb_rank, n_bits - 1) + ((bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u) : 0;
+    counters[CTR_SEPRANK] = sep_ord < n_bits ? ordinal_rank(bitmap, sb_rank, sep_ord) : ~0ull;
+}
+
+// counters[CTR_SEP] = smallest listed ordinal that is a winner (its bitmap bit is set)
+__global__ void __launch_bounds__(256) first_fresh_kernel(const uint32_t *bitmap, const u64 *ords, u64 n, u64 *counters) {
+    const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const u64 ord = ords[k];
+    if (bitmap[ord >> 5] >> (ord & 31) & 1u) atomicMin(&counters[CTR_SEP], ord);
 }
 
 // ---- host-side level bookkeeping ------------------------------------------------------
@@ -157,6 +165,7 @@ private:
     DeviceArray<uint32_t> bitmap_;
     DeviceArray<uint32_t> sb_rank_;
     DeviceArray<uint32_t> scan_tmp_;
+    DeviceArray<u64> sep_list_;
     u64 *d_counters_ = nullptr;
     BlockDesc *d_blocks_ = nullptr;
     static constexpr int kMaxBlocks = 512;
@@ -179,7 +188,8 @@ private:
     void read_counters();
     void decode(const LevelMeta &lv, u64 ord, int32_t *op, int64_t *left, int64_t *right) const;
     u64 constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) const;
-    void launch_enumerate(const NarrowParams &P, int grid);
+    void launch_enumerate(NarrowParams P, const LevelMeta &lv);
+    u64 chunk_exact_separator(const LevelMeta &lv, u64 n_seps, u64 batch);
 };
 
 template <typename T>
@@ -219,6 +229,14 @@ void Engine::reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems) {
     }
     a.ptr = p;
     a.cap = cap;
+}
+
+template <int LW>
+static int occupancy_of() {
+    int occ = 0, best = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, OP_UNTIL>, CTA_THREADS, 0) == cudaSuccess)
+        best = std::max(best, occ);
+    return best;
 }
 
 static uint4 pack_lanes16(const uint64_t *lanes, int T, int lane_bits) {
@@ -269,18 +287,7 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     held_ += h_atoms.size() * sizeof(uint4) + CTR_COUNT * sizeof(u64) + kMaxBlocks * sizeof(BlockDesc);
-    {
-        int occ = 0;
-        cudaError_t err = cudaSuccess;
-        switch (lw_) {
-            case 8: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<8>, CTA_THREADS, 0); break;
-            case 16: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<16>, CTA_THREADS, 0); break;
-            case 32: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<32>, CTA_THREADS, 0); break;
-            default: err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<64>, CTA_THREADS, 0); break;
-        }
-        CUDA_CHECK(err);
-        occupancy_ = std::max(occ, 1);
-    }
+    occupancy_ = lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>();
     rebuild_table(1 << 12);
     st_.row_bytes = row_bytes_;
     st_.key_bytes = 16;
@@ -296,6 +303,7 @@ Engine::~Engine() {
     release(bitmap_);
     release(sb_rank_);
     release(scan_tmp_);
+    release(sep_list_);
     cudaFree(d_atoms_);
     cudaFree(d_counters_);
     cudaFree(d_blocks_);
@@ -478,16 +486,75 @@ u64 Engine::constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) con
     return b.ord0 + end;
 }
 
-void Engine::launch_enumerate(const NarrowParams &P, int grid) {
-    switch (lw_) {
-        case 8: narrow_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-        case 16: narrow_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-        case 32: narrow_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-        default: narrow_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+// Exhaustive mode: from the ordinals of ALL separating candidates of the level, pick what
+// the reference's chunked merge loop reports -- walk the chunks in order, look only at each
+// chunk's first separating candidate, and take the first of those that is fresh, i.e. that
+// won its CM (bit set in the winners bitmap).  Leaves the result in counters[CTR_SEP].
+u64 Engine::chunk_exact_separator(const LevelMeta &lv, u64 n_seps, u64 batch) {
+    std::vector<u64> seps((size_t)n_seps);
+    CUDA_CHECK(cudaMemcpyAsync(seps.data(), sep_list_.ptr, n_seps * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += n_seps * sizeof(u64);
+    std::sort(seps.begin(), seps.end());
+    std::vector<u64> firsts;
+    u64 chunk_end = 0;
+    for (u64 o : seps) {
+        if (o < chunk_end) continue;  // not the first separating candidate of its chunk
+        firsts.push_back(o);
+        chunk_end = constructed_through(lv, o, batch);
     }
+    const u64 none = VAL_EMPTY;
+    CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SEP, &none, sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaMemcpyAsync(sep_list_.ptr, firsts.data(), firsts.size() * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    st_.h2d_bytes += firsts.size() * sizeof(u64);
+    first_fresh_kernel<<<(unsigned)((firsts.size() + 255) / 256), 256, 0, stream_>>>(bitmap_.ptr, sep_list_.ptr, firsts.size(), d_counters_);
     CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // `firsts` must outlive the copy
     st_.kernel_launches++;
-    st_.enumerate_launches++;
+    return firsts.size();
+}
+
+template <int LW>
+static void launch_op(int op, const NarrowParams &P, int grid, cudaStream_t st) {
+    switch (op) {
+        case OP_ATOM: narrow_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_NOT: narrow_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_NEXT: narrow_level_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_FUTURE: narrow_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_AND: narrow_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_UNTIL: narrow_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        default: narrow_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
+    }
+}
+
+// One launch per operator, in canonical operator order (blocks of a level are grouped by
+// operator already); each launch covers all (c1, c2) blocks of its operator.
+void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
+    size_t b0 = 0;
+    int group = 0;
+    while (b0 < lv.blocks.size()) {
+        size_t b1 = b0;
+        while (b1 < lv.blocks.size() && lv.blocks[b1].op == lv.blocks[b0].op) ++b1;
+        const BlockDesc &last = lv.blocks[b1 - 1];
+        P.block_begin = (int)b0;
+        P.block_end = (int)b1;
+        P.tile_begin = lv.blocks[b0].tile0;
+        P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
+        P.ticket = CTR_TICKET0 + group;
+        const int grid = (int)std::min<u64>(P.tile_end - P.tile_begin, (u64)sm_count_ * occupancy_);
+        const int op = (int)lv.blocks[b0].op;
+        switch (lw_) {
+            case 8: launch_op<8>(op, P, grid, stream_); break;
+            case 16: launch_op<16>(op, P, grid, stream_); break;
+            case 32: launch_op<32>(op, P, grid, stream_); break;
+            default: launch_op<64>(op, P, grid, stream_); break;
+        }
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+        st_.enumerate_launches++;
+        b0 = b1;
+        ++group;
+    }
 }
 
 int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
@@ -529,10 +596,13 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             const u64 want_slots = next_pow2(2 * (total_ + est + (exact ? 0 : kSlack)));
             if (want_slots > slots_.cap) rebuild_table(want_slots);
             reserve(new_list_, est + (exact ? 64 : kSlack), false);
-            u64 init[CTR_COUNT] = {0, 0, VAL_EMPTY, 0, 0, 0, 0, 0};
+            if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
+            u64 init[CTR_COUNT];
+            for (auto &c : init) c = 0;
+            init[CTR_SEP] = VAL_EMPTY;
             // the special-key register (CTR_SPECIAL) persists across levels
-            CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, 3 * sizeof(u64), cudaMemcpyHostToDevice, stream_));
-            CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_OVERFLOW, init + CTR_OVERFLOW, 4 * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+            CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, CTR_SPECIAL * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+            CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_OVERFLOW, init + CTR_OVERFLOW, (CTR_COUNT - CTR_OVERFLOW) * sizeof(u64), cudaMemcpyHostToDevice, stream_));
             NarrowParams P{};
             P.store = store_.ptr;
             P.atoms = d_atoms_;
@@ -542,16 +612,15 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             P.new_list_cap = new_list_.cap;
             P.counters = d_counters_;
             P.blocks = d_blocks_;
-            P.n_blocks = (int)lv.blocks.size();
-            P.n_tiles = n_tiles;
             P.valid = valid_;
             P.target = target_;
             P.prune_after_sep = exhaustive ? 0 : 1;
             P.special_possible = special_possible_ ? 1 : 0;
             P.claim_limit = exact ? ~0ull : est;
-            const int grid = (int)std::min<u64>(n_tiles, (u64)sm_count_ * occupancy_);
+            P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
+            P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
             CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
-            launch_enumerate(P, grid);
+            launch_enumerate(P, lv);
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
             read_counters();
             float ms = 0;
@@ -565,6 +634,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         }
         n_claimed = h_counters_[CTR_CLAIMED];
         sep_ord = h_counters_[CTR_SEP];
+        const u64 n_seps = h_counters_[CTR_SEPCOUNT];
 
         // ---- finalise: rank winners by ordinal, append to the cache
         const bool cut = !exhaustive && sep_ord != VAL_EMPTY;
@@ -613,7 +683,10 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
                 st_.kernel_launches += 2;
             }
         }
-        level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, sep_ord, d_counters_);
+        // exhaustive runs: the reference reports, per level, the first CHUNK whose first
+        // separating candidate is fresh (engine.py:331,425-433); reproduce that exactly
+        if (exhaustive && n_seps > 0 && n_seps <= sep_list_.cap) chunk_exact_separator(lv, n_seps, (u64)batch);
+        level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
         narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
         CUDA_CHECK(cudaGetLastError());
         CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
@@ -622,8 +695,9 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         float fms = 0;
         CUDA_CHECK(cudaEventElapsedTime(&fms, ev_[2], ev_[3]));
         st_.finalize_ms += fms;
-        lv.n = h_counters_[5];
-        if (sep_ord != VAL_EMPTY) *sep_gid = (int64_t)(total_ + h_counters_[6]);
+        lv.n = h_counters_[CTR_WINNERS];
+        sep_ord = h_counters_[CTR_SEP];
+        if (sep_ord != VAL_EMPTY) *sep_gid = (int64_t)(total_ + h_counters_[CTR_SEPRANK]);
         if (cut) table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
     } catch (const MemoryBudget &e) {
         g_last_error = e.what();

@@ -22,7 +22,13 @@ namespace ltlb200 {
 
 constexpr int CTA_THREADS = 256;
 constexpr int TILE_S = 64;      // scalar-dimension rows of a binary tile (staged in shared memory)
-constexpr int PROBE_BATCH = 4;  // hash probes each thread keeps in flight
+#ifndef LTLB200_PROBE_BATCH
+#define LTLB200_PROBE_BATCH 4
+#endif
+#ifndef LTLB200_MIN_CTAS
+#define LTLB200_MIN_CTAS 3
+#endif
+constexpr int PROBE_BATCH = LTLB200_PROBE_BATCH;  // hash probes each thread keeps in flight
 constexpr int UNARY_ITEMS = 8;  // candidates per thread in a unary tile
 constexpr u64 LEVEL_FLAG = 1ull << 62;
 constexpr u64 VAL_EMPTY = ~0ull;
@@ -60,16 +66,21 @@ struct NarrowParams {
     u64 new_list_cap;
     u64 *counters;  // [0] tile ticket, [1] claimed slots, [2] separator ordinal (min), [3] special-key val, [4] overflow flag
     const BlockDesc *blocks;
-    int n_blocks;
-    u64 n_tiles;
+    int block_begin, block_end;  // this launch's blocks (all of one operator)
+    u64 tile_begin, tile_end;    // their tiles in the level's flattened tile space
+    int ticket;                  // index of this launch's ticket counter
     uint4 valid;   // Layout.masks packed
     uint4 target;  // Layout.target packed
     int prune_after_sep;  // non-exhaustive: skip work ordered after the best separator so far
     int special_possible;
     u64 claim_limit;
+    u64 *sep_list;  // exhaustive runs: ordinals of every separating candidate (NULL otherwise)
+    u64 sep_list_cap;
 };
 
-enum : int { CTR_TICKET = 0, CTR_CLAIMED = 1, CTR_SEP = 2, CTR_SPECIAL = 3, CTR_OVERFLOW = 4, CTR_COUNT = 8 };
+// [5] winners (summary), [6] rank of the separator (summary), [7] separating candidates recorded
+// [8..14] one tile ticket per operator launch
+enum : int { CTR_UNUSED = 0, CTR_CLAIMED = 1, CTR_SEP = 2, CTR_SPECIAL = 3, CTR_OVERFLOW = 4, CTR_WINNERS = 5, CTR_SEPRANK = 6, CTR_SEPCOUNT = 7, CTR_TICKET0 = 8, CTR_COUNT = 16 };
 
 __device__ __forceinline__ uint4 ld_cg_u4(const uint4 *p) { return __ldcg(p); }
 
@@ -125,11 +136,46 @@ __device__ __forceinline__ void claims_flush(const NarrowParams &P, const WarpCl
     __syncwarp();
 }
 
-// Insert (key -> min val).  k0/v0 are the already loaded contents of `slot`.
-// Returns true when the CM was not stored by an earlier level (fresh for this level).
-__device__ __forceinline__ bool table_resolve(const NarrowParams &P, const WarpClaims &wc, uint4 key, u64 val,
-                                              u64 slot, uint4 k0, u64 v0) {
+// ---- deferred slow path -------------------------------------------------------------
+// The hot loop only decides, per candidate, between "duplicate of a CM finalised at an
+// earlier level" (the common case: nothing to write) and "needs work".  The latter are
+// parked in a per-warp shared-memory queue and drained by the whole warp after each
+// batch, one parked candidate per lane: the claim / atomicMin / separator code then runs
+// with full lanes and outside the hot loop's register budget.
+
+struct __align__(16) Parked {
+    uint4 key;
+    u64 ord;
+    uint32_t slot;   // where the probe stopped (empty slot or the slot holding `key`)
+    uint32_t flags;  // PK_*
+};
+enum : uint32_t { PK_SEP = 1u, PK_OLD = 2u, PK_SPECIAL = 4u };
+constexpr int WARP_QUEUE = 32 * PROBE_BATCH;
+
+struct WarpCtx {
+    uint32_t *claim_buf;   // WARP_BUF newly claimed slots waiting for a flush
+    uint32_t *claim_fill;
+    Parked *queue;         // WARP_QUEUE parked candidates
+    uint32_t *queue_fill;
+};
+
+__device__ __forceinline__ void park(const WarpCtx &w, uint4 key, u64 ord, u64 slot, uint32_t flags) {
+    const uint32_t pos = atomicAdd(w.queue_fill, 1u);
+    Parked e;
+    e.key = key;
+    e.ord = ord;
+    e.slot = (uint32_t)slot;
+    e.flags = flags;
+    w.queue[pos] = e;
+}
+
+// Insert (key -> min val) starting at `slot`; returns true when the CM was not stored by
+// an earlier level (fresh for this level).
+__device__ __forceinline__ bool table_claim(const NarrowParams &P, const WarpCtx &w, uint4 key, u64 val, u64 slot) {
     const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    const WarpClaims wc{w.claim_buf, w.claim_fill};
+    uint4 k0 = ld_cg_u4(&P.slots[slot].key);
+    u64 v0 = __ldcg(&P.slots[slot].val);
     for (int probes = 0;; ++probes) {
         if (v_eq(k0, key)) {
             if (v0 > val) atomicMin(&P.slots[slot].val, val);
@@ -157,70 +203,116 @@ __device__ __forceinline__ bool table_resolve(const NarrowParams &P, const WarpC
     }
 }
 
-__device__ __forceinline__ bool special_insert(const NarrowParams &P, const WarpClaims &wc, u64 val) {
-    u64 old = atomicMin(&P.counters[CTR_SPECIAL], val);
-    if (old == VAL_EMPTY) claims_push(wc, SLOT_SPECIAL);
-    return old >= LEVEL_FLAG;
+// warp-collective: resolve every parked candidate, then flush full groups of claims
+__device__ __forceinline__ void drain_parked(const NarrowParams &P, const WarpCtx &w) {
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = *(volatile uint32_t *)w.queue_fill;
+    for (uint32_t idx = lane; idx < n; idx += 32) {
+        const Parked e = w.queue[idx];
+        const u64 val = LEVEL_FLAG | e.ord;
+        bool fresh = false;
+        if (e.flags & PK_SPECIAL) {
+            const u64 old = atomicMin(&P.counters[CTR_SPECIAL], val);
+            if (old == VAL_EMPTY) claims_push(WarpClaims{w.claim_buf, w.claim_fill}, SLOT_SPECIAL);
+            fresh = old >= LEVEL_FLAG;
+        } else if (!(e.flags & PK_OLD)) {
+            fresh = table_claim(P, w, e.key, val, e.slot);
+        }
+        if (e.flags & PK_SEP) {
+            if (fresh) atomicMin(&P.counters[CTR_SEP], e.ord);
+            if (P.sep_list) {  // exhaustive runs keep every separating ordinal (chunk-exact separator id)
+                const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+                if (pos < P.sep_list_cap) P.sep_list[pos] = e.ord;
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) *(volatile uint32_t *)w.queue_fill = 0;
+    claims_flush(P, WarpClaims{w.claim_buf, w.claim_fill}, false);
 }
 
-// Probe and resolve up to PROBE_BATCH candidates of one thread; all loads are issued
-// before the first one is consumed so that a warp keeps 32*PROBE_BATCH sectors in flight.
-template <int LW>
-__device__ __forceinline__ void insert_batch(const NarrowParams &P, const WarpClaims &wc,
-                                             const uint4 (&cand)[PROBE_BATCH], const u64 (&ord)[PROBE_BATCH],
-                                             const bool (&live)[PROBE_BATCH]) {
-    u64 slot[PROBE_BATCH];
+// Probe up to PROBE_BATCH candidates of one thread; all first probes are issued before
+// any is consumed so that a warp keeps 32*PROBE_BATCH sectors in flight.  Only the high
+// word of a slot's val is read: it alone tells "finalised at an earlier level" (< 2^62).
+// `known[r]`: the candidate equals one of its operands, i.e. a CM that is already in the
+// cache -- a duplicate by construction, no probe needed.  `ord_of(r)` recomputes the
+// ordinal for the few candidates that get parked, so ordinals hold no registers here.
+template <int LW, typename OrdOf>
+__device__ __forceinline__ void insert_batch(const NarrowParams &P, const WarpCtx &w,
+                                             const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                             const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
+    constexpr uint32_t FLAG_HI = (uint32_t)(LEVEL_FLAG >> 32);
+    const uint32_t mask32 = (uint32_t)P.slot_mask;
+    uint32_t slot[PROBE_BATCH];
     uint4 k0[PROBE_BATCH];
-    u64 v0[PROBE_BATCH];
+    uint32_t vhi[PROBE_BATCH];
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        slot[r] = hash_vec(cand[r], 0) & P.slot_mask;
-        if (live[r]) {
+        slot[r] = (uint32_t)hash_vec(cand[r], 0) & mask32;
+        if (live[r] && !known[r]) {
             k0[r] = ld_cg_u4(&P.slots[slot[r]].key);
-            v0[r] = __ldcg(&P.slots[slot[r]].val);
+            vhi[r] = __ldcg(reinterpret_cast<const uint32_t *>(&P.slots[slot[r]].val) + 1);
         }
     }
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
         if (!live[r]) continue;
-        const u64 val = LEVEL_FLAG | ord[r];
-        bool fresh;
-        if (P.special_possible && key_is_empty(cand[r])) fresh = special_insert(P, wc, val);
-        else fresh = table_resolve(P, wc, cand[r], val, slot[r], k0[r], v0[r]);
-        if (fresh && cm_sep_diff<LW>(cand[r], P.target) == 0u) atomicMin(&P.counters[CTR_SEP], ord[r]);
+        uint32_t flags = cm_sep_diff<LW>(cand[r], P.target) == 0u ? PK_SEP : 0u;
+        uint32_t s = slot[r];
+        if (known[r]) {
+            flags |= PK_OLD;
+        } else if (P.special_possible && key_is_empty(cand[r])) {
+            flags |= PK_SPECIAL;
+        } else {
+            uint4 k = k0[r];
+            uint32_t v = vhi[r];
+            while (!v_eq(k, cand[r]) && !key_is_empty(k)) {  // linear probing past other CMs
+                s = (s + 1) & mask32;
+                k = ld_cg_u4(&P.slots[s].key);
+                v = __ldcg(reinterpret_cast<const uint32_t *>(&P.slots[s].val) + 1);
+            }
+            if (v_eq(k, cand[r]) && v < FLAG_HI) flags |= PK_OLD;  // duplicate of an earlier level
+        }
+        if (flags != PK_OLD) park(w, cand[r], ord_of(r), s, flags);
     }
-    claims_flush(P, wc, false);
+    drain_parked(P, w);
 }
 
 template <int LW, int OP>
-__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, const WarpClaims &wc, const BlockDesc &B,
+__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, const WarpCtx &wc, const BlockDesc &B,
                                                u64 tile_local, u64 sep_now) {
     const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off;
-    const u64 first = tile_local * (u64)(CTA_THREADS * UNARY_ITEMS);
+    const u64 first = tile_local * (u64)(CTA_THREADS * UNARY_ITEMS) + threadIdx.x;
+    const u64 ord0 = B.ord0;
 #pragma unroll 1
     for (int g = 0; g < UNARY_ITEMS; g += PROBE_BATCH) {
         uint4 cand[PROBE_BATCH];
-        u64 ord[PROBE_BATCH];
-        bool live[PROBE_BATCH];
+        bool live[PROBE_BATCH], known[PROBE_BATCH];
         uint4 x[PROBE_BATCH];
+        auto ord_of = [&](int r) { return ord0 + first + (u64)(g + r) * CTA_THREADS; };
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
-            const u64 i = first + (u64)(g + r) * CTA_THREADS + threadIdx.x;
-            ord[r] = B.ord0 + i;
-            live[r] = i < B.na && ord[r] <= sep_now;
+            const u64 i = first + (u64)(g + r) * CTA_THREADS;
+            live[r] = i < B.na && ord0 + i <= sep_now;
             x[r] = live[r] ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int r = 0; r < PROBE_BATCH; ++r) cand[r] = cm_apply<LW, OP>(x[r], x[r], P.valid);
-        insert_batch<LW>(P, wc, cand, ord, live);
+        for (int r = 0; r < PROBE_BATCH; ++r) {
+            cand[r] = cm_apply<LW, OP>(x[r], x[r], P.valid);
+            known[r] = OP != OP_ATOM && v_eq(cand[r], x[r]);
+        }
+        insert_batch<LW>(P, wc, cand, live, known, ord_of);
     }
 }
 
 // Binary tile: each thread keeps one row of the "vector" operand in registers and walks
-// TILE_S rows of the "scalar" operand staged in shared memory.
+// up to TILE_S rows of the "scalar" operand staged in shared memory together with the
+// row's ordinal term, so that a candidate's ordinal is one 64-bit add:
+//   rectangle  ord = ord0 + i*nb + j          triangle (i <= j < n)  ord = ord0 + i*n - i(i-1)/2 + (j - i)
 template <int LW, int OP>
-__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, const WarpClaims &wc, const BlockDesc &B,
-                                                u64 tile_local, uint4 *s_rows, u64 sep_now) {
+__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, const WarpCtx &wc, const BlockDesc &B,
+                                                u64 tile_local, uint4 *s_rows, u64 *s_term, u64 sep_now) {
     const bool tri = B.kind == BK_TRI;
     const bool vec_b = B.vec_is_b != 0;
     // tile order follows the canonical order: left operand (i) outer, right operand (j) inner
@@ -233,78 +325,87 @@ __device__ __forceinline__ void run_binary_tile(const NarrowParams &P, const War
     if (tri && v0 + CTA_THREADS - 1 < s0) return;  // tile entirely below the diagonal (j < i)
     const uint4 *vec_rows = P.store + (vec_b ? B.b_off : B.a_off);
     const uint4 *sc_rows = P.store + (vec_b ? B.a_off : B.b_off);
-    __syncthreads();  // previous tile's readers of s_rows are done
-    if ((int)threadIdx.x < s_cnt) s_rows[threadIdx.x] = __ldg(sc_rows + s0 + threadIdx.x);
+    __syncthreads();  // previous tile's readers of the staged rows are done
+    if ((int)threadIdx.x < s_cnt) {
+        const u64 s = s0 + threadIdx.x;
+        s_rows[threadIdx.x] = __ldg(sc_rows + s);
+        // scalar-row part of the ordinal; the thread part is j (vec_b) or ord0 + i*nb (!vec_b)
+        s_term[threadIdx.x] = !vec_b ? s : B.ord0 + (tri ? s * B.na - (s ? (s * (s - 1)) / 2 : 0) - s : s * B.nb);
+    }
     __syncthreads();
     const u64 v = v0 + threadIdx.x;
     const bool v_ok = v < n_vec;
     const uint4 xv = v_ok ? __ldg(vec_rows + v) : make_uint4(0, 0, 0, 0);
+    const u64 thread_term = vec_b ? v : B.ord0 + v * B.nb;
+    // triangle: row s0+sr pairs with columns j >= i only
+    const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
+    const int s_live = v_ok ? first_bad : 0;
+    const bool prune = sep_now != ~0ull;
 #pragma unroll 1
     for (int g = 0; g < s_cnt; g += PROBE_BATCH) {
         uint4 cand[PROBE_BATCH];
-        u64 ord[PROBE_BATCH];
-        bool live[PROBE_BATCH];
+        bool live[PROBE_BATCH], known[PROBE_BATCH];
+        auto ord_of = [&](int r) { return s_term[min(g + r, s_cnt - 1)] + thread_term; };
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
-            const int sr = g + r;
-            const u64 s = s0 + sr;
-            const uint4 xs = s_rows[sr < s_cnt ? sr : 0];
-            const u64 i = vec_b ? s : v, j = vec_b ? v : s;
-            live[r] = v_ok && sr < s_cnt && (!tri || j >= i);
-            // rectangle: i*nb + j ; triangle (i <= j < n): i*n - i(i-1)/2 + (j - i)
-            ord[r] = B.ord0 + (tri ? i * B.na - (i * (i - 1)) / 2 + (j - i) : i * B.nb + j);
-            live[r] = live[r] && ord[r] <= sep_now;
+            const int sr = min(g + r, s_cnt - 1);
+            const uint4 xs = s_rows[sr];
+            live[r] = g + r < s_live && (!prune || s_term[sr] + thread_term <= sep_now);
             const uint4 a = vec_b ? xs : xv, b = vec_b ? xv : xs;
             cand[r] = cm_apply<LW, OP>(a, b, P.valid);
+            known[r] = v_eq(cand[r], a) || v_eq(cand[r], b);
         }
-        insert_batch<LW>(P, wc, cand, ord, live);
+        insert_batch<LW>(P, wc, cand, live, known, ord_of);
     }
 }
 
-template <int LW>
-__global__ void __launch_bounds__(CTA_THREADS, 2) narrow_level_kernel(const NarrowParams P) {
+// One persistent launch per (level, operator): CTAs draw tiles of the operator's blocks from
+// a ticket counter in canonical order.  The operator is a template parameter so that each
+// kernel holds exactly one hot loop (a single kernel switching over all operators needed
+// > 240 registers); launches of one level run back to back on the stream, in canonical
+// operator order, with no host synchronisation in between.
+template <int LW, int OP>
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_kernel(const NarrowParams P) {
+    __shared__ BlockDesc B;
     __shared__ uint4 s_rows[TILE_S];
+    __shared__ u64 s_term[TILE_S];
     __shared__ uint32_t s_claims[(CTA_THREADS / 32) * WARP_BUF];
     __shared__ uint32_t s_fill[CTA_THREADS / 32];
+    __shared__ Parked s_queue[(CTA_THREADS / 32) * WARP_QUEUE];
+    __shared__ uint32_t s_qfill[CTA_THREADS / 32];
     __shared__ u64 s_ticket;
     __shared__ u64 s_sep;
     const int warp = threadIdx.x >> 5;
-    WarpClaims wc{s_claims + warp * WARP_BUF, s_fill + warp};
-    if ((threadIdx.x & 31) == 0) s_fill[warp] = 0;
+    const WarpCtx wc{s_claims + warp * WARP_BUF, s_fill + warp, s_queue + warp * WARP_QUEUE, s_qfill + warp};
+    if ((threadIdx.x & 31) == 0) {
+        s_fill[warp] = 0;
+        s_qfill[warp] = 0;
+    }
     __syncthreads();
     for (;;) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            u64 t = P.n_tiles;
-            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull) t = atomicAdd(&P.counters[CTR_TICKET], 1ull);
+            u64 t = P.tile_end;
+            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull) t = P.tile_begin + atomicAdd(&P.counters[P.ticket], 1ull);
             s_ticket = t;
             s_sep = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
+            if (t < P.tile_end) {
+                int bi = P.block_begin;
+                while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
+                B = P.blocks[bi];
+            }
         }
         __syncthreads();
         const u64 tile = s_ticket;
         const u64 sep_now = s_sep;
-        if (tile >= P.n_tiles) break;
-        int bi = 0;
-        while (bi + 1 < P.n_blocks && tile >= P.blocks[bi + 1].tile0) ++bi;
-        const BlockDesc B = P.blocks[bi];
+        if (tile >= P.tile_end) break;
         if (B.ord0 > sep_now) continue;  // the whole block is ordered after the separator
-        const u64 tl = tile - B.tile0;
-        if (B.kind == BK_UNARY) {
-            switch (B.op) {
-                case OP_ATOM: run_unary_tile<LW, OP_ATOM>(P, wc, B, tl, sep_now); break;
-                case OP_NOT: run_unary_tile<LW, OP_NOT>(P, wc, B, tl, sep_now); break;
-                case OP_NEXT: run_unary_tile<LW, OP_NEXT>(P, wc, B, tl, sep_now); break;
-                default: run_unary_tile<LW, OP_FUTURE>(P, wc, B, tl, sep_now); break;
-            }
-        } else {
-            switch (B.op) {
-                case OP_AND: run_binary_tile<LW, OP_AND>(P, wc, B, tl, s_rows, sep_now); break;
-                case OP_OR: run_binary_tile<LW, OP_OR>(P, wc, B, tl, s_rows, sep_now); break;
-                default: run_binary_tile<LW, OP_UNTIL>(P, wc, B, tl, s_rows, sep_now); break;
-            }
-        }
+        if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL)
+            run_binary_tile<LW, OP>(P, wc, B, tile - B.tile0, s_rows, s_term, sep_now);
+        else
+            run_unary_tile<LW, OP>(P, wc, B, tile - B.tile0, sep_now);
     }
-    claims_flush(P, wc, true);
+    claims_flush(P, WarpClaims{wc.claim_buf, wc.claim_fill}, true);
 }
 
 // ---- finalisation: order the level's winners by ordinal without a sort -------------
