@@ -70,6 +70,9 @@ typedef struct ltlb200_stats {
     uint64_t d2h_bytes;          /* bytes copied device->host since creation */
     uint32_t row_bytes;          /* CM bytes (T * lane_bits / 8) */
     uint32_t key_bytes;          /* CM bytes as stored in HBM (row_bytes padded to 16) */
+    double alloc_ms;             /* host time spent in device allocations */
+    double rebuild_host_ms;      /* host time spent issuing hash-set regrows */
+    double create_ms;            /* host time of ltlb200_create */
 } ltlb200_stats;
 
 /* ABI version of the loaded library (== LTLB200_ABI_VERSION it was built with). */
@@ -97,6 +100,10 @@ ltlb200_engine *ltlb200_create(int32_t trace_count, int32_t lane_bits, const uin
 
 /* Frees every device allocation of the handle. */
 void ltlb200_destroy(ltlb200_engine *e);
+
+/* Empties the store (a fresh CandidateStore on the same specification) while keeping the
+ * handle's device buffers, so that repeated searches do not re-allocate. */
+int ltlb200_reset(ltlb200_engine *e);
 
 /*
  * Replaces expand_level (engine.py:367-451) together with _tasks_for_level (:219-266),
@@ -138,6 +145,9 @@ int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t c
 
 /* CandidateStore.entry (engine.py:140-145): provenance of one global id. */
 int ltlb200_entry(ltlb200_engine *e, int64_t gid, int32_t *op, int64_t *left, int64_t *right);
+
+/* Returns the device blocks cached by destroyed / regrown handles on `device` to the driver. */
+void ltlb200_trim(int32_t device);
 
 /* approx_bytes of the reference's accounting (engine.py:131,442). */
 uint64_t ltlb200_approx_bytes(const ltlb200_engine *e);

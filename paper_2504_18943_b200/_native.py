@@ -26,6 +26,8 @@ EXPORTED_SYMBOLS = (
     "ltlb200_device_count",
     "ltlb200_create",
     "ltlb200_destroy",
+    "ltlb200_reset",
+    "ltlb200_trim",
     "ltlb200_expand_level",
     "ltlb200_now",
     "ltlb200_level_info",
@@ -57,6 +59,9 @@ class Stats(ctypes.Structure):
         ("d2h_bytes", ctypes.c_uint64),
         ("row_bytes", ctypes.c_uint32),
         ("key_bytes", ctypes.c_uint32),
+        ("alloc_ms", ctypes.c_double),
+        ("rebuild_host_ms", ctypes.c_double),
+        ("create_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -89,6 +94,10 @@ def load():
     L.ltlb200_create.argtypes = [i32, i32, p, p, p, i32, i32, u64, p]
     L.ltlb200_destroy.argtypes = [p]
     L.ltlb200_destroy.restype = None
+    L.ltlb200_trim.restype = None
+    L.ltlb200_trim.argtypes = [i32]
+    L.ltlb200_reset.restype = ctypes.c_int
+    L.ltlb200_reset.argtypes = [p]
     L.ltlb200_expand_level.restype = ctypes.c_int
     L.ltlb200_expand_level.argtypes = [p, i32, u32, i32, i64, u64, dbl,
                                        ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]

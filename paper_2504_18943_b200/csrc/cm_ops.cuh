@@ -102,18 +102,18 @@ __device__ __forceinline__ uint4 cm_apply(uint4 a, uint4 b, uint4 valid) {
     else return cm_until<LW>(a, b, valid);
 }
 
-// 64-bit mix of a 16-byte vector; `seed` chains vectors of a wide key
-__device__ __forceinline__ u64 hash_vec(uint4 k, u64 seed) {
-    u64 a = ((u64)k.y << 32 | k.x) ^ seed;
-    u64 b = ((u64)k.w << 32 | k.z);
-    a *= 0x9E3779B97F4A7C15ull;
-    a ^= a >> 29;
-    b *= 0xC2B2AE3D27D4EB4Full;
-    b ^= b >> 31;
-    u64 h = (a + b) * 0xD6E8FEB86659FD93ull;
-    h ^= h >> 32;
-    h *= 0xD6E8FEB86659FD93ull;
-    h ^= h >> 29;
+// 32-bit mix of a 16-byte vector (four multiply / xor-shift rounds, one per word); `seed`
+// chains the vectors of a wide key.  Hash sets here have < 2^32 slots, so 32 bits suffice,
+// and 32-bit IMADs are single instructions where a 64-bit multiply costs four.
+__device__ __forceinline__ uint32_t hash_vec(uint4 k, uint32_t seed) {
+    uint32_t h = (k.x ^ seed) * 0x9E3779B1u + k.y;
+    h ^= h >> 15;
+    h = h * 0x85EBCA77u + k.z;
+    h ^= h >> 13;
+    h = h * 0xC2B2AE3Du + k.w;
+    h ^= h >> 16;
+    h *= 0x27D4EB2Fu;
+    h ^= h >> 15;
     return h;
 }
 

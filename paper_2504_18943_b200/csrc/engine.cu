@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstring>
 #include <ctime>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -55,6 +57,102 @@ static u64 next_pow2(u64 x) {
     u64 p = 1;
     while (p < x) p <<= 1;
     return p;
+}
+
+// ---- process-wide device block cache ------------------------------------------------------
+// A search regrows its hash set and its cache every level, and a caller typically runs many
+// searches (one per specification, or one per benchmark step).  cudaMalloc/cudaFree cost
+// milliseconds per GB and synchronise the device, so freed blocks are kept here, rounded to
+// a few size classes per power of two, and handed to the next request of the same class.
+// After the first search of a given size no allocation reaches the driver.
+struct BlockCache {
+    std::mutex mu;
+    std::map<std::pair<int, u64>, std::vector<void *>> free_blocks;
+    std::map<int, u64> cached_bytes;
+
+    static u64 size_class(u64 bytes) {
+        if (bytes <= 4096) return 4096;
+        u64 p = next_pow2(bytes);           // 2^k >= bytes
+        if (bytes <= (1u << 20)) return p;  // small: plain powers of two
+        u64 q = p / 8;                      // large: eighths between 2^(k-1) and 2^k
+        return ((bytes + q - 1) / q) * q;
+    }
+    void *get(int dev, u64 cls) {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = free_blocks.find({dev, cls});
+        if (it == free_blocks.end() || it->second.empty()) return nullptr;
+        void *p = it->second.back();
+        it->second.pop_back();
+        cached_bytes[dev] -= cls;
+        return p;
+    }
+    void put(int dev, u64 cls, void *p) {
+        std::lock_guard<std::mutex> lock(mu);
+        free_blocks[{dev, cls}].push_back(p);
+        cached_bytes[dev] += cls;
+    }
+    u64 cached(int dev) {
+        std::lock_guard<std::mutex> lock(mu);
+        return cached_bytes[dev];
+    }
+    void trim(int dev) {  // give everything cached for `dev` back to the driver
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto &kv : free_blocks)
+            if (kv.first.first == dev) {
+                for (void *p : kv.second) cudaFree(p);
+                kv.second.clear();
+            }
+        cached_bytes[dev] = 0;
+    }
+};
+static BlockCache g_blocks;
+
+struct DeviceInfo {
+    int major = 0, sm_count = 0;
+    bool known = false;
+};
+static DeviceInfo device_info(int dev) {
+    static std::mutex mu;
+    static std::map<int, DeviceInfo> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    DeviceInfo &d = cache[dev];
+    if (!d.known) {
+        int major = 0, sms = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return DeviceInfo{};
+        }
+        d.major = major;
+        d.sm_count = sms;
+        d.known = true;
+    }
+    return d;
+}
+
+// pinned staging words for the per-level counter read-back, recycled across handles
+static std::mutex g_pinned_mu;
+static std::vector<u64 *> g_pinned_free;
+static u64 *pinned_get() {
+    {
+        std::lock_guard<std::mutex> lock(g_pinned_mu);
+        if (!g_pinned_free.empty()) {
+            u64 *p = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return p;
+        }
+    }
+    u64 *p = nullptr;
+    if (cudaMallocHost(&p, 64 * sizeof(u64)) != cudaSuccess) {
+        cudaGetLastError();
+        throw std::runtime_error("cudaMallocHost failed");
+    }
+    return p;
+}
+static void pinned_put(u64 *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lock(g_pinned_mu);
+    g_pinned_free.push_back(p);
 }
 
 // ---- small device kernels shared by both key widths --------------------------------
@@ -128,7 +226,8 @@ struct LevelMeta {
 template <typename T>
 struct DeviceArray {
     T *ptr = nullptr;
-    u64 cap = 0;  // elements
+    u64 cap = 0;    // elements
+    u64 bytes = 0;  // size class of the block
 };
 
 class Engine {
@@ -143,6 +242,7 @@ public:
     int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
+    void reset();
     int num_levels() const { return (int)levels_.size(); }
     u64 approx_bytes() const { return approx_bytes_; }
 
@@ -166,6 +266,8 @@ private:
     DeviceArray<uint32_t> sb_rank_;
     DeviceArray<uint32_t> scan_tmp_;
     DeviceArray<u64> sep_list_;
+    DeviceArray<uint8_t> misc_;
+    static constexpr u64 kMinSlots = 1ull << 16;
     u64 *d_counters_ = nullptr;
     BlockDesc *d_blocks_ = nullptr;
     static constexpr int kMaxBlocks = 512;
@@ -183,6 +285,10 @@ private:
     void reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems = 0);
     template <typename T>
     void release(DeviceArray<T> &a);
+    void *pool_alloc(u64 bytes);
+    void pool_free(void *p, u64 bytes);
+    void recycle_retired(bool synchronise);
+    std::vector<std::pair<void *, u64>> retired_;
     void plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &constructed, u64 &n_tiles);
     void rebuild_table(u64 slots);
     void read_counters();
@@ -192,43 +298,75 @@ private:
     u64 chunk_exact_separator(const LevelMeta &lv, u64 n_seps, u64 batch);
 };
 
+// Blocks come from the process-wide cache (see BlockCache); `bytes` must be a size class.
+void *Engine::pool_alloc(u64 bytes) {
+    const double t0 = monotonic_s();
+    void *p = g_blocks.get(device_, bytes);
+    if (!p) {
+        cudaError_t err = cudaMalloc(&p, bytes);
+        if (err != cudaSuccess) {  // make room by dropping cached blocks of other classes, once
+            cudaGetLastError();
+            CUDA_CHECK(cudaStreamSynchronize(stream_));
+            g_blocks.trim(device_);
+            err = cudaMalloc(&p, bytes);
+        }
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            st_.alloc_ms += 1e3 * (monotonic_s() - t0);
+            throw MemoryBudget(std::string("cudaMalloc failed: ") + cudaGetErrorString(err));
+        }
+    }
+    st_.alloc_ms += 1e3 * (monotonic_s() - t0);
+    return p;
+}
+
+// Stream-ordered reuse: a block released here may be handed out again to THIS handle while
+// earlier work of its stream still reads it, which is safe because the next user runs on
+// the same stream; blocks become visible to other handles only after the stream drained.
+void Engine::pool_free(void *p, u64 bytes) {
+    if (p) retired_.push_back({p, bytes});
+}
+
+void Engine::recycle_retired(bool synchronise) {
+    if (retired_.empty()) return;
+    if (synchronise) cudaStreamSynchronize(stream_);
+    for (auto &r : retired_) g_blocks.put(device_, r.second, r.first);
+    retired_.clear();
+}
+
 template <typename T>
 void Engine::release(DeviceArray<T> &a) {
     if (a.ptr) {
-        cudaFree(a.ptr);
-        held_ -= a.cap * sizeof(T);
+        pool_free(a.ptr, a.bytes);
+        held_ -= a.bytes;
     }
     a.ptr = nullptr;
     a.cap = 0;
+    a.bytes = 0;
 }
 
 // grow `a` to at least `want` elements; with keep, the first keep_elems survive
 template <typename T>
 void Engine::reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems) {
     if (want <= a.cap) return;
-    u64 cap = keep ? std::max(want, a.cap + a.cap / 2) : want;
-    u64 extra_needed = cap * sizeof(T) - (keep ? 0 : a.cap * sizeof(T));
-    if (held_ + extra_needed > budget_) {
-        cap = want;  // retry without head-room
-        extra_needed = cap * sizeof(T) - (keep ? 0 : a.cap * sizeof(T));
-        if (held_ + extra_needed > budget_) throw MemoryBudget("device memory budget exhausted");
+    u64 bytes = BlockCache::size_class(std::max<u64>(keep ? std::max(want, 2 * a.cap) : want, 1) * sizeof(T));
+    u64 extra = bytes - (keep ? 0 : a.bytes);
+    if (held_ + extra > budget_) {
+        bytes = BlockCache::size_class(want * sizeof(T));  // retry without head-room
+        extra = bytes - (keep ? 0 : a.bytes);
+        if (held_ + extra > budget_) throw MemoryBudget("device memory budget exhausted");
     }
     if (!keep) release(a);
-    T *p = nullptr;
-    cudaError_t err = cudaMalloc(&p, cap * sizeof(T));
-    if (err != cudaSuccess) {
-        cudaGetLastError();
-        throw MemoryBudget(std::string("cudaMalloc failed: ") + cudaGetErrorString(err));
-    }
-    held_ += cap * sizeof(T);
+    T *p = static_cast<T *>(pool_alloc(bytes));
+    held_ += bytes;
     if (keep && a.ptr) {
         if (keep_elems) CUDA_CHECK(cudaMemcpyAsync(p, a.ptr, keep_elems * sizeof(T), cudaMemcpyDeviceToDevice, stream_));
-        CUDA_CHECK(cudaStreamSynchronize(stream_));
-        cudaFree(a.ptr);
-        held_ -= a.cap * sizeof(T);
+        pool_free(a.ptr, a.bytes);  // recycled once the stream has drained
+        held_ -= a.bytes;
     }
     a.ptr = p;
-    a.cap = cap;
+    a.bytes = bytes;
+    a.cap = bytes / sizeof(T);
 }
 
 template <int LW>
@@ -252,50 +390,56 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
                int device, u64 budget, void *stream)
     : T_(T), lw_(lane_bits), row_bytes_(T * lane_bits / 8), key_words_((T * lane_bits / 8 + 7) / 8), n_atoms_(n_atoms),
       device_(device) {
+    const double t_create = monotonic_s();
     CUDA_CHECK(cudaSetDevice(device_));
-    cudaDeviceProp prop;
-    CUDA_CHECK(cudaGetDeviceProperties(&prop, device_));
-    if (prop.major != 10) throw CudaError("device is not sm_100 (Blackwell B200); this library has no other code path");
-    sm_count_ = prop.multiProcessorCount;
+    const DeviceInfo info = device_info(device_);
+    if (!info.known) throw CudaError("cannot query the CUDA device");
+    if (info.major != 10) throw CudaError("device is not sm_100 (Blackwell B200); this library has no other code path");
+    sm_count_ = info.sm_count;
     if (row_bytes_ > 16) throw std::invalid_argument("CMs wider than 16 bytes are not supported by this build");
     if (stream) stream_ = (cudaStream_t)stream;
     else {
         CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
         own_stream_ = true;
     }
-    size_t free_b = 0, total_b = 0;
-    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-    budget_ = budget ? budget : (u64)(free_b * 0.9);
+    if (budget) budget_ = budget;
+    else {  // 90% of what is free now, counting blocks parked in the process-wide cache as free
+        size_t free_b = 0, total_b = 0;
+        CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        budget_ = (u64)((free_b + g_blocks.cached(device_)) * 0.9);
+    }
     valid_ = pack_lanes16(masks, T, lane_bits);
     target_ = pack_lanes16(target, T, lane_bits);
     // the all-ones vector doubles as the empty-slot marker; it is a legal CM only when
     // the row fills the vector and every lane is fully valid
     special_possible_ = (valid_.x & valid_.y & valid_.z & valid_.w) == 0xFFFFFFFFu;
 
+    // one small block: counters | block descriptors | atom rows
+    const u64 off_blocks = 256, off_atoms = off_blocks + kMaxBlocks * sizeof(BlockDesc);
     std::vector<uint4> h_atoms(std::max(n_atoms, 1));
     for (int p = 0; p < n_atoms; ++p) h_atoms[p] = pack_lanes16(atoms + (size_t)p * T, T, lane_bits);
-    CUDA_CHECK(cudaMalloc(&d_atoms_, h_atoms.size() * sizeof(uint4)));
+    reserve(misc_, off_atoms + h_atoms.size() * sizeof(uint4), false);
+    d_counters_ = reinterpret_cast<u64 *>(misc_.ptr);
+    d_blocks_ = reinterpret_cast<BlockDesc *>(misc_.ptr + off_blocks);
+    d_atoms_ = reinterpret_cast<uint4 *>(misc_.ptr + off_atoms);
     CUDA_CHECK(cudaMemcpyAsync(d_atoms_, h_atoms.data(), h_atoms.size() * sizeof(uint4), cudaMemcpyHostToDevice, stream_));
     st_.h2d_bytes += h_atoms.size() * sizeof(uint4);
-    CUDA_CHECK(cudaMalloc(&d_counters_, CTR_COUNT * sizeof(u64)));
-    CUDA_CHECK(cudaMalloc(&d_blocks_, kMaxBlocks * sizeof(BlockDesc)));
-    CUDA_CHECK(cudaMallocHost(&h_counters_, CTR_COUNT * sizeof(u64)));
+    h_counters_ = pinned_get();
     for (auto &e : ev_) CUDA_CHECK(cudaEventCreate(&e));
     u64 init[CTR_COUNT];
     for (auto &c : init) c = 0;
     init[CTR_SPECIAL] = VAL_EMPTY;
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));
-    held_ += h_atoms.size() * sizeof(uint4) + CTR_COUNT * sizeof(u64) + kMaxBlocks * sizeof(BlockDesc);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_atoms / init leave scope
     occupancy_ = lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>();
-    rebuild_table(1 << 12);
+    rebuild_table(kMinSlots);
     st_.row_bytes = row_bytes_;
     st_.key_bytes = 16;
+    st_.create_ms = 1e3 * (monotonic_s() - t_create);
 }
 
 Engine::~Engine() {
     cudaSetDevice(device_);
-    if (stream_) cudaStreamSynchronize(stream_);
     release(store_);
     release(ords_);
     release(slots_);
@@ -304,10 +448,9 @@ Engine::~Engine() {
     release(sb_rank_);
     release(scan_tmp_);
     release(sep_list_);
-    cudaFree(d_atoms_);
-    cudaFree(d_counters_);
-    cudaFree(d_blocks_);
-    cudaFreeHost(h_counters_);
+    release(misc_);
+    recycle_retired(true);
+    pinned_put(h_counters_);
     for (auto &e : ev_)
         if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(stream_);
@@ -315,7 +458,8 @@ Engine::~Engine() {
 
 // Fresh table of `slots` entries holding every finalised CM (val = global id).
 void Engine::rebuild_table(u64 slots) {
-    slots = std::max<u64>(next_pow2(slots), 1 << 12);
+    const double t0 = monotonic_s();
+    slots = std::max<u64>(next_pow2(slots), kMinSlots);
     if (slots > (1ull << 32) - 2) throw MemoryBudget("hash set would exceed 2^32 slots");
     if (slots != slots_.cap) {
         release(slots_);
@@ -332,6 +476,19 @@ void Engine::rebuild_table(u64 slots) {
     }
     table_dirty_ = false;
     st_.table_rebuilds++;
+    st_.rebuild_host_ms += 1e3 * (monotonic_s() - t0);
+}
+
+// Forget every level but keep the device buffers (and the hash set's capacity) for the next search.
+void Engine::reset() {
+    CUDA_CHECK(cudaSetDevice(device_));
+    levels_.clear();
+    total_ = 0;
+    approx_bytes_ = 0;
+    last_constructed_ = 0;
+    rebuild_table(slots_.cap);
+    st_.constructed = 0;
+    st_.unique = 0;
 }
 
 void Engine::read_counters() {
@@ -360,8 +517,9 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.from_atoms = 1;
         b.na = (u64)n_atoms_;
         b.size = b.na;
-        b.tiles_v = ceil_div(b.na, (u64)CTA_THREADS * UNARY_ITEMS);
+        b.tiles_v = ceil_div(b.na, (u64)TILE_V * UNARY_ITEMS);
         b.tiles_s = 1;
+        b.vg = 1;
         push(b);
         return;
     }
@@ -376,8 +534,9 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.a_off = prev.base;
         b.na = prev.n;
         b.size = prev.n;
-        b.tiles_v = ceil_div(b.na, (u64)CTA_THREADS * UNARY_ITEMS);
+        b.tiles_v = ceil_div(b.na, (u64)TILE_V * UNARY_ITEMS);
         b.tiles_s = 1;
+        b.vg = 1;
         push(b);
     }
     for (int tag : binary_tags) {
@@ -404,8 +563,10 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
                 b.size = la.n * lb.n;
             }
             const u64 n_vec = b.vec_is_b ? b.nb : b.na, n_sc = b.vec_is_b ? b.na : b.nb;
-            b.tiles_v = ceil_div(n_vec, CTA_THREADS);
             b.tiles_s = ceil_div(n_sc, TILE_S);
+            // few scalar rows: widen the tile over several groups of 32 vector rows
+            b.vg = b.tiles_s == 1 ? (uint32_t)std::min<u64>(64, std::max<u64>(1, TILE_S / n_sc)) : 1u;
+            b.tiles_v = ceil_div(n_vec, (u64)TILE_V * b.vg);
             push(b);
         }
     }
@@ -541,7 +702,7 @@ void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
         P.tile_begin = lv.blocks[b0].tile0;
         P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
         P.ticket = CTR_TICKET0 + group;
-        const int grid = (int)std::min<u64>(P.tile_end - P.tile_begin, (u64)sm_count_ * occupancy_);
+        const int grid = (int)std::min<u64>((P.tile_end - P.tile_begin + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * occupancy_);
         const int op = (int)lv.blocks[b0].op;
         switch (lw_) {
             case 8: launch_op<8>(op, P, grid, stream_); break;
@@ -594,7 +755,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         for (int attempt = 0;; ++attempt) {
             const bool exact = est >= constructed;
             const u64 want_slots = next_pow2(2 * (total_ + est + (exact ? 0 : kSlack)));
-            if (want_slots > slots_.cap) rebuild_table(want_slots);
+            if (want_slots > slots_.cap) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most
             reserve(new_list_, est + (exact ? 64 : kSlack), false);
             if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
             u64 init[CTR_COUNT];
@@ -695,6 +856,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         float fms = 0;
         CUDA_CHECK(cudaEventElapsedTime(&fms, ev_[2], ev_[3]));
         st_.finalize_ms += fms;
+        recycle_retired(false);  // the stream has drained: blocks retired by regrows can be reused
         lv.n = h_counters_[CTR_WINNERS];
         sep_ord = h_counters_[CTR_SEP];
         if (sep_ord != VAL_EMPTY) *sep_gid = (int64_t)(total_ + h_counters_[CTR_SEPRANK]);
@@ -819,8 +981,7 @@ int ltlb200_device_count(void) {
     }
     int usable = 0;
     for (int d = 0; d < n; ++d) {
-        cudaDeviceProp p;
-        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++usable;
+        if (ltlb200::device_info(d).major == 10) ++usable;
     }
     if (!usable) g_last_error = "no sm_100 (B200) device visible";
     return usable;
@@ -875,6 +1036,20 @@ int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t c
 int ltlb200_entry(ltlb200_engine *e, int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
     if (!e || !op || !left || !right) return LTLB200_ERR_ARGUMENT;
     return guarded([&] { return e->impl->entry(gid, op, left, right); });
+}
+
+int ltlb200_reset(ltlb200_engine *e) {
+    if (!e) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        e->impl->reset();
+        return LTLB200_OK;
+    });
+}
+
+void ltlb200_trim(int32_t device) {
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    ltlb200::g_blocks.trim(device);
 }
 
 uint64_t ltlb200_approx_bytes(const ltlb200_engine *e) { return e ? e->impl->approx_bytes() : 0; }

@@ -12,28 +12,41 @@
 //   * val < 2^62  : global id of a CM finalised at an earlier level (immutable)
 //     val >= 2^62 : LEVEL_FLAG | ordinal of the best constructor seen so far this level
 //     so "first construction wins" is atomicMin on val, and duplicates of old CMs
-//     (the common case) cost one sector read and no atomic;
-//   * newly claimed slots are appended to a list through per-warp shared-memory
-//     buffers (one global atomic per 32 claims) for the finalisation kernels.
+//     (the common case) cost one sector read and no atomic.
+//
+// Execution shape (what the first ncu capture asked for): tiles are owned by WARPS, not
+// CTAs, so there is no block barrier anywhere; the hot loop issues exactly one probe per
+// candidate (PROBE_BATCH of them in flight per lane) and never loops on a probe chain;
+// whatever is not settled by that one probe -- a new CM, a collision, a same-level
+// duplicate, a separating candidate -- is parked in a per-warp shared-memory queue and
+// resolved in ROUNDS of 32 parked candidates, one per lane, re-compacted after every
+// probe step, so chains of different length never idle a warp's lanes.  Queue and claim
+// positions come from warp ballots, not from shared-memory atomics.
 #pragma once
 #include "cm_ops.cuh"
 
 namespace ltlb200 {
 
-constexpr int CTA_THREADS = 256;
-constexpr int TILE_S = 64;      // scalar-dimension rows of a binary tile (staged in shared memory)
 #ifndef LTLB200_PROBE_BATCH
 #define LTLB200_PROBE_BATCH 4
 #endif
 #ifndef LTLB200_MIN_CTAS
-#define LTLB200_MIN_CTAS 3
+#define LTLB200_MIN_CTAS 4
 #endif
-constexpr int PROBE_BATCH = LTLB200_PROBE_BATCH;  // hash probes each thread keeps in flight
-constexpr int UNARY_ITEMS = 8;  // candidates per thread in a unary tile
+#ifndef LTLB200_TILE_S
+#define LTLB200_TILE_S 128
+#endif
+constexpr int WARPS_PER_CTA = 4;
+constexpr int CTA_THREADS = 32 * WARPS_PER_CTA;
+constexpr int PROBE_BATCH = LTLB200_PROBE_BATCH;  // first probes each lane keeps in flight
+constexpr int TILE_V = 32;                        // vector-dimension rows of a tile: one per lane
+constexpr int TILE_S = LTLB200_TILE_S;            // scalar-dimension rows of a binary tile (staged in shared memory)
+constexpr int UNARY_ITEMS = 64;                   // candidates per lane in a unary tile
+constexpr int QUEUE_CAP = 32 * PROBE_BATCH + 32;
+constexpr int CLAIM_CAP = 64;
 constexpr u64 LEVEL_FLAG = 1ull << 62;
 constexpr u64 VAL_EMPTY = ~0ull;
 constexpr uint32_t SLOT_SPECIAL = 0xFFFFFFFFu;  // pseudo slot of the all-ones key
-constexpr int WARP_BUF = 32 + 32 * PROBE_BATCH;
 
 struct __align__(32) Slot16 {
     uint4 key;  // all ones = empty
@@ -47,14 +60,16 @@ enum : uint32_t { BK_UNARY = 0, BK_RECT = 1, BK_TRI = 2 };
 struct BlockDesc {
     uint32_t op;
     uint32_t kind;
-    uint32_t vec_is_b;  // binary blocks: thread dimension walks the right operand (j) if 1, else the left (i)
+    uint32_t vec_is_b;    // binary blocks: lane dimension walks the right operand (j) if 1, else the left (i)
     uint32_t from_atoms;  // unary source rows come from the atom table (cost 1)
-    u64 a_off, na;      // first global id and count of the left operand level (unary: the source level)
-    u64 b_off, nb;      // right operand level
-    u64 ord0;           // level-local ordinal of the block's first candidate
-    u64 size;           // candidates in the block
-    u64 tile0;          // first tile index of the block in the level's flattened tile space
+    u64 a_off, na;        // first global id and count of the left operand level (unary: the source level)
+    u64 b_off, nb;        // right operand level
+    u64 ord0;             // level-local ordinal of the block's first candidate
+    u64 size;             // candidates in the block
+    u64 tile0;            // first tile index of the block in the level's flattened tile space
     u64 tiles_v, tiles_s;
+    uint32_t vg;  // vector groups (of 32 rows) per tile; > 1 when the scalar operand has few rows
+    uint32_t pad_;
 };
 
 struct NarrowParams {
@@ -64,22 +79,23 @@ struct NarrowParams {
     u64 slot_mask;
     uint32_t *new_list;
     u64 new_list_cap;
-    u64 *counters;  // [0] tile ticket, [1] claimed slots, [2] separator ordinal (min), [3] special-key val, [4] overflow flag
+    u64 *counters;  // see CTR_*
     const BlockDesc *blocks;
     int block_begin, block_end;  // this launch's blocks (all of one operator)
     u64 tile_begin, tile_end;    // their tiles in the level's flattened tile space
     int ticket;                  // index of this launch's ticket counter
-    uint4 valid;   // Layout.masks packed
-    uint4 target;  // Layout.target packed
-    int prune_after_sep;  // non-exhaustive: skip work ordered after the best separator so far
+    uint4 valid;                 // Layout.masks packed
+    uint4 target;                // Layout.target packed
+    int prune_after_sep;         // non-exhaustive: skip work ordered after the best separator so far
     int special_possible;
     u64 claim_limit;
     u64 *sep_list;  // exhaustive runs: ordinals of every separating candidate (NULL otherwise)
     u64 sep_list_cap;
 };
 
-// [5] winners (summary), [6] rank of the separator (summary), [7] separating candidates recorded
-// [8..14] one tile ticket per operator launch
+// [1] claimed slots, [2] separator ordinal (min), [3] special-key val (persists across levels),
+// [4] overflow flag, [5] winners (summary), [6] rank of the separator (summary),
+// [7] separating candidates recorded, [8..14] one tile ticket per operator launch
 enum : int { CTR_UNUSED = 0, CTR_CLAIMED = 1, CTR_SEP = 2, CTR_SPECIAL = 3, CTR_OVERFLOW = 4, CTR_WINNERS = 5, CTR_SEPRANK = 6, CTR_SEPCOUNT = 7, CTR_TICKET0 = 8, CTR_COUNT = 16 };
 
 __device__ __forceinline__ uint4 ld_cg_u4(const uint4 *p) { return __ldcg(p); }
@@ -104,122 +120,99 @@ __device__ __forceinline__ uint4 cas128(uint4 *addr, uint4 expect, uint4 desired
 
 __device__ __forceinline__ bool key_is_empty(uint4 k) { return (k.x & k.y & k.z & k.w) == 0xFFFFFFFFu; }
 
-struct WarpClaims {
-    uint32_t *buf;   // WARP_BUF entries of this warp
-    uint32_t *fill;  // this warp's fill counter
+// ---- per-warp state -------------------------------------------------------------------
+
+struct __align__(16) Parked {
+    uint4 key;
+    u64 ord;
+    uint32_t slot;   // slot to look at next
+    uint32_t flags;  // PK_*
+};
+// PK_OLD: known duplicate of an earlier level (parked only because it separates)
+// PK_EMPTY: the first probe saw this slot empty, go straight to the CAS
+enum : uint32_t { PK_SEP = 1u, PK_OLD = 2u, PK_SPECIAL = 4u, PK_EMPTY = 8u };
+
+struct __align__(16) WarpShared {
+    Parked queue[QUEUE_CAP];
+    uint4 rows[TILE_S];  // scalar-operand rows of the current binary tile
+    u64 term[TILE_S];    // their ordinal terms
+    uint32_t claims[CLAIM_CAP];
+    BlockDesc block;
+    u64 ticket, sep_now;
 };
 
-__device__ __forceinline__ void claims_push(const WarpClaims &wc, uint32_t slot) {
-    uint32_t pos = atomicAdd(wc.fill, 1u);
-    wc.buf[pos] = slot;
+struct WarpState {  // warp-uniform registers
+    uint32_t qfill = 0, cfill = 0;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
-// warp-collective: move full groups of 32 claims (all of them when `all`) to the global list
-__device__ __forceinline__ void claims_flush(const NarrowParams &P, const WarpClaims &wc, bool all) {
-    __syncwarp();
+// warp-collective: move 32 claims (or all of them when `all`) to the global list
+__device__ __forceinline__ void claims_flush(const NarrowParams &P, WarpShared &ws, WarpState &st, bool all) {
     const int lane = threadIdx.x & 31;
-    uint32_t fill = *(volatile uint32_t *)wc.fill;
-    while (fill >= 32u || (all && fill > 0u)) {
-        uint32_t n = fill >= 32u ? 32u : fill;
+    while (st.cfill >= 32u || (all && st.cfill > 0u)) {
+        const uint32_t n = st.cfill >= 32u ? 32u : st.cfill;
         u64 base = 0;
         if (lane == 0) base = atomicAdd(&P.counters[CTR_CLAIMED], (u64)n);
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
         if (base + n > P.claim_limit || base + n > P.new_list_cap) {
             if (lane == 0) atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
         } else if ((uint32_t)lane < n) {
-            P.new_list[base + lane] = wc.buf[fill - n + lane];
+            P.new_list[base + lane] = ws.claims[st.cfill - n + lane];
         }
-        fill -= n;
+        st.cfill -= n;
     }
     __syncwarp();
-    if (lane == 0) *(volatile uint32_t *)wc.fill = fill;
-    __syncwarp();
 }
 
-// ---- deferred slow path -------------------------------------------------------------
-// The hot loop only decides, per candidate, between "duplicate of a CM finalised at an
-// earlier level" (the common case: nothing to write) and "needs work".  The latter are
-// parked in a per-warp shared-memory queue and drained by the whole warp after each
-// batch, one parked candidate per lane: the claim / atomicMin / separator code then runs
-// with full lanes and outside the hot loop's register budget.
-
-struct __align__(16) Parked {
-    uint4 key;
-    u64 ord;
-    uint32_t slot;   // where the probe stopped (empty slot or the slot holding `key`)
-    uint32_t flags;  // PK_*
-};
-enum : uint32_t { PK_SEP = 1u, PK_OLD = 2u, PK_SPECIAL = 4u };
-constexpr int WARP_QUEUE = 32 * PROBE_BATCH;
-
-struct WarpCtx {
-    uint32_t *claim_buf;   // WARP_BUF newly claimed slots waiting for a flush
-    uint32_t *claim_fill;
-    Parked *queue;         // WARP_QUEUE parked candidates
-    uint32_t *queue_fill;
-};
-
-__device__ __forceinline__ void park(const WarpCtx &w, uint4 key, u64 ord, u64 slot, uint32_t flags) {
-    const uint32_t pos = atomicAdd(w.queue_fill, 1u);
-    Parked e;
-    e.key = key;
-    e.ord = ord;
-    e.slot = (uint32_t)slot;
-    e.flags = flags;
-    w.queue[pos] = e;
-}
-
-// Insert (key -> min val) starting at `slot`; returns true when the CM was not stored by
-// an earlier level (fresh for this level).
-__device__ __forceinline__ bool table_claim(const NarrowParams &P, const WarpCtx &w, uint4 key, u64 val, u64 slot) {
-    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
-    const WarpClaims wc{w.claim_buf, w.claim_fill};
-    uint4 k0 = ld_cg_u4(&P.slots[slot].key);
-    u64 v0 = __ldcg(&P.slots[slot].val);
-    for (int probes = 0;; ++probes) {
-        if (v_eq(k0, key)) {
-            if (v0 > val) atomicMin(&P.slots[slot].val, val);
-            return v0 >= LEVEL_FLAG;
-        }
-        if (key_is_empty(k0)) {
-            uint4 old = cas128(&P.slots[slot].key, empty, key);
-            if (key_is_empty(old)) {
-                atomicMin(&P.slots[slot].val, val);
-                claims_push(wc, (uint32_t)slot);
-                return true;
-            }
-            if (v_eq(old, key)) {
-                atomicMin(&P.slots[slot].val, val);
-                return true;  // claimed this level by a concurrent constructor
-            }
-        }
-        if (probes > (1 << 16)) {  // table saturated: give up, the host regrows and redoes the level
-            atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
-            return false;
-        }
-        slot = (slot + 1) & P.slot_mask;
-        k0 = ld_cg_u4(&P.slots[slot].key);
-        v0 = __ldcg(&P.slots[slot].val);
-    }
-}
-
-// warp-collective: resolve every parked candidate, then flush full groups of claims
-__device__ __forceinline__ void drain_parked(const NarrowParams &P, const WarpCtx &w) {
-    __syncwarp();
+// One resolution round: the top (up to) 32 parked candidates take one probe step each.
+// Settled ones leave (recording claims / separators), the rest are re-queued compacted.
+__device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &ws, WarpState &st) {
     const int lane = threadIdx.x & 31;
-    const uint32_t n = *(volatile uint32_t *)w.queue_fill;
-    for (uint32_t idx = lane; idx < n; idx += 32) {
-        const Parked e = w.queue[idx];
+    const uint32_t lt = lanemask_lt();
+    const uint32_t take = st.qfill < 32u ? st.qfill : 32u;
+    const uint32_t base = st.qfill - take;
+    const bool active = (uint32_t)lane < take;
+    Parked e = ws.queue[base + (active ? lane : 0)];
+    __syncwarp();  // every lane holds its entry before the slots are reused
+    bool again = false, claimed = false, fresh = false;
+    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (active) {
         const u64 val = LEVEL_FLAG | e.ord;
-        bool fresh = false;
         if (e.flags & PK_SPECIAL) {
             const u64 old = atomicMin(&P.counters[CTR_SPECIAL], val);
-            if (old == VAL_EMPTY) claims_push(WarpClaims{w.claim_buf, w.claim_fill}, SLOT_SPECIAL);
+            claimed = old == VAL_EMPTY;
             fresh = old >= LEVEL_FLAG;
         } else if (!(e.flags & PK_OLD)) {
-            fresh = table_claim(P, w, e.key, val, e.slot);
+            Slot16 *slot = &P.slots[e.slot];
+            uint4 k = empty;
+            u64 v = VAL_EMPTY;
+            if (!(e.flags & PK_EMPTY)) {
+                k = ld_cg_u4(&slot->key);
+                v = __ldcg(&slot->val);
+            }
+            if (key_is_empty(k)) {
+                k = cas128(&slot->key, empty, e.key);
+                if (key_is_empty(k)) {
+                    claimed = true;
+                    k = e.key;
+                }
+                v = VAL_EMPTY;  // whoever claimed it this instant, the val is at best this level's
+            }
+            if (v_eq(k, e.key)) {
+                if (v > val) atomicMin(&slot->val, val);
+                fresh = v >= LEVEL_FLAG;
+            } else {  // another CM lives here: linear probing
+                again = true;
+                e.slot = (e.slot + 1) & (uint32_t)P.slot_mask;
+                e.flags &= ~PK_EMPTY;
+            }
         }
-        if (e.flags & PK_SEP) {
+        if (!again && (e.flags & PK_SEP)) {
             if (fresh) atomicMin(&P.counters[CTR_SEP], e.ord);
             if (P.sep_list) {  // exhaustive runs keep every separating ordinal (chunk-exact separator id)
                 const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
@@ -227,29 +220,35 @@ __device__ __forceinline__ void drain_parked(const NarrowParams &P, const WarpCt
             }
         }
     }
+    const uint32_t mq = __ballot_sync(0xFFFFFFFFu, again);
+    if (again) ws.queue[base + __popc(mq & lt)] = e;
+    st.qfill = base + __popc(mq);
+    const uint32_t mc = __ballot_sync(0xFFFFFFFFu, claimed);
+    if (claimed) ws.claims[st.cfill + __popc(mc & lt)] = (e.flags & PK_SPECIAL) ? SLOT_SPECIAL : e.slot;
+    st.cfill += __popc(mc);
     __syncwarp();
-    if (lane == 0) *(volatile uint32_t *)w.queue_fill = 0;
-    claims_flush(P, WarpClaims{w.claim_buf, w.claim_fill}, false);
+    if (st.cfill >= 32u) claims_flush(P, ws, st, false);
 }
 
-// Probe up to PROBE_BATCH candidates of one thread; all first probes are issued before
-// any is consumed so that a warp keeps 32*PROBE_BATCH sectors in flight.  Only the high
+// Probe PROBE_BATCH candidates of one lane with ONE sector read each (all issued before
+// any is consumed), settle the duplicates of earlier levels, park the rest.  Only the high
 // word of a slot's val is read: it alone tells "finalised at an earlier level" (< 2^62).
-// `known[r]`: the candidate equals one of its operands, i.e. a CM that is already in the
-// cache -- a duplicate by construction, no probe needed.  `ord_of(r)` recomputes the
-// ordinal for the few candidates that get parked, so ordinals hold no registers here.
+// `known[r]`: the candidate equals one of its operands, i.e. a CM already in the cache --
+// a duplicate by construction, no probe.  `ord_of(r)` recomputes the ordinal for the
+// candidates that get parked, so ordinals hold no registers in the hot loop.
 template <int LW, typename OrdOf>
-__device__ __forceinline__ void insert_batch(const NarrowParams &P, const WarpCtx &w,
+__device__ __forceinline__ void insert_batch(const NarrowParams &P, WarpShared &ws, WarpState &st,
                                              const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
                                              const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
     constexpr uint32_t FLAG_HI = (uint32_t)(LEVEL_FLAG >> 32);
     const uint32_t mask32 = (uint32_t)P.slot_mask;
+    const uint32_t lt = lanemask_lt();
     uint32_t slot[PROBE_BATCH];
     uint4 k0[PROBE_BATCH];
     uint32_t vhi[PROBE_BATCH];
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        slot[r] = (uint32_t)hash_vec(cand[r], 0) & mask32;
+        slot[r] = hash_vec(cand[r], 0u) & mask32;
         if (live[r] && !known[r]) {
             k0[r] = ld_cg_u4(&P.slots[slot[r]].key);
             vhi[r] = __ldcg(reinterpret_cast<const uint32_t *>(&P.slots[slot[r]].val) + 1);
@@ -257,44 +256,57 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, const WarpCt
     }
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        if (!live[r]) continue;
         uint32_t flags = cm_sep_diff<LW>(cand[r], P.target) == 0u ? PK_SEP : 0u;
         uint32_t s = slot[r];
         if (known[r]) {
             flags |= PK_OLD;
         } else if (P.special_possible && key_is_empty(cand[r])) {
             flags |= PK_SPECIAL;
-        } else {
-            uint4 k = k0[r];
-            uint32_t v = vhi[r];
-            while (!v_eq(k, cand[r]) && !key_is_empty(k)) {  // linear probing past other CMs
-                s = (s + 1) & mask32;
-                k = ld_cg_u4(&P.slots[s].key);
-                v = __ldcg(reinterpret_cast<const uint32_t *>(&P.slots[s].val) + 1);
+        } else if (live[r]) {
+            if (v_eq(k0[r], cand[r])) {
+                if (vhi[r] < FLAG_HI) flags |= PK_OLD;  // duplicate of an earlier level: settled
+            } else if (key_is_empty(k0[r])) {
+                flags |= PK_EMPTY;
+            } else {
+                s = (s + 1) & mask32;  // collision: continue at the next slot
             }
-            if (v_eq(k, cand[r]) && v < FLAG_HI) flags |= PK_OLD;  // duplicate of an earlier level
         }
-        if (flags != PK_OLD) park(w, cand[r], ord_of(r), s, flags);
+        const bool need = live[r] && flags != PK_OLD;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
+        if (need) {
+            Parked e;
+            e.key = cand[r];
+            e.ord = ord_of(r);
+            e.slot = s;
+            e.flags = flags;
+            ws.queue[st.qfill + __popc(m & lt)] = e;
+        }
+        st.qfill += __popc(m);
     }
-    drain_parked(P, w);
+    __syncwarp();
+    while (st.qfill >= 32u) drain_round(P, ws, st);
 }
 
 template <int LW, int OP>
-__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, const WarpCtx &wc, const BlockDesc &B,
-                                               u64 tile_local, u64 sep_now) {
+__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WarpShared &ws, WarpState &st, u64 tile_local,
+                                               u64 sep_now) {
+    const BlockDesc &B = ws.block;
+    const int lane = threadIdx.x & 31;
     const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off;
-    const u64 first = tile_local * (u64)(CTA_THREADS * UNARY_ITEMS) + threadIdx.x;
-    const u64 ord0 = B.ord0;
+    const u64 first = tile_local * (u64)(TILE_V * UNARY_ITEMS) + lane;
+    const u64 ord0 = B.ord0, n = B.na;
+    if (ord0 + tile_local * (u64)(TILE_V * UNARY_ITEMS) > sep_now) return;  // tile ordered after the separator
+    const int n_groups = (int)min((u64)UNARY_ITEMS, (n - tile_local * (u64)(TILE_V * UNARY_ITEMS) + TILE_V - 1) / TILE_V);
 #pragma unroll 1
-    for (int g = 0; g < UNARY_ITEMS; g += PROBE_BATCH) {
+    for (int g = 0; g < n_groups; g += PROBE_BATCH) {
         uint4 cand[PROBE_BATCH];
         bool live[PROBE_BATCH], known[PROBE_BATCH];
         uint4 x[PROBE_BATCH];
-        auto ord_of = [&](int r) { return ord0 + first + (u64)(g + r) * CTA_THREADS; };
+        auto ord_of = [&](int r) { return ord0 + first + (u64)(g + r) * TILE_V; };
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
-            const u64 i = first + (u64)(g + r) * CTA_THREADS;
-            live[r] = i < B.na && ord0 + i <= sep_now;
+            const u64 i = first + (u64)(g + r) * TILE_V;
+            live[r] = g + r < n_groups && i < n;
             x[r] = live[r] ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
@@ -302,110 +314,117 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, const Warp
             cand[r] = cm_apply<LW, OP>(x[r], x[r], P.valid);
             known[r] = OP != OP_ATOM && v_eq(cand[r], x[r]);
         }
-        insert_batch<LW>(P, wc, cand, live, known, ord_of);
+        insert_batch<LW>(P, ws, st, cand, live, known, ord_of);
     }
 }
 
-// Binary tile: each thread keeps one row of the "vector" operand in registers and walks
-// up to TILE_S rows of the "scalar" operand staged in shared memory together with the
-// row's ordinal term, so that a candidate's ordinal is one 64-bit add:
+// Binary tile: each lane keeps one row of the "vector" operand in registers and walks up
+// to TILE_S rows of the "scalar" operand staged in the warp's shared memory together with
+// the row's ordinal term, so that a candidate's ordinal is one 64-bit add:
 //   rectangle  ord = ord0 + i*nb + j          triangle (i <= j < n)  ord = ord0 + i*n - i(i-1)/2 + (j - i)
-template <int LW, int OP>
-__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, const WarpCtx &wc, const BlockDesc &B,
-                                                u64 tile_local, uint4 *s_rows, u64 *s_term, u64 sep_now) {
+// When the scalar operand has few rows (an early, small level) a tile takes B.vg groups
+// of 32 vector rows against the same staged rows, so tiles stay a few thousand candidates.
+// VEC_B: the lane dimension walks the right operand; irrelevant for the commutative ones.
+template <int LW, int OP, bool VEC_B>
+__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WarpShared &ws, WarpState &st, u64 tile_local,
+                                                u64 sep_now) {
+    const BlockDesc &B = ws.block;
+    const int lane = threadIdx.x & 31;
     const bool tri = B.kind == BK_TRI;
-    const bool vec_b = B.vec_is_b != 0;
+    const uint32_t vg_n = B.vg;
     // tile order follows the canonical order: left operand (i) outer, right operand (j) inner
     u64 tv, ts;
-    if (vec_b) { ts = tile_local / B.tiles_v; tv = tile_local % B.tiles_v; }
+    if (VEC_B) { ts = tile_local / B.tiles_v; tv = tile_local % B.tiles_v; }
     else { tv = tile_local / B.tiles_s; ts = tile_local % B.tiles_s; }
-    const u64 n_vec = vec_b ? B.nb : B.na, n_sc = vec_b ? B.na : B.nb;
-    const u64 v0 = tv * CTA_THREADS, s0 = ts * TILE_S;
+    const u64 n_vec = VEC_B ? B.nb : B.na, n_sc = VEC_B ? B.na : B.nb;
+    const u64 v0 = tv * (u64)(TILE_V * vg_n), s0 = ts * TILE_S;
     const int s_cnt = (int)min((u64)TILE_S, n_sc - s0);
-    if (tri && v0 + CTA_THREADS - 1 < s0) return;  // tile entirely below the diagonal (j < i)
-    const uint4 *vec_rows = P.store + (vec_b ? B.b_off : B.a_off);
-    const uint4 *sc_rows = P.store + (vec_b ? B.a_off : B.b_off);
-    __syncthreads();  // previous tile's readers of the staged rows are done
-    if ((int)threadIdx.x < s_cnt) {
-        const u64 s = s0 + threadIdx.x;
-        s_rows[threadIdx.x] = __ldg(sc_rows + s);
-        // scalar-row part of the ordinal; the thread part is j (vec_b) or ord0 + i*nb (!vec_b)
-        s_term[threadIdx.x] = !vec_b ? s : B.ord0 + (tri ? s * B.na - (s ? (s * (s - 1)) / 2 : 0) - s : s * B.nb);
+    if (tri && v0 + (u64)TILE_V * vg_n - 1 < s0) return;  // tile entirely below the diagonal (j < i)
+    const u64 ord0 = B.ord0, na = B.na, nb = B.nb;
+    // a lower bound of the tile's ordinals: skip tiles ordered after the separator
+    const u64 tile_min = ord0 + (VEC_B ? (tri ? s0 * na - (s0 ? (s0 * (s0 - 1)) / 2 : 0) : s0 * nb + v0) : v0 * nb + s0);
+    if (tile_min > sep_now) return;
+    const uint4 *vec_rows = P.store + (VEC_B ? B.b_off : B.a_off);
+    const uint4 *sc_rows = P.store + (VEC_B ? B.a_off : B.b_off);
+    __syncwarp();
+    for (int k = lane; k < s_cnt; k += 32) {
+        const u64 s = s0 + k;
+        ws.rows[k] = __ldg(sc_rows + s);
+        // scalar-row part of the ordinal; the lane part is j (VEC_B) or ord0 + i*nb (!VEC_B)
+        ws.term[k] = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
     }
-    __syncthreads();
-    const u64 v = v0 + threadIdx.x;
-    const bool v_ok = v < n_vec;
-    const uint4 xv = v_ok ? __ldg(vec_rows + v) : make_uint4(0, 0, 0, 0);
-    const u64 thread_term = vec_b ? v : B.ord0 + v * B.nb;
-    // triangle: row s0+sr pairs with columns j >= i only
-    const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
-    const int s_live = v_ok ? first_bad : 0;
-    const bool prune = sep_now != ~0ull;
+    __syncwarp();
 #pragma unroll 1
-    for (int g = 0; g < s_cnt; g += PROBE_BATCH) {
-        uint4 cand[PROBE_BATCH];
-        bool live[PROBE_BATCH], known[PROBE_BATCH];
-        auto ord_of = [&](int r) { return s_term[min(g + r, s_cnt - 1)] + thread_term; };
+    for (uint32_t vg = 0; vg < vg_n; ++vg) {
+        const u64 v = v0 + (u64)vg * TILE_V + lane;
+        if (v0 + (u64)vg * TILE_V >= n_vec) break;
+        const bool v_ok = v < n_vec;
+        const uint4 xv = v_ok ? __ldg(vec_rows + v) : make_uint4(0, 0, 0, 0);
+        const u64 lane_term = VEC_B ? v : ord0 + v * nb;
+        // triangle: row s0+sr pairs with columns j >= i only
+        const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
+        const int s_live = v_ok ? first_bad : 0;
+#pragma unroll 1
+        for (int g = 0; g < s_cnt; g += PROBE_BATCH) {
+            uint4 cand[PROBE_BATCH];
+            bool live[PROBE_BATCH], known[PROBE_BATCH];
+            auto ord_of = [&](int r) { return ws.term[min(g + r, s_cnt - 1)] + lane_term; };
 #pragma unroll
-        for (int r = 0; r < PROBE_BATCH; ++r) {
-            const int sr = min(g + r, s_cnt - 1);
-            const uint4 xs = s_rows[sr];
-            live[r] = g + r < s_live && (!prune || s_term[sr] + thread_term <= sep_now);
-            const uint4 a = vec_b ? xs : xv, b = vec_b ? xv : xs;
-            cand[r] = cm_apply<LW, OP>(a, b, P.valid);
-            known[r] = v_eq(cand[r], a) || v_eq(cand[r], b);
+            for (int r = 0; r < PROBE_BATCH; ++r) {
+                const uint4 xs = ws.rows[min(g + r, s_cnt - 1)];
+                live[r] = g + r < s_live;
+                cand[r] = VEC_B ? cm_apply<LW, OP>(xs, xv, P.valid) : cm_apply<LW, OP>(xv, xs, P.valid);
+                known[r] = v_eq(cand[r], xs) || v_eq(cand[r], xv);
+            }
+            insert_batch<LW>(P, ws, st, cand, live, known, ord_of);
         }
-        insert_batch<LW>(P, wc, cand, live, known, ord_of);
     }
 }
 
-// One persistent launch per (level, operator): CTAs draw tiles of the operator's blocks from
-// a ticket counter in canonical order.  The operator is a template parameter so that each
-// kernel holds exactly one hot loop (a single kernel switching over all operators needed
-// > 240 registers); launches of one level run back to back on the stream, in canonical
-// operator order, with no host synchronisation in between.
+// One persistent launch per (level, operator): WARPS draw tiles of the operator's blocks
+// from a ticket counter in canonical order.  The operator is a template parameter so that
+// each kernel holds exactly one hot loop (a single kernel switching over all operators
+// needed > 240 registers); launches of one level run back to back on the stream, in
+// canonical operator order, with no host synchronisation in between.
 template <int LW, int OP>
 __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_kernel(const NarrowParams P) {
-    __shared__ BlockDesc B;
-    __shared__ uint4 s_rows[TILE_S];
-    __shared__ u64 s_term[TILE_S];
-    __shared__ uint32_t s_claims[(CTA_THREADS / 32) * WARP_BUF];
-    __shared__ uint32_t s_fill[CTA_THREADS / 32];
-    __shared__ Parked s_queue[(CTA_THREADS / 32) * WARP_QUEUE];
-    __shared__ uint32_t s_qfill[CTA_THREADS / 32];
-    __shared__ u64 s_ticket;
-    __shared__ u64 s_sep;
-    const int warp = threadIdx.x >> 5;
-    const WarpCtx wc{s_claims + warp * WARP_BUF, s_fill + warp, s_queue + warp * WARP_QUEUE, s_qfill + warp};
-    if ((threadIdx.x & 31) == 0) {
-        s_fill[warp] = 0;
-        s_qfill[warp] = 0;
-    }
-    __syncthreads();
+    __shared__ WarpShared s_warp[WARPS_PER_CTA];
+    WarpShared &ws = s_warp[threadIdx.x >> 5];
+    WarpState st;
+    const int lane = threadIdx.x & 31;
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        __syncwarp();
+        if (lane == 0) {
             u64 t = P.tile_end;
             if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull) t = P.tile_begin + atomicAdd(&P.counters[P.ticket], 1ull);
-            s_ticket = t;
-            s_sep = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
+            ws.ticket = t;
+            ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
             if (t < P.tile_end) {
                 int bi = P.block_begin;
                 while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
-                B = P.blocks[bi];
+                ws.block = P.blocks[bi];
             }
         }
-        __syncthreads();
-        const u64 tile = s_ticket;
-        const u64 sep_now = s_sep;
+        __syncwarp();
+        const u64 tile = ws.ticket;
+        const u64 sep_now = ws.sep_now;
         if (tile >= P.tile_end) break;
-        if (B.ord0 > sep_now) continue;  // the whole block is ordered after the separator
-        if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL)
-            run_binary_tile<LW, OP>(P, wc, B, tile - B.tile0, s_rows, s_term, sep_now);
-        else
-            run_unary_tile<LW, OP>(P, wc, B, tile - B.tile0, sep_now);
+        if (ws.block.ord0 > sep_now) continue;  // the whole block is ordered after the separator
+        const u64 tile_local = tile - ws.block.tile0;
+        if constexpr (OP == OP_AND || OP == OP_OR) {
+            // commutative: which operand sits in the lanes does not change the result, only the ordinal
+            if (ws.block.vec_is_b) run_binary_tile<LW, OP, true>(P, ws, st, tile_local, sep_now);
+            else run_binary_tile<LW, OP, false>(P, ws, st, tile_local, sep_now);
+        } else if constexpr (OP == OP_UNTIL) {
+            if (ws.block.vec_is_b) run_binary_tile<LW, OP, true>(P, ws, st, tile_local, sep_now);
+            else run_binary_tile<LW, OP, false>(P, ws, st, tile_local, sep_now);
+        } else {
+            run_unary_tile<LW, OP>(P, ws, st, tile_local, sep_now);
+        }
     }
-    claims_flush(P, WarpClaims{wc.claim_buf, wc.claim_fill}, true);
+    if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+        while (st.qfill > 0u) drain_round(P, ws, st);
+    claims_flush(P, ws, st, true);
 }
 
 // ---- finalisation: order the level's winners by ordinal without a sort -------------
@@ -418,12 +437,12 @@ struct FinalizeParams {
     const uint32_t *new_list;
     u64 n_claimed;
     u64 *counters;
-    uint32_t *bitmap;        // one bit per ordinal
-    const uint32_t *sb_rank; // exclusive popcount prefix per 32-word superblock
-    u64 ord_limit;           // keep ordinals <= limit (separator in a non-exhaustive run, else all ones)
+    uint32_t *bitmap;         // one bit per ordinal
+    const uint32_t *sb_rank;  // exclusive popcount prefix per 32-word superblock
+    u64 ord_limit;            // keep ordinals <= limit (separator in a non-exhaustive run, else all ones)
     uint4 *store;
     u64 *ords;
-    u64 base;                // global id of the level's first entry
+    u64 base;  // global id of the level's first entry
 };
 
 __device__ __forceinline__ u64 claimed_val(const FinalizeParams &F, uint32_t slot) {
@@ -468,7 +487,7 @@ __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 
             counters[CTR_SPECIAL] = gid;
             continue;
         }
-        u64 slot = hash_vec(key, 0) & slot_mask;
+        u64 slot = hash_vec(key, 0u) & slot_mask;
         for (;;) {
             uint4 old = cas128(&slots[slot].key, empty, key);
             if (key_is_empty(old)) {

@@ -160,6 +160,11 @@ class CandidateStore:
 
     __del__ = close
 
+    def reset(self):
+        """Empty the store but keep its device buffers (a fresh store on the same specification)."""
+        _native.check(_native.load().ltlb200_reset(self._handle), "reset")
+        self.levels = []
+
     # -- reference-shaped accessors -------------------------------------------------
     @property
     def total(self) -> int:

@@ -48,7 +48,8 @@ def main():
         st = store.device_stats()
         print(json.dumps(dict(rep=rep, wall_s=round(wall, 4), constructed=stats.constructed, unique=store.total,
                               enum_ms=round(st["enumerate_ms"], 3), fin_ms=round(st["finalize_ms"], 3),
-                              cand_per_s=round(stats.constructed / wall), launches=st["kernel_launches"])), flush=True)
+                              cand_per_s=round(stats.constructed / wall), launches=st["kernel_launches"],
+                              alloc_ms=round(st["alloc_ms"], 3), rebuild_host_ms=round(st["rebuild_host_ms"], 3), create_ms=round(st["create_ms"], 3), rebuilds=st["table_rebuilds"])), flush=True)
         store.close()
 
 
