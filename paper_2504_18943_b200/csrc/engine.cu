@@ -27,6 +27,7 @@
 
 #include "../../include/ltlsynth_b200.h"
 #include "narrow.cuh"
+#include "wide.cuh"
 
 namespace ltlb200 {
 
@@ -255,6 +256,9 @@ private:
     u64 budget_ = 0, held_ = 0;
     uint4 valid_{}, target_{};
     bool special_possible_ = false;
+    bool wide_ = false;  // CMs of more than one uint4
+    int nvec_ = 1, log2g_ = 0;
+    uint4 *d_valid_ = nullptr, *d_target_ = nullptr;
 
     // device state
     uint4 *d_atoms_ = nullptr;
@@ -262,6 +266,10 @@ private:
     DeviceArray<u64> ords_;
     DeviceArray<Slot16> slots_;
     DeviceArray<uint32_t> new_list_;
+    DeviceArray<u64> wslots_;          // wide path: slot words
+    DeviceArray<uint4> stage_rows_;    // wide path: this level's new rows
+    DeviceArray<u64> stage_ord_;
+    DeviceArray<uint32_t> stage_slot_;
     DeviceArray<uint32_t> bitmap_;
     DeviceArray<uint32_t> sb_rank_;
     DeviceArray<uint32_t> scan_tmp_;
@@ -295,6 +303,8 @@ private:
     void decode(const LevelMeta &lv, u64 ord, int32_t *op, int64_t *left, int64_t *right) const;
     u64 constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) const;
     void launch_enumerate(NarrowParams P, const LevelMeta &lv);
+    void launch_enumerate_wide(WideParams P, const LevelMeta &lv);
+    u64 table_slots() const { return wide_ ? wslots_.cap : slots_.cap; }
     u64 chunk_exact_separator(const LevelMeta &lv, u64 n_seps, u64 batch);
 };
 
@@ -377,13 +387,12 @@ static int occupancy_of() {
     return best;
 }
 
-static uint4 pack_lanes16(const uint64_t *lanes, int T, int lane_bits) {
-    uint8_t bytes[16] = {0};
+// byte image of one CM row (T lanes, little endian), zero padded to nvec uint4 vectors
+static void pack_row(const uint64_t *lanes, int T, int lane_bits, int nvec, uint4 *out) {
+    std::vector<uint8_t> bytes((size_t)nvec * 16, 0);
     const int lb = lane_bits / 8;
-    for (int t = 0; t < T; ++t) memcpy(bytes + t * lb, &lanes[t], lb);
-    uint4 v;
-    memcpy(&v, bytes, 16);
-    return v;
+    for (int t = 0; t < T; ++t) memcpy(bytes.data() + (size_t)t * lb, &lanes[t], lb);
+    memcpy(out, bytes.data(), bytes.size());
 }
 
 Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *target, const uint64_t *atoms, int n_atoms,
@@ -396,7 +405,10 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     if (!info.known) throw CudaError("cannot query the CUDA device");
     if (info.major != 10) throw CudaError("device is not sm_100 (Blackwell B200); this library has no other code path");
     sm_count_ = info.sm_count;
-    if (row_bytes_ > 16) throw std::invalid_argument("CMs wider than 16 bytes are not supported by this build");
+    nvec_ = (row_bytes_ + 15) / 16;
+    wide_ = nvec_ > 1;
+    if (nvec_ > MAX_NVEC) throw std::invalid_argument("CMs wider than 512 bytes are not supported");
+    for (log2g_ = wide_ ? 1 : 0; (1 << log2g_) < nvec_; ++log2g_) {}
     if (stream) stream_ = (cudaStream_t)stream;
     else {
         CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -408,33 +420,40 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
         CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
         budget_ = (u64)((free_b + g_blocks.cached(device_)) * 0.9);
     }
-    valid_ = pack_lanes16(masks, T, lane_bits);
-    target_ = pack_lanes16(target, T, lane_bits);
+    std::vector<uint4> h_valid(nvec_), h_target(nvec_);
+    pack_row(masks, T, lane_bits, nvec_, h_valid.data());
+    pack_row(target, T, lane_bits, nvec_, h_target.data());
+    valid_ = h_valid[0];
+    target_ = h_target[0];
     // the all-ones vector doubles as the empty-slot marker; it is a legal CM only when
     // the row fills the vector and every lane is fully valid
     special_possible_ = (valid_.x & valid_.y & valid_.z & valid_.w) == 0xFFFFFFFFu;
 
-    // one small block: counters | block descriptors | atom rows
-    const u64 off_blocks = 256, off_atoms = off_blocks + kMaxBlocks * sizeof(BlockDesc);
-    std::vector<uint4> h_atoms(std::max(n_atoms, 1));
-    for (int p = 0; p < n_atoms; ++p) h_atoms[p] = pack_lanes16(atoms + (size_t)p * T, T, lane_bits);
-    reserve(misc_, off_atoms + h_atoms.size() * sizeof(uint4), false);
+    // one small block: counters | block descriptors | masks | target | atom rows
+    const u64 off_blocks = 256, off_rows = off_blocks + kMaxBlocks * sizeof(BlockDesc);
+    std::vector<uint4> h_rows((size_t)(2 + std::max(n_atoms, 1)) * nvec_);
+    memcpy(h_rows.data(), h_valid.data(), (size_t)nvec_ * 16);
+    memcpy(h_rows.data() + nvec_, h_target.data(), (size_t)nvec_ * 16);
+    for (int p = 0; p < n_atoms; ++p) pack_row(atoms + (size_t)p * T, T, lane_bits, nvec_, h_rows.data() + (size_t)(2 + p) * nvec_);
+    reserve(misc_, off_rows + h_rows.size() * sizeof(uint4), false);
     d_counters_ = reinterpret_cast<u64 *>(misc_.ptr);
     d_blocks_ = reinterpret_cast<BlockDesc *>(misc_.ptr + off_blocks);
-    d_atoms_ = reinterpret_cast<uint4 *>(misc_.ptr + off_atoms);
-    CUDA_CHECK(cudaMemcpyAsync(d_atoms_, h_atoms.data(), h_atoms.size() * sizeof(uint4), cudaMemcpyHostToDevice, stream_));
-    st_.h2d_bytes += h_atoms.size() * sizeof(uint4);
+    d_valid_ = reinterpret_cast<uint4 *>(misc_.ptr + off_rows);
+    d_target_ = d_valid_ + nvec_;
+    d_atoms_ = d_target_ + nvec_;
+    CUDA_CHECK(cudaMemcpyAsync(d_valid_, h_rows.data(), h_rows.size() * sizeof(uint4), cudaMemcpyHostToDevice, stream_));
+    st_.h2d_bytes += h_rows.size() * sizeof(uint4);
     h_counters_ = pinned_get();
     for (auto &e : ev_) CUDA_CHECK(cudaEventCreate(&e));
     u64 init[CTR_COUNT];
     for (auto &c : init) c = 0;
     init[CTR_SPECIAL] = VAL_EMPTY;
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_atoms / init leave scope
-    occupancy_ = lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>();
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_rows / init leave scope
+    occupancy_ = wide_ ? 4 : (lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>());
     rebuild_table(kMinSlots);
     st_.row_bytes = row_bytes_;
-    st_.key_bytes = 16;
+    st_.key_bytes = 16 * nvec_;
     st_.create_ms = 1e3 * (monotonic_s() - t_create);
 }
 
@@ -444,6 +463,10 @@ Engine::~Engine() {
     release(ords_);
     release(slots_);
     release(new_list_);
+    release(wslots_);
+    release(stage_rows_);
+    release(stage_ord_);
+    release(stage_slot_);
     release(bitmap_);
     release(sb_rank_);
     release(scan_tmp_);
@@ -461,18 +484,34 @@ void Engine::rebuild_table(u64 slots) {
     const double t0 = monotonic_s();
     slots = std::max<u64>(next_pow2(slots), kMinSlots);
     if (slots > (1ull << 32) - 2) throw MemoryBudget("hash set would exceed 2^32 slots");
-    if (slots != slots_.cap) {
-        release(slots_);
-        reserve(slots_, slots, false);
-    }
-    CUDA_CHECK(cudaMemsetAsync(slots_.ptr, 0xFF, slots_.cap * sizeof(Slot16), stream_));
-    u64 special = VAL_EMPTY;
-    CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SPECIAL, &special, sizeof(u64), cudaMemcpyHostToDevice, stream_));
-    if (total_) {
-        int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
-        narrow_rebuild_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, store_.ptr, 0, total_, d_counters_);
-        CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches++;
+    if (wide_) {
+        if (slots != wslots_.cap) {
+            release(wslots_);
+            reserve(wslots_, slots, false);
+            wslots_.cap = slots;  // capacity must stay a power of two
+        }
+        CUDA_CHECK(cudaMemsetAsync(wslots_.ptr, 0, wslots_.cap * sizeof(u64), stream_));
+        if (total_) {
+            int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
+            wide_rebuild_kernel<<<grid, 256, 0, stream_>>>(wslots_.ptr, wslots_.cap - 1, store_.ptr, total_, nvec_, log2g_);
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+        }
+    } else {
+        if (slots != slots_.cap) {
+            release(slots_);
+            reserve(slots_, slots, false);
+            slots_.cap = slots;  // capacity must stay a power of two
+        }
+        CUDA_CHECK(cudaMemsetAsync(slots_.ptr, 0xFF, slots_.cap * sizeof(Slot16), stream_));
+        u64 special = VAL_EMPTY;
+        CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SPECIAL, &special, sizeof(u64), cudaMemcpyHostToDevice, stream_));
+        if (total_) {
+            int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
+            narrow_rebuild_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, store_.ptr, 0, total_, d_counters_);
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+        }
     }
     table_dirty_ = false;
     st_.table_rebuilds++;
@@ -486,7 +525,7 @@ void Engine::reset() {
     total_ = 0;
     approx_bytes_ = 0;
     last_constructed_ = 0;
-    rebuild_table(slots_.cap);
+    rebuild_table(table_slots());
     st_.constructed = 0;
     st_.unique = 0;
 }
@@ -501,6 +540,10 @@ void Engine::read_counters() {
 void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &constructed, u64 &n_tiles) {
     constructed = 0;
     n_tiles = 0;
+    // tile geometry: narrow = one lane per vector row; wide = one group of G lanes per vector row
+    const u64 tile_v = wide_ ? (u64)(32 >> log2g_) : (u64)TILE_V;
+    const u64 tile_s = wide_ ? (u64)(WIDE_ROW_VECS >> log2g_) : (u64)TILE_S;
+    const u64 tile_target = wide_ ? 2048 : (u64)TILE_V * TILE_S;  // candidates a tile should hold
     auto push = [&](BlockDesc b) {
         if (b.size == 0) return;
         b.ord0 = constructed;
@@ -517,7 +560,7 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.from_atoms = 1;
         b.na = (u64)n_atoms_;
         b.size = b.na;
-        b.tiles_v = ceil_div(b.na, (u64)TILE_V * UNARY_ITEMS);
+        b.tiles_v = ceil_div(b.na, tile_v * UNARY_ITEMS);
         b.tiles_s = 1;
         b.vg = 1;
         push(b);
@@ -534,7 +577,7 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.a_off = prev.base;
         b.na = prev.n;
         b.size = prev.n;
-        b.tiles_v = ceil_div(b.na, (u64)TILE_V * UNARY_ITEMS);
+        b.tiles_v = ceil_div(b.na, tile_v * UNARY_ITEMS);
         b.tiles_s = 1;
         b.vg = 1;
         push(b);
@@ -563,10 +606,10 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
                 b.size = la.n * lb.n;
             }
             const u64 n_vec = b.vec_is_b ? b.nb : b.na, n_sc = b.vec_is_b ? b.na : b.nb;
-            b.tiles_s = ceil_div(n_sc, TILE_S);
-            // few scalar rows: widen the tile over several groups of 32 vector rows
-            b.vg = b.tiles_s == 1 ? (uint32_t)std::min<u64>(64, std::max<u64>(1, TILE_S / n_sc)) : 1u;
-            b.tiles_v = ceil_div(n_vec, (u64)TILE_V * b.vg);
+            b.tiles_s = ceil_div(n_sc, tile_s);
+            // few scalar rows per tile: widen the tile over several groups of vector rows
+            b.vg = (uint32_t)std::min<u64>(256, std::max<u64>(1, tile_target / (tile_v * std::min(n_sc, tile_s))));
+            b.tiles_v = ceil_div(n_vec, tile_v * b.vg);
             push(b);
         }
     }
@@ -688,9 +731,23 @@ static void launch_op(int op, const NarrowParams &P, int grid, cudaStream_t st) 
     }
 }
 
+template <int LW>
+static void launch_op_wide(int op, const WideParams &P, int grid, cudaStream_t st) {
+    switch (op) {
+        case OP_ATOM: wide_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_NOT: wide_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_NEXT: wide_level_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_FUTURE: wide_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_AND: wide_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_UNTIL: wide_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        default: wide_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
+    }
+}
+
 // One launch per operator, in canonical operator order (blocks of a level are grouped by
 // operator already); each launch covers all (c1, c2) blocks of its operator.
-void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
+template <typename Params, typename Launch>
+static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int occupancy, ltlb200_stats &st, Launch launch) {
     size_t b0 = 0;
     int group = 0;
     while (b0 < lv.blocks.size()) {
@@ -702,20 +759,36 @@ void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
         P.tile_begin = lv.blocks[b0].tile0;
         P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
         P.ticket = CTR_TICKET0 + group;
-        const int grid = (int)std::min<u64>((P.tile_end - P.tile_begin + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * occupancy_);
-        const int op = (int)lv.blocks[b0].op;
-        switch (lw_) {
-            case 8: launch_op<8>(op, P, grid, stream_); break;
-            case 16: launch_op<16>(op, P, grid, stream_); break;
-            case 32: launch_op<32>(op, P, grid, stream_); break;
-            default: launch_op<64>(op, P, grid, stream_); break;
-        }
+        const int grid = (int)std::min<u64>((P.tile_end - P.tile_begin + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count * occupancy);
+        launch((int)lv.blocks[b0].op, P, grid);
         CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches++;
-        st_.enumerate_launches++;
+        st.kernel_launches++;
+        st.enumerate_launches++;
         b0 = b1;
         ++group;
     }
+}
+
+void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
+    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const NarrowParams &Q, int grid) {
+        switch (lw_) {
+            case 8: launch_op<8>(op, Q, grid, stream_); break;
+            case 16: launch_op<16>(op, Q, grid, stream_); break;
+            case 32: launch_op<32>(op, Q, grid, stream_); break;
+            default: launch_op<64>(op, Q, grid, stream_); break;
+        }
+    });
+}
+
+void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
+    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid) {
+        switch (lw_) {
+            case 8: launch_op_wide<8>(op, Q, grid, stream_); break;
+            case 16: launch_op_wide<16>(op, Q, grid, stream_); break;
+            case 32: launch_op_wide<32>(op, Q, grid, stream_); break;
+            default: launch_op_wide<64>(op, Q, grid, stream_); break;
+        }
+    });
 }
 
 int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
@@ -739,7 +812,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     }
     u64 n_claimed = 0, sep_ord = VAL_EMPTY;
     try {
-        if (table_dirty_) rebuild_table(slots_.cap);
+        if (table_dirty_) rebuild_table(table_slots());
         CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
         st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
 
@@ -754,9 +827,12 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         }
         for (int attempt = 0;; ++attempt) {
             const bool exact = est >= constructed;
-            const u64 want_slots = next_pow2(2 * (total_ + est + (exact ? 0 : kSlack)));
-            if (want_slots > slots_.cap) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most
-            reserve(new_list_, est + (exact ? 64 : kSlack), false);
+            // staging / claim capacity: the estimate plus what warps may over-reserve in flight
+            // (wide: every resident group may hold one partly used chunk of staging entries)
+            const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * (32 >> log2g_) * WIDE_CHUNK + 1024;
+            const u64 claim_cap = est + (wide_ ? wide_slack : (exact ? 64 : kSlack));
+            const u64 want_slots = next_pow2(2 * (total_ + claim_cap));
+            if (want_slots > table_slots()) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most
             if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
             u64 init[CTR_COUNT];
             for (auto &c : init) c = 0;
@@ -764,24 +840,53 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             // the special-key register (CTR_SPECIAL) persists across levels
             CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, CTR_SPECIAL * sizeof(u64), cudaMemcpyHostToDevice, stream_));
             CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_OVERFLOW, init + CTR_OVERFLOW, (CTR_COUNT - CTR_OVERFLOW) * sizeof(u64), cudaMemcpyHostToDevice, stream_));
-            NarrowParams P{};
-            P.store = store_.ptr;
-            P.atoms = d_atoms_;
-            P.slots = slots_.ptr;
-            P.slot_mask = slots_.cap - 1;
-            P.new_list = new_list_.ptr;
-            P.new_list_cap = new_list_.cap;
-            P.counters = d_counters_;
-            P.blocks = d_blocks_;
-            P.valid = valid_;
-            P.target = target_;
-            P.prune_after_sep = exhaustive ? 0 : 1;
-            P.special_possible = special_possible_ ? 1 : 0;
-            P.claim_limit = exact ? ~0ull : est;
-            P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
-            P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
-            CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
-            launch_enumerate(P, lv);
+            if (wide_) {
+                reserve(stage_rows_, claim_cap * nvec_, false);
+                reserve(stage_ord_, claim_cap, false);
+                reserve(stage_slot_, claim_cap, false);
+                CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+                WideParams P{};
+                P.store = store_.ptr;
+                P.atoms = d_atoms_;
+                P.slots = wslots_.ptr;
+                P.slot_mask = wslots_.cap - 1;
+                P.stage_rows = stage_rows_.ptr;
+                P.stage_ord = stage_ord_.ptr;
+                P.stage_slot = stage_slot_.ptr;
+                P.stage_cap = claim_cap;
+                P.total_before = total_;
+                P.counters = d_counters_;
+                P.blocks = d_blocks_;
+                P.valid = d_valid_;
+                P.target = d_target_;
+                P.nvec = nvec_;
+                P.log2g = log2g_;
+                P.prune_after_sep = exhaustive ? 0 : 1;
+                P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
+                P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+                CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+                launch_enumerate_wide(P, lv);
+            } else {
+                reserve(new_list_, claim_cap, false);
+                NarrowParams P{};
+                P.store = store_.ptr;
+                P.atoms = d_atoms_;
+                P.slots = slots_.ptr;
+                P.slot_mask = slots_.cap - 1;
+                P.new_list = new_list_.ptr;
+                P.new_list_cap = new_list_.cap;
+                P.counters = d_counters_;
+                P.blocks = d_blocks_;
+                P.valid = valid_;
+                P.target = target_;
+                P.prune_after_sep = exhaustive ? 0 : 1;
+                P.special_possible = special_possible_ ? 1 : 0;
+                P.claim_limit = exact ? ~0ull : est;
+                P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
+                P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+                CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+                launch_enumerate(P, lv);
+            }
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
             read_counters();
             float ms = 0;
@@ -789,11 +894,11 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             st_.enumerate_ms += ms;
             st_.enumerate_candidates += constructed;
             if (h_counters_[CTR_OVERFLOW] == 0) break;
-            if (exact || attempt > 8) throw CudaError("hash set overflow on an exactly sized table");
+            if (attempt > 8 || (exact && !wide_)) throw CudaError("hash set overflow on an exactly sized table");
             est = std::min(constructed, est * 4);
             rebuild_table(next_pow2(2 * (total_ + est + kSlack)));  // drops this attempt's claims
         }
-        n_claimed = h_counters_[CTR_CLAIMED];
+        n_claimed = h_counters_[CTR_CLAIMED];  // narrow: claimed slots; wide: reserved staging entries
         sep_ord = h_counters_[CTR_SEP];
         const u64 n_seps = h_counters_[CTR_SEPCOUNT];
 
@@ -803,23 +908,41 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
         reserve(bitmap_, n_words + 1, false);
         reserve(sb_rank_, n_sb + 1, false);
-        reserve(store_, total_ + n_claimed, true, total_);
+        reserve(store_, (total_ + n_claimed) * nvec_, true, total_ * nvec_);
         reserve(ords_, total_ + n_claimed, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
         CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+        const u64 ord_limit = cut ? sep_ord : VAL_EMPTY - 1;
         FinalizeParams F{};
-        F.slots = slots_.ptr;
-        F.new_list = new_list_.ptr;
-        F.n_claimed = n_claimed;
-        F.counters = d_counters_;
-        F.bitmap = bitmap_.ptr;
-        F.sb_rank = sb_rank_.ptr;
-        F.ord_limit = cut ? sep_ord : VAL_EMPTY - 1;
-        F.store = store_.ptr;
-        F.ords = ords_.ptr;
-        F.base = total_;
+        WideFinalize W{};
         const int fgrid = (int)std::max<u64>(1, std::min<u64>((n_claimed + 255) / 256, (u64)sm_count_ * 16));
-        narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        if (wide_) {
+            W.slots = wslots_.ptr;
+            W.stage_rows = stage_rows_.ptr;
+            W.stage_ord = stage_ord_.ptr;
+            W.stage_slot = stage_slot_.ptr;
+            W.n_staged = std::min(n_claimed, stage_ord_.cap);
+            W.bitmap = bitmap_.ptr;
+            W.sb_rank = sb_rank_.ptr;
+            W.ord_limit = ord_limit;
+            W.store = store_.ptr;
+            W.ords = ords_.ptr;
+            W.base = total_;
+            W.nvec = nvec_;
+            wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
+        } else {
+            F.slots = slots_.ptr;
+            F.new_list = new_list_.ptr;
+            F.n_claimed = n_claimed;
+            F.counters = d_counters_;
+            F.bitmap = bitmap_.ptr;
+            F.sb_rank = sb_rank_.ptr;
+            F.ord_limit = ord_limit;
+            F.store = store_.ptr;
+            F.ords = ords_.ptr;
+            F.base = total_;
+            narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        }
         CUDA_CHECK(cudaGetLastError());
         // popcount prefix per superblock: up to three scan levels of 1024
         {
@@ -848,7 +971,13 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         // separating candidate is fresh (engine.py:331,425-433); reproduce that exactly
         if (exhaustive && n_seps > 0 && n_seps <= sep_list_.cap) chunk_exact_separator(lv, n_seps, (u64)batch);
         level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
-        narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        if (wide_) {
+            const u64 work = W.n_staged * (u64)nvec_;
+            const int wgrid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
+            wide_scatter_kernel<<<wgrid, 256, 0, stream_>>>(W);
+        } else {
+            narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        }
         CUDA_CHECK(cudaGetLastError());
         CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
         st_.kernel_launches += 3;
@@ -895,11 +1024,11 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
     CUDA_CHECK(cudaSetDevice(device_));
     const u64 g0 = lv.base + (u64)first;
     if (cms) {
-        std::vector<uint4> rows((size_t)count);
-        CUDA_CHECK(cudaMemcpyAsync(rows.data(), store_.ptr + g0, (size_t)count * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
+        std::vector<uint4> rows((size_t)count * nvec_);
+        CUDA_CHECK(cudaMemcpyAsync(rows.data(), store_.ptr + g0 * nvec_, rows.size() * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
         CUDA_CHECK(cudaStreamSynchronize(stream_));
-        st_.d2h_bytes += (u64)count * sizeof(uint4);
-        for (int64_t k = 0; k < count; ++k) memcpy(cms + (size_t)k * row_bytes_, &rows[(size_t)k], (size_t)row_bytes_);
+        st_.d2h_bytes += rows.size() * sizeof(uint4);
+        for (int64_t k = 0; k < count; ++k) memcpy(cms + (size_t)k * row_bytes_, &rows[(size_t)k * nvec_], (size_t)row_bytes_);
     }
     if (op || left || right) {
         std::vector<u64> ords((size_t)count);
@@ -933,7 +1062,7 @@ int Engine::entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
 }
 
 void Engine::get_stats(ltlb200_stats *out) {
-    st_.table_slots = slots_.cap;
+    st_.table_slots = table_slots();
     st_.device_bytes = held_;
     *out = st_;
 }

@@ -1,0 +1,399 @@
+// wide.cuh -- construction + dedup kernels for CMs wider than one uint4 (17..512 bytes).
+//
+// Same contract as narrow.cuh (canonical ordinals, first construction wins, fused
+// separation check), different data layout, because a multi-vector key cannot be claimed
+// with one compare-and-swap:
+//
+//   * a CM is `nvec` uint4 vectors; a GROUP of G = pow2 >= nvec lanes owns one candidate,
+//     lane p of the group holding vector p (every connective is lane local, so the lanes
+//     never exchange CM bits; only hash, equality and the separation flag are reduced
+//     across the group, with ballots and xor-shuffles);
+//   * the hash set holds 8-byte words  [fingerprint:24 | row index + 1 : 40]  (0 = empty).
+//     The row index points either into the language cache (a CM finalised at an earlier
+//     level: index < total_before) or into this level's STAGING pool of new rows;
+//   * to claim a slot a group first writes its full row to a private staging entry, fences,
+//     and only then publishes it with one 64-bit CAS on the slot word.  A reader that finds
+//     a matching fingerprint therefore always finds a complete row behind it -- no waiting,
+//     no locks -- and compares the whole CM (coalesced: G lanes x 16 bytes);
+//   * per staging entry an atomicMin keeps the smallest ordinal that built the row.
+//
+// Finalisation ranks the staging entries by ordinal (bitmap + popcount prefix, as in the
+// narrow path), copies the rows into the cache in that order and re-points the slot words
+// at the final ids.
+#pragma once
+#include "narrow.cuh"
+
+namespace ltlb200 {
+
+constexpr int WIDE_ROW_VECS = 256;   // uint4 vectors of scalar-operand rows staged per warp (4 KiB)
+constexpr int WIDE_TERMS = 128;      // max scalar rows per tile (G = 2)
+constexpr int WIDE_CHUNK = 16;       // staging entries a group reserves at a time
+constexpr int WIDE_BATCH = 2;        // first slot probes a group keeps in flight
+constexpr u64 SLOT_IDX_MASK = (1ull << 40) - 1;
+constexpr int MAX_NVEC = 32;
+
+struct WideParams {
+    const uint4 *store;  // finalised rows by global id, nvec vectors each
+    const uint4 *atoms;  // atom rows, nvec vectors each
+    u64 *slots;
+    u64 slot_mask;
+    uint4 *stage_rows;  // this level's new rows, nvec vectors each
+    u64 *stage_ord;     // min ordinal per staging entry (all ones = unused)
+    uint32_t *stage_slot;
+    u64 stage_cap;
+    u64 total_before;  // rows finalised before this level
+    u64 *counters;     // CTR_*; CTR_CLAIMED counts reserved staging entries
+    const BlockDesc *blocks;
+    int block_begin, block_end;
+    u64 tile_begin, tile_end;
+    int ticket;
+    const uint4 *valid;   // Layout.masks packed, nvec vectors
+    const uint4 *target;  // Layout.target packed, nvec vectors
+    int nvec, log2g;
+    int prune_after_sep;
+    u64 *sep_list;
+    u64 sep_list_cap;
+};
+
+struct __align__(16) WideWarpShared {
+    uint4 rows[WIDE_ROW_VECS];  // (256 / G) scalar rows x G vectors
+    u64 term[WIDE_TERMS];
+    BlockDesc block;
+    u64 ticket, sep_now;
+};
+
+// per-group registers (uniform inside a group)
+struct GroupState {
+    u64 chunk_next = 0, chunk_end = 0;  // staging entries reserved for this group
+    u64 spare = ~0ull;                  // a reserved entry whose publish lost its race
+};
+
+struct GroupGeom {
+    uint32_t mask;   // lanes of this group
+    int base;        // first lane of the group
+    int part;        // this lane's vector index inside the row
+    int leader;      // base lane
+    bool has_part;   // part < nvec
+};
+
+__device__ __forceinline__ u64 slot_word(uint32_t fp, u64 idx) { return ((u64)(fp & 0xFFFFFFu) << 40) | (idx + 1); }
+
+// group-wide reductions
+__device__ __forceinline__ bool group_all_zero(uint32_t diff, const GroupGeom &g) {
+    return (__ballot_sync(g.mask, diff != 0u) & g.mask) == 0u;
+}
+
+// two independent 32-bit hashes of the whole row (slot index and fingerprint)
+__device__ __forceinline__ void row_hash(uint4 part, const GroupGeom &g, int log2g, uint32_t &h_slot, uint32_t &h_fp) {
+    uint32_t a = g.has_part ? hash_vec(part, 0x9E3779B9u * (uint32_t)(g.part + 1)) : 0u;
+    uint32_t b = g.has_part ? hash_vec(part, 0x7F4A7C15u * (uint32_t)(g.part + 1) + 0x632BE5ABu) : 0u;
+    for (int d = 1; d < (1 << log2g); d <<= 1) {
+        a ^= __shfl_xor_sync(g.mask, a, d);
+        b ^= __shfl_xor_sync(g.mask, b, d);
+    }
+    a ^= a >> 16;
+    a *= 0x85EBCA6Bu;
+    a ^= a >> 13;
+    b ^= b >> 15;
+    b *= 0xC2B2AE35u;
+    b ^= b >> 16;
+    h_slot = a;
+    h_fp = b >> 8;
+}
+
+// Group-collective insert of one candidate row.  `w0` is the already loaded word of slot `s`.
+// Returns true when the CM was not stored by an earlier level (fresh for this level).
+__device__ __forceinline__ bool wide_insert(const WideParams &P, const GroupGeom &g, GroupState &gs, uint4 part,
+                                            uint32_t s, uint32_t fp, u64 w0, u64 ord) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t mask32 = (uint32_t)P.slot_mask;
+    bool row_staged = false;
+    u64 w = w0;
+    for (;;) {
+        if (w == 0ull) {
+            // ---- empty slot: stage the row, then publish it with one CAS
+            if (!row_staged) {
+                if (gs.spare == ~0ull) {
+                    if (gs.chunk_next == gs.chunk_end) {
+                        u64 first = 0;
+                        if (lane == g.leader) first = atomicAdd(&P.counters[CTR_CLAIMED], (u64)WIDE_CHUNK);
+                        first = __shfl_sync(g.mask, first, g.leader);
+                        gs.chunk_next = first;
+                        gs.chunk_end = first + WIDE_CHUNK;
+                    }
+                    gs.spare = gs.chunk_next++;
+                }
+                if (gs.spare >= P.stage_cap) {  // staging pool exhausted: the host regrows and redoes the level
+                    if (lane == g.leader) atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+                    return false;
+                }
+                if (g.has_part) P.stage_rows[gs.spare * P.nvec + g.part] = part;
+                __threadfence();
+                row_staged = true;
+            }
+            __syncwarp(g.mask);
+            u64 old = 0;
+            if (lane == g.leader) old = atomicCAS(&P.slots[s], 0ull, slot_word(fp, P.total_before + gs.spare));
+            old = __shfl_sync(g.mask, old, g.leader);
+            if (old == 0ull) {
+                if (lane == g.leader) {
+                    atomicMin(&P.stage_ord[gs.spare], ord);
+                    P.stage_slot[gs.spare] = s;
+                }
+                gs.spare = ~0ull;
+                return true;
+            }
+            w = old;  // somebody else published here first: look at what they put
+        }
+        if ((uint32_t)(w >> 40) == (fp & 0xFFFFFFu)) {
+            const u64 idx = (w & SLOT_IDX_MASK) - 1;
+            const bool staged = idx >= P.total_before;
+            const uint4 *row = staged ? P.stage_rows + (idx - P.total_before) * P.nvec : P.store + idx * P.nvec;
+            uint32_t diff = 0;
+            if (g.has_part) {
+                const uint4 k = __ldcg(row + g.part);
+                diff = (k.x ^ part.x) | (k.y ^ part.y) | (k.z ^ part.z) | (k.w ^ part.w);
+            }
+            if (group_all_zero(diff, g)) {
+                if (!staged) return false;  // duplicate of an earlier level
+                if (lane == g.leader) atomicMin(&P.stage_ord[idx - P.total_before], ord);
+                return true;
+            }
+        }
+        s = (s + 1) & mask32;
+        w = __ldcg(&P.slots[s]);
+    }
+}
+
+// Process WIDE_BATCH candidates of one group: hash, first slot probe (all in flight), then insert.
+template <int LW, typename OrdOf>
+__device__ __forceinline__ void wide_batch(const WideParams &P, const GroupGeom &g, GroupState &gs,
+                                           const uint4 (&cand)[WIDE_BATCH], const bool (&live)[WIDE_BATCH],
+                                           const bool (&known)[WIDE_BATCH], uint4 target, OrdOf ord_of) {
+    const int lane = threadIdx.x & 31;
+    uint32_t slot[WIDE_BATCH], fp[WIDE_BATCH];
+    u64 w0[WIDE_BATCH];
+#pragma unroll
+    for (int r = 0; r < WIDE_BATCH; ++r) {
+        row_hash(cand[r], g, P.log2g, slot[r], fp[r]);
+        slot[r] &= (uint32_t)P.slot_mask;
+        w0[r] = 0;
+        if (live[r] && !known[r]) w0[r] = __ldcg(&P.slots[slot[r]]);
+    }
+#pragma unroll
+    for (int r = 0; r < WIDE_BATCH; ++r) {
+        if (!live[r]) continue;  // group-uniform
+        const uint32_t sep_diff = g.has_part ? cm_sep_diff<LW>(cand[r], target) : 0u;
+        const bool sep = group_all_zero(sep_diff, g);
+        bool fresh = false;
+        if (!known[r]) fresh = wide_insert(P, g, gs, cand[r], slot[r], fp[r], w0[r], ord_of(r));
+        if (sep && lane == g.leader) {
+            const u64 ord = ord_of(r);
+            if (fresh) atomicMin(&P.counters[CTR_SEP], ord);
+            if (P.sep_list) {
+                const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+                if (pos < P.sep_list_cap) P.sep_list[pos] = ord;
+            }
+        }
+    }
+}
+
+template <int LW, int OP>
+__device__ __forceinline__ void wide_unary_tile(const WideParams &P, WideWarpShared &ws, const GroupGeom &g,
+                                                GroupState &gs, uint4 valid, uint4 target, u64 tile_local, u64 sep_now) {
+    const BlockDesc &B = ws.block;
+    const int groups = 32 >> P.log2g;
+    const int gi = (threadIdx.x & 31) >> P.log2g;  // this group's index in the warp
+    const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off * P.nvec;
+    const u64 per_tile = (u64)groups * UNARY_ITEMS;
+    const u64 first = tile_local * per_tile + gi;
+    const u64 ord0 = B.ord0, n = B.na;
+    if (ord0 + tile_local * per_tile > sep_now) return;
+    const int n_steps = (int)min((u64)UNARY_ITEMS, (n - tile_local * per_tile + groups - 1) / groups);
+#pragma unroll 1
+    for (int k = 0; k < n_steps; k += WIDE_BATCH) {
+        uint4 cand[WIDE_BATCH];
+        bool live[WIDE_BATCH], known[WIDE_BATCH];
+        auto ord_of = [&](int r) { return ord0 + first + (u64)(k + r) * groups; };
+#pragma unroll
+        for (int r = 0; r < WIDE_BATCH; ++r) {
+            const u64 i = first + (u64)(k + r) * groups;
+            live[r] = k + r < n_steps && i < n;
+            const uint4 x = (live[r] && g.has_part) ? __ldg(src + i * P.nvec + g.part) : make_uint4(0, 0, 0, 0);
+            cand[r] = cm_apply<LW, OP>(x, x, valid);
+            const uint32_t d = (cand[r].x ^ x.x) | (cand[r].y ^ x.y) | (cand[r].z ^ x.z) | (cand[r].w ^ x.w);
+            known[r] = OP != OP_ATOM && group_all_zero(d, g);
+        }
+        wide_batch<LW>(P, g, gs, cand, live, known, target, ord_of);
+    }
+}
+
+template <int LW, int OP, bool VEC_B>
+__device__ __forceinline__ void wide_binary_tile(const WideParams &P, WideWarpShared &ws, const GroupGeom &g,
+                                                 GroupState &gs, uint4 valid, uint4 target, u64 tile_local, u64 sep_now) {
+    const BlockDesc &B = ws.block;
+    const int lane = threadIdx.x & 31;
+    const int G = 1 << P.log2g, groups = 32 >> P.log2g, gi = lane >> P.log2g;
+    const int tile_s = WIDE_ROW_VECS >> P.log2g;  // scalar rows per tile
+    const bool tri = B.kind == BK_TRI;
+    const uint32_t vg_n = B.vg;
+    u64 tv, ts;
+    if (VEC_B) { ts = tile_local / B.tiles_v; tv = tile_local % B.tiles_v; }
+    else { tv = tile_local / B.tiles_s; ts = tile_local % B.tiles_s; }
+    const u64 n_vec = VEC_B ? B.nb : B.na, n_sc = VEC_B ? B.na : B.nb;
+    const u64 v0 = tv * (u64)(groups * vg_n), s0 = ts * (u64)tile_s;
+    const int s_cnt = (int)min((u64)tile_s, n_sc - s0);
+    if (tri && v0 + (u64)groups * vg_n - 1 < s0) return;
+    const u64 ord0 = B.ord0, na = B.na, nb = B.nb;
+    const u64 tile_min = ord0 + (VEC_B ? (tri ? s0 * na - (s0 ? (s0 * (s0 - 1)) / 2 : 0) : s0 * nb + v0) : v0 * nb + s0);
+    if (tile_min > sep_now) return;
+    const uint4 *vec_rows = P.store + (VEC_B ? B.b_off : B.a_off) * P.nvec;
+    const uint4 *sc_rows = P.store + (VEC_B ? B.a_off : B.b_off) * P.nvec;
+    __syncwarp();
+    // stage the scalar rows: row k occupies vectors [k*G, k*G + nvec)
+    for (int k = gi; k < s_cnt; k += groups) {
+        const u64 s = s0 + k;
+        if (g.has_part) ws.rows[k * G + g.part] = __ldg(sc_rows + s * P.nvec + g.part);
+        if (lane == g.leader)
+            ws.term[k] = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (uint32_t vg = 0; vg < vg_n; ++vg) {
+        if (v0 + (u64)vg * groups >= n_vec) break;
+        const u64 v = v0 + (u64)vg * groups + gi;
+        const bool v_ok = v < n_vec;
+        const uint4 xv = (v_ok && g.has_part) ? __ldg(vec_rows + v * P.nvec + g.part) : make_uint4(0, 0, 0, 0);
+        const u64 lane_term = VEC_B ? v : ord0 + v * nb;
+        const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
+        const int s_live = v_ok ? first_bad : 0;
+#pragma unroll 1
+        for (int k = 0; k < s_cnt; k += WIDE_BATCH) {
+            uint4 cand[WIDE_BATCH];
+            bool live[WIDE_BATCH], known[WIDE_BATCH];
+            auto ord_of = [&](int r) { return ws.term[min(k + r, s_cnt - 1)] + lane_term; };
+#pragma unroll
+            for (int r = 0; r < WIDE_BATCH; ++r) {
+                const int sr = min(k + r, s_cnt - 1);
+                const uint4 xs = g.has_part ? ws.rows[sr * G + g.part] : make_uint4(0, 0, 0, 0);
+                live[r] = k + r < s_live;
+                cand[r] = VEC_B ? cm_apply<LW, OP>(xs, xv, valid) : cm_apply<LW, OP>(xv, xs, valid);
+                const uint32_t da = (cand[r].x ^ xs.x) | (cand[r].y ^ xs.y) | (cand[r].z ^ xs.z) | (cand[r].w ^ xs.w);
+                const uint32_t db = (cand[r].x ^ xv.x) | (cand[r].y ^ xv.y) | (cand[r].z ^ xv.z) | (cand[r].w ^ xv.w);
+                const uint32_t ma = __ballot_sync(g.mask, da != 0u) & g.mask, mb = __ballot_sync(g.mask, db != 0u) & g.mask;
+                known[r] = ma == 0u || mb == 0u;
+            }
+            wide_batch<LW>(P, g, gs, cand, live, known, target, ord_of);
+        }
+    }
+}
+
+template <int LW, int OP>
+__global__ void __launch_bounds__(CTA_THREADS, 4) wide_level_kernel(const WideParams P) {
+    __shared__ WideWarpShared s_warp[WARPS_PER_CTA];
+    WideWarpShared &ws = s_warp[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const int G = 1 << P.log2g;
+    GroupGeom g;
+    g.base = lane & ~(G - 1);
+    g.part = lane & (G - 1);
+    g.leader = g.base;
+    g.has_part = g.part < P.nvec;
+    g.mask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << g.base;
+    GroupState gs;
+    const uint4 valid = g.has_part ? P.valid[g.part] : make_uint4(0, 0, 0, 0);
+    const uint4 target = g.has_part ? P.target[g.part] : make_uint4(0, 0, 0, 0);
+    for (;;) {
+        __syncwarp();
+        if (lane == 0) {
+            u64 t = P.tile_end;
+            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull) t = P.tile_begin + atomicAdd(&P.counters[P.ticket], 1ull);
+            ws.ticket = t;
+            ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
+            if (t < P.tile_end) {
+                int bi = P.block_begin;
+                while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
+                ws.block = P.blocks[bi];
+            }
+        }
+        __syncwarp();
+        const u64 tile = ws.ticket;
+        const u64 sep_now = ws.sep_now;
+        if (tile >= P.tile_end) break;
+        if (ws.block.ord0 > sep_now) continue;
+        const u64 tile_local = tile - ws.block.tile0;
+        if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
+            if (ws.block.vec_is_b) wide_binary_tile<LW, OP, true>(P, ws, g, gs, valid, target, tile_local, sep_now);
+            else wide_binary_tile<LW, OP, false>(P, ws, g, gs, valid, target, tile_local, sep_now);
+        } else {
+            wide_unary_tile<LW, OP>(P, ws, g, gs, valid, target, tile_local, sep_now);
+        }
+    }
+}
+
+// ---- finalisation (wide) -------------------------------------------------------------------
+
+struct WideFinalize {
+    u64 *slots;
+    const uint4 *stage_rows;
+    const u64 *stage_ord;
+    const uint32_t *stage_slot;
+    u64 n_staged;  // staging entries reserved (some unused: ord = all ones)
+    uint32_t *bitmap;
+    const uint32_t *sb_rank;
+    u64 ord_limit;
+    uint4 *store;
+    u64 *ords;
+    u64 base;
+    int nvec;
+};
+
+__global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < F.n_staged; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = F.stage_ord[t];
+        if (ord <= F.ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
+    }
+}
+
+// one thread per (staging entry, vector)
+__global__ void __launch_bounds__(256) wide_scatter_kernel(const WideFinalize F) {
+    const u64 total = F.n_staged * (u64)F.nvec;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+        const u64 k = t / F.nvec;
+        const int part = (int)(t % F.nvec);
+        const u64 ord = F.stage_ord[k];
+        if (ord > F.ord_limit) continue;  // unused entry, or ordered after the separator
+        const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
+        F.store[gid * F.nvec + part] = F.stage_rows[k * F.nvec + part];
+        if (part == 0) {
+            F.ords[gid] = ord;
+            u64 *slot = &F.slots[F.stage_slot[k]];
+            *slot = (*slot & ~SLOT_IDX_MASK) | (gid + 1);  // same fingerprint, final row id
+        }
+    }
+}
+
+// re-insert finalised rows [0, count) into a fresh table: rows of the cache are pairwise
+// distinct, so claiming the first empty slot of the probe sequence is enough
+__global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_mask, const uint4 *store, u64 count,
+                                                           int nvec, int log2g) {
+    for (u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x; gid < count; gid += (u64)gridDim.x * blockDim.x) {
+        uint32_t a = 0, b = 0;
+        for (int p = 0; p < nvec; ++p) {
+            const uint4 part = store[gid * nvec + p];
+            a ^= hash_vec(part, 0x9E3779B9u * (uint32_t)(p + 1));
+            b ^= hash_vec(part, 0x7F4A7C15u * (uint32_t)(p + 1) + 0x632BE5ABu);
+        }
+        a ^= a >> 16;
+        a *= 0x85EBCA6Bu;
+        a ^= a >> 13;
+        b ^= b >> 15;
+        b *= 0xC2B2AE35u;
+        b ^= b >> 16;
+        u64 s = a & slot_mask;
+        const u64 word = slot_word(b >> 8, gid);
+        while (atomicCAS(&slots[s], 0ull, word) != 0ull) s = (s + 1) & slot_mask;
+    }
+}
+
+}  // namespace ltlb200
