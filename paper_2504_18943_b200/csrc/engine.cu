@@ -542,17 +542,38 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
     n_tiles = 0;
     // tile geometry: narrow = one lane per vector row; wide = one group of G lanes per vector row
     const u64 tile_v = wide_ ? (u64)(32 >> log2g_) : (u64)TILE_V;
-    const u64 tile_s = wide_ ? (u64)(WIDE_ROW_VECS >> log2g_) : (u64)TILE_S;
-    const u64 tile_target = wide_ ? 2048 : (u64)TILE_V * TILE_S;  // candidates a tile should hold
+    const u64 tile_s_max = wide_ ? (u64)(WIDE_ROW_VECS >> log2g_) : (u64)TILE_S;
+    const u64 tile_max = wide_ ? 2048 : (u64)TILE_V * TILE_S;  // candidates of a full-size tile
+    // A block is cut into at least ~4 tiles per resident warp so that small levels still
+    // spread over the whole GPU instead of a few warps grinding through full-size tiles.
+    const u64 want_tiles = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * 4;
+    auto tile_candidates = [&](u64 size) {
+        u64 per = std::max<u64>(size / want_tiles, tile_v * 4);
+        return std::min<u64>(next_pow2(per), tile_max);
+    };
+    auto ceil_div = [](u64 a, u64 b) { return (a + b - 1) / b; };
     auto push = [&](BlockDesc b) {
         if (b.size == 0) return;
+        const u64 per = tile_candidates(b.size);
+        if (b.kind == BK_UNARY) {
+            b.tile_s = (uint32_t)std::min<u64>(std::max<u64>(per / tile_v, 4), UNARY_ITEMS);
+            b.vg = 1;
+            b.tiles_v = ceil_div(b.na, tile_v * b.tile_s);
+            b.tiles_s = 1;
+        } else {
+            const u64 n_vec = b.vec_is_b ? b.nb : b.na, n_sc = b.vec_is_b ? b.na : b.nb;
+            b.tile_s = (uint32_t)std::min<u64>(std::max<u64>(per / tile_v, 4), std::min(tile_s_max, n_sc));
+            b.tiles_s = ceil_div(n_sc, b.tile_s);
+            // few scalar rows per tile: widen the tile over several groups of vector rows
+            b.vg = (uint32_t)std::min<u64>(256, std::max<u64>(1, per / (tile_v * b.tile_s)));
+            b.tiles_v = ceil_div(n_vec, tile_v * b.vg);
+        }
         b.ord0 = constructed;
         b.tile0 = n_tiles;
         constructed += b.size;
         n_tiles += b.tiles_v * b.tiles_s;
         lv.blocks.push_back(b);
     };
-    auto ceil_div = [](u64 a, u64 b) { return (a + b - 1) / b; };
     if (cost == 1) {
         BlockDesc b{};
         b.op = OP_ATOM;
@@ -560,9 +581,6 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.from_atoms = 1;
         b.na = (u64)n_atoms_;
         b.size = b.na;
-        b.tiles_v = ceil_div(b.na, tile_v * UNARY_ITEMS);
-        b.tiles_s = 1;
-        b.vg = 1;
         push(b);
         return;
     }
@@ -577,9 +595,6 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.a_off = prev.base;
         b.na = prev.n;
         b.size = prev.n;
-        b.tiles_v = ceil_div(b.na, tile_v * UNARY_ITEMS);
-        b.tiles_s = 1;
-        b.vg = 1;
         push(b);
     }
     for (int tag : binary_tags) {
@@ -605,11 +620,6 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
                 b.vec_is_b = lb.n >= la.n;
                 b.size = la.n * lb.n;
             }
-            const u64 n_vec = b.vec_is_b ? b.nb : b.na, n_sc = b.vec_is_b ? b.na : b.nb;
-            b.tiles_s = ceil_div(n_sc, tile_s);
-            // few scalar rows per tile: widen the tile over several groups of vector rows
-            b.vg = (uint32_t)std::min<u64>(256, std::max<u64>(1, tile_target / (tile_v * std::min(n_sc, tile_s))));
-            b.tiles_v = ceil_div(n_vec, tile_v * b.vg);
             push(b);
         }
     }
@@ -828,8 +838,8 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         for (int attempt = 0;; ++attempt) {
             const bool exact = est >= constructed;
             // staging / claim capacity: the estimate plus what warps may over-reserve in flight
-            // (wide: every resident group may hold one partly used chunk of staging entries)
-            const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * (32 >> log2g_) * WIDE_CHUNK + 1024;
+            // (wide: every group of every operator launch may end with a partly used chunk of staging entries)
+            const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * (32 >> log2g_) * WIDE_CHUNK * 8 + 1024;
             const u64 claim_cap = est + (wide_ ? wide_slack : (exact ? 64 : kSlack));
             const u64 want_slots = next_pow2(2 * (total_ + claim_cap));
             if (want_slots > table_slots()) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most

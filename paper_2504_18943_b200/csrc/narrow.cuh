@@ -69,7 +69,8 @@ struct BlockDesc {
     u64 tile0;            // first tile index of the block in the level's flattened tile space
     u64 tiles_v, tiles_s;
     uint32_t vg;  // vector groups (of 32 rows) per tile; > 1 when the scalar operand has few rows
-    uint32_t pad_;
+    uint32_t tile_s;  // scalar rows per tile (<= TILE_S) or, for unary blocks, candidates per lane per tile;
+                      // the host shrinks tiles of small blocks so that they still spread over the whole GPU
 };
 
 struct NarrowParams {
@@ -293,10 +294,11 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WarpShared
     const BlockDesc &B = ws.block;
     const int lane = threadIdx.x & 31;
     const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off;
-    const u64 first = tile_local * (u64)(TILE_V * UNARY_ITEMS) + lane;
+    const u64 per_tile = (u64)TILE_V * B.tile_s;
+    const u64 first = tile_local * per_tile + lane;
     const u64 ord0 = B.ord0, n = B.na;
-    if (ord0 + tile_local * (u64)(TILE_V * UNARY_ITEMS) > sep_now) return;  // tile ordered after the separator
-    const int n_groups = (int)min((u64)UNARY_ITEMS, (n - tile_local * (u64)(TILE_V * UNARY_ITEMS) + TILE_V - 1) / TILE_V);
+    if (ord0 + tile_local * per_tile > sep_now) return;  // tile ordered after the separator
+    const int n_groups = (int)min((u64)B.tile_s, (n - tile_local * per_tile + TILE_V - 1) / TILE_V);
 #pragma unroll 1
     for (int g = 0; g < n_groups; g += PROBE_BATCH) {
         uint4 cand[PROBE_BATCH];
@@ -337,8 +339,8 @@ __device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WarpShare
     if (VEC_B) { ts = tile_local / B.tiles_v; tv = tile_local % B.tiles_v; }
     else { tv = tile_local / B.tiles_s; ts = tile_local % B.tiles_s; }
     const u64 n_vec = VEC_B ? B.nb : B.na, n_sc = VEC_B ? B.na : B.nb;
-    const u64 v0 = tv * (u64)(TILE_V * vg_n), s0 = ts * TILE_S;
-    const int s_cnt = (int)min((u64)TILE_S, n_sc - s0);
+    const u64 v0 = tv * (u64)(TILE_V * vg_n), s0 = ts * (u64)B.tile_s;
+    const int s_cnt = (int)min((u64)B.tile_s, n_sc - s0);
     if (tri && v0 + (u64)TILE_V * vg_n - 1 < s0) return;  // tile entirely below the diagonal (j < i)
     const u64 ord0 = B.ord0, na = B.na, nb = B.nb;
     // a lower bound of the tile's ordinals: skip tiles ordered after the separator

@@ -205,11 +205,11 @@ __device__ __forceinline__ void wide_unary_tile(const WideParams &P, WideWarpSha
     const int groups = 32 >> P.log2g;
     const int gi = (threadIdx.x & 31) >> P.log2g;  // this group's index in the warp
     const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off * P.nvec;
-    const u64 per_tile = (u64)groups * UNARY_ITEMS;
+    const u64 per_tile = (u64)groups * B.tile_s;
     const u64 first = tile_local * per_tile + gi;
     const u64 ord0 = B.ord0, n = B.na;
     if (ord0 + tile_local * per_tile > sep_now) return;
-    const int n_steps = (int)min((u64)UNARY_ITEMS, (n - tile_local * per_tile + groups - 1) / groups);
+    const int n_steps = (int)min((u64)B.tile_s, (n - tile_local * per_tile + groups - 1) / groups);
 #pragma unroll 1
     for (int k = 0; k < n_steps; k += WIDE_BATCH) {
         uint4 cand[WIDE_BATCH];
@@ -234,7 +234,7 @@ __device__ __forceinline__ void wide_binary_tile(const WideParams &P, WideWarpSh
     const BlockDesc &B = ws.block;
     const int lane = threadIdx.x & 31;
     const int G = 1 << P.log2g, groups = 32 >> P.log2g, gi = lane >> P.log2g;
-    const int tile_s = WIDE_ROW_VECS >> P.log2g;  // scalar rows per tile
+    const int tile_s = (int)B.tile_s;  // scalar rows per tile (<= WIDE_ROW_VECS / G)
     const bool tri = B.kind == BK_TRI;
     const uint32_t vg_n = B.vg;
     u64 tv, ts;
