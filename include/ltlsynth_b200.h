@@ -126,6 +126,36 @@ int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int3
                          int64_t batch_size, uint64_t memory_budget_bytes, double deadline_s,
                          int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
 
+/*
+ * One search sharded over several GPUs: the level is split into
+ *   ltlb200_level_begin   enumerate the tiles of shard `shard_index` of `shard_count` into the
+ *                         local hash set (every rank holds the whole cache of earlier levels);
+ *                         outputs the local claim count, the smallest ordinal of a fresh
+ *                         separating candidate (all ones = none) and how many separating
+ *                         ordinals were recorded (exhaustive runs);
+ *   ltlb200_claims_count / _pack   export this level's local claims as records
+ *                         {CM row (ltlb200_key_bytes bytes), ordinal u64} grouped by hash owner,
+ *                         into DEVICE buffers the caller hands to NCCL;
+ *   ltlb200_claims_import insert-or-min received records (device buffers) into the local set;
+ *   ltlb200_level_end     finalise with the GLOBAL separator ordinal (and, for exhaustive runs,
+ *                         every separating ordinal of the level, host array; NULL = local ones).
+ * ltlb200_expand_level == level_begin(shard 0 of 1) + level_end.  The reference has no
+ * counterpart: its only parallelism is a thread pool inside expand_level (engine.py:386-391).
+ */
+int ltlb200_level_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, double deadline_s,
+                        int32_t shard_index, int32_t shard_count, uint64_t *n_claimed, uint64_t *sep_ord,
+                        uint64_t *n_seps);
+int ltlb200_level_end(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps,
+                      int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
+                      int64_t *constructed_delta);
+int ltlb200_claims_count(ltlb200_engine *e, int32_t owners, uint64_t *counts);
+int ltlb200_claims_pack(ltlb200_engine *e, int32_t owners, void *rows_dev, void *ords_dev);
+int ltlb200_claims_import(ltlb200_engine *e, const void *rows_dev, const void *ords_dev, uint64_t n);
+/* Copies the separating ordinals recorded by level_begin (exhaustive runs); returns how many. */
+int64_t ltlb200_seps_copy(ltlb200_engine *e, uint64_t *out, uint64_t cap);
+/* Bytes of one CM row as stored on the device and in exchange records (16 * vectors). */
+int32_t ltlb200_key_bytes(const ltlb200_engine *e);
+
 /* CLOCK_MONOTONIC now, in seconds (time base of deadline_s). */
 double ltlb200_now(void);
 

@@ -29,6 +29,13 @@ EXPORTED_SYMBOLS = (
     "ltlb200_reset",
     "ltlb200_trim",
     "ltlb200_expand_level",
+    "ltlb200_level_begin",
+    "ltlb200_level_end",
+    "ltlb200_claims_count",
+    "ltlb200_claims_pack",
+    "ltlb200_claims_import",
+    "ltlb200_seps_copy",
+    "ltlb200_key_bytes",
     "ltlb200_now",
     "ltlb200_level_info",
     "ltlb200_num_levels",
@@ -101,6 +108,21 @@ def load():
     L.ltlb200_expand_level.restype = ctypes.c_int
     L.ltlb200_expand_level.argtypes = [p, i32, u32, i32, i64, u64, dbl,
                                        ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    pu64 = ctypes.POINTER(u64)
+    L.ltlb200_level_begin.restype = ctypes.c_int
+    L.ltlb200_level_begin.argtypes = [p, i32, u32, i32, dbl, i32, i32, pu64, pu64, pu64]
+    L.ltlb200_level_end.restype = ctypes.c_int
+    L.ltlb200_level_end.argtypes = [p, u64, p, u64, i64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.ltlb200_claims_count.restype = ctypes.c_int
+    L.ltlb200_claims_count.argtypes = [p, i32, p]
+    L.ltlb200_claims_pack.restype = ctypes.c_int
+    L.ltlb200_claims_pack.argtypes = [p, i32, p, p]
+    L.ltlb200_claims_import.restype = ctypes.c_int
+    L.ltlb200_claims_import.argtypes = [p, p, p, u64]
+    L.ltlb200_seps_copy.restype = i64
+    L.ltlb200_seps_copy.argtypes = [p, p, u64]
+    L.ltlb200_key_bytes.restype = i32
+    L.ltlb200_key_bytes.argtypes = [p]
     L.ltlb200_now.restype = dbl
     L.ltlb200_level_info.restype = ctypes.c_int
     L.ltlb200_level_info.argtypes = [p, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]

@@ -244,6 +244,15 @@ public:
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
     void reset();
+    int level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
+                    u64 *n_claimed, u64 *sep_ord, u64 *n_seps);
+    int level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid,
+                  int64_t *constructed_delta);
+    void claims_count(int owners, u64 *counts);
+    void claims_pack(int owners, void *rows_dev, void *ords_dev);
+    void claims_import(const void *rows_dev, const void *ords_dev, u64 n);
+    u64 seps_copy(u64 *out, u64 cap);
+    int key_bytes() const { return 16 * nvec_; }
     int num_levels() const { return (int)levels_.size(); }
     u64 approx_bytes() const { return approx_bytes_; }
 
@@ -275,6 +284,15 @@ private:
     DeviceArray<uint32_t> scan_tmp_;
     DeviceArray<u64> sep_list_;
     DeviceArray<uint8_t> misc_;
+    DeviceArray<u64> xchg_;  // per-owner counts and cursors of the claim exchange
+    struct PendingLevel {
+        LevelMeta lv;
+        u64 constructed = 0, n_claimed = 0, sep_ord = ~0ull, n_seps = 0, claim_cap = 0;
+        bool exhaustive = false, active = false, seps_overflow = false;
+        int cost = 0;
+        std::vector<u64> owner_counts;
+    } pending_;
+    WideParams wide_params(bool exhaustive) const;
     static constexpr u64 kMinSlots = 1ull << 16;
     u64 *d_counters_ = nullptr;
     BlockDesc *d_blocks_ = nullptr;
@@ -305,7 +323,7 @@ private:
     void launch_enumerate(NarrowParams P, const LevelMeta &lv);
     void launch_enumerate_wide(WideParams P, const LevelMeta &lv);
     u64 table_slots() const { return wide_ ? wslots_.cap : slots_.cap; }
-    u64 chunk_exact_separator(const LevelMeta &lv, u64 n_seps, u64 batch);
+    u64 chunk_exact_separator(const LevelMeta &lv, std::vector<u64> &seps, u64 batch);
 };
 
 // Blocks come from the process-wide cache (see BlockCache); `bytes` must be a size class.
@@ -472,6 +490,7 @@ Engine::~Engine() {
     release(scan_tmp_);
     release(sep_list_);
     release(misc_);
+    release(xchg_);
     recycle_retired(true);
     pinned_put(h_counters_);
     for (auto &e : ev_)
@@ -704,11 +723,8 @@ u64 Engine::constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) con
 // the reference's chunked merge loop reports -- walk the chunks in order, look only at each
 // chunk's first separating candidate, and take the first of those that is fresh, i.e. that
 // won its CM (bit set in the winners bitmap).  Leaves the result in counters[CTR_SEP].
-u64 Engine::chunk_exact_separator(const LevelMeta &lv, u64 n_seps, u64 batch) {
-    std::vector<u64> seps((size_t)n_seps);
-    CUDA_CHECK(cudaMemcpyAsync(seps.data(), sep_list_.ptr, n_seps * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));
-    st_.d2h_bytes += n_seps * sizeof(u64);
+u64 Engine::chunk_exact_separator(const LevelMeta &lv, std::vector<u64> &seps, u64 batch) {
+    reserve(sep_list_, seps.size() + 1, false);
     std::sort(seps.begin(), seps.end());
     std::vector<u64> firsts;
     u64 chunk_end = 0;
@@ -801,26 +817,34 @@ void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
     });
 }
 
-int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
-                         int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
-    if (cost != (int)levels_.size() + 1 || batch < 1) throw std::invalid_argument("cost must be the next unbuilt level and batch_size >= 1");
+// ---- one level = begin (enumerate this rank's shard) [+ exchange] + end (finalise) ---------
+
+// Enumerates the tiles of level `cost` that belong to shard `shard_index` of `shard_count`
+// (tile-strided) into the local hash set.  Nothing is appended yet; level_end() does that.
+int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
+                        u64 *n_claimed_out, u64 *sep_ord_out, u64 *n_seps_out) {
+    if (pending_.active) throw std::invalid_argument("level_begin: the previous level was not ended");
+    if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
+    if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count) throw std::invalid_argument("bad shard");
     CUDA_CHECK(cudaSetDevice(device_));
-    *n_new = 0;
-    *sep_gid = -1;
-    *constructed_delta = 0;
-    LevelMeta lv;
-    lv.base = total_;
+    pending_ = PendingLevel{};
+    PendingLevel &pl = pending_;
+    pl.lv.base = total_;
+    pl.exhaustive = exhaustive;
+    pl.cost = cost;
+    *n_claimed_out = 0;
+    *sep_ord_out = VAL_EMPTY;
+    *n_seps_out = 0;
     if (deadline >= 0 && monotonic_s() > deadline) {  // engine.py:416-417, before the first chunk
-        levels_.push_back(lv);
+        levels_.push_back(pl.lv);
         return LTLB200_TIME_BUDGET;
     }
-    u64 constructed = 0, n_tiles = 0;
-    plan_level(cost, op_mask, lv, constructed, n_tiles);
-    if (constructed == 0) {
-        levels_.push_back(lv);
-        return LTLB200_OK;
-    }
-    u64 n_claimed = 0, sep_ord = VAL_EMPTY;
+    u64 n_tiles = 0;
+    plan_level(cost, op_mask, pl.lv, pl.constructed, n_tiles);
+    pl.active = true;
+    if (pl.constructed == 0) return LTLB200_OK;
+    const LevelMeta &lv = pl.lv;
+    const u64 constructed = pl.constructed;
     try {
         if (table_dirty_) rebuild_table(table_slots());
         CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
@@ -850,30 +874,15 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             // the special-key register (CTR_SPECIAL) persists across levels
             CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, CTR_SPECIAL * sizeof(u64), cudaMemcpyHostToDevice, stream_));
             CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_OVERFLOW, init + CTR_OVERFLOW, (CTR_COUNT - CTR_OVERFLOW) * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+            pl.claim_cap = claim_cap;
             if (wide_) {
                 reserve(stage_rows_, claim_cap * nvec_, false);
                 reserve(stage_ord_, claim_cap, false);
                 reserve(stage_slot_, claim_cap, false);
                 CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
-                WideParams P{};
-                P.store = store_.ptr;
-                P.atoms = d_atoms_;
-                P.slots = wslots_.ptr;
-                P.slot_mask = wslots_.cap - 1;
-                P.stage_rows = stage_rows_.ptr;
-                P.stage_ord = stage_ord_.ptr;
-                P.stage_slot = stage_slot_.ptr;
-                P.stage_cap = claim_cap;
-                P.total_before = total_;
-                P.counters = d_counters_;
-                P.blocks = d_blocks_;
-                P.valid = d_valid_;
-                P.target = d_target_;
-                P.nvec = nvec_;
-                P.log2g = log2g_;
-                P.prune_after_sep = exhaustive ? 0 : 1;
-                P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
-                P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+                WideParams P = wide_params(exhaustive);
+                P.shard_stride = (u64)shard_count;
+                P.shard_offset = (u64)shard_index;
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
                 launch_enumerate_wide(P, lv);
             } else {
@@ -894,6 +903,8 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
                 P.claim_limit = exact ? ~0ull : est;
                 P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
                 P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+                P.shard_stride = (u64)shard_count;
+                P.shard_offset = (u64)shard_index;
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
                 launch_enumerate(P, lv);
             }
@@ -902,17 +913,80 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
             st_.enumerate_ms += ms;
-            st_.enumerate_candidates += constructed;
+            st_.enumerate_candidates += constructed / (u64)shard_count;
             if (h_counters_[CTR_OVERFLOW] == 0) break;
             if (attempt > 8 || (exact && !wide_)) throw CudaError("hash set overflow on an exactly sized table");
             est = std::min(constructed, est * 4);
             rebuild_table(next_pow2(2 * (total_ + est + kSlack)));  // drops this attempt's claims
         }
-        n_claimed = h_counters_[CTR_CLAIMED];  // narrow: claimed slots; wide: reserved staging entries
-        sep_ord = h_counters_[CTR_SEP];
-        const u64 n_seps = h_counters_[CTR_SEPCOUNT];
+    } catch (const MemoryBudget &e) {
+        g_last_error = e.what();
+        table_dirty_ = true;
+        pl.active = false;
+        levels_.push_back(LevelMeta{0, total_, {}});
+        return LTLB200_MEMORY_BUDGET;
+    }
+    pl.n_claimed = h_counters_[CTR_CLAIMED];  // narrow: claimed slots; wide: reserved staging entries
+    pl.sep_ord = h_counters_[CTR_SEP];
+    pl.n_seps = std::min<u64>(h_counters_[CTR_SEPCOUNT], sep_list_.cap);
+    pl.seps_overflow = h_counters_[CTR_SEPCOUNT] > sep_list_.cap;
+    *n_claimed_out = pl.n_claimed;
+    *sep_ord_out = pl.sep_ord;
+    *n_seps_out = pl.n_seps;
+    return LTLB200_OK;
+}
 
-        // ---- finalise: rank winners by ordinal, append to the cache
+WideParams Engine::wide_params(bool exhaustive) const {
+    WideParams P{};
+    P.store = store_.ptr;
+    P.atoms = d_atoms_;
+    P.slots = wslots_.ptr;
+    P.slot_mask = wslots_.cap - 1;
+    P.stage_rows = stage_rows_.ptr;
+    P.stage_ord = stage_ord_.ptr;
+    P.stage_slot = stage_slot_.ptr;
+    P.stage_cap = pending_.claim_cap;
+    P.total_before = total_;
+    P.counters = d_counters_;
+    P.blocks = d_blocks_;
+    P.valid = d_valid_;
+    P.target = d_target_;
+    P.nvec = nvec_;
+    P.log2g = log2g_;
+    P.prune_after_sep = exhaustive ? 0 : 1;
+    P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
+    P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+    P.shard_stride = 1;
+    P.shard_offset = 0;
+    return P;
+}
+
+// Finalises the pending level.  `sep_ord` = smallest ordinal of a fresh separating candidate
+// over ALL shards (all ones = none); `seps` = every separating ordinal of the level (exhaustive
+// runs; NULL = use what this handle recorded itself).
+int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new,
+                      int64_t *sep_gid, int64_t *constructed_delta) {
+    if (!pending_.active) throw std::invalid_argument("level_end without level_begin");
+    if (batch < 1) throw std::invalid_argument("batch_size must be >= 1");
+    CUDA_CHECK(cudaSetDevice(device_));
+    PendingLevel &pl = pending_;
+    LevelMeta &lv = pl.lv;
+    const bool exhaustive = pl.exhaustive;
+    const u64 constructed = pl.constructed;
+    *n_new = 0;
+    *sep_gid = -1;
+    *constructed_delta = 0;
+    pl.active = false;
+    if (constructed == 0) {
+        levels_.push_back(lv);
+        return LTLB200_OK;
+    }
+    try {
+        // claims may have grown through claims_import
+        CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        if (h_counters_[CTR_OVERFLOW]) throw CudaError("hash set overflow while importing claims");
+        const u64 n_claimed = h_counters_[CTR_CLAIMED];
         const bool cut = !exhaustive && sep_ord != VAL_EMPTY;
         const u64 n_bits = cut ? sep_ord + 1 : constructed;
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
@@ -922,6 +996,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         reserve(ords_, total_ + n_claimed, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
         CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+        CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SEP, &sep_ord, sizeof(u64), cudaMemcpyHostToDevice, stream_));
         const u64 ord_limit = cut ? sep_ord : VAL_EMPTY - 1;
         FinalizeParams F{};
         WideFinalize W{};
@@ -931,7 +1006,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
             W.stage_rows = stage_rows_.ptr;
             W.stage_ord = stage_ord_.ptr;
             W.stage_slot = stage_slot_.ptr;
-            W.n_staged = std::min(n_claimed, stage_ord_.cap);
+            W.n_staged = std::min(n_claimed, pl.claim_cap);
             W.bitmap = bitmap_.ptr;
             W.sb_rank = sb_rank_.ptr;
             W.ord_limit = ord_limit;
@@ -979,7 +1054,17 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
         }
         // exhaustive runs: the reference reports, per level, the first CHUNK whose first
         // separating candidate is fresh (engine.py:331,425-433); reproduce that exactly
-        if (exhaustive && n_seps > 0 && n_seps <= sep_list_.cap) chunk_exact_separator(lv, n_seps, (u64)batch);
+        if (exhaustive) {
+            std::vector<u64> all;
+            if (seps) all.assign(seps, seps + n_seps);
+            else if (pl.n_seps && !pl.seps_overflow) {
+                all.resize((size_t)pl.n_seps);
+                CUDA_CHECK(cudaMemcpyAsync(all.data(), sep_list_.ptr, pl.n_seps * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+                CUDA_CHECK(cudaStreamSynchronize(stream_));
+                st_.d2h_bytes += pl.n_seps * sizeof(u64);
+            }
+            if (!all.empty()) chunk_exact_separator(lv, all, (u64)batch);
+        }
         level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
         if (wide_) {
             const u64 work = W.n_staged * (u64)nvec_;
@@ -1017,6 +1102,94 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     levels_.push_back(std::move(lv));
     if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
     return LTLB200_OK;
+}
+
+int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
+                         int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
+    if (batch < 1) throw std::invalid_argument("batch_size must be >= 1");
+    *n_new = 0;
+    *sep_gid = -1;
+    *constructed_delta = 0;
+    u64 n_claimed = 0, sep_ord = VAL_EMPTY, n_seps = 0;
+    const int rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps);
+    if (rc != LTLB200_OK) return rc;
+    return level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
+}
+
+// ---- claim exchange (one search over several GPUs) --------------------------------------------
+
+// counts[o] = number of this level's local claims whose hash owner is rank o
+void Engine::claims_count(int owners, u64 *counts) {
+    if (!pending_.active) throw std::invalid_argument("claims_count outside a level");
+    CUDA_CHECK(cudaSetDevice(device_));
+    reserve(xchg_, (u64)owners * 2, false);
+    CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, (u64)owners * 2 * sizeof(u64), stream_));
+    CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    const u64 n = wide_ ? std::min(h_counters_[CTR_CLAIMED], pending_.claim_cap) : h_counters_[CTR_CLAIMED];
+    pending_.n_claimed = n;
+    if (n) {
+        const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
+        if (wide_) wide_export_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
+        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, new_list_.ptr, n, d_counters_, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(counts, xchg_.ptr, (u64)owners * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    pending_.owner_counts.assign(counts, counts + owners);
+}
+
+// writes the local claims grouped by owner (owner 0 first) to device buffers sized by claims_count
+void Engine::claims_pack(int owners, void *rows_dev, void *ords_dev) {
+    if (!pending_.active || (int)pending_.owner_counts.size() != owners) throw std::invalid_argument("claims_pack needs claims_count first");
+    CUDA_CHECK(cudaSetDevice(device_));
+    std::vector<u64> cursors((size_t)owners);
+    u64 acc = 0;
+    for (int o = 0; o < owners; ++o) {
+        cursors[o] = acc;
+        acc += pending_.owner_counts[o];
+    }
+    CUDA_CHECK(cudaMemcpyAsync(xchg_.ptr + owners, cursors.data(), (u64)owners * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    const u64 n = pending_.n_claimed;
+    if (n) {
+        const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
+        if (wide_) wide_export_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
+        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, new_list_.ptr, n, d_counters_, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+    }
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // `cursors` leaves scope; the caller hands the buffers to NCCL next
+}
+
+// insert-or-min `n` records (device buffers) into the local set
+void Engine::claims_import(const void *rows_dev, const void *ords_dev, u64 n) {
+    if (!pending_.active) throw std::invalid_argument("claims_import outside a level");
+    if (!n) return;
+    CUDA_CHECK(cudaSetDevice(device_));
+    if (wide_) {
+        WideParams P = wide_params(pending_.exhaustive);
+        P.sep_list = nullptr;
+        const u64 groups = (u64)(CTA_THREADS >> log2g_);
+        const int grid = (int)std::max<u64>(1, std::min<u64>((n + groups - 1) / groups, (u64)sm_count_ * 8));
+        wide_import_kernel<<<grid, CTA_THREADS, 0, stream_>>>(P, (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
+    } else {
+        const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
+        narrow_import_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, d_counters_, new_list_.ptr, new_list_.cap,
+                                                        (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
+    }
+    CUDA_CHECK(cudaGetLastError());
+    st_.kernel_launches++;
+}
+
+// every separating ordinal this handle recorded in the pending level (exhaustive runs)
+u64 Engine::seps_copy(u64 *out, u64 cap) {
+    const u64 n = std::min(pending_.n_seps, cap);
+    if (n) {
+        CUDA_CHECK(cudaMemcpyAsync(out, sep_list_.ptr, n * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
+    return n;
 }
 
 int Engine::level_info(int cost, int64_t *n, int64_t *base) const {
@@ -1156,6 +1329,64 @@ int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int3
                                      sep_gid, constructed_delta);
     });
 }
+
+int ltlb200_level_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, double deadline_s,
+                        int32_t shard_index, int32_t shard_count, uint64_t *n_claimed, uint64_t *sep_ord, uint64_t *n_seps) {
+    if (!e || !n_claimed || !sep_ord || !n_seps) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        ltlb200::u64 a = 0, b = 0, c = 0;
+        int rc = e->impl->level_begin(cost, op_mask, exhaustive != 0, deadline_s, shard_index, shard_count, &a, &b, &c);
+        *n_claimed = a;
+        *sep_ord = b;
+        *n_seps = c;
+        return rc;
+    });
+}
+
+int ltlb200_level_end(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, int64_t batch_size,
+                      uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
+    if (!e || !n_new || !sep_gid || !constructed_delta) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        return e->impl->level_end(sep_ord, (const ltlb200::u64 *)seps, n_seps, batch_size, memory_budget_bytes, n_new, sep_gid,
+                                  constructed_delta);
+    });
+}
+
+int ltlb200_claims_count(ltlb200_engine *e, int32_t owners, uint64_t *counts) {
+    if (!e || !counts || owners < 1) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        e->impl->claims_count(owners, (ltlb200::u64 *)counts);
+        return LTLB200_OK;
+    });
+}
+
+int ltlb200_claims_pack(ltlb200_engine *e, int32_t owners, void *rows_dev, void *ords_dev) {
+    if (!e || owners < 1) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        e->impl->claims_pack(owners, rows_dev, ords_dev);
+        return LTLB200_OK;
+    });
+}
+
+int ltlb200_claims_import(ltlb200_engine *e, const void *rows_dev, const void *ords_dev, uint64_t n) {
+    if (!e) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        e->impl->claims_import(rows_dev, ords_dev, n);
+        return LTLB200_OK;
+    });
+}
+
+int64_t ltlb200_seps_copy(ltlb200_engine *e, uint64_t *out, uint64_t cap) {
+    if (!e || (!out && cap)) return LTLB200_ERR_ARGUMENT;
+    int64_t n = 0;
+    int rc = guarded([&] {
+        n = (int64_t)e->impl->seps_copy((ltlb200::u64 *)out, cap);
+        return LTLB200_OK;
+    });
+    return rc < 0 ? rc : n;
+}
+
+int32_t ltlb200_key_bytes(const ltlb200_engine *e) { return e ? e->impl->key_bytes() : 0; }
 
 double ltlb200_now(void) { return ltlb200::monotonic_s(); }
 

@@ -84,6 +84,7 @@ struct NarrowParams {
     const BlockDesc *blocks;
     int block_begin, block_end;  // this launch's blocks (all of one operator)
     u64 tile_begin, tile_end;    // their tiles in the level's flattened tile space
+    u64 shard_stride, shard_offset;  // this rank takes tiles tile_begin + shard_offset + k*shard_stride (1, 0 = all)
     int ticket;                  // index of this launch's ticket counter
     uint4 valid;                 // Layout.masks packed
     uint4 target;                // Layout.target packed
@@ -398,7 +399,8 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_ke
         __syncwarp();
         if (lane == 0) {
             u64 t = P.tile_end;
-            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull) t = P.tile_begin + atomicAdd(&P.counters[P.ticket], 1ull);
+            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+                t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
             ws.ticket = t;
             ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
             if (t < P.tile_end) {
@@ -497,6 +499,71 @@ __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 
                 break;
             }
             slot = (slot + 1) & slot_mask;
+        }
+    }
+}
+
+// ---- exchange of a level's claims between ranks (one search sharded over several GPUs) ----
+// A record is {key (uint4), ordinal (u64)}.  owner(key) = a hash independent of the slot hash.
+
+__device__ __forceinline__ uint32_t key_owner(uint4 key, uint32_t owners) {
+    return hash_vec(key, 0x5BD1E995u) % owners;
+}
+
+// counts[o] += claims of this level owned by rank o; with `cursors`, also writes the records
+// grouped by owner (cursors[o] = next free position of owner o's range)
+__global__ void __launch_bounds__(256) narrow_export_kernel(const Slot16 *slots, const uint32_t *new_list, u64 n_claimed,
+                                                            const u64 *counters, uint32_t owners, u64 *counts,
+                                                            u64 *cursors, uint4 *keys_out, u64 *ords_out) {
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
+        const uint32_t slot = new_list[t];
+        const uint4 key = slot == SLOT_SPECIAL ? make_uint4(~0u, ~0u, ~0u, ~0u) : slots[slot].key;
+        const u64 ord = (slot == SLOT_SPECIAL ? counters[CTR_SPECIAL] : slots[slot].val) & ~LEVEL_FLAG;
+        const uint32_t o = key_owner(key, owners);
+        if (cursors) {
+            const u64 pos = atomicAdd(&cursors[o], 1ull);
+            keys_out[pos] = key;
+            ords_out[pos] = ord;
+        } else {
+            atomicAdd(&counts[o], 1ull);
+        }
+    }
+}
+
+// insert-or-min received records into the local set; newly claimed slots join the level's claim list
+__global__ void __launch_bounds__(256) narrow_import_kernel(Slot16 *slots, u64 slot_mask, u64 *counters, uint32_t *new_list,
+                                                            u64 new_list_cap, const uint4 *keys, const u64 *ords, u64 n) {
+    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (u64)gridDim.x * blockDim.x) {
+        const uint4 key = keys[t];
+        const u64 val = LEVEL_FLAG | ords[t];
+        bool claimed = false;
+        uint32_t where = SLOT_SPECIAL;
+        if (key_is_empty(key)) {
+            claimed = atomicMin(&counters[CTR_SPECIAL], val) == VAL_EMPTY;
+        } else {
+            u64 slot = hash_vec(key, 0u) & slot_mask;
+            for (;;) {
+                uint4 k = ld_cg_u4(&slots[slot].key);
+                if (key_is_empty(k)) {
+                    k = cas128(&slots[slot].key, empty, key);
+                    if (key_is_empty(k)) {
+                        claimed = true;
+                        k = key;
+                    }
+                }
+                if (v_eq(k, key)) {
+                    atomicMin(&slots[slot].val, val);
+                    where = (uint32_t)slot;
+                    break;
+                }
+                slot = (slot + 1) & slot_mask;
+            }
+        }
+        if (claimed) {
+            const u64 pos = atomicAdd(&counters[CTR_CLAIMED], 1ull);
+            if (pos < new_list_cap) new_list[pos] = where;
+            else atomicExch(&counters[CTR_OVERFLOW], 1ull);
         }
     }
 }

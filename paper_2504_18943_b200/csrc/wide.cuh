@@ -46,6 +46,7 @@ struct WideParams {
     const BlockDesc *blocks;
     int block_begin, block_end;
     u64 tile_begin, tile_end;
+    u64 shard_stride, shard_offset;
     int ticket;
     const uint4 *valid;   // Layout.masks packed, nvec vectors
     const uint4 *target;  // Layout.target packed, nvec vectors
@@ -307,7 +308,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) wide_level_kernel(const WidePa
         __syncwarp();
         if (lane == 0) {
             u64 t = P.tile_end;
-            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull) t = P.tile_begin + atomicAdd(&P.counters[P.ticket], 1ull);
+            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+                t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
             ws.ticket = t;
             ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
             if (t < P.tile_end) {
@@ -393,6 +395,57 @@ __global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_
         u64 s = a & slot_mask;
         const u64 word = slot_word(b >> 8, gid);
         while (atomicCAS(&slots[s], 0ull, word) != 0ull) s = (s + 1) & slot_mask;
+    }
+}
+
+// ---- exchange of a level's claims between ranks (wide rows) ----------------------------------
+
+__device__ __forceinline__ uint32_t row_owner(const uint4 *row, int nvec, uint32_t owners) {
+    uint32_t h = 0;
+    for (int p = 0; p < nvec; ++p) h ^= hash_vec(row[p], 0x5BD1E995u * (uint32_t)(p + 1));
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 13;
+    return h % owners;
+}
+
+// one thread per staging entry: count per owner, or (with cursors) copy the records out grouped by owner
+__global__ void __launch_bounds__(256) wide_export_kernel(const uint4 *stage_rows, const u64 *stage_ord, u64 n_staged, int nvec,
+                                                          uint32_t owners, u64 *counts, u64 *cursors, uint4 *rows_out,
+                                                          u64 *ords_out) {
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_staged; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = stage_ord[t];
+        if (ord == VAL_EMPTY) continue;  // reserved but never published
+        const uint32_t o = row_owner(stage_rows + t * nvec, nvec, owners);
+        if (cursors) {
+            const u64 pos = atomicAdd(&cursors[o], 1ull);
+            for (int p = 0; p < nvec; ++p) rows_out[pos * nvec + p] = stage_rows[t * nvec + p];
+            ords_out[pos] = ord;
+        } else {
+            atomicAdd(&counts[o], 1ull);
+        }
+    }
+}
+
+// one group per received record: the same insert as the enumeration kernel
+__global__ void __launch_bounds__(CTA_THREADS) wide_import_kernel(const WideParams P, const uint4 *rows, const u64 *ords, u64 n) {
+    const int lane = threadIdx.x & 31;
+    const int G = 1 << P.log2g;
+    GroupGeom g;
+    g.base = lane & ~(G - 1);
+    g.part = lane & (G - 1);
+    g.leader = g.base;
+    g.has_part = g.part < P.nvec;
+    g.mask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << g.base;
+    GroupState gs;
+    const u64 groups_per_block = (u64)(CTA_THREADS >> P.log2g);
+    const u64 first = (u64)blockIdx.x * groups_per_block + (threadIdx.x >> P.log2g);
+    for (u64 t = first; t < n; t += (u64)gridDim.x * groups_per_block) {
+        const uint4 part = g.has_part ? rows[t * P.nvec + g.part] : make_uint4(0, 0, 0, 0);
+        uint32_t slot, fp;
+        row_hash(part, g, P.log2g, slot, fp);
+        slot &= (uint32_t)P.slot_mask;
+        wide_insert(P, g, gs, part, slot, fp, __ldcg(&P.slots[slot]), ords[t]);
     }
 }
 

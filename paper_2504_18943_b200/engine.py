@@ -141,6 +141,7 @@ class CandidateStore:
         self.trace_count = spec.trace_count
         self.key_words = -(-(self.trace_count * self.dtype.itemsize) // 8)
         self.levels: list[_Level] = []
+        self._device = int(device)
         lib = _native.load()
         if lib.ltlb200_device_count() < 1:
             raise _native.NativeEngineError("no usable B200: " + _native.last_error())
@@ -208,6 +209,87 @@ class CandidateStore:
         )
         base = self.total
         self.levels.append(_Level(self, cost, n_new.value, base))
+        return status, n_new.value, (None if sep.value < 0 else sep.value), delta.value
+
+    # -- shard-engine interface used by dist.sharded_expand_level (one search over several GPUs) ----
+    @property
+    def key_bytes(self) -> int:
+        return int(_native.load().ltlb200_key_bytes(self._handle))
+
+    @property
+    def torch_device(self):
+        import torch
+
+        return torch.device("cuda", self._device)
+
+    def level_begin(self, cost, op_mask, exhaustive, deadline, shard_index, shard_count):
+        """Enumerate this rank's shard of level ``cost``; ``deadline`` is on ``time.perf_counter()``."""
+        n_claimed, sep_ord, n_seps = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        native_deadline = -1.0 if deadline is None else _monotonic() + (deadline - time.perf_counter())
+        status = _native.check(
+            _native.load().ltlb200_level_begin(self._handle, cost, op_mask, int(exhaustive), native_deadline,
+                                               shard_index, shard_count, ctypes.byref(n_claimed),
+                                               ctypes.byref(sep_ord), ctypes.byref(n_seps)),
+            f"level_begin({cost})",
+        )
+        self._pending_seps = n_seps.value
+        if status != _native.OK:  # the level was closed (empty) by the engine
+            self.levels.append(_Level(self, cost, 0, self.total))
+        return status, n_claimed.value, sep_ord.value, n_seps.value
+
+    def claims_count(self, owners: int) -> list[int]:
+        counts = (ctypes.c_uint64 * owners)()
+        _native.check(_native.load().ltlb200_claims_count(self._handle, owners, counts), "claims_count")
+        return [int(c) for c in counts]
+
+    def claims_pack(self, owners: int, total: int):
+        import torch
+
+        rows = torch.empty((total, self.key_bytes), dtype=torch.uint8, device=self.torch_device)
+        ords = torch.empty((total,), dtype=torch.int64, device=self.torch_device)
+        _native.check(
+            _native.load().ltlb200_claims_pack(self._handle, owners, ctypes.c_void_p(rows.data_ptr()),
+                                               ctypes.c_void_p(ords.data_ptr())),
+            "claims_pack",
+        )
+        return rows, ords
+
+    def claims_import(self, rows, ords) -> None:
+        import torch
+
+        n = int(ords.shape[0])
+        if n == 0:
+            return
+        rows, ords = rows.contiguous(), ords.contiguous()
+        torch.cuda.current_stream(self.torch_device).synchronize()  # NCCL wrote these on torch's stream
+        _native.check(
+            _native.load().ltlb200_claims_import(self._handle, ctypes.c_void_p(rows.data_ptr()),
+                                                 ctypes.c_void_p(ords.data_ptr()), n),
+            "claims_import",
+        )
+
+    def separating_ordinals(self):
+        import torch
+
+        n = int(getattr(self, "_pending_seps", 0))
+        host = np.empty(max(n, 1), dtype=np.uint64)
+        got = _native.load().ltlb200_seps_copy(self._handle, host.ctypes.data, n)
+        _native.check(int(got), "seps_copy")
+        return torch.from_numpy(host[: int(got)].astype(np.int64)).to(self.torch_device)
+
+    def level_end(self, sep_ord, seps, batch_size, memory_budget_bytes):
+        n_new, sep, delta = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        seps_ptr, n_seps = None, 0
+        if seps is not None:
+            host = np.ascontiguousarray(seps.detach().cpu().numpy().astype(np.uint64))
+            seps_ptr, n_seps = host.ctypes.data, len(host)
+        status = _native.check(
+            _native.load().ltlb200_level_end(self._handle, int(sep_ord), seps_ptr, n_seps, int(batch_size),
+                                             int(memory_budget_bytes), ctypes.byref(n_new), ctypes.byref(sep),
+                                             ctypes.byref(delta)),
+            "level_end",
+        )
+        self.levels.append(_Level(self, len(self.levels) + 1, n_new.value, self.total))
         return status, n_new.value, (None if sep.value < 0 else sep.value), delta.value
 
     def _copy_level(self, cost: int, n: int):

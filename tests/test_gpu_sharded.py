@@ -1,0 +1,109 @@
+"""GPU tests of the sharded-search primitives of the C ABI (level_begin / claims_* / level_end).
+
+Only one GPU is available to the test run, so two stores on the same device play two ranks
+and the test moves the exchange records between them by hand, step for step as
+dist.sharded_expand_level does over NCCL; a second test drives the real protocol code through
+a one-rank NCCL group.  Bar: both "ranks" end every level byte-identical to the CPU oracle."""
+
+import os
+import socket
+
+import pytest
+import torch
+
+import oracle
+from helpers import assert_levels_equal
+from paper_2504_18943_b200 import dist as pdist
+from paper_2504_18943_b200 import engine, to_text, workloads
+
+pytestmark = pytest.mark.gpu
+NO_SEP = (1 << 64) - 1
+
+
+def _exchange_level(stores, cost, cfg):
+    world = len(stores)
+    mask = engine.operator_mask(cfg.operators)
+    begun = [s.level_begin(cost, mask, cfg.exhaustive, None, r, world) for r, s in enumerate(stores)]
+    assert all(b[0] == 0 for b in begun)
+    # 1. route to owners
+    packed = []
+    for s in stores:
+        counts = s.claims_count(world)
+        rows, ords = s.claims_pack(world, sum(counts))
+        packed.append((counts, rows, ords))
+    for owner, s in enumerate(stores):
+        rows_in, ords_in = [], []
+        for counts, rows, ords in packed:
+            lo = sum(counts[:owner])
+            rows_in.append(rows[lo:lo + counts[owner]])
+            ords_in.append(ords[lo:lo + counts[owner]])
+        s.claims_import(torch.cat(rows_in), torch.cat(ords_in))  # 2. owner reduces
+    # 3. owners publish
+    winners_rows, winners_ords = [], []
+    for owner, s in enumerate(stores):
+        counts = s.claims_count(world)
+        rows, ords = s.claims_pack(world, sum(counts))
+        lo = sum(counts[:owner])
+        winners_rows.append(rows[lo:lo + counts[owner]])
+        winners_ords.append(ords[lo:lo + counts[owner]])
+    all_rows, all_ords = torch.cat(winners_rows), torch.cat(winners_ords)
+    for s in stores:
+        s.claims_import(all_rows, all_ords)
+    # 4. separator
+    sep = min(b[2] for b in begun)
+    seps = torch.cat([s.separating_ordinals() for s in stores]) if cfg.exhaustive else None
+    return [s.level_end(sep, seps, cfg.batch_size, 0) for s in stores]
+
+
+@pytest.mark.parametrize("workload,seed,max_cost,exhaustive,world", [
+    ("spec1", 0, 6, False, 2),
+    ("spec2", 0, 10, True, 2),
+    ("c3", 0, 9, True, 3),
+    ("c5", 0, 7, True, 2),       # 128-byte rows
+    ("c3wide", 0, 7, True, 2),   # 80-byte rows (5 vectors in groups of 8 lanes)
+    ("c1", 1, 14, False, 2),
+])
+def test_shards_on_one_gpu_agree_with_oracle(workload, seed, max_cost, exhaustive, world):
+    spec = workloads.named_workload(workload, seed)
+    cfg = engine.EngineConfig(max_cost=max_cost, exhaustive=exhaustive, memory_budget_mb=1 << 20)
+    stores = [engine.CandidateStore(spec) for _ in range(world)]
+    ref = oracle.OracleStore(spec)
+    try:
+        found = None
+        for cost in range(1, max_cost + 1):
+            results = _exchange_level(stores, cost, cfg)
+            o_new, o_sep, o_delta, _ = ref.expand_level(cost, cfg.operators, exhaustive, cfg.batch_size, memory_budget_mb=1 << 20)
+            for r, (status, n_new, sep, delta) in enumerate(results):
+                where = f"{workload} cost {cost} rank {r}"
+                assert (status, n_new, sep, delta) == (0, o_new, o_sep, o_delta), where
+                assert_levels_equal(stores[r].level(cost), ref.level(cost), where)
+            if o_sep is not None and found is None:
+                found = (o_sep, cost)
+                if not exhaustive:
+                    break
+        if found:
+            want = to_text(oracle.reconstruct(ref, found[0]), spec.alphabet)
+            assert all(to_text(engine.reconstruct(s, found[0]), spec.alphabet) == want for s in stores)
+    finally:
+        for s in stores:
+            s.close()
+
+
+def test_protocol_over_nccl_with_one_rank():
+    import torch.distributed as dist
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        spec = workloads.spec2()
+        cfg = engine.EngineConfig(max_cost=11, exhaustive=True, memory_budget_mb=1 << 20)
+        res = pdist.synthesize_sharded(spec, cfg)
+        want = oracle.synthesize(spec, max_cost=11, exhaustive=True)
+        assert (res.outcome, res.stats.unique, res.stats.constructed) == (want.outcome, want.unique, want.constructed)
+        res = pdist.synthesize_sharded(workloads.spec1(), engine.EngineConfig())
+        assert to_text(res.formula, workloads.spec1().alphabet) == "!(b U a)"
+    finally:
+        dist.destroy_process_group()
