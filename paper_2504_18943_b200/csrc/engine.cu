@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <ctime>
 #include <map>
@@ -46,6 +47,19 @@ struct MemoryBudget : std::runtime_error {
         if (err__ != cudaSuccess)                                                                     \
             throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(err__) + " (" __FILE__ ":" + \
                             std::to_string(__LINE__) + ")");                                          \
+    } while (0)
+
+static bool debug_on() {
+    static const bool on = getenv("LTLB200_DEBUG") != nullptr;
+    return on;
+}
+#define DBG(...)                                   \
+    do {                                           \
+        if (debug_on()) {                          \
+            fprintf(stderr, "[ltlb200] " __VA_ARGS__); \
+            fputc('\n', stderr);                   \
+            fflush(stderr);                        \
+        }                                          \
     } while (0)
 
 static double monotonic_s() {
@@ -786,8 +800,13 @@ static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int o
         P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
         P.ticket = CTR_TICKET0 + group;
         const int grid = (int)std::min<u64>((P.tile_end - P.tile_begin + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count * occupancy);
+        DBG("launch op=%d blocks=[%zu,%zu) tiles=[%llu,%llu) grid=%d", (int)lv.blocks[b0].op, b0, b1, (unsigned long long)P.tile_begin, (unsigned long long)P.tile_end, grid);
         launch((int)lv.blocks[b0].op, P, grid);
         CUDA_CHECK(cudaGetLastError());
+        if (debug_on()) {
+            CUDA_CHECK(cudaDeviceSynchronize());
+            DBG("  done");
+        }
         st.kernel_launches++;
         st.enumerate_launches++;
         b0 = b1;
@@ -866,6 +885,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * (32 >> log2g_) * WIDE_CHUNK * 8 + 1024;
             const u64 claim_cap = est + (wide_ ? wide_slack : (exact ? 64 : kSlack));
             const u64 want_slots = next_pow2(2 * (total_ + claim_cap));
+            DBG("level %d attempt %d: constructed=%llu est=%llu claim_cap=%llu slots=%llu want=%llu", cost, attempt, (unsigned long long)constructed, (unsigned long long)est, (unsigned long long)claim_cap, (unsigned long long)table_slots(), (unsigned long long)want_slots);
             if (want_slots > table_slots()) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most
             if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
             u64 init[CTR_COUNT];
@@ -926,6 +946,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         levels_.push_back(LevelMeta{0, total_, {}});
         return LTLB200_MEMORY_BUDGET;
     }
+    DBG("level %d enumerated: claimed=%llu sep=%llx", cost, (unsigned long long)h_counters_[CTR_CLAIMED], (unsigned long long)h_counters_[CTR_SEP]);
     pl.n_claimed = h_counters_[CTR_CLAIMED];  // narrow: claimed slots; wide: reserved staging entries
     pl.sep_ord = h_counters_[CTR_SEP];
     pl.n_seps = std::min<u64>(h_counters_[CTR_SEPCOUNT], sep_list_.cap);

@@ -28,7 +28,10 @@ namespace ltlb200 {
 constexpr int WIDE_ROW_VECS = 256;   // uint4 vectors of scalar-operand rows staged per warp (4 KiB)
 constexpr int WIDE_TERMS = 128;      // max scalar rows per tile (G = 2)
 constexpr int WIDE_CHUNK = 16;       // staging entries a group reserves at a time
-constexpr int WIDE_BATCH = 2;        // first slot probes a group keeps in flight
+#ifndef LTLB200_WIDE_BATCH
+#define LTLB200_WIDE_BATCH 4
+#endif
+constexpr int WIDE_BATCH = LTLB200_WIDE_BATCH;  // candidates a group settles per phase round
 constexpr u64 SLOT_IDX_MASK = (1ull << 40) - 1;
 constexpr int MAX_NVEC = 32;
 
@@ -102,10 +105,20 @@ __device__ __forceinline__ void row_hash(uint4 part, const GroupGeom &g, int log
     h_fp = b >> 8;
 }
 
-// Group-collective insert of one candidate row.  `w0` is the already loaded word of slot `s`.
-// Returns true when the CM was not stored by an earlier level (fresh for this level).
-__device__ __forceinline__ bool wide_insert(const WideParams &P, const GroupGeom &g, GroupState &gs, uint4 part,
-                                            uint32_t s, uint32_t fp, u64 w0, u64 ord) {
+// the slot word as seen by the group's leader, broadcast to the group: every lane must act on
+// the SAME value (a slot can be published by another group between two lanes' loads)
+__device__ __forceinline__ u64 group_load_slot(const u64 *slot, const GroupGeom &g) {
+    u64 w = 0;
+    if ((int)(threadIdx.x & 31) == g.leader) w = __ldcg(slot);
+    return __shfl_sync(g.mask, w, g.leader);
+}
+
+// Serial slow path: group-collective insert of one candidate row.  `w0` is the (group-uniform)
+// word of slot `s`.  Returns true when the CM was not stored by an earlier level (fresh for
+// this level).  Out of line on purpose: it is rare after wide_batch's phases, and inlining it
+// at every call site blew the kernel past the instruction cache (25 % no-instruction stalls).
+__device__ __noinline__ bool wide_insert(const WideParams &P, GroupGeom g, GroupState &gs, uint4 part, uint32_t s,
+                                         uint32_t fp, u64 w0, u64 ord) {
     const int lane = threadIdx.x & 31;
     const uint32_t mask32 = (uint32_t)P.slot_mask;
     bool row_staged = false;
@@ -162,32 +175,124 @@ __device__ __forceinline__ bool wide_insert(const WideParams &P, const GroupGeom
             }
         }
         s = (s + 1) & mask32;
-        w = __ldcg(&P.slots[s]);
+        w = group_load_slot(&P.slots[s], g);
     }
 }
 
-// Process WIDE_BATCH candidates of one group: hash, first slot probe (all in flight), then insert.
+// Process WIDE_BATCH candidates of one group in lock-step PHASES, so that the latencies of a
+// claim (slot probe -> row write + fence -> CAS) and of a duplicate check (slot probe -> row
+// read) are paid once per batch, not once per candidate:
+//   1. hash all, issue all first slot probes;
+//   2. per candidate: empty slot -> reserve a staging entry and write the row;
+//      fingerprint match -> issue the read of the stored row;  one fence for the whole batch;
+//   3. the group leader issues all publishing CASes back to back;
+//   4. settle: CAS won -> record ordinal; stored row equal -> duplicate (old) or atomicMin (this
+//      level); anything else (lost race, fingerprint alias, collision) -> the serial slow path.
 template <int LW, typename OrdOf>
 __device__ __forceinline__ void wide_batch(const WideParams &P, const GroupGeom &g, GroupState &gs,
                                            const uint4 (&cand)[WIDE_BATCH], const bool (&live)[WIDE_BATCH],
                                            const bool (&known)[WIDE_BATCH], uint4 target, OrdOf ord_of) {
     const int lane = threadIdx.x & 31;
+    enum : int { ST_SKIP = 0, ST_CLAIM = 1, ST_CHECK = 2, ST_SLOW = 3 };
     uint32_t slot[WIDE_BATCH], fp[WIDE_BATCH];
-    u64 w0[WIDE_BATCH];
+    u64 w[WIDE_BATCH];
+    int state[WIDE_BATCH];
+    // ---- 1. hashes and first probes
 #pragma unroll
     for (int r = 0; r < WIDE_BATCH; ++r) {
         row_hash(cand[r], g, P.log2g, slot[r], fp[r]);
         slot[r] &= (uint32_t)P.slot_mask;
-        w0[r] = 0;
-        if (live[r] && !known[r]) w0[r] = __ldcg(&P.slots[slot[r]]);
+        w[r] = 0;
+        if (live[r] && !known[r] && lane == g.leader) w[r] = __ldcg(&P.slots[slot[r]]);
     }
+#pragma unroll
+    for (int r = 0; r < WIDE_BATCH; ++r) w[r] = __shfl_sync(0xFFFFFFFFu, w[r], g.leader);  // one value per group
+    // ---- 2. stage rows of the claims, start the row reads of the fingerprint matches
+    uint4 stored[WIDE_BATCH];
+    u64 entry[WIDE_BATCH];
+    int n_claims = 0;
+#pragma unroll
+    for (int r = 0; r < WIDE_BATCH; ++r) {
+        state[r] = ST_SKIP;
+        entry[r] = 0;
+        stored[r] = make_uint4(0, 0, 0, 0);
+        if (!live[r] || known[r]) continue;
+        if (w[r] == 0ull) {
+            state[r] = ST_CLAIM;
+            ++n_claims;
+        } else if ((uint32_t)(w[r] >> 40) == (fp[r] & 0xFFFFFFu)) {
+            state[r] = ST_CHECK;
+            const u64 idx = (w[r] & SLOT_IDX_MASK) - 1;
+            const uint4 *row = idx >= P.total_before ? P.stage_rows + (idx - P.total_before) * P.nvec : P.store + idx * P.nvec;
+            if (g.has_part) stored[r] = __ldcg(row + g.part);
+        } else {
+            state[r] = ST_SLOW;
+        }
+    }
+    if (n_claims) {  // group-uniform
+        if (gs.chunk_next + (u64)n_claims > gs.chunk_end) {  // the rest of the old chunk stays unused
+            u64 first = 0;
+            if (lane == g.leader) first = atomicAdd(&P.counters[CTR_CLAIMED], (u64)WIDE_CHUNK);
+            first = __shfl_sync(g.mask, first, g.leader);
+            gs.chunk_next = first;
+            gs.chunk_end = first + WIDE_CHUNK;
+        }
+#pragma unroll
+        for (int r = 0; r < WIDE_BATCH; ++r) {
+            if (state[r] != ST_CLAIM) continue;
+            entry[r] = gs.chunk_next++;
+            if (entry[r] >= P.stage_cap) {  // staging pool exhausted: the host regrows and redoes the level
+                if (lane == g.leader) atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+                state[r] = ST_SKIP;
+                continue;
+            }
+            if (g.has_part) P.stage_rows[entry[r] * P.nvec + g.part] = cand[r];
+        }
+        __threadfence();
+        __syncwarp(g.mask);
+        // ---- 3. publish: all CASes in flight together
+        u64 old[WIDE_BATCH];
+#pragma unroll
+        for (int r = 0; r < WIDE_BATCH; ++r) {
+            old[r] = 0;
+            if (state[r] == ST_CLAIM && lane == g.leader)
+                old[r] = atomicCAS(&P.slots[slot[r]], 0ull, slot_word(fp[r], P.total_before + entry[r]));
+        }
+#pragma unroll
+        for (int r = 0; r < WIDE_BATCH; ++r) {
+            if (state[r] != ST_CLAIM) continue;
+            w[r] = __shfl_sync(g.mask, old[r], g.leader);
+            if (w[r] != 0ull) state[r] = ST_SLOW;  // lost the race: the staged entry stays unused
+        }
+    }
+    // ---- 4. settle
 #pragma unroll
     for (int r = 0; r < WIDE_BATCH; ++r) {
         if (!live[r]) continue;  // group-uniform
         const uint32_t sep_diff = g.has_part ? cm_sep_diff<LW>(cand[r], target) : 0u;
         const bool sep = group_all_zero(sep_diff, g);
         bool fresh = false;
-        if (!known[r]) fresh = wide_insert(P, g, gs, cand[r], slot[r], fp[r], w0[r], ord_of(r));
+        if (state[r] == ST_CLAIM) {
+            if (lane == g.leader) {
+                atomicMin(&P.stage_ord[entry[r]], ord_of(r));
+                P.stage_slot[entry[r]] = slot[r];
+            }
+            fresh = true;
+        } else if (state[r] == ST_CHECK) {
+            const uint32_t diff = (stored[r].x ^ cand[r].x) | (stored[r].y ^ cand[r].y) | (stored[r].z ^ cand[r].z) | (stored[r].w ^ cand[r].w);
+            if (group_all_zero(g.has_part ? diff : 0u, g)) {
+                const u64 idx = (w[r] & SLOT_IDX_MASK) - 1;
+                if (idx >= P.total_before) {
+                    if (lane == g.leader) atomicMin(&P.stage_ord[idx - P.total_before], ord_of(r));
+                    fresh = true;
+                }
+            } else {  // fingerprint alias: keep probing from the next slot
+                const uint32_t s = (slot[r] + 1) & (uint32_t)P.slot_mask;
+                fresh = wide_insert(P, g, gs, cand[r], s, fp[r], group_load_slot(&P.slots[s], g), ord_of(r));
+            }
+        } else if (state[r] == ST_SLOW) {
+            fresh = wide_insert(P, g, gs, cand[r], slot[r], fp[r], w[r], ord_of(r));
+        }
         if (sep && lane == g.leader) {
             const u64 ord = ord_of(r);
             if (fresh) atomicMin(&P.counters[CTR_SEP], ord);
@@ -290,7 +395,7 @@ __device__ __forceinline__ void wide_binary_tile(const WideParams &P, WideWarpSh
 }
 
 template <int LW, int OP>
-__global__ void __launch_bounds__(CTA_THREADS, 4) wide_level_kernel(const WideParams P) {
+__global__ void __launch_bounds__(CTA_THREADS, 4) wide_level_kernel(const __grid_constant__ WideParams P) {
     __shared__ WideWarpShared s_warp[WARPS_PER_CTA];
     WideWarpShared &ws = s_warp[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -428,7 +533,7 @@ __global__ void __launch_bounds__(256) wide_export_kernel(const uint4 *stage_row
 }
 
 // one group per received record: the same insert as the enumeration kernel
-__global__ void __launch_bounds__(CTA_THREADS) wide_import_kernel(const WideParams P, const uint4 *rows, const u64 *ords, u64 n) {
+__global__ void __launch_bounds__(CTA_THREADS) wide_import_kernel(const __grid_constant__ WideParams P, const uint4 *rows, const u64 *ords, u64 n) {
     const int lane = threadIdx.x & 31;
     const int G = 1 << P.log2g;
     GroupGeom g;
@@ -445,7 +550,7 @@ __global__ void __launch_bounds__(CTA_THREADS) wide_import_kernel(const WidePara
         uint32_t slot, fp;
         row_hash(part, g, P.log2g, slot, fp);
         slot &= (uint32_t)P.slot_mask;
-        wide_insert(P, g, gs, part, slot, fp, __ldcg(&P.slots[slot]), ords[t]);
+        wide_insert(P, g, gs, part, slot, fp, group_load_slot(&P.slots[slot], g), ords[t]);
     }
 }
 
