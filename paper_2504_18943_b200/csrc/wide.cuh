@@ -29,7 +29,7 @@ constexpr int WIDE_ROW_VECS = 256;   // uint4 vectors of scalar-operand rows sta
 constexpr int WIDE_TERMS = 128;      // max scalar rows per tile (G = 2)
 constexpr int WIDE_CHUNK = 16;       // staging entries a group reserves at a time
 #ifndef LTLB200_WIDE_BATCH
-#define LTLB200_WIDE_BATCH 4
+#define LTLB200_WIDE_BATCH 2
 #endif
 constexpr int WIDE_BATCH = LTLB200_WIDE_BATCH;  // candidates a group settles per phase round
 constexpr u64 SLOT_IDX_MASK = (1ull << 40) - 1;
@@ -188,11 +188,21 @@ __device__ __noinline__ bool wide_insert(const WideParams &P, GroupGeom g, Group
 //   3. the group leader issues all publishing CASes back to back;
 //   4. settle: CAS won -> record ordinal; stored row equal -> duplicate (old) or atomicMin (this
 //      level); anything else (lost race, fingerprint alias, collision) -> the serial slow path.
-template <int LW, typename OrdOf>
-__device__ __forceinline__ void wide_batch(const WideParams &P, const GroupGeom &g, GroupState &gs,
-                                           const uint4 (&cand)[WIDE_BATCH], const bool (&live)[WIDE_BATCH],
-                                           const bool (&known)[WIDE_BATCH], uint4 target, OrdOf ord_of) {
+#ifndef LTLB200_WIDE_INLINE_BATCH
+#define LTLB200_WIDE_INLINE_BATCH 1
+#endif
+#if LTLB200_WIDE_INLINE_BATCH
+#define WIDE_BATCH_LINKAGE __forceinline__
+#else
+#define WIDE_BATCH_LINKAGE __noinline__  // one copy per kernel: the hot loop must fit the instruction cache
+#endif
+template <int LW>
+__device__ WIDE_BATCH_LINKAGE void wide_batch(const WideParams &P, const GroupGeom g, GroupState &gs,
+                                              const uint4 (&cand)[WIDE_BATCH], const bool (&live)[WIDE_BATCH],
+                                              const bool (&known)[WIDE_BATCH], const uint4 target,
+                                              const u64 (&ords)[WIDE_BATCH]) {
     const int lane = threadIdx.x & 31;
+    auto ord_of = [&](int r) { return ords[r]; };
     enum : int { ST_SKIP = 0, ST_CLAIM = 1, ST_CHECK = 2, ST_SLOW = 3 };
     uint32_t slot[WIDE_BATCH], fp[WIDE_BATCH];
     u64 w[WIDE_BATCH];
@@ -320,17 +330,18 @@ __device__ __forceinline__ void wide_unary_tile(const WideParams &P, WideWarpSha
     for (int k = 0; k < n_steps; k += WIDE_BATCH) {
         uint4 cand[WIDE_BATCH];
         bool live[WIDE_BATCH], known[WIDE_BATCH];
-        auto ord_of = [&](int r) { return ord0 + first + (u64)(k + r) * groups; };
+        u64 ords[WIDE_BATCH];
 #pragma unroll
         for (int r = 0; r < WIDE_BATCH; ++r) {
             const u64 i = first + (u64)(k + r) * groups;
+            ords[r] = ord0 + i;
             live[r] = k + r < n_steps && i < n;
             const uint4 x = (live[r] && g.has_part) ? __ldg(src + i * P.nvec + g.part) : make_uint4(0, 0, 0, 0);
             cand[r] = cm_apply<LW, OP>(x, x, valid);
             const uint32_t d = (cand[r].x ^ x.x) | (cand[r].y ^ x.y) | (cand[r].z ^ x.z) | (cand[r].w ^ x.w);
             known[r] = OP != OP_ATOM && group_all_zero(d, g);
         }
-        wide_batch<LW>(P, g, gs, cand, live, known, target, ord_of);
+        wide_batch<LW>(P, g, gs, cand, live, known, target, ords);
     }
 }
 
@@ -377,10 +388,11 @@ __device__ __forceinline__ void wide_binary_tile(const WideParams &P, WideWarpSh
         for (int k = 0; k < s_cnt; k += WIDE_BATCH) {
             uint4 cand[WIDE_BATCH];
             bool live[WIDE_BATCH], known[WIDE_BATCH];
-            auto ord_of = [&](int r) { return ws.term[min(k + r, s_cnt - 1)] + lane_term; };
+            u64 ords[WIDE_BATCH];
 #pragma unroll
             for (int r = 0; r < WIDE_BATCH; ++r) {
                 const int sr = min(k + r, s_cnt - 1);
+                ords[r] = ws.term[sr] + lane_term;
                 const uint4 xs = g.has_part ? ws.rows[sr * G + g.part] : make_uint4(0, 0, 0, 0);
                 live[r] = k + r < s_live;
                 cand[r] = VEC_B ? cm_apply<LW, OP>(xs, xv, valid) : cm_apply<LW, OP>(xv, xs, valid);
@@ -389,7 +401,7 @@ __device__ __forceinline__ void wide_binary_tile(const WideParams &P, WideWarpSh
                 const uint32_t ma = __ballot_sync(g.mask, da != 0u) & g.mask, mb = __ballot_sync(g.mask, db != 0u) & g.mask;
                 known[r] = ma == 0u || mb == 0u;
             }
-            wide_batch<LW>(P, g, gs, cand, live, known, target, ord_of);
+            wide_batch<LW>(P, g, gs, cand, live, known, target, ords);
         }
     }
 }
