@@ -288,7 +288,8 @@ private:
     DeviceArray<uint4> store_;
     DeviceArray<u64> ords_;
     DeviceArray<Slot16> slots_;
-    DeviceArray<uint32_t> new_list_;
+    DeviceArray<uint4> claim_key_;   // narrow path: this level's new CMs by claim index
+    DeviceArray<u64> claim_ord_;
     DeviceArray<u64> wslots_;          // wide path: slot words
     DeviceArray<uint4> stage_rows_;    // wide path: this level's new rows
     DeviceArray<u64> stage_ord_;
@@ -307,6 +308,7 @@ private:
         std::vector<u64> owner_counts;
     } pending_;
     WideParams wide_params(bool exhaustive) const;
+    NarrowParams narrow_params(bool exhaustive) const;
     static constexpr u64 kMinSlots = 1ull << 16;
     u64 *d_counters_ = nullptr;
     BlockDesc *d_blocks_ = nullptr;
@@ -494,7 +496,8 @@ Engine::~Engine() {
     release(store_);
     release(ords_);
     release(slots_);
-    release(new_list_);
+    release(claim_key_);
+    release(claim_ord_);
     release(wslots_);
     release(stage_rows_);
     release(stage_ord_);
@@ -883,7 +886,9 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             // staging / claim capacity: the estimate plus what warps may over-reserve in flight
             // (wide: every group of every operator launch may end with a partly used chunk of staging entries)
             const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * (32 >> log2g_) * WIDE_CHUNK * 8 + 1024;
-            const u64 claim_cap = est + (wide_ ? wide_slack : (exact ? 64 : kSlack));
+            // (narrow: every warp of every operator launch may end with a partly used chunk of claim indices)
+            const u64 narrow_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8 + 1024;
+            const u64 claim_cap = est + (wide_ ? wide_slack : narrow_slack);
             const u64 want_slots = next_pow2(2 * (total_ + claim_cap));
             DBG("level %d attempt %d: constructed=%llu est=%llu claim_cap=%llu slots=%llu want=%llu", cost, attempt, (unsigned long long)constructed, (unsigned long long)est, (unsigned long long)claim_cap, (unsigned long long)table_slots(), (unsigned long long)want_slots);
             if (want_slots > table_slots()) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most
@@ -906,23 +911,10 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
                 launch_enumerate_wide(P, lv);
             } else {
-                reserve(new_list_, claim_cap, false);
-                NarrowParams P{};
-                P.store = store_.ptr;
-                P.atoms = d_atoms_;
-                P.slots = slots_.ptr;
-                P.slot_mask = slots_.cap - 1;
-                P.new_list = new_list_.ptr;
-                P.new_list_cap = new_list_.cap;
-                P.counters = d_counters_;
-                P.blocks = d_blocks_;
-                P.valid = valid_;
-                P.target = target_;
-                P.prune_after_sep = exhaustive ? 0 : 1;
-                P.special_possible = special_possible_ ? 1 : 0;
-                P.claim_limit = exact ? ~0ull : est;
-                P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
-                P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+                reserve(claim_key_, claim_cap, false);
+                reserve(claim_ord_, claim_cap, false);
+                CUDA_CHECK(cudaMemsetAsync(claim_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+                NarrowParams P = narrow_params(exhaustive);
                 P.shard_stride = (u64)shard_count;
                 P.shard_offset = (u64)shard_index;
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
@@ -955,6 +947,29 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     *sep_ord_out = pl.sep_ord;
     *n_seps_out = pl.n_seps;
     return LTLB200_OK;
+}
+
+NarrowParams Engine::narrow_params(bool exhaustive) const {
+    NarrowParams P{};
+    P.store = store_.ptr;
+    P.atoms = d_atoms_;
+    P.slots = slots_.ptr;
+    P.slot_mask = slots_.cap - 1;
+    P.claim_key = claim_key_.ptr;
+    P.claim_ord = claim_ord_.ptr;
+    P.claim_cap = pending_.claim_cap;
+    P.epoch = (u64)pending_.cost << EPOCH_SHIFT;
+    P.counters = d_counters_;
+    P.blocks = d_blocks_;
+    P.valid = valid_;
+    P.target = target_;
+    P.prune_after_sep = exhaustive ? 0 : 1;
+    P.special_possible = special_possible_ ? 1 : 0;
+    P.sep_list = exhaustive ? sep_list_.ptr : nullptr;
+    P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
+    P.shard_stride = 1;
+    P.shard_offset = 0;
+    return P;
 }
 
 WideParams Engine::wide_params(bool exhaustive) const {
@@ -1037,10 +1052,9 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
             W.nvec = nvec_;
             wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
         } else {
-            F.slots = slots_.ptr;
-            F.new_list = new_list_.ptr;
-            F.n_claimed = n_claimed;
-            F.counters = d_counters_;
+            F.claim_key = claim_key_.ptr;
+            F.claim_ord = claim_ord_.ptr;
+            F.n_claimed = std::min(n_claimed, pl.claim_cap);
             F.bitmap = bitmap_.ptr;
             F.sb_rank = sb_rank_.ptr;
             F.ord_limit = ord_limit;
@@ -1147,12 +1161,12 @@ void Engine::claims_count(int owners, u64 *counts) {
     CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, (u64)owners * 2 * sizeof(u64), stream_));
     CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
-    const u64 n = wide_ ? std::min(h_counters_[CTR_CLAIMED], pending_.claim_cap) : h_counters_[CTR_CLAIMED];
+    const u64 n = std::min(h_counters_[CTR_CLAIMED], pending_.claim_cap);
     pending_.n_claimed = n;
     if (n) {
         const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
         if (wide_) wide_export_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
-        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, new_list_.ptr, n, d_counters_, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
+        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
         CUDA_CHECK(cudaGetLastError());
         st_.kernel_launches++;
     }
@@ -1176,7 +1190,7 @@ void Engine::claims_pack(int owners, void *rows_dev, void *ords_dev) {
     if (n) {
         const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
         if (wide_) wide_export_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
-        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, new_list_.ptr, n, d_counters_, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
+        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
         CUDA_CHECK(cudaGetLastError());
         st_.kernel_launches++;
     }
@@ -1196,8 +1210,7 @@ void Engine::claims_import(const void *rows_dev, const void *ords_dev, u64 n) {
         wide_import_kernel<<<grid, CTA_THREADS, 0, stream_>>>(P, (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
     } else {
         const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
-        narrow_import_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, d_counters_, new_list_.ptr, new_list_.cap,
-                                                        (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
+        narrow_import_kernel<<<grid, 256, 0, stream_>>>(narrow_params(pending_.exhaustive), (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
     }
     CUDA_CHECK(cudaGetLastError());
     st_.kernel_launches++;

@@ -9,10 +9,13 @@
 //     (CM -> min ordinal) into an open-addressing hash set in HBM whose slot is one
 //     32-byte sector {uint4 key, u64 val}; the key is claimed with ONE 128-bit
 //     atomicCAS, so the full CM is compared, never a fingerprint;
-//   * val < 2^62  : global id of a CM finalised at an earlier level (immutable)
-//     val >= 2^62 : LEVEL_FLAG | ordinal of the best constructor seen so far this level
-//     so "first construction wins" is atomicMin on val, and duplicates of old CMs
-//     (the common case) cost one sector read and no atomic.
+//   * val = [epoch:16 | claim index:48], all ones while unpublished.  The epoch is the cost
+//     level that stored the CM, so "duplicate of an earlier level" (the common case) is one
+//     compare on the high word of the probed sector and needs no write at all, and no slot
+//     has to be rewritten when a level is finalised;
+//   * this level's new CMs live in two dense arrays indexed by claim index -- claim_key
+//     (the CM) and claim_ord (the smallest ordinal that built it, atomicMin) -- which
+//     finalisation reads sequentially; "first construction wins" is that atomicMin.
 //
 // Execution shape (what the first ncu capture asked for): tiles are owned by WARPS, not
 // CTAs, so there is no block barrier anywhere; the hot loop issues exactly one probe per
@@ -43,10 +46,10 @@ constexpr int TILE_V = 32;                        // vector-dimension rows of a 
 constexpr int TILE_S = LTLB200_TILE_S;            // scalar-dimension rows of a binary tile (staged in shared memory)
 constexpr int UNARY_ITEMS = 64;                   // candidates per lane in a unary tile
 constexpr int QUEUE_CAP = 32 * PROBE_BATCH + 32;
-constexpr int CLAIM_CAP = 64;
-constexpr u64 LEVEL_FLAG = 1ull << 62;
+constexpr int CLAIM_CHUNK = 64;  // claim indices a warp reserves at a time
 constexpr u64 VAL_EMPTY = ~0ull;
-constexpr uint32_t SLOT_SPECIAL = 0xFFFFFFFFu;  // pseudo slot of the all-ones key
+constexpr int EPOCH_SHIFT = 48;
+constexpr u64 CLAIM_IDX_MASK = (1ull << EPOCH_SHIFT) - 1;
 
 struct __align__(32) Slot16 {
     uint4 key;  // all ones = empty
@@ -78,9 +81,11 @@ struct NarrowParams {
     const uint4 *atoms;
     Slot16 *slots;
     u64 slot_mask;
-    uint32_t *new_list;
-    u64 new_list_cap;
-    u64 *counters;  // see CTR_*
+    uint4 *claim_key;  // this level's new CMs by claim index
+    u64 *claim_ord;    // smallest ordinal per claim index (all ones = index reserved but unused)
+    u64 claim_cap;
+    u64 epoch;         // this level's epoch (= cost), already shifted into the val's high bits
+    u64 *counters;     // see CTR_*
     const BlockDesc *blocks;
     int block_begin, block_end;  // this launch's blocks (all of one operator)
     u64 tile_begin, tile_end;    // their tiles in the level's flattened tile space
@@ -90,12 +95,11 @@ struct NarrowParams {
     uint4 target;                // Layout.target packed
     int prune_after_sep;         // non-exhaustive: skip work ordered after the best separator so far
     int special_possible;
-    u64 claim_limit;
     u64 *sep_list;  // exhaustive runs: ordinals of every separating candidate (NULL otherwise)
     u64 sep_list_cap;
 };
 
-// [1] claimed slots, [2] separator ordinal (min), [3] special-key val (persists across levels),
+// [1] claim indices reserved, [2] separator ordinal (min), [3] special-key val (persists across levels),
 // [4] overflow flag, [5] winners (summary), [6] rank of the separator (summary),
 // [7] separating candidates recorded, [8..14] one tile ticket per operator launch
 enum : int { CTR_UNUSED = 0, CTR_CLAIMED = 1, CTR_SEP = 2, CTR_SPECIAL = 3, CTR_OVERFLOW = 4, CTR_WINNERS = 5, CTR_SEPRANK = 6, CTR_SEPCOUNT = 7, CTR_TICKET0 = 8, CTR_COUNT = 16 };
@@ -138,13 +142,13 @@ struct __align__(16) WarpShared {
     Parked queue[QUEUE_CAP];
     uint4 rows[TILE_S];  // scalar-operand rows of the current binary tile
     u64 term[TILE_S];    // their ordinal terms
-    uint32_t claims[CLAIM_CAP];
     BlockDesc block;
     u64 ticket, sep_now;
 };
 
 struct WarpState {  // warp-uniform registers
-    uint32_t qfill = 0, cfill = 0;
+    uint32_t qfill = 0;
+    u64 chunk_next = 0, chunk_end = 0;  // claim indices reserved for this warp
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -153,26 +157,8 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// warp-collective: move 32 claims (or all of them when `all`) to the global list
-__device__ __forceinline__ void claims_flush(const NarrowParams &P, WarpShared &ws, WarpState &st, bool all) {
-    const int lane = threadIdx.x & 31;
-    while (st.cfill >= 32u || (all && st.cfill > 0u)) {
-        const uint32_t n = st.cfill >= 32u ? 32u : st.cfill;
-        u64 base = 0;
-        if (lane == 0) base = atomicAdd(&P.counters[CTR_CLAIMED], (u64)n);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
-        if (base + n > P.claim_limit || base + n > P.new_list_cap) {
-            if (lane == 0) atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
-        } else if ((uint32_t)lane < n) {
-            P.new_list[base + lane] = ws.claims[st.cfill - n + lane];
-        }
-        st.cfill -= n;
-    }
-    __syncwarp();
-}
-
 // One resolution round: the top (up to) 32 parked candidates take one probe step each.
-// Settled ones leave (recording claims / separators), the rest are re-queued compacted.
+// Settled ones leave (recording separators), the rest are re-queued compacted.
 __device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &ws, WarpState &st) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = lanemask_lt();
@@ -180,56 +166,92 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &w
     const uint32_t base = st.qfill - take;
     const bool active = (uint32_t)lane < take;
     Parked e = ws.queue[base + (active ? lane : 0)];
-    __syncwarp();  // every lane holds its entry before the slots are reused
-    bool again = false, claimed = false, fresh = false;
+    __syncwarp();  // every lane holds its entry before the queue slots are reused
     const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
-    if (active) {
-        const u64 val = LEVEL_FLAG | e.ord;
-        if (e.flags & PK_SPECIAL) {
-            const u64 old = atomicMin(&P.counters[CTR_SPECIAL], val);
-            claimed = old == VAL_EMPTY;
-            fresh = old >= LEVEL_FLAG;
-        } else if (!(e.flags & PK_OLD)) {
-            Slot16 *slot = &P.slots[e.slot];
-            uint4 k = empty;
-            u64 v = VAL_EMPTY;
-            if (!(e.flags & PK_EMPTY)) {
-                k = ld_cg_u4(&slot->key);
-                v = __ldcg(&slot->val);
+    const bool special = active && (e.flags & PK_SPECIAL);
+    const bool probing = active && !(e.flags & (PK_SPECIAL | PK_OLD));
+    Slot16 *slot = &P.slots[e.slot];
+    // ---- look at the slot (skipped when the first probe already saw it empty)
+    uint4 k = empty;
+    u64 v = VAL_EMPTY;
+    if (probing && !(e.flags & PK_EMPTY)) {
+        k = ld_cg_u4(&slot->key);
+        v = __ldcg(&slot->val);
+    }
+    if (special) v = *(volatile u64 *)&P.counters[CTR_SPECIAL];
+    // ---- lanes that will try to claim reserve their claim index first (ballot, no atomics)
+    const bool attempt = (probing && key_is_empty(k)) || (special && v == VAL_EMPTY);
+    const uint32_t ma = __ballot_sync(0xFFFFFFFFu, attempt);
+    const uint32_t n_att = __popc(ma);
+    // indices come from the warp's current chunk; when it runs out mid-round the tail of the
+    // round continues in a freshly reserved chunk (nothing is abandoned)
+    const uint32_t rem = (uint32_t)(st.chunk_end - st.chunk_next);
+    u64 fresh_chunk = 0;
+    if (n_att > rem) {
+        if (lane == 0) fresh_chunk = atomicAdd(&P.counters[CTR_CLAIMED], (u64)CLAIM_CHUNK);
+        fresh_chunk = __shfl_sync(0xFFFFFFFFu, fresh_chunk, 0);
+    }
+    const uint32_t my_rank = __popc(ma & lt);
+    const u64 my_idx = my_rank < rem ? st.chunk_next + my_rank : fresh_chunk + (my_rank - rem);
+    if (n_att > rem) {
+        st.chunk_next = fresh_chunk + (n_att - rem);
+        st.chunk_end = fresh_chunk + CLAIM_CHUNK;
+    } else {
+        st.chunk_next += n_att;
+    }
+    bool again = false, fresh = false, settled_here = false;
+    if (attempt) {
+        if (my_idx >= P.claim_cap) {  // claim arrays exhausted: the host regrows and redoes the level
+            atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+        } else if (special) {
+            const u64 old = atomicCAS(&P.counters[CTR_SPECIAL], VAL_EMPTY, P.epoch | my_idx);
+            if (old == VAL_EMPTY) {
+                P.claim_key[my_idx] = empty;
+                atomicMin(&P.claim_ord[my_idx], e.ord);
+                fresh = settled_here = true;
+            } else {
+                v = old;
             }
-            if (key_is_empty(k)) {
-                k = cas128(&slot->key, empty, e.key);
-                if (key_is_empty(k)) {
-                    claimed = true;
-                    k = e.key;
-                }
-                v = VAL_EMPTY;  // whoever claimed it this instant, the val is at best this level's
-            }
-            if (v_eq(k, e.key)) {
-                if (v > val) atomicMin(&slot->val, val);
-                fresh = v >= LEVEL_FLAG;
-            } else {  // another CM lives here: linear probing
-                again = true;
-                e.slot = (e.slot + 1) & (uint32_t)P.slot_mask;
-                e.flags &= ~PK_EMPTY;
+        } else {
+            const uint4 old = cas128(&slot->key, empty, e.key);
+            if (key_is_empty(old)) {  // claimed: publish the claim index, record key and ordinal
+                __stcg(&slot->val, P.epoch | my_idx);
+                P.claim_key[my_idx] = e.key;
+                atomicMin(&P.claim_ord[my_idx], e.ord);
+                fresh = settled_here = true;
+            } else {
+                k = old;
+                v = VAL_EMPTY;  // whoever claimed it: their val may not be visible yet, look again next round
             }
         }
-        if (!again && (e.flags & PK_SEP)) {
-            if (fresh) atomicMin(&P.counters[CTR_SEP], e.ord);
-            if (P.sep_list) {  // exhaustive runs keep every separating ordinal (chunk-exact separator id)
-                const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
-                if (pos < P.sep_list_cap) P.sep_list[pos] = e.ord;
-            }
+    }
+    if ((probing || special) && !settled_here) {
+        if (special || v_eq(k, e.key)) {
+            if (v == VAL_EMPTY) {  // key is there, claim index not published yet
+                again = true;
+                e.flags &= ~PK_EMPTY;
+            } else if (v >= P.epoch) {  // built earlier in this level: keep the smaller ordinal
+                const u64 idx = v & CLAIM_IDX_MASK;
+                if (__ldcg(&P.claim_ord[idx]) > e.ord) atomicMin(&P.claim_ord[idx], e.ord);
+                fresh = true;
+            }  // else: stored by an earlier level
+        } else {  // another CM lives here: linear probing
+            again = true;
+            e.slot = (e.slot + 1) & (uint32_t)P.slot_mask;
+            e.flags &= ~PK_EMPTY;
+        }
+    }
+    if (active && !again && (e.flags & PK_SEP)) {
+        if (fresh) atomicMin(&P.counters[CTR_SEP], e.ord);
+        if (P.sep_list) {  // exhaustive runs keep every separating ordinal (chunk-exact separator id)
+            const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+            if (pos < P.sep_list_cap) P.sep_list[pos] = e.ord;
         }
     }
     const uint32_t mq = __ballot_sync(0xFFFFFFFFu, again);
     if (again) ws.queue[base + __popc(mq & lt)] = e;
     st.qfill = base + __popc(mq);
-    const uint32_t mc = __ballot_sync(0xFFFFFFFFu, claimed);
-    if (claimed) ws.claims[st.cfill + __popc(mc & lt)] = (e.flags & PK_SPECIAL) ? SLOT_SPECIAL : e.slot;
-    st.cfill += __popc(mc);
     __syncwarp();
-    if (st.cfill >= 32u) claims_flush(P, ws, st, false);
 }
 
 // Probe PROBE_BATCH candidates of one lane with ONE sector read each (all issued before
@@ -242,7 +264,7 @@ template <int LW, typename OrdOf>
 __device__ __forceinline__ void insert_batch(const NarrowParams &P, WarpShared &ws, WarpState &st,
                                              const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
                                              const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
-    constexpr uint32_t FLAG_HI = (uint32_t)(LEVEL_FLAG >> 32);
+    const uint32_t epoch_hi = (uint32_t)(P.epoch >> 32);  // vals of earlier levels have a smaller high word
     const uint32_t mask32 = (uint32_t)P.slot_mask;
     const uint32_t lt = lanemask_lt();
     uint32_t slot[PROBE_BATCH];
@@ -266,7 +288,7 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, WarpShared &
             flags |= PK_SPECIAL;
         } else if (live[r]) {
             if (v_eq(k0[r], cand[r])) {
-                if (vhi[r] < FLAG_HI) flags |= PK_OLD;  // duplicate of an earlier level: settled
+                if (vhi[r] < epoch_hi) flags |= PK_OLD;  // duplicate of an earlier level: settled
             } else if (key_is_empty(k0[r])) {
                 flags |= PK_EMPTY;
             } else {
@@ -428,7 +450,6 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_ke
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
         while (st.qfill > 0u) drain_round(P, ws, st);
-    claims_flush(P, ws, st, true);
 }
 
 // ---- finalisation: order the level's winners by ordinal without a sort -------------
@@ -437,25 +458,20 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_ke
 // level (reference order = ordinal order), and the rows are scattered straight to it.
 
 struct FinalizeParams {
-    Slot16 *slots;
-    const uint32_t *new_list;
-    u64 n_claimed;
-    u64 *counters;
+    const uint4 *claim_key;
+    const u64 *claim_ord;
+    u64 n_claimed;  // claim indices reserved (some unused: ord = all ones)
     uint32_t *bitmap;         // one bit per ordinal
     const uint32_t *sb_rank;  // exclusive popcount prefix per 32-word superblock
-    u64 ord_limit;            // keep ordinals <= limit (separator in a non-exhaustive run, else all ones)
+    u64 ord_limit;            // keep ordinals <= limit (separator in a non-exhaustive run, else all ones - 1)
     uint4 *store;
     u64 *ords;
     u64 base;  // global id of the level's first entry
 };
 
-__device__ __forceinline__ u64 claimed_val(const FinalizeParams &F, uint32_t slot) {
-    return slot == SLOT_SPECIAL ? F.counters[CTR_SPECIAL] : F.slots[slot].val;
-}
-
 __global__ void __launch_bounds__(256) narrow_mark_kernel(const FinalizeParams F) {
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < F.n_claimed; t += (u64)gridDim.x * blockDim.x) {
-        const u64 ord = claimed_val(F, F.new_list[t]) & ~LEVEL_FLAG;
+        const u64 ord = F.claim_ord[t];
         if (ord <= F.ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
     }
 }
@@ -469,14 +485,11 @@ __device__ __forceinline__ u64 ordinal_rank(const uint32_t *bitmap, const uint32
 
 __global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParams F) {
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < F.n_claimed; t += (u64)gridDim.x * blockDim.x) {
-        const uint32_t slot = F.new_list[t];
-        const u64 ord = claimed_val(F, slot) & ~LEVEL_FLAG;
-        if (ord > F.ord_limit) continue;  // ordered after the separator: not part of the level
+        const u64 ord = F.claim_ord[t];
+        if (ord > F.ord_limit) continue;  // unused index, or ordered after the separator
         const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
-        F.store[gid] = slot == SLOT_SPECIAL ? make_uint4(~0u, ~0u, ~0u, ~0u) : F.slots[slot].key;
+        F.store[gid] = F.claim_key[t];
         F.ords[gid] = ord;
-        if (slot == SLOT_SPECIAL) F.counters[CTR_SPECIAL] = gid;
-        else F.slots[slot].val = gid;
     }
 }
 
@@ -512,13 +525,13 @@ __device__ __forceinline__ uint32_t key_owner(uint4 key, uint32_t owners) {
 
 // counts[o] += claims of this level owned by rank o; with `cursors`, also writes the records
 // grouped by owner (cursors[o] = next free position of owner o's range)
-__global__ void __launch_bounds__(256) narrow_export_kernel(const Slot16 *slots, const uint32_t *new_list, u64 n_claimed,
-                                                            const u64 *counters, uint32_t owners, u64 *counts,
-                                                            u64 *cursors, uint4 *keys_out, u64 *ords_out) {
+__global__ void __launch_bounds__(256) narrow_export_kernel(const uint4 *claim_key, const u64 *claim_ord, u64 n_claimed,
+                                                            uint32_t owners, u64 *counts, u64 *cursors, uint4 *keys_out,
+                                                            u64 *ords_out) {
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
-        const uint32_t slot = new_list[t];
-        const uint4 key = slot == SLOT_SPECIAL ? make_uint4(~0u, ~0u, ~0u, ~0u) : slots[slot].key;
-        const u64 ord = (slot == SLOT_SPECIAL ? counters[CTR_SPECIAL] : slots[slot].val) & ~LEVEL_FLAG;
+        const u64 ord = claim_ord[t];
+        if (ord == VAL_EMPTY) continue;  // reserved but never used
+        const uint4 key = claim_key[t];
         const uint32_t o = key_owner(key, owners);
         if (cursors) {
             const u64 pos = atomicAdd(&cursors[o], 1ull);
@@ -530,40 +543,57 @@ __global__ void __launch_bounds__(256) narrow_export_kernel(const Slot16 *slots,
     }
 }
 
-// insert-or-min received records into the local set; newly claimed slots join the level's claim list
-__global__ void __launch_bounds__(256) narrow_import_kernel(Slot16 *slots, u64 slot_mask, u64 *counters, uint32_t *new_list,
-                                                            u64 new_list_cap, const uint4 *keys, const u64 *ords, u64 n) {
+// insert-or-min received records into the local set; new CMs get a claim index of their own
+__global__ void __launch_bounds__(256) narrow_import_kernel(const NarrowParams P, const uint4 *keys, const u64 *ords, u64 n) {
     const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (u64)gridDim.x * blockDim.x) {
         const uint4 key = keys[t];
-        const u64 val = LEVEL_FLAG | ords[t];
-        bool claimed = false;
-        uint32_t where = SLOT_SPECIAL;
-        if (key_is_empty(key)) {
-            claimed = atomicMin(&counters[CTR_SPECIAL], val) == VAL_EMPTY;
+        const u64 ord = ords[t];
+        u64 *val_at = nullptr;
+        bool claimed = false, overflow = false;
+        u64 my_idx = 0;
+        if (key_is_empty(key)) {  // the all-ones CM has a register instead of a slot
+            val_at = &P.counters[CTR_SPECIAL];
+            if (*(volatile u64 *)val_at == VAL_EMPTY) {
+                my_idx = atomicAdd(&P.counters[CTR_CLAIMED], 1ull);
+                if (my_idx >= P.claim_cap) overflow = true;
+                else claimed = atomicCAS(val_at, VAL_EMPTY, P.epoch | my_idx) == VAL_EMPTY;
+            }
         } else {
-            u64 slot = hash_vec(key, 0u) & slot_mask;
+            u64 slot = hash_vec(key, 0u) & P.slot_mask;
             for (;;) {
-                uint4 k = ld_cg_u4(&slots[slot].key);
+                uint4 k = ld_cg_u4(&P.slots[slot].key);
                 if (key_is_empty(k)) {
-                    k = cas128(&slots[slot].key, empty, key);
+                    my_idx = atomicAdd(&P.counters[CTR_CLAIMED], 1ull);  // stays unused if the CAS below loses
+                    if (my_idx >= P.claim_cap) {
+                        overflow = true;
+                        break;
+                    }
+                    k = cas128(&P.slots[slot].key, empty, key);
                     if (key_is_empty(k)) {
                         claimed = true;
+                        __stcg(&P.slots[slot].val, P.epoch | my_idx);
                         k = key;
                     }
                 }
                 if (v_eq(k, key)) {
-                    atomicMin(&slots[slot].val, val);
-                    where = (uint32_t)slot;
+                    val_at = &P.slots[slot].val;
                     break;
                 }
-                slot = (slot + 1) & slot_mask;
+                slot = (slot + 1) & P.slot_mask;
             }
         }
+        if (overflow) {
+            atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+            continue;
+        }
         if (claimed) {
-            const u64 pos = atomicAdd(&counters[CTR_CLAIMED], 1ull);
-            if (pos < new_list_cap) new_list[pos] = where;
-            else atomicExch(&counters[CTR_OVERFLOW], 1ull);
+            P.claim_key[my_idx] = key;
+            atomicMin(&P.claim_ord[my_idx], ord);
+        } else {
+            u64 v;
+            while ((v = *(volatile u64 *)val_at) == VAL_EMPTY) {}  // a claimer publishes right after its CAS
+            if (v >= P.epoch) atomicMin(&P.claim_ord[v & CLAIM_IDX_MASK], ord);
         }
     }
 }
