@@ -49,6 +49,9 @@ typedef struct {
     int64_t total, rows_cap;
     level_t *levels;
     int n_levels, levels_cap;
+    int64_t dup_hist[64]; /* analysis only: candidates of the last level by the cost level of the entry they
+                             duplicate ([0] = new CM, [c] = duplicate of a CM stored at cost c) */
+    int64_t last_match;   /* id matched by the last seen_add that returned 0 */
     /* seen set (engine.py:130): open addressing over row ids, keyed by the row bytes */
     int64_t *slots; /* id+1, 0 = empty */
     int64_t n_slots;
@@ -158,7 +161,10 @@ static int seen_add(oracle_t *o, const uint8_t *row) {
     int64_t s = (int64_t)(h & (uint64_t)(o->n_slots - 1));
     while (o->slots[s]) {
         int64_t id = o->slots[s] - 1;
-        if (memcmp(o->rows + (size_t)id * o->row_bytes, row, (size_t)o->row_bytes) == 0) return 0;
+        if (memcmp(o->rows + (size_t)id * o->row_bytes, row, (size_t)o->row_bytes) == 0) {
+            o->last_match = id;
+            return 0;
+        }
         s = (s + 1) & (o->n_slots - 1);
     }
     if (o->total == o->rows_cap) {
@@ -330,6 +336,16 @@ static void do_chunk(run_t *r, const chunk_t *c) {
         pack_row(o, res, o->packed);
         int fresh = seen_add(o, o->packed); /* engine.py:333,421-424 */
         if (fresh) {
+            o->dup_hist[0]++;
+        } else { /* analysis only: which cost level holds the duplicated entry */
+            int cost_of = o->n_levels + 1; /* the level being built */
+            if (o->last_match < r->lv.base) {
+                cost_of = o->n_levels;
+                while (cost_of > 1 && o->last_match < o->levels[cost_of - 1].base) cost_of--;
+            }
+            if (cost_of < 64) o->dup_hist[cost_of]++;
+        }
+        if (fresh) {
             lv_push(r, c->tag, left, right); /* engine.py:434-441 */
             fresh_in_chunk++;
             fresh_bytes_rows += o->row_bytes;
@@ -366,6 +382,7 @@ int orc_expand_level(oracle_t *o, int cost, unsigned op_mask, int exhaustive, in
                      int64_t mem_limit_bytes, double deadline_s, int64_t *n_new, int64_t *sep_gid,
                      int64_t *constructed_delta) {
     if (!o || cost != o->n_levels + 1 || batch < 1) return ST_BAD;
+    memset(o->dup_hist, 0, sizeof(o->dup_hist));
     run_t r;
     memset(&r, 0, sizeof(r));
     r.o = o;
@@ -479,6 +496,8 @@ double orc_now(void) { return now_s(); }
 int64_t orc_total(const oracle_t *o) { return o->total; }
 int64_t orc_approx_bytes(const oracle_t *o) { return o->approx_bytes; }
 int orc_num_levels(const oracle_t *o) { return o->n_levels; }
+/* analysis only (tools/dup_profile.py): duplicate histogram of the most recently expanded level */
+void orc_dup_hist(const oracle_t *o, int64_t *out64) { memcpy(out64, o->dup_hist, sizeof(o->dup_hist)); }
 int orc_row_bytes(const oracle_t *o) { return o->row_bytes; }
 
 int orc_level_info(const oracle_t *o, int cost, int64_t *n, int64_t *base) {

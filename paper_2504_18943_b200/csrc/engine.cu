@@ -28,6 +28,7 @@
 
 #include "../../include/ltlsynth_b200.h"
 #include "narrow.cuh"
+#include "narrow_part.cuh"
 #include "wide.cuh"
 
 namespace ltlb200 {
@@ -300,6 +301,25 @@ private:
     DeviceArray<u64> sep_list_;
     DeviceArray<uint8_t> misc_;
     DeviceArray<u64> xchg_;  // per-owner counts and cursors of the claim exchange
+    // partitioned path (narrow_part.cuh): record pool, chunk metadata, counters
+    DeviceArray<uint4> pool_keys_;
+    DeviceArray<u64> pool_ords_;
+    DeviceArray<uint8_t> chunk_meta_;   // [0, cap/2) bucket of each chunk, [cap/2, cap) its fill
+    DeviceArray<uint32_t> chunk_order_; // chunk ids grouped by bucket
+    DeviceArray<u64> wstate_;           // open chunks + chunk-id stash of every warp slot, carried across operator launches
+    DeviceArray<u64> pc_;
+    // hot set (narrow path): bare keys of the low cost levels, small enough to stay L2 resident
+    DeviceArray<uint4> hot_;
+    u64 hot_slots_ = 0, hot_entries_ = 0;
+    int hot_levels_ = 0;       // levels 1..hot_levels_ are in the hot set
+    bool hot_closed_ = false;  // the next level no longer fits: the hot set stays as it is
+    static u64 hot_max_bytes();
+    void update_hot();
+    int part_occupancy_ = 2;
+    bool store_has_separator_ = false;  // some stored CM separates: a separating candidate need not be fresh
+    static bool partition_enabled();
+    bool use_partition(u64 constructed) const;
+    void launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles);
     struct PendingLevel {
         LevelMeta lv;
         u64 constructed = 0, n_claimed = 0, sep_ord = ~0ull, n_seps = 0, claim_cap = 0;
@@ -310,6 +330,7 @@ private:
     WideParams wide_params(bool exhaustive) const;
     NarrowParams narrow_params(bool exhaustive) const;
     static constexpr u64 kMinSlots = 1ull << 16;
+    static constexpr int kPoolOverflowWord = 32;  // pinned staging word beside the CTR_* read-back
     u64 *d_counters_ = nullptr;
     BlockDesc *d_blocks_ = nullptr;
     static constexpr int kMaxBlocks = 512;
@@ -414,6 +435,9 @@ void Engine::reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems) {
 }
 
 template <int LW>
+static int part_occupancy_of();
+
+template <int LW>
 static int occupancy_of() {
     int occ = 0, best = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, OP_UNTIL>, CTA_THREADS, 0) == cudaSuccess)
@@ -485,6 +509,7 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_rows / init leave scope
     occupancy_ = wide_ ? 4 : (lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>());
+    if (!wide_) part_occupancy_ = lw_ == 8 ? part_occupancy_of<8>() : lw_ == 16 ? part_occupancy_of<16>() : lw_ == 32 ? part_occupancy_of<32>() : part_occupancy_of<64>();
     rebuild_table(kMinSlots);
     st_.row_bytes = row_bytes_;
     st_.key_bytes = 16 * nvec_;
@@ -508,6 +533,13 @@ Engine::~Engine() {
     release(sep_list_);
     release(misc_);
     release(xchg_);
+    release(hot_);
+    release(pool_keys_);
+    release(pool_ords_);
+    release(chunk_meta_);
+    release(chunk_order_);
+    release(wstate_);
+    release(pc_);
     recycle_retired(true);
     pinned_put(h_counters_);
     for (auto &e : ev_)
@@ -561,7 +593,11 @@ void Engine::reset() {
     total_ = 0;
     approx_bytes_ = 0;
     last_constructed_ = 0;
-    rebuild_table(table_slots());
+    store_has_separator_ = false;
+    hot_slots_ = hot_entries_ = 0;
+    hot_levels_ = 0;
+    hot_closed_ = false;
+    rebuild_table(kMinSlots);  // small levels probe an L2-resident set again; it regrows with the search
     st_.constructed = 0;
     st_.unique = 0;
 }
@@ -839,6 +875,231 @@ void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
     });
 }
 
+// ---- hot set ----------------------------------------------------------------------------------
+
+// LTLB200_HOT_MB: size cap of the hot set in MiB (0 disables it); default 64 of the 126 MB L2.
+u64 Engine::hot_max_bytes() {
+    static const u64 bytes = [] {
+        const char *env = getenv("LTLB200_HOT_MB");
+        return (env ? strtoull(env, nullptr, 10) : 64ull) << 20;
+    }();
+    return bytes;
+}
+
+// After a level is appended: add it to the hot set while everything stored so far fits at a load
+// factor <= 1/2 under the size cap; the first level that does not fit closes the set.
+void Engine::update_hot() {
+    if (hot_closed_ || hot_max_bytes() == 0) return;
+    const int newest = (int)levels_.size();
+    if (hot_levels_ != newest - 1) return;  // (a level was skipped: budget outcome)
+    const LevelMeta &lv = levels_.back();
+    const u64 entries = lv.base + lv.n;
+    const u64 want = std::max<u64>(next_pow2(2 * entries), 1ull << 12);
+    if (want * sizeof(uint4) > hot_max_bytes()) {
+        hot_closed_ = true;
+        return;
+    }
+    u64 first = lv.base, count = lv.n;
+    if (want > hot_slots_) {  // regrow: re-insert every level
+        const u64 slots = std::min<u64>(want * 4, hot_max_bytes() / sizeof(uint4));
+        reserve(hot_, slots, false);
+        hot_slots_ = next_pow2(slots) > slots ? next_pow2(slots) / 2 : slots;
+        CUDA_CHECK(cudaMemsetAsync(hot_.ptr, 0xFF, hot_slots_ * sizeof(uint4), stream_));
+        first = 0;
+        count = entries;
+    }
+    if (count) {
+        const int grid = (int)std::min<u64>((count + 255) / 256, (u64)sm_count_ * 16);
+        hot_insert_kernel<<<grid, 256, 0, stream_>>>(hot_.ptr, (uint32_t)(hot_slots_ - 1), store_.ptr, first, count);
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+    }
+    hot_levels_ = newest;
+    hot_entries_ = entries;
+}
+
+// ---- partitioned path (narrow_part.cuh) ------------------------------------------------------
+
+constexpr size_t kPartSmem = sizeof(WarpSharedPart) * WARPS_PER_CTA;
+
+template <int LW, int OP>
+static void launch_part_instance(const NarrowParams &P, const PartParams &Q, int grid, cudaStream_t st) {
+    static std::once_flag once;  // opt in to > 48 KB of dynamic shared memory, once per instance
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(narrow_partition_kernel<LW, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem);
+    });
+    narrow_partition_kernel<LW, OP><<<grid, CTA_THREADS, kPartSmem, st>>>(P, Q);
+}
+
+template <int LW>
+static void launch_part_op(int op, const NarrowParams &P, const PartParams &Q, int grid, cudaStream_t st) {
+    switch (op) {
+        case OP_ATOM: launch_part_instance<LW, OP_ATOM>(P, Q, grid, st); break;
+        case OP_NOT: launch_part_instance<LW, OP_NOT>(P, Q, grid, st); break;
+        case OP_NEXT: launch_part_instance<LW, OP_NEXT>(P, Q, grid, st); break;
+        case OP_FUTURE: launch_part_instance<LW, OP_FUTURE>(P, Q, grid, st); break;
+        case OP_AND: launch_part_instance<LW, OP_AND>(P, Q, grid, st); break;
+        case OP_UNTIL: launch_part_instance<LW, OP_UNTIL>(P, Q, grid, st); break;
+        default: launch_part_instance<LW, OP_OR>(P, Q, grid, st); break;
+    }
+}
+
+template <int LW>
+static int part_occupancy_of() {
+    int occ = 0;
+    cudaFuncSetAttribute(narrow_partition_kernel<LW, OP_UNTIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_partition_kernel<LW, OP_UNTIL>, CTA_THREADS, kPartSmem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    return std::max(occ, 1);
+}
+
+// LTLB200_PARTITION=0 forces the direct path, =1 forces the partitioned path for every level
+// (tests), unset = by size.
+bool Engine::partition_enabled() {
+    static const char *env = getenv("LTLB200_PARTITION");
+    return !(env && env[0] == '0');
+}
+
+bool Engine::use_partition(u64 constructed) const {
+    if (wide_ || !partition_enabled()) return false;
+    static const char *env = getenv("LTLB200_PARTITION");
+    if (env && env[0] == '1') return true;
+    // worth it once the set no longer fits the L2 and the level amortises the extra launches
+    return slots_.cap * sizeof(Slot16) > (96ull << 20) && constructed >= (1ull << 21);
+}
+
+// Phase A per operator (records into bucket chunks), chunk ordering, phase B (bucket by bucket
+// probing), over segments of the level's tile space so that the record pool stays bounded.
+void Engine::launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles) {
+    const u64 kSegCandidates = 1ull << 28;  // records per segment (6 GiB of pool)
+    // segment ends in the level's flattened tile space, each segment bounded by kSegCandidates
+    std::vector<u64> seg_end, seg_records;
+    {
+        u64 acc = 0;
+        for (const BlockDesc &b : lv.blocks) {
+            const u64 per_tile = (u64)TILE_V * b.tile_s * (b.kind == BK_UNARY ? 1 : b.vg);
+            u64 t = b.tile0;
+            const u64 t_end = b.tile0 + b.tiles_v * b.tiles_s;
+            while (t < t_end) {
+                const u64 fit = (kSegCandidates - acc) / per_tile;
+                if (fit == 0) {
+                    seg_end.push_back(t);
+                    seg_records.push_back(acc);
+                    acc = 0;
+                    continue;
+                }
+                const u64 take = std::min(fit, t_end - t);
+                t += take;
+                acc += take * per_tile;
+            }
+        }
+        seg_end.push_back(n_tiles);
+        seg_records.push_back(acc);
+    }
+    const u64 warps = (u64)sm_count_ * part_occupancy_ * WARPS_PER_CTA;
+    int bucket_shift = 0;
+    while ((slots_.cap >> bucket_shift) > (u64)PART_NB) ++bucket_shift;
+    reserve(pc_, PC_COUNT, false);
+    u64 h_pc[PC_COUNT];
+    for (auto &c : h_pc) c = 0;
+    h_pc[PC_SEPBOUND] = VAL_EMPTY;
+    CUDA_CHECK(cudaMemcpyAsync(pc_.ptr, h_pc, sizeof(h_pc), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_pc leaves scope; also the last level's pool is idle now
+    for (size_t seg = 0; seg < seg_end.size(); ++seg) {
+        const u64 s0 = seg ? seg_end[seg - 1] : 0, s1 = seg_end[seg];
+        if (s0 == s1) continue;
+        // operator groups of the level that overlap the segment
+        struct Group { size_t b0, b1; u64 t0, t1; int index; };
+        std::vector<Group> groups;
+        {
+            size_t b0 = 0;
+            int index = 0;
+            while (b0 < lv.blocks.size()) {
+                size_t b1 = b0;
+                while (b1 < lv.blocks.size() && lv.blocks[b1].op == lv.blocks[b0].op) ++b1;
+                const BlockDesc &last = lv.blocks[b1 - 1];
+                const u64 t0 = std::max(lv.blocks[b0].tile0, s0), t1 = std::min(last.tile0 + last.tiles_v * last.tiles_s, s1);
+                if (t0 < t1) groups.push_back({b0, b1, t0, t1, index});
+                b0 = b1;
+                ++index;
+            }
+        }
+        const u64 records_max = std::min(constructed, seg_records[seg]);
+        // full chunks + one open chunk per (warp, bucket) + ids abandoned at stash refills / left in the last stash
+        u64 pool_chunks = records_max / PART_CHUNK + records_max / (PART_CHUNK * 8) + warps * (PART_NB + PART_STASH) + 1024;
+        if (pool_chunks * PART_CHUNK >= (1ull << 32)) throw std::invalid_argument("record pool exceeds 2^32 records");
+        reserve(pool_keys_, pool_chunks * PART_CHUNK, false);
+        reserve(pool_ords_, pool_chunks * PART_CHUNK, false);
+        reserve(chunk_meta_, 2 * pool_chunks, false);
+        reserve(chunk_order_, pool_chunks, false);
+        reserve(wstate_, warps * PART_WSTATE, false);
+        PartParams Q{};
+        Q.pool_keys = pool_keys_.ptr;
+        Q.pool_ords = pool_ords_.ptr;
+        Q.chunk_bucket = chunk_meta_.ptr;
+        Q.chunk_fill = chunk_meta_.ptr + pool_chunks;
+        Q.order = chunk_order_.ptr;
+        Q.wstate = wstate_.ptr;
+        Q.wstate_slots = warps;
+        Q.pool_chunks = pool_chunks;
+        Q.pc = pc_.ptr;
+        Q.bucket_shift = bucket_shift;
+        Q.sep_bound_ok = (P.prune_after_sep && !store_has_separator_) ? 1 : 0;
+        CUDA_CHECK(cudaMemsetAsync(Q.chunk_bucket, 0xFF, pool_chunks, stream_));
+        CUDA_CHECK(cudaMemsetAsync(Q.chunk_fill, PART_CHUNK, pool_chunks, stream_));
+        CUDA_CHECK(cudaMemsetAsync(wstate_.ptr, 0, warps * PART_WSTATE * sizeof(u64), stream_));
+        if (s0 > 0) {  // later segments: everything but the pruning bound starts over, tile tickets too
+            CUDA_CHECK(cudaMemsetAsync(pc_.ptr, 0, PC_SEPBOUND * sizeof(u64), stream_));
+            CUDA_CHECK(cudaMemsetAsync(pc_.ptr + PC_TICKET, 0, (PC_COUNT - PC_TICKET) * sizeof(u64), stream_));
+            CUDA_CHECK(cudaMemsetAsync(d_counters_ + CTR_TICKET0, 0, (CTR_COUNT - CTR_TICKET0) * sizeof(u64), stream_));
+        }
+        for (const Group &g : groups) {
+            P.block_begin = (int)g.b0;
+            P.block_end = (int)g.b1;
+            P.tile_begin = g.t0;
+            P.tile_end = g.t1;
+            P.ticket = CTR_TICKET0 + g.index;
+            const int grid = (int)std::min<u64>((g.t1 - g.t0 + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * part_occupancy_);
+            const int op = (int)lv.blocks[g.b0].op;
+            DBG("partition op=%d tiles=[%llu,%llu) grid=%d", op, (unsigned long long)g.t0, (unsigned long long)g.t1, grid);
+            switch (lw_) {
+                case 8: launch_part_op<8>(op, P, Q, grid, stream_); break;
+                case 16: launch_part_op<16>(op, P, Q, grid, stream_); break;
+                case 32: launch_part_op<32>(op, P, Q, grid, stream_); break;
+                default: launch_part_op<64>(op, P, Q, grid, stream_); break;
+            }
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+            st_.enumerate_launches++;
+        }
+        part_seal_kernel<<<sm_count_ * 4, 256, 0, stream_>>>(Q);
+        CUDA_CHECK(cudaGetLastError());
+        part_order_kernel<<<(unsigned)((pool_chunks + PART_ORDER_PER_BLOCK - 1) / PART_ORDER_PER_BLOCK), 256, 0, stream_>>>(Q);
+        CUDA_CHECK(cudaGetLastError());
+        const int pgrid = sm_count_ * LTLB200_PROBE_MIN_CTAS;
+        switch (lw_) {
+            case 8: narrow_probe_kernel<8><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
+            case 16: narrow_probe_kernel<16><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
+            case 32: narrow_probe_kernel<32><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
+            default: narrow_probe_kernel<64><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
+        }
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches += 3;
+        st_.enumerate_launches += 3;
+        if (debug_on()) {
+            CUDA_CHECK(cudaStreamSynchronize(stream_));
+            u64 pcs[PC_COUNT];
+            CUDA_CHECK(cudaMemcpy(pcs, pc_.ptr, sizeof(pcs), cudaMemcpyDeviceToHost));
+            DBG("segment [%llu,%llu): pool chunks drawn=%llu ordered=%llu overflow=%llu sepbound=%llx", (unsigned long long)s0, (unsigned long long)s1, (unsigned long long)pcs[PC_POOL], (unsigned long long)pcs[PC_ORDERED], (unsigned long long)pcs[PC_OVERFLOW], (unsigned long long)pcs[PC_SEPBOUND]);
+        }
+    }
+    // a pool overflow cannot happen by construction of pool_chunks; level_begin checks the flag
+    // after its counter read-back and fails loudly if it ever does
+    CUDA_CHECK(cudaMemcpyAsync(h_counters_ + kPoolOverflowWord, pc_.ptr + PC_OVERFLOW, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+}
+
 // ---- one level = begin (enumerate this rank's shard) [+ exchange] + end (finalise) ---------
 
 // Enumerates the tiles of level `cost` that belong to shard `shard_index` of `shard_count`
@@ -891,7 +1152,9 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             const u64 claim_cap = est + (wide_ ? wide_slack : narrow_slack);
             const u64 want_slots = next_pow2(2 * (total_ + claim_cap));
             DBG("level %d attempt %d: constructed=%llu est=%llu claim_cap=%llu slots=%llu want=%llu", cost, attempt, (unsigned long long)constructed, (unsigned long long)est, (unsigned long long)claim_cap, (unsigned long long)table_slots(), (unsigned long long)want_slots);
-            if (want_slots > table_slots()) rebuild_table(2 * want_slots);  // regrow in 4x steps: every other level at most
+            // regrow in 4x steps (every other level at most) while the set is small; a big set is sized
+            // exactly: clearing and streaming gigabytes of empty slots costs more than regrowing again
+            if (want_slots > table_slots()) rebuild_table(want_slots * sizeof(Slot16) >= (1ull << 30) ? want_slots : 2 * want_slots);
             if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
             u64 init[CTR_COUNT];
             for (auto &c : init) c = 0;
@@ -918,10 +1181,13 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
                 P.shard_stride = (u64)shard_count;
                 P.shard_offset = (u64)shard_index;
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
-                launch_enumerate(P, lv);
+                if (use_partition(constructed)) launch_partitioned(P, lv, constructed, n_tiles);
+                else launch_enumerate(P, lv);
             }
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+            h_counters_[kPoolOverflowWord] = 0;
             read_counters();
+            if (h_counters_[kPoolOverflowWord]) throw CudaError("record pool overflow in the partitioned path");
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
             st_.enumerate_ms += ms;
@@ -941,6 +1207,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     DBG("level %d enumerated: claimed=%llu sep=%llx", cost, (unsigned long long)h_counters_[CTR_CLAIMED], (unsigned long long)h_counters_[CTR_SEP]);
     pl.n_claimed = h_counters_[CTR_CLAIMED];  // narrow: claimed slots; wide: reserved staging entries
     pl.sep_ord = h_counters_[CTR_SEP];
+    if (pl.sep_ord != VAL_EMPTY || h_counters_[CTR_SEPCOUNT]) store_has_separator_ = true;
     pl.n_seps = std::min<u64>(h_counters_[CTR_SEPCOUNT], sep_list_.cap);
     pl.seps_overflow = h_counters_[CTR_SEPCOUNT] > sep_list_.cap;
     *n_claimed_out = pl.n_claimed;
@@ -955,6 +1222,8 @@ NarrowParams Engine::narrow_params(bool exhaustive) const {
     P.atoms = d_atoms_;
     P.slots = slots_.ptr;
     P.slot_mask = slots_.cap - 1;
+    P.hot = hot_slots_ ? hot_.ptr : nullptr;
+    P.hot_mask = hot_slots_ ? (uint32_t)(hot_slots_ - 1) : 0u;
     P.claim_key = claim_key_.ptr;
     P.claim_ord = claim_ord_.ptr;
     P.claim_cap = pending_.claim_cap;
@@ -1004,6 +1273,7 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
                       int64_t *sep_gid, int64_t *constructed_delta) {
     if (!pending_.active) throw std::invalid_argument("level_end without level_begin");
     if (batch < 1) throw std::invalid_argument("batch_size must be >= 1");
+    if (sep_ord != VAL_EMPTY || n_seps) store_has_separator_ = true;  // found by another shard
     CUDA_CHECK(cudaSetDevice(device_));
     PendingLevel &pl = pending_;
     LevelMeta &lv = pl.lv;
@@ -1135,6 +1405,13 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
     st_.unique = total_;
     approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
     levels_.push_back(std::move(lv));
+    if (!wide_) {
+        try {
+            update_hot();
+        } catch (const MemoryBudget &) {  // no room for it: carry on without
+            hot_closed_ = true;
+        }
+    }
     if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
     return LTLB200_OK;
 }

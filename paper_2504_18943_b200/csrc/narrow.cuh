@@ -81,6 +81,8 @@ struct NarrowParams {
     const uint4 *atoms;
     Slot16 *slots;
     u64 slot_mask;
+    const uint4 *hot;   // hot set: keys of the low cost levels, 16-byte slots, read-only during a level (NULL = none)
+    uint32_t hot_mask;
     uint4 *claim_key;  // this level's new CMs by claim index
     u64 *claim_ord;    // smallest ordinal per claim index (all ones = index reserved but unused)
     u64 claim_cap;
@@ -126,6 +128,35 @@ __device__ __forceinline__ uint4 cas128(uint4 *addr, uint4 expect, uint4 desired
 
 __device__ __forceinline__ bool key_is_empty(uint4 k) { return (k.x & k.y & k.z & k.w) == 0xFFFFFFFFu; }
 
+// L2 residency control.  Probes of the multi-GB main set touch every sector once: they are
+// loaded evict-first (and never allocate in L1, so a slot changed by another SM is never read
+// stale), otherwise they flush the hot set out of the L2 -- measured: with default policies the
+// hot set ADDED 40 % DRAM traffic instead of removing two thirds of it.  Hot-set loads carry an
+// evict-last policy.
+__device__ __forceinline__ u64 l2_policy_evict_last() {
+    u64 p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint4 ld_hot(const uint4 *p, u64 policy) {
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(policy));
+    return v;
+}
+
+// one 32-byte slot = one sector = one 256-bit load: key and val are a consistent snapshot
+__device__ __forceinline__ void ld_slot(const Slot16 *p, uint4 &key, u64 &val) {
+    uint32_t v0, v1, pad0, pad1;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
+                 : "l"(p)
+                 : "memory");
+    val = (u64)v1 << 32 | v0;
+}
+
 // ---- per-warp state -------------------------------------------------------------------
 
 struct __align__(16) Parked {
@@ -157,15 +188,39 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// Lanes with `attempt` set reserve one claim index each (ballot ranks, no atomics); indices come
+// from the warp's current chunk, and when it runs out mid-way the tail continues in a freshly
+// reserved chunk (nothing is abandoned).  Warp-uniform control flow; every lane must call.
+__device__ __forceinline__ u64 reserve_claims(const NarrowParams &P, WarpState &st, bool attempt) {
+    const uint32_t ma = __ballot_sync(0xFFFFFFFFu, attempt);
+    const uint32_t n_att = __popc(ma);
+    if (n_att == 0u) return 0;
+    const uint32_t rem = (uint32_t)(st.chunk_end - st.chunk_next);
+    u64 fresh_chunk = 0;
+    if (n_att > rem) {
+        if ((threadIdx.x & 31) == 0) fresh_chunk = atomicAdd(&P.counters[CTR_CLAIMED], (u64)CLAIM_CHUNK);
+        fresh_chunk = __shfl_sync(0xFFFFFFFFu, fresh_chunk, 0);
+    }
+    const uint32_t my_rank = __popc(ma & lanemask_lt());
+    const u64 my_idx = my_rank < rem ? st.chunk_next + my_rank : fresh_chunk + (my_rank - rem);
+    if (n_att > rem) {
+        st.chunk_next = fresh_chunk + (n_att - rem);
+        st.chunk_end = fresh_chunk + CLAIM_CHUNK;
+    } else {
+        st.chunk_next += n_att;
+    }
+    return my_idx;
+}
+
 // One resolution round: the top (up to) 32 parked candidates take one probe step each.
 // Settled ones leave (recording separators), the rest are re-queued compacted.
-__device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &ws, WarpState &st) {
+__device__ __forceinline__ void drain_round(const NarrowParams &P, Parked *queue, WarpState &st) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = lanemask_lt();
     const uint32_t take = st.qfill < 32u ? st.qfill : 32u;
     const uint32_t base = st.qfill - take;
     const bool active = (uint32_t)lane < take;
-    Parked e = ws.queue[base + (active ? lane : 0)];
+    Parked e = queue[base + (active ? lane : 0)];
     __syncwarp();  // every lane holds its entry before the queue slots are reused
     const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
     const bool special = active && (e.flags & PK_SPECIAL);
@@ -174,31 +229,11 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &w
     // ---- look at the slot (skipped when the first probe already saw it empty)
     uint4 k = empty;
     u64 v = VAL_EMPTY;
-    if (probing && !(e.flags & PK_EMPTY)) {
-        k = ld_cg_u4(&slot->key);
-        v = __ldcg(&slot->val);
-    }
+    if (probing && !(e.flags & PK_EMPTY)) ld_slot(slot, k, v);
     if (special) v = *(volatile u64 *)&P.counters[CTR_SPECIAL];
-    // ---- lanes that will try to claim reserve their claim index first (ballot, no atomics)
+    // ---- lanes that will try to claim reserve their claim index first
     const bool attempt = (probing && key_is_empty(k)) || (special && v == VAL_EMPTY);
-    const uint32_t ma = __ballot_sync(0xFFFFFFFFu, attempt);
-    const uint32_t n_att = __popc(ma);
-    // indices come from the warp's current chunk; when it runs out mid-round the tail of the
-    // round continues in a freshly reserved chunk (nothing is abandoned)
-    const uint32_t rem = (uint32_t)(st.chunk_end - st.chunk_next);
-    u64 fresh_chunk = 0;
-    if (n_att > rem) {
-        if (lane == 0) fresh_chunk = atomicAdd(&P.counters[CTR_CLAIMED], (u64)CLAIM_CHUNK);
-        fresh_chunk = __shfl_sync(0xFFFFFFFFu, fresh_chunk, 0);
-    }
-    const uint32_t my_rank = __popc(ma & lt);
-    const u64 my_idx = my_rank < rem ? st.chunk_next + my_rank : fresh_chunk + (my_rank - rem);
-    if (n_att > rem) {
-        st.chunk_next = fresh_chunk + (n_att - rem);
-        st.chunk_end = fresh_chunk + CLAIM_CHUNK;
-    } else {
-        st.chunk_next += n_att;
-    }
+    const u64 my_idx = reserve_claims(P, st, attempt);
     bool again = false, fresh = false, settled_here = false;
     if (attempt) {
         if (my_idx >= P.claim_cap) {  // claim arrays exhausted: the host regrows and redoes the level
@@ -231,8 +266,7 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &w
                 again = true;
                 e.flags &= ~PK_EMPTY;
             } else if (v >= P.epoch) {  // built earlier in this level: keep the smaller ordinal
-                const u64 idx = v & CLAIM_IDX_MASK;
-                if (__ldcg(&P.claim_ord[idx]) > e.ord) atomicMin(&P.claim_ord[idx], e.ord);
+                atomicMin(&P.claim_ord[v & CLAIM_IDX_MASK], e.ord);
                 fresh = true;
             }  // else: stored by an earlier level
         } else {  // another CM lives here: linear probing
@@ -249,70 +283,156 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, WarpShared &w
         }
     }
     const uint32_t mq = __ballot_sync(0xFFFFFFFFu, again);
-    if (again) ws.queue[base + __popc(mq & lt)] = e;
+    if (again) queue[base + __popc(mq & lt)] = e;
     st.qfill = base + __popc(mq);
     __syncwarp();
 }
 
-// Probe PROBE_BATCH candidates of one lane with ONE sector read each (all issued before
-// any is consumed), settle the duplicates of earlier levels, park the rest.  Only the high
-// word of a slot's val is read: it alone tells "finalised at an earlier level" (< 2^62).
-// `known[r]`: the candidate equals one of its operands, i.e. a CM already in the cache --
-// a duplicate by construction, no probe.  `ord_of(r)` recomputes the ordinal for the
-// candidates that get parked, so ordinals hold no registers in the hot loop.
-template <int LW, typename OrdOf>
-__device__ __forceinline__ void insert_batch(const NarrowParams &P, WarpShared &ws, WarpState &st,
-                                             const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
-                                             const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
-    const uint32_t epoch_hi = (uint32_t)(P.epoch >> 32);  // vals of earlier levels have a smaller high word
-    const uint32_t mask32 = (uint32_t)P.slot_mask;
-    const uint32_t lt = lanemask_lt();
-    uint32_t slot[PROBE_BATCH];
-    uint4 k0[PROBE_BATCH];
-    uint32_t vhi[PROBE_BATCH];
+// Probe PROBE_BATCH candidates of one lane with ONE sector read each (all issued before any
+// is consumed) and settle the three common outcomes on the spot:
+//   * the slot holds the same CM, stored by an earlier level   -> duplicate, nothing to write;
+//   * the slot holds the same CM, claimed earlier in this level -> one fire-and-forget min on its ordinal;
+//   * the slot is empty -> reserve a claim index, claim the key with a 128-bit CAS (all CASes of
+//     the batch in flight together), publish index / key / ordinal.
+// What is left -- collisions, lost CAS races, claims whose index is not published yet, the
+// all-ones key and every separating candidate -- is parked and resolved by drain_round.
+// `known[r]`: the candidate equals one of its operands, i.e. a CM already in the cache -- a
+// duplicate by construction, no probe.  `ord_of(r)` recomputes the ordinal where one is
+// needed, so ordinals hold no registers in the hot loop.
+// The hot set: most duplicates are duplicates of LOW cost levels (tools/dup_profile.py: at cost
+// 14 of the paper's example 66 % of all candidates repeat a CM of cost <= 11, 2.7 MB of keys),
+// so those levels' keys are kept a second time in a small open-addressing table of bare 16-byte
+// keys that stays L2 (and partly L1) resident.  It is read-only while a level is enumerated --
+// plain cached loads, no atomics -- and a hit means "duplicate of an earlier level", which is
+// all a duplicate needs to know: the multi-GB main set in HBM is then probed only by the
+// candidates that miss here.  Sets known[r] for hits.
+__device__ __forceinline__ void hot_filter(const NarrowParams &P, const uint4 (&cand)[PROBE_BATCH], const uint32_t (&hash)[PROBE_BATCH],
+                                           const bool (&live)[PROBE_BATCH], bool (&known)[PROBE_BATCH]) {
+    if (P.hot == nullptr) return;
+    const u64 keep = l2_policy_evict_last();
+    uint32_t s[PROBE_BATCH];
+    uint4 k[PROBE_BATCH];
+    bool pend[PROBE_BATCH];
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        slot[r] = hash_vec(cand[r], 0u) & mask32;
-        if (live[r] && !known[r]) {
-            k0[r] = ld_cg_u4(&P.slots[slot[r]].key);
-            vhi[r] = __ldcg(reinterpret_cast<const uint32_t *>(&P.slots[slot[r]].val) + 1);
+        pend[r] = live[r] && !known[r];
+        s[r] = hash[r] & P.hot_mask;
+        if (pend[r]) k[r] = ld_hot(&P.hot[s[r]], keep);
+    }
+    bool again;
+    do {
+        again = false;
+#pragma unroll
+        for (int r = 0; r < PROBE_BATCH; ++r) {
+            if (!pend[r]) continue;
+            if (key_is_empty(k[r])) {  // (first: the all-ones CM looks like an empty slot and is never in here)
+                pend[r] = false;
+            } else if (v_eq(k[r], cand[r])) {
+                known[r] = true;
+                pend[r] = false;
+            } else {  // another key: linear probing (usually the other half of the same sector)
+                s[r] = (s[r] + 1) & P.hot_mask;
+                k[r] = ld_hot(&P.hot[s[r]], keep);
+                again = true;
+            }
         }
+    } while (again);
+}
+
+template <int LW, bool HOT, typename OrdOf>
+__device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queue, WarpState &st,
+                                             const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                             const bool (&known_in)[PROBE_BATCH], OrdOf ord_of) {
+    const uint32_t mask32 = (uint32_t)P.slot_mask;
+    const uint32_t lt = lanemask_lt();
+    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    enum : uint32_t { ACT_NONE = 0u, ACT_PARK = 1u, ACT_CLAIM = 2u };
+    uint32_t slot[PROBE_BATCH], flags[PROBE_BATCH], act[PROBE_BATCH];
+    uint4 k0[PROBE_BATCH];
+    u64 v0[PROBE_BATCH];
+    bool known[PROBE_BATCH];
+#pragma unroll
+    for (int r = 0; r < PROBE_BATCH; ++r) {
+        slot[r] = hash_vec(cand[r], 0u);
+        known[r] = known_in[r];
+    }
+    if constexpr (HOT) hot_filter(P, cand, slot, live, known);
+#pragma unroll
+    for (int r = 0; r < PROBE_BATCH; ++r) {
+        slot[r] &= mask32;
+        if (live[r] && !known[r]) ld_slot(&P.slots[slot[r]], k0[r], v0[r]);
     }
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        uint32_t flags = cm_sep_diff<LW>(cand[r], P.target) == 0u ? PK_SEP : 0u;
-        uint32_t s = slot[r];
+        const bool sep = cm_sep_diff<LW>(cand[r], P.target) == 0u;
+        flags[r] = sep ? PK_SEP : 0u;
+        act[r] = ACT_NONE;
+        if (!live[r]) continue;
         if (known[r]) {
-            flags |= PK_OLD;
+            if (sep) { flags[r] |= PK_OLD; act[r] = ACT_PARK; }
         } else if (P.special_possible && key_is_empty(cand[r])) {
-            flags |= PK_SPECIAL;
-        } else if (live[r]) {
-            if (v_eq(k0[r], cand[r])) {
-                if (vhi[r] < epoch_hi) flags |= PK_OLD;  // duplicate of an earlier level: settled
-            } else if (key_is_empty(k0[r])) {
-                flags |= PK_EMPTY;
+            flags[r] |= PK_SPECIAL;
+            act[r] = ACT_PARK;
+        } else if (v_eq(k0[r], cand[r])) {
+            if (v0[r] == VAL_EMPTY || sep) {
+                act[r] = ACT_PARK;  // index not published yet / separating: the queue handles it
+            } else if (v0[r] >= P.epoch) {
+                atomicMin(&P.claim_ord[v0[r] & CLAIM_IDX_MASK], ord_of(r));  // same level: keep the smaller ordinal
+            }  // else: stored by an earlier level
+        } else if (key_is_empty(k0[r])) {
+            if (sep) { flags[r] |= PK_EMPTY; act[r] = ACT_PARK; }
+            else act[r] = ACT_CLAIM;
+        } else {
+            slot[r] = (slot[r] + 1) & mask32;  // collision: continue at the next slot
+            act[r] = ACT_PARK;
+        }
+    }
+    // ---- claims: indices first (warp-uniform), then every CAS of the batch in flight at once
+    u64 idx[PROBE_BATCH];
+#pragma unroll
+    for (int r = 0; r < PROBE_BATCH; ++r) {
+        idx[r] = reserve_claims(P, st, act[r] == ACT_CLAIM);
+        if (act[r] == ACT_CLAIM && idx[r] >= P.claim_cap) {  // claim arrays exhausted: the host regrows and redoes the level
+            atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+            act[r] = ACT_NONE;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < PROBE_BATCH; ++r)
+        if (act[r] == ACT_CLAIM) k0[r] = cas128(&P.slots[slot[r]].key, empty, cand[r]);
+#pragma unroll
+    for (int r = 0; r < PROBE_BATCH; ++r) {
+        if (act[r] == ACT_CLAIM) {
+            if (key_is_empty(k0[r])) {  // claimed: publish the claim index, record key and ordinal
+                __stcg(&P.slots[slot[r]].val, P.epoch | idx[r]);
+                P.claim_key[idx[r]] = cand[r];
+                atomicMin(&P.claim_ord[idx[r]], ord_of(r));
+                act[r] = ACT_NONE;
             } else {
-                s = (s + 1) & mask32;  // collision: continue at the next slot
+                act[r] = ACT_PARK;  // lost the race: look at the slot again (the reserved index stays unused)
             }
         }
-        const bool need = live[r] && flags != PK_OLD;
+        const bool need = act[r] == ACT_PARK;
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, need);
         if (need) {
             Parked e;
             e.key = cand[r];
             e.ord = ord_of(r);
-            e.slot = s;
-            e.flags = flags;
-            ws.queue[st.qfill + __popc(m & lt)] = e;
+            e.slot = slot[r];
+            e.flags = flags[r];
+            queue[st.qfill + __popc(m & lt)] = e;
         }
         st.qfill += __popc(m);
     }
     __syncwarp();
-    while (st.qfill >= 32u) drain_round(P, ws, st);
+    while (st.qfill >= 32u) drain_round(P, queue, st);
 }
 
-template <int LW, int OP>
-__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WarpShared &ws, WarpState &st, u64 tile_local,
+// The tile runners are generic over where candidates go: `sink.emit<LW>(cand, live, known, ord_of)`
+// is the direct insert (DirectSink -> insert_batch) or the bucket scatter of the partitioned
+// path (narrow_part.cuh); WS is the warp's shared state (rows / term / block).
+template <int LW, int OP, class WS, class Sink>
+__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WS &ws, Sink &sink, u64 tile_local,
                                                u64 sep_now) {
     const BlockDesc &B = ws.block;
     const int lane = threadIdx.x & 31;
@@ -339,7 +459,7 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WarpShared
             cand[r] = cm_apply<LW, OP>(x[r], x[r], P.valid);
             known[r] = OP != OP_ATOM && v_eq(cand[r], x[r]);
         }
-        insert_batch<LW>(P, ws, st, cand, live, known, ord_of);
+        sink.template emit<LW>(cand, live, known, ord_of);
     }
 }
 
@@ -350,8 +470,8 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WarpShared
 // When the scalar operand has few rows (an early, small level) a tile takes B.vg groups
 // of 32 vector rows against the same staged rows, so tiles stay a few thousand candidates.
 // VEC_B: the lane dimension walks the right operand; irrelevant for the commutative ones.
-template <int LW, int OP, bool VEC_B>
-__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WarpShared &ws, WarpState &st, u64 tile_local,
+template <int LW, int OP, bool VEC_B, class WS, class Sink>
+__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WS &ws, Sink &sink, u64 tile_local,
                                                 u64 sep_now) {
     const BlockDesc &B = ws.block;
     const int lane = threadIdx.x & 31;
@@ -401,8 +521,87 @@ __device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WarpShare
                 cand[r] = VEC_B ? cm_apply<LW, OP>(xs, xv, P.valid) : cm_apply<LW, OP>(xv, xs, P.valid);
                 known[r] = v_eq(cand[r], xs) || v_eq(cand[r], xv);
             }
-            insert_batch<LW>(P, ws, st, cand, live, known, ord_of);
+            sink.template emit<LW>(cand, live, known, ord_of);
         }
+    }
+}
+
+struct DirectSink {
+    const NarrowParams &P;
+    WarpShared &ws;
+    WarpState &st;
+    template <int LW, typename OrdOf>
+    __device__ __forceinline__ void emit(const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                         const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
+        insert_batch<LW, true>(P, ws.queue, st, cand, live, known, ord_of);
+    }
+};
+
+// Tile tickets are drawn ONE TILE AHEAD: the atomicAdd for the next tile, and the reads of the
+// overflow flag and of the separator bound that go with it, are issued before the current tile
+// is processed and consumed after it, so their latency hides behind the tile's work (the first
+// profile of the partitioned path had half of its stall samples on exactly these round trips).
+// The bound is therefore one tile stale, which only makes pruning marginally later.
+struct TileFetch {  // meaningful in lane 0
+    u64 t = 0, sep = ~0ull, ovf = 0;
+};
+
+__device__ __forceinline__ TileFetch fetch_tile(const NarrowParams &P, const u64 *sep_extra) {
+    TileFetch f;
+    if ((threadIdx.x & 31) == 0) {
+        f.ovf = __ldcg(&P.counters[CTR_OVERFLOW]);
+        f.t = atomicAdd(&P.counters[P.ticket], 1ull);
+        if (P.prune_after_sep) f.sep = __ldcg(&P.counters[CTR_SEP]);
+        if (sep_extra) {
+            const u64 x = __ldcg(sep_extra);
+            f.sep = x < f.sep ? x : f.sep;
+        }
+    }
+    return f;
+}
+
+// Turns a fetched ticket into the warp's current tile: finds its block (the launch's blocks are
+// the (c1, c2) splits of one operator, sorted by first tile; 32 of them are tested per step, one
+// per lane) and copies the descriptor to shared memory.  False when the launch has no tiles left
+// (or the level overflowed).
+template <class WS>
+__device__ __forceinline__ bool open_tile(const NarrowParams &P, WS &ws, const TileFetch &f) {
+    const int lane = threadIdx.x & 31;
+    const u64 ticket = __shfl_sync(0xFFFFFFFFu, f.t, 0);
+    const u64 ovf = __shfl_sync(0xFFFFFFFFu, f.ovf, 0);
+    const u64 sep = __shfl_sync(0xFFFFFFFFu, f.sep, 0);
+    const u64 t = ovf ? P.tile_end : P.tile_begin + P.shard_offset + ticket * P.shard_stride;
+    if (t >= P.tile_end) return false;
+    int bi = P.block_begin;
+    for (int b0 = P.block_begin + 1; b0 < P.block_end; b0 += 32) {
+        const int b = b0 + lane;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, b < P.block_end && P.blocks[b].tile0 <= t);
+        bi += __popc(m);
+        if (m != 0xFFFFFFFFu) break;
+    }
+    static_assert(sizeof(BlockDesc) % 4 == 0 && sizeof(BlockDesc) / 4 <= 32, "descriptor copied one word per lane");
+    __syncwarp();
+    if (lane < (int)(sizeof(BlockDesc) / 4))
+        reinterpret_cast<uint32_t *>(&ws.block)[lane] = reinterpret_cast<const uint32_t *>(&P.blocks[bi])[lane];
+    if (lane == 0) {
+        ws.ticket = t;
+        ws.sep_now = sep;
+    }
+    __syncwarp();
+    return true;
+}
+
+template <int LW, int OP, class WS, class Sink>
+__device__ __forceinline__ void run_tile(const NarrowParams &P, WS &ws, Sink &sink) {
+    const u64 sep_now = ws.sep_now;
+    if (ws.block.ord0 > sep_now) return;  // the whole block is ordered after the separator
+    const u64 tile_local = ws.ticket - ws.block.tile0;
+    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
+        // which operand sits in the lanes changes only how the ordinal is formed, not the result
+        if (ws.block.vec_is_b) run_binary_tile<LW, OP, true>(P, ws, sink, tile_local, sep_now);
+        else run_binary_tile<LW, OP, false>(P, ws, sink, tile_local, sep_now);
+    } else {
+        run_unary_tile<LW, OP>(P, ws, sink, tile_local, sep_now);
     }
 }
 
@@ -416,40 +615,16 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_ke
     __shared__ WarpShared s_warp[WARPS_PER_CTA];
     WarpShared &ws = s_warp[threadIdx.x >> 5];
     WarpState st;
-    const int lane = threadIdx.x & 31;
+    DirectSink sink{P, ws, st};
+    TileFetch next = fetch_tile(P, nullptr);
     for (;;) {
-        __syncwarp();
-        if (lane == 0) {
-            u64 t = P.tile_end;
-            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
-                t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
-            ws.ticket = t;
-            ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
-            if (t < P.tile_end) {
-                int bi = P.block_begin;
-                while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
-                ws.block = P.blocks[bi];
-            }
-        }
-        __syncwarp();
-        const u64 tile = ws.ticket;
-        const u64 sep_now = ws.sep_now;
-        if (tile >= P.tile_end) break;
-        if (ws.block.ord0 > sep_now) continue;  // the whole block is ordered after the separator
-        const u64 tile_local = tile - ws.block.tile0;
-        if constexpr (OP == OP_AND || OP == OP_OR) {
-            // commutative: which operand sits in the lanes does not change the result, only the ordinal
-            if (ws.block.vec_is_b) run_binary_tile<LW, OP, true>(P, ws, st, tile_local, sep_now);
-            else run_binary_tile<LW, OP, false>(P, ws, st, tile_local, sep_now);
-        } else if constexpr (OP == OP_UNTIL) {
-            if (ws.block.vec_is_b) run_binary_tile<LW, OP, true>(P, ws, st, tile_local, sep_now);
-            else run_binary_tile<LW, OP, false>(P, ws, st, tile_local, sep_now);
-        } else {
-            run_unary_tile<LW, OP>(P, ws, st, tile_local, sep_now);
-        }
+        const TileFetch cur = next;
+        if (!open_tile(P, ws, cur)) break;
+        next = fetch_tile(P, nullptr);
+        run_tile<LW, OP>(P, ws, sink);
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
-        while (st.qfill > 0u) drain_round(P, ws, st);
+        while (st.qfill > 0u) drain_round(P, ws.queue, st);
 }
 
 // ---- finalisation: order the level's winners by ordinal without a sort -------------
@@ -512,6 +687,22 @@ __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 
                 break;
             }
             slot = (slot + 1) & slot_mask;
+        }
+    }
+}
+
+// add finalised rows [first, first+count) to the hot set (bare keys; the all-ones CM stays out:
+// it is the empty marker, and takes the main set's side register as always)
+__global__ void __launch_bounds__(256) hot_insert_kernel(uint4 *hot, uint32_t hot_mask, const uint4 *store, u64 first, u64 count) {
+    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (u64)gridDim.x * blockDim.x) {
+        const uint4 key = store[first + t];
+        if (key_is_empty(key)) continue;
+        uint32_t slot = hash_vec(key, 0u) & hot_mask;
+        for (;;) {
+            const uint4 old = cas128(&hot[slot], empty, key);
+            if (key_is_empty(old) || v_eq(old, key)) break;
+            slot = (slot + 1) & hot_mask;
         }
     }
 }
