@@ -28,6 +28,7 @@
 
 #include "../../include/ltlsynth_b200.h"
 #include "narrow.cuh"
+#include "narrow_async.cuh"
 #include "narrow_part.cuh"
 #include "wide.cuh"
 
@@ -68,6 +69,32 @@ static double monotonic_s() {
     clock_gettime(CLOCK_MONOTONIC, &ts);
     return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
+
+// LTLB200_TIMING=1: host-side phase timers of the level loop, printed when a handle is destroyed
+struct PhaseTimers {
+    static constexpr int N = 12;
+    double acc[N] = {};
+    const char *name[N] = {};
+    bool on = getenv("LTLB200_TIMING") != nullptr;
+    void add(int i, const char *n, double dt) {
+        acc[i] += dt;
+        name[i] = n;
+    }
+    void dump() const {
+        if (!on) return;
+        for (int i = 0; i < N; ++i)
+            if (name[i]) fprintf(stderr, "[ltlb200 timing] %-28s %9.3f ms\n", name[i], 1e3 * acc[i]);
+    }
+};
+static PhaseTimers g_phase;
+#define PHASE(i, label, t0)                              \
+    do {                                                 \
+        if (g_phase.on) {                                \
+            const double now__ = monotonic_s();          \
+            g_phase.add(i, label, now__ - (t0));         \
+            (t0) = now__;                                \
+        }                                                \
+    } while (0)
 
 static u64 next_pow2(u64 x) {
     u64 p = 1;
@@ -217,6 +244,11 @@ __global__ void __launch_bounds__(1024) sb_add_kernel(uint32_t *out, u64 n, cons
     if (i < n) out[i] += block_prefix[blockIdx.x];
 }
 
+__global__ void level_init_kernel(u64 *counters) {
+    const int i = threadIdx.x;
+    if (i < CTR_COUNT && i != CTR_SPECIAL) counters[i] = i == CTR_SEP ? VAL_EMPTY : 0ull;
+}
+
 // number of winners and rank of the separator's ordinal (the separator is counters[CTR_SEP])
 __global__ void level_summary_kernel(const uint32_t *bitmap, const uint32_t *sb_rank, u64 n_bits, u64 *counters) {
     const u64 sep_ord = counters[CTR_SEP];
@@ -289,6 +321,7 @@ private:
     DeviceArray<uint4> store_;
     DeviceArray<u64> ords_;
     DeviceArray<Slot16> slots_;
+    u64 grown_size(u64 want_slots) const;
     DeviceArray<uint4> claim_key_;   // narrow path: this level's new CMs by claim index
     DeviceArray<u64> claim_ord_;
     DeviceArray<u64> wslots_;          // wide path: slot words
@@ -323,7 +356,7 @@ private:
     struct PendingLevel {
         LevelMeta lv;
         u64 constructed = 0, n_claimed = 0, sep_ord = ~0ull, n_seps = 0, claim_cap = 0;
-        bool exhaustive = false, active = false, seps_overflow = false;
+        bool exhaustive = false, active = false, seps_overflow = false, imported = false;
         int cost = 0;
         std::vector<u64> owner_counts;
     } pending_;
@@ -436,6 +469,9 @@ void Engine::reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems) {
 
 template <int LW>
 static int part_occupancy_of();
+template <int LW>
+static int async_occupancy_of();
+static bool async_enabled();
 
 template <int LW>
 static int occupancy_of() {
@@ -509,6 +545,8 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_rows / init leave scope
     occupancy_ = wide_ ? 4 : (lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>());
+    if (!wide_ && async_enabled())
+        occupancy_ = lw_ == 8 ? async_occupancy_of<8>() : lw_ == 16 ? async_occupancy_of<16>() : lw_ == 32 ? async_occupancy_of<32>() : async_occupancy_of<64>();
     if (!wide_) part_occupancy_ = lw_ == 8 ? part_occupancy_of<8>() : lw_ == 16 ? part_occupancy_of<16>() : lw_ == 32 ? part_occupancy_of<32>() : part_occupancy_of<64>();
     rebuild_table(kMinSlots);
     st_.row_bytes = row_bytes_;
@@ -542,9 +580,22 @@ Engine::~Engine() {
     release(pc_);
     recycle_retired(true);
     pinned_put(h_counters_);
+    g_phase.dump();
     for (auto &e : ev_)
         if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+// Regrowing re-inserts every stored CM and clears the new set, so it should be rare: grow 8x (two
+// to three levels of a search that widens ~2.5x per level), 4x once the set passes 1 GiB, and
+// exactly to what the level needs when even that is more than a quarter of the budget.
+// (Clearing the next set ahead of time on a side stream was tried and does not overlap: the
+// persistent enumerate CTAs fill every SM, so the memset kernel simply runs after them.)
+u64 Engine::grown_size(u64 want_slots) const {
+    const u64 slot_bytes = wide_ ? sizeof(u64) : sizeof(Slot16);
+    u64 grown = want_slots * (want_slots * slot_bytes >= (1ull << 30) ? 4 : 8);
+    while (grown > want_slots && grown * slot_bytes > budget_ / 4) grown /= 2;
+    return grown;
 }
 
 // Fresh table of `slots` entries holding every finalised CM (val = global id).
@@ -810,6 +861,53 @@ static void launch_op(int op, const NarrowParams &P, int grid, cudaStream_t st) 
     }
 }
 
+constexpr size_t kAsyncSmem = sizeof(WarpSharedAsync) * WARPS_PER_CTA;
+
+template <int LW, int OP>
+static void launch_async_instance(const NarrowParams &P, int grid, cudaStream_t st) {
+    static std::once_flag once;  // opt in to > 48 KB of dynamic shared memory, once per instance
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(narrow_async_kernel<LW, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmem);
+    });
+    narrow_async_kernel<LW, OP><<<grid, CTA_THREADS, kAsyncSmem, st>>>(P);
+}
+
+template <int LW>
+static void launch_op_async(int op, const NarrowParams &P, int grid, cudaStream_t st) {
+    switch (op) {
+        case OP_ATOM: launch_async_instance<LW, OP_ATOM>(P, grid, st); break;
+        case OP_NOT: launch_async_instance<LW, OP_NOT>(P, grid, st); break;
+        case OP_NEXT: launch_async_instance<LW, OP_NEXT>(P, grid, st); break;
+        case OP_FUTURE: launch_async_instance<LW, OP_FUTURE>(P, grid, st); break;
+        case OP_AND: launch_async_instance<LW, OP_AND>(P, grid, st); break;
+        case OP_UNTIL: launch_async_instance<LW, OP_UNTIL>(P, grid, st); break;
+        default: launch_async_instance<LW, OP_OR>(P, grid, st); break;
+    }
+}
+
+template <int LW>
+static int async_occupancy_of() {
+    int occ = 0;
+    cudaFuncSetAttribute(narrow_async_kernel<LW, OP_UNTIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_async_kernel<LW, OP_UNTIL>, CTA_THREADS, kAsyncSmem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    return std::max(occ, 1);
+}
+
+// LTLB200_ASYNC=1 selects the cp.async pipeline (narrow_async_kernel) instead of the synchronous
+// direct kernel (narrow_level_kernel).  Off by default: with 8 warps per SM (its stages need
+// 105 KB of shared memory per CTA) it is 5-15 % faster on mid-size levels and 20 % slower on the
+// largest one of spec2; kept for A/B measurements.
+static bool async_enabled() {
+    static const bool on = [] {
+        const char *env = getenv("LTLB200_ASYNC");
+        return env && env[0] == '1';
+    }();
+    return on;
+}
+
 template <int LW>
 static void launch_op_wide(int op, const WideParams &P, int grid, cudaStream_t st) {
     switch (op) {
@@ -855,6 +953,15 @@ static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int o
 
 void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
     for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const NarrowParams &Q, int grid) {
+        if (async_enabled()) {
+            switch (lw_) {
+                case 8: launch_op_async<8>(op, Q, grid, stream_); break;
+                case 16: launch_op_async<16>(op, Q, grid, stream_); break;
+                case 32: launch_op_async<32>(op, Q, grid, stream_); break;
+                default: launch_op_async<64>(op, Q, grid, stream_); break;
+            }
+            return;
+        }
         switch (lw_) {
             case 8: launch_op<8>(op, Q, grid, stream_); break;
             case 16: launch_op<16>(op, Q, grid, stream_); break;
@@ -877,11 +984,13 @@ void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
 
 // ---- hot set ----------------------------------------------------------------------------------
 
-// LTLB200_HOT_MB: size cap of the hot set in MiB (0 disables it); default 64 of the 126 MB L2.
+// LTLB200_HOT_MB: size cap of the hot set in MiB.  Default 0 = off: measured on B200 (spec2, DESIGN.md
+// section 4) the extra dependent L2 round trip costs the latency-bound kernel more than the DRAM probes
+// it saves, with or without a persisting-L2 window.
 u64 Engine::hot_max_bytes() {
     static const u64 bytes = [] {
         const char *env = getenv("LTLB200_HOT_MB");
-        return (env ? strtoull(env, nullptr, 10) : 64ull) << 20;
+        return (env ? strtoull(env, nullptr, 10) : 0ull) << 20;
     }();
     return bytes;
 }
@@ -889,7 +998,7 @@ u64 Engine::hot_max_bytes() {
 // After a level is appended: add it to the hot set while everything stored so far fits at a load
 // factor <= 1/2 under the size cap; the first level that does not fit closes the set.
 void Engine::update_hot() {
-    if (hot_closed_ || hot_max_bytes() == 0) return;
+    if (!LTLB200_ENABLE_HOT || hot_closed_ || hot_max_bytes() == 0) return;
     const int newest = (int)levels_.size();
     if (hot_levels_ != newest - 1) return;  // (a level was skipped: budget outcome)
     const LevelMeta &lv = levels_.back();
@@ -916,6 +1025,27 @@ void Engine::update_hot() {
     }
     hot_levels_ = newest;
     hot_entries_ = entries;
+    // pin the hot set in the L2: persisting carve-out + access-policy window on this stream
+    static const bool persist = [] { const char *e = getenv("LTLB200_HOT_PERSIST"); return !(e && e[0] == '0'); }();
+    if (persist) {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device_);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device_);
+        const size_t bytes = hot_slots_ * sizeof(uint4);
+        const size_t carve = std::min<size_t>(bytes, (size_t)max_persist);
+        if (carve) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = hot_.ptr;
+            attr.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
+            attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)carve / (double)bytes);
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr);
+            DBG("hot set: %zu bytes, persisting carve-out %zu (max %d), window max %d", bytes, carve, max_persist, max_window);
+        }
+        cudaGetLastError();
+    }
 }
 
 // ---- partitioned path (narrow_part.cuh) ------------------------------------------------------
@@ -966,8 +1096,10 @@ bool Engine::use_partition(u64 constructed) const {
     if (wide_ || !partition_enabled()) return false;
     static const char *env = getenv("LTLB200_PARTITION");
     if (env && env[0] == '1') return true;
-    // worth it once the set no longer fits the L2 and the level amortises the extra launches
-    return slots_.cap * sizeof(Slot16) > (96ull << 20) && constructed >= (1ull << 21);
+    // Opt-in only (LTLB200_PARTITION=1): on spec2 the two phases together (3.4 ms at cost 16) do not
+    // yet beat the direct kernel (2.8 ms); see DESIGN.md section 4.
+    (void)constructed;
+    return false;
 }
 
 // Phase A per operator (records into bucket chunks), chunk ordering, phase B (bucket by bucket
@@ -1123,7 +1255,9 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         return LTLB200_TIME_BUDGET;
     }
     u64 n_tiles = 0;
+    double tp = monotonic_s();
     plan_level(cost, op_mask, pl.lv, pl.constructed, n_tiles);
+    PHASE(0, "begin: plan", tp);
     pl.active = true;
     if (pl.constructed == 0) return LTLB200_OK;
     const LevelMeta &lv = pl.lv;
@@ -1150,18 +1284,16 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             // (narrow: every warp of every operator launch may end with a partly used chunk of claim indices)
             const u64 narrow_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8 + 1024;
             const u64 claim_cap = est + (wide_ ? wide_slack : narrow_slack);
-            const u64 want_slots = next_pow2(2 * (total_ + claim_cap));
+            // the set is sized for the CMs it can receive (est; exact for small levels, and beyond est the
+            // claim arrays overflow first because est >= kExact > their slack), not for the claim slack:
+            // small levels then probe a set that stays in the L2
+            const u64 want_slots = next_pow2(2 * (total_ + est));
             DBG("level %d attempt %d: constructed=%llu est=%llu claim_cap=%llu slots=%llu want=%llu", cost, attempt, (unsigned long long)constructed, (unsigned long long)est, (unsigned long long)claim_cap, (unsigned long long)table_slots(), (unsigned long long)want_slots);
-            // regrow in 4x steps (every other level at most) while the set is small; a big set is sized
-            // exactly: clearing and streaming gigabytes of empty slots costs more than regrowing again
-            if (want_slots > table_slots()) rebuild_table(want_slots * sizeof(Slot16) >= (1ull << 30) ? want_slots : 2 * want_slots);
+            if (want_slots > table_slots()) rebuild_table(grown_size(want_slots));
             if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
-            u64 init[CTR_COUNT];
-            for (auto &c : init) c = 0;
-            init[CTR_SEP] = VAL_EMPTY;
-            // the special-key register (CTR_SPECIAL) persists across levels
-            CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, CTR_SPECIAL * sizeof(u64), cudaMemcpyHostToDevice, stream_));
-            CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_OVERFLOW, init + CTR_OVERFLOW, (CTR_COUNT - CTR_OVERFLOW) * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+            // counters start at zero (CTR_SEP at "none"); the special-key register persists across levels
+            level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+            CUDA_CHECK(cudaGetLastError());
             pl.claim_cap = claim_cap;
             if (wide_) {
                 reserve(stage_rows_, claim_cap * nvec_, false);
@@ -1180,14 +1312,17 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
                 NarrowParams P = narrow_params(exhaustive);
                 P.shard_stride = (u64)shard_count;
                 P.shard_offset = (u64)shard_index;
+                PHASE(1, "begin: setup (copies, memsets)", tp);
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
                 if (use_partition(constructed)) launch_partitioned(P, lv, constructed, n_tiles);
                 else launch_enumerate(P, lv);
             }
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+            PHASE(2, "begin: launches", tp);
             h_counters_[kPoolOverflowWord] = 0;
             read_counters();
             if (h_counters_[kPoolOverflowWord]) throw CudaError("record pool overflow in the partitioned path");
+            PHASE(3, "begin: sync + read counters", tp);
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
             st_.enumerate_ms += ms;
@@ -1287,10 +1422,13 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
         levels_.push_back(lv);
         return LTLB200_OK;
     }
+    double tp = monotonic_s();
     try {
-        // claims may have grown through claims_import
-        CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        if (pl.imported) {  // claims grew through claims_import: read the counters again
+            CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+            CUDA_CHECK(cudaStreamSynchronize(stream_));
+        }
+        PHASE(4, "end: re-read counters", tp);
         if (h_counters_[CTR_OVERFLOW]) throw CudaError("hash set overflow while importing claims");
         const u64 n_claimed = h_counters_[CTR_CLAIMED];
         const bool cut = !exhaustive && sep_ord != VAL_EMPTY;
@@ -1381,7 +1519,9 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
         CUDA_CHECK(cudaGetLastError());
         CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
         st_.kernel_launches += 3;
+        PHASE(5, "end: reserve + launches", tp);
         read_counters();
+        PHASE(6, "end: sync + read counters", tp);
         float fms = 0;
         CUDA_CHECK(cudaEventElapsedTime(&fms, ev_[2], ev_[3]));
         st_.finalize_ms += fms;
@@ -1405,6 +1545,7 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
     st_.unique = total_;
     approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
     levels_.push_back(std::move(lv));
+    PHASE(7, "end: bookkeeping", tp);
     if (!wide_) {
         try {
             update_hot();
@@ -1479,6 +1620,7 @@ void Engine::claims_import(const void *rows_dev, const void *ords_dev, u64 n) {
     if (!pending_.active) throw std::invalid_argument("claims_import outside a level");
     if (!n) return;
     CUDA_CHECK(cudaSetDevice(device_));
+    pending_.imported = true;
     if (wide_) {
         WideParams P = wide_params(pending_.exhaustive);
         P.sep_list = nullptr;

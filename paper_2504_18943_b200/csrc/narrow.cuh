@@ -30,11 +30,18 @@
 
 namespace ltlb200 {
 
+// The hot set (see hot_filter) is compiled out by default: it is a measured loss on B200
+// and its code costs the direct kernel registers even when unused.
+#ifndef LTLB200_ENABLE_HOT
+#define LTLB200_ENABLE_HOT 0
+#endif
 #ifndef LTLB200_PROBE_BATCH
 #define LTLB200_PROBE_BATCH 4
 #endif
+// CTAs per SM of the direct kernel.  Measured on spec2 (enumerate ms per search): 3 -> 5.34,
+// 4 -> 5.78, 5 -> 6.47, 6 -> 7.10: registers without spills beat resident warps.
 #ifndef LTLB200_MIN_CTAS
-#define LTLB200_MIN_CTAS 4
+#define LTLB200_MIN_CTAS 3
 #endif
 #ifndef LTLB200_TILE_S
 #define LTLB200_TILE_S 128
@@ -147,13 +154,23 @@ __device__ __forceinline__ uint4 ld_hot(const uint4 *p, u64 policy) {
     return v;
 }
 
-// one 32-byte slot = one sector = one 256-bit load: key and val are a consistent snapshot
-__device__ __forceinline__ void ld_slot(const Slot16 *p, uint4 &key, u64 &val) {
+// one 32-byte slot = one sector = one 256-bit load: key and val are a consistent snapshot.
+// Relaxed gpu-scope load (LDG.256.STRONG.GPU): served by the L2, never by a stale L1 line.
+// `streaming`: evict-first, used while a hot set wants the L2 for itself.
+__device__ __forceinline__ void ld_slot(const Slot16 *p, uint4 &key, u64 &val, bool streaming) {
     uint32_t v0, v1, pad0, pad1;
-    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
-                 : "l"(p)
-                 : "memory");
+    if (streaming)
+        asm volatile("ld.relaxed.gpu.global.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
+                     : "l"(p)
+                     : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
+                     : "l"(p)
+                     : "memory");
+    (void)pad0;
+    (void)pad1;
     val = (u64)v1 << 32 | v0;
 }
 
@@ -229,7 +246,7 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, Parked *queue
     // ---- look at the slot (skipped when the first probe already saw it empty)
     uint4 k = empty;
     u64 v = VAL_EMPTY;
-    if (probing && !(e.flags & PK_EMPTY)) ld_slot(slot, k, v);
+    if (probing && !(e.flags & PK_EMPTY)) ld_slot(slot, k, v, P.hot != nullptr);
     if (special) v = *(volatile u64 *)&P.counters[CTR_SPECIAL];
     // ---- lanes that will try to claim reserve their claim index first
     const bool attempt = (probing && key_is_empty(k)) || (special && v == VAL_EMPTY);
@@ -356,11 +373,11 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queu
         slot[r] = hash_vec(cand[r], 0u);
         known[r] = known_in[r];
     }
-    if constexpr (HOT) hot_filter(P, cand, slot, live, known);
+    if constexpr (HOT && LTLB200_ENABLE_HOT) hot_filter(P, cand, slot, live, known);
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
         slot[r] &= mask32;
-        if (live[r] && !known[r]) ld_slot(&P.slots[slot[r]], k0[r], v0[r]);
+        if (live[r] && !known[r]) ld_slot(&P.slots[slot[r]], k0[r], v0[r], P.hot != nullptr);
     }
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
@@ -431,8 +448,11 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queu
 // The tile runners are generic over where candidates go: `sink.emit<LW>(cand, live, known, ord_of)`
 // is the direct insert (DirectSink -> insert_batch) or the bucket scatter of the partitioned
 // path (narrow_part.cuh); WS is the warp's shared state (rows / term / block).
+// Both return true when this tile AND every later tile of the launch are ordered after the
+// separator (tiles follow the canonical order of their outer index), so the warp can stop
+// drawing tickets instead of fetching and skipping them one by one.
 template <int LW, int OP, class WS, class Sink>
-__device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WS &ws, Sink &sink, u64 tile_local,
+__device__ __forceinline__ bool run_unary_tile(const NarrowParams &P, WS &ws, Sink &sink, u64 tile_local,
                                                u64 sep_now) {
     const BlockDesc &B = ws.block;
     const int lane = threadIdx.x & 31;
@@ -440,7 +460,7 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WS &ws, Si
     const u64 per_tile = (u64)TILE_V * B.tile_s;
     const u64 first = tile_local * per_tile + lane;
     const u64 ord0 = B.ord0, n = B.na;
-    if (ord0 + tile_local * per_tile > sep_now) return;  // tile ordered after the separator
+    if (ord0 + tile_local * per_tile > sep_now) return true;  // this and all later tiles are ordered after the separator
     const int n_groups = (int)min((u64)B.tile_s, (n - tile_local * per_tile + TILE_V - 1) / TILE_V);
 #pragma unroll 1
     for (int g = 0; g < n_groups; g += PROBE_BATCH) {
@@ -461,6 +481,7 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WS &ws, Si
         }
         sink.template emit<LW>(cand, live, known, ord_of);
     }
+    return false;
 }
 
 // Binary tile: each lane keeps one row of the "vector" operand in registers and walks up
@@ -471,7 +492,7 @@ __device__ __forceinline__ void run_unary_tile(const NarrowParams &P, WS &ws, Si
 // of 32 vector rows against the same staged rows, so tiles stay a few thousand candidates.
 // VEC_B: the lane dimension walks the right operand; irrelevant for the commutative ones.
 template <int LW, int OP, bool VEC_B, class WS, class Sink>
-__device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WS &ws, Sink &sink, u64 tile_local,
+__device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, Sink &sink, u64 tile_local,
                                                 u64 sep_now) {
     const BlockDesc &B = ws.block;
     const int lane = threadIdx.x & 31;
@@ -484,11 +505,15 @@ __device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WS &ws, S
     const u64 n_vec = VEC_B ? B.nb : B.na, n_sc = VEC_B ? B.na : B.nb;
     const u64 v0 = tv * (u64)(TILE_V * vg_n), s0 = ts * (u64)B.tile_s;
     const int s_cnt = (int)min((u64)B.tile_s, n_sc - s0);
-    if (tri && v0 + (u64)TILE_V * vg_n - 1 < s0) return;  // tile entirely below the diagonal (j < i)
     const u64 ord0 = B.ord0, na = B.na, nb = B.nb;
+    // smallest ordinal of this tile's outer row of tiles (the left operand is the outer index
+    // in both layouts): beyond the separator => so is everything that follows in the launch
+    const u64 outer_min = ord0 + (VEC_B ? (tri ? s0 * na - (s0 ? (s0 * (s0 - 1)) / 2 : 0) : s0 * nb) : v0 * nb);
+    if (outer_min > sep_now) return true;
+    if (tri && v0 + (u64)TILE_V * vg_n - 1 < s0) return false;  // tile entirely below the diagonal (j < i)
     // a lower bound of the tile's ordinals: skip tiles ordered after the separator
-    const u64 tile_min = ord0 + (VEC_B ? (tri ? s0 * na - (s0 ? (s0 * (s0 - 1)) / 2 : 0) : s0 * nb + v0) : v0 * nb + s0);
-    if (tile_min > sep_now) return;
+    const u64 tile_min = outer_min + (VEC_B ? (tri ? 0 : v0) : s0);
+    if (tile_min > sep_now) return false;
     const uint4 *vec_rows = P.store + (VEC_B ? B.b_off : B.a_off);
     const uint4 *sc_rows = P.store + (VEC_B ? B.a_off : B.b_off);
     __syncwarp();
@@ -499,12 +524,15 @@ __device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WS &ws, S
         ws.term[k] = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
     }
     __syncwarp();
+    // the vector row of the NEXT group is loaded while this group is processed
+    uint4 xv_next = v0 + lane < n_vec ? __ldg(vec_rows + v0 + lane) : make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (uint32_t vg = 0; vg < vg_n; ++vg) {
         const u64 v = v0 + (u64)vg * TILE_V + lane;
         if (v0 + (u64)vg * TILE_V >= n_vec) break;
         const bool v_ok = v < n_vec;
-        const uint4 xv = v_ok ? __ldg(vec_rows + v) : make_uint4(0, 0, 0, 0);
+        const uint4 xv = xv_next;
+        if (vg + 1 < vg_n && v + TILE_V < n_vec) xv_next = __ldg(vec_rows + v + TILE_V);
         const u64 lane_term = VEC_B ? v : ord0 + v * nb;
         // triangle: row s0+sr pairs with columns j >= i only
         const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
@@ -524,6 +552,7 @@ __device__ __forceinline__ void run_binary_tile(const NarrowParams &P, WS &ws, S
             sink.template emit<LW>(cand, live, known, ord_of);
         }
     }
+    return false;
 }
 
 struct DirectSink {
@@ -592,16 +621,16 @@ __device__ __forceinline__ bool open_tile(const NarrowParams &P, WS &ws, const T
 }
 
 template <int LW, int OP, class WS, class Sink>
-__device__ __forceinline__ void run_tile(const NarrowParams &P, WS &ws, Sink &sink) {
+__device__ __forceinline__ bool run_tile(const NarrowParams &P, WS &ws, Sink &sink) {
     const u64 sep_now = ws.sep_now;
-    if (ws.block.ord0 > sep_now) return;  // the whole block is ordered after the separator
+    if (ws.block.ord0 > sep_now) return true;  // the whole block, and every later one, is ordered after the separator
     const u64 tile_local = ws.ticket - ws.block.tile0;
     if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
         // which operand sits in the lanes changes only how the ordinal is formed, not the result
-        if (ws.block.vec_is_b) run_binary_tile<LW, OP, true>(P, ws, sink, tile_local, sep_now);
-        else run_binary_tile<LW, OP, false>(P, ws, sink, tile_local, sep_now);
+        if (ws.block.vec_is_b) return run_binary_tile<LW, OP, true>(P, ws, sink, tile_local, sep_now);
+        return run_binary_tile<LW, OP, false>(P, ws, sink, tile_local, sep_now);
     } else {
-        run_unary_tile<LW, OP>(P, ws, sink, tile_local, sep_now);
+        return run_unary_tile<LW, OP>(P, ws, sink, tile_local, sep_now);
     }
 }
 
@@ -621,7 +650,7 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_ke
         const TileFetch cur = next;
         if (!open_tile(P, ws, cur)) break;
         next = fetch_tile(P, nullptr);
-        run_tile<LW, OP>(P, ws, sink);
+        if (run_tile<LW, OP>(P, ws, sink)) break;
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
         while (st.qfill > 0u) drain_round(P, ws.queue, st);

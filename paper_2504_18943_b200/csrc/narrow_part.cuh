@@ -189,7 +189,7 @@ struct PartSink {
             hash[r] = hash_vec(cand[r], 0u);
             known[r] = known_in[r];
         }
-        hot_filter(P, cand, hash, live, known);  // duplicates of the low levels never reach the pool
+        if constexpr (LTLB200_ENABLE_HOT) hot_filter(P, cand, hash, live, known);  // duplicates of the low levels never reach the pool
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
             const bool sep = cm_sep_diff<LW>(cand[r], P.target) == 0u;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_PART_MIN_CTAS) narrow_par
         const TileFetch cur = next;
         if (!open_tile(P, ws, cur)) break;
         next = fetch_tile(P, bound);
-        run_tile<LW, OP>(P, ws, sink);
+        if (run_tile<LW, OP>(P, ws, sink)) break;
     }
     sink.finish(slot);
 }
