@@ -292,9 +292,12 @@ public:
     void get_stats(ltlb200_stats *out);
     void reset();
     int level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
-                    u64 *n_claimed, u64 *sep_ord, u64 *n_seps);
+                    u64 *n_claimed, u64 *sep_ord, u64 *n_seps, bool defer = false);
     int level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid,
                   int64_t *constructed_delta);
+    int level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
+    void launch_rank_scan(u64 n_words, u64 n_sb);
+    static constexpr int kRetryLevel = 100;  // internal status: the deferred attempt overflowed, redo synchronously
     void claims_count(int owners, u64 *counts);
     void claims_pack(int owners, void *rows_dev, void *ords_dev);
     void claims_import(const void *rows_dev, const void *ords_dev, u64 n);
@@ -341,13 +344,6 @@ private:
     DeviceArray<uint32_t> chunk_order_; // chunk ids grouped by bucket
     DeviceArray<u64> wstate_;           // open chunks + chunk-id stash of every warp slot, carried across operator launches
     DeviceArray<u64> pc_;
-    // hot set (narrow path): bare keys of the low cost levels, small enough to stay L2 resident
-    DeviceArray<uint4> hot_;
-    u64 hot_slots_ = 0, hot_entries_ = 0;
-    int hot_levels_ = 0;       // levels 1..hot_levels_ are in the hot set
-    bool hot_closed_ = false;  // the next level no longer fits: the hot set stays as it is
-    static u64 hot_max_bytes();
-    void update_hot();
     int part_occupancy_ = 2;
     bool store_has_separator_ = false;  // some stored CM separates: a separating candidate need not be fresh
     static bool partition_enabled();
@@ -356,7 +352,7 @@ private:
     struct PendingLevel {
         LevelMeta lv;
         u64 constructed = 0, n_claimed = 0, sep_ord = ~0ull, n_seps = 0, claim_cap = 0;
-        bool exhaustive = false, active = false, seps_overflow = false, imported = false;
+        bool exhaustive = false, active = false, seps_overflow = false, imported = false, deferred = false;
         int cost = 0;
         std::vector<u64> owner_counts;
     } pending_;
@@ -571,7 +567,6 @@ Engine::~Engine() {
     release(sep_list_);
     release(misc_);
     release(xchg_);
-    release(hot_);
     release(pool_keys_);
     release(pool_ords_);
     release(chunk_meta_);
@@ -586,14 +581,16 @@ Engine::~Engine() {
     if (own_stream_) cudaStreamDestroy(stream_);
 }
 
-// Regrowing re-inserts every stored CM and clears the new set, so it should be rare: grow 8x (two
-// to three levels of a search that widens ~2.5x per level), 4x once the set passes 1 GiB, and
-// exactly to what the level needs when even that is more than a quarter of the budget.
+// Regrowing re-inserts every stored CM and clears the new set, so it should be rare while it is
+// cheap and tight once clearing costs real time (6 GB/ms): grow 8x (two to three levels of a search
+// that widens ~2.5x per level) below 256 MiB, 4x below 1 GiB, 2x beyond, and exactly to what the
+// level needs when even that is more than a quarter of the budget.
 // (Clearing the next set ahead of time on a side stream was tried and does not overlap: the
 // persistent enumerate CTAs fill every SM, so the memset kernel simply runs after them.)
 u64 Engine::grown_size(u64 want_slots) const {
     const u64 slot_bytes = wide_ ? sizeof(u64) : sizeof(Slot16);
-    u64 grown = want_slots * (want_slots * slot_bytes >= (1ull << 30) ? 4 : 8);
+    const u64 want_bytes = want_slots * slot_bytes;
+    u64 grown = want_slots * (want_bytes >= (1ull << 30) ? 2 : want_bytes >= (256ull << 20) ? 4 : 8);
     while (grown > want_slots && grown * slot_bytes > budget_ / 4) grown /= 2;
     return grown;
 }
@@ -645,9 +642,6 @@ void Engine::reset() {
     approx_bytes_ = 0;
     last_constructed_ = 0;
     store_has_separator_ = false;
-    hot_slots_ = hot_entries_ = 0;
-    hot_levels_ = 0;
-    hot_closed_ = false;
     rebuild_table(kMinSlots);  // small levels probe an L2-resident set again; it regrows with the search
     st_.constructed = 0;
     st_.unique = 0;
@@ -951,7 +945,30 @@ static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int o
     }
 }
 
+// levels up to this many candidates take the one-launch kernel (narrow_small_level_kernel)
+static constexpr u64 kSmallLevel = 1ull << 19;
+
 void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
+    const BlockDesc &last_block = lv.blocks.back();
+    const u64 level_candidates = last_block.ord0 + last_block.size;
+    if (level_candidates <= kSmallLevel && !async_enabled()) {
+        P.block_begin = 0;
+        P.block_end = (int)lv.blocks.size();
+        P.tile_begin = 0;
+        P.tile_end = last_block.tile0 + last_block.tiles_v * last_block.tiles_s;
+        P.ticket = CTR_TICKET0;
+        const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
+        switch (lw_) {
+            case 8: narrow_small_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            case 16: narrow_small_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            case 32: narrow_small_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            default: narrow_small_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+        }
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+        st_.enumerate_launches++;
+        return;
+    }
     for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const NarrowParams &Q, int grid) {
         if (async_enabled()) {
             switch (lw_) {
@@ -980,72 +997,6 @@ void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
             default: launch_op_wide<64>(op, Q, grid, stream_); break;
         }
     });
-}
-
-// ---- hot set ----------------------------------------------------------------------------------
-
-// LTLB200_HOT_MB: size cap of the hot set in MiB.  Default 0 = off: measured on B200 (spec2, DESIGN.md
-// section 4) the extra dependent L2 round trip costs the latency-bound kernel more than the DRAM probes
-// it saves, with or without a persisting-L2 window.
-u64 Engine::hot_max_bytes() {
-    static const u64 bytes = [] {
-        const char *env = getenv("LTLB200_HOT_MB");
-        return (env ? strtoull(env, nullptr, 10) : 0ull) << 20;
-    }();
-    return bytes;
-}
-
-// After a level is appended: add it to the hot set while everything stored so far fits at a load
-// factor <= 1/2 under the size cap; the first level that does not fit closes the set.
-void Engine::update_hot() {
-    if (!LTLB200_ENABLE_HOT || hot_closed_ || hot_max_bytes() == 0) return;
-    const int newest = (int)levels_.size();
-    if (hot_levels_ != newest - 1) return;  // (a level was skipped: budget outcome)
-    const LevelMeta &lv = levels_.back();
-    const u64 entries = lv.base + lv.n;
-    const u64 want = std::max<u64>(next_pow2(2 * entries), 1ull << 12);
-    if (want * sizeof(uint4) > hot_max_bytes()) {
-        hot_closed_ = true;
-        return;
-    }
-    u64 first = lv.base, count = lv.n;
-    if (want > hot_slots_) {  // regrow: re-insert every level
-        const u64 slots = std::min<u64>(want * 4, hot_max_bytes() / sizeof(uint4));
-        reserve(hot_, slots, false);
-        hot_slots_ = next_pow2(slots) > slots ? next_pow2(slots) / 2 : slots;
-        CUDA_CHECK(cudaMemsetAsync(hot_.ptr, 0xFF, hot_slots_ * sizeof(uint4), stream_));
-        first = 0;
-        count = entries;
-    }
-    if (count) {
-        const int grid = (int)std::min<u64>((count + 255) / 256, (u64)sm_count_ * 16);
-        hot_insert_kernel<<<grid, 256, 0, stream_>>>(hot_.ptr, (uint32_t)(hot_slots_ - 1), store_.ptr, first, count);
-        CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches++;
-    }
-    hot_levels_ = newest;
-    hot_entries_ = entries;
-    // pin the hot set in the L2: persisting carve-out + access-policy window on this stream
-    static const bool persist = [] { const char *e = getenv("LTLB200_HOT_PERSIST"); return !(e && e[0] == '0'); }();
-    if (persist) {
-        int max_persist = 0, max_window = 0;
-        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device_);
-        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device_);
-        const size_t bytes = hot_slots_ * sizeof(uint4);
-        const size_t carve = std::min<size_t>(bytes, (size_t)max_persist);
-        if (carve) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
-            cudaStreamAttrValue attr{};
-            attr.accessPolicyWindow.base_ptr = hot_.ptr;
-            attr.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
-            attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)carve / (double)bytes);
-            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr);
-            DBG("hot set: %zu bytes, persisting carve-out %zu (max %d), window max %d", bytes, carve, max_persist, max_window);
-        }
-        cudaGetLastError();
-    }
 }
 
 // ---- partitioned path (narrow_part.cuh) ------------------------------------------------------
@@ -1236,8 +1187,10 @@ void Engine::launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constru
 
 // Enumerates the tiles of level `cost` that belong to shard `shard_index` of `shard_count`
 // (tile-strided) into the local hash set.  Nothing is appended yet; level_end() does that.
+// `defer` (single-GPU, non-exhaustive, narrow): do not wait for the enumeration -- level_end launches
+// the finalisation right behind it with device-side bounds and synchronises once for both.
 int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
-                        u64 *n_claimed_out, u64 *sep_ord_out, u64 *n_seps_out) {
+                        u64 *n_claimed_out, u64 *sep_ord_out, u64 *n_seps_out, bool defer) {
     if (pending_.active) throw std::invalid_argument("level_begin: the previous level was not ended");
     if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
     if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count) throw std::invalid_argument("bad shard");
@@ -1319,6 +1272,11 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             }
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
             PHASE(2, "begin: launches", tp);
+            if (defer && !wide_ && !exhaustive && !use_partition(constructed)) {
+                pl.deferred = true;
+                st_.enumerate_candidates += constructed / (u64)shard_count;
+                return LTLB200_OK;
+            }
             h_counters_[kPoolOverflowWord] = 0;
             read_counters();
             if (h_counters_[kPoolOverflowWord]) throw CudaError("record pool overflow in the partitioned path");
@@ -1357,8 +1315,6 @@ NarrowParams Engine::narrow_params(bool exhaustive) const {
     P.atoms = d_atoms_;
     P.slots = slots_.ptr;
     P.slot_mask = slots_.cap - 1;
-    P.hot = hot_slots_ ? hot_.ptr : nullptr;
-    P.hot_mask = hot_slots_ ? (uint32_t)(hot_slots_ - 1) : 0u;
     P.claim_key = claim_key_.ptr;
     P.claim_ord = claim_ord_.ptr;
     P.claim_cap = pending_.claim_cap;
@@ -1423,6 +1379,7 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
         return LTLB200_OK;
     }
     double tp = monotonic_s();
+    if (pl.deferred) return level_end_deferred(batch, mem_budget, n_new, sep_gid, constructed_delta);
     try {
         if (pl.imported) {  // claims grew through claims_import: read the counters again
             CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
@@ -1472,29 +1429,7 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
             narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
         }
         CUDA_CHECK(cudaGetLastError());
-        // popcount prefix per superblock: up to three scan levels of 1024
-        {
-            const u64 nb1 = (n_sb + 1023) / 1024;
-            reserve(scan_tmp_, 2 * (nb1 + 1024) + 2048, false);
-            uint32_t *sums1 = scan_tmp_.ptr, *pre1 = sums1 + nb1 + 8;
-            sb_scan_kernel<<<(unsigned)nb1, 1024, 0, stream_>>>(bitmap_.ptr, n_words, nullptr, sb_rank_.ptr, n_sb, sums1);
-            CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches++;
-            if (nb1 > 1) {
-                const u64 nb2 = (nb1 + 1023) / 1024;
-                uint32_t *sums2 = pre1 + nb1 + 8, *pre2 = sums2 + nb2 + 8;
-                sb_scan_kernel<<<(unsigned)nb2, 1024, 0, stream_>>>(nullptr, 0, sums1, pre1, nb1, sums2);
-                if (nb2 > 1) {
-                    if (nb2 > 1024) throw std::invalid_argument("level too large for the rank scan");
-                    sb_scan_kernel<<<1, 1024, 0, stream_>>>(nullptr, 0, sums2, pre2, nb2, nullptr);
-                    sb_add_kernel<<<(unsigned)nb2, 1024, 0, stream_>>>(pre1, nb1, pre2);
-                    st_.kernel_launches += 2;
-                }
-                sb_add_kernel<<<(unsigned)nb1, 1024, 0, stream_>>>(sb_rank_.ptr, n_sb, pre1);
-                CUDA_CHECK(cudaGetLastError());
-                st_.kernel_launches += 2;
-            }
-        }
+        launch_rank_scan(n_words, n_sb);
         // exhaustive runs: the reference reports, per level, the first CHUNK whose first
         // separating candidate is fresh (engine.py:331,425-433); reproduce that exactly
         if (exhaustive) {
@@ -1546,13 +1481,113 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
     approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
     levels_.push_back(std::move(lv));
     PHASE(7, "end: bookkeeping", tp);
-    if (!wide_) {
-        try {
-            update_hot();
-        } catch (const MemoryBudget &) {  // no room for it: carry on without
-            hot_closed_ = true;
+    if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
+    return LTLB200_OK;
+}
+
+// popcount prefix per 1024-bit superblock of the winners bitmap: up to three scan levels of 1024
+void Engine::launch_rank_scan(u64 n_words, u64 n_sb) {
+        {
+    const u64 nb1 = (n_sb + 1023) / 1024;
+    reserve(scan_tmp_, 2 * (nb1 + 1024) + 2048, false);
+    uint32_t *sums1 = scan_tmp_.ptr, *pre1 = sums1 + nb1 + 8;
+    sb_scan_kernel<<<(unsigned)nb1, 1024, 0, stream_>>>(bitmap_.ptr, n_words, nullptr, sb_rank_.ptr, n_sb, sums1);
+    CUDA_CHECK(cudaGetLastError());
+    st_.kernel_launches++;
+    if (nb1 > 1) {
+        const u64 nb2 = (nb1 + 1023) / 1024;
+        uint32_t *sums2 = pre1 + nb1 + 8, *pre2 = sums2 + nb2 + 8;
+        sb_scan_kernel<<<(unsigned)nb2, 1024, 0, stream_>>>(nullptr, 0, sums1, pre1, nb1, sums2);
+        if (nb2 > 1) {
+            if (nb2 > 1024) throw std::invalid_argument("level too large for the rank scan");
+            sb_scan_kernel<<<1, 1024, 0, stream_>>>(nullptr, 0, sums2, pre2, nb2, nullptr);
+            sb_add_kernel<<<(unsigned)nb2, 1024, 0, stream_>>>(pre1, nb1, pre2);
+            st_.kernel_launches += 2;
         }
+        sb_add_kernel<<<(unsigned)nb1, 1024, 0, stream_>>>(sb_rank_.ptr, n_sb, pre1);
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches += 2;
     }
+}
+}
+
+// Finalisation launched right behind the enumeration (see level_begin's `defer`): every bound the
+// host would have read from the counters is resolved on the device, and the one synchronisation
+// at the end serves both phases.  Returns kRetryLevel when the enumeration overflowed.
+int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
+    PendingLevel &pl = pending_;
+    LevelMeta &lv = pl.lv;
+    const u64 constructed = pl.constructed;
+    double tp = monotonic_s();
+    u64 sep_ord = VAL_EMPTY;
+    try {
+        const u64 n_bits = constructed;
+        const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
+        reserve(bitmap_, n_words + 1, false);
+        reserve(sb_rank_, n_sb + 1, false);
+        reserve(store_, (total_ + pl.claim_cap) * nvec_, true, total_ * nvec_);
+        reserve(ords_, total_ + pl.claim_cap, true, total_);
+        CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
+        CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+        FinalizeParams F{};
+        F.claim_key = claim_key_.ptr;
+        F.claim_ord = claim_ord_.ptr;
+        F.bitmap = bitmap_.ptr;
+        F.sb_rank = sb_rank_.ptr;
+        F.store = store_.ptr;
+        F.ords = ords_.ptr;
+        F.base = total_;
+        F.live = d_counters_;
+        F.claim_cap = pl.claim_cap;
+        F.cut_allowed = 1;
+        // the grid is sized by what the level can have claimed at most (its candidates, or the claim arrays)
+        const u64 claim_bound = std::min(constructed + (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK, pl.claim_cap);
+        const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
+        narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        CUDA_CHECK(cudaGetLastError());
+        launch_rank_scan(n_words, n_sb);
+        level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+        narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        CUDA_CHECK(cudaGetLastError());
+        CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
+        st_.kernel_launches += 3;
+        PHASE(5, "end: reserve + launches", tp);
+        read_counters();
+        PHASE(6, "end: sync + read counters", tp);
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        st_.enumerate_ms += ms;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+        st_.finalize_ms += ms;
+        recycle_retired(false);
+        pl.active = false;
+        if (h_counters_[CTR_OVERFLOW]) {  // the guess of new CMs was too small: nothing was finalised
+            table_dirty_ = true;
+            return kRetryLevel;
+        }
+        lv.n = h_counters_[CTR_WINNERS];
+        sep_ord = h_counters_[CTR_SEP];
+        if (sep_ord != VAL_EMPTY) {
+            *sep_gid = (int64_t)(total_ + h_counters_[CTR_SEPRANK]);
+            store_has_separator_ = true;
+            table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
+        }
+    } catch (const MemoryBudget &e) {
+        g_last_error = e.what();
+        table_dirty_ = true;
+        pl.active = false;
+        levels_.push_back(LevelMeta{0, total_, {}});
+        return LTLB200_MEMORY_BUDGET;
+    }
+    *constructed_delta = (int64_t)(sep_ord != VAL_EMPTY ? constructed_through(lv, sep_ord, (u64)batch) : constructed);
+    last_constructed_ = constructed;
+    *n_new = (int64_t)lv.n;
+    total_ += lv.n;
+    st_.constructed += (u64)*constructed_delta;
+    st_.unique = total_;
+    approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
+    levels_.push_back(std::move(lv));
+    PHASE(7, "end: bookkeeping", tp);
     if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
     return LTLB200_OK;
 }
@@ -1564,7 +1599,12 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     *sep_gid = -1;
     *constructed_delta = 0;
     u64 n_claimed = 0, sep_ord = VAL_EMPTY, n_seps = 0;
-    const int rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps);
+    static const bool defer = getenv("LTLB200_NO_DEFER") == nullptr;
+    int rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps, defer);
+    if (rc != LTLB200_OK) return rc;
+    rc = level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
+    if (rc != kRetryLevel) return rc;
+    rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps, false);
     if (rc != LTLB200_OK) return rc;
     return level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
 }

@@ -30,11 +30,6 @@
 
 namespace ltlb200 {
 
-// The hot set (see hot_filter) is compiled out by default: it is a measured loss on B200
-// and its code costs the direct kernel registers even when unused.
-#ifndef LTLB200_ENABLE_HOT
-#define LTLB200_ENABLE_HOT 0
-#endif
 #ifndef LTLB200_PROBE_BATCH
 #define LTLB200_PROBE_BATCH 4
 #endif
@@ -88,8 +83,6 @@ struct NarrowParams {
     const uint4 *atoms;
     Slot16 *slots;
     u64 slot_mask;
-    const uint4 *hot;   // hot set: keys of the low cost levels, 16-byte slots, read-only during a level (NULL = none)
-    uint32_t hot_mask;
     uint4 *claim_key;  // this level's new CMs by claim index
     u64 *claim_ord;    // smallest ordinal per claim index (all ones = index reserved but unused)
     u64 claim_cap;
@@ -135,40 +128,14 @@ __device__ __forceinline__ uint4 cas128(uint4 *addr, uint4 expect, uint4 desired
 
 __device__ __forceinline__ bool key_is_empty(uint4 k) { return (k.x & k.y & k.z & k.w) == 0xFFFFFFFFu; }
 
-// L2 residency control.  Probes of the multi-GB main set touch every sector once: they are
-// loaded evict-first (and never allocate in L1, so a slot changed by another SM is never read
-// stale), otherwise they flush the hot set out of the L2 -- measured: with default policies the
-// hot set ADDED 40 % DRAM traffic instead of removing two thirds of it.  Hot-set loads carry an
-// evict-last policy.
-__device__ __forceinline__ u64 l2_policy_evict_last() {
-    u64 p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-__device__ __forceinline__ uint4 ld_hot(const uint4 *p, u64 policy) {
-    uint4 v;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p), "l"(policy));
-    return v;
-}
-
 // one 32-byte slot = one sector = one 256-bit load: key and val are a consistent snapshot.
-// Relaxed gpu-scope load (LDG.256.STRONG.GPU): served by the L2, never by a stale L1 line.
-// `streaming`: evict-first, used while a hot set wants the L2 for itself.
-__device__ __forceinline__ void ld_slot(const Slot16 *p, uint4 &key, u64 &val, bool streaming) {
+// Relaxed gpu-scope load (LDG.E.256.STRONG.GPU): served by the L2, never by a stale L1 line.
+__device__ __forceinline__ void ld_slot(const Slot16 *p, uint4 &key, u64 &val) {
     uint32_t v0, v1, pad0, pad1;
-    if (streaming)
-        asm volatile("ld.relaxed.gpu.global.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
-                     : "l"(p)
-                     : "memory");
-    else
-        asm volatile("ld.relaxed.gpu.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
-                     : "l"(p)
-                     : "memory");
+    asm volatile("ld.relaxed.gpu.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(key.x), "=r"(key.y), "=r"(key.z), "=r"(key.w), "=r"(v0), "=r"(v1), "=r"(pad0), "=r"(pad1)
+                 : "l"(p)
+                 : "memory");
     (void)pad0;
     (void)pad1;
     val = (u64)v1 << 32 | v0;
@@ -246,7 +213,7 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, Parked *queue
     // ---- look at the slot (skipped when the first probe already saw it empty)
     uint4 k = empty;
     u64 v = VAL_EMPTY;
-    if (probing && !(e.flags & PK_EMPTY)) ld_slot(slot, k, v, P.hot != nullptr);
+    if (probing && !(e.flags & PK_EMPTY)) ld_slot(slot, k, v);
     if (special) v = *(volatile u64 *)&P.counters[CTR_SPECIAL];
     // ---- lanes that will try to claim reserve their claim index first
     const bool attempt = (probing && key_is_empty(k)) || (special && v == VAL_EMPTY);
@@ -316,47 +283,7 @@ __device__ __forceinline__ void drain_round(const NarrowParams &P, Parked *queue
 // `known[r]`: the candidate equals one of its operands, i.e. a CM already in the cache -- a
 // duplicate by construction, no probe.  `ord_of(r)` recomputes the ordinal where one is
 // needed, so ordinals hold no registers in the hot loop.
-// The hot set: most duplicates are duplicates of LOW cost levels (tools/dup_profile.py: at cost
-// 14 of the paper's example 66 % of all candidates repeat a CM of cost <= 11, 2.7 MB of keys),
-// so those levels' keys are kept a second time in a small open-addressing table of bare 16-byte
-// keys that stays L2 (and partly L1) resident.  It is read-only while a level is enumerated --
-// plain cached loads, no atomics -- and a hit means "duplicate of an earlier level", which is
-// all a duplicate needs to know: the multi-GB main set in HBM is then probed only by the
-// candidates that miss here.  Sets known[r] for hits.
-__device__ __forceinline__ void hot_filter(const NarrowParams &P, const uint4 (&cand)[PROBE_BATCH], const uint32_t (&hash)[PROBE_BATCH],
-                                           const bool (&live)[PROBE_BATCH], bool (&known)[PROBE_BATCH]) {
-    if (P.hot == nullptr) return;
-    const u64 keep = l2_policy_evict_last();
-    uint32_t s[PROBE_BATCH];
-    uint4 k[PROBE_BATCH];
-    bool pend[PROBE_BATCH];
-#pragma unroll
-    for (int r = 0; r < PROBE_BATCH; ++r) {
-        pend[r] = live[r] && !known[r];
-        s[r] = hash[r] & P.hot_mask;
-        if (pend[r]) k[r] = ld_hot(&P.hot[s[r]], keep);
-    }
-    bool again;
-    do {
-        again = false;
-#pragma unroll
-        for (int r = 0; r < PROBE_BATCH; ++r) {
-            if (!pend[r]) continue;
-            if (key_is_empty(k[r])) {  // (first: the all-ones CM looks like an empty slot and is never in here)
-                pend[r] = false;
-            } else if (v_eq(k[r], cand[r])) {
-                known[r] = true;
-                pend[r] = false;
-            } else {  // another key: linear probing (usually the other half of the same sector)
-                s[r] = (s[r] + 1) & P.hot_mask;
-                k[r] = ld_hot(&P.hot[s[r]], keep);
-                again = true;
-            }
-        }
-    } while (again);
-}
-
-template <int LW, bool HOT, typename OrdOf>
+template <int LW, typename OrdOf>
 __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queue, WarpState &st,
                                              const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
                                              const bool (&known_in)[PROBE_BATCH], OrdOf ord_of) {
@@ -373,11 +300,10 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queu
         slot[r] = hash_vec(cand[r], 0u);
         known[r] = known_in[r];
     }
-    if constexpr (HOT && LTLB200_ENABLE_HOT) hot_filter(P, cand, slot, live, known);
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
         slot[r] &= mask32;
-        if (live[r] && !known[r]) ld_slot(&P.slots[slot[r]], k0[r], v0[r], P.hot != nullptr);
+        if (live[r] && !known[r]) ld_slot(&P.slots[slot[r]], k0[r], v0[r]);
     }
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
@@ -562,7 +488,7 @@ struct DirectSink {
     template <int LW, typename OrdOf>
     __device__ __forceinline__ void emit(const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
                                          const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
-        insert_batch<LW, true>(P, ws.queue, st, cand, live, known, ord_of);
+        insert_batch<LW>(P, ws.queue, st, cand, live, known, ord_of);
     }
 };
 
@@ -656,6 +582,36 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_level_ke
         while (st.qfill > 0u) drain_round(P, ws.queue, st);
 }
 
+// Small levels: ONE launch covers every operator (the operator is a run-time switch per tile).
+// The per-operator kernels exist because a single hot loop needs fewer registers; a level of a
+// few thousand candidates is pure launch latency instead, and five launches cost five times it.
+template <int LW>
+__global__ void __launch_bounds__(CTA_THREADS, 1) narrow_small_level_kernel(const NarrowParams P) {
+    __shared__ WarpShared s_warp[WARPS_PER_CTA];
+    WarpShared &ws = s_warp[threadIdx.x >> 5];
+    WarpState st;
+    DirectSink sink{P, ws, st};
+    TileFetch next = fetch_tile(P, nullptr);
+    for (;;) {
+        const TileFetch cur = next;
+        if (!open_tile(P, ws, cur)) break;
+        next = fetch_tile(P, nullptr);
+        bool stop;
+        switch (ws.block.op) {
+            case OP_ATOM: stop = run_tile<LW, OP_ATOM>(P, ws, sink); break;
+            case OP_NOT: stop = run_tile<LW, OP_NOT>(P, ws, sink); break;
+            case OP_NEXT: stop = run_tile<LW, OP_NEXT>(P, ws, sink); break;
+            case OP_FUTURE: stop = run_tile<LW, OP_FUTURE>(P, ws, sink); break;
+            case OP_AND: stop = run_tile<LW, OP_AND>(P, ws, sink); break;
+            case OP_UNTIL: stop = run_tile<LW, OP_UNTIL>(P, ws, sink); break;
+            default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
+        }
+        if (stop) break;
+    }
+    if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+        while (st.qfill > 0u) drain_round(P, ws.queue, st);
+}
+
 // ---- finalisation: order the level's winners by ordinal without a sort -------------
 // A bitmap with one bit per candidate ordinal marks the winners; a popcount prefix over
 // 1024-bit superblocks turns an ordinal into its rank, i.e. the entry's position in the
@@ -671,12 +627,32 @@ struct FinalizeParams {
     uint4 *store;
     u64 *ords;
     u64 base;  // global id of the level's first entry
+    // Deferred mode (live != NULL): the host has not read the level's counters yet -- it launched
+    // the finalisation right behind the enumeration, one synchronisation per level instead of
+    // two -- so the claim count, the separator and the overflow flag are read here.
+    const u64 *live;
+    u64 claim_cap;
+    int cut_allowed;  // non-exhaustive: keep only ordinals <= the separator
 };
 
+// resolves n_claimed / ord_limit in deferred mode; false = the level overflowed and is redone
+__device__ __forceinline__ bool finalize_bounds(const FinalizeParams &F, u64 &n_claimed, u64 &ord_limit) {
+    n_claimed = F.n_claimed;
+    ord_limit = F.ord_limit;
+    if (F.live == nullptr) return true;
+    if (F.live[CTR_OVERFLOW]) return false;
+    const u64 claimed = F.live[CTR_CLAIMED], sep = F.live[CTR_SEP];
+    n_claimed = claimed < F.claim_cap ? claimed : F.claim_cap;
+    ord_limit = (F.cut_allowed && sep != VAL_EMPTY) ? sep : VAL_EMPTY - 1;
+    return true;
+}
+
 __global__ void __launch_bounds__(256) narrow_mark_kernel(const FinalizeParams F) {
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < F.n_claimed; t += (u64)gridDim.x * blockDim.x) {
+    u64 n_claimed, ord_limit;
+    if (!finalize_bounds(F, n_claimed, ord_limit)) return;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
         const u64 ord = F.claim_ord[t];
-        if (ord <= F.ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
+        if (ord <= ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
     }
 }
 
@@ -688,9 +664,11 @@ __device__ __forceinline__ u64 ordinal_rank(const uint32_t *bitmap, const uint32
 }
 
 __global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParams F) {
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < F.n_claimed; t += (u64)gridDim.x * blockDim.x) {
+    u64 n_claimed, ord_limit;
+    if (!finalize_bounds(F, n_claimed, ord_limit)) return;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
         const u64 ord = F.claim_ord[t];
-        if (ord > F.ord_limit) continue;  // unused index, or ordered after the separator
+        if (ord > ord_limit) continue;  // unused index, or ordered after the separator
         const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
         F.store[gid] = F.claim_key[t];
         F.ords[gid] = ord;
@@ -716,22 +694,6 @@ __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 
                 break;
             }
             slot = (slot + 1) & slot_mask;
-        }
-    }
-}
-
-// add finalised rows [first, first+count) to the hot set (bare keys; the all-ones CM stays out:
-// it is the empty marker, and takes the main set's side register as always)
-__global__ void __launch_bounds__(256) hot_insert_kernel(uint4 *hot, uint32_t hot_mask, const uint4 *store, u64 first, u64 count) {
-    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (u64)gridDim.x * blockDim.x) {
-        const uint4 key = store[first + t];
-        if (key_is_empty(key)) continue;
-        uint32_t slot = hash_vec(key, 0u) & hot_mask;
-        for (;;) {
-            const uint4 old = cas128(&hot[slot], empty, key);
-            if (key_is_empty(old) || v_eq(old, key)) break;
-            slot = (slot + 1) & hot_mask;
         }
     }
 }

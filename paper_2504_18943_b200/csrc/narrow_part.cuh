@@ -189,7 +189,6 @@ struct PartSink {
             hash[r] = hash_vec(cand[r], 0u);
             known[r] = known_in[r];
         }
-        if constexpr (LTLB200_ENABLE_HOT) hot_filter(P, cand, hash, live, known);  // duplicates of the low levels never reach the pool
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
             const bool sep = cm_sep_diff<LW>(cand[r], P.target) == 0u;
@@ -401,7 +400,7 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_PROBE_MIN_CTAS) narrow_pr
             if (step + 1 < STEPS) probe_load(Q, T, step + 1, nxt);
             const bool known[PROBE_BATCH] = {};
             auto ord_of = [&](int r) { return cur.ords[r]; };
-            insert_batch<LW, false>(P, queue, st, cur.cand, cur.live, known, ord_of);  // phase A applied the hot set already
+            insert_batch<LW>(P, queue, st, cur.cand, cur.live, known, ord_of);
             cur = nxt;
         }
         T = next;
