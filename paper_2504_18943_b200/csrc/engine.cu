@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -490,7 +491,9 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     : T_(T), lw_(lane_bits), row_bytes_(T * lane_bits / 8), key_words_((T * lane_bits / 8 + 7) / 8), n_atoms_(n_atoms),
       device_(device) {
     const double t_create = monotonic_s();
+    double tp = monotonic_s();
     CUDA_CHECK(cudaSetDevice(device_));
+    PHASE(8, "create: set device", tp);
     const DeviceInfo info = device_info(device_);
     if (!info.known) throw CudaError("cannot query the CUDA device");
     if (info.major != 10) throw CudaError("device is not sm_100 (Blackwell B200); this library has no other code path");
@@ -504,27 +507,23 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
         CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
         own_stream_ = true;
     }
+    PHASE(9, "create: stream", tp);
     if (budget) budget_ = budget;
-    else {  // 90% of what is free now, counting blocks parked in the process-wide cache as free
-        size_t free_b = 0, total_b = 0;
-        CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-        budget_ = (u64)((free_b + g_blocks.cached(device_)) * 0.9);
+    else {  // 90% of what was free when this process first asked (cudaMemGetInfo costs milliseconds once
+            // gigabytes are mapped, and everything this library holds is either in use by a live
+            // handle -- counted in held_ -- or parked in the process-wide block cache)
+        static std::mutex mu;
+        static std::map<int, u64> free_at_start;
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = free_at_start.find(device_);
+        if (it == free_at_start.end()) {
+            size_t free_b = 0, total_b = 0;
+            CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            it = free_at_start.emplace(device_, (u64)free_b + g_blocks.cached(device_)).first;
+        }
+        budget_ = (u64)(it->second * 0.9);
     }
-    std::vector<uint4> h_valid(nvec_), h_target(nvec_);
-    pack_row(masks, T, lane_bits, nvec_, h_valid.data());
-    pack_row(target, T, lane_bits, nvec_, h_target.data());
-    valid_ = h_valid[0];
-    target_ = h_target[0];
-    // the all-ones vector doubles as the empty-slot marker; it is a legal CM only when
-    // the row fills the vector and every lane is fully valid
-    special_possible_ = (valid_.x & valid_.y & valid_.z & valid_.w) == 0xFFFFFFFFu;
-
-    // one small block: counters | block descriptors | masks | target | atom rows
-    const u64 off_blocks = 256, off_rows = off_blocks + kMaxBlocks * sizeof(BlockDesc);
-    std::vector<uint4> h_rows((size_t)(2 + std::max(n_atoms, 1)) * nvec_);
-    memcpy(h_rows.data(), h_valid.data(), (size_t)nvec_ * 16);
-    memcpy(h_rows.data() + nvec_, h_target.data(), (size_t)nvec_ * 16);
-    for (int p = 0; p < n_atoms; ++p) pack_row(atoms + (size_t)p * T, T, lane_bits, nvec_, h_rows.data() + (size_t)(2 + p) * nvec_);
+    PHASE(10, "create: mem info", tp);
     reserve(misc_, off_rows + h_rows.size() * sizeof(uint4), false);
     d_counters_ = reinterpret_cast<u64 *>(misc_.ptr);
     d_blocks_ = reinterpret_cast<BlockDesc *>(misc_.ptr + off_blocks);
@@ -540,10 +539,24 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     init[CTR_SPECIAL] = VAL_EMPTY;
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_rows / init leave scope
-    occupancy_ = wide_ ? 4 : (lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>());
-    if (!wide_ && async_enabled())
-        occupancy_ = lw_ == 8 ? async_occupancy_of<8>() : lw_ == 16 ? async_occupancy_of<16>() : lw_ == 32 ? async_occupancy_of<32>() : async_occupancy_of<64>();
-    if (!wide_) part_occupancy_ = lw_ == 8 ? part_occupancy_of<8>() : lw_ == 16 ? part_occupancy_of<16>() : lw_ == 32 ? part_occupancy_of<32>() : part_occupancy_of<64>();
+    PHASE(11, "create: copies + sync", tp);
+    {   // occupancy queries (and the dynamic-shared-memory opt-ins they need) once per process, device and lane width
+        static std::mutex mu;
+        static std::map<std::pair<int, int>, std::array<int, 3>> cache;
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find({device_, lw_});
+        if (it == cache.end()) {
+            std::array<int, 3> occ{4, 2, 2};
+            if (!wide_) {
+                occ[0] = lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>();
+                occ[1] = lw_ == 8 ? async_occupancy_of<8>() : lw_ == 16 ? async_occupancy_of<16>() : lw_ == 32 ? async_occupancy_of<32>() : async_occupancy_of<64>();
+                occ[2] = lw_ == 8 ? part_occupancy_of<8>() : lw_ == 16 ? part_occupancy_of<16>() : lw_ == 32 ? part_occupancy_of<32>() : part_occupancy_of<64>();
+            }
+            it = cache.emplace(std::make_pair(device_, lw_), occ).first;
+        }
+        occupancy_ = wide_ ? 4 : (async_enabled() ? it->second[1] : it->second[0]);
+        part_occupancy_ = it->second[2];
+    }
     rebuild_table(kMinSlots);
     st_.row_bytes = row_bytes_;
     st_.key_bytes = 16 * nvec_;

@@ -1,0 +1,43 @@
+"""GPU parity of the alternative narrow-path kernels.
+
+The engine chooses its kernel path per level by size; the alternatives are selected with
+environment switches that the library reads once per process, so each variant runs the parity
+cases in a child process:
+
+  LTLB200_PARTITION=1   radix-partitioned dedup for EVERY level (narrow_part.cuh)
+  LTLB200_ASYNC=1       cp.async probe pipeline (narrow_async.cuh)
+  LTLB200_NO_DEFER=1    two synchronisations per level (finalisation launched after the counters
+                        were read) instead of the deferred, device-bounded finalisation
+
+Every variant must reproduce the golden fixtures of the unmodified reference bit for bit.
+"""
+
+import os
+import pathlib
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+CASES = ["spec1_found", "spec1_exh10", "spec2_exh11", "c1_s1", "c3_s0_exh12", "c3_s1_found", "spec2_fuo_exh8"]
+
+CHILD = """
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import test_gpu_parity as t
+for name in {cases!r}:
+    t._run_case(name)
+print("variant ok")
+"""
+
+
+@pytest.mark.parametrize("switch", ["LTLB200_PARTITION", "LTLB200_ASYNC", "LTLB200_NO_DEFER"])
+def test_variant_matches_reference(switch):
+    env = dict(os.environ)
+    env[switch] = "1"
+    code = CHILD.format(root=str(ROOT), tests=str(ROOT / "tests"), cases=CASES)
+    proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0 and "variant ok" in proc.stdout, proc.stdout[-2000:] + proc.stderr[-4000:]
