@@ -272,6 +272,27 @@ def main() -> int:
     peak, peak_src = measured_peaks()
     alg_bytes = algorithmic_bytes(key_bytes, constructed_per_step, unique_per_step, unary)
     achieved = alg_bytes / (enum_ms * 1e-3) / 1e9 if enum_ms > 0 else 0.0
+    # DRAM bytes the enumerate kernels actually moved in one search: from the committed ncu pass of
+    # this workload (dram__bytes_read.sum + dram__bytes_write.sum summed over the enumerate launches)
+    traffic, traffic_src = None, None
+    prof = ROOT / "profiles" / f"r01_s2_dram_{args.workload}.json"
+    if prof.exists():
+        pj = json.loads(prof.read_text())
+        traffic, traffic_src = pj["enumerate_dram_bytes"], f"profiles/{prof.name} (bytes per search over {pj['enumerate_launches']} enumerate launches)"
+    # measured ceiling of the probe's access pattern on this device (random 32-byte slots, 256-bit loads)
+    probe = None
+    tool = ROOT / "tools" / "random_probe_bench"
+    if tool.exists():
+        try:
+            mb = max(128, int(table_slots * 32 >> 20))
+            out = subprocess.run([str(tool), str(mb)], capture_output=True, text=True, timeout=60).stdout
+            rates = [float(line.split(":")[1].split()[0]) for line in out.splitlines() if "probes/ns" in line]
+            if rates:
+                probes_per_step = constructed_per_step  # at most one first probe per candidate
+                probe = {"table_mb": mb, "ceiling_probes_per_ns": max(rates),
+                         "kernel_candidates_per_ns": probes_per_step / (enum_ms * 1e6) if enum_ms > 0 else None}
+        except (OSError, subprocess.SubprocessError, ValueError):
+            probe = None
     line = {
         "metric": METRIC,
         "value": total_unique * args.steps / (device_ms * 1e-3),
@@ -308,12 +329,16 @@ def main() -> int:
         "clocks": clocks.summary(),
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None,
-            "kernel": "narrow_level_kernel<lane_bits, op> (construction + separation check + hash-set dedup)",
+            "traffic": traffic,
+            "kernel": ("narrow_level_kernel<lane_bits, op> + narrow_small_level_kernel (construction + separation check + "
+                       "hash-set dedup)") if key_bytes == 16 else "wide_level_kernel<lane_bits, op>",
             "launches_per_step": int(enum_launches), "kernel_ms_per_step": enum_ms, "finalize_ms_per_step": fin_ms,
             "algorithmic_bytes_per_step": alg_bytes, "peak_source": peak_src,
-            "note": "probes are random 32-byte sectors; the measured ceiling for that access pattern on this "
-                    "part is ~19.9 sectors/ns (tools/random_probe_bench.cu), far below the copy peak used here",
+            "traffic_source": traffic_src,
+            "random_probe": probe,
+            "note": "the dedup probe is one random 32-byte sector per candidate; the ceiling for that access pattern "
+                    "(tools/random_probe_bench.cu, 37-40 probes/ns = 1.2 TB/s of useful sectors for 2-8 GiB tables) is "
+                    "what bounds the kernel, not the copy bandwidth used as `peak`",
         },
     }
     if not args.no_cpu_baseline:

@@ -56,6 +56,20 @@ def build_native(force: bool = False, verbose: bool = False, defines=(), out: pa
     return target
 
 
+def build_tools() -> None:
+    """Measurement tools (not part of the product path): the random-probe ceiling microbenchmark
+    that bench.py runs beside the kernel."""
+    root = PKG.parent / "tools"
+    for name in ("random_probe_bench", "window_probe_bench"):
+        src, exe = root / f"{name}.cu", root / name
+        if exe.exists() and exe.stat().st_mtime >= src.stat().st_mtime:
+            continue
+        proc = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", str(exe), str(src)],
+                              capture_output=True, text=True)
+        if proc.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + proc.stdout + proc.stderr)
+
+
 if __name__ == "__main__":
     import sys
 

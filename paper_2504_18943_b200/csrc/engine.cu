@@ -524,6 +524,21 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
         budget_ = (u64)(it->second * 0.9);
     }
     PHASE(10, "create: mem info", tp);
+    std::vector<uint4> h_valid(nvec_), h_target(nvec_);
+    pack_row(masks, T, lane_bits, nvec_, h_valid.data());
+    pack_row(target, T, lane_bits, nvec_, h_target.data());
+    valid_ = h_valid[0];
+    target_ = h_target[0];
+    // the all-ones vector doubles as the empty-slot marker; it is a legal CM only when
+    // the row fills the vector and every lane is fully valid
+    special_possible_ = (valid_.x & valid_.y & valid_.z & valid_.w) == 0xFFFFFFFFu;
+
+    // one small block: counters | block descriptors | masks | target | atom rows
+    const u64 off_blocks = 256, off_rows = off_blocks + kMaxBlocks * sizeof(BlockDesc);
+    std::vector<uint4> h_rows((size_t)(2 + std::max(n_atoms, 1)) * nvec_);
+    memcpy(h_rows.data(), h_valid.data(), (size_t)nvec_ * 16);
+    memcpy(h_rows.data() + nvec_, h_target.data(), (size_t)nvec_ * 16);
+    for (int p = 0; p < n_atoms; ++p) pack_row(atoms + (size_t)p * T, T, lane_bits, nvec_, h_rows.data() + (size_t)(2 + p) * nvec_);
     reserve(misc_, off_rows + h_rows.size() * sizeof(uint4), false);
     d_counters_ = reinterpret_cast<u64 *>(misc_.ptr);
     d_blocks_ = reinterpret_cast<BlockDesc *>(misc_.ptr + off_blocks);
@@ -677,8 +692,13 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
     // A block is cut into at least ~4 tiles per resident warp so that small levels still
     // spread over the whole GPU instead of a few warps grinding through full-size tiles.
     const u64 want_tiles = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * 4;
+    // ... but not below ~1024 candidates (8 probe batches) while that still leaves every warp a
+    // tile: a ticket costs a global atomic, and the first ncu capture of mid-size levels had 28 %
+    // of its stall samples waiting on one ticket per 256 candidates.
+    const u64 resident_warps = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA;
     auto tile_candidates = [&](u64 size) {
-        u64 per = std::max<u64>(size / want_tiles, tile_v * 4);
+        const u64 floor_per = wide_ ? tile_v * 4 : std::max<u64>(tile_v * 4, std::min<u64>(1024, size / resident_warps));
+        u64 per = std::max<u64>(size / want_tiles, floor_per);
         return std::min<u64>(next_pow2(per), tile_max);
     };
     auto ceil_div = [](u64 a, u64 b) { return (a + b - 1) / b; };

@@ -5,6 +5,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/random_probe_bench tools/random_probe_bench.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 typedef unsigned long long u64;
 
@@ -46,8 +47,18 @@ void run(const uint4* t, u64 slots, int ctas_per_sm, uint32_t* out) {
            U * ctas_per_sm * threads, n / (ms * 1e6));
 }
 
-int main() {
+int main(int argc, char** argv) {
     uint32_t* out; cudaMalloc(&out, 4);
+    if (argc > 1) {  // one table size (MiB, rounded up to a power of two), two occupancies
+        u64 slots = 1;
+        while (slots * 32 < (u64)atoll(argv[1]) << 20) slots <<= 1;
+        uint4* t;
+        if (cudaMalloc(&t, slots * 32) != cudaSuccess) return 1;
+        cudaMemset(t, 1, slots * 32);
+        run<4>(t, slots, 4, out);
+        run<8>(t, slots, 8, out);
+        return 0;
+    }
     for (u64 slots : {1ull << 22, 1ull << 24, 1ull << 25, 1ull << 26, 1ull << 27, 1ull << 28}) {
         uint4* t;
         if (cudaMalloc(&t, slots * 32) != cudaSuccess) break;
