@@ -48,6 +48,9 @@ UNIT = "unique CS/s"
 WORKLOADS = {
     "spec2": dict(max_cost=16, exhaustive=False, cpu_max_cost=13),
     "c3": dict(max_cost=13, exhaustive=True, cpu_max_cost=11),
+    # BASELINE configs[2]: "<= 128-bit CS, enumerated until the cache fills HBM on 1 GPU": cost 17 stores 639 M CMs
+    # (100 GB); cost 18 would need a hash set beyond 2^32 slots and ends the run with "memory budget exhausted"
+    "c3-fill": dict(max_cost=18, exhaustive=True, cpu_max_cost=11, base="c3"),
     "c1": dict(max_cost=14, exhaustive=False, cpu_max_cost=14),
     "spec1": dict(max_cost=10, exhaustive=True, cpu_max_cost=10),
     "c5": dict(max_cost=10, exhaustive=True, cpu_max_cost=9),
@@ -116,7 +119,7 @@ def run_reference(args, rank: int) -> int:
     from paper_2504_18943_b200 import workloads
 
     cfg = WORKLOADS[args.workload]
-    spec = workloads.named_workload(args.workload, args.seed)
+    spec = workloads.named_workload(cfg.get("base", args.workload), args.seed)
     oracle.build()
     times, last = [], None
     for step in range(args.warmup + args.steps):
@@ -198,7 +201,7 @@ def main() -> int:
     wl = WORKLOADS[args.workload]
     # N > 1: ONE search whose pair space is sharded over the ranks, one exchange per level
     # (route claims to hash owners, all-gather winners, min-reduce the separator): strong scaling.
-    spec = workloads.named_workload(args.workload, args.seed)
+    spec = workloads.named_workload(wl.get("base", args.workload), args.seed)
     cfg = engine.EngineConfig(max_cost=wl["max_cost"], exhaustive=wl["exhaustive"], time_budget_s=3600.0,
                               memory_budget_mb=1 << 20, device=local_rank)
     stream = torch.cuda.current_stream()
@@ -211,10 +214,13 @@ def main() -> int:
         stats = engine.RunStats()
         found = None
         for cost in range(1, cfg.max_cost + 1):
-            if distributed:
-                _, sep = pdist.sharded_expand_level(store, cost, cfg.operators, cfg, stats)
-            else:
-                _, sep = engine.expand_level(store, cost, cfg.operators, config=cfg, stats=stats)
+            try:
+                if distributed:
+                    _, sep = pdist.sharded_expand_level(store, cost, cfg.operators, cfg, stats)
+                else:
+                    _, sep = engine.expand_level(store, cost, cfg.operators, config=cfg, stats=stats)
+            except engine._BudgetExceeded:  # the cache filled the device: the search ends here (outcome "exhausted")
+                break
             if sep is not None and found is None:
                 found = (sep, cost)
                 if not cfg.exhaustive:
@@ -346,7 +352,7 @@ def main() -> int:
 
         oracle.build()
         t0 = time.perf_counter()
-        ref = oracle.synthesize(workloads.named_workload(args.workload, args.seed), max_cost=wl["cpu_max_cost"],
+        ref = oracle.synthesize(workloads.named_workload(wl.get("base", args.workload), args.seed), max_cost=wl["cpu_max_cost"],
                                 exhaustive=wl["exhaustive"], time_budget_s=3600.0, memory_budget_mb=1 << 20)
         cpu_s = time.perf_counter() - t0
         line["cpu_baseline"] = {
