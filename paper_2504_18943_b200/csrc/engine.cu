@@ -569,7 +569,7 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
             }
             it = cache.emplace(std::make_pair(device_, lw_), occ).first;
         }
-        occupancy_ = wide_ ? 4 : (async_enabled() ? it->second[1] : it->second[0]);
+        occupancy_ = wide_ ? LTLB200_WIDE_MIN_CTAS : (async_enabled() ? it->second[1] : it->second[0]);
         part_occupancy_ = it->second[2];
     }
     rebuild_table(kMinSlots);
@@ -1022,6 +1022,25 @@ void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
 }
 
 void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
+    const BlockDesc &last_block = lv.blocks.back();
+    if (last_block.ord0 + last_block.size <= kSmallLevel / 4) {  // (a wide candidate is several vectors of work)
+        P.block_begin = 0;
+        P.block_end = (int)lv.blocks.size();
+        P.tile_begin = 0;
+        P.tile_end = last_block.tile0 + last_block.tiles_v * last_block.tiles_s;
+        P.ticket = CTR_TICKET0;
+        const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
+        switch (lw_) {
+            case 8: wide_small_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            case 16: wide_small_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            case 32: wide_small_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            default: wide_small_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+        }
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+        st_.enumerate_launches++;
+        return;
+    }
     for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid) {
         switch (lw_) {
             case 8: launch_op_wide<8>(op, Q, grid, stream_); break;

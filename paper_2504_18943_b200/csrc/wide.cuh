@@ -28,6 +28,12 @@ namespace ltlb200 {
 constexpr int WIDE_ROW_VECS = 256;   // uint4 vectors of scalar-operand rows staged per warp (4 KiB)
 constexpr int WIDE_TERMS = 128;      // max scalar rows per tile (G = 2)
 constexpr int WIDE_CHUNK = 16;       // staging entries a group reserves at a time
+// CTAs per SM of the wide kernel.  Unlike the narrow kernel it wants resident warps more than
+// registers (every batch is a chain probe -> row write + fence -> CAS): c5 enumerate time per
+// search with 3 / 4 / 6 / 8 / 10 CTAs per SM = 3.76 / 3.06 / 2.65 / 2.58 / 2.86 ms.
+#ifndef LTLB200_WIDE_MIN_CTAS
+#define LTLB200_WIDE_MIN_CTAS 6
+#endif
 #ifndef LTLB200_WIDE_BATCH
 #define LTLB200_WIDE_BATCH 2
 #endif
@@ -406,10 +412,8 @@ __device__ __forceinline__ void wide_binary_tile(const WideParams &P, WideWarpSh
     }
 }
 
-template <int LW, int OP>
-__global__ void __launch_bounds__(CTA_THREADS, 4) wide_level_kernel(const __grid_constant__ WideParams P) {
-    __shared__ WideWarpShared s_warp[WARPS_PER_CTA];
-    WideWarpShared &ws = s_warp[threadIdx.x >> 5];
+// group geometry of the calling lane
+__device__ __forceinline__ GroupGeom wide_geometry(const WideParams &P) {
     const int lane = threadIdx.x & 31;
     const int G = 1 << P.log2g;
     GroupGeom g;
@@ -418,34 +422,72 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) wide_level_kernel(const __grid
     g.leader = g.base;
     g.has_part = g.part < P.nvec;
     g.mask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << g.base;
+    return g;
+}
+
+// draws the warp's next tile (lane 0 takes a ticket) and loads its block descriptor
+__device__ __forceinline__ bool wide_next_tile(const WideParams &P, WideWarpShared &ws) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    if (lane == 0) {
+        u64 t = P.tile_end;
+        if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+            t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
+        ws.ticket = t;
+        ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
+        if (t < P.tile_end) {
+            int bi = P.block_begin;
+            while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
+            ws.block = P.blocks[bi];
+        }
+    }
+    __syncwarp();
+    return ws.ticket < P.tile_end;
+}
+
+template <int LW, int OP>
+__device__ __forceinline__ void wide_run_tile(const WideParams &P, WideWarpShared &ws, const GroupGeom &g, GroupState &gs,
+                                              uint4 valid, uint4 target) {
+    const u64 sep_now = ws.sep_now;
+    if (ws.block.ord0 > sep_now) return;
+    const u64 tile_local = ws.ticket - ws.block.tile0;
+    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
+        if (ws.block.vec_is_b) wide_binary_tile<LW, OP, true>(P, ws, g, gs, valid, target, tile_local, sep_now);
+        else wide_binary_tile<LW, OP, false>(P, ws, g, gs, valid, target, tile_local, sep_now);
+    } else {
+        wide_unary_tile<LW, OP>(P, ws, g, gs, valid, target, tile_local, sep_now);
+    }
+}
+
+template <int LW, int OP>
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_WIDE_MIN_CTAS) wide_level_kernel(const __grid_constant__ WideParams P) {
+    __shared__ WideWarpShared s_warp[WARPS_PER_CTA];
+    WideWarpShared &ws = s_warp[threadIdx.x >> 5];
+    const GroupGeom g = wide_geometry(P);
     GroupState gs;
     const uint4 valid = g.has_part ? P.valid[g.part] : make_uint4(0, 0, 0, 0);
     const uint4 target = g.has_part ? P.target[g.part] : make_uint4(0, 0, 0, 0);
-    for (;;) {
-        __syncwarp();
-        if (lane == 0) {
-            u64 t = P.tile_end;
-            if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
-                t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
-            ws.ticket = t;
-            ws.sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
-            if (t < P.tile_end) {
-                int bi = P.block_begin;
-                while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
-                ws.block = P.blocks[bi];
-            }
-        }
-        __syncwarp();
-        const u64 tile = ws.ticket;
-        const u64 sep_now = ws.sep_now;
-        if (tile >= P.tile_end) break;
-        if (ws.block.ord0 > sep_now) continue;
-        const u64 tile_local = tile - ws.block.tile0;
-        if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
-            if (ws.block.vec_is_b) wide_binary_tile<LW, OP, true>(P, ws, g, gs, valid, target, tile_local, sep_now);
-            else wide_binary_tile<LW, OP, false>(P, ws, g, gs, valid, target, tile_local, sep_now);
-        } else {
-            wide_unary_tile<LW, OP>(P, ws, g, gs, valid, target, tile_local, sep_now);
+    while (wide_next_tile(P, ws)) wide_run_tile<LW, OP>(P, ws, g, gs, valid, target);
+}
+
+// Small levels: one launch for every operator (run-time switch per tile), as in the narrow path.
+template <int LW>
+__global__ void __launch_bounds__(CTA_THREADS, 1) wide_small_level_kernel(const __grid_constant__ WideParams P) {
+    __shared__ WideWarpShared s_warp[WARPS_PER_CTA];
+    WideWarpShared &ws = s_warp[threadIdx.x >> 5];
+    const GroupGeom g = wide_geometry(P);
+    GroupState gs;
+    const uint4 valid = g.has_part ? P.valid[g.part] : make_uint4(0, 0, 0, 0);
+    const uint4 target = g.has_part ? P.target[g.part] : make_uint4(0, 0, 0, 0);
+    while (wide_next_tile(P, ws)) {
+        switch (ws.block.op) {
+            case OP_ATOM: wide_run_tile<LW, OP_ATOM>(P, ws, g, gs, valid, target); break;
+            case OP_NOT: wide_run_tile<LW, OP_NOT>(P, ws, g, gs, valid, target); break;
+            case OP_NEXT: wide_run_tile<LW, OP_NEXT>(P, ws, g, gs, valid, target); break;
+            case OP_FUTURE: wide_run_tile<LW, OP_FUTURE>(P, ws, g, gs, valid, target); break;
+            case OP_AND: wide_run_tile<LW, OP_AND>(P, ws, g, gs, valid, target); break;
+            case OP_UNTIL: wide_run_tile<LW, OP_UNTIL>(P, ws, g, gs, valid, target); break;
+            default: wide_run_tile<LW, OP_OR>(P, ws, g, gs, valid, target); break;
         }
     }
 }
