@@ -32,6 +32,7 @@
 #include "narrow_async.cuh"
 #include "narrow_part.cuh"
 #include "wide.cuh"
+#include "wide2.cuh"
 
 namespace ltlb200 {
 
@@ -317,6 +318,7 @@ private:
     uint4 valid_{}, target_{};
     bool special_possible_ = false;
     bool wide_ = false;  // CMs of more than one uint4
+    bool wide2_ = false; // ... enumerated by the lane-per-candidate kernel (wide2.cuh) instead of wide.cuh's groups
     int nvec_ = 1, log2g_ = 0;
     uint4 *d_valid_ = nullptr, *d_target_ = nullptr;
 
@@ -469,6 +471,9 @@ static int part_occupancy_of();
 template <int LW>
 static int async_occupancy_of();
 static bool async_enabled();
+template <int LW>
+static int wide2_occupancy_of(int nvec);
+static bool wide2_enabled();
 
 template <int LW>
 static int occupancy_of() {
@@ -570,6 +575,8 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
             it = cache.emplace(std::make_pair(device_, lw_), occ).first;
         }
         occupancy_ = wide_ ? LTLB200_WIDE_MIN_CTAS : (async_enabled() ? it->second[1] : it->second[0]);
+        wide2_ = wide_ && wide2_enabled();
+        if (wide2_) occupancy_ = lw_ == 8 ? wide2_occupancy_of<8>(nvec_) : lw_ == 16 ? wide2_occupancy_of<16>(nvec_) : lw_ == 32 ? wide2_occupancy_of<32>(nvec_) : wide2_occupancy_of<64>(nvec_);
         part_occupancy_ = it->second[2];
     }
     rebuild_table(kMinSlots);
@@ -686,9 +693,9 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
     constructed = 0;
     n_tiles = 0;
     // tile geometry: narrow = one lane per vector row; wide = one group of G lanes per vector row
-    const u64 tile_v = wide_ ? (u64)(32 >> log2g_) : (u64)TILE_V;
-    const u64 tile_s_max = wide_ ? (u64)(WIDE_ROW_VECS >> log2g_) : (u64)TILE_S;
-    const u64 tile_max = wide_ ? 2048 : (u64)TILE_V * TILE_S;  // candidates of a full-size tile
+    const u64 tile_v = (wide_ && !wide2_) ? (u64)(32 >> log2g_) : (u64)TILE_V;
+    const u64 tile_s_max = wide2_ ? (u64)wide2_tile_s(nvec_) : wide_ ? (u64)(WIDE_ROW_VECS >> log2g_) : (u64)TILE_S;
+    const u64 tile_max = (wide_ && !wide2_) ? 2048 : (u64)TILE_V * TILE_S;  // candidates of a full-size tile
     // A block is cut into at least ~4 tiles per resident warp so that small levels still
     // spread over the whole GPU instead of a few warps grinding through full-size tiles.
     const u64 want_tiles = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * 4;
@@ -1021,7 +1028,93 @@ void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
     });
 }
 
+// ---- wide2: lane-per-candidate kernel --------------------------------------------------------
+
+static size_t wide2_smem_bytes(int nvec) { return wide2_warp_vecs(nvec) * sizeof(uint4) * WARPS_PER_CTA; }
+
+template <int LW, int OP>
+static void launch_wide2_instance(const WideParams &P, int grid, size_t smem, cudaStream_t st) {
+    static std::once_flag once;  // opt in to the largest dynamic shared memory any nvec needs, once per instance
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(wide2_level_kernel<LW, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
+    });
+    wide2_level_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
+}
+
+template <int LW>
+static void launch_wide2_op(int op, const WideParams &P, int grid, size_t smem, cudaStream_t st) {
+    switch (op) {
+        case OP_ATOM: launch_wide2_instance<LW, OP_ATOM>(P, grid, smem, st); break;
+        case OP_NOT: launch_wide2_instance<LW, OP_NOT>(P, grid, smem, st); break;
+        case OP_NEXT: launch_wide2_instance<LW, OP_NEXT>(P, grid, smem, st); break;
+        case OP_FUTURE: launch_wide2_instance<LW, OP_FUTURE>(P, grid, smem, st); break;
+        case OP_AND: launch_wide2_instance<LW, OP_AND>(P, grid, smem, st); break;
+        case OP_UNTIL: launch_wide2_instance<LW, OP_UNTIL>(P, grid, smem, st); break;
+        default: launch_wide2_instance<LW, OP_OR>(P, grid, smem, st); break;
+    }
+}
+
+template <int LW>
+static void launch_wide2_small(const WideParams &P, int grid, size_t smem, cudaStream_t st) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(wide2_small_level_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
+    });
+    wide2_small_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
+}
+
+template <int LW>
+static int wide2_occupancy_of(int nvec) {
+    int occ = 0;
+    cudaFuncSetAttribute(wide2_level_kernel<LW, OP_UNTIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_level_kernel<LW, OP_UNTIL>, CTA_THREADS, wide2_smem_bytes(nvec)) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    return std::max(occ, 1);
+}
+
+// LTLB200_WIDE2=0 selects wide.cuh's group-per-candidate kernel instead of wide2.cuh's lane-per-candidate one.
+static bool wide2_enabled() {
+    static const bool on = [] {
+        const char *env = getenv("LTLB200_WIDE2");
+        return !(env && env[0] == '0');
+    }();
+    return on;
+}
+
 void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
+    if (wide2_) {
+        const size_t smem = wide2_smem_bytes(nvec_);
+        const BlockDesc &last = lv.blocks.back();
+        if (last.ord0 + last.size <= kSmallLevel) {
+            P.block_begin = 0;
+            P.block_end = (int)lv.blocks.size();
+            P.tile_begin = 0;
+            P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
+            P.ticket = CTR_TICKET0;
+            const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
+            switch (lw_) {
+                case 8: launch_wide2_small<8>(P, grid, smem, stream_); break;
+                case 16: launch_wide2_small<16>(P, grid, smem, stream_); break;
+                case 32: launch_wide2_small<32>(P, grid, smem, stream_); break;
+                default: launch_wide2_small<64>(P, grid, smem, stream_); break;
+            }
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+            st_.enumerate_launches++;
+            return;
+        }
+        for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid) {
+            switch (lw_) {
+                case 8: launch_wide2_op<8>(op, Q, grid, smem, stream_); break;
+                case 16: launch_wide2_op<16>(op, Q, grid, smem, stream_); break;
+                case 32: launch_wide2_op<32>(op, Q, grid, smem, stream_); break;
+                default: launch_wide2_op<64>(op, Q, grid, smem, stream_); break;
+            }
+        });
+        return;
+    }
     const BlockDesc &last_block = lv.blocks.back();
     if (last_block.ord0 + last_block.size <= kSmallLevel / 4) {  // (a wide candidate is several vectors of work)
         P.block_begin = 0;
@@ -1285,7 +1378,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             const bool exact = est >= constructed;
             // staging / claim capacity: the estimate plus what warps may over-reserve in flight
             // (wide: every group of every operator launch may end with a partly used chunk of staging entries)
-            const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * (32 >> log2g_) * WIDE_CHUNK * 8 + 1024;
+            const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * std::max<u64>((u64)(32 >> log2g_) * WIDE_CHUNK, CLAIM_CHUNK) * 8 + 1024;
             // (narrow: every warp of every operator launch may end with a partly used chunk of claim indices)
             const u64 narrow_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8 + 1024;
             const u64 claim_cap = est + (wide_ ? wide_slack : narrow_slack);

@@ -1,0 +1,388 @@
+// wide2.cuh -- construction + dedup kernel for multi-vector CMs, one LANE per candidate.
+//
+// wide.cuh gives a candidate to a group of G lanes (one uint4 each).  Its ncu capture on the
+// LTL configuration of BASELINE.json (c5: 128-byte CMs) shows why that is slow: 96 warp
+// instructions per candidate, because everything that is scalar per candidate -- hashing,
+// the slot probe, the claim, the CAS -- runs with 1/G of the lanes, and every step is a
+// group-wide ballot or shuffle.  Here a lane owns a whole candidate, like in the narrow path:
+//
+//   * a tile = 32 vector-operand rows (one per lane) x up to tile_s scalar-operand rows; both are
+//     staged in the warp's shared memory, the vector rows TRANSPOSED (vec[p*32 + lane]) so that
+//     the 32 lanes read 32 consecutive uint4 (no bank conflicts), the scalar rows as they are
+//     (all lanes read the same address: a broadcast);
+//   * a candidate is never held in registers as a whole.  Pass 1 streams over its nvec vectors:
+//     build vector p, fold it into the two row hashes, the separation flag and the
+//     "equals an operand" flags.  Then one 8-byte slot probe.  Then, only for the candidates that
+//     need it, pass 2 streams over the vectors again: a CLAIM writes them to its staging entry,
+//     a fingerprint MATCH compares them with the stored row.  Rebuilding a vector costs a few
+//     dozen integer instructions; keeping 32 rows x nvec vectors in registers is impossible;
+//   * the hash set, the staging pool, the publish protocol (row -> fence -> 64-bit CAS) and the
+//     finalisation are wide.cuh's, unchanged: both kernels can run against the same set (the
+//     sharded import and the regrow still use wide.cuh's code), and the results are identical.
+#pragma once
+#include "wide.cuh"
+
+namespace ltlb200 {
+
+// CTAs per SM: 2..6 measure the same on c5 (the big levels run at ~70 % of the random-access
+// ceiling of the memory system, not at an occupancy limit); 4 = 128 registers, no spills.
+#ifndef LTLB200_WIDE2_MIN_CTAS
+#define LTLB200_WIDE2_MIN_CTAS 4
+#endif
+constexpr int W2_BATCH = 2;        // candidates a lane carries through the passes together
+constexpr int W2_SC_VECS = 512;    // uint4 vectors of scalar-operand rows staged per warp (8 KiB)
+constexpr int W2_TERMS = 128;      // max scalar rows per tile
+
+struct __align__(16) Wide2Fixed {  // per-warp shared state behind the row areas
+    u64 term[W2_TERMS];
+    BlockDesc block;
+    u64 ticket, sep_now;
+};
+
+// per-warp shared memory in uint4 units: vec rows | scalar rows | valid + target | fixed part
+__host__ __device__ inline size_t wide2_warp_vecs(int nvec) {
+    return (size_t)nvec * 32 + W2_SC_VECS + 2 * (size_t)nvec + (sizeof(Wide2Fixed) + 15) / 16;
+}
+__host__ __device__ inline int wide2_tile_s(int nvec) { return W2_SC_VECS / nvec < W2_TERMS ? W2_SC_VECS / nvec : W2_TERMS; }
+
+struct Wide2Warp {
+    uint4 *vec;     // [nvec][32] transposed vector-operand rows
+    uint4 *sc;      // [tile_s][nvec] scalar-operand rows
+    uint4 *consts;  // [0, nvec) valid masks, [nvec, 2 nvec) targets
+    Wide2Fixed *fx;
+};
+
+struct Wide2State {  // warp-uniform registers
+    u64 chunk_next = 0, chunk_end = 0;  // staging entries reserved for this warp
+};
+
+// lanes with `want` get one staging entry each (ballot ranks; one atomicAdd per CLAIM_CHUNK entries)
+__device__ __forceinline__ u64 wide2_reserve(const WideParams &P, Wide2State &st, bool want) {
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, want);
+    const uint32_t n = __popc(m);
+    if (n == 0u) return 0;
+    const uint32_t rem = (uint32_t)(st.chunk_end - st.chunk_next);
+    u64 fresh = 0;
+    if (n > rem) {
+        if ((threadIdx.x & 31) == 0) fresh = atomicAdd(&P.counters[CTR_CLAIMED], (u64)CLAIM_CHUNK);
+        fresh = __shfl_sync(0xFFFFFFFFu, fresh, 0);
+    }
+    const uint32_t rank = __popc(m & lanemask_lt());
+    const u64 mine = rank < rem ? st.chunk_next + rank : fresh + (rank - rem);
+    if (n > rem) {
+        st.chunk_next = fresh + (n - rem);
+        st.chunk_end = fresh + CLAIM_CHUNK;
+    } else {
+        st.chunk_next += n;
+    }
+    return mine;
+}
+
+__device__ __forceinline__ uint32_t v_diff(uint4 a, uint4 b) { return (a.x ^ b.x) | (a.y ^ b.y) | (a.z ^ b.z) | (a.w ^ b.w); }
+
+// Carries W2_BATCH candidates of one lane through hash -> probe -> claim / compare.
+// `gen(r, p, a, b)` yields the operands of candidate r's vector p in formula order.
+template <int LW, int OP, class Gen>
+__device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp &W, Wide2State &st, Gen gen,
+                                            const bool (&live)[W2_BATCH], const u64 (&ords)[W2_BATCH]) {
+    const int nvec = P.nvec;
+    const uint32_t mask32 = (uint32_t)P.slot_mask;
+    // ---- pass 1: hashes, separation flag, duplicate-by-construction flags
+    uint32_t ha[W2_BATCH], hb[W2_BATCH], sepacc[W2_BATCH], da[W2_BATCH], db[W2_BATCH];
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) ha[r] = hb[r] = sepacc[r] = da[r] = db[r] = 0u;
+#pragma unroll 1
+    for (int p = 0; p < nvec; ++p) {
+        const uint4 valid = W.consts[p], target = W.consts[nvec + p];
+        const uint32_t seed_a = 0x9E3779B9u * (uint32_t)(p + 1), seed_b = 0x7F4A7C15u * (uint32_t)(p + 1) + 0x632BE5ABu;
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            uint4 a, b;
+            gen(r, p, a, b);
+            const uint4 c = cm_apply<LW, OP>(a, b, valid);
+            ha[r] ^= hash_vec(c, seed_a);
+            hb[r] ^= hash_vec(c, seed_b);
+            sepacc[r] |= cm_sep_diff<LW>(c, target);
+            da[r] |= v_diff(c, a);
+            db[r] |= v_diff(c, b);
+        }
+    }
+    uint32_t slot[W2_BATCH], fp[W2_BATCH];
+    u64 w[W2_BATCH], entry[W2_BATCH];
+    bool active[W2_BATCH], fresh[W2_BATCH];
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) {  // final mix of wide.cuh's row_hash
+        uint32_t a = ha[r], b = hb[r];
+        a ^= a >> 16;
+        a *= 0x85EBCA6Bu;
+        a ^= a >> 13;
+        b ^= b >> 15;
+        b *= 0xC2B2AE35u;
+        b ^= b >> 16;
+        slot[r] = a & mask32;
+        fp[r] = (b >> 8) & 0xFFFFFFu;
+        const bool known = OP != OP_ATOM && (da[r] == 0u || db[r] == 0u);  // equals an operand: already in the cache
+        active[r] = live[r] && !known;
+        fresh[r] = false;
+        entry[r] = ~0ull;
+        w[r] = active[r] ? __ldcg(&P.slots[slot[r]]) : 0ull;
+    }
+    // ---- resolve: every round, claims write their row and matches compare theirs in ONE pass over the vectors
+    for (;;) {
+        bool claim[W2_BATCH], match[W2_BATCH];
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            claim[r] = active[r] && w[r] == 0ull;
+            match[r] = active[r] && !claim[r] && (uint32_t)(w[r] >> 40) == fp[r];
+            if (active[r] && !claim[r] && !match[r]) {  // another CM lives there: linear probing
+                slot[r] = (slot[r] + 1) & mask32;
+                w[r] = __ldcg(&P.slots[slot[r]]);
+            }
+            any = any || active[r];
+        }
+        if (!__any_sync(0xFFFFFFFFu, any)) break;
+        bool staged_row[W2_BATCH];
+        const uint4 *row[W2_BATCH];
+        uint32_t diff[W2_BATCH];
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            const bool want = claim[r] && entry[r] == ~0ull;  // (a lost race left this candidate its entry)
+            const u64 got = wide2_reserve(P, st, want);
+            if (want) entry[r] = got;
+            if (claim[r] && entry[r] >= P.stage_cap) {  // staging pool exhausted: the host regrows and redoes the level
+                atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+                claim[r] = active[r] = false;
+            }
+            const u64 idx = (w[r] & SLOT_IDX_MASK) - 1;
+            staged_row[r] = match[r] && idx >= P.total_before;
+            row[r] = match[r] ? (staged_row[r] ? P.stage_rows + (idx - P.total_before) * nvec : P.store + idx * nvec) : nullptr;
+            diff[r] = 0u;
+        }
+        const bool any_claim = __any_sync(0xFFFFFFFFu, claim[0] || claim[W2_BATCH - 1]);
+#pragma unroll 1
+        for (int p = 0; p < nvec; ++p) {
+            const uint4 valid = W.consts[p];
+#pragma unroll
+            for (int r = 0; r < W2_BATCH; ++r) {
+                if (!claim[r] && !match[r]) continue;
+                uint4 a, b;
+                gen(r, p, a, b);
+                const uint4 c = cm_apply<LW, OP>(a, b, valid);
+                if (claim[r]) P.stage_rows[entry[r] * nvec + p] = c;
+                else diff[r] |= v_diff(c, __ldcg(row[r] + p));
+            }
+        }
+        if (any_claim) __threadfence();  // rows before the words that publish them
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            if (claim[r]) {
+                const u64 old = atomicCAS(&P.slots[slot[r]], 0ull, slot_word(fp[r], P.total_before + entry[r]));
+                if (old == 0ull) {
+                    atomicMin(&P.stage_ord[entry[r]], ords[r]);
+                    P.stage_slot[entry[r]] = slot[r];
+                    fresh[r] = true;
+                    active[r] = false;
+                } else {
+                    w[r] = old;  // somebody published here first: look at what they put (the entry is kept for a retry)
+                }
+            } else if (match[r]) {
+                if (diff[r] == 0u) {
+                    if (staged_row[r]) {
+                        atomicMin(&P.stage_ord[(w[r] & SLOT_IDX_MASK) - 1 - P.total_before], ords[r]);
+                        fresh[r] = true;
+                    }
+                    active[r] = false;
+                } else {  // fingerprint alias: keep probing
+                    slot[r] = (slot[r] + 1) & mask32;
+                    w[r] = __ldcg(&P.slots[slot[r]]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) {
+        if (live[r] && sepacc[r] == 0u) {
+            if (fresh[r]) atomicMin(&P.counters[CTR_SEP], ords[r]);
+            if (P.sep_list) {
+                const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+                if (pos < P.sep_list_cap) P.sep_list[pos] = ords[r];
+            }
+        }
+    }
+}
+
+template <int LW, int OP>
+__device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
+                                                 u64 sep_now) {
+    const BlockDesc &B = W.fx->block;
+    const int lane = threadIdx.x & 31;
+    const int nvec = P.nvec;
+    const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off * nvec;
+    const u64 per_tile = (u64)32 * B.tile_s;
+    const u64 first = tile_local * per_tile + lane;
+    const u64 ord0 = B.ord0, n = B.na;
+    if (ord0 + tile_local * per_tile > sep_now) return;
+    const int n_steps = (int)min((u64)B.tile_s, (n - tile_local * per_tile + 31) / 32);
+#pragma unroll 1
+    for (int k = 0; k < n_steps; k += W2_BATCH) {
+        bool live[W2_BATCH];
+        u64 ords[W2_BATCH];
+        const uint4 *rows[W2_BATCH];
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            const u64 i = first + (u64)(k + r) * 32;
+            live[r] = k + r < n_steps && i < n;
+            ords[r] = ord0 + i;
+            rows[r] = src + (live[r] ? i : 0) * nvec;
+        }
+        auto gen = [&](int r, int p, uint4 &a, uint4 &b) {
+            a = __ldg(rows[r] + p);
+            b = a;
+        };
+        wide2_batch<LW, OP>(P, W, st, gen, live, ords);
+    }
+}
+
+template <int LW, int OP, bool VEC_B>
+__device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
+                                                  u64 sep_now) {
+    const BlockDesc &B = W.fx->block;
+    const int lane = threadIdx.x & 31;
+    const int nvec = P.nvec;
+    const int tile_s = (int)B.tile_s;
+    const bool tri = B.kind == BK_TRI;
+    const uint32_t vg_n = B.vg;
+    u64 tv, ts;
+    if (VEC_B) { ts = tile_local / B.tiles_v; tv = tile_local % B.tiles_v; }
+    else { tv = tile_local / B.tiles_s; ts = tile_local % B.tiles_s; }
+    const u64 n_vec = VEC_B ? B.nb : B.na, n_sc = VEC_B ? B.na : B.nb;
+    const u64 v0 = tv * (u64)(32 * vg_n), s0 = ts * (u64)tile_s;
+    const int s_cnt = (int)min((u64)tile_s, n_sc - s0);
+    if (tri && v0 + (u64)32 * vg_n - 1 < s0) return;
+    const u64 ord0 = B.ord0, na = B.na, nb = B.nb;
+    const u64 tile_min = ord0 + (VEC_B ? (tri ? s0 * na - (s0 ? (s0 * (s0 - 1)) / 2 : 0) : s0 * nb + v0) : v0 * nb + s0);
+    if (tile_min > sep_now) return;
+    const uint4 *vec_rows = P.store + (VEC_B ? B.b_off : B.a_off) * nvec;
+    const uint4 *sc_rows = P.store + (VEC_B ? B.a_off : B.b_off) * nvec;
+    __syncwarp();
+    // stage the scalar rows (contiguous in the cache: one coalesced copy) and their ordinal terms
+    for (int t = lane; t < s_cnt * nvec; t += 32) W.sc[t] = __ldg(sc_rows + s0 * nvec + t);
+    for (int k = lane; k < s_cnt; k += 32) {
+        const u64 s = s0 + k;
+        W.fx->term[k] = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
+    }
+#pragma unroll 1
+    for (uint32_t vg = 0; vg < vg_n; ++vg) {
+        const u64 vbase = v0 + (u64)vg * 32;
+        if (vbase >= n_vec) break;
+        __syncwarp();
+        // stage 32 vector rows transposed: the warp copies row after row (coalesced reads), vec[p*32 + row]
+        const int rows_here = (int)min((u64)32, n_vec - vbase);
+        for (int t = lane; t < rows_here * nvec; t += 32) {
+            const int rrow = t / nvec, p = t - rrow * nvec;
+            W.vec[p * 32 + rrow] = __ldg(vec_rows + vbase * nvec + t);
+        }
+        __syncwarp();
+        const u64 v = vbase + lane;
+        const bool v_ok = v < n_vec;
+        const u64 lane_term = VEC_B ? v : ord0 + v * nb;
+        const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
+        const int s_live = v_ok ? first_bad : 0;
+#pragma unroll 1
+        for (int k = 0; k < s_cnt; k += W2_BATCH) {
+            bool live[W2_BATCH];
+            u64 ords[W2_BATCH];
+            int srow[W2_BATCH];
+#pragma unroll
+            for (int r = 0; r < W2_BATCH; ++r) {
+                srow[r] = min(k + r, s_cnt - 1);
+                live[r] = k + r < s_live;
+                ords[r] = W.fx->term[srow[r]] + lane_term;
+            }
+            auto gen = [&](int r, int p, uint4 &a, uint4 &b) {
+                const uint4 xv = W.vec[p * 32 + lane], xs = W.sc[srow[r] * nvec + p];
+                a = VEC_B ? xs : xv;
+                b = VEC_B ? xv : xs;
+            };
+            wide2_batch<LW, OP>(P, W, st, gen, live, ords);
+        }
+    }
+}
+
+__device__ __forceinline__ Wide2Warp wide2_carve(const WideParams &P, uint4 *base) {
+    Wide2Warp W;
+    uint4 *mine = base + (threadIdx.x >> 5) * wide2_warp_vecs(P.nvec);
+    W.vec = mine;
+    W.sc = W.vec + (size_t)P.nvec * 32;
+    W.consts = W.sc + W2_SC_VECS;
+    W.fx = reinterpret_cast<Wide2Fixed *>(W.consts + 2 * (size_t)P.nvec);
+    const int lane = threadIdx.x & 31;
+    for (int p = lane; p < P.nvec; p += 32) {
+        W.consts[p] = P.valid[p];
+        W.consts[P.nvec + p] = P.target[p];
+    }
+    __syncwarp();
+    return W;
+}
+
+__device__ __forceinline__ bool wide2_next_tile(const WideParams &P, const Wide2Warp &W) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    if (lane == 0) {
+        u64 t = P.tile_end;
+        if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+            t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
+        W.fx->ticket = t;
+        W.fx->sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;
+        if (t < P.tile_end) {
+            int bi = P.block_begin;
+            while (bi + 1 < P.block_end && t >= P.blocks[bi + 1].tile0) ++bi;
+            W.fx->block = P.blocks[bi];
+        }
+    }
+    __syncwarp();
+    return W.fx->ticket < P.tile_end;
+}
+
+template <int LW, int OP>
+__device__ __forceinline__ void wide2_run_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st) {
+    const u64 sep_now = W.fx->sep_now;
+    if (W.fx->block.ord0 > sep_now) return;
+    const u64 tile_local = W.fx->ticket - W.fx->block.tile0;
+    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
+        if (W.fx->block.vec_is_b) wide2_binary_tile<LW, OP, true>(P, W, st, tile_local, sep_now);
+        else wide2_binary_tile<LW, OP, false>(P, W, st, tile_local, sep_now);
+    } else {
+        wide2_unary_tile<LW, OP>(P, W, st, tile_local, sep_now);
+    }
+}
+
+template <int LW, int OP>
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_WIDE2_MIN_CTAS) wide2_level_kernel(const __grid_constant__ WideParams P) {
+    extern __shared__ __align__(16) uint4 s_w2[];
+    const Wide2Warp W = wide2_carve(P, s_w2);
+    Wide2State st;
+    while (wide2_next_tile(P, W)) wide2_run_tile<LW, OP>(P, W, st);
+}
+
+// small levels: one launch for every operator
+template <int LW>
+__global__ void __launch_bounds__(CTA_THREADS, 1) wide2_small_level_kernel(const __grid_constant__ WideParams P) {
+    extern __shared__ __align__(16) uint4 s_w2[];
+    const Wide2Warp W = wide2_carve(P, s_w2);
+    Wide2State st;
+    while (wide2_next_tile(P, W)) {
+        switch (W.fx->block.op) {
+            case OP_ATOM: wide2_run_tile<LW, OP_ATOM>(P, W, st); break;
+            case OP_NOT: wide2_run_tile<LW, OP_NOT>(P, W, st); break;
+            case OP_NEXT: wide2_run_tile<LW, OP_NEXT>(P, W, st); break;
+            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE>(P, W, st); break;
+            case OP_AND: wide2_run_tile<LW, OP_AND>(P, W, st); break;
+            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL>(P, W, st); break;
+            default: wide2_run_tile<LW, OP_OR>(P, W, st); break;
+        }
+    }
+}
+
+}  // namespace ltlb200

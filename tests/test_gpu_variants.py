@@ -8,6 +8,8 @@ cases in a child process:
   LTLB200_ASYNC=1       cp.async probe pipeline (narrow_async.cuh)
   LTLB200_NO_DEFER=1    two synchronisations per level (finalisation launched after the counters
                         were read) instead of the deferred, device-bounded finalisation
+  LTLB200_WIDE2=0       multi-vector CMs by wide.cuh's group-per-candidate kernel instead of
+                        wide2.cuh's lane-per-candidate kernel (the default)
 
 Every variant must reproduce the golden fixtures of the unmodified reference bit for bit.
 """
@@ -23,6 +25,8 @@ pytestmark = pytest.mark.gpu
 
 ROOT = pathlib.Path(__file__).resolve().parent.parent
 CASES = ["spec1_found", "spec1_exh10", "spec2_exh11", "c1_s1", "c3_s0_exh12", "c3_s1_found", "spec2_fuo_exh8"]
+WIDE_CASES = ["c3wide_s0_exh8", "c4-512_s0_exh8", "c4-1024_s0_exh8", "c4xl_s0_exh7", "c5_s0_exh8", "c5_s0_or_exh7",
+              "w32_s1_found", "w64n_s0_exh9"]
 
 CHILD = """
 import sys
@@ -34,10 +38,11 @@ print("variant ok")
 """
 
 
-@pytest.mark.parametrize("switch", ["LTLB200_PARTITION", "LTLB200_ASYNC", "LTLB200_NO_DEFER"])
-def test_variant_matches_reference(switch):
+@pytest.mark.parametrize("switch,value,cases", [("LTLB200_PARTITION", "1", CASES), ("LTLB200_ASYNC", "1", CASES),
+                                                 ("LTLB200_NO_DEFER", "1", CASES), ("LTLB200_WIDE2", "0", WIDE_CASES)])
+def test_variant_matches_reference(switch, value, cases):
     env = dict(os.environ)
-    env[switch] = "1"
-    code = CHILD.format(root=str(ROOT), tests=str(ROOT / "tests"), cases=CASES)
+    env[switch] = value
+    code = CHILD.format(root=str(ROOT), tests=str(ROOT / "tests"), cases=cases)
     proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert proc.returncode == 0 and "variant ok" in proc.stdout, proc.stdout[-2000:] + proc.stderr[-4000:]
