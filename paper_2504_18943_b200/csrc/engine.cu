@@ -334,6 +334,7 @@ private:
     DeviceArray<uint4> stage_rows_;    // wide path: this level's new rows
     DeviceArray<u64> stage_ord_;
     DeviceArray<uint32_t> stage_slot_;
+    DeviceArray<u64> stage_gid_;
     DeviceArray<uint32_t> bitmap_;
     DeviceArray<uint32_t> sb_rank_;
     DeviceArray<uint32_t> scan_tmp_;
@@ -596,6 +597,7 @@ Engine::~Engine() {
     release(stage_rows_);
     release(stage_ord_);
     release(stage_slot_);
+    release(stage_gid_);
     release(bitmap_);
     release(sb_rank_);
     release(scan_tmp_);
@@ -1552,6 +1554,8 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
             W.stage_rows = stage_rows_.ptr;
             W.stage_ord = stage_ord_.ptr;
             W.stage_slot = stage_slot_.ptr;
+            reserve(stage_gid_, std::max<u64>(1, std::min(n_claimed, pl.claim_cap)), false);
+            W.stage_gid = stage_gid_.ptr;
             W.n_staged = std::min(n_claimed, pl.claim_cap);
             W.bitmap = bitmap_.ptr;
             W.sb_rank = sb_rank_.ptr;
@@ -1590,9 +1594,11 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
         }
         level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
         if (wide_) {
+            wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
             const u64 work = W.n_staged * (u64)nvec_;
             const int wgrid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
-            wide_scatter_kernel<<<wgrid, 256, 0, stream_>>>(W);
+            wide_copy_kernel<<<wgrid, 256, 0, stream_>>>(W);
+            st_.kernel_launches++;
         } else {
             narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
         }

@@ -507,6 +507,7 @@ struct WideFinalize {
     u64 *ords;
     u64 base;
     int nvec;
+    u64 *stage_gid;  // final id per staging entry (written by wide_rank_kernel)
 };
 
 __global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
@@ -516,21 +517,34 @@ __global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
     }
 }
 
-// one thread per (staging entry, vector)
-__global__ void __launch_bounds__(256) wide_scatter_kernel(const WideFinalize F) {
+// Scatter in two steps, so that the rank of an entry is computed once, not once per vector:
+//   wide_rank_kernel   one thread per staging entry: final id = base + rank(ordinal); records the
+//                      ordinal, re-points the entry's slot word at the final id, leaves the id in
+//                      stage_gid (all ones = entry unused or ordered after the separator);
+//   wide_copy_kernel   one thread per (staging entry, vector): coalesced copy of the row to its
+//                      place in the cache.
+__global__ void __launch_bounds__(256) wide_rank_kernel(const WideFinalize F) {
+    for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < F.n_staged; k += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = F.stage_ord[k];
+        if (ord > F.ord_limit) {
+            F.stage_gid[k] = ~0ull;
+            continue;
+        }
+        const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
+        F.stage_gid[k] = gid;
+        F.ords[gid] = ord;
+        u64 *slot = &F.slots[F.stage_slot[k]];
+        *slot = (*slot & ~SLOT_IDX_MASK) | (gid + 1);  // same fingerprint, final row id
+    }
+}
+
+__global__ void __launch_bounds__(256) wide_copy_kernel(const WideFinalize F) {
     const u64 total = F.n_staged * (u64)F.nvec;
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
         const u64 k = t / F.nvec;
-        const int part = (int)(t % F.nvec);
-        const u64 ord = F.stage_ord[k];
-        if (ord > F.ord_limit) continue;  // unused entry, or ordered after the separator
-        const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
-        F.store[gid * F.nvec + part] = F.stage_rows[k * F.nvec + part];
-        if (part == 0) {
-            F.ords[gid] = ord;
-            u64 *slot = &F.slots[F.stage_slot[k]];
-            *slot = (*slot & ~SLOT_IDX_MASK) | (gid + 1);  // same fingerprint, final row id
-        }
+        const u64 gid = F.stage_gid[k];
+        if (gid == ~0ull) continue;
+        F.store[gid * F.nvec + (t - k * F.nvec)] = F.stage_rows[t];
     }
 }
 
