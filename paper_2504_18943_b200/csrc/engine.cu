@@ -1382,7 +1382,10 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             // (wide: every group of every operator launch may end with a partly used chunk of staging entries)
             const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * std::max<u64>((u64)(32 >> log2g_) * WIDE_CHUNK, CLAIM_CHUNK) * 8 + 1024;
             // (narrow: every warp of every operator launch may end with a partly used chunk of claim indices)
-            const u64 narrow_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8 + 1024;
+            // (a small level is one launch of at most 2 CTAs per SM: narrow_small_level_kernel)
+            const u64 narrow_slack = constructed <= kSmallLevel && !async_enabled() && !use_partition(constructed)
+                                         ? (u64)sm_count_ * 2 * WARPS_PER_CTA * CLAIM_CHUNK + 1024
+                                         : (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8 + 1024;
             const u64 claim_cap = est + (wide_ ? wide_slack : narrow_slack);
             // the set is sized for the CMs it can receive (est; exact for small levels, and beyond est the
             // claim arrays overflow first because est >= kExact > their slack), not for the claim slack:
@@ -1674,12 +1677,14 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
     try {
         const u64 n_bits = constructed;
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
-        reserve(bitmap_, n_words + 1, false);
-        reserve(sb_rank_, n_sb + 1, false);
+        const bool small = n_bits <= SMALL_FIN_MAX_BITS;  // bitmap in shared memory, one launch
+        if (!small) {
+            reserve(bitmap_, n_words + 1, false);
+            reserve(sb_rank_, n_sb + 1, false);
+        }
         reserve(store_, (total_ + pl.claim_cap) * nvec_, true, total_ * nvec_);
         reserve(ords_, total_ + pl.claim_cap, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
-        CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
         FinalizeParams F{};
         F.claim_key = claim_key_.ptr;
         F.claim_ord = claim_ord_.ptr;
@@ -1691,17 +1696,30 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         F.live = d_counters_;
         F.claim_cap = pl.claim_cap;
         F.cut_allowed = 1;
-        // the grid is sized by what the level can have claimed at most (its candidates, or the claim arrays)
-        const u64 claim_bound = std::min(constructed + (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK, pl.claim_cap);
-        const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
-        narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
-        CUDA_CHECK(cudaGetLastError());
-        launch_rank_scan(n_words, n_sb);
-        level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
-        narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
-        CUDA_CHECK(cudaGetLastError());
+        if (small) {
+            static std::once_flag once;
+            std::call_once(once, [] {
+                cudaFuncSetAttribute(narrow_small_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((SMALL_FIN_MAX_BITS / 8) + 512 * sizeof(uint32_t) + 256));
+            });
+            const size_t smem = (size_t)n_sb * 32 * sizeof(uint32_t) + (size_t)n_sb * sizeof(uint32_t);
+            narrow_small_finalize_kernel<<<1, SMALL_FIN_THREADS, smem, stream_>>>(F, n_bits, d_counters_);
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+        } else {
+            CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+            // the grid is sized by what the level can have claimed at most (its candidates, or the claim arrays)
+            const u64 claim_bound = std::min(constructed + (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK, pl.claim_cap);
+            const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
+            narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+            CUDA_CHECK(cudaGetLastError());
+            launch_rank_scan(n_words, n_sb);
+            level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+            narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches += 3;
+        }
         CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
-        st_.kernel_launches += 3;
         PHASE(5, "end: reserve + launches", tp);
         read_counters();
         PHASE(6, "end: sync + read counters", tp);

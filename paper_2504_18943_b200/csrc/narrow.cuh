@@ -675,6 +675,67 @@ __global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParam
     }
 }
 
+// Small levels: the whole finalisation in ONE CTA.  The winners bitmap of a level of up to 2^19
+// candidates is 64 KiB and lives in shared memory, so mark -> superblock ranks -> summary ->
+// scatter need no global bitmap, no scan launches and no separate summary launch: such a level
+// is launch latency, and this is one launch instead of five.
+constexpr int SMALL_FIN_THREADS = 1024;
+constexpr u64 SMALL_FIN_MAX_BITS = 1ull << 15;
+
+__global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kernel(const FinalizeParams F, u64 n_bits, u64 *counters) {
+    extern __shared__ uint32_t s_fin[];
+    const u64 n_words = (n_bits + 31) >> 5, n_sb = (n_words + 31) >> 5;  // <= 16384 words, <= 512 superblocks
+    uint32_t *bitmap = s_fin, *sb_rank = s_fin + n_sb * 32;              // bitmap padded to whole superblocks
+    __shared__ uint32_t warp_tot[32];
+    u64 n_claimed, ord_limit;
+    if (!finalize_bounds(F, n_claimed, ord_limit)) return;  // uniform: the level overflowed and is redone
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (u64 w = tid; w < n_sb * 32; w += SMALL_FIN_THREADS) bitmap[w] = 0u;
+    __syncthreads();
+    for (u64 t = tid; t < n_claimed; t += SMALL_FIN_THREADS) {
+        const u64 ord = F.claim_ord[t];
+        if (ord <= ord_limit) atomicOr(&bitmap[ord >> 5], 1u << (ord & 31));
+    }
+    __syncthreads();
+    // exclusive popcount prefix per superblock (n_sb <= 512 <= threads)
+    uint32_t v = 0;
+    if ((u64)tid < n_sb)
+        for (int k = 0; k < 32; ++k) v += __popc(bitmap[tid * 32 + k]);
+    uint32_t incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = warp_tot[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+            if (lane >= d) wi += t;
+        }
+        warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    if ((u64)tid < n_sb) sb_rank[tid] = warp_tot[warp] + incl - v;
+    __syncthreads();
+    if (tid == 0) {  // winners of the level, rank of the separator
+        const u64 sep_ord = counters[CTR_SEP];
+        counters[CTR_WINNERS] = n_bits ? ordinal_rank(bitmap, sb_rank, n_bits - 1) + ((bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u) : 0;
+        counters[CTR_SEPRANK] = sep_ord < n_bits ? ordinal_rank(bitmap, sb_rank, sep_ord) : ~0ull;
+    }
+    for (u64 t = tid; t < n_claimed; t += SMALL_FIN_THREADS) {
+        const u64 ord = F.claim_ord[t];
+        if (ord > ord_limit) continue;
+        const u64 gid = F.base + ordinal_rank(bitmap, sb_rank, ord);
+        F.store[gid] = F.claim_key[t];
+        F.ords[gid] = ord;
+    }
+}
+
 // re-insert finalised rows [first, first+count) into a fresh table (regrow / rollback)
 __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 slot_mask, const uint4 *store,
                                                              u64 first, u64 count, u64 *counters) {
