@@ -25,6 +25,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/ltlsynth_b200.h"
@@ -577,7 +578,15 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
         }
         occupancy_ = wide_ ? LTLB200_WIDE_MIN_CTAS : (async_enabled() ? it->second[1] : it->second[0]);
         wide2_ = wide_ && wide2_enabled();
-        if (wide2_) occupancy_ = lw_ == 8 ? wide2_occupancy_of<8>(nvec_) : lw_ == 16 ? wide2_occupancy_of<16>(nvec_) : lw_ == 32 ? wide2_occupancy_of<32>(nvec_) : wide2_occupancy_of<64>(nvec_);
+        if (wide2_) {  // depends on the shared memory the row areas need, i.e. on nvec: cached per (device, lanes, nvec)
+            static std::map<std::tuple<int, int, int>, int> w2cache;
+            auto w2 = w2cache.find({device_, lw_, nvec_});
+            if (w2 == w2cache.end())
+                w2 = w2cache.emplace(std::make_tuple(device_, lw_, nvec_),
+                                     lw_ == 8 ? wide2_occupancy_of<8>(nvec_) : lw_ == 16 ? wide2_occupancy_of<16>(nvec_)
+                                     : lw_ == 32 ? wide2_occupancy_of<32>(nvec_) : wide2_occupancy_of<64>(nvec_)).first;
+            occupancy_ = w2->second;
+        }
         part_occupancy_ = it->second[2];
     }
     rebuild_table(kMinSlots);
