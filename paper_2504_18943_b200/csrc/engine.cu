@@ -1431,7 +1431,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             }
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
             PHASE(2, "begin: launches", tp);
-            if (defer && !wide_ && !exhaustive && !use_partition(constructed)) {
+            if (defer && !use_partition(constructed)) {
                 pl.deferred = true;
                 st_.enumerate_candidates += constructed / (u64)shard_count;
                 return LTLB200_OK;
@@ -1681,52 +1681,82 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
     PendingLevel &pl = pending_;
     LevelMeta &lv = pl.lv;
     const u64 constructed = pl.constructed;
+    const bool exhaustive = pl.exhaustive;
     double tp = monotonic_s();
     u64 sep_ord = VAL_EMPTY;
     try {
         const u64 n_bits = constructed;
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
-        const bool small = n_bits <= SMALL_FIN_MAX_BITS;  // bitmap in shared memory, one launch
-        if (!small) {
-            reserve(bitmap_, n_words + 1, false);
+        const bool small = !wide_ && n_bits <= SMALL_FIN_MAX_BITS;  // bitmap in shared memory, one launch
+        if (!small || exhaustive) {
+            reserve(bitmap_, n_sb * 32 + 1, false);
             reserve(sb_rank_, n_sb + 1, false);
         }
         reserve(store_, (total_ + pl.claim_cap) * nvec_, true, total_ * nvec_);
         reserve(ords_, total_ + pl.claim_cap, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
-        FinalizeParams F{};
-        F.claim_key = claim_key_.ptr;
-        F.claim_ord = claim_ord_.ptr;
-        F.bitmap = bitmap_.ptr;
-        F.sb_rank = sb_rank_.ptr;
-        F.store = store_.ptr;
-        F.ords = ords_.ptr;
-        F.base = total_;
-        F.live = d_counters_;
-        F.claim_cap = pl.claim_cap;
-        F.cut_allowed = 1;
-        if (small) {
-            static std::once_flag once;
-            std::call_once(once, [] {
-                cudaFuncSetAttribute(narrow_small_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((SMALL_FIN_MAX_BITS / 8) + 512 * sizeof(uint32_t) + 256));
-            });
-            const size_t smem = (size_t)n_sb * 32 * sizeof(uint32_t) + (size_t)n_sb * sizeof(uint32_t);
-            narrow_small_finalize_kernel<<<1, SMALL_FIN_THREADS, smem, stream_>>>(F, n_bits, d_counters_);
-            CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches++;
-        } else {
+        // the grids are sized by what the level can have claimed at most (its candidates, or the claim arrays)
+        const u64 claim_bound = std::min(constructed + (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8, pl.claim_cap);
+        const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
+        if (wide_) {
+            WideFinalize W{};
+            W.slots = wslots_.ptr;
+            W.stage_rows = stage_rows_.ptr;
+            W.stage_ord = stage_ord_.ptr;
+            W.stage_slot = stage_slot_.ptr;
+            W.bitmap = bitmap_.ptr;
+            W.sb_rank = sb_rank_.ptr;
+            W.store = store_.ptr;
+            W.ords = ords_.ptr;
+            W.base = total_;
+            W.nvec = nvec_;
+            reserve(stage_gid_, std::max<u64>(1, pl.claim_cap), false);
+            W.stage_gid = stage_gid_.ptr;
+            W.live = d_counters_;
+            W.stage_cap = pl.claim_cap;
+            W.cut_allowed = exhaustive ? 0 : 1;
             CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
-            // the grid is sized by what the level can have claimed at most (its candidates, or the claim arrays)
-            const u64 claim_bound = std::min(constructed + (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK, pl.claim_cap);
-            const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
-            narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+            wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
             CUDA_CHECK(cudaGetLastError());
             launch_rank_scan(n_words, n_sb);
             level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
-            narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+            wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
+            const int wgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound * (u64)nvec_ + 255) / 256, (u64)sm_count_ * 16));
+            wide_copy_kernel<<<wgrid, 256, 0, stream_>>>(W);
             CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches += 3;
+            st_.kernel_launches += 4;
+        } else {
+            FinalizeParams F{};
+            F.claim_key = claim_key_.ptr;
+            F.claim_ord = claim_ord_.ptr;
+            F.bitmap = bitmap_.ptr;
+            F.sb_rank = sb_rank_.ptr;
+            F.store = store_.ptr;
+            F.ords = ords_.ptr;
+            F.base = total_;
+            F.live = d_counters_;
+            F.claim_cap = pl.claim_cap;
+            F.cut_allowed = exhaustive ? 0 : 1;
+            if (small) {
+                static std::once_flag once;
+                std::call_once(once, [] {
+                    cudaFuncSetAttribute(narrow_small_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)((SMALL_FIN_MAX_BITS / 8) + 512 * sizeof(uint32_t) + 256));
+                });
+                const size_t smem = (size_t)n_sb * 32 * sizeof(uint32_t) + (size_t)n_sb * sizeof(uint32_t);
+                narrow_small_finalize_kernel<<<1, SMALL_FIN_THREADS, smem, stream_>>>(F, n_bits, d_counters_, exhaustive ? 1 : 0);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches++;
+            } else {
+                CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+                narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+                CUDA_CHECK(cudaGetLastError());
+                launch_rank_scan(n_words, n_sb);
+                level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+                narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches += 3;
+            }
         }
         CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
         PHASE(5, "end: reserve + launches", tp);
@@ -1745,10 +1775,31 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         }
         lv.n = h_counters_[CTR_WINNERS];
         sep_ord = h_counters_[CTR_SEP];
+        if (sep_ord != VAL_EMPTY || h_counters_[CTR_SEPCOUNT]) store_has_separator_ = true;
+        if (exhaustive && h_counters_[CTR_SEPCOUNT]) {
+            // the reference reports, per level, the first CHUNK whose first separating candidate is fresh
+            // (engine.py:331,425-433): walk the recorded ordinals against the winners bitmap (one more round trip,
+            // only on levels that contain a separating candidate at all)
+            const u64 n_seps = std::min<u64>(h_counters_[CTR_SEPCOUNT], sep_list_.cap);
+            std::vector<u64> all;
+            if (h_counters_[CTR_SEPCOUNT] <= sep_list_.cap) {
+                all.resize((size_t)n_seps);
+                CUDA_CHECK(cudaMemcpyAsync(all.data(), sep_list_.ptr, n_seps * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+                CUDA_CHECK(cudaStreamSynchronize(stream_));
+                st_.d2h_bytes += n_seps * sizeof(u64);
+            }
+            if (!all.empty()) {
+                chunk_exact_separator(lv, all, (u64)batch);
+                level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches++;
+                read_counters();
+                sep_ord = h_counters_[CTR_SEP];
+            }
+        }
         if (sep_ord != VAL_EMPTY) {
             *sep_gid = (int64_t)(total_ + h_counters_[CTR_SEPRANK]);
-            store_has_separator_ = true;
-            table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
+            if (!exhaustive) table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
         }
     } catch (const MemoryBudget &e) {
         g_last_error = e.what();
@@ -1757,7 +1808,8 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         levels_.push_back(LevelMeta{0, total_, {}});
         return LTLB200_MEMORY_BUDGET;
     }
-    *constructed_delta = (int64_t)(sep_ord != VAL_EMPTY ? constructed_through(lv, sep_ord, (u64)batch) : constructed);
+    const bool found_cut = !exhaustive && sep_ord != VAL_EMPTY;
+    *constructed_delta = (int64_t)(found_cut ? constructed_through(lv, sep_ord, (u64)batch) : constructed);
     last_constructed_ = constructed;
     *n_new = (int64_t)lv.n;
     total_ += lv.n;

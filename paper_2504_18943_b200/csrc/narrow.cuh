@@ -682,7 +682,8 @@ __global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParam
 constexpr int SMALL_FIN_THREADS = 1024;
 constexpr u64 SMALL_FIN_MAX_BITS = 1ull << 15;
 
-__global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kernel(const FinalizeParams F, u64 n_bits, u64 *counters) {
+__global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kernel(const FinalizeParams F, u64 n_bits, u64 *counters,
+                                                                                  int export_bitmap) {
     extern __shared__ uint32_t s_fin[];
     const u64 n_words = (n_bits + 31) >> 5, n_sb = (n_words + 31) >> 5;  // <= 16384 words, <= 512 superblocks
     uint32_t *bitmap = s_fin, *sb_rank = s_fin + n_sb * 32;              // bitmap padded to whole superblocks
@@ -722,6 +723,10 @@ __global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kerne
     __syncthreads();
     if ((u64)tid < n_sb) sb_rank[tid] = warp_tot[warp] + incl - v;
     __syncthreads();
+    if (export_bitmap) {  // exhaustive runs pick their reported separator against the winners bitmap afterwards
+        for (u64 w = tid; w < n_sb * 32; w += SMALL_FIN_THREADS) F.bitmap[w] = bitmap[w];
+        if ((u64)tid < n_sb) const_cast<uint32_t *>(F.sb_rank)[tid] = sb_rank[tid];
+    }
     if (tid == 0) {  // winners of the level, rank of the separator
         const u64 sep_ord = counters[CTR_SEP];
         counters[CTR_WINNERS] = n_bits ? ordinal_rank(bitmap, sb_rank, n_bits - 1) + ((bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u) : 0;

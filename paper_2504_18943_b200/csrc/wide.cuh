@@ -508,12 +508,29 @@ struct WideFinalize {
     u64 base;
     int nvec;
     u64 *stage_gid;  // final id per staging entry (written by wide_rank_kernel)
+    // deferred mode (see FinalizeParams in narrow.cuh): bounds resolved on the device
+    const u64 *live;
+    u64 stage_cap;
+    int cut_allowed;
 };
 
+__device__ __forceinline__ bool wide_finalize_bounds(const WideFinalize &F, u64 &n_staged, u64 &ord_limit) {
+    n_staged = F.n_staged;
+    ord_limit = F.ord_limit;
+    if (F.live == nullptr) return true;
+    if (F.live[CTR_OVERFLOW]) return false;
+    const u64 claimed = F.live[CTR_CLAIMED], sep = F.live[CTR_SEP];
+    n_staged = claimed < F.stage_cap ? claimed : F.stage_cap;
+    ord_limit = (F.cut_allowed && sep != VAL_EMPTY) ? sep : VAL_EMPTY - 1;
+    return true;
+}
+
 __global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < F.n_staged; t += (u64)gridDim.x * blockDim.x) {
+    u64 n_staged, ord_limit;
+    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_staged; t += (u64)gridDim.x * blockDim.x) {
         const u64 ord = F.stage_ord[t];
-        if (ord <= F.ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
+        if (ord <= ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
     }
 }
 
@@ -524,9 +541,11 @@ __global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
 //   wide_copy_kernel   one thread per (staging entry, vector): coalesced copy of the row to its
 //                      place in the cache.
 __global__ void __launch_bounds__(256) wide_rank_kernel(const WideFinalize F) {
-    for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < F.n_staged; k += (u64)gridDim.x * blockDim.x) {
+    u64 n_staged, ord_limit;
+    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
+    for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n_staged; k += (u64)gridDim.x * blockDim.x) {
         const u64 ord = F.stage_ord[k];
-        if (ord > F.ord_limit) {
+        if (ord > ord_limit) {
             F.stage_gid[k] = ~0ull;
             continue;
         }
@@ -539,7 +558,9 @@ __global__ void __launch_bounds__(256) wide_rank_kernel(const WideFinalize F) {
 }
 
 __global__ void __launch_bounds__(256) wide_copy_kernel(const WideFinalize F) {
-    const u64 total = F.n_staged * (u64)F.nvec;
+    u64 n_staged, ord_limit;
+    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
+    const u64 total = n_staged * (u64)F.nvec;
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
         const u64 k = t / F.nvec;
         const u64 gid = F.stage_gid[k];
