@@ -371,6 +371,16 @@ private:
     u64 *h_counters_ = nullptr;  // pinned
     cudaEvent_t ev_[4] = {};
     bool table_dirty_ = false;
+    // The operator launches of one big level are independent of each other (they share the set, the claim
+    // arrays and the counters, all updated atomically), so they go to different streams: the next operator's
+    // CTAs move into the SMs as the previous launch's last tiles finish, instead of waiting for its tail.
+    static constexpr int kSideStreams = 4;
+    cudaStream_t side_[kSideStreams] = {};
+    cudaEvent_t fork_ev_ = nullptr, join_ev_[kSideStreams] = {};
+    uint32_t side_used_ = 0;  // side streams of the current fan-out
+    void fan_begin();
+    cudaStream_t fan_stream(int group);
+    void fan_end();
 
     std::vector<LevelMeta> levels_;
     u64 total_ = 0, approx_bytes_ = 0, last_constructed_ = 0;
@@ -556,6 +566,9 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     st_.h2d_bytes += h_rows.size() * sizeof(uint4);
     h_counters_ = pinned_get();
     for (auto &e : ev_) CUDA_CHECK(cudaEventCreate(&e));
+    for (auto &st : side_) CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+    for (auto &e : join_ev_) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     u64 init[CTR_COUNT];
     for (auto &c : init) c = 0;
     init[CTR_SPECIAL] = VAL_EMPTY;
@@ -623,6 +636,11 @@ Engine::~Engine() {
     pinned_put(h_counters_);
     g_phase.dump();
     for (auto &e : ev_)
+        if (e) cudaEventDestroy(e);
+    for (auto &st : side_)
+        if (st) cudaStreamDestroy(st);
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
+    for (auto &e : join_ev_)
         if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(stream_);
 }
@@ -983,7 +1001,7 @@ static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int o
         P.ticket = CTR_TICKET0 + group;
         const int grid = (int)std::min<u64>((P.tile_end - P.tile_begin + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count * occupancy);
         DBG("launch op=%d blocks=[%zu,%zu) tiles=[%llu,%llu) grid=%d", (int)lv.blocks[b0].op, b0, b1, (unsigned long long)P.tile_begin, (unsigned long long)P.tile_end, grid);
-        launch((int)lv.blocks[b0].op, P, grid);
+        launch((int)lv.blocks[b0].op, P, grid, group);
         CUDA_CHECK(cudaGetLastError());
         if (debug_on()) {
             CUDA_CHECK(cudaDeviceSynchronize());
@@ -998,6 +1016,42 @@ static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int o
 
 // levels up to this many candidates take the one-launch kernel (narrow_small_level_kernel)
 static constexpr u64 kSmallLevel = 1ull << 19;
+
+// LTLB200_OPSTREAMS=0: every operator launch of a level on the engine's own stream, one after the other
+static bool fan_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LTLB200_OPSTREAMS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+void Engine::fan_begin() {
+    side_used_ = 0;
+    if (fan_enabled()) CUDA_CHECK(cudaEventRecord(fork_ev_, stream_));
+}
+
+// stream of the level's `group`-th operator launch: the first stays on the engine's stream, the others
+// start on a side stream once everything queued before the fan-out (level init, memsets) is done
+cudaStream_t Engine::fan_stream(int group) {
+    if (group == 0 || !fan_enabled()) return stream_;
+    const int k = (group - 1) % kSideStreams;
+    if (!(side_used_ >> k & 1u)) {
+        CUDA_CHECK(cudaStreamWaitEvent(side_[k], fork_ev_, 0));
+        side_used_ |= 1u << k;
+    }
+    return side_[k];
+}
+
+// the engine's stream continues (finalisation, counters read-back) after every side stream has drained
+void Engine::fan_end() {
+    for (int k = 0; k < kSideStreams; ++k) {
+        if (!(side_used_ >> k & 1u)) continue;
+        CUDA_CHECK(cudaEventRecord(join_ev_[k], side_[k]));
+        CUDA_CHECK(cudaStreamWaitEvent(stream_, join_ev_[k], 0));
+    }
+    side_used_ = 0;
+}
 
 void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
     const BlockDesc &last_block = lv.blocks.back();
@@ -1020,23 +1074,26 @@ void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
         st_.enumerate_launches++;
         return;
     }
-    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const NarrowParams &Q, int grid) {
+    fan_begin();
+    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const NarrowParams &Q, int grid, int group) {
+        cudaStream_t st = fan_stream(group);
         if (async_enabled()) {
             switch (lw_) {
-                case 8: launch_op_async<8>(op, Q, grid, stream_); break;
-                case 16: launch_op_async<16>(op, Q, grid, stream_); break;
-                case 32: launch_op_async<32>(op, Q, grid, stream_); break;
-                default: launch_op_async<64>(op, Q, grid, stream_); break;
+                case 8: launch_op_async<8>(op, Q, grid, st); break;
+                case 16: launch_op_async<16>(op, Q, grid, st); break;
+                case 32: launch_op_async<32>(op, Q, grid, st); break;
+                default: launch_op_async<64>(op, Q, grid, st); break;
             }
             return;
         }
         switch (lw_) {
-            case 8: launch_op<8>(op, Q, grid, stream_); break;
-            case 16: launch_op<16>(op, Q, grid, stream_); break;
-            case 32: launch_op<32>(op, Q, grid, stream_); break;
-            default: launch_op<64>(op, Q, grid, stream_); break;
+            case 8: launch_op<8>(op, Q, grid, st); break;
+            case 16: launch_op<16>(op, Q, grid, st); break;
+            case 32: launch_op<32>(op, Q, grid, st); break;
+            default: launch_op<64>(op, Q, grid, st); break;
         }
     });
+    fan_end();
 }
 
 // ---- wide2: lane-per-candidate kernel --------------------------------------------------------
@@ -1116,14 +1173,17 @@ void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
             st_.enumerate_launches++;
             return;
         }
-        for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid) {
+        fan_begin();
+        for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid, int group) {
+            cudaStream_t st = fan_stream(group);
             switch (lw_) {
-                case 8: launch_wide2_op<8>(op, Q, grid, smem, stream_); break;
-                case 16: launch_wide2_op<16>(op, Q, grid, smem, stream_); break;
-                case 32: launch_wide2_op<32>(op, Q, grid, smem, stream_); break;
-                default: launch_wide2_op<64>(op, Q, grid, smem, stream_); break;
+                case 8: launch_wide2_op<8>(op, Q, grid, smem, st); break;
+                case 16: launch_wide2_op<16>(op, Q, grid, smem, st); break;
+                case 32: launch_wide2_op<32>(op, Q, grid, smem, st); break;
+                default: launch_wide2_op<64>(op, Q, grid, smem, st); break;
             }
         });
+        fan_end();
         return;
     }
     const BlockDesc &last_block = lv.blocks.back();
@@ -1145,14 +1205,17 @@ void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
         st_.enumerate_launches++;
         return;
     }
-    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid) {
+    fan_begin();
+    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid, int group) {
+        cudaStream_t st = fan_stream(group);
         switch (lw_) {
-            case 8: launch_op_wide<8>(op, Q, grid, stream_); break;
-            case 16: launch_op_wide<16>(op, Q, grid, stream_); break;
-            case 32: launch_op_wide<32>(op, Q, grid, stream_); break;
-            default: launch_op_wide<64>(op, Q, grid, stream_); break;
+            case 8: launch_op_wide<8>(op, Q, grid, st); break;
+            case 16: launch_op_wide<16>(op, Q, grid, st); break;
+            case 32: launch_op_wide<32>(op, Q, grid, st); break;
+            default: launch_op_wide<64>(op, Q, grid, st); break;
         }
     });
+    fan_end();
 }
 
 // ---- partitioned path (narrow_part.cuh) ------------------------------------------------------
