@@ -281,7 +281,8 @@ def main() -> int:
     # DRAM bytes the enumerate kernels actually moved in one search: from the committed ncu pass of
     # this workload (dram__bytes_read.sum + dram__bytes_write.sum summed over the enumerate launches)
     traffic, traffic_src = None, None
-    prof = ROOT / "profiles" / f"r01_s2_dram_{args.workload}.json"
+    profs = sorted((ROOT / "profiles").glob(f"r*_dram_{args.workload}.json"))  # the latest committed pass
+    prof = profs[-1] if profs else ROOT / "profiles" / "none"
     if prof.exists():
         pj = json.loads(prof.read_text())
         traffic, traffic_src = pj["enumerate_dram_bytes"], f"profiles/{prof.name} (bytes per search over {pj['enumerate_launches']} enumerate launches)"

@@ -662,6 +662,12 @@ u64 Engine::grown_size(u64 want_slots) const {
 // Fresh table of `slots` entries holding every finalised CM (val = global id).
 void Engine::rebuild_table(u64 slots) {
     const double t0 = monotonic_s();
+    cudaEvent_t tev[2] = {nullptr, nullptr};
+    if (g_phase.on) {  // LTLB200_TIMING: device time of this rebuild (synchronises; measurement only)
+        for (auto &e : tev) CUDA_CHECK(cudaEventCreate(&e));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        CUDA_CHECK(cudaEventRecord(tev[0], stream_));
+    }
     slots = std::max<u64>(next_pow2(slots), kMinSlots);
     if (slots > (1ull << 32) - 2) throw MemoryBudget("hash set would exceed 2^32 slots");
     if (wide_) {
@@ -692,6 +698,15 @@ void Engine::rebuild_table(u64 slots) {
             CUDA_CHECK(cudaGetLastError());
             st_.kernel_launches++;
         }
+    }
+    if (g_phase.on) {
+        CUDA_CHECK(cudaEventRecord(tev[1], stream_));
+        CUDA_CHECK(cudaEventSynchronize(tev[1]));
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, tev[0], tev[1]));
+        fprintf(stderr, "[ltlb200 timing] rebuild_table: %llu slots, %llu stored CMs: %.3f ms on the device, %.3f ms host\n",
+                (unsigned long long)slots, (unsigned long long)total_, ms, 1e3 * (monotonic_s() - t0));
+        for (auto &e : tev) cudaEventDestroy(e);
     }
     table_dirty_ = false;
     st_.table_rebuilds++;

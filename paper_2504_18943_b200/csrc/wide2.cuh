@@ -25,11 +25,15 @@
 namespace ltlb200 {
 
 // CTAs per SM: 2..6 measure the same on c5 (the big levels run at ~70 % of the random-access
-// ceiling of the memory system, not at an occupancy limit); 4 = 128 registers, no spills.
+// ceiling of the memory system, not at an occupancy limit); 3 leaves 168 registers for the row prefetch.
 #ifndef LTLB200_WIDE2_MIN_CTAS
-#define LTLB200_WIDE2_MIN_CTAS 4
+#define LTLB200_WIDE2_MIN_CTAS 3
 #endif
 constexpr int W2_BATCH = 2;        // candidates a lane carries through the passes together
+#ifndef LTLB200_W2_PREFETCH
+#define LTLB200_W2_PREFETCH 4
+#endif
+constexpr int W2_PREFETCH = LTLB200_W2_PREFETCH;  // vectors of a stored row fetched ahead of the full-row compare
 constexpr int W2_SC_VECS = 512;    // uint4 vectors of scalar-operand rows staged per warp (8 KiB)
 constexpr int W2_TERMS = 128;      // max scalar rows per tile
 
@@ -160,17 +164,31 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
             diff[r] = 0u;
         }
         const bool any_claim = __any_sync(0xFFFFFFFFu, claim[0] || claim[W2_BATCH - 1]);
+        // The stored rows of the fingerprint matches are fetched W2_PREFETCH vectors ahead of the compare: taken one
+        // at a time (load, compare, next vector) a 128-byte CM costs eight dependent trips to the L2 / DRAM, and
+        // the first ncu capture had a third of this kernel's stall samples on exactly that compare.
 #pragma unroll 1
-        for (int p = 0; p < nvec; ++p) {
-            const uint4 valid = W.consts[p];
+        for (int p0 = 0; p0 < nvec; p0 += W2_PREFETCH) {
+            uint4 stored[W2_BATCH][W2_PREFETCH];
 #pragma unroll
-            for (int r = 0; r < W2_BATCH; ++r) {
-                if (!claim[r] && !match[r]) continue;
-                uint4 a, b;
-                gen(r, p, a, b);
-                const uint4 c = cm_apply<LW, OP>(a, b, valid);
-                if (claim[r]) P.stage_rows[entry[r] * nvec + p] = c;
-                else diff[r] |= v_diff(c, __ldcg(row[r] + p));
+            for (int r = 0; r < W2_BATCH; ++r)
+#pragma unroll
+                for (int q = 0; q < W2_PREFETCH; ++q)
+                    if (match[r] && p0 + q < nvec) stored[r][q] = __ldcg(row[r] + p0 + q);
+#pragma unroll
+            for (int q = 0; q < W2_PREFETCH; ++q) {
+                const int p = p0 + q;
+                if (p >= nvec) break;
+                const uint4 valid = W.consts[p];
+#pragma unroll
+                for (int r = 0; r < W2_BATCH; ++r) {
+                    if (!claim[r] && !match[r]) continue;
+                    uint4 a, b;
+                    gen(r, p, a, b);
+                    const uint4 c = cm_apply<LW, OP>(a, b, valid);
+                    if (claim[r]) P.stage_rows[entry[r] * nvec + p] = c;
+                    else diff[r] |= v_diff(c, stored[r][q]);
+                }
             }
         }
         if (any_claim) __threadfence();  // rows before the words that publish them
