@@ -201,6 +201,43 @@ static void pinned_put(u64 *p) {
     g_pinned_free.push_back(p);
 }
 
+// Streams and events of a handle, recycled process-wide: a caller that runs one search per specification
+// creates and destroys a handle per search, and creating five streams and ten events costs more than the
+// small levels of the search (the end-to-end time of spec2 rose by 0.6 ms when the side streams were added).
+struct StreamBundle {
+    cudaStream_t own = nullptr;  // the handle's stream when the caller passed none
+    cudaEvent_t ev[4] = {};      // timing: enumerate begin/end, finalise begin/end
+    cudaStream_t side[4] = {};   // operator fan-out (Engine::fan_*)
+    cudaEvent_t fork = nullptr, join[4] = {};
+};
+static std::mutex g_bundle_mu;
+static std::map<int, std::vector<StreamBundle>> g_bundles;
+
+static StreamBundle bundle_get(int dev) {
+    {
+        std::lock_guard<std::mutex> lock(g_bundle_mu);
+        auto &pool = g_bundles[dev];
+        if (!pool.empty()) {
+            StreamBundle b = pool.back();
+            pool.pop_back();
+            return b;
+        }
+    }
+    StreamBundle b;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&b.own, cudaStreamNonBlocking));
+    for (auto &e : b.ev) CUDA_CHECK(cudaEventCreate(&e));
+    for (auto &st : b.side) CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
+    for (auto &e : b.join) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return b;
+}
+
+// (every stream of the bundle has drained: the handle synchronises before it lets go)
+static void bundle_put(int dev, const StreamBundle &b) {
+    std::lock_guard<std::mutex> lock(g_bundle_mu);
+    g_bundles[dev].push_back(b);
+}
+
 // ---- small device kernels shared by both key widths --------------------------------
 
 // exclusive scan of per-superblock popcounts, 1024 values per CTA; block totals go to `sums`
@@ -315,6 +352,7 @@ private:
     int device_;
     cudaStream_t stream_ = nullptr;
     bool own_stream_ = false;
+    StreamBundle res_;  // recycled streams / events (ev_, side_, fork_ev_, join_ev_ below are copies of its handles)
     u64 budget_ = 0, held_ = 0;
     uint4 valid_{}, target_{};
     bool special_possible_ = false;
@@ -519,9 +557,10 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     wide_ = nvec_ > 1;
     if (nvec_ > MAX_NVEC) throw std::invalid_argument("CMs wider than 512 bytes are not supported");
     for (log2g_ = wide_ ? 1 : 0; (1 << log2g_) < nvec_; ++log2g_) {}
+    res_ = bundle_get(device_);
     if (stream) stream_ = (cudaStream_t)stream;
     else {
-        CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        stream_ = res_.own;
         own_stream_ = true;
     }
     PHASE(9, "create: stream", tp);
@@ -565,10 +604,10 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     CUDA_CHECK(cudaMemcpyAsync(d_valid_, h_rows.data(), h_rows.size() * sizeof(uint4), cudaMemcpyHostToDevice, stream_));
     st_.h2d_bytes += h_rows.size() * sizeof(uint4);
     h_counters_ = pinned_get();
-    for (auto &e : ev_) CUDA_CHECK(cudaEventCreate(&e));
-    for (auto &st : side_) CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    CUDA_CHECK(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
-    for (auto &e : join_ev_) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int k = 0; k < 4; ++k) ev_[k] = res_.ev[k];
+    for (int k = 0; k < kSideStreams; ++k) side_[k] = res_.side[k];
+    fork_ev_ = res_.fork;
+    for (int k = 0; k < kSideStreams; ++k) join_ev_[k] = res_.join[k];
     u64 init[CTR_COUNT];
     for (auto &c : init) c = 0;
     init[CTR_SPECIAL] = VAL_EMPTY;
@@ -635,14 +674,10 @@ Engine::~Engine() {
     recycle_retired(true);
     pinned_put(h_counters_);
     g_phase.dump();
-    for (auto &e : ev_)
-        if (e) cudaEventDestroy(e);
-    for (auto &st : side_)
-        if (st) cudaStreamDestroy(st);
-    if (fork_ev_) cudaEventDestroy(fork_ev_);
-    for (auto &e : join_ev_)
-        if (e) cudaEventDestroy(e);
-    if (own_stream_) cudaStreamDestroy(stream_);
+    if (res_.own) {
+        cudaStreamSynchronize(stream_);  // (side streams are joined into it at the end of every fan-out)
+        bundle_put(device_, res_);
+    }
 }
 
 // Regrowing re-inserts every stored CM and clears the new set, so it should be rare while it is
