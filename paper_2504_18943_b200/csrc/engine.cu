@@ -389,6 +389,10 @@ private:
     DeviceArray<u64> pc_;
     int part_occupancy_ = 2;
     bool store_has_separator_ = false;  // some stored CM separates: a separating candidate need not be fresh
+    // Associativity pruning (narrow.cuh: run_binary_tile) is sound while every stored level is complete and
+    // all levels were built with one operator set; the first cut level or change of operators ends it.
+    bool prune_ok_ = true;
+    uint32_t prune_mask_ = 0;  // operator set of the levels built so far (0 = none yet)
     static bool partition_enabled();
     bool use_partition(u64 constructed) const;
     void launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles);
@@ -756,6 +760,8 @@ void Engine::reset() {
     approx_bytes_ = 0;
     last_constructed_ = 0;
     store_has_separator_ = false;
+    prune_ok_ = true;
+    prune_mask_ = 0;
     rebuild_table(kMinSlots);  // small levels probe an L2-resident set again; it regrows with the search
     st_.constructed = 0;
     st_.unique = 0;
@@ -855,6 +861,23 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
                 b.kind = BK_RECT;
                 b.vec_is_b = lb.n >= la.n;
                 b.size = la.n * lb.n;
+            }
+            b.c_left = (uint32_t)c1;
+            if (tag == OP_AND && !wide_) {
+                // left operand rows that are AND nodes; right operand rows that are AND nodes whose left child
+                // costs less than c1 (AND blocks of a level are contiguous, in ascending order of their left cost)
+                auto and_range = [](const LevelMeta &lv, uint32_t left_cost_below, u64 &lo, u64 &hi) {
+                    lo = hi = 0;
+                    bool any = false;
+                    for (const BlockDesc &q : lv.blocks) {
+                        if (q.op != (uint32_t)OP_AND || q.c_left >= left_cost_below) continue;
+                        if (!any) lo = q.ord0;
+                        hi = q.ord0 + q.size;
+                        any = true;
+                    }
+                };
+                and_range(la, ~0u, b.skip_a_lo, b.skip_a_hi);
+                and_range(lb, (uint32_t)c1, b.skip_b_lo, b.skip_b_hi);
             }
             push(b);
         }
@@ -1473,9 +1496,12 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     *sep_ord_out = VAL_EMPTY;
     *n_seps_out = 0;
     if (deadline >= 0 && monotonic_s() > deadline) {  // engine.py:416-417, before the first chunk
+        prune_ok_ = false;
         levels_.push_back(pl.lv);
         return LTLB200_TIME_BUDGET;
     }
+    if (prune_mask_ == 0) prune_mask_ = op_mask;
+    else if (prune_mask_ != op_mask) prune_ok_ = false;  // (see prune_ok_)
     u64 n_tiles = 0;
     double tp = monotonic_s();
     plan_level(cost, op_mask, pl.lv, pl.constructed, n_tiles);
@@ -1566,6 +1592,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         g_last_error = e.what();
         table_dirty_ = true;
         pl.active = false;
+        prune_ok_ = false;
         levels_.push_back(LevelMeta{0, total_, {}});
         return LTLB200_MEMORY_BUDGET;
     }
@@ -1601,6 +1628,11 @@ NarrowParams Engine::narrow_params(bool exhaustive) const {
     P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
     P.shard_stride = 1;
     P.shard_offset = 0;
+    static const bool prune_on = [] {  // LTLB200_PRUNE=0: every AND candidate is probed
+        const char *e = getenv("LTLB200_PRUNE");
+        return !(e && e[0] == '0');
+    }();
+    P.ords = prune_on && prune_ok_ && total_ ? ords_.ptr : nullptr;
     return P;
 }
 
@@ -1744,10 +1776,12 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
     } catch (const MemoryBudget &e) {
         g_last_error = e.what();
         table_dirty_ = true;
+        prune_ok_ = false;
         levels_.push_back(LevelMeta{0, total_, {}});
         return LTLB200_MEMORY_BUDGET;
     }
     const bool found_cut = !exhaustive && sep_ord != VAL_EMPTY;
+    if (found_cut) prune_ok_ = false;  // the level keeps only what precedes its separator: no longer complete
     *constructed_delta = (int64_t)(found_cut ? constructed_through(lv, sep_ord, (u64)batch) : constructed);
     last_constructed_ = constructed;
     *n_new = (int64_t)lv.n;
@@ -1918,10 +1952,12 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         g_last_error = e.what();
         table_dirty_ = true;
         pl.active = false;
+        prune_ok_ = false;
         levels_.push_back(LevelMeta{0, total_, {}});
         return LTLB200_MEMORY_BUDGET;
     }
     const bool found_cut = !exhaustive && sep_ord != VAL_EMPTY;
+    if (found_cut) prune_ok_ = false;  // the level keeps only what precedes its separator: no longer complete
     *constructed_delta = (int64_t)(found_cut ? constructed_through(lv, sep_ord, (u64)batch) : constructed);
     last_constructed_ = constructed;
     *n_new = (int64_t)lv.n;

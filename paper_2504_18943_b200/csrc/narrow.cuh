@@ -73,6 +73,12 @@ struct BlockDesc {
     u64 size;             // candidates in the block
     u64 tile0;            // first tile index of the block in the level's flattened tile space
     u64 tiles_v, tiles_s;
+    // Associativity pruning (AND blocks of a store whose levels are all complete and were built with one
+    // operator set): an operand row whose own winning ordinal lies in [lo, hi) makes the candidate a
+    // duplicate by construction (run_binary_tile).  Left operand: it is itself an AND node.  Right operand:
+    // it is an AND node whose left child costs less than this block's left operand.  lo == hi: no such rows.
+    u64 skip_a_lo, skip_a_hi, skip_b_lo, skip_b_hi;
+    uint32_t c_left;  // cost of the left operand level (0 for unary blocks)
     uint32_t vg;  // vector groups (of 32 rows) per tile; > 1 when the scalar operand has few rows
     uint32_t tile_s;  // scalar rows per tile (<= TILE_S) or, for unary blocks, candidates per lane per tile;
                       // the host shrinks tiles of small blocks so that they still spread over the whole GPU
@@ -99,6 +105,7 @@ struct NarrowParams {
     int special_possible;
     u64 *sep_list;  // exhaustive runs: ordinals of every separating candidate (NULL otherwise)
     u64 sep_list_cap;
+    const u64 *ords;  // winning ordinal of every finalised CM by global id, or NULL: no associativity pruning
 };
 
 // [1] claim indices reserved, [2] separator ordinal (min), [3] special-key val (persists across levels),
@@ -442,12 +449,30 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
     if (tile_min > sep_now) return false;
     const uint4 *vec_rows = P.store + (VEC_B ? B.b_off : B.a_off);
     const uint4 *sc_rows = P.store + (VEC_B ? B.a_off : B.b_off);
+    // Associativity pruning.  (x & y) & r has the same CM as x & (y & r): the CM of y & r is in the cache
+    // (its level is complete), at a cost that puts x & rep(y & r) either in an earlier level -- then the CM
+    // is an older one -- or in this level in a block whose left operand costs cost(x) < cost(x & y), i.e.
+    // at a smaller ordinal.  Either way the candidate never wins its CM: it is a duplicate by
+    // construction (`known`), like one that equals an operand.  Mirrored for l & (y & z) when
+    // cost(y) < cost(l).  The test is a range check on the operand row's own winning ordinal (AND blocks
+    // are contiguous in a level's canonical order, by ascending left cost); bit 63 of `term` carries it
+    // for the staged rows.
+    constexpr u64 SKIP_BIT = 1ull << 63;
+    const bool prune = (OP == OP_AND) && P.ords != nullptr;
+    const u64 sc_lo = VEC_B ? B.skip_a_lo : B.skip_b_lo, sc_hi = VEC_B ? B.skip_a_hi : B.skip_b_hi;
+    const u64 vec_lo = VEC_B ? B.skip_b_lo : B.skip_a_lo, vec_hi = VEC_B ? B.skip_b_hi : B.skip_a_hi;
+    const u64 *sc_ords = P.ords + (VEC_B ? B.a_off : B.b_off), *vec_ords = P.ords + (VEC_B ? B.b_off : B.a_off);
     __syncwarp();
     for (int k = lane; k < s_cnt; k += 32) {
         const u64 s = s0 + k;
         ws.rows[k] = __ldg(sc_rows + s);
         // scalar-row part of the ordinal; the lane part is j (VEC_B) or ord0 + i*nb (!VEC_B)
-        ws.term[k] = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
+        u64 term = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
+        if (prune && sc_hi > sc_lo) {
+            const u64 o = __ldg(sc_ords + s);
+            if (o >= sc_lo && o < sc_hi) term |= SKIP_BIT;
+        }
+        ws.term[k] = term;
     }
     __syncwarp();
     // the vector row of the NEXT group is loaded while this group is processed
@@ -459,6 +484,11 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
         const bool v_ok = v < n_vec;
         const uint4 xv = xv_next;
         if (vg + 1 < vg_n && v + TILE_V < n_vec) xv_next = __ldg(vec_rows + v + TILE_V);
+        bool skip_v = false;
+        if (prune && vec_hi > vec_lo && v_ok) {
+            const u64 o = __ldg(vec_ords + v);
+            skip_v = o >= vec_lo && o < vec_hi;
+        }
         const u64 lane_term = VEC_B ? v : ord0 + v * nb;
         // triangle: row s0+sr pairs with columns j >= i only
         const int first_bad = tri ? (v >= s0 ? (int)min((u64)s_cnt, v - s0 + 1) : 0) : s_cnt;
@@ -467,13 +497,14 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
         for (int g = 0; g < s_cnt; g += PROBE_BATCH) {
             uint4 cand[PROBE_BATCH];
             bool live[PROBE_BATCH], known[PROBE_BATCH];
-            auto ord_of = [&](int r) { return ws.term[min(g + r, s_cnt - 1)] + lane_term; };
+            auto ord_of = [&](int r) { return (ws.term[min(g + r, s_cnt - 1)] & ~SKIP_BIT) + lane_term; };
 #pragma unroll
             for (int r = 0; r < PROBE_BATCH; ++r) {
                 const uint4 xs = ws.rows[min(g + r, s_cnt - 1)];
                 live[r] = g + r < s_live;
                 cand[r] = VEC_B ? cm_apply<LW, OP>(xs, xv, P.valid) : cm_apply<LW, OP>(xv, xs, P.valid);
                 known[r] = v_eq(cand[r], xs) || v_eq(cand[r], xv);
+                if (prune) known[r] = known[r] || skip_v || (ws.term[min(g + r, s_cnt - 1)] & SKIP_BIT) != 0ull;
             }
             sink.template emit<LW>(cand, live, known, ord_of);
         }
@@ -534,10 +565,10 @@ __device__ __forceinline__ bool open_tile(const NarrowParams &P, WS &ws, const T
         bi += __popc(m);
         if (m != 0xFFFFFFFFu) break;
     }
-    static_assert(sizeof(BlockDesc) % 4 == 0 && sizeof(BlockDesc) / 4 <= 32, "descriptor copied one word per lane");
+    static_assert(sizeof(BlockDesc) % 4 == 0 && sizeof(BlockDesc) / 4 <= 64, "descriptor copied two words per lane at most");
     __syncwarp();
-    if (lane < (int)(sizeof(BlockDesc) / 4))
-        reinterpret_cast<uint32_t *>(&ws.block)[lane] = reinterpret_cast<const uint32_t *>(&P.blocks[bi])[lane];
+    for (int w = lane; w < (int)(sizeof(BlockDesc) / 4); w += 32)
+        reinterpret_cast<uint32_t *>(&ws.block)[w] = reinterpret_cast<const uint32_t *>(&P.blocks[bi])[w];
     if (lane == 0) {
         ws.ticket = t;
         ws.sep_now = sep;

@@ -10,6 +10,7 @@ cases in a child process:
                         were read) instead of the deferred, device-bounded finalisation
   LTLB200_WIDE2=0       multi-vector CMs by wide.cuh's group-per-candidate kernel instead of
                         wide2.cuh's lane-per-candidate kernel (the default)
+  LTLB200_PRUNE=0       no associativity pruning: every AND candidate is probed
   LTLB200_OPSTREAMS=0   every operator launch of a level on the engine's own stream, one after the
                         other, instead of fanned out over side streams (the default)
 
@@ -42,7 +43,8 @@ print("variant ok")
 
 @pytest.mark.parametrize("switch,value,cases", [("LTLB200_PARTITION", "1", CASES), ("LTLB200_ASYNC", "1", CASES),
                                                  ("LTLB200_NO_DEFER", "1", CASES), ("LTLB200_WIDE2", "0", WIDE_CASES),
-                                                 ("LTLB200_OPSTREAMS", "0", CASES + WIDE_CASES)])
+                                                 ("LTLB200_OPSTREAMS", "0", CASES + WIDE_CASES),
+                                                 ("LTLB200_PRUNE", "0", CASES)])
 def test_variant_matches_reference(switch, value, cases):
     env = dict(os.environ)
     env[switch] = value
