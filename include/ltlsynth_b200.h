@@ -162,6 +162,14 @@ double ltlb200_now(void);
 /* _Level.n / _Level.base (engine.py:101-111).  cost is 1-based. */
 int ltlb200_level_info(const ltlb200_engine *e, int32_t cost, int64_t *n, int64_t *base);
 
+/*
+ * Number of candidates the next level (cost = levels built + 1) constructs when it is built in full: the sum of
+ * the chunk sizes of _tasks_for_level (engine.py:219-266), a closed form of the stored level sizes.  Identical
+ * on every rank of a sharded search, which is what lets the ranks agree without communication to build a
+ * small level redundantly instead of sharding it (dist.py).
+ */
+int ltlb200_level_candidates(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int64_t *n);
+
 /* Number of levels built (len(store.levels)). */
 int32_t ltlb200_num_levels(const ltlb200_engine *e);
 

@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "ltlb200_key_bytes",
     "ltlb200_now",
     "ltlb200_level_info",
+    "ltlb200_level_candidates",
     "ltlb200_num_levels",
     "ltlb200_level_copy",
     "ltlb200_entry",
@@ -126,6 +127,8 @@ def load():
     L.ltlb200_now.restype = dbl
     L.ltlb200_level_info.restype = ctypes.c_int
     L.ltlb200_level_info.argtypes = [p, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.ltlb200_level_candidates.restype = ctypes.c_int
+    L.ltlb200_level_candidates.argtypes = [p, i32, ctypes.c_uint32, ctypes.POINTER(i64)]
     L.ltlb200_num_levels.restype = i32
     L.ltlb200_num_levels.argtypes = [p]
     L.ltlb200_level_copy.restype = ctypes.c_int

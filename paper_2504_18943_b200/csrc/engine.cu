@@ -327,6 +327,7 @@ public:
     int expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline,
                      int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
     int level_info(int cost, int64_t *n, int64_t *base) const;
+    int64_t level_candidates(int cost, uint32_t op_mask);
     int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
@@ -2064,6 +2065,15 @@ u64 Engine::seps_copy(u64 *out, u64 cap) {
     return n;
 }
 
+// candidates the next level would construct in full (the closed form of engine.py:219-266: sum of the block sizes)
+int64_t Engine::level_candidates(int cost, uint32_t op_mask) {
+    if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
+    LevelMeta lv;
+    u64 constructed = 0, n_tiles = 0;
+    plan_level(cost, op_mask, lv, constructed, n_tiles);
+    return (int64_t)constructed;
+}
+
 int Engine::level_info(int cost, int64_t *n, int64_t *base) const {
     if (cost < 1 || cost > (int)levels_.size()) return LTLB200_ERR_ARGUMENT;
     *n = (int64_t)levels_[cost - 1].n;
@@ -2265,6 +2275,14 @@ double ltlb200_now(void) { return ltlb200::monotonic_s(); }
 int ltlb200_level_info(const ltlb200_engine *e, int32_t cost, int64_t *n, int64_t *base) {
     if (!e || !n || !base) return LTLB200_ERR_ARGUMENT;
     return e->impl->level_info(cost, n, base);
+}
+
+int ltlb200_level_candidates(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int64_t *n) {
+    if (!e || !n) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        *n = e->impl->level_candidates(cost, op_mask);
+        return LTLB200_OK;
+    });
 }
 
 int32_t ltlb200_num_levels(const ltlb200_engine *e) { return e ? e->impl->num_levels() : 0; }

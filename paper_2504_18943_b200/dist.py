@@ -23,6 +23,7 @@ a numpy stand-in.  Collectives move torch tensors that live wherever the engine 
 
 from __future__ import annotations
 
+import os
 import time
 from typing import Protocol
 
@@ -46,6 +47,12 @@ from .traces import validate_feasible
 
 NO_SEPARATOR = (1 << 64) - 1
 
+# Levels with fewer candidates than this are built REDUNDANTLY on every rank instead of being sharded: the
+# cache is replicated and the engine is deterministic, so every rank gets the same level without a single
+# data-path collective, and a level of a few thousand candidates costs less than one exchange.  The count is
+# a closed form of the stored level sizes (`level_candidates`), hence identical on every rank.
+REPLICATE_BELOW = int(os.environ.get("LTLB200_REPLICATE_BELOW", str(1 << 22)))
+
 
 class ShardEngine(Protocol):
     """What the exchange needs from a store (CandidateStore implements it on the GPU)."""
@@ -67,6 +74,12 @@ class ShardEngine(Protocol):
 
     def level_end(self, sep_ord: int, seps, batch_size: int, memory_budget_bytes: int):
         """-> (status, n_new, sep_gid or None, constructed_delta)"""
+
+    # optional: without these two every level is sharded
+    def level_candidates(self, cost: int, op_mask: int) -> int: ...
+
+    def expand_local(self, cost: int, op_mask: int, exhaustive: bool, batch_size: int, memory_budget_bytes: int, deadline):
+        """-> (status, n_new, sep_gid or None, constructed_delta): the whole level on this rank"""
 
 
 def _all_to_all_v(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group) -> torch.Tensor:
@@ -124,6 +137,19 @@ def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfi
     stats = stats if stats is not None else RunStats()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     mask = operator_mask(ops)
+    if hasattr(store, "level_candidates") and hasattr(store, "expand_local") \
+            and store.level_candidates(cost, mask) < REPLICATE_BELOW:
+        # small level: every rank builds all of it (see REPLICATE_BELOW); only the budget status is agreed on,
+        # because the time budget is read from each rank's own clock
+        status, n_new, sep_gid, delta = store.expand_local(cost, mask, config.exhaustive, config.batch_size,
+                                                           config.memory_budget_mb << 20, deadline)
+        flag = torch.tensor([status], dtype=torch.int64, device=_device_of(store))
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+        stats.constructed += delta
+        stats.unique = store.total
+        if int(flag.item()) in _FAILURE_TEXT:
+            raise _BudgetExceeded(_FAILURE_TEXT[int(flag.item())])
+        return n_new, sep_gid
     status, _, sep_local, _ = store.level_begin(cost, mask, config.exhaustive, deadline, rank, world)
 
     # a budget stop must be collective: every rank stops or none does

@@ -212,6 +212,18 @@ class CandidateStore:
         return status, n_new.value, (None if sep.value < 0 else sep.value), delta.value
 
     # -- shard-engine interface used by dist.sharded_expand_level (one search over several GPUs) ----
+    def level_candidates(self, cost: int, op_mask: int) -> int:
+        """Candidates level ``cost`` constructs when built in full (same number on every rank)."""
+        n = ctypes.c_int64()
+        _native.check(_native.load().ltlb200_level_candidates(self._handle, cost, op_mask, ctypes.byref(n)),
+                      f"level_candidates({cost})")
+        return int(n.value)
+
+    def expand_local(self, cost, op_mask, exhaustive, batch_size, memory_budget_bytes, deadline):
+        """The whole level on this device (``_expand``): what a sharded search does for its small levels."""
+        native_deadline = None if deadline is None else _monotonic() + (deadline - time.perf_counter())
+        return self._expand(cost, op_mask, exhaustive, batch_size, memory_budget_bytes, native_deadline)
+
     @property
     def key_bytes(self) -> int:
         return int(_native.load().ltlb200_key_bytes(self._handle))

@@ -188,6 +188,15 @@ class CpuShardEngine:
                              exhaustive=exhaustive)
         return 0, len(claims), sep_local, len(seps)
 
+    def level_candidates(self, cost, op_mask):
+        return self._blocks(cost, op_mask)[1]
+
+    def expand_local(self, cost, op_mask, exhaustive, batch_size, memory_budget_bytes, deadline):
+        """The whole level on this rank: what dist.py does for levels below REPLICATE_BELOW."""
+        _, _, sep_local, _ = self.level_begin(cost, op_mask, exhaustive, deadline, 0, 1)
+        seps = torch.tensor(self._pending["seps"], dtype=torch.int64) if exhaustive else None
+        return self.level_end(sep_local, seps, batch_size, memory_budget_bytes)
+
     def _owner(self, key: bytes, owners: int) -> int:
         return zlib.crc32(key) % owners
 

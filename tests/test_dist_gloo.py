@@ -25,12 +25,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(tmp_path, workload, seed, max_cost, exhaustive, ops=DEFAULT_OPS, world=2):
+def _run(tmp_path, workload, seed, max_cost, exhaustive, ops=DEFAULT_OPS, world=2, replicate_below=0):
+    """replicate_below: levels with fewer candidates are built redundantly on every rank (dist.REPLICATE_BELOW);
+    0 = every level goes through the exchange."""
     port = _free_port()
     out = tmp_path / "report"
     procs = []
     for rank in range(world):
-        env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   LTLB200_REPLICATE_BELOW=str(replicate_below))
         procs.append(subprocess.Popen(
             [sys.executable, str(ROOT / "tests" / "dist_worker.py"), workload, str(seed), str(max_cost),
              "1" if exhaustive else "0", ops, str(out)], env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
@@ -60,3 +63,12 @@ def test_two_ranks_wide_rows_and_or_operator(tmp_path):
 def test_three_ranks_c1(tmp_path):
     rep = _run(tmp_path, "c1", 4, 9, exhaustive=False, world=3)
     assert rep["formula"] == "!F !(!F p1 U p0)"
+
+
+def test_small_levels_replicated_large_levels_sharded(tmp_path):
+    # levels under 200 candidates are built on every rank without an exchange, the rest are sharded:
+    # the mix must give the same levels as the all-sharded run and as the oracle
+    mixed = _run(tmp_path, "c1", 4, 9, exhaustive=False, replicate_below=200)
+    assert mixed["formula"] == "!F !(!F p1 U p0)"
+    everything_local = _run(tmp_path, "spec1", 0, 6, exhaustive=True, replicate_below=1 << 30)
+    assert everything_local["levels"] == [3, 8, 14, 21, 32, 34]

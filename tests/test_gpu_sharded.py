@@ -97,13 +97,18 @@ def test_protocol_over_nccl_with_one_rank():
         port = sock.getsockname()[1]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    default_threshold = pdist.REPLICATE_BELOW
     try:
         spec = workloads.spec2()
         cfg = engine.EngineConfig(max_cost=11, exhaustive=True, memory_budget_mb=1 << 20)
-        res = pdist.synthesize_sharded(spec, cfg)
         want = oracle.synthesize(spec, max_cost=11, exhaustive=True)
-        assert (res.outcome, res.stats.unique, res.stats.constructed) == (want.outcome, want.unique, want.constructed)
-        res = pdist.synthesize_sharded(workloads.spec1(), engine.EngineConfig())
-        assert to_text(res.formula, workloads.spec1().alphabet) == "!(b U a)"
+        # every level through the exchange / levels under 10,000 candidates built locally / (default) all local
+        for replicate_below in (0, 10_000, default_threshold):
+            pdist.REPLICATE_BELOW = replicate_below
+            res = pdist.synthesize_sharded(spec, cfg)
+            assert (res.outcome, res.stats.unique, res.stats.constructed) == (want.outcome, want.unique, want.constructed)
+            res = pdist.synthesize_sharded(workloads.spec1(), engine.EngineConfig())
+            assert to_text(res.formula, workloads.spec1().alphabet) == "!(b U a)"
     finally:
+        pdist.REPLICATE_BELOW = default_threshold
         dist.destroy_process_group()
