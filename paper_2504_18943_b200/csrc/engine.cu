@@ -394,6 +394,13 @@ private:
     // all levels were built with one operator set; the first cut level or change of operators ends it.
     bool prune_ok_ = true;
     uint32_t prune_mask_ = 0;  // operator set of the levels built so far (0 = none yet)
+    // Non-exhaustive level over a store that already holds a separating CM (narrow path, one GPU): the chunks
+    // the reference truncates at a separating candidate are found by a scan pass and their tails excluded
+    // from the enumeration (NarrowParams::dead).  batch_size is known to expand_level only.
+    DeviceArray<u64> dead_;
+    u64 dead_n_ = 0;
+    int64_t mode_batch_ = 0;
+    void collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch);
     static bool partition_enabled();
     bool use_partition(u64 constructed) const;
     void launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles);
@@ -657,6 +664,7 @@ Engine::~Engine() {
     release(store_);
     release(ords_);
     release(slots_);
+    release(dead_);
     release(claim_key_);
     release(claim_ord_);
     release(wslots_);
@@ -1130,6 +1138,24 @@ void Engine::fan_end() {
 void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
     const BlockDesc &last_block = lv.blocks.back();
     const u64 level_candidates = last_block.ord0 + last_block.size;
+    if (P.scan_only || P.dead_n) {  // rare mode (collect_dead_ranges): one launch of the guarded kernel, any size
+        P.block_begin = 0;
+        P.block_end = (int)lv.blocks.size();
+        P.tile_begin = 0;
+        P.tile_end = last_block.tile0 + last_block.tiles_v * last_block.tiles_s;
+        P.ticket = CTR_TICKET0;
+        const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
+        switch (lw_) {
+            case 8: narrow_guarded_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            case 16: narrow_guarded_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            case 32: narrow_guarded_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+            default: narrow_guarded_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
+        }
+        CUDA_CHECK(cudaGetLastError());
+        st_.kernel_launches++;
+        st_.enumerate_launches++;
+        return;
+    }
     if (level_candidates <= kSmallLevel && !async_enabled()) {
         P.block_begin = 0;
         P.block_end = (int)lv.blocks.size();
@@ -1482,6 +1508,55 @@ void Engine::launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constru
 // (tile-strided) into the local hash set.  Nothing is appended yet; level_end() does that.
 // `defer` (single-GPU, non-exhaustive, narrow): do not wait for the enumeration -- level_end launches
 // the finalisation right behind it with device-side bounds and synchronises once for both.
+// Scan pass of a non-exhaustive level over a store that already holds a separating CM.  The reference cuts every
+// chunk at its FIRST separating candidate, fresh or not (engine.py:330-335), and goes on with the next chunk
+// until a fresh one ends the level (:425-446): whatever follows such a candidate inside its chunk does not
+// exist for this level.  Here: every separating ordinal is recorded without touching the set, the host walks
+// them chunk by chunk (constructed_through = end of the chunk that holds an ordinal) and the tails become
+// the dead ranges of the enumeration that follows.
+void Engine::collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch) {
+    dead_n_ = 0;
+    u64 want = std::max<u64>(1ull << 20, constructed / 16), n = 0;
+    for (;;) {
+        reserve(sep_list_, want, false);
+        level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+        CUDA_CHECK(cudaGetLastError());
+        NarrowParams Q = narrow_params(false);
+        Q.scan_only = 1;
+        Q.prune_after_sep = 0;
+        Q.sep_list = sep_list_.ptr;
+        Q.sep_list_cap = sep_list_.cap;
+        Q.ords = nullptr;
+        launch_enumerate(Q, lv);
+        read_counters();
+        n = h_counters_[CTR_SEPCOUNT];
+        if (n <= sep_list_.cap) break;
+        want = n;
+    }
+    if (n == 0) return;
+    std::vector<u64> seps((size_t)n);
+    CUDA_CHECK(cudaMemcpyAsync(seps.data(), sep_list_.ptr, n * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += n * sizeof(u64);
+    std::sort(seps.begin(), seps.end());
+    std::vector<u64> ranges;
+    u64 chunk_end = 0;
+    for (u64 o : seps) {
+        if (o < chunk_end) continue;  // not the first separating candidate of its chunk
+        chunk_end = constructed_through(lv, o, batch);
+        if (o + 1 < chunk_end) {
+            ranges.push_back(o + 1);
+            ranges.push_back(chunk_end);
+        }
+    }
+    if (ranges.empty()) return;
+    reserve(dead_, ranges.size(), false);
+    CUDA_CHECK(cudaMemcpyAsync(dead_.ptr, ranges.data(), ranges.size() * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // `ranges` must outlive the copy
+    st_.h2d_bytes += ranges.size() * sizeof(u64);
+    dead_n_ = ranges.size() / 2;
+}
+
 int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
                         u64 *n_claimed_out, u64 *sep_ord_out, u64 *n_seps_out, bool defer) {
     if (pending_.active) throw std::invalid_argument("level_begin: the previous level was not ended");
@@ -1515,6 +1590,12 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         if (table_dirty_) rebuild_table(table_slots());
         CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
         st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
+        dead_n_ = 0;
+        if (!exhaustive && store_has_separator_ && !wide_ && shard_count == 1 && mode_batch_ > 0 && !async_enabled() &&
+            !use_partition(constructed)) {
+            collect_dead_ranges(lv, constructed, (u64)mode_batch_);
+            defer = false;  // (rare mode: the plain two-synchronisation path)
+        }
 
         // expected number of new CMs: everything for small levels, else the previous level's
         // uniqueness with head-room; a wrong guess trips the overflow flag and the level is redone
@@ -1634,6 +1715,9 @@ NarrowParams Engine::narrow_params(bool exhaustive) const {
         return !(e && e[0] == '0');
     }();
     P.ords = prune_on && prune_ok_ && total_ ? ords_.ptr : nullptr;
+    P.dead = dead_n_ ? dead_.ptr : nullptr;
+    P.dead_n = (uint32_t)dead_n_;
+    P.scan_only = 0;
     return P;
 }
 
@@ -1980,11 +2064,18 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     *constructed_delta = 0;
     u64 n_claimed = 0, sep_ord = VAL_EMPTY, n_seps = 0;
     static const bool defer = getenv("LTLB200_NO_DEFER") == nullptr;
+    mode_batch_ = batch;  // (collect_dead_ranges needs the reference's chunk schedule)
     int rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps, defer);
-    if (rc != LTLB200_OK) return rc;
+    if (rc != LTLB200_OK) {
+        mode_batch_ = 0;
+        return rc;
+    }
+    mode_batch_ = 0;
     rc = level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
     if (rc != kRetryLevel) return rc;
+    mode_batch_ = batch;
     rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps, false);
+    mode_batch_ = 0;
     if (rc != LTLB200_OK) return rc;
     return level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
 }

@@ -106,6 +106,12 @@ struct NarrowParams {
     u64 *sep_list;  // exhaustive runs: ordinals of every separating candidate (NULL otherwise)
     u64 sep_list_cap;
     const u64 *ords;  // winning ordinal of every finalised CM by global id, or NULL: no associativity pruning
+    // Non-exhaustive level over a store that already holds a separating CM: the reference truncates every chunk
+    // at its first separating candidate, fresh or not (engine.py:334-335).  `dead` = dead_n sorted, disjoint
+    // ordinal ranges [lo, hi) -- the rest of each such chunk -- whose candidates do not exist for this level.
+    const u64 *dead;
+    uint32_t dead_n;
+    int scan_only;  // the pass that finds those chunks: only record the ordinal of every separating candidate
 };
 
 // [1] claim indices reserved, [2] separator ordinal (min), [3] special-key val (persists across levels),
@@ -378,6 +384,22 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queu
     while (st.qfill >= 32u) drain_round(P, queue, st);
 }
 
+template <class S, class = void>
+struct sink_is_guarded : std::false_type {};
+template <class S>
+struct sink_is_guarded<S, std::void_t<decltype(S::kGuarded)>> : std::bool_constant<S::kGuarded> {};
+
+// true when `ord` lies in one of the level's dead ranges (see NarrowParams::dead); cold path, out of line
+__device__ __noinline__ bool ordinal_is_dead(const u64 *dead, uint32_t n, u64 ord) {
+    uint32_t a = 0, b = n;  // first range whose lo is > ord
+    while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (dead[2 * m] <= ord) a = m + 1;
+        else b = m;
+    }
+    return a > 0 && ord < dead[2 * (a - 1) + 1];
+}
+
 // The tile runners are generic over where candidates go: `sink.emit<LW>(cand, live, known, ord_of)`
 // is the direct insert (DirectSink -> insert_batch) or the bucket scatter of the partitioned
 // path (narrow_part.cuh); WS is the warp's shared state (rows / term / block).
@@ -411,6 +433,11 @@ __device__ __forceinline__ bool run_unary_tile(const NarrowParams &P, WS &ws, Si
         for (int r = 0; r < PROBE_BATCH; ++r) {
             cand[r] = cm_apply<LW, OP>(x[r], x[r], P.valid);
             known[r] = OP != OP_ATOM && v_eq(cand[r], x[r]);
+        }
+        if (sink_is_guarded<Sink>::value && P.dead_n) {
+#pragma unroll
+            for (int r = 0; r < PROBE_BATCH; ++r)
+                if (live[r] && ordinal_is_dead(P.dead, P.dead_n, ord_of(r))) live[r] = false;
         }
         sink.template emit<LW>(cand, live, known, ord_of);
     }
@@ -506,10 +533,27 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
                 known[r] = v_eq(cand[r], xs) || v_eq(cand[r], xv);
                 if (prune) known[r] = known[r] || skip_v || (ws.term[min(g + r, s_cnt - 1)] & SKIP_BIT) != 0ull;
             }
+            if (sink_is_guarded<Sink>::value && P.dead_n) {
+#pragma unroll
+                for (int r = 0; r < PROBE_BATCH; ++r)
+                    if (live[r] && ordinal_is_dead(P.dead, P.dead_n, ord_of(r))) live[r] = false;
+            }
             sink.template emit<LW>(cand, live, known, ord_of);
         }
     }
     return false;
+}
+
+// scan pass (NarrowParams::scan_only): no set, no claims -- the ordinal of every separating candidate, fresh or not
+template <int LW, typename OrdOf>
+__device__ __noinline__ void scan_batch(const NarrowParams &P, const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                        OrdOf ord_of) {
+#pragma unroll
+    for (int r = 0; r < PROBE_BATCH; ++r) {
+        if (!live[r] || cm_sep_diff<LW>(cand[r], P.target) != 0u) continue;
+        const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+        if (pos < P.sep_list_cap) P.sep_list[pos] = ord_of(r);
+    }
 }
 
 struct DirectSink {
@@ -520,6 +564,22 @@ struct DirectSink {
     __device__ __forceinline__ void emit(const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
                                          const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
         insert_batch<LW>(P, ws.queue, st, cand, live, known, ord_of);
+    }
+};
+
+// The sink of narrow_guarded_level_kernel: the scan pass and the enumeration with dead ranges (NarrowParams::dead)
+// of a non-exhaustive level over a store that already holds a separating CM.  Only tile runners instantiated with
+// a guarded sink contain that code, so the hot kernels carry none of it.
+struct GuardedSink {
+    static constexpr bool kGuarded = true;
+    const NarrowParams &P;
+    WarpShared &ws;
+    WarpState &st;
+    template <int LW, typename OrdOf>
+    __device__ __forceinline__ void emit(const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                         const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
+        if (P.scan_only) scan_batch<LW>(P, cand, live, ord_of);
+        else insert_batch<LW>(P, ws.queue, st, cand, live, known, ord_of);
     }
 };
 
@@ -622,6 +682,35 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) narrow_small_level_kernel(cons
     WarpShared &ws = s_warp[threadIdx.x >> 5];
     WarpState st;
     DirectSink sink{P, ws, st};
+    TileFetch next = fetch_tile(P, nullptr);
+    for (;;) {
+        const TileFetch cur = next;
+        if (!open_tile(P, ws, cur)) break;
+        next = fetch_tile(P, nullptr);
+        bool stop;
+        switch (ws.block.op) {
+            case OP_ATOM: stop = run_tile<LW, OP_ATOM>(P, ws, sink); break;
+            case OP_NOT: stop = run_tile<LW, OP_NOT>(P, ws, sink); break;
+            case OP_NEXT: stop = run_tile<LW, OP_NEXT>(P, ws, sink); break;
+            case OP_FUTURE: stop = run_tile<LW, OP_FUTURE>(P, ws, sink); break;
+            case OP_AND: stop = run_tile<LW, OP_AND>(P, ws, sink); break;
+            case OP_UNTIL: stop = run_tile<LW, OP_UNTIL>(P, ws, sink); break;
+            default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
+        }
+        if (stop) break;
+    }
+    if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+        while (st.qfill > 0u) drain_round(P, ws.queue, st);
+}
+
+// Non-exhaustive level over a store that already holds a separating CM (rare: synthesize() stops at the first
+// separator): one launch for every operator like the small-level kernel, with the guarded sink.
+template <int LW>
+__global__ void __launch_bounds__(CTA_THREADS, 1) narrow_guarded_level_kernel(const NarrowParams P) {
+    __shared__ WarpShared s_warp[WARPS_PER_CTA];
+    WarpShared &ws = s_warp[threadIdx.x >> 5];
+    WarpState st;
+    GuardedSink sink{P, ws, st};
     TileFetch next = fetch_tile(P, nullptr);
     for (;;) {
         const TileFetch cur = next;

@@ -8,7 +8,8 @@ The reference API lets a caller pass a different operator set and a different `e
 `expand_level` call (reference engine.py:367-375).  tests/golden/ holds uniform runs; this file pins the mixed
 ones: operator sets that change between levels, exhaustive levels on top of a level that was cut at its
 separator, and non-exhaustive levels on top of such a level (where the reference truncates every chunk at its
-first separating candidate, fresh or not -- engine.py:334-335 -- the CUDA engine's documented divergence).
+first separating candidate, fresh or not -- engine.py:334-335 -- which the CUDA engine reproduces on its narrow
+path with a scan pass and dead ordinal ranges; "engine_exact": false marks those cases).
 """
 import hashlib
 import json

@@ -7,8 +7,9 @@ that on purpose -- the operator set changes between levels, exhaustive levels ar
 was cut at its separator -- and every level must still be the reference's, bit for bit
 (tests/golden_schedules/schedules.json; the same file pins the CPU oracle in test_oracle_schedules.py).
 
-Cases with "engine_exact": false are the documented divergence of DESIGN.md section 1 (NON-exhaustive levels over
-a store that already holds a separating CM): there the levels up to the first such level must match.
+Cases with "engine_exact": false are NON-exhaustive levels over a store that already holds a separating CM,
+where the reference truncates every chunk at its first separating candidate, fresh or not; the narrow path
+reproduces that with a scan pass and dead ordinal ranges, so they must match as well.
 """
 
 import json
@@ -29,10 +30,7 @@ def test_engine_reproduces_reference_schedule(case):
     spec = workloads.named_workload(case["workload"], case["seed"])
     store = engine.CandidateStore(spec)
     try:
-        holds_separator = False
         for (ops, exhaustive), gl in zip(case["schedule"], case["levels"]):
-            if not case["engine_exact"] and holds_separator and not exhaustive:
-                break  # the documented divergence starts here
             cfg = engine.EngineConfig(exhaustive=exhaustive)
             stats = engine.RunStats()
             n_new, sep = engine.expand_level(store, gl["cost"], tuple(ops), config=cfg, stats=stats)
@@ -40,6 +38,5 @@ def test_engine_reproduces_reference_schedule(case):
             assert (n_new, sep, stats.constructed) == (gl["n"], gl["sep_gid"], gl["constructed"]), where
             gold = dict(gl, base=store.level(gl["cost"]).base)
             assert_level_matches_golden(store.level(gl["cost"]), gold, where)
-            holds_separator = holds_separator or sep is not None
     finally:
         store.close()
