@@ -1251,10 +1251,37 @@ static bool wide2_enabled() {
     return on;
 }
 
+template <int LW>
+static void launch_wide2_guarded(const WideParams &P, int grid, size_t smem, cudaStream_t st) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(wide2_guarded_level_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
+    });
+    wide2_guarded_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
+}
+
 void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
     if (wide2_) {
         const size_t smem = wide2_smem_bytes(nvec_);
         const BlockDesc &last = lv.blocks.back();
+        if (P.scan_only || P.dead_n) {  // rare mode (collect_dead_ranges): one launch of the guarded kernel, any size
+            P.block_begin = 0;
+            P.block_end = (int)lv.blocks.size();
+            P.tile_begin = 0;
+            P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
+            P.ticket = CTR_TICKET0;
+            const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
+            switch (lw_) {
+                case 8: launch_wide2_guarded<8>(P, grid, smem, stream_); break;
+                case 16: launch_wide2_guarded<16>(P, grid, smem, stream_); break;
+                case 32: launch_wide2_guarded<32>(P, grid, smem, stream_); break;
+                default: launch_wide2_guarded<64>(P, grid, smem, stream_); break;
+            }
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+            st_.enumerate_launches++;
+            return;
+        }
         if (last.ord0 + last.size <= kSmallLevel) {
             P.block_begin = 0;
             P.block_end = (int)lv.blocks.size();
@@ -1521,13 +1548,22 @@ void Engine::collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch
         reserve(sep_list_, want, false);
         level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
         CUDA_CHECK(cudaGetLastError());
-        NarrowParams Q = narrow_params(false);
-        Q.scan_only = 1;
-        Q.prune_after_sep = 0;
-        Q.sep_list = sep_list_.ptr;
-        Q.sep_list_cap = sep_list_.cap;
-        Q.ords = nullptr;
-        launch_enumerate(Q, lv);
+        if (wide_) {
+            WideParams Q = wide_params(false);
+            Q.scan_only = 1;
+            Q.prune_after_sep = 0;
+            Q.sep_list = sep_list_.ptr;
+            Q.sep_list_cap = sep_list_.cap;
+            launch_enumerate_wide(Q, lv);
+        } else {
+            NarrowParams Q = narrow_params(false);
+            Q.scan_only = 1;
+            Q.prune_after_sep = 0;
+            Q.sep_list = sep_list_.ptr;
+            Q.sep_list_cap = sep_list_.cap;
+            Q.ords = nullptr;
+            launch_enumerate(Q, lv);
+        }
         read_counters();
         n = h_counters_[CTR_SEPCOUNT];
         if (n <= sep_list_.cap) break;
@@ -1591,8 +1627,8 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
         st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
         dead_n_ = 0;
-        if (!exhaustive && store_has_separator_ && !wide_ && shard_count == 1 && mode_batch_ > 0 && !async_enabled() &&
-            !use_partition(constructed)) {
+        if (!exhaustive && store_has_separator_ && (!wide_ || wide2_) && shard_count == 1 && mode_batch_ > 0 &&
+            !async_enabled() && !use_partition(constructed)) {
             collect_dead_ranges(lv, constructed, (u64)mode_batch_);
             defer = false;  // (rare mode: the plain two-synchronisation path)
         }
@@ -1743,6 +1779,9 @@ WideParams Engine::wide_params(bool exhaustive) const {
     P.sep_list_cap = exhaustive ? sep_list_.cap : 0;
     P.shard_stride = 1;
     P.shard_offset = 0;
+    P.dead = dead_n_ ? dead_.ptr : nullptr;
+    P.dead_n = (uint32_t)dead_n_;
+    P.scan_only = 0;
     return P;
 }
 

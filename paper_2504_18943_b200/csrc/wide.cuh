@@ -63,6 +63,11 @@ struct WideParams {
     int prune_after_sep;
     u64 *sep_list;
     u64 sep_list_cap;
+    // non-exhaustive level over a store that already holds a separating CM (see NarrowParams::dead / scan_only;
+    // wide2_guarded_level_kernel only)
+    const u64 *dead;
+    uint32_t dead_n;
+    int scan_only;
 };
 
 struct __align__(16) WideWarpShared {

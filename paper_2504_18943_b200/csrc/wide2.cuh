@@ -86,11 +86,19 @@ __device__ __forceinline__ uint32_t v_diff(uint4 a, uint4 b) { return (a.x ^ b.x
 
 // Carries W2_BATCH candidates of one lane through hash -> probe -> claim / compare.
 // `gen(r, p, a, b)` yields the operands of candidate r's vector p in formula order.
-template <int LW, int OP, class Gen>
+// GUARD (wide2_guarded_level_kernel): candidates whose ordinal lies in a dead range do not exist, and in the scan
+// pass only the ordinal of every separating candidate is recorded (NarrowParams::dead / scan_only).
+template <int LW, int OP, bool GUARD, class Gen>
 __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp &W, Wide2State &st, Gen gen,
-                                            const bool (&live)[W2_BATCH], const u64 (&ords)[W2_BATCH]) {
+                                            const bool (&live_in)[W2_BATCH], const u64 (&ords)[W2_BATCH]) {
     const int nvec = P.nvec;
     const uint32_t mask32 = (uint32_t)P.slot_mask;
+    bool live[W2_BATCH];
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) {
+        live[r] = live_in[r];
+        if (GUARD && P.dead_n && live[r] && ordinal_is_dead(P.dead, P.dead_n, ords[r])) live[r] = false;
+    }
     // ---- pass 1: hashes, separation flag, duplicate-by-construction flags
     uint32_t ha[W2_BATCH], hb[W2_BATCH], sepacc[W2_BATCH], da[W2_BATCH], db[W2_BATCH];
 #pragma unroll
@@ -110,6 +118,15 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
             da[r] |= v_diff(c, a);
             db[r] |= v_diff(c, b);
         }
+    }
+    if (GUARD && P.scan_only) {
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            if (!live[r] || sepacc[r] != 0u) continue;
+            const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+            if (pos < P.sep_list_cap) P.sep_list[pos] = ords[r];
+        }
+        return;
     }
     uint32_t slot[W2_BATCH], fp[W2_BATCH];
     u64 w[W2_BATCH], entry[W2_BATCH];
@@ -230,7 +247,7 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
     }
 }
 
-template <int LW, int OP>
+template <int LW, int OP, bool GUARD>
 __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
                                                  u64 sep_now) {
     const BlockDesc &B = W.fx->block;
@@ -258,11 +275,11 @@ __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide
             a = __ldg(rows[r] + p);
             b = a;
         };
-        wide2_batch<LW, OP>(P, W, st, gen, live, ords);
+        wide2_batch<LW, OP, GUARD>(P, W, st, gen, live, ords);
     }
 }
 
-template <int LW, int OP, bool VEC_B>
+template <int LW, int OP, bool VEC_B, bool GUARD>
 __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
                                                   u64 sep_now) {
     const BlockDesc &B = W.fx->block;
@@ -323,7 +340,7 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
                 a = VEC_B ? xs : xv;
                 b = VEC_B ? xv : xs;
             };
-            wide2_batch<LW, OP>(P, W, st, gen, live, ords);
+            wide2_batch<LW, OP, GUARD>(P, W, st, gen, live, ords);
         }
     }
 }
@@ -363,16 +380,16 @@ __device__ __forceinline__ bool wide2_next_tile(const WideParams &P, const Wide2
     return W.fx->ticket < P.tile_end;
 }
 
-template <int LW, int OP>
+template <int LW, int OP, bool GUARD = false>
 __device__ __forceinline__ void wide2_run_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st) {
     const u64 sep_now = W.fx->sep_now;
     if (W.fx->block.ord0 > sep_now) return;
     const u64 tile_local = W.fx->ticket - W.fx->block.tile0;
     if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
-        if (W.fx->block.vec_is_b) wide2_binary_tile<LW, OP, true>(P, W, st, tile_local, sep_now);
-        else wide2_binary_tile<LW, OP, false>(P, W, st, tile_local, sep_now);
+        if (W.fx->block.vec_is_b) wide2_binary_tile<LW, OP, true, GUARD>(P, W, st, tile_local, sep_now);
+        else wide2_binary_tile<LW, OP, false, GUARD>(P, W, st, tile_local, sep_now);
     } else {
-        wide2_unary_tile<LW, OP>(P, W, st, tile_local, sep_now);
+        wide2_unary_tile<LW, OP, GUARD>(P, W, st, tile_local, sep_now);
     }
 }
 
@@ -399,6 +416,25 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_small_level_kernel(const
             case OP_AND: wide2_run_tile<LW, OP_AND>(P, W, st); break;
             case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL>(P, W, st); break;
             default: wide2_run_tile<LW, OP_OR>(P, W, st); break;
+        }
+    }
+}
+
+// non-exhaustive level over a store that already holds a separating CM (see narrow_guarded_level_kernel)
+template <int LW>
+__global__ void __launch_bounds__(CTA_THREADS, 1) wide2_guarded_level_kernel(const __grid_constant__ WideParams P) {
+    extern __shared__ __align__(16) uint4 s_w2[];
+    const Wide2Warp W = wide2_carve(P, s_w2);
+    Wide2State st;
+    while (wide2_next_tile(P, W)) {
+        switch (W.fx->block.op) {
+            case OP_ATOM: wide2_run_tile<LW, OP_ATOM, true>(P, W, st); break;
+            case OP_NOT: wide2_run_tile<LW, OP_NOT, true>(P, W, st); break;
+            case OP_NEXT: wide2_run_tile<LW, OP_NEXT, true>(P, W, st); break;
+            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE, true>(P, W, st); break;
+            case OP_AND: wide2_run_tile<LW, OP_AND, true>(P, W, st); break;
+            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL, true>(P, W, st); break;
+            default: wide2_run_tile<LW, OP_OR, true>(P, W, st); break;
         }
     }
 }

@@ -8,8 +8,8 @@ The reference API lets a caller pass a different operator set and a different `e
 `expand_level` call (reference engine.py:367-375).  tests/golden/ holds uniform runs; this file pins the mixed
 ones: operator sets that change between levels, exhaustive levels on top of a level that was cut at its
 separator, and non-exhaustive levels on top of such a level (where the reference truncates every chunk at its
-first separating candidate, fresh or not -- engine.py:334-335 -- which the CUDA engine reproduces on its narrow
-path with a scan pass and dead ordinal ranges; "engine_exact": false marks those cases).
+first separating candidate, fresh or not -- engine.py:334-335 -- which the CUDA engine reproduces
+with a scan pass and dead ordinal ranges; "engine_exact": false marks those cases).
 """
 import hashlib
 import json
@@ -52,6 +52,13 @@ for seed, found in ((0, 4), (2, 5), (3, 6), (4, 8)):
         dict(name=f"c1_s{seed}_cut_then_exhaustive", workload="c1", seed=seed, engine_exact=True,
              schedule=sched((FULL, False, found), (FULL, True, 3))),
         dict(name=f"c1_s{seed}_cut_then_nonexhaustive", workload="c1", seed=seed, engine_exact=False,
+             schedule=sched((FULL, False, found + 2), (FULL, True, 1))),
+    ]
+for seed, found in ((0, 5), (1, 5)):  # 24-byte CMs: the wide path
+    CASES += [
+        dict(name=f"w32_s{seed}_cut_then_exhaustive", workload="w32", seed=seed, engine_exact=True,
+             schedule=sched((FULL, False, found), (FULL, True, 3))),
+        dict(name=f"w32_s{seed}_cut_then_nonexhaustive", workload="w32", seed=seed, engine_exact=False,
              schedule=sched((FULL, False, found + 2), (FULL, True, 1))),
     ]
 CASES.append(dict(name="c3_s2_exh11", workload="c3", seed=2, engine_exact=True, schedule=sched((FULL, True, 11))))

@@ -8,8 +8,9 @@ was cut at its separator -- and every level must still be the reference's, bit f
 (tests/golden_schedules/schedules.json; the same file pins the CPU oracle in test_oracle_schedules.py).
 
 Cases with "engine_exact": false are NON-exhaustive levels over a store that already holds a separating CM,
-where the reference truncates every chunk at its first separating candidate, fresh or not; the narrow path
-reproduces that with a scan pass and dead ordinal ranges, so they must match as well.
+where the reference truncates every chunk at its first separating candidate, fresh or not; the engine
+reproduces that with a scan pass and dead ordinal ranges (c1 = narrow path, w32 = wide path),
+so they must match as well.
 """
 
 import json
