@@ -153,3 +153,33 @@ def test_naive_semantics_fixtures():
     spec = workloads.spec1()
     assert semantics.separates_by_sat(spec, parse_formula("!(b U a)", spec.alphabet))
     assert not semantics.separates_by_sat(spec, parse_formula("c", spec.alphabet))
+
+
+def test_fast_witness_check_agrees_with_the_quantifier_semantics():
+    """semantics._truth_table_fast (expansion laws, one backward pass per node) == semantics._truth_table
+    (quantifiers of F and U written out) on random formulas over random traces."""
+    import random
+
+    from paper_2504_18943_b200.formulas import And, Future, Next, Not, Or, Until
+    from paper_2504_18943_b200.traces import Trace
+
+    rng = random.Random(0xF457)
+
+    def formula(depth):
+        if depth == 0 or rng.random() < 0.2:
+            return Atom(rng.randrange(3))
+        kind = rng.choice(("not", "next", "future", "and", "or", "until"))
+        if kind == "not":
+            return Not(formula(depth - 1))
+        if kind == "next":
+            return Next(formula(depth - 1))
+        if kind == "future":
+            return Future(formula(depth - 1))
+        node = {"and": And, "or": Or, "until": Until}[kind]
+        return node(formula(depth - 1), formula(depth - 1))
+
+    for _ in range(300):
+        length = rng.randint(1, 9)
+        tr = Trace(tuple(frozenset(p for p in range(3) if rng.random() < 0.5) for _ in range(length)))
+        f = formula(rng.randint(1, 5))
+        assert semantics._truth_table_fast(tr, f) == semantics._truth_table(tr, f), (tr, f)
