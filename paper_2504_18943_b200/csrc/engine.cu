@@ -401,6 +401,9 @@ private:
     u64 dead_n_ = 0;
     int64_t mode_batch_ = 0;
     void collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch);
+    static constexpr u64 kEntryCache = 1ull << 14;  // entries whose ordinals entry() keeps on the host (128 KB)
+    std::vector<u64> entry_cache_;
+    u64 entry_cache_total_ = 0;
     static bool partition_enabled();
     bool use_partition(u64 constructed) const;
     void launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles);
@@ -771,6 +774,7 @@ void Engine::reset() {
     store_has_separator_ = false;
     prune_ok_ = true;
     prune_mask_ = 0;
+    entry_cache_total_ = 0;
     rebuild_table(kMinSlots);  // small levels probe an L2-resident set again; it regrows with the search
     st_.constructed = 0;
     st_.unique = 0;
@@ -2248,10 +2252,25 @@ int Engine::entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
     while (li + 1 < levels_.size() && (u64)gid >= levels_[li + 1].base) ++li;
     while (levels_[li].n == 0 || (u64)gid < levels_[li].base) --li;
     CUDA_CHECK(cudaSetDevice(device_));
+    // Witness reconstruction walks a tree whose nodes are almost all in the low levels: the ordinals of the first
+    // kEntryCache entries come over in ONE copy on the first call and serve every later one (finalised entries
+    // never change; reset() and new levels below the prefix size drop the copy), instead of a copy + synchronise
+    // per node.
+    if (entry_cache_total_ != std::min<u64>(total_, kEntryCache)) {
+        entry_cache_total_ = std::min<u64>(total_, kEntryCache);
+        entry_cache_.resize((size_t)entry_cache_total_);
+        CUDA_CHECK(cudaMemcpyAsync(entry_cache_.data(), ords_.ptr, entry_cache_total_ * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        st_.d2h_bytes += entry_cache_total_ * sizeof(u64);
+    }
     u64 ord = 0;
-    CUDA_CHECK(cudaMemcpyAsync(&ord, ords_.ptr + gid, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));
-    st_.d2h_bytes += sizeof(u64);
+    if ((u64)gid < entry_cache_total_) {
+        ord = entry_cache_[(size_t)gid];
+    } else {
+        CUDA_CHECK(cudaMemcpyAsync(&ord, ords_.ptr + gid, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaStreamSynchronize(stream_));
+        st_.d2h_bytes += sizeof(u64);
+    }
     decode(levels_[li], ord, op, left, right);
     return LTLB200_OK;
 }
