@@ -170,6 +170,13 @@ int ltlb200_level_info(const ltlb200_engine *e, int32_t cost, int64_t *n, int64_
  */
 int ltlb200_level_candidates(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int64_t *n);
 
+/*
+ * 1 when some stored CM separates the examples (a level found a separator, or an exhaustive level recorded a
+ * separating candidate).  A NON-exhaustive expand_level on such a store follows the reference's chunk truncation
+ * (engine.py:334-335), which only ltlb200_expand_level reproduces: a sharded search builds such a level locally.
+ */
+int32_t ltlb200_holds_separator(const ltlb200_engine *e);
+
 /* Number of levels built (len(store.levels)). */
 int32_t ltlb200_num_levels(const ltlb200_engine *e);
 

@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "ltlb200_now",
     "ltlb200_level_info",
     "ltlb200_level_candidates",
+    "ltlb200_holds_separator",
     "ltlb200_num_levels",
     "ltlb200_level_copy",
     "ltlb200_entry",
@@ -129,6 +130,8 @@ def load():
     L.ltlb200_level_info.argtypes = [p, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.ltlb200_level_candidates.restype = ctypes.c_int
     L.ltlb200_level_candidates.argtypes = [p, i32, ctypes.c_uint32, ctypes.POINTER(i64)]
+    L.ltlb200_holds_separator.restype = i32
+    L.ltlb200_holds_separator.argtypes = [p]
     L.ltlb200_num_levels.restype = i32
     L.ltlb200_num_levels.argtypes = [p]
     L.ltlb200_level_copy.restype = ctypes.c_int

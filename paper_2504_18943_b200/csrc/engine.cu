@@ -345,6 +345,7 @@ public:
     u64 seps_copy(u64 *out, u64 cap);
     int key_bytes() const { return 16 * nvec_; }
     int num_levels() const { return (int)levels_.size(); }
+    bool holds_separator() const { return store_has_separator_; }
     u64 approx_bytes() const { return approx_bytes_; }
 
 private:
@@ -2433,6 +2434,8 @@ int ltlb200_level_candidates(ltlb200_engine *e, int32_t cost, uint32_t op_mask, 
         return LTLB200_OK;
     });
 }
+
+int32_t ltlb200_holds_separator(const ltlb200_engine *e) { return e && e->impl->holds_separator() ? 1 : 0; }
 
 int32_t ltlb200_num_levels(const ltlb200_engine *e) { return e ? e->impl->num_levels() : 0; }
 

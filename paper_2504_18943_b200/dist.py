@@ -137,8 +137,12 @@ def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfi
     stats = stats if stats is not None else RunStats()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     mask = operator_mask(ops)
+    # ... and so is a NON-exhaustive level over a store that already holds a separating CM, whatever its size: the
+    # reference then truncates every chunk at its first separating candidate (engine.py:334-335), which the
+    # single-handle expand_level reproduces and the claim exchange (minimum ordinal per CM) cannot
+    truncating = (not config.exhaustive) and getattr(store, "holds_separator", lambda: False)()
     if hasattr(store, "level_candidates") and hasattr(store, "expand_local") \
-            and store.level_candidates(cost, mask) < REPLICATE_BELOW:
+            and (truncating or store.level_candidates(cost, mask) < REPLICATE_BELOW):
         # small level: every rank builds all of it (see REPLICATE_BELOW); only the budget status is agreed on,
         # because the time budget is read from each rank's own clock
         status, n_new, sep_gid, delta = store.expand_local(cost, mask, config.exhaustive, config.batch_size,

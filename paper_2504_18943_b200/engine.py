@@ -219,6 +219,11 @@ class CandidateStore:
                       f"level_candidates({cost})")
         return int(n.value)
 
+    def holds_separator(self) -> bool:
+        """Some stored CM separates the examples (then a non-exhaustive level follows the reference's chunk
+        truncation, which only the single-handle ``expand_level`` reproduces)."""
+        return bool(_native.load().ltlb200_holds_separator(self._handle))
+
     def expand_local(self, cost, op_mask, exhaustive, batch_size, memory_budget_bytes, deadline):
         """The whole level on this device (``_expand``): what a sharded search does for its small levels."""
         native_deadline = None if deadline is None else _monotonic() + (deadline - time.perf_counter())

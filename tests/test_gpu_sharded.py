@@ -112,3 +112,43 @@ def test_protocol_over_nccl_with_one_rank():
     finally:
         pdist.REPLICATE_BELOW = default_threshold
         dist.destroy_process_group()
+
+
+def test_sharded_protocol_follows_the_reference_on_truncating_levels():
+    """Non-exhaustive levels over a store that already holds a separating CM through dist.sharded_expand_level with
+    every level forced through the exchange: the protocol must hand exactly those levels to the single-handle path
+    (reference chunk truncation, engine.py:334-335) and so reproduce the reference's fixtures."""
+    import json
+    import pathlib
+
+    import torch.distributed as dist
+
+    from helpers import assert_level_matches_golden
+
+    cases = [c for c in json.loads((pathlib.Path(__file__).resolve().parent / "golden_schedules" / "schedules.json").read_text())
+             if c["name"] in ("c1_s0_cut_then_nonexhaustive", "c1_s4_cut_then_nonexhaustive", "w32_s0_cut_then_nonexhaustive")]
+    assert len(cases) == 3
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    default_threshold = pdist.REPLICATE_BELOW
+    try:
+        pdist.REPLICATE_BELOW = 0
+        for case in cases:
+            spec = workloads.named_workload(case["workload"], case["seed"])
+            store = engine.CandidateStore(spec)
+            try:
+                for (ops, exhaustive), gl in zip(case["schedule"], case["levels"]):
+                    cfg = engine.EngineConfig(exhaustive=exhaustive, operators=tuple(ops), memory_budget_mb=1 << 20)
+                    stats = engine.RunStats()
+                    n_new, sep = pdist.sharded_expand_level(store, gl["cost"], tuple(ops), cfg, stats)
+                    where = f"{case['name']} cost {gl['cost']}"
+                    assert (n_new, sep, stats.constructed) == (gl["n"], gl["sep_gid"], gl["constructed"]), where
+                    assert_level_matches_golden(store.level(gl["cost"]), dict(gl, base=store.level(gl["cost"]).base), where)
+            finally:
+                store.close()
+    finally:
+        pdist.REPLICATE_BELOW = default_threshold
+        dist.destroy_process_group()
