@@ -2,10 +2,15 @@
 
 The shared library lands in ``paper_2504_18943_b200/_lib/`` so that it travels with the
 repository snapshot to the GPU box.  ``__graft_entry__.build()`` calls ``build_native``.
+
+The enumeration kernels are templates over (lane width, operator); ``csrc/inst.cu`` is compiled
+once per (lane width, narrow | wide) beside ``csrc/engine.cu`` (host side, finalisation and
+exchange kernels), all objects in parallel, then linked into one library.
 """
 
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import pathlib
 import shutil
@@ -14,15 +19,22 @@ import subprocess
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
+OBJ_DIR = LIB_DIR / "obj"
 LIB_PATH = LIB_DIR / "libltlsynth_b200.so"
 
-SOURCES = ["engine.cu"]
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-O2,-Wall",
-    "-shared", "-cudart", "static",
-]
+ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMPILE_FLAGS = [*ARCH_FLAGS, "-Xfatbin", "-compress-all", "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2,-Wall"]
+LINK_FLAGS = [*ARCH_FLAGS, "-shared", "-cudart", "static"]
+LANE_WIDTHS = (8, 16, 32, 64)
+
+
+def _units() -> list[tuple[str, str, list[str]]]:
+    """(object name, source file, extra defines) of every translation unit."""
+    units = [("engine", "engine.cu", [])]
+    for lw in LANE_WIDTHS:
+        units.append((f"narrow_lw{lw}", "inst.cu", [f"-DLTLB200_INST_LW={lw}", "-DLTLB200_INST_WIDE=0"]))
+        units.append((f"wide_lw{lw}", "inst.cu", [f"-DLTLB200_INST_LW={lw}", "-DLTLB200_INST_WIDE=1"]))
+    return units
 
 
 def _nvcc() -> str:
@@ -32,27 +44,45 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA engine cannot be built")
 
 
-def _stale() -> bool:
-    if not LIB_PATH.exists():
-        return True
-    built = LIB_PATH.stat().st_mtime
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "ltlsynth_b200.h"]
-    return any(p.stat().st_mtime > built for p in deps)
+def _newest_source() -> float:
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [PKG.parent / "include" / "ltlsynth_b200.h"]
+    return max(p.stat().st_mtime for p in deps)
+
+
+def _stale(path: pathlib.Path) -> bool:
+    return not path.exists() or path.stat().st_mtime < _newest_source()
 
 
 def build_native(force: bool = False, verbose: bool = False, defines=(), out: pathlib.Path | None = None) -> pathlib.Path:
     """``defines``/``out`` build a tuning variant (e.g. ("LTLB200_PROBE_BATCH=2",)) beside the default library."""
     target = pathlib.Path(out) if out else LIB_PATH
-    if not force and out is None and not _stale():
+    variant = out is not None or bool(defines)
+    if not force and not variant and not _stale(LIB_PATH):
         return LIB_PATH
-    LIB_DIR.mkdir(exist_ok=True)
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
-           "-o", str(target), *[str(CSRC / s) for s in SOURCES]]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
-    if proc.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + proc.stdout + proc.stderr)
+    obj_dir = OBJ_DIR if not variant else LIB_DIR / ("obj_" + target.stem)
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    nvcc = _nvcc()
+    extra = [*(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines]]
+
+    def compile_unit(unit):
+        name, source, unit_defines = unit
+        obj = obj_dir / f"{name}.o"
+        if not force and not variant and not _stale(obj):
+            return obj, ""
+        cmd = [nvcc, *COMPILE_FLAGS, *extra, *unit_defines, "-c", "-o", str(obj), str(CSRC / source)]
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        if proc.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {name}:\n" + proc.stdout + proc.stderr)
+        return obj, proc.stdout + proc.stderr
+
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(_units()), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(compile_unit, _units()))
     if verbose:
-        print(proc.stdout + proc.stderr)
+        for obj, log in results:
+            print(f"---- {obj.name}\n{log}")
+    proc = subprocess.run([nvcc, *LINK_FLAGS, "-o", str(target), *[str(obj) for obj, _ in results]], capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError("link failed:\n" + proc.stdout + proc.stderr)
     return target
 
 
@@ -64,8 +94,7 @@ def build_tools() -> None:
         src, exe = root / f"{name}.cu", root / name
         if exe.exists() and exe.stat().st_mtime >= src.stat().st_mtime:
             continue
-        proc = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", str(exe), str(src)],
-                              capture_output=True, text=True)
+        proc = subprocess.run([_nvcc(), *ARCH_FLAGS, "-O3", "-o", str(exe), str(src)], capture_output=True, text=True)
         if proc.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + proc.stdout + proc.stderr)
 

@@ -29,11 +29,10 @@
 #include <vector>
 
 #include "../../include/ltlsynth_b200.h"
-#include "narrow.cuh"
-#include "narrow_async.cuh"
-#include "narrow_part.cuh"
-#include "wide.cuh"
+#include "launch.h"
+#include "narrow_fin.cuh"
 #include "wide2.cuh"
+#include "wide_fin.cuh"
 
 namespace ltlb200 {
 
@@ -359,7 +358,6 @@ private:
     uint4 valid_{}, target_{};
     bool special_possible_ = false;
     bool wide_ = false;  // CMs of more than one uint4
-    bool wide2_ = false; // ... enumerated by the lane-per-candidate kernel (wide2.cuh) instead of wide.cuh's groups
     int nvec_ = 1, log2g_ = 0;
     uint4 *d_valid_ = nullptr, *d_target_ = nullptr;
 
@@ -382,14 +380,6 @@ private:
     DeviceArray<u64> sep_list_;
     DeviceArray<uint8_t> misc_;
     DeviceArray<u64> xchg_;  // per-owner counts and cursors of the claim exchange
-    // partitioned path (narrow_part.cuh): record pool, chunk metadata, counters
-    DeviceArray<uint4> pool_keys_;
-    DeviceArray<u64> pool_ords_;
-    DeviceArray<uint8_t> chunk_meta_;   // [0, cap/2) bucket of each chunk, [cap/2, cap) its fill
-    DeviceArray<uint32_t> chunk_order_; // chunk ids grouped by bucket
-    DeviceArray<u64> wstate_;           // open chunks + chunk-id stash of every warp slot, carried across operator launches
-    DeviceArray<u64> pc_;
-    int part_occupancy_ = 2;
     bool store_has_separator_ = false;  // some stored CM separates: a separating candidate need not be fresh
     // Associativity pruning (narrow.cuh: run_binary_tile) is sound while every stored level is complete and
     // all levels were built with one operator set; the first cut level or change of operators ends it.
@@ -401,13 +391,11 @@ private:
     DeviceArray<u64> dead_;
     u64 dead_n_ = 0;
     int64_t mode_batch_ = 0;
+    u64 sep_want_ = 0;  // separating candidates the last attempt counted beyond the list's capacity
     void collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch);
     static constexpr u64 kEntryCache = 1ull << 14;  // entries whose ordinals entry() keeps on the host (128 KB)
     std::vector<u64> entry_cache_;
     u64 entry_cache_total_ = 0;
-    static bool partition_enabled();
-    bool use_partition(u64 constructed) const;
-    void launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles);
     struct PendingLevel {
         LevelMeta lv;
         u64 constructed = 0, n_claimed = 0, sep_ord = ~0ull, n_seps = 0, claim_cap = 0;
@@ -418,7 +406,6 @@ private:
     WideParams wide_params(bool exhaustive) const;
     NarrowParams narrow_params(bool exhaustive) const;
     static constexpr u64 kMinSlots = 1ull << 16;
-    static constexpr int kPoolOverflowWord = 32;  // pinned staging word beside the CTR_* read-back
     u64 *d_counters_ = nullptr;
     BlockDesc *d_blocks_ = nullptr;
     static constexpr int kMaxBlocks = 512;
@@ -456,6 +443,10 @@ private:
     void decode(const LevelMeta &lv, u64 ord, int32_t *op, int64_t *left, int64_t *right) const;
     u64 constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) const;
     void launch_enumerate(NarrowParams P, const LevelMeta &lv);
+    void launch_narrow(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st);
+    void launch_wide(int kind, int op, const WideParams &P, int grid, cudaStream_t st);
+    template <typename Params>
+    void launch_level(Params P, const LevelMeta &lv);
     void launch_enumerate_wide(WideParams P, const LevelMeta &lv);
     u64 table_slots() const { return wide_ ? wslots_.cap : slots_.cap; }
     u64 chunk_exact_separator(const LevelMeta &lv, std::vector<u64> &seps, u64 batch);
@@ -530,23 +521,6 @@ void Engine::reserve(DeviceArray<T> &a, u64 want, bool keep, u64 keep_elems) {
     a.ptr = p;
     a.bytes = bytes;
     a.cap = bytes / sizeof(T);
-}
-
-template <int LW>
-static int part_occupancy_of();
-template <int LW>
-static int async_occupancy_of();
-static bool async_enabled();
-template <int LW>
-static int wide2_occupancy_of(int nvec);
-static bool wide2_enabled();
-
-template <int LW>
-static int occupancy_of() {
-    int occ = 0, best = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, OP_UNTIL>, CTA_THREADS, 0) == cudaSuccess)
-        best = std::max(best, occ);
-    return best;
 }
 
 // byte image of one CM row (T lanes, little endian), zero padded to nvec uint4 vectors
@@ -630,32 +604,19 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
     CUDA_CHECK(cudaMemcpyAsync(d_counters_, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_rows / init leave scope
     PHASE(11, "create: copies + sync", tp);
-    {   // occupancy queries (and the dynamic-shared-memory opt-ins they need) once per process, device and lane width
+    {   // occupancy queries once per process, device, lane width and (wide: shared memory depends on it) nvec
         static std::mutex mu;
-        static std::map<std::pair<int, int>, std::array<int, 3>> cache;
+        static std::map<std::tuple<int, int, int>, int> cache;
         std::lock_guard<std::mutex> lock(mu);
-        auto it = cache.find({device_, lw_});
+        auto it = cache.find({device_, lw_, nvec_});
         if (it == cache.end()) {
-            std::array<int, 3> occ{4, 2, 2};
-            if (!wide_) {
-                occ[0] = lw_ == 8 ? occupancy_of<8>() : lw_ == 16 ? occupancy_of<16>() : lw_ == 32 ? occupancy_of<32>() : occupancy_of<64>();
-                occ[1] = lw_ == 8 ? async_occupancy_of<8>() : lw_ == 16 ? async_occupancy_of<16>() : lw_ == 32 ? async_occupancy_of<32>() : async_occupancy_of<64>();
-                occ[2] = lw_ == 8 ? part_occupancy_of<8>() : lw_ == 16 ? part_occupancy_of<16>() : lw_ == 32 ? part_occupancy_of<32>() : part_occupancy_of<64>();
-            }
-            it = cache.emplace(std::make_pair(device_, lw_), occ).first;
+            int occ;
+            if (wide_) occ = lw_ == 8 ? wide2_occupancy_8(nvec_, device_) : lw_ == 16 ? wide2_occupancy_16(nvec_, device_)
+                             : lw_ == 32 ? wide2_occupancy_32(nvec_, device_) : wide2_occupancy_64(nvec_, device_);
+            else occ = lw_ == 8 ? narrow_occupancy_8() : lw_ == 16 ? narrow_occupancy_16() : lw_ == 32 ? narrow_occupancy_32() : narrow_occupancy_64();
+            it = cache.emplace(std::make_tuple(device_, lw_, nvec_), occ).first;
         }
-        occupancy_ = wide_ ? LTLB200_WIDE_MIN_CTAS : (async_enabled() ? it->second[1] : it->second[0]);
-        wide2_ = wide_ && wide2_enabled();
-        if (wide2_) {  // depends on the shared memory the row areas need, i.e. on nvec: cached per (device, lanes, nvec)
-            static std::map<std::tuple<int, int, int>, int> w2cache;
-            auto w2 = w2cache.find({device_, lw_, nvec_});
-            if (w2 == w2cache.end())
-                w2 = w2cache.emplace(std::make_tuple(device_, lw_, nvec_),
-                                     lw_ == 8 ? wide2_occupancy_of<8>(nvec_) : lw_ == 16 ? wide2_occupancy_of<16>(nvec_)
-                                     : lw_ == 32 ? wide2_occupancy_of<32>(nvec_) : wide2_occupancy_of<64>(nvec_)).first;
-            occupancy_ = w2->second;
-        }
-        part_occupancy_ = it->second[2];
+        occupancy_ = it->second;
     }
     rebuild_table(kMinSlots);
     st_.row_bytes = row_bytes_;
@@ -682,12 +643,6 @@ Engine::~Engine() {
     release(sep_list_);
     release(misc_);
     release(xchg_);
-    release(pool_keys_);
-    release(pool_ords_);
-    release(chunk_meta_);
-    release(chunk_order_);
-    release(wstate_);
-    release(pc_);
     recycle_retired(true);
     pinned_put(h_counters_);
     g_phase.dump();
@@ -792,9 +747,9 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
     constructed = 0;
     n_tiles = 0;
     // tile geometry: narrow = one lane per vector row; wide = one group of G lanes per vector row
-    const u64 tile_v = (wide_ && !wide2_) ? (u64)(32 >> log2g_) : (u64)TILE_V;
-    const u64 tile_s_max = wide2_ ? (u64)wide2_tile_s(nvec_) : wide_ ? (u64)(WIDE_ROW_VECS >> log2g_) : (u64)TILE_S;
-    const u64 tile_max = (wide_ && !wide2_) ? 2048 : (u64)TILE_V * TILE_S;  // candidates of a full-size tile
+    const u64 tile_v = (u64)TILE_V;
+    const u64 tile_s_max = wide_ ? (u64)wide2_tile_s(nvec_) : (u64)TILE_S;
+    const u64 tile_max = (u64)TILE_V * TILE_S;  // candidates of a full-size tile
     // A block is cut into at least ~4 tiles per resident warp so that small levels still
     // spread over the whole GPU instead of a few warps grinding through full-size tiles.
     const u64 want_tiles = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * 4;
@@ -998,83 +953,10 @@ u64 Engine::chunk_exact_separator(const LevelMeta &lv, std::vector<u64> &seps, u
     return firsts.size();
 }
 
-template <int LW>
-static void launch_op(int op, const NarrowParams &P, int grid, cudaStream_t st) {
-    switch (op) {
-        case OP_ATOM: narrow_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_NOT: narrow_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_NEXT: narrow_level_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_FUTURE: narrow_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_AND: narrow_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_UNTIL: narrow_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        default: narrow_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
-    }
-}
-
-constexpr size_t kAsyncSmem = sizeof(WarpSharedAsync) * WARPS_PER_CTA;
-
-template <int LW, int OP>
-static void launch_async_instance(const NarrowParams &P, int grid, cudaStream_t st) {
-    static std::once_flag once;  // opt in to > 48 KB of dynamic shared memory, once per instance
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(narrow_async_kernel<LW, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmem);
-    });
-    narrow_async_kernel<LW, OP><<<grid, CTA_THREADS, kAsyncSmem, st>>>(P);
-}
-
-template <int LW>
-static void launch_op_async(int op, const NarrowParams &P, int grid, cudaStream_t st) {
-    switch (op) {
-        case OP_ATOM: launch_async_instance<LW, OP_ATOM>(P, grid, st); break;
-        case OP_NOT: launch_async_instance<LW, OP_NOT>(P, grid, st); break;
-        case OP_NEXT: launch_async_instance<LW, OP_NEXT>(P, grid, st); break;
-        case OP_FUTURE: launch_async_instance<LW, OP_FUTURE>(P, grid, st); break;
-        case OP_AND: launch_async_instance<LW, OP_AND>(P, grid, st); break;
-        case OP_UNTIL: launch_async_instance<LW, OP_UNTIL>(P, grid, st); break;
-        default: launch_async_instance<LW, OP_OR>(P, grid, st); break;
-    }
-}
-
-template <int LW>
-static int async_occupancy_of() {
-    int occ = 0;
-    cudaFuncSetAttribute(narrow_async_kernel<LW, OP_UNTIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAsyncSmem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_async_kernel<LW, OP_UNTIL>, CTA_THREADS, kAsyncSmem) != cudaSuccess) {
-        cudaGetLastError();
-        occ = 1;
-    }
-    return std::max(occ, 1);
-}
-
-// LTLB200_ASYNC=1 selects the cp.async pipeline (narrow_async_kernel) instead of the synchronous
-// direct kernel (narrow_level_kernel).  Off by default: with 8 warps per SM (its stages need
-// 105 KB of shared memory per CTA) it is 5-15 % faster on mid-size levels and 20 % slower on the
-// largest one of spec2; kept for A/B measurements.
-static bool async_enabled() {
-    static const bool on = [] {
-        const char *env = getenv("LTLB200_ASYNC");
-        return env && env[0] == '1';
-    }();
-    return on;
-}
-
-template <int LW>
-static void launch_op_wide(int op, const WideParams &P, int grid, cudaStream_t st) {
-    switch (op) {
-        case OP_ATOM: wide_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_NOT: wide_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_NEXT: wide_level_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_FUTURE: wide_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_AND: wide_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_UNTIL: wide_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        default: wide_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
-    }
-}
-
 // One launch per operator, in canonical operator order (blocks of a level are grouped by
 // operator already); each launch covers all (c1, c2) blocks of its operator.
 template <typename Params, typename Launch>
-static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int occupancy, ltlb200_stats &st, Launch launch) {
+static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int occupancy, Launch launch) {
     size_t b0 = 0;
     int group = 0;
     while (b0 < lv.blocks.size()) {
@@ -1089,13 +971,10 @@ static void for_each_operator(Params P, const LevelMeta &lv, int sm_count, int o
         const int grid = (int)std::min<u64>((P.tile_end - P.tile_begin + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count * occupancy);
         DBG("launch op=%d blocks=[%zu,%zu) tiles=[%llu,%llu) grid=%d", (int)lv.blocks[b0].op, b0, b1, (unsigned long long)P.tile_begin, (unsigned long long)P.tile_end, grid);
         launch((int)lv.blocks[b0].op, P, grid, group);
-        CUDA_CHECK(cudaGetLastError());
         if (debug_on()) {
             CUDA_CHECK(cudaDeviceSynchronize());
             DBG("  done");
         }
-        st.kernel_launches++;
-        st.enumerate_launches++;
         b0 = b1;
         ++group;
     }
@@ -1140,399 +1019,61 @@ void Engine::fan_end() {
     side_used_ = 0;
 }
 
-void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) {
-    const BlockDesc &last_block = lv.blocks.back();
-    const u64 level_candidates = last_block.ord0 + last_block.size;
-    if (P.scan_only || P.dead_n) {  // rare mode (collect_dead_ranges): one launch of the guarded kernel, any size
-        P.block_begin = 0;
-        P.block_end = (int)lv.blocks.size();
-        P.tile_begin = 0;
-        P.tile_end = last_block.tile0 + last_block.tiles_v * last_block.tiles_s;
-        P.ticket = CTR_TICKET0;
-        const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
-        switch (lw_) {
-            case 8: narrow_guarded_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            case 16: narrow_guarded_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            case 32: narrow_guarded_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            default: narrow_guarded_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-        }
-        CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches++;
-        st_.enumerate_launches++;
-        return;
+void Engine::launch_narrow(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st) {
+    switch (lw_) {
+        case 8: narrow_launch_8(kind, op, P, grid, st); break;
+        case 16: narrow_launch_16(kind, op, P, grid, st); break;
+        case 32: narrow_launch_32(kind, op, P, grid, st); break;
+        default: narrow_launch_64(kind, op, P, grid, st); break;
     }
-    if (level_candidates <= kSmallLevel && !async_enabled()) {
+    CUDA_CHECK(cudaGetLastError());
+    st_.kernel_launches++;
+    st_.enumerate_launches++;
+}
+
+void Engine::launch_wide(int kind, int op, const WideParams &P, int grid, cudaStream_t st) {
+    const size_t smem = wide2_warp_vecs(nvec_) * sizeof(uint4) * WARPS_PER_CTA;
+    switch (lw_) {
+        case 8: wide2_launch_8(kind, op, P, grid, smem, device_, st); break;
+        case 16: wide2_launch_16(kind, op, P, grid, smem, device_, st); break;
+        case 32: wide2_launch_32(kind, op, P, grid, smem, device_, st); break;
+        default: wide2_launch_64(kind, op, P, grid, smem, device_, st); break;
+    }
+    CUDA_CHECK(cudaGetLastError());
+    st_.kernel_launches++;
+    st_.enumerate_launches++;
+}
+
+// Small levels and the rare guarded mode (collect_dead_ranges) take ONE launch for every operator;
+// big levels one launch per operator, fanned out over the side streams.
+template <typename Params>
+void Engine::launch_level(Params P, const LevelMeta &lv) {
+    constexpr bool kWide = std::is_same<Params, WideParams>::value;
+    const BlockDesc &last = lv.blocks.back();
+    const u64 level_candidates = last.ord0 + last.size;
+    const bool guarded = P.scan_only || P.dead_n;
+    if (guarded || level_candidates <= kSmallLevel) {
         P.block_begin = 0;
         P.block_end = (int)lv.blocks.size();
         P.tile_begin = 0;
-        P.tile_end = last_block.tile0 + last_block.tiles_v * last_block.tiles_s;
+        P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
         P.ticket = CTR_TICKET0;
         const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
-        switch (lw_) {
-            case 8: narrow_small_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            case 16: narrow_small_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            case 32: narrow_small_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            default: narrow_small_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-        }
-        CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches++;
-        st_.enumerate_launches++;
+        if constexpr (kWide) launch_wide(guarded ? LK_GUARDED : LK_SMALL, 0, P, grid, stream_);
+        else launch_narrow(guarded ? LK_GUARDED : LK_SMALL, 0, P, grid, stream_);
         return;
     }
     fan_begin();
-    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const NarrowParams &Q, int grid, int group) {
+    for_each_operator(P, lv, sm_count_, occupancy_, [&](int op, const Params &Q, int grid, int group) {
         cudaStream_t st = fan_stream(group);
-        if (async_enabled()) {
-            switch (lw_) {
-                case 8: launch_op_async<8>(op, Q, grid, st); break;
-                case 16: launch_op_async<16>(op, Q, grid, st); break;
-                case 32: launch_op_async<32>(op, Q, grid, st); break;
-                default: launch_op_async<64>(op, Q, grid, st); break;
-            }
-            return;
-        }
-        switch (lw_) {
-            case 8: launch_op<8>(op, Q, grid, st); break;
-            case 16: launch_op<16>(op, Q, grid, st); break;
-            case 32: launch_op<32>(op, Q, grid, st); break;
-            default: launch_op<64>(op, Q, grid, st); break;
-        }
+        if constexpr (kWide) launch_wide(LK_OPERATOR, op, Q, grid, st);
+        else launch_narrow(LK_OPERATOR, op, Q, grid, st);
     });
     fan_end();
 }
 
-// ---- wide2: lane-per-candidate kernel --------------------------------------------------------
-
-static size_t wide2_smem_bytes(int nvec) { return wide2_warp_vecs(nvec) * sizeof(uint4) * WARPS_PER_CTA; }
-
-template <int LW, int OP>
-static void launch_wide2_instance(const WideParams &P, int grid, size_t smem, cudaStream_t st) {
-    static std::once_flag once;  // opt in to the largest dynamic shared memory any nvec needs, once per instance
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(wide2_level_kernel<LW, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
-    });
-    wide2_level_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
-}
-
-template <int LW>
-static void launch_wide2_op(int op, const WideParams &P, int grid, size_t smem, cudaStream_t st) {
-    switch (op) {
-        case OP_ATOM: launch_wide2_instance<LW, OP_ATOM>(P, grid, smem, st); break;
-        case OP_NOT: launch_wide2_instance<LW, OP_NOT>(P, grid, smem, st); break;
-        case OP_NEXT: launch_wide2_instance<LW, OP_NEXT>(P, grid, smem, st); break;
-        case OP_FUTURE: launch_wide2_instance<LW, OP_FUTURE>(P, grid, smem, st); break;
-        case OP_AND: launch_wide2_instance<LW, OP_AND>(P, grid, smem, st); break;
-        case OP_UNTIL: launch_wide2_instance<LW, OP_UNTIL>(P, grid, smem, st); break;
-        default: launch_wide2_instance<LW, OP_OR>(P, grid, smem, st); break;
-    }
-}
-
-template <int LW>
-static void launch_wide2_small(const WideParams &P, int grid, size_t smem, cudaStream_t st) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(wide2_small_level_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
-    });
-    wide2_small_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
-}
-
-template <int LW>
-static int wide2_occupancy_of(int nvec) {
-    int occ = 0;
-    cudaFuncSetAttribute(wide2_level_kernel<LW, OP_UNTIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_level_kernel<LW, OP_UNTIL>, CTA_THREADS, wide2_smem_bytes(nvec)) != cudaSuccess) {
-        cudaGetLastError();
-        occ = 1;
-    }
-    return std::max(occ, 1);
-}
-
-// LTLB200_WIDE2=0 selects wide.cuh's group-per-candidate kernel instead of wide2.cuh's lane-per-candidate one.
-static bool wide2_enabled() {
-    static const bool on = [] {
-        const char *env = getenv("LTLB200_WIDE2");
-        return !(env && env[0] == '0');
-    }();
-    return on;
-}
-
-template <int LW>
-static void launch_wide2_guarded(const WideParams &P, int grid, size_t smem, cudaStream_t st) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(wide2_guarded_level_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide2_smem_bytes(MAX_NVEC));
-    });
-    wide2_guarded_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
-}
-
-void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) {
-    if (wide2_) {
-        const size_t smem = wide2_smem_bytes(nvec_);
-        const BlockDesc &last = lv.blocks.back();
-        if (P.scan_only || P.dead_n) {  // rare mode (collect_dead_ranges): one launch of the guarded kernel, any size
-            P.block_begin = 0;
-            P.block_end = (int)lv.blocks.size();
-            P.tile_begin = 0;
-            P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
-            P.ticket = CTR_TICKET0;
-            const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
-            switch (lw_) {
-                case 8: launch_wide2_guarded<8>(P, grid, smem, stream_); break;
-                case 16: launch_wide2_guarded<16>(P, grid, smem, stream_); break;
-                case 32: launch_wide2_guarded<32>(P, grid, smem, stream_); break;
-                default: launch_wide2_guarded<64>(P, grid, smem, stream_); break;
-            }
-            CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches++;
-            st_.enumerate_launches++;
-            return;
-        }
-        if (last.ord0 + last.size <= kSmallLevel) {
-            P.block_begin = 0;
-            P.block_end = (int)lv.blocks.size();
-            P.tile_begin = 0;
-            P.tile_end = last.tile0 + last.tiles_v * last.tiles_s;
-            P.ticket = CTR_TICKET0;
-            const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
-            switch (lw_) {
-                case 8: launch_wide2_small<8>(P, grid, smem, stream_); break;
-                case 16: launch_wide2_small<16>(P, grid, smem, stream_); break;
-                case 32: launch_wide2_small<32>(P, grid, smem, stream_); break;
-                default: launch_wide2_small<64>(P, grid, smem, stream_); break;
-            }
-            CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches++;
-            st_.enumerate_launches++;
-            return;
-        }
-        fan_begin();
-        for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid, int group) {
-            cudaStream_t st = fan_stream(group);
-            switch (lw_) {
-                case 8: launch_wide2_op<8>(op, Q, grid, smem, st); break;
-                case 16: launch_wide2_op<16>(op, Q, grid, smem, st); break;
-                case 32: launch_wide2_op<32>(op, Q, grid, smem, st); break;
-                default: launch_wide2_op<64>(op, Q, grid, smem, st); break;
-            }
-        });
-        fan_end();
-        return;
-    }
-    const BlockDesc &last_block = lv.blocks.back();
-    if (last_block.ord0 + last_block.size <= kSmallLevel / 4) {  // (a wide candidate is several vectors of work)
-        P.block_begin = 0;
-        P.block_end = (int)lv.blocks.size();
-        P.tile_begin = 0;
-        P.tile_end = last_block.tile0 + last_block.tiles_v * last_block.tiles_s;
-        P.ticket = CTR_TICKET0;
-        const int grid = (int)std::min<u64>((P.tile_end + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * 2);
-        switch (lw_) {
-            case 8: wide_small_level_kernel<8><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            case 16: wide_small_level_kernel<16><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            case 32: wide_small_level_kernel<32><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-            default: wide_small_level_kernel<64><<<grid, CTA_THREADS, 0, stream_>>>(P); break;
-        }
-        CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches++;
-        st_.enumerate_launches++;
-        return;
-    }
-    fan_begin();
-    for_each_operator(P, lv, sm_count_, occupancy_, st_, [&](int op, const WideParams &Q, int grid, int group) {
-        cudaStream_t st = fan_stream(group);
-        switch (lw_) {
-            case 8: launch_op_wide<8>(op, Q, grid, st); break;
-            case 16: launch_op_wide<16>(op, Q, grid, st); break;
-            case 32: launch_op_wide<32>(op, Q, grid, st); break;
-            default: launch_op_wide<64>(op, Q, grid, st); break;
-        }
-    });
-    fan_end();
-}
-
-// ---- partitioned path (narrow_part.cuh) ------------------------------------------------------
-
-constexpr size_t kPartSmem = sizeof(WarpSharedPart) * WARPS_PER_CTA;
-
-template <int LW, int OP>
-static void launch_part_instance(const NarrowParams &P, const PartParams &Q, int grid, cudaStream_t st) {
-    static std::once_flag once;  // opt in to > 48 KB of dynamic shared memory, once per instance
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(narrow_partition_kernel<LW, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem);
-    });
-    narrow_partition_kernel<LW, OP><<<grid, CTA_THREADS, kPartSmem, st>>>(P, Q);
-}
-
-template <int LW>
-static void launch_part_op(int op, const NarrowParams &P, const PartParams &Q, int grid, cudaStream_t st) {
-    switch (op) {
-        case OP_ATOM: launch_part_instance<LW, OP_ATOM>(P, Q, grid, st); break;
-        case OP_NOT: launch_part_instance<LW, OP_NOT>(P, Q, grid, st); break;
-        case OP_NEXT: launch_part_instance<LW, OP_NEXT>(P, Q, grid, st); break;
-        case OP_FUTURE: launch_part_instance<LW, OP_FUTURE>(P, Q, grid, st); break;
-        case OP_AND: launch_part_instance<LW, OP_AND>(P, Q, grid, st); break;
-        case OP_UNTIL: launch_part_instance<LW, OP_UNTIL>(P, Q, grid, st); break;
-        default: launch_part_instance<LW, OP_OR>(P, Q, grid, st); break;
-    }
-}
-
-template <int LW>
-static int part_occupancy_of() {
-    int occ = 0;
-    cudaFuncSetAttribute(narrow_partition_kernel<LW, OP_UNTIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_partition_kernel<LW, OP_UNTIL>, CTA_THREADS, kPartSmem) != cudaSuccess) {
-        cudaGetLastError();
-        occ = 1;
-    }
-    return std::max(occ, 1);
-}
-
-// LTLB200_PARTITION=0 forces the direct path, =1 forces the partitioned path for every level
-// (tests), unset = by size.
-bool Engine::partition_enabled() {
-    static const char *env = getenv("LTLB200_PARTITION");
-    return !(env && env[0] == '0');
-}
-
-bool Engine::use_partition(u64 constructed) const {
-    if (wide_ || !partition_enabled()) return false;
-    static const char *env = getenv("LTLB200_PARTITION");
-    if (env && env[0] == '1') return true;
-    // Opt-in only (LTLB200_PARTITION=1): on spec2 the two phases together (3.4 ms at cost 16) do not
-    // yet beat the direct kernel (2.8 ms); see DESIGN.md section 4.
-    (void)constructed;
-    return false;
-}
-
-// Phase A per operator (records into bucket chunks), chunk ordering, phase B (bucket by bucket
-// probing), over segments of the level's tile space so that the record pool stays bounded.
-void Engine::launch_partitioned(NarrowParams P, const LevelMeta &lv, u64 constructed, u64 n_tiles) {
-    const u64 kSegCandidates = 1ull << 28;  // records per segment (6 GiB of pool)
-    // segment ends in the level's flattened tile space, each segment bounded by kSegCandidates
-    std::vector<u64> seg_end, seg_records;
-    {
-        u64 acc = 0;
-        for (const BlockDesc &b : lv.blocks) {
-            const u64 per_tile = (u64)TILE_V * b.tile_s * (b.kind == BK_UNARY ? 1 : b.vg);
-            u64 t = b.tile0;
-            const u64 t_end = b.tile0 + b.tiles_v * b.tiles_s;
-            while (t < t_end) {
-                const u64 fit = (kSegCandidates - acc) / per_tile;
-                if (fit == 0) {
-                    seg_end.push_back(t);
-                    seg_records.push_back(acc);
-                    acc = 0;
-                    continue;
-                }
-                const u64 take = std::min(fit, t_end - t);
-                t += take;
-                acc += take * per_tile;
-            }
-        }
-        seg_end.push_back(n_tiles);
-        seg_records.push_back(acc);
-    }
-    const u64 warps = (u64)sm_count_ * part_occupancy_ * WARPS_PER_CTA;
-    int bucket_shift = 0;
-    while ((slots_.cap >> bucket_shift) > (u64)PART_NB) ++bucket_shift;
-    reserve(pc_, PC_COUNT, false);
-    u64 h_pc[PC_COUNT];
-    for (auto &c : h_pc) c = 0;
-    h_pc[PC_SEPBOUND] = VAL_EMPTY;
-    CUDA_CHECK(cudaMemcpyAsync(pc_.ptr, h_pc, sizeof(h_pc), cudaMemcpyHostToDevice, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));  // h_pc leaves scope; also the last level's pool is idle now
-    for (size_t seg = 0; seg < seg_end.size(); ++seg) {
-        const u64 s0 = seg ? seg_end[seg - 1] : 0, s1 = seg_end[seg];
-        if (s0 == s1) continue;
-        // operator groups of the level that overlap the segment
-        struct Group { size_t b0, b1; u64 t0, t1; int index; };
-        std::vector<Group> groups;
-        {
-            size_t b0 = 0;
-            int index = 0;
-            while (b0 < lv.blocks.size()) {
-                size_t b1 = b0;
-                while (b1 < lv.blocks.size() && lv.blocks[b1].op == lv.blocks[b0].op) ++b1;
-                const BlockDesc &last = lv.blocks[b1 - 1];
-                const u64 t0 = std::max(lv.blocks[b0].tile0, s0), t1 = std::min(last.tile0 + last.tiles_v * last.tiles_s, s1);
-                if (t0 < t1) groups.push_back({b0, b1, t0, t1, index});
-                b0 = b1;
-                ++index;
-            }
-        }
-        const u64 records_max = std::min(constructed, seg_records[seg]);
-        // full chunks + one open chunk per (warp, bucket) + ids abandoned at stash refills / left in the last stash
-        u64 pool_chunks = records_max / PART_CHUNK + records_max / (PART_CHUNK * 8) + warps * (PART_NB + PART_STASH) + 1024;
-        if (pool_chunks * PART_CHUNK >= (1ull << 32)) throw std::invalid_argument("record pool exceeds 2^32 records");
-        reserve(pool_keys_, pool_chunks * PART_CHUNK, false);
-        reserve(pool_ords_, pool_chunks * PART_CHUNK, false);
-        reserve(chunk_meta_, 2 * pool_chunks, false);
-        reserve(chunk_order_, pool_chunks, false);
-        reserve(wstate_, warps * PART_WSTATE, false);
-        PartParams Q{};
-        Q.pool_keys = pool_keys_.ptr;
-        Q.pool_ords = pool_ords_.ptr;
-        Q.chunk_bucket = chunk_meta_.ptr;
-        Q.chunk_fill = chunk_meta_.ptr + pool_chunks;
-        Q.order = chunk_order_.ptr;
-        Q.wstate = wstate_.ptr;
-        Q.wstate_slots = warps;
-        Q.pool_chunks = pool_chunks;
-        Q.pc = pc_.ptr;
-        Q.bucket_shift = bucket_shift;
-        Q.sep_bound_ok = (P.prune_after_sep && !store_has_separator_) ? 1 : 0;
-        CUDA_CHECK(cudaMemsetAsync(Q.chunk_bucket, 0xFF, pool_chunks, stream_));
-        CUDA_CHECK(cudaMemsetAsync(Q.chunk_fill, PART_CHUNK, pool_chunks, stream_));
-        CUDA_CHECK(cudaMemsetAsync(wstate_.ptr, 0, warps * PART_WSTATE * sizeof(u64), stream_));
-        if (s0 > 0) {  // later segments: everything but the pruning bound starts over, tile tickets too
-            CUDA_CHECK(cudaMemsetAsync(pc_.ptr, 0, PC_SEPBOUND * sizeof(u64), stream_));
-            CUDA_CHECK(cudaMemsetAsync(pc_.ptr + PC_TICKET, 0, (PC_COUNT - PC_TICKET) * sizeof(u64), stream_));
-            CUDA_CHECK(cudaMemsetAsync(d_counters_ + CTR_TICKET0, 0, (CTR_COUNT - CTR_TICKET0) * sizeof(u64), stream_));
-        }
-        for (const Group &g : groups) {
-            P.block_begin = (int)g.b0;
-            P.block_end = (int)g.b1;
-            P.tile_begin = g.t0;
-            P.tile_end = g.t1;
-            P.ticket = CTR_TICKET0 + g.index;
-            const int grid = (int)std::min<u64>((g.t1 - g.t0 + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * part_occupancy_);
-            const int op = (int)lv.blocks[g.b0].op;
-            DBG("partition op=%d tiles=[%llu,%llu) grid=%d", op, (unsigned long long)g.t0, (unsigned long long)g.t1, grid);
-            switch (lw_) {
-                case 8: launch_part_op<8>(op, P, Q, grid, stream_); break;
-                case 16: launch_part_op<16>(op, P, Q, grid, stream_); break;
-                case 32: launch_part_op<32>(op, P, Q, grid, stream_); break;
-                default: launch_part_op<64>(op, P, Q, grid, stream_); break;
-            }
-            CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches++;
-            st_.enumerate_launches++;
-        }
-        part_seal_kernel<<<sm_count_ * 4, 256, 0, stream_>>>(Q);
-        CUDA_CHECK(cudaGetLastError());
-        part_order_kernel<<<(unsigned)((pool_chunks + PART_ORDER_PER_BLOCK - 1) / PART_ORDER_PER_BLOCK), 256, 0, stream_>>>(Q);
-        CUDA_CHECK(cudaGetLastError());
-        const int pgrid = sm_count_ * LTLB200_PROBE_MIN_CTAS;
-        switch (lw_) {
-            case 8: narrow_probe_kernel<8><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
-            case 16: narrow_probe_kernel<16><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
-            case 32: narrow_probe_kernel<32><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
-            default: narrow_probe_kernel<64><<<pgrid, CTA_THREADS, 0, stream_>>>(P, Q); break;
-        }
-        CUDA_CHECK(cudaGetLastError());
-        st_.kernel_launches += 3;
-        st_.enumerate_launches += 3;
-        if (debug_on()) {
-            CUDA_CHECK(cudaStreamSynchronize(stream_));
-            u64 pcs[PC_COUNT];
-            CUDA_CHECK(cudaMemcpy(pcs, pc_.ptr, sizeof(pcs), cudaMemcpyDeviceToHost));
-            DBG("segment [%llu,%llu): pool chunks drawn=%llu ordered=%llu overflow=%llu sepbound=%llx", (unsigned long long)s0, (unsigned long long)s1, (unsigned long long)pcs[PC_POOL], (unsigned long long)pcs[PC_ORDERED], (unsigned long long)pcs[PC_OVERFLOW], (unsigned long long)pcs[PC_SEPBOUND]);
-        }
-    }
-    // a pool overflow cannot happen by construction of pool_chunks; level_begin checks the flag
-    // after its counter read-back and fails loudly if it ever does
-    CUDA_CHECK(cudaMemcpyAsync(h_counters_ + kPoolOverflowWord, pc_.ptr + PC_OVERFLOW, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-}
+void Engine::launch_enumerate(NarrowParams P, const LevelMeta &lv) { launch_level(P, lv); }
+void Engine::launch_enumerate_wide(WideParams P, const LevelMeta &lv) { launch_level(P, lv); }
 
 // ---- one level = begin (enumerate this rank's shard) [+ exchange] + end (finalise) ---------
 
@@ -1632,8 +1173,11 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
         st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
         dead_n_ = 0;
-        if (!exhaustive && store_has_separator_ && (!wide_ || wide2_) && shard_count == 1 && mode_batch_ > 0 &&
-            !async_enabled() && !use_partition(constructed)) {
+        if (!exhaustive && store_has_separator_ && shard_count == 1 && mode_batch_ > 0) {
+            // The dead ranges delete candidates -- among them the smaller-ordinal witnesses x & (y & r) that the
+            // associativity pruning of AND blocks relies on -- and leave this level incomplete: no pruning here
+            // nor in any later level of this store.
+            prune_ok_ = false;
             collect_dead_ranges(lv, constructed, (u64)mode_batch_);
             defer = false;  // (rare mode: the plain two-synchronisation path)
         }
@@ -1654,7 +1198,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             const u64 wide_slack = (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * std::max<u64>((u64)(32 >> log2g_) * WIDE_CHUNK, CLAIM_CHUNK) * 8 + 1024;
             // (narrow: every warp of every operator launch may end with a partly used chunk of claim indices)
             // (a small level is one launch of at most 2 CTAs per SM: narrow_small_level_kernel)
-            const u64 narrow_slack = constructed <= kSmallLevel && !async_enabled() && !use_partition(constructed)
+            const u64 narrow_slack = constructed <= kSmallLevel
                                          ? (u64)sm_count_ * 2 * WARPS_PER_CTA * CLAIM_CHUNK + 1024
                                          : (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8 + 1024;
             const u64 claim_cap = est + (wide_ ? wide_slack : narrow_slack);
@@ -1664,7 +1208,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             const u64 want_slots = next_pow2(2 * (total_ + est));
             DBG("level %d attempt %d: constructed=%llu est=%llu claim_cap=%llu slots=%llu want=%llu", cost, attempt, (unsigned long long)constructed, (unsigned long long)est, (unsigned long long)claim_cap, (unsigned long long)table_slots(), (unsigned long long)want_slots);
             if (want_slots > table_slots()) rebuild_table(grown_size(want_slots));
-            if (exhaustive) reserve(sep_list_, std::max<u64>(1ull << 20, constructed / 16), false);
+            if (exhaustive) reserve(sep_list_, std::max<u64>(std::max<u64>(1ull << 20, constructed / 16), sep_want_), false);
             // counters start at zero (CTR_SEP at "none"); the special-key register persists across levels
             level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
             CUDA_CHECK(cudaGetLastError());
@@ -1688,24 +1232,28 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
                 P.shard_offset = (u64)shard_index;
                 PHASE(1, "begin: setup (copies, memsets)", tp);
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
-                if (use_partition(constructed)) launch_partitioned(P, lv, constructed, n_tiles);
-                else launch_enumerate(P, lv);
+                launch_enumerate(P, lv);
             }
             CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
             PHASE(2, "begin: launches", tp);
-            if (defer && !use_partition(constructed)) {
+            if (defer) {
                 pl.deferred = true;
                 st_.enumerate_candidates += constructed / (u64)shard_count;
                 return LTLB200_OK;
             }
-            h_counters_[kPoolOverflowWord] = 0;
             read_counters();
-            if (h_counters_[kPoolOverflowWord]) throw CudaError("record pool overflow in the partitioned path");
             PHASE(3, "begin: sync + read counters", tp);
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
             st_.enumerate_ms += ms;
             st_.enumerate_candidates += constructed / (u64)shard_count;
+            if (exhaustive && h_counters_[CTR_OVERFLOW] == 0 && h_counters_[CTR_SEPCOUNT] > sep_list_.cap) {
+                // more separating candidates than the list holds: the chunk-exact separator needs all of them
+                sep_want_ = h_counters_[CTR_SEPCOUNT] + 1024;
+                if (attempt > 8) throw CudaError("separator list keeps overflowing");
+                rebuild_table(table_slots());  // drops this attempt's claims
+                continue;
+            }
             if (h_counters_[CTR_OVERFLOW] == 0) break;
             if (attempt > 8 || (exact && !wide_)) throw CudaError("hash set overflow on an exactly sized table");
             est = std::min(constructed, est * 4);
@@ -2014,11 +1562,16 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
             F.claim_cap = pl.claim_cap;
             F.cut_allowed = exhaustive ? 0 : 1;
             if (small) {
-                static std::once_flag once;
-                std::call_once(once, [] {
-                    cudaFuncSetAttribute(narrow_small_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((SMALL_FIN_MAX_BITS / 8) + 512 * sizeof(uint32_t) + 256));
-                });
+                {   // opt in to > 48 KB of dynamic shared memory: a per-device attribute of the kernel
+                    static std::mutex mu;
+                    static unsigned long long seen = 0;
+                    std::lock_guard<std::mutex> lock(mu);
+                    if (!(seen >> (device_ & 63) & 1ull)) {
+                        cudaFuncSetAttribute(narrow_small_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)((SMALL_FIN_MAX_BITS / 8) + 512 * sizeof(uint32_t) + 256));
+                        seen |= 1ull << (device_ & 63);
+                    }
+                }
                 const size_t smem = (size_t)n_sb * 32 * sizeof(uint32_t) + (size_t)n_sb * sizeof(uint32_t);
                 narrow_small_finalize_kernel<<<1, SMALL_FIN_THREADS, smem, stream_>>>(F, n_bits, d_counters_, exhaustive ? 1 : 0);
                 CUDA_CHECK(cudaGetLastError());
@@ -2046,6 +1599,11 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         recycle_retired(false);
         pl.active = false;
         if (h_counters_[CTR_OVERFLOW]) {  // the guess of new CMs was too small: nothing was finalised
+            table_dirty_ = true;
+            return kRetryLevel;
+        }
+        if (exhaustive && h_counters_[CTR_SEPCOUNT] > sep_list_.cap) {  // redo with a list that holds them all
+            sep_want_ = h_counters_[CTR_SEPCOUNT] + 1024;
             table_dirty_ = true;
             return kRetryLevel;
         }

@@ -1,0 +1,122 @@
+// inst.cu -- instantiates the enumeration kernels of ONE lane width (see launch.h).
+//
+//   nvcc -DLTLB200_INST_LW=8|16|32|64 -DLTLB200_INST_WIDE=0|1 -c inst.cu
+//
+// INST_WIDE=0: narrow.cuh (CMs of one uint4), INST_WIDE=1: wide2.cuh (multi-vector CMs).
+#include <mutex>
+
+#include "launch.h"
+#if LTLB200_INST_WIDE
+#include "wide2.cuh"
+#else
+#include "narrow.cuh"
+#endif
+
+#ifndef LTLB200_INST_LW
+#error "compile with -DLTLB200_INST_LW=<lane bits>"
+#endif
+
+#define LTLB200_CAT_(a, b) a##b
+#define LTLB200_CAT(a, b) LTLB200_CAT_(a, b)
+
+namespace ltlb200 {
+
+constexpr int LW = LTLB200_INST_LW;
+
+#if !LTLB200_INST_WIDE
+
+void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st) {
+    if (kind == LK_SMALL) {
+        narrow_small_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
+        return;
+    }
+    if (kind == LK_GUARDED) {
+        narrow_guarded_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
+        return;
+    }
+    switch (op) {
+        case OP_ATOM: narrow_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_NOT: narrow_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_NEXT: narrow_level_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_FUTURE: narrow_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_AND: narrow_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_UNTIL: narrow_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        default: narrow_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
+    }
+}
+
+int LTLB200_CAT(narrow_occupancy_, LTLB200_INST_LW)() {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, OP_UNTIL>, CTA_THREADS, 0) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    return occ > 1 ? occ : 1;
+}
+
+#else  // wide
+
+static size_t max_smem() { return wide2_warp_vecs(MAX_NVEC) * sizeof(uint4) * WARPS_PER_CTA; }
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-DEVICE attribute of a kernel: a process that drives
+// several GPUs (synthesize_dnc(devices=[0, 1]), one store per device) must opt in on each of them.
+template <typename Kernel>
+static void opt_in(Kernel kernel, int device, unsigned long long &seen, std::mutex &mu) {
+    std::lock_guard<std::mutex> lock(mu);
+    const unsigned long long bit = 1ull << (device & 63);
+    if (seen & bit) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem());
+    seen |= bit;
+}
+
+template <int OP>
+static void launch_operator(const WideParams &P, int grid, size_t smem, int device, cudaStream_t st) {
+    static unsigned long long seen = 0;
+    static std::mutex mu;
+    opt_in(wide2_level_kernel<LW, OP>, device, seen, mu);
+    wide2_level_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
+}
+
+void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WideParams &P, int grid, size_t smem, int device,
+                                                 cudaStream_t st) {
+    if (kind == LK_SMALL) {
+        static unsigned long long seen = 0;
+        static std::mutex mu;
+        opt_in(wide2_small_level_kernel<LW>, device, seen, mu);
+        wide2_small_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
+        return;
+    }
+    if (kind == LK_GUARDED) {
+        static unsigned long long seen = 0;
+        static std::mutex mu;
+        opt_in(wide2_guarded_level_kernel<LW>, device, seen, mu);
+        wide2_guarded_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
+        return;
+    }
+    switch (op) {
+        case OP_ATOM: launch_operator<OP_ATOM>(P, grid, smem, device, st); break;
+        case OP_NOT: launch_operator<OP_NOT>(P, grid, smem, device, st); break;
+        case OP_NEXT: launch_operator<OP_NEXT>(P, grid, smem, device, st); break;
+        case OP_FUTURE: launch_operator<OP_FUTURE>(P, grid, smem, device, st); break;
+        case OP_AND: launch_operator<OP_AND>(P, grid, smem, device, st); break;
+        case OP_UNTIL: launch_operator<OP_UNTIL>(P, grid, smem, device, st); break;
+        default: launch_operator<OP_OR>(P, grid, smem, device, st); break;
+    }
+}
+
+int LTLB200_CAT(wide2_occupancy_, LTLB200_INST_LW)(int nvec, int device) {
+    static unsigned long long seen = 0;
+    static std::mutex mu;
+    opt_in(wide2_level_kernel<LW, OP_UNTIL>, device, seen, mu);
+    int occ = 0;
+    const size_t smem = wide2_warp_vecs(nvec) * sizeof(uint4) * WARPS_PER_CTA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_level_kernel<LW, OP_UNTIL>, CTA_THREADS, smem) != cudaSuccess) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    return occ > 1 ? occ : 1;
+}
+
+#endif
+
+}  // namespace ltlb200

@@ -1,0 +1,33 @@
+// launch.h -- host-side entry points of the enumeration kernels, one set per lane width.
+//
+// The construction + dedup kernels are templates over (lane width, operator); instantiating all of
+// them in one translation unit took four minutes of nvcc.  inst.cu is compiled once per
+// (lane width, narrow | wide) with -DLTLB200_INST_LW / -DLTLB200_INST_WIDE and exports the plain
+// functions below; engine.cu dispatches on the lane width at run time.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace ltlb200 {
+
+struct NarrowParams;
+struct WideParams;
+
+// which kernel of a (lane width) set: one launch per operator (big levels), one launch for every
+// operator (levels up to kSmallLevel candidates), the guarded kernel (scan pass / dead ranges)
+enum : int { LK_OPERATOR = 0, LK_SMALL = 1, LK_GUARDED = 2 };
+
+#define LTLB200_DECLARE_LW(LW)                                                                                     \
+    void narrow_launch_##LW(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st);                    \
+    int narrow_occupancy_##LW();                                                                                    \
+    void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \
+    int wide2_occupancy_##LW(int nvec, int device);
+
+LTLB200_DECLARE_LW(8)
+LTLB200_DECLARE_LW(16)
+LTLB200_DECLARE_LW(32)
+LTLB200_DECLARE_LW(64)
+#undef LTLB200_DECLARE_LW
+
+}  // namespace ltlb200

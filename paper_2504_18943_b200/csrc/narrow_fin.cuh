@@ -1,0 +1,242 @@
+// narrow_fin.cuh -- finalisation, regrow and claim exchange kernels of the narrow path (non-template
+// kernels: included by engine.cu only, so that they exist once in the library).
+#pragma once
+#include "narrow.cuh"
+
+namespace ltlb200 {
+
+// ---- finalisation: order the level's winners by ordinal without a sort -------------
+// A bitmap with one bit per candidate ordinal marks the winners; a popcount prefix over
+// 1024-bit superblocks turns an ordinal into its rank, i.e. the entry's position in the
+// level (reference order = ordinal order), and the rows are scattered straight to it.
+
+struct FinalizeParams {
+    const uint4 *claim_key;
+    const u64 *claim_ord;
+    u64 n_claimed;  // claim indices reserved (some unused: ord = all ones)
+    uint32_t *bitmap;         // one bit per ordinal
+    const uint32_t *sb_rank;  // exclusive popcount prefix per 32-word superblock
+    u64 ord_limit;            // keep ordinals <= limit (separator in a non-exhaustive run, else all ones - 1)
+    uint4 *store;
+    u64 *ords;
+    u64 base;  // global id of the level's first entry
+    // Deferred mode (live != NULL): the host has not read the level's counters yet -- it launched
+    // the finalisation right behind the enumeration, one synchronisation per level instead of
+    // two -- so the claim count, the separator and the overflow flag are read here.
+    const u64 *live;
+    u64 claim_cap;
+    int cut_allowed;  // non-exhaustive: keep only ordinals <= the separator
+};
+
+// resolves n_claimed / ord_limit in deferred mode; false = the level overflowed and is redone
+__device__ __forceinline__ bool finalize_bounds(const FinalizeParams &F, u64 &n_claimed, u64 &ord_limit) {
+    n_claimed = F.n_claimed;
+    ord_limit = F.ord_limit;
+    if (F.live == nullptr) return true;
+    if (F.live[CTR_OVERFLOW]) return false;
+    const u64 claimed = F.live[CTR_CLAIMED], sep = F.live[CTR_SEP];
+    n_claimed = claimed < F.claim_cap ? claimed : F.claim_cap;
+    ord_limit = (F.cut_allowed && sep != VAL_EMPTY) ? sep : VAL_EMPTY - 1;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) narrow_mark_kernel(const FinalizeParams F) {
+    u64 n_claimed, ord_limit;
+    if (!finalize_bounds(F, n_claimed, ord_limit)) return;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = F.claim_ord[t];
+        if (ord <= ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
+    }
+}
+
+__device__ __forceinline__ u64 ordinal_rank(const uint32_t *bitmap, const uint32_t *sb_rank, u64 ord) {
+    const u64 word = ord >> 5, sb = word >> 5;
+    u64 rank = sb_rank[sb];
+    for (u64 w = sb << 5; w < word; ++w) rank += __popc(bitmap[w]);
+    return rank + __popc(bitmap[word] & ((1u << (ord & 31)) - 1u));
+}
+
+__global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParams F) {
+    u64 n_claimed, ord_limit;
+    if (!finalize_bounds(F, n_claimed, ord_limit)) return;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = F.claim_ord[t];
+        if (ord > ord_limit) continue;  // unused index, or ordered after the separator
+        const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
+        F.store[gid] = F.claim_key[t];
+        F.ords[gid] = ord;
+    }
+}
+
+// Small levels: the whole finalisation in ONE CTA.  The winners bitmap of a level of up to 2^19
+// candidates is 64 KiB and lives in shared memory, so mark -> superblock ranks -> summary ->
+// scatter need no global bitmap, no scan launches and no separate summary launch: such a level
+// is launch latency, and this is one launch instead of five.
+constexpr int SMALL_FIN_THREADS = 1024;
+constexpr u64 SMALL_FIN_MAX_BITS = 1ull << 15;
+
+__global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kernel(const FinalizeParams F, u64 n_bits, u64 *counters,
+                                                                                  int export_bitmap) {
+    extern __shared__ uint32_t s_fin[];
+    const u64 n_words = (n_bits + 31) >> 5, n_sb = (n_words + 31) >> 5;  // <= 16384 words, <= 512 superblocks
+    uint32_t *bitmap = s_fin, *sb_rank = s_fin + n_sb * 32;              // bitmap padded to whole superblocks
+    __shared__ uint32_t warp_tot[32];
+    u64 n_claimed, ord_limit;
+    if (!finalize_bounds(F, n_claimed, ord_limit)) return;  // uniform: the level overflowed and is redone
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (u64 w = tid; w < n_sb * 32; w += SMALL_FIN_THREADS) bitmap[w] = 0u;
+    __syncthreads();
+    for (u64 t = tid; t < n_claimed; t += SMALL_FIN_THREADS) {
+        const u64 ord = F.claim_ord[t];
+        if (ord <= ord_limit) atomicOr(&bitmap[ord >> 5], 1u << (ord & 31));
+    }
+    __syncthreads();
+    // exclusive popcount prefix per superblock (n_sb <= 512 <= threads)
+    uint32_t v = 0;
+    if ((u64)tid < n_sb)
+        for (int k = 0; k < 32; ++k) v += __popc(bitmap[tid * 32 + k]);
+    uint32_t incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = warp_tot[lane];
+        uint32_t wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+            if (lane >= d) wi += t;
+        }
+        warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    if ((u64)tid < n_sb) sb_rank[tid] = warp_tot[warp] + incl - v;
+    __syncthreads();
+    if (export_bitmap) {  // exhaustive runs pick their reported separator against the winners bitmap afterwards
+        for (u64 w = tid; w < n_sb * 32; w += SMALL_FIN_THREADS) F.bitmap[w] = bitmap[w];
+        if ((u64)tid < n_sb) const_cast<uint32_t *>(F.sb_rank)[tid] = sb_rank[tid];
+    }
+    if (tid == 0) {  // winners of the level, rank of the separator
+        const u64 sep_ord = counters[CTR_SEP];
+        counters[CTR_WINNERS] = n_bits ? ordinal_rank(bitmap, sb_rank, n_bits - 1) + ((bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u) : 0;
+        counters[CTR_SEPRANK] = sep_ord < n_bits ? ordinal_rank(bitmap, sb_rank, sep_ord) : ~0ull;
+    }
+    for (u64 t = tid; t < n_claimed; t += SMALL_FIN_THREADS) {
+        const u64 ord = F.claim_ord[t];
+        if (ord > ord_limit) continue;
+        const u64 gid = F.base + ordinal_rank(bitmap, sb_rank, ord);
+        F.store[gid] = F.claim_key[t];
+        F.ords[gid] = ord;
+    }
+}
+
+// re-insert finalised rows [first, first+count) into a fresh table (regrow / rollback)
+__global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 slot_mask, const uint4 *store,
+                                                             u64 first, u64 count, u64 *counters) {
+    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (u64)gridDim.x * blockDim.x) {
+        const u64 gid = first + t;
+        const uint4 key = store[gid];
+        if (key_is_empty(key)) {
+            counters[CTR_SPECIAL] = gid;
+            continue;
+        }
+        u64 slot = hash_vec(key, 0u) & slot_mask;
+        for (;;) {
+            uint4 old = cas128(&slots[slot].key, empty, key);
+            if (key_is_empty(old)) {
+                slots[slot].val = gid;
+                break;
+            }
+            slot = (slot + 1) & slot_mask;
+        }
+    }
+}
+
+// ---- exchange of a level's claims between ranks (one search sharded over several GPUs) ----
+// A record is {key (uint4), ordinal (u64)}.  owner(key) = a hash independent of the slot hash.
+
+__device__ __forceinline__ uint32_t key_owner(uint4 key, uint32_t owners) {
+    return hash_vec(key, 0x5BD1E995u) % owners;
+}
+
+// counts[o] += claims of this level owned by rank o; with `cursors`, also writes the records
+// grouped by owner (cursors[o] = next free position of owner o's range)
+__global__ void __launch_bounds__(256) narrow_export_kernel(const uint4 *claim_key, const u64 *claim_ord, u64 n_claimed,
+                                                            uint32_t owners, u64 *counts, u64 *cursors, uint4 *keys_out,
+                                                            u64 *ords_out) {
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = claim_ord[t];
+        if (ord == VAL_EMPTY) continue;  // reserved but never used
+        const uint4 key = claim_key[t];
+        const uint32_t o = key_owner(key, owners);
+        if (cursors) {
+            const u64 pos = atomicAdd(&cursors[o], 1ull);
+            keys_out[pos] = key;
+            ords_out[pos] = ord;
+        } else {
+            atomicAdd(&counts[o], 1ull);
+        }
+    }
+}
+
+// insert-or-min received records into the local set; new CMs get a claim index of their own
+__global__ void __launch_bounds__(256) narrow_import_kernel(const NarrowParams P, const uint4 *keys, const u64 *ords, u64 n) {
+    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (u64)gridDim.x * blockDim.x) {
+        const uint4 key = keys[t];
+        const u64 ord = ords[t];
+        u64 *val_at = nullptr;
+        bool claimed = false, overflow = false;
+        u64 my_idx = 0;
+        if (key_is_empty(key)) {  // the all-ones CM has a register instead of a slot
+            val_at = &P.counters[CTR_SPECIAL];
+            if (*(volatile u64 *)val_at == VAL_EMPTY) {
+                my_idx = atomicAdd(&P.counters[CTR_CLAIMED], 1ull);
+                if (my_idx >= P.claim_cap) overflow = true;
+                else claimed = atomicCAS(val_at, VAL_EMPTY, P.epoch | my_idx) == VAL_EMPTY;
+            }
+        } else {
+            u64 slot = hash_vec(key, 0u) & P.slot_mask;
+            for (;;) {
+                uint4 k = ld_cg_u4(&P.slots[slot].key);
+                if (key_is_empty(k)) {
+                    my_idx = atomicAdd(&P.counters[CTR_CLAIMED], 1ull);  // stays unused if the CAS below loses
+                    if (my_idx >= P.claim_cap) {
+                        overflow = true;
+                        break;
+                    }
+                    k = cas128(&P.slots[slot].key, empty, key);
+                    if (key_is_empty(k)) {
+                        claimed = true;
+                        __stcg(&P.slots[slot].val, P.epoch | my_idx);
+                        k = key;
+                    }
+                }
+                if (v_eq(k, key)) {
+                    val_at = &P.slots[slot].val;
+                    break;
+                }
+                slot = (slot + 1) & P.slot_mask;
+            }
+        }
+        if (overflow) {
+            atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
+            continue;
+        }
+        if (claimed) {
+            P.claim_key[my_idx] = key;
+            atomicMin(&P.claim_ord[my_idx], ord);
+        } else {
+            u64 v;
+            while ((v = *(volatile u64 *)val_at) == VAL_EMPTY) {}  // a claimer publishes right after its CAS
+            if (v >= P.epoch) atomicMin(&P.claim_ord[v & CLAIM_IDX_MASK], ord);
+        }
+    }
+}
+
+}  // namespace ltlb200

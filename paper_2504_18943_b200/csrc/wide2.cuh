@@ -20,7 +20,7 @@
 //     finalisation are wide.cuh's, unchanged: both kernels can run against the same set (the
 //     sharded import and the regrow still use wide.cuh's code), and the results are identical.
 #pragma once
-#include "wide.cuh"
+#include "wide_common.cuh"
 
 namespace ltlb200 {
 

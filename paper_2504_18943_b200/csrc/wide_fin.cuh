@@ -1,0 +1,159 @@
+// wide_fin.cuh -- finalisation, regrow and claim exchange kernels of the wide path (non-template
+// kernels: included by engine.cu only, so that they exist once in the library).
+#pragma once
+#include "wide_common.cuh"
+
+namespace ltlb200 {
+
+// ---- finalisation (wide) -------------------------------------------------------------------
+
+struct WideFinalize {
+    u64 *slots;
+    const uint4 *stage_rows;
+    const u64 *stage_ord;
+    const uint32_t *stage_slot;
+    u64 n_staged;  // staging entries reserved (some unused: ord = all ones)
+    uint32_t *bitmap;
+    const uint32_t *sb_rank;
+    u64 ord_limit;
+    uint4 *store;
+    u64 *ords;
+    u64 base;
+    int nvec;
+    u64 *stage_gid;  // final id per staging entry (written by wide_rank_kernel)
+    // deferred mode (see FinalizeParams in narrow.cuh): bounds resolved on the device
+    const u64 *live;
+    u64 stage_cap;
+    int cut_allowed;
+};
+
+__device__ __forceinline__ bool wide_finalize_bounds(const WideFinalize &F, u64 &n_staged, u64 &ord_limit) {
+    n_staged = F.n_staged;
+    ord_limit = F.ord_limit;
+    if (F.live == nullptr) return true;
+    if (F.live[CTR_OVERFLOW]) return false;
+    const u64 claimed = F.live[CTR_CLAIMED], sep = F.live[CTR_SEP];
+    n_staged = claimed < F.stage_cap ? claimed : F.stage_cap;
+    ord_limit = (F.cut_allowed && sep != VAL_EMPTY) ? sep : VAL_EMPTY - 1;
+    return true;
+}
+
+__global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
+    u64 n_staged, ord_limit;
+    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_staged; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = F.stage_ord[t];
+        if (ord <= ord_limit) atomicOr(&F.bitmap[ord >> 5], 1u << (ord & 31));
+    }
+}
+
+// Scatter in two steps, so that the rank of an entry is computed once, not once per vector:
+//   wide_rank_kernel   one thread per staging entry: final id = base + rank(ordinal); records the
+//                      ordinal, re-points the entry's slot word at the final id, leaves the id in
+//                      stage_gid (all ones = entry unused or ordered after the separator);
+//   wide_copy_kernel   one thread per (staging entry, vector): coalesced copy of the row to its
+//                      place in the cache.
+__global__ void __launch_bounds__(256) wide_rank_kernel(const WideFinalize F) {
+    u64 n_staged, ord_limit;
+    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
+    for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n_staged; k += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = F.stage_ord[k];
+        if (ord > ord_limit) {
+            F.stage_gid[k] = ~0ull;
+            continue;
+        }
+        const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
+        F.stage_gid[k] = gid;
+        F.ords[gid] = ord;
+        u64 *slot = &F.slots[F.stage_slot[k]];
+        *slot = (*slot & ~SLOT_IDX_MASK) | (gid + 1);  // same fingerprint, final row id
+    }
+}
+
+__global__ void __launch_bounds__(256) wide_copy_kernel(const WideFinalize F) {
+    u64 n_staged, ord_limit;
+    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
+    const u64 total = n_staged * (u64)F.nvec;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+        const u64 k = t / F.nvec;
+        const u64 gid = F.stage_gid[k];
+        if (gid == ~0ull) continue;
+        F.store[gid * F.nvec + (t - k * F.nvec)] = F.stage_rows[t];
+    }
+}
+
+// re-insert finalised rows [0, count) into a fresh table: rows of the cache are pairwise
+// distinct, so claiming the first empty slot of the probe sequence is enough
+__global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_mask, const uint4 *store, u64 count,
+                                                           int nvec, int log2g) {
+    for (u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x; gid < count; gid += (u64)gridDim.x * blockDim.x) {
+        uint32_t a = 0, b = 0;
+        for (int p = 0; p < nvec; ++p) {
+            const uint4 part = store[gid * nvec + p];
+            a ^= hash_vec(part, 0x9E3779B9u * (uint32_t)(p + 1));
+            b ^= hash_vec(part, 0x7F4A7C15u * (uint32_t)(p + 1) + 0x632BE5ABu);
+        }
+        a ^= a >> 16;
+        a *= 0x85EBCA6Bu;
+        a ^= a >> 13;
+        b ^= b >> 15;
+        b *= 0xC2B2AE35u;
+        b ^= b >> 16;
+        u64 s = a & slot_mask;
+        const u64 word = slot_word(b >> 8, gid);
+        while (atomicCAS(&slots[s], 0ull, word) != 0ull) s = (s + 1) & slot_mask;
+    }
+}
+
+// ---- exchange of a level's claims between ranks (wide rows) ----------------------------------
+
+__device__ __forceinline__ uint32_t row_owner(const uint4 *row, int nvec, uint32_t owners) {
+    uint32_t h = 0;
+    for (int p = 0; p < nvec; ++p) h ^= hash_vec(row[p], 0x5BD1E995u * (uint32_t)(p + 1));
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 13;
+    return h % owners;
+}
+
+// one thread per staging entry: count per owner, or (with cursors) copy the records out grouped by owner
+__global__ void __launch_bounds__(256) wide_export_kernel(const uint4 *stage_rows, const u64 *stage_ord, u64 n_staged, int nvec,
+                                                          uint32_t owners, u64 *counts, u64 *cursors, uint4 *rows_out,
+                                                          u64 *ords_out) {
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_staged; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = stage_ord[t];
+        if (ord == VAL_EMPTY) continue;  // reserved but never published
+        const uint32_t o = row_owner(stage_rows + t * nvec, nvec, owners);
+        if (cursors) {
+            const u64 pos = atomicAdd(&cursors[o], 1ull);
+            for (int p = 0; p < nvec; ++p) rows_out[pos * nvec + p] = stage_rows[t * nvec + p];
+            ords_out[pos] = ord;
+        } else {
+            atomicAdd(&counts[o], 1ull);
+        }
+    }
+}
+
+// one group per received record: the same insert as the enumeration kernel
+__global__ void __launch_bounds__(CTA_THREADS) wide_import_kernel(const __grid_constant__ WideParams P, const uint4 *rows, const u64 *ords, u64 n) {
+    const int lane = threadIdx.x & 31;
+    const int G = 1 << P.log2g;
+    GroupGeom g;
+    g.base = lane & ~(G - 1);
+    g.part = lane & (G - 1);
+    g.leader = g.base;
+    g.has_part = g.part < P.nvec;
+    g.mask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << g.base;
+    GroupState gs;
+    const u64 groups_per_block = (u64)(CTA_THREADS >> P.log2g);
+    const u64 first = (u64)blockIdx.x * groups_per_block + (threadIdx.x >> P.log2g);
+    for (u64 t = first; t < n; t += (u64)gridDim.x * groups_per_block) {
+        const uint4 part = g.has_part ? rows[t * P.nvec + g.part] : make_uint4(0, 0, 0, 0);
+        uint32_t slot, fp;
+        row_hash(part, g, P.log2g, slot, fp);
+        slot &= (uint32_t)P.slot_mask;
+        wide_insert(P, g, gs, part, slot, fp, group_load_slot(&P.slots[slot], g), ords[t]);
+    }
+}
+
+}  // namespace ltlb200

@@ -62,6 +62,15 @@ for seed, found in ((0, 5), (1, 5)):  # 24-byte CMs: the wide path
              schedule=sched((FULL, False, found + 2), (FULL, True, 1))),
     ]
 CASES.append(dict(name="c3_s2_exh11", workload="c3", seed=2, engine_exact=True, schedule=sched((FULL, True, 11))))
+# exhaustive levels that record a separating CM, then a NON-exhaustive level: chunk truncation over complete levels
+# (the associativity pruning of AND blocks must be off there: the dead ranges delete the witnesses it relies on)
+NAN = ["not", "and", "next"]
+for batch in (64, 65536):
+    CASES.append(dict(name=f"c1_s3_nan_exh7_then_nonexhaustive_b{batch}", workload="c1", seed=3, engine_exact=False,
+                      batch_size=batch, schedule=sched((NAN, True, 7), (NAN, False, 2), (NAN, True, 1))))
+for seed in (0, 2, 4):
+    CASES.append(dict(name=f"c1_s{seed}_exh_then_nonexhaustive_b256", workload="c1", seed=seed, engine_exact=False,
+                      batch_size=256, schedule=sched((FULL, True, 7), (FULL, False, 2))))
 
 
 def sha(a):
@@ -76,7 +85,7 @@ def main():
         store = ref_engine.CandidateStore(rspec)
         levels = []
         for cost, (ops, exhaustive) in enumerate(case["schedule"], 1):
-            cfg = ref_engine.EngineConfig(exhaustive=exhaustive, threads=1)
+            cfg = ref_engine.EngineConfig(exhaustive=exhaustive, threads=1, batch_size=case.get("batch_size", 65536))
             stats = ref_engine.RunStats()
             n, sep = ref_engine.expand_level(store, cost, tuple(ops), config=cfg, stats=stats)
             lv = store.level(cost)

@@ -32,7 +32,7 @@ def test_engine_reproduces_reference_schedule(case):
     store = engine.CandidateStore(spec)
     try:
         for (ops, exhaustive), gl in zip(case["schedule"], case["levels"]):
-            cfg = engine.EngineConfig(exhaustive=exhaustive)
+            cfg = engine.EngineConfig(exhaustive=exhaustive, batch_size=case.get("batch_size", 65536))
             stats = engine.RunStats()
             n_new, sep = engine.expand_level(store, gl["cost"], tuple(ops), config=cfg, stats=stats)
             where = f"{case['name']} cost {gl['cost']}"

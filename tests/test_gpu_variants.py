@@ -1,15 +1,10 @@
-"""GPU parity of the alternative narrow-path kernels.
+"""GPU parity of the engine's run-time switches.
 
-The engine chooses its kernel path per level by size; the alternatives are selected with
-environment switches that the library reads once per process, so each variant runs the parity
+The switches are environment variables that the library reads once per process, so each variant runs the parity
 cases in a child process:
 
-  LTLB200_PARTITION=1   radix-partitioned dedup for EVERY level (narrow_part.cuh)
-  LTLB200_ASYNC=1       cp.async probe pipeline (narrow_async.cuh)
   LTLB200_NO_DEFER=1    two synchronisations per level (finalisation launched after the counters
                         were read) instead of the deferred, device-bounded finalisation
-  LTLB200_WIDE2=0       multi-vector CMs by wide.cuh's group-per-candidate kernel instead of
-                        wide2.cuh's lane-per-candidate kernel (the default)
   LTLB200_PRUNE=0       no associativity pruning: every AND candidate is probed
   LTLB200_OPSTREAMS=0   every operator launch of a level on the engine's own stream, one after the
                         other, instead of fanned out over side streams (the default)
@@ -41,8 +36,7 @@ print("variant ok")
 """
 
 
-@pytest.mark.parametrize("switch,value,cases", [("LTLB200_PARTITION", "1", CASES), ("LTLB200_ASYNC", "1", CASES),
-                                                 ("LTLB200_NO_DEFER", "1", CASES), ("LTLB200_WIDE2", "0", WIDE_CASES),
+@pytest.mark.parametrize("switch,value,cases", [("LTLB200_NO_DEFER", "1", CASES + WIDE_CASES),
                                                  ("LTLB200_OPSTREAMS", "0", CASES + WIDE_CASES),
                                                  ("LTLB200_PRUNE", "0", CASES)])
 def test_variant_matches_reference(switch, value, cases):
