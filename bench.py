@@ -3,27 +3,34 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
 
-A *step* is one complete search of the workload's example set: every cost level is
-enumerated on the device until the minimal separating formula is found (or the cost cap
-is hit).  The default workload is BASELINE.json's second configuration -- "the paper's
-running example with the default cost function" -- which SURVEY.md section 8(d) maps onto
-the paper's 7+7-trace LTL example (``spec2``: 142,066,187 candidates, 16,258,320 unique
-CMs, witness of cost 16).
+A *step* is one complete search of the workload's example set: every cost level is enumerated on the device
+until the minimal separating formula is found (or the cost cap is hit).
+
+* N = 1 (default): BASELINE.json's second configuration -- "the paper's running example with the default cost
+  function" -- which SURVEY.md section 8(d) maps onto the paper's 7+7-trace LTL example (``spec2``: 142,066,187
+  candidates, 16,258,320 unique CMs, witness of cost 16).
+* N > 1: ONE search sharded over the N GPUs (owner-sharded dedup set, candidates routed to their hash owners,
+  paper_2504_18943_b200/dist.py): strong scaling, so the default workload is one with seconds of work,
+  ``c3-16`` (BASELINE configs[2]'s example set exhaustively to cost 16); the line also carries the same search on
+  ONE GPU of the same box (``single_gpu``), so every N > 1 line is a self-contained scaling point.
+  Without torchrun's environment ``--gpus N`` starts the N ranks itself (torch.distributed.run, 127.0.0.1).
 
 Numbers on the line:
 
-* ``value``            unique CMs per second, device-resident: the specification is already
-                       on the GPU, K searches are timed with CUDA events on the engine's
-                       stream (max over ranks);
-* ``e2e``              the same metric through the public API ``synthesize(spec, config)``
-                       with host inputs, a fresh store per step, host<->device copies and the
-                       witness read-back inside the timed region (wall clock, max over ranks);
-* ``roofline``         the construction+dedup kernels: algorithmic bytes over
-                       their CUDA-event time, against the measured HBM copy peak;
-* ``cpu_baseline``     the CPU oracle port timed on this host on a bounded sample.
+* ``value``         unique CMs per second, device-resident: the specification is already on the GPU, K searches are
+                    timed with CUDA events on the engine's stream (max over ranks);
+* ``e2e``           the same metric through the public API ``synthesize(spec, config)`` with host inputs, a fresh
+                    store per step, host<->device copies (counted by the handle that ran the search) and the
+                    witness read-back inside the timed region (wall clock, max over ranks);
+* ``roofline``      the construction+dedup kernels: algorithmic bytes over their CUDA-event time,
+                    against the measured HBM copy peak;
+* ``cpu_baseline``  the reference's own CPU implementation (``oracle/_ref``: the unmodified ``ltlsynth`` package,
+                    installed there by ``__graft_entry__.build()``; else the C port ``oracle/ltl_oracle.c``) timed on
+                    this host on a bounded sample of the same workload;
+* ``workloads``     (N = 1) BASELINE configs[2], [3], [4] in short device-resident runs: ``c3-fill`` (<= 128-bit CMs
+                    until the set cannot grow), ``c4-1024`` (1024-bit CMs), ``c5-12`` (LTL, 128-byte CMs, cost 12).
 
-``--impl reference`` times the CPU restatement of the reference (``oracle/``: the reference
-itself is Python + numpy and does not travel to the GPU box) on a bounded sample.
+``--impl reference`` times the reference's CPU implementation alone (rank 0; the other ranks exit).
 Only that leg and ``cpu_baseline`` touch ``oracle/``; the measured product path never does.
 """
 
@@ -33,6 +40,7 @@ import argparse
 import json
 import os
 import pathlib
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,19 +52,27 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "unique_cs_per_s"
 UNIT = "unique CS/s"
-# per-workload: (max_cost, exhaustive, CPU sample max_cost)
+# per workload: cost cap and mode of the GPU search; `sample_cost` = cost cap of the bounded CPU sample
+# (chosen so that one CPU step takes seconds); `base` = the example set when the name is a variant
 WORKLOADS = {
-    "spec2": dict(max_cost=16, exhaustive=False, cpu_max_cost=14),
-    "c3": dict(max_cost=13, exhaustive=True, cpu_max_cost=11),
-    # BASELINE configs[2]: "<= 128-bit CS, enumerated until the cache fills HBM on 1 GPU": cost 17 stores 639 M CMs
-    # (100 GB); cost 18 would need a hash set beyond 2^32 slots and ends the run with "memory budget exhausted"
-    "c3-fill": dict(max_cost=18, exhaustive=True, cpu_max_cost=11, base="c3"),
-    "c1": dict(max_cost=14, exhaustive=False, cpu_max_cost=14),
-    "spec1": dict(max_cost=10, exhaustive=True, cpu_max_cost=10),
-    "c5": dict(max_cost=10, exhaustive=True, cpu_max_cost=9),
-    "c4-512": dict(max_cost=10, exhaustive=True, cpu_max_cost=9),
-    "c4-1024": dict(max_cost=10, exhaustive=True, cpu_max_cost=9),
+    "spec2": dict(max_cost=16, exhaustive=False, sample_cost=13),
+    "c3": dict(max_cost=13, exhaustive=True, sample_cost=11),
+    # BASELINE configs[2]: "<= 128-bit CS, enumerated until the cache fills HBM on 1 GPU": cost 17 stores 639 M CMs;
+    # cost 18 would need a hash set beyond 2^32 slots and ends the run with "memory budget exhausted"
+    "c3-fill": dict(max_cost=18, exhaustive=True, sample_cost=11, base="c3"),
+    "c3-16": dict(max_cost=16, exhaustive=True, sample_cost=11, base="c3"),
+    "c1": dict(max_cost=14, exhaustive=False, sample_cost=14),
+    "spec1": dict(max_cost=10, exhaustive=True, sample_cost=10),
+    "c5": dict(max_cost=10, exhaustive=True, sample_cost=9),
+    "c5-12": dict(max_cost=12, exhaustive=True, sample_cost=9, base="c5"),
+    "c4-512": dict(max_cost=10, exhaustive=True, sample_cost=9),
+    "c4-1024": dict(max_cost=10, exhaustive=True, sample_cost=9),
+    "c4-1024-11": dict(max_cost=11, exhaustive=True, sample_cost=9, base="c4-1024"),
 }
+DEFAULT_WORKLOAD = {1: "spec2"}
+DEFAULT_SHARDED_WORKLOAD = "c3-16"
+EXTRA_WORKLOADS = ("c3-fill", "c4-1024-11", "c5-12")
+OPERATORS = "not,next,future,and,until"
 
 
 def measured_peaks() -> tuple[float, str]:
@@ -112,34 +128,74 @@ def algorithmic_bytes(key_bytes: int, constructed: int, unique: int, unary_candi
     return key_bytes * (unary_candidates + constructed + 2 * unique) + 8 * unique
 
 
+def workload_config(name: str, seed: int) -> dict:
+    wl = WORKLOADS[name]
+    return {"workload": name, "seed": seed, "operators": OPERATORS, "max_cost": wl["max_cost"], "exhaustive": wl["exhaustive"]}
+
+
+# ---- the reference's CPU implementation -------------------------------------------------------------------------
+
+def cpu_reference(name: str, seed: int, repeats: int, warmup: int) -> dict:
+    """Times the reference's CPU enumerator on a bounded sample of workload `name` (cost cap `sample_cost`):
+    `warmup` untimed runs, then `repeats` timed ones.  oracle/_ref (the unmodified reference, all host threads:
+    its own benchmark protocol, pkg/scripts/benchmark_throughput.py:28-40) when it is installed, else the
+    single-core C port.  -> dict(kind, cores, times, unique, constructed, sample)."""
+    from paper_2504_18943_b200 import workloads
+
+    wl = WORKLOADS[name]
+    spec = workloads.named_workload(wl.get("base", name), seed)
+    ref_dir = ROOT / "oracle" / "_ref"
+    times, unique, constructed = [], 0, 0
+    if (ref_dir / "ltlsynth" / "engine.py").exists():
+        sys.path.insert(0, str(ref_dir))
+        try:
+            import ltlsynth
+            from paper_2504_18943_b200.traces import serialize_specification
+
+            rspec = ltlsynth.parse_specification(serialize_specification(spec))
+            cores = os.cpu_count() or 1
+            cfg = ltlsynth.EngineConfig(max_cost=wl["sample_cost"], exhaustive=wl["exhaustive"], threads=cores,
+                                        time_budget_s=3600.0, memory_budget_mb=1 << 20)
+            for step in range(warmup + repeats):
+                t0 = time.perf_counter()
+                res = ltlsynth.synthesize(rspec, cfg)
+                if step >= warmup:
+                    times.append(time.perf_counter() - t0)
+                unique, constructed = res.stats.unique, res.stats.constructed
+            kind, what = "reference", f"oracle/_ref: unmodified ltlsynth {getattr(ltlsynth, '__version__', '0.1.0')}, threads={cores}"
+        finally:
+            sys.path.remove(str(ref_dir))
+    else:
+        import oracle
+
+        oracle.build()
+        cores = 1
+        for step in range(warmup + repeats):
+            t0 = time.perf_counter()
+            res = oracle.synthesize(spec, max_cost=wl["sample_cost"], exhaustive=wl["exhaustive"], time_budget_s=3600.0,
+                                    memory_budget_mb=1 << 20)
+            if step >= warmup:
+                times.append(time.perf_counter() - t0)
+            unique, constructed = res.unique, res.constructed
+        kind, what = "port", "oracle/ltl_oracle.c on one host core (oracle/_ref is not installed)"
+    sample = (f"{name} cost levels 1..{wl['sample_cost']} of {wl['max_cost']}: {constructed} candidates, {unique} unique CMs "
+              f"per step ({what})")
+    return dict(kind=kind, cores=cores, times=times, unique=unique, constructed=constructed, sample=sample)
+
+
 def run_reference(args, rank: int) -> int:
     if rank != 0:
         return 0
-    import oracle
-    from paper_2504_18943_b200 import workloads
-
-    cfg = WORKLOADS[args.workload]
-    spec = workloads.named_workload(cfg.get("base", args.workload), args.seed)
-    oracle.build()
-    times, last = [], None
-    for step in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        last = oracle.synthesize(spec, max_cost=cfg["cpu_max_cost"], exhaustive=cfg["exhaustive"],
-                                 time_budget_s=3600.0, memory_budget_mb=1 << 20)
-        if step >= args.warmup:
-            times.append(time.perf_counter() - t0)
-    per_step = sum(times) / len(times)
-    value = last.unique / per_step
-    sample = (f"{args.workload} cost levels 1..{cfg['cpu_max_cost']}: {last.constructed} candidates, "
-              f"{last.unique} unique CMs per step")
+    ref = cpu_reference(args.workload, args.seed, args.steps, args.warmup)
+    per_step = sum(ref["times"]) / len(ref["times"])
+    value = ref["unique"] / per_step
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": args.workload, "seed": args.seed, "operators": "not,next,future,and,until",
-                   "max_cost": cfg["cpu_max_cost"], "exhaustive": cfg["exhaustive"]},
-        "constructed_per_s": last.constructed / per_step,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "config": workload_config(args.workload, args.seed),
+        "constructed_per_s": ref["constructed"] / per_step,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref["cores"], "kind": ref["kind"], "sample": ref["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -147,28 +203,137 @@ def run_reference(args, rank: int) -> int:
     return 0
 
 
+# ---- launching N ranks ----------------------------------------------------------------------------------------
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def respawn_under_torchrun(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start the N ranks here (one process per GPU) and pass their output on."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(ROOT / "bench.py"), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "WARN")
+    return subprocess.call(cmd, env=env)
+
+
+# ---- one device-resident measurement ---------------------------------------------------------------------------
+
+def search_loop(store, cfg, expand):
+    """One search on a store that is already on the device -> (stats, (separator id, cost) or None)."""
+    from paper_2504_18943_b200 import engine
+
+    store.reset()
+    stats, found = engine.RunStats(), None
+    for cost in range(1, cfg.max_cost + 1):
+        stats.max_cost_reached = cost
+        try:
+            _, sep = expand(store, cost, cfg, stats)
+        except engine._BudgetExceeded:  # the cache filled the device: the search ends here (outcome "exhausted")
+            break
+        if sep is not None and found is None:
+            found = (sep, cost)
+            if not cfg.exhaustive:
+                break
+    return stats, found
+
+
+def device_arm(name, seed, device, stream, steps, warmup, expand, sync, clocks_index=None):
+    """K searches of workload `name`, specification resident in HBM, timed with CUDA events on `stream`."""
+    import torch
+
+    from paper_2504_18943_b200 import engine, workloads
+
+    wl = WORKLOADS[name]
+    spec = workloads.named_workload(wl.get("base", name), seed)
+    cfg = engine.EngineConfig(max_cost=wl["max_cost"], exhaustive=wl["exhaustive"], time_budget_s=3600.0,
+                              memory_budget_mb=1 << 20, device=device)
+    store = engine.CandidateStore(spec, device=device, stream=stream.cuda_stream)
+    try:
+        for _ in range(warmup):
+            stats, found = search_loop(store, cfg, expand)
+        before = store.device_stats()
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sync()
+        sampler = ClockSampler(clocks_index) if clocks_index is not None else None
+        if sampler:
+            sampler.__enter__()
+        start.record(stream)
+        for _ in range(steps):
+            stats, found = search_loop(store, cfg, expand)
+        stop.record(stream)
+        sync()
+        if sampler:
+            sampler.__exit__()
+        after = store.device_stats()
+        out = dict(spec=spec, cfg=cfg, stats=stats, found=found, device_ms=start.elapsed_time(stop), before=before, after=after,
+                   clocks=sampler.summary() if sampler else None, levels=[store.level(c).n for c in range(1, len(store.levels) + 1)])
+        out["witness"] = None
+        if found:
+            from paper_2504_18943_b200 import to_text
+
+            out["witness"] = to_text(engine.reconstruct(store, found[0]), spec.alphabet)
+        return out
+    finally:
+        store.close()
+
+
+def kernel_numbers(arm, steps) -> dict:
+    """Per-step kernel figures of a device arm and the roofline fraction of its construction+dedup kernels."""
+    before, after, stats = arm["before"], arm["after"], arm["stats"]
+    enum_ms = (after["enumerate_ms"] - before["enumerate_ms"]) / steps
+    unary = 3 * sum(arm["levels"][:-1])  # not, next, future over every level but the last
+    alg = algorithmic_bytes(after["key_bytes"], stats.constructed, stats.unique, unary)
+    peak, peak_src = measured_peaks()
+    achieved = alg / (enum_ms * 1e-3) / 1e9 if enum_ms > 0 else 0.0
+    return dict(enum_ms=enum_ms, fin_ms=(after["finalize_ms"] - before["finalize_ms"]) / steps,
+                enum_launches=(after["enumerate_launches"] - before["enumerate_launches"]) // steps,
+                launches=(after["kernel_launches"] - before["kernel_launches"]) // steps,
+                alg_bytes=alg, achieved=achieved, peak=peak, peak_src=peak_src, frac=achieved / peak)
+
+
 def main() -> int:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="spec2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the `workloads` table (N = 1)")
+    ap.add_argument("--selftest-cpu", action="store_true",
+                    help="launch check without GPUs: the sharded protocol over gloo with the numpy shard engine of tests/")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
 
+    under_launcher = "WORLD_SIZE" in os.environ and "RANK" in os.environ
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
+        args.workload = args.workload or "spec2"
         return run_reference(args, rank)
+    if args.gpus > 1 and not under_launcher:
+        return respawn_under_torchrun(args)
+    if under_launcher and world != args.gpus:
+        if rank == 0:
+            print(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks; measuring {world}", file=sys.stderr)
+    if args.selftest_cpu:
+        return selftest_cpu(args, rank, world)
+    args.warmup = max(args.warmup, 3)
+    args.workload = args.workload or (DEFAULT_WORKLOAD[1] if world == 1 else DEFAULT_SHARDED_WORKLOAD)
 
     import torch
     import torch.distributed as dist
 
-    from paper_2504_18943_b200 import engine, to_text, workloads
+    from paper_2504_18943_b200 import _native, engine, to_text, workloads
+    from paper_2504_18943_b200 import dist as pdist
+    from paper_2504_18943_b200.traces import smallest_lane_dtype
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the engine has no CPU path")
@@ -182,165 +347,145 @@ def main() -> int:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x: float) -> float:
+    def reduce_over_ranks(x: float, op) -> float:
         if not distributed:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def sum_over_ranks(x: float) -> float:
-        if not distributed:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
-    from paper_2504_18943_b200 import dist as pdist
-
-    wl = WORKLOADS[args.workload]
-    # N > 1: ONE search whose pair space is sharded over the ranks, one exchange per level
-    # (route claims to hash owners, all-gather winners, min-reduce the separator): strong scaling.
-    spec = workloads.named_workload(wl.get("base", args.workload), args.seed)
-    cfg = engine.EngineConfig(max_cost=wl["max_cost"], exhaustive=wl["exhaustive"], time_budget_s=3600.0,
-                              memory_budget_mb=1 << 20, device=local_rank)
     stream = torch.cuda.current_stream()
+    single = lambda store, cost, cfg, stats: engine.expand_level(store, cost, cfg.operators, config=cfg, stats=stats)
+    sharded = lambda store, cost, cfg, stats: pdist.sharded_expand_level(store, cost, cfg.operators, cfg, stats)
 
-    # ---- device-resident arm: specification already in HBM, K searches timed with CUDA events
-    store = engine.CandidateStore(spec, device=local_rank, stream=stream.cuda_stream)
+    # ---- device-resident arm
+    arm = device_arm(args.workload, args.seed, local_rank, stream, args.steps, args.warmup, sharded if distributed else single,
+                     barrier, clocks_index=local_rank)
+    device_ms = reduce_over_ranks(arm["device_ms"], dist.ReduceOp.MAX if distributed else None)
+    spec, cfg, stats = arm["spec"], arm["cfg"], arm["stats"]
+    k = kernel_numbers(arm, args.steps)
+    launches = int(reduce_over_ranks(float(k["launches"]), dist.ReduceOp.SUM if distributed else None))
 
-    def search_once():
-        store.reset()
-        stats = engine.RunStats()
-        found = None
-        for cost in range(1, cfg.max_cost + 1):
-            try:
-                if distributed:
-                    _, sep = pdist.sharded_expand_level(store, cost, cfg.operators, cfg, stats)
-                else:
-                    _, sep = engine.expand_level(store, cost, cfg.operators, config=cfg, stats=stats)
-            except engine._BudgetExceeded:  # the cache filled the device: the search ends here (outcome "exhausted")
-                break
-            if sep is not None and found is None:
-                found = (sep, cost)
-                if not cfg.exhaustive:
-                    break
-        return stats, found
-
-    for _ in range(args.warmup):
-        stats, found = search_once()
-    before = store.device_stats()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    with ClockSampler(local_rank) as clocks:
-        start.record(stream)
-        for _ in range(args.steps):
-            stats, found = search_once()
-        stop.record(stream)
-        barrier()
-    device_ms = max_over_ranks(start.elapsed_time(stop))
-    after = store.device_stats()
-    unique_per_step, constructed_per_step = stats.unique, stats.constructed
-    witness = to_text(engine.reconstruct(store, found[0]), spec.alphabet) if found else None
-    enum_ms = (after["enumerate_ms"] - before["enumerate_ms"]) / args.steps
-    fin_ms = (after["finalize_ms"] - before["finalize_ms"]) / args.steps
-    enum_launches = (after["enumerate_launches"] - before["enumerate_launches"]) // args.steps
-    launches = (after["kernel_launches"] - before["kernel_launches"]) // args.steps
-    key_bytes, table_slots, device_bytes = after["key_bytes"], after["table_slots"], after["device_bytes"]
-    unary = 0
-    for cost in range(2, len(store.levels) + 1):
-        unary += 3 * store.level(cost - 1).n  # not, next, future over the previous level
-    store.close()
-
-    # ---- end-to-end arm: public API, host inputs, fresh store per step
+    # ---- end-to-end arm: public API, host inputs, fresh store per step; the copies are counted by the handle
     run_api = (lambda: pdist.synthesize_sharded(spec, cfg)) if distributed else (lambda: engine.synthesize(spec, cfg))
     for _ in range(2):
         res = run_api()
     barrier()
+    h2d = d2h = 0
     t0 = time.perf_counter()
     for _ in range(args.steps):
         res = run_api()
+        h2d += res.device_stats["h2d_bytes"]
+        d2h += res.device_stats["d2h_bytes"]
     torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    # copies of one search (block tables up, counters / witness provenance down) + the specification upload
-    h2d = (after["h2d_bytes"] - before["h2d_bytes"]) // args.steps + 16 * (spec.alphabet.n + 2)
-    d2h = (after["d2h_bytes"] - before["d2h_bytes"]) // args.steps + 8 * (2 * (found[1] if found else 1))
+    e2e_s = reduce_over_ranks(time.perf_counter() - t0, dist.ReduceOp.MAX if distributed else None)
 
-    # every rank ends with the same (replicated) store: the job's units are those of one search
-    total_unique = float(unique_per_step)
-    total_constructed = float(constructed_per_step)
-    launches = int(sum_over_ranks(float(launches)))
+    # ---- N > 1: the same search on ONE GPU of this box (rank 0 alone), so that the line is a scaling point by itself
+    single_gpu = None
+    if distributed:
+        if rank == 0:
+            one = device_arm(args.workload, args.seed, local_rank, stream, max(1, min(args.steps, 3)), 1, single, torch.cuda.synchronize)
+            n1 = max(1, min(args.steps, 3))
+            single_gpu = {"ms_per_step": one["device_ms"] / n1, "value": one["stats"].unique * n1 / (one["device_ms"] * 1e-3),
+                          "unit": UNIT, "steps": n1, "unique_per_step": one["stats"].unique}
+        barrier()
+
+    extra = None
+    if not distributed and not args.no_extra and args.workload == DEFAULT_WORKLOAD[1]:
+        extra = {}
+        for name in EXTRA_WORKLOADS:
+            _native.load().ltlb200_trim(local_rank)
+            try:
+                a = device_arm(name, args.seed, local_rank, stream, 2, 1, single, torch.cuda.synchronize)
+            except Exception as err:  # noqa: BLE001  (a workload that does not fit this device is reported, not fatal)
+                extra[name] = {"error": str(err)[:200]}
+                continue
+            kk = kernel_numbers(a, 2)
+            extra[name] = {"ms_per_step": a["device_ms"] / 2, "unique_per_s": a["stats"].unique * 2 / (a["device_ms"] * 1e-3),
+                           "constructed_per_s": a["stats"].constructed * 2 / (a["device_ms"] * 1e-3),
+                           "unique_per_step": a["stats"].unique, "constructed_per_step": a["stats"].constructed,
+                           "max_cost_reached": a["stats"].max_cost_reached, "cm_bytes": a["after"]["row_bytes"],
+                           "device_bytes": a["after"]["device_bytes"], "kernel_ms_per_step": kk["enum_ms"],
+                           "finalize_ms_per_step": kk["fin_ms"], "roofline_frac": kk["frac"], "steps": 2, "warmup": 1}
+        _native.load().ltlb200_trim(local_rank)
+
     if rank != 0:
         if distributed:
             dist.destroy_process_group()
         return 0
 
-    peak, peak_src = measured_peaks()
-    alg_bytes = algorithmic_bytes(key_bytes, constructed_per_step, unique_per_step, unary)
-    achieved = alg_bytes / (enum_ms * 1e-3) / 1e9 if enum_ms > 0 else 0.0
+    after = arm["after"]
+    key_bytes, table_slots, device_bytes = after["key_bytes"], after["table_slots"], after["device_bytes"]
+    slot_bytes = 32 if key_bytes == 16 else 8
     # DRAM bytes the enumerate kernels actually moved in one search: from the committed ncu pass of
     # this workload (dram__bytes_read.sum + dram__bytes_write.sum summed over the enumerate launches)
     traffic, traffic_src = None, None
     profs = sorted((ROOT / "profiles").glob(f"r*_dram_{args.workload}.json"))  # the latest committed pass
-    prof = profs[-1] if profs else ROOT / "profiles" / "none"
-    if prof.exists():
-        pj = json.loads(prof.read_text())
-        traffic, traffic_src = pj["enumerate_dram_bytes"], f"profiles/{prof.name} (bytes per search over {pj['enumerate_launches']} enumerate launches)"
+    if profs:
+        pj = json.loads(profs[-1].read_text())
+        traffic, traffic_src = pj["enumerate_dram_bytes"], f"profiles/{profs[-1].name} (bytes per search over {pj['enumerate_launches']} enumerate launches)"
     # measured ceiling of the probe's access pattern on this device (random 32-byte slots, 256-bit loads)
     probe = None
     tool = ROOT / "tools" / "random_probe_bench"
-    if tool.exists():
+    if tool.exists() and not distributed:
         try:
-            mb = max(128, int(table_slots * 32 >> 20))
+            mb = max(128, int(table_slots * slot_bytes >> 20))
             out = subprocess.run([str(tool), str(mb)], capture_output=True, text=True, timeout=60).stdout
             rates = [float(line.split(":")[1].split()[0]) for line in out.splitlines() if "probes/ns" in line]
             if rates:
-                probes_per_step = constructed_per_step  # at most one first probe per candidate
                 probe = {"table_mb": mb, "ceiling_probes_per_ns": max(rates),
-                         "kernel_candidates_per_ns": probes_per_step / (enum_ms * 1e6) if enum_ms > 0 else None}
+                         "kernel_candidates_per_ns": stats.constructed / (k["enum_ms"] * 1e6) if k["enum_ms"] > 0 else None}
         except (OSError, subprocess.SubprocessError, ValueError):
             probe = None
+    config = workload_config(args.workload, args.seed)
+    config.update({
+        "cm_bytes": after["row_bytes"],
+        "parallelism": (f"one search over {world} GPUs: pair space tile-sharded, dedup set owner-sharded, per level one NCCL "
+                        "all-to-all of candidate records to their hash owners, one all-reduce of the winners bitmap, one "
+                        "all-gather of the winners") if distributed else "single GPU",
+        "l2": f"working set {device_bytes >> 20} MiB (hash set {table_slots * slot_bytes >> 20} MiB) exceeds the 126 MB L2; no flush needed",
+    })
+    lane = "lane_bits"
+    kernel_name = (f"narrow_level_kernel<{lane}, op> + narrow_small_level_kernel<{lane}> (construction + separation check + hash-set dedup)"
+                   if key_bytes == 16 else
+                   f"wide2_level_kernel<{lane}, op> + wide2_small_level_kernel<{lane}> (construction + separation check + hash-set dedup)")
+    if distributed:
+        kernel_name = ("narrow_route_kernel + narrow_probe_kernel" if key_bytes == 16 else "wide2_route_kernel + wide_import_kernel") + \
+            " (construction + routing to hash owners; owner-side dedup)"
     line = {
         "metric": METRIC,
-        "value": total_unique * args.steps / (device_ms * 1e-3),
+        "value": stats.unique * args.steps / (device_ms * 1e-3),
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": device_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak",
+        "scaling": "strong" if distributed else "weak",
         "vs_baseline": None,
-        "dtype": "u8" if key_bytes == 16 else "u16",
+        "dtype": "u%d" % (8 * smallest_lane_dtype(spec.max_length).itemsize),
         "data": "synthetic",
-        "config": {
-            "workload": args.workload, "seed": args.seed, "operators": ",".join(cfg.operators),
-            "max_cost": cfg.max_cost, "exhaustive": cfg.exhaustive, "cm_bytes": after["row_bytes"],
-            "parallelism": (f"one search, pair space tile-sharded over {world} GPUs, per-level NCCL all-to-all to hash "
-                            "owners + all-gather of winners") if world > 1 else "single GPU",
-            "l2": f"working set {device_bytes >> 20} MiB (hash set {table_slots * 32 >> 20} MiB) exceeds the 126 MB L2; no flush needed",
-        },
+        "config": config,
         "time_to_solution_ms": device_ms / args.steps,
-        "constructed_per_s": total_constructed * args.steps / (device_ms * 1e-3),
-        "unique_per_step": unique_per_step,
-        "constructed_per_step": constructed_per_step,
-        "witness": witness,
+        "constructed_per_s": stats.constructed * args.steps / (device_ms * 1e-3),
+        "unique_per_step": stats.unique,
+        "constructed_per_step": stats.constructed,
+        "witness": arm["witness"],
         "e2e": {
-            "value": total_unique * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "time_to_solution_ms": 1e3 * e2e_s / args.steps,
-            "api": ("paper_2504_18943_b200.dist.synthesize_sharded(spec, EngineConfig)" if world > 1
+            "value": stats.unique * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d // args.steps),
+            "d2h_bytes_per_step": int(d2h // args.steps), "time_to_solution_ms": 1e3 * e2e_s / args.steps,
+            "api": ("paper_2504_18943_b200.dist.synthesize_sharded(spec, EngineConfig)" if distributed
                     else "paper_2504_18943_b200.engine.synthesize(spec, EngineConfig)"),
+            "bytes_source": "ltlb200_stats.h2d_bytes / d2h_bytes of the handles that ran the timed searches",
             "witness": to_text(res.formula, spec.alphabet) if res.formula is not None else None,
         },
         "gpu_launches": int(launches * args.steps),
-        "clocks": clocks.summary(),
+        "clocks": arm["clocks"],
         "roofline": {
-            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic,
-            "kernel": ("narrow_level_kernel<lane_bits, op> + narrow_small_level_kernel (construction + separation check + "
-                       "hash-set dedup)") if key_bytes == 16 else "wide_level_kernel<lane_bits, op>",
-            "launches_per_step": int(enum_launches), "kernel_ms_per_step": enum_ms, "finalize_ms_per_step": fin_ms,
-            "algorithmic_bytes_per_step": alg_bytes, "peak_source": peak_src,
+            "bound": "hbm", "achieved": k["achieved"], "peak": k["peak"], "unit": "GB/s", "frac": k["frac"],
+            "traffic": traffic, "kernel": kernel_name,
+            "launches_per_step": int(k["enum_launches"]), "kernel_ms_per_step": k["enum_ms"], "finalize_ms_per_step": k["fin_ms"],
+            "algorithmic_bytes_per_step": k["alg_bytes"], "peak_source": k["peak_src"],
             "traffic_source": traffic_src,
             "random_probe": probe,
             "note": "the dedup probe is one random 32-byte sector per candidate; the ceiling for that access pattern "
@@ -348,23 +493,53 @@ def main() -> int:
                     "what bounds the kernel, not the copy bandwidth used as `peak`",
         },
     }
+    if single_gpu is not None:
+        line["single_gpu"] = single_gpu
+    if extra is not None:
+        line["workloads"] = extra
     if not args.no_cpu_baseline:
-        import oracle
-
-        oracle.build()
-        t0 = time.perf_counter()
-        ref = oracle.synthesize(workloads.named_workload(wl.get("base", args.workload), args.seed), max_cost=wl["cpu_max_cost"],
-                                exhaustive=wl["exhaustive"], time_budget_s=3600.0, memory_budget_mb=1 << 20)
-        cpu_s = time.perf_counter() - t0
+        ref = cpu_reference(args.workload, args.seed, 3, 1)  # one warm-up, best of three (the reference's own protocol)
+        best = min(ref["times"])
         line["cpu_baseline"] = {
-            "value": ref.unique / cpu_s, "unit": UNIT, "cores": 1, "kind": "port",
-            "constructed_per_s": ref.constructed / cpu_s,
-            "sample": f"{args.workload} cost levels 1..{wl['cpu_max_cost']}: {ref.constructed} candidates, "
-                      f"{ref.unique} unique CMs, {cpu_s:.1f} s on one host core (oracle/ltl_oracle.c)",
+            "value": ref["unique"] / best, "unit": UNIT, "cores": ref["cores"], "kind": ref["kind"],
+            "constructed_per_s": ref["constructed"] / best,
+            "sample": ref["sample"] + f", best of 3 = {best:.2f} s",
         }
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
+    return 0
+
+
+def selftest_cpu(args, rank: int, world: int) -> int:
+    """`bench.py --gpus N --selftest-cpu`: proves that the launch path starts N ranks and that they run the sharded
+    protocol together -- gloo instead of NCCL, the numpy shard engine of tests/ instead of the CUDA engine.
+    Not a measurement: the line says so."""
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from cpu_shard_engine import CpuShardEngine
+
+    from paper_2504_18943_b200 import dist as pdist
+    from paper_2504_18943_b200 import engine, to_text, workloads
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("gloo", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{free_port()}")
+    pdist.REPLICATE_BELOW = 0
+    spec = workloads.spec1()
+    t0 = time.perf_counter()
+    res = pdist.synthesize_sharded(spec, engine.EngineConfig(), store_factory=CpuShardEngine)
+    elapsed = time.perf_counter() - t0
+    pids = [None] * world
+    dist.all_gather_object(pids, os.getpid())
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"impl": "selftest-cpu-shards", "n_gpus": world, "processes": len(set(pids)), "backend": "gloo",
+                          "witness": to_text(res.formula, spec.alphabet), "unique_per_step": res.stats.unique,
+                          "ms_per_step": 1e3 * elapsed, "note": "launch check, not a measurement"}), flush=True)
     return 0
 
 

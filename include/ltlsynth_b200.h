@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define LTLB200_ABI_VERSION 1
+#define LTLB200_ABI_VERSION 2
 
 /* operator tags == reference engine.py:42 (OP_ATOM..OP_OR) */
 enum {
@@ -127,31 +127,50 @@ int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int3
                          int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
 
 /*
- * One search sharded over several GPUs: the level is split into
- *   ltlb200_level_begin   enumerate the tiles of shard `shard_index` of `shard_count` into the
- *                         local hash set (every rank holds the whole cache of earlier levels);
- *                         outputs the local claim count, the smallest ordinal of a fresh
- *                         separating candidate (all ones = none) and how many separating
- *                         ordinals were recorded (exhaustive runs);
- *   ltlb200_claims_count / _pack   export this level's local claims as records
- *                         {CM row (ltlb200_key_bytes bytes), ordinal u64} grouped by hash owner,
- *                         into DEVICE buffers the caller hands to NCCL;
- *   ltlb200_claims_import insert-or-min received records (device buffers) into the local set;
- *   ltlb200_level_end     finalise with the GLOBAL separator ordinal (and, for exhaustive runs,
- *                         every separating ordinal of the level, host array; NULL = local ones).
- * ltlb200_expand_level == level_begin(shard 0 of 1) + level_end.  The reference has no
- * counterpart: its only parallelism is a thread pool inside expand_level (engine.py:386-391).
+ * One search sharded over several GPUs.  The language cache is replicated on every rank; the dedup set
+ * is OWNER-SHARDED (rank r holds the CMs whose hash owner is r), so its capacity grows with the number of GPUs and
+ * every rank probes 1/N of the level's candidates.  The reference has no counterpart: its only parallelism is a
+ * thread pool inside expand_level (engine.py:386-391) whose results must not depend on the thread count
+ * (tests/test_engine.py:162-175) -- the contract kept here: N ranks == 1 rank, bit for bit.
+ *
+ * One level (the collectives in brackets are the caller's: NCCL through torch.distributed in dist.py; all
+ * buffers are DEVICE memory owned by the handle, records are {CM row of ltlb200_key_bytes bytes, ordinal u64}):
+ *
+ *   ltlb200_route_begin     builds this rank's tile-strided share of the pair space; every candidate that is not
+ *                           a duplicate by construction is appended to the send region of its hash owner.
+ *                           Outputs, per owner o: send_counts[o] records starting at record send_offsets[o] of
+ *                           *rows_dev / *ords_dev; the smallest ordinal of a separating candidate this rank built
+ *                           (all ones = none) and how many separating ordinals it recorded (exhaustive runs,
+ *                           ltlb200_seps_copy).
+ *   [all-to-all]            into the buffers ltlb200_exchange_recv hands out (source-major, dense)
+ *   ltlb200_owner_reduce    insert-or-min of the first n_records received records into the owned part of the set;
+ *                           marks this owner's winners in the level's bitmap (one bit per candidate ordinal of the
+ *                           whole level; *bitmap_words 32-bit words at *bitmap_dev)
+ *   [all-reduce SUM]        of the bitmaps (the owners' bits are disjoint, so the sum is the union); min of the
+ *                           separator ordinal
+ *   ltlb200_winners_export  this owner's winners with ordinal <= sep_ord, as dense records
+ *   [all-gather]            every rank receives the winners of the OTHER owners (ltlb200_exchange_recv again)
+ *   ltlb200_level_commit    ids from the global bitmap; own winners and the n_received records appended to the
+ *                           cache; outputs as ltlb200_expand_level (`seps`: every separating ordinal of the level,
+ *                           host array, exhaustive runs).
+ *
+ * A non-exhaustive level over a store that already holds a separating CM is refused (the reference's chunk
+ * truncation, engine.py:334-335, needs the whole set): build it with ltlb200_expand_level on every rank.
+ * ltlb200_expand_level on a sharded handle rebuilds the full set first, and vice versa.
  */
-int ltlb200_level_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, double deadline_s,
-                        int32_t shard_index, int32_t shard_count, uint64_t *n_claimed, uint64_t *sep_ord,
-                        uint64_t *n_seps);
-int ltlb200_level_end(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps,
-                      int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
-                      int64_t *constructed_delta);
-int ltlb200_claims_count(ltlb200_engine *e, int32_t owners, uint64_t *counts);
-int ltlb200_claims_pack(ltlb200_engine *e, int32_t owners, void *rows_dev, void *ords_dev);
-int ltlb200_claims_import(ltlb200_engine *e, const void *rows_dev, const void *ords_dev, uint64_t n);
-/* Copies the separating ordinals recorded by level_begin (exhaustive runs); returns how many. */
+int ltlb200_route_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, double deadline_s, int32_t rank,
+                        int32_t world, uint64_t *send_counts, uint64_t *send_offsets, void **rows_dev, void **ords_dev,
+                        uint64_t *sep_ord, uint64_t *n_seps);
+int ltlb200_exchange_recv(ltlb200_engine *e, uint64_t n_records, void **rows_dev, void **ords_dev);
+int ltlb200_owner_reduce(ltlb200_engine *e, uint64_t n_records, uint64_t *n_claimed, void **bitmap_dev, uint64_t *bitmap_words);
+int ltlb200_winners_export(ltlb200_engine *e, uint64_t sep_ord, uint64_t *n_winners, void **rows_dev, void **ords_dev);
+int ltlb200_level_commit(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, uint64_t n_received,
+                         int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
+                         int64_t *constructed_delta);
+/* Ends the pending routed level empty: another rank ran out of its time or memory budget (statuses 1 / 2 of
+ * ltlb200_route_begin / ltlb200_owner_reduce), and every rank stops or none does. */
+int ltlb200_level_abort(ltlb200_engine *e);
+/* Copies the separating ordinals recorded by ltlb200_route_begin (exhaustive runs); returns how many. */
 int64_t ltlb200_seps_copy(ltlb200_engine *e, uint64_t *out, uint64_t cap);
 /* Bytes of one CM row as stored on the device and in exchange records (16 * vectors). */
 int32_t ltlb200_key_bytes(const ltlb200_engine *e);
@@ -173,7 +192,7 @@ int ltlb200_level_candidates(ltlb200_engine *e, int32_t cost, uint32_t op_mask, 
 /*
  * 1 when some stored CM separates the examples (a level found a separator, or an exhaustive level recorded a
  * separating candidate).  A NON-exhaustive expand_level on such a store follows the reference's chunk truncation
- * (engine.py:334-335), which only ltlb200_expand_level reproduces: a sharded search builds such a level locally.
+ * (engine.py:334-335), which only ltlb200_expand_level reproduces: a sharded search builds such a level on every rank.
  */
 int32_t ltlb200_holds_separator(const ltlb200_engine *e);
 

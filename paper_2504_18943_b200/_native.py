@@ -17,7 +17,7 @@ LIB_PATH = pathlib.Path(os.environ.get("LTLB200_LIB") or pathlib.Path(__file__).
 
 OK, TIME_BUDGET, MEMORY_BUDGET = 0, 1, 2
 ERR_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED = -1, -2, -3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # every symbol include/ltlsynth_b200.h declares
 EXPORTED_SYMBOLS = (
@@ -29,11 +29,12 @@ EXPORTED_SYMBOLS = (
     "ltlb200_reset",
     "ltlb200_trim",
     "ltlb200_expand_level",
-    "ltlb200_level_begin",
-    "ltlb200_level_end",
-    "ltlb200_claims_count",
-    "ltlb200_claims_pack",
-    "ltlb200_claims_import",
+    "ltlb200_route_begin",
+    "ltlb200_exchange_recv",
+    "ltlb200_owner_reduce",
+    "ltlb200_winners_export",
+    "ltlb200_level_commit",
+    "ltlb200_level_abort",
     "ltlb200_seps_copy",
     "ltlb200_key_bytes",
     "ltlb200_now",
@@ -111,16 +112,19 @@ def load():
     L.ltlb200_expand_level.argtypes = [p, i32, u32, i32, i64, u64, dbl,
                                        ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     pu64 = ctypes.POINTER(u64)
-    L.ltlb200_level_begin.restype = ctypes.c_int
-    L.ltlb200_level_begin.argtypes = [p, i32, u32, i32, dbl, i32, i32, pu64, pu64, pu64]
-    L.ltlb200_level_end.restype = ctypes.c_int
-    L.ltlb200_level_end.argtypes = [p, u64, p, u64, i64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
-    L.ltlb200_claims_count.restype = ctypes.c_int
-    L.ltlb200_claims_count.argtypes = [p, i32, p]
-    L.ltlb200_claims_pack.restype = ctypes.c_int
-    L.ltlb200_claims_pack.argtypes = [p, i32, p, p]
-    L.ltlb200_claims_import.restype = ctypes.c_int
-    L.ltlb200_claims_import.argtypes = [p, p, p, u64]
+    pp = ctypes.POINTER(p)
+    L.ltlb200_route_begin.restype = ctypes.c_int
+    L.ltlb200_route_begin.argtypes = [p, i32, u32, i32, dbl, i32, i32, pu64, pu64, pp, pp, pu64, pu64]
+    L.ltlb200_exchange_recv.restype = ctypes.c_int
+    L.ltlb200_exchange_recv.argtypes = [p, u64, pp, pp]
+    L.ltlb200_owner_reduce.restype = ctypes.c_int
+    L.ltlb200_owner_reduce.argtypes = [p, u64, pu64, pp, pu64]
+    L.ltlb200_winners_export.restype = ctypes.c_int
+    L.ltlb200_winners_export.argtypes = [p, u64, pu64, pp, pp]
+    L.ltlb200_level_abort.restype = ctypes.c_int
+    L.ltlb200_level_abort.argtypes = [p]
+    L.ltlb200_level_commit.restype = ctypes.c_int
+    L.ltlb200_level_commit.argtypes = [p, u64, p, u64, u64, i64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.ltlb200_seps_copy.restype = i64
     L.ltlb200_seps_copy.argtypes = [p, p, u64]
     L.ltlb200_key_bytes.restype = i32

@@ -331,16 +331,22 @@ public:
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
     void reset();
-    int level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
-                    u64 *n_claimed, u64 *sep_ord, u64 *n_seps, bool defer = false);
+    int level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, u64 *n_claimed, u64 *sep_ord, u64 *n_seps,
+                    bool defer = false);
     int level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid,
                   int64_t *constructed_delta);
     int level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
     void launch_rank_scan(u64 n_words, u64 n_sb);
     static constexpr int kRetryLevel = 100;  // internal status: the deferred attempt overflowed, redo synchronously
-    void claims_count(int owners, u64 *counts);
-    void claims_pack(int owners, void *rows_dev, void *ords_dev);
-    void claims_import(const void *rows_dev, const void *ords_dev, u64 n);
+    // one search sharded over several GPUs: owner-sharded set, candidates routed to their hash owners
+    int route_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int rank, int world, u64 *send_counts,
+                    u64 *send_offsets, void **rows_dev, void **ords_dev, u64 *sep_ord, u64 *n_seps);
+    void exchange_recv(u64 n_records, void **rows_dev, void **ords_dev);
+    int owner_reduce(u64 n_records, u64 *n_claimed, void **bitmap_dev, u64 *bitmap_words);
+    void level_abort();
+    void winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void **ords_dev);
+    int level_commit(u64 sep_ord, const u64 *seps, u64 n_seps, u64 n_received, int64_t batch, u64 mem_budget, int64_t *n_new,
+                     int64_t *sep_gid, int64_t *constructed_delta);
     u64 seps_copy(u64 *out, u64 cap);
     int key_bytes() const { return 16 * nvec_; }
     int num_levels() const { return (int)levels_.size(); }
@@ -379,7 +385,15 @@ private:
     DeviceArray<uint32_t> scan_tmp_;
     DeviceArray<u64> sep_list_;
     DeviceArray<uint8_t> misc_;
-    DeviceArray<u64> xchg_;  // per-owner counts and cursors of the claim exchange
+    DeviceArray<u64> xchg_;  // per-owner record counts of the route phase; winners cursor
+    // sharded search: send side (route regions, then this owner's winners) and receive side (records from the
+    // other ranks, then their winners) of the two exchanges of a level
+    DeviceArray<uint4> xs_rows_, xr_rows_;
+    DeviceArray<u64> xs_ords_, xr_ords_;
+    int owner_world_ = 1, owner_rank_ = 0;  // the set holds the CMs whose hash owner is owner_rank_ (world 1: all)
+    void set_sharding(int world, int rank);
+    int finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new, int64_t *sep_gid,
+                       int64_t *constructed_delta, bool global_bitmap, u64 n_received);
     bool store_has_separator_ = false;  // some stored CM separates: a separating candidate need not be fresh
     // Associativity pruning (narrow.cuh: run_binary_tile) is sound while every stored level is complete and
     // all levels were built with one operator set; the first cut level or change of operators ends it.
@@ -399,9 +413,9 @@ private:
     struct PendingLevel {
         LevelMeta lv;
         u64 constructed = 0, n_claimed = 0, sep_ord = ~0ull, n_seps = 0, claim_cap = 0;
-        bool exhaustive = false, active = false, seps_overflow = false, imported = false, deferred = false;
+        bool exhaustive = false, active = false, seps_overflow = false, deferred = false, routed = false, reduced = false;
         int cost = 0;
-        std::vector<u64> owner_counts;
+        u64 n_received = 0, n_winners = 0, region_cap = 0;
     } pending_;
     WideParams wide_params(bool exhaustive) const;
     NarrowParams narrow_params(bool exhaustive) const;
@@ -643,6 +657,10 @@ Engine::~Engine() {
     release(sep_list_);
     release(misc_);
     release(xchg_);
+    release(xs_rows_);
+    release(xr_rows_);
+    release(xs_ords_);
+    release(xr_ords_);
     recycle_retired(true);
     pinned_put(h_counters_);
     g_phase.dump();
@@ -686,7 +704,7 @@ void Engine::rebuild_table(u64 slots) {
         CUDA_CHECK(cudaMemsetAsync(wslots_.ptr, 0, wslots_.cap * sizeof(u64), stream_));
         if (total_) {
             int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
-            wide_rebuild_kernel<<<grid, 256, 0, stream_>>>(wslots_.ptr, wslots_.cap - 1, store_.ptr, total_, nvec_, log2g_);
+            wide_rebuild_kernel<<<grid, 256, 0, stream_>>>(wslots_.ptr, wslots_.cap - 1, store_.ptr, total_, nvec_, log2g_, (uint32_t)owner_world_, (uint32_t)owner_rank_);
             CUDA_CHECK(cudaGetLastError());
             st_.kernel_launches++;
         }
@@ -701,7 +719,7 @@ void Engine::rebuild_table(u64 slots) {
         CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SPECIAL, &special, sizeof(u64), cudaMemcpyHostToDevice, stream_));
         if (total_) {
             int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
-            narrow_rebuild_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, store_.ptr, 0, total_, d_counters_);
+            narrow_rebuild_kernel<<<grid, 256, 0, stream_>>>(slots_.ptr, slots_.cap - 1, store_.ptr, 0, total_, d_counters_, (uint32_t)owner_world_, (uint32_t)owner_rank_);
             CUDA_CHECK(cudaGetLastError());
             st_.kernel_launches++;
         }
@@ -1052,7 +1070,8 @@ void Engine::launch_level(Params P, const LevelMeta &lv) {
     const BlockDesc &last = lv.blocks.back();
     const u64 level_candidates = last.ord0 + last.size;
     const bool guarded = P.scan_only || P.dead_n;
-    if (guarded || level_candidates <= kSmallLevel) {
+    const bool route = P.route_rows != nullptr;  // sharded search: one launch per operator, whatever the size
+    if (!route && (guarded || level_candidates <= kSmallLevel)) {
         P.block_begin = 0;
         P.block_end = (int)lv.blocks.size();
         P.tile_begin = 0;
@@ -1066,8 +1085,8 @@ void Engine::launch_level(Params P, const LevelMeta &lv) {
     fan_begin();
     for_each_operator(P, lv, sm_count_, occupancy_, [&](int op, const Params &Q, int grid, int group) {
         cudaStream_t st = fan_stream(group);
-        if constexpr (kWide) launch_wide(LK_OPERATOR, op, Q, grid, st);
-        else launch_narrow(LK_OPERATOR, op, Q, grid, st);
+        if constexpr (kWide) launch_wide(route ? LK_ROUTE : LK_OPERATOR, op, Q, grid, st);
+        else launch_narrow(route ? LK_ROUTE : LK_OPERATOR, op, Q, grid, st);
     });
     fan_end();
 }
@@ -1139,12 +1158,12 @@ void Engine::collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch
     dead_n_ = ranges.size() / 2;
 }
 
-int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int shard_index, int shard_count,
-                        u64 *n_claimed_out, u64 *sep_ord_out, u64 *n_seps_out, bool defer) {
+int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, u64 *n_claimed_out, u64 *sep_ord_out,
+                        u64 *n_seps_out, bool defer) {
     if (pending_.active) throw std::invalid_argument("level_begin: the previous level was not ended");
     if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
-    if (shard_count < 1 || shard_index < 0 || shard_index >= shard_count) throw std::invalid_argument("bad shard");
     CUDA_CHECK(cudaSetDevice(device_));
+    set_sharding(1, 0);  // a level built by one handle needs the whole set
     pending_ = PendingLevel{};
     PendingLevel &pl = pending_;
     pl.lv.base = total_;
@@ -1173,7 +1192,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
         st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
         dead_n_ = 0;
-        if (!exhaustive && store_has_separator_ && shard_count == 1 && mode_batch_ > 0) {
+        if (!exhaustive && store_has_separator_ && mode_batch_ > 0) {
             // The dead ranges delete candidates -- among them the smaller-ordinal witnesses x & (y & r) that the
             // associativity pruning of AND blocks relies on -- and leave this level incomplete: no pruning here
             // nor in any later level of this store.
@@ -1219,8 +1238,6 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
                 reserve(stage_slot_, claim_cap, false);
                 CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
                 WideParams P = wide_params(exhaustive);
-                P.shard_stride = (u64)shard_count;
-                P.shard_offset = (u64)shard_index;
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
                 launch_enumerate_wide(P, lv);
             } else {
@@ -1228,8 +1245,6 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
                 reserve(claim_ord_, claim_cap, false);
                 CUDA_CHECK(cudaMemsetAsync(claim_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
                 NarrowParams P = narrow_params(exhaustive);
-                P.shard_stride = (u64)shard_count;
-                P.shard_offset = (u64)shard_index;
                 PHASE(1, "begin: setup (copies, memsets)", tp);
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
                 launch_enumerate(P, lv);
@@ -1238,7 +1253,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             PHASE(2, "begin: launches", tp);
             if (defer) {
                 pl.deferred = true;
-                st_.enumerate_candidates += constructed / (u64)shard_count;
+                st_.enumerate_candidates += constructed;
                 return LTLB200_OK;
             }
             read_counters();
@@ -1246,7 +1261,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
             st_.enumerate_ms += ms;
-            st_.enumerate_candidates += constructed / (u64)shard_count;
+            st_.enumerate_candidates += constructed;
             if (exhaustive && h_counters_[CTR_OVERFLOW] == 0 && h_counters_[CTR_SEPCOUNT] > sep_list_.cap) {
                 // more separating candidates than the list holds: the chunk-exact separator needs all of them
                 sep_want_ = h_counters_[CTR_SEPCOUNT] + 1024;
@@ -1343,6 +1358,15 @@ WideParams Engine::wide_params(bool exhaustive) const {
 // runs; NULL = use what this handle recorded itself).
 int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new,
                       int64_t *sep_gid, int64_t *constructed_delta) {
+    if (pending_.routed) throw std::invalid_argument("level_end on a routed level (level_commit ends it)");
+    return finalize_level(sep_ord, seps, n_seps, batch, mem_budget, n_new, sep_gid, constructed_delta, false, 0);
+}
+
+// `global_bitmap`: the winners bitmap already holds the marks of every owner (sharded search: owner_reduce marked,
+// the ranks all-reduced); this owner's claims are placed as usual and `n_received` records published by the other
+// owners (exchange_recv buffers) are placed by the rank of their ordinals.
+int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u64 mem_budget, int64_t *n_new,
+                           int64_t *sep_gid, int64_t *constructed_delta, bool global_bitmap, u64 n_received) {
     if (!pending_.active) throw std::invalid_argument("level_end without level_begin");
     if (batch < 1) throw std::invalid_argument("batch_size must be >= 1");
     if (sep_ord != VAL_EMPTY || n_seps) store_has_separator_ = true;  // found by another shard
@@ -1362,22 +1386,16 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
     double tp = monotonic_s();
     if (pl.deferred) return level_end_deferred(batch, mem_budget, n_new, sep_gid, constructed_delta);
     try {
-        if (pl.imported) {  // claims grew through claims_import: read the counters again
-            CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-            CUDA_CHECK(cudaStreamSynchronize(stream_));
-        }
-        PHASE(4, "end: re-read counters", tp);
-        if (h_counters_[CTR_OVERFLOW]) throw CudaError("hash set overflow while importing claims");
-        const u64 n_claimed = h_counters_[CTR_CLAIMED];
+        const u64 n_claimed = std::min(h_counters_[CTR_CLAIMED], pl.claim_cap);
         const bool cut = !exhaustive && sep_ord != VAL_EMPTY;
         const u64 n_bits = cut ? sep_ord + 1 : constructed;
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
         reserve(bitmap_, n_words + 1, false);
         reserve(sb_rank_, n_sb + 1, false);
-        reserve(store_, (total_ + n_claimed) * nvec_, true, total_ * nvec_);
-        reserve(ords_, total_ + n_claimed, true, total_);
+        reserve(store_, (total_ + n_claimed + n_received) * nvec_, true, total_ * nvec_);
+        reserve(ords_, total_ + n_claimed + n_received, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
-        CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+        if (!global_bitmap) CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
         CUDA_CHECK(cudaMemcpyAsync(d_counters_ + CTR_SEP, &sep_ord, sizeof(u64), cudaMemcpyHostToDevice, stream_));
         const u64 ord_limit = cut ? sep_ord : VAL_EMPTY - 1;
         FinalizeParams F{};
@@ -1398,7 +1416,7 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
             W.ords = ords_.ptr;
             W.base = total_;
             W.nvec = nvec_;
-            wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
+            if (!global_bitmap) wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
         } else {
             F.claim_key = claim_key_.ptr;
             F.claim_ord = claim_ord_.ptr;
@@ -1409,7 +1427,7 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
             F.store = store_.ptr;
             F.ords = ords_.ptr;
             F.base = total_;
-            narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+            if (!global_bitmap) narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
         }
         CUDA_CHECK(cudaGetLastError());
         launch_rank_scan(n_words, n_sb);
@@ -1437,6 +1455,14 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
             narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
         }
         CUDA_CHECK(cudaGetLastError());
+        if (n_received) {  // what the other owners published
+            const u64 work = n_received * (u64)(wide_ ? nvec_ : 1);
+            const int rgrid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
+            if (wide_) wide_scatter_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, nvec_, bitmap_.ptr, sb_rank_.ptr, store_.ptr, ords_.ptr, total_);
+            else narrow_scatter_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, bitmap_.ptr, sb_rank_.ptr, store_.ptr, ords_.ptr, total_);
+            CUDA_CHECK(cudaGetLastError());
+            st_.kernel_launches++;
+        }
         CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
         st_.kernel_launches += 3;
         PHASE(5, "end: reserve + launches", tp);
@@ -1447,6 +1473,9 @@ int Engine::level_end(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t batch, u
         st_.finalize_ms += fms;
         recycle_retired(false);  // the stream has drained: blocks retired by regrows can be reused
         lv.n = h_counters_[CTR_WINNERS];
+        if (global_bitmap && lv.n != pl.n_winners + n_received)
+            throw CudaError("sharded level: the winners bitmap holds " + std::to_string(lv.n) + " entries, the owners published " +
+                            std::to_string(pl.n_winners + n_received));
         sep_ord = h_counters_[CTR_SEP];
         if (sep_ord != VAL_EMPTY) *sep_gid = (int64_t)(total_ + h_counters_[CTR_SEPRANK]);
         if (cut) table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
@@ -1667,7 +1696,7 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     u64 n_claimed = 0, sep_ord = VAL_EMPTY, n_seps = 0;
     static const bool defer = getenv("LTLB200_NO_DEFER") == nullptr;
     mode_batch_ = batch;  // (collect_dead_ranges needs the reference's chunk schedule)
-    int rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps, defer);
+    int rc = level_begin(cost, op_mask, exhaustive, deadline, &n_claimed, &sep_ord, &n_seps, defer);
     if (rc != LTLB200_OK) {
         mode_batch_ = 0;
         return rc;
@@ -1676,76 +1705,331 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     rc = level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
     if (rc != kRetryLevel) return rc;
     mode_batch_ = batch;
-    rc = level_begin(cost, op_mask, exhaustive, deadline, 0, 1, &n_claimed, &sep_ord, &n_seps, false);
+    rc = level_begin(cost, op_mask, exhaustive, deadline, &n_claimed, &sep_ord, &n_seps, false);
     mode_batch_ = 0;
     if (rc != LTLB200_OK) return rc;
     return level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
 }
 
-// ---- claim exchange (one search over several GPUs) --------------------------------------------
+// ---- one search sharded over several GPUs ----------------------------------------------------------------------
+//
+// The language cache (rows + winning ordinals of every finished level) is replicated: any rank reads any operand.
+// The dedup set is OWNER-SHARDED: rank r holds the CMs with hash owner r, of every level, so the set of an N-GPU
+// search has N times the capacity and every rank probes 1/N of the candidates.  One level =
+//
+//   route_begin    build this rank's tile-strided share of the pair space; every candidate that is not a duplicate
+//                  by construction goes, as a record {CM, ordinal}, to the send region of its owner (phase A)
+//   [all-to-all]   the caller moves the regions (exchange_recv hands out the receive buffers)
+//   owner_reduce   insert-or-min of the received records into the owned part of the set (phase B); marks the
+//                  ordinals of this owner's winners in the level's bitmap
+//   [all-reduce]   the caller sums the bitmaps (disjoint bits: a sum is the union); min of the separator
+//   winners_export this owner's winners up to the separator as dense records
+//   [all-gather]   every rank receives the winners of the others (exchange_recv again)
+//   level_commit   ranks of the global bitmap -> ids; own winners and received records appended to the cache
+//
+// Per rank: C/N candidates built, (K+8)C/N bytes out and in, C/N random probes, and the u*C new rows every replica
+// of the cache has to store anyway.
 
-// counts[o] = number of this level's local claims whose hash owner is rank o
-void Engine::claims_count(int owners, u64 *counts) {
-    if (!pending_.active) throw std::invalid_argument("claims_count outside a level");
+void Engine::set_sharding(int world, int rank) {
+    if (world == owner_world_ && rank == owner_rank_) return;
+    owner_world_ = world;
+    owner_rank_ = rank;
+    table_dirty_ = true;  // the set is rebuilt with the CMs this rank owns now
+}
+
+int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double deadline, int rank, int world, u64 *send_counts,
+                        u64 *send_offsets, void **rows_dev, void **ords_dev, u64 *sep_ord_out, u64 *n_seps_out) {
+    if (pending_.active) throw std::invalid_argument("route_begin: the previous level was not ended");
+    if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
+    if (world < 1 || world > ROUTE_MAX_WORLD || rank < 0 || rank >= world) throw std::invalid_argument("bad shard (at most 8 ranks)");
     CUDA_CHECK(cudaSetDevice(device_));
-    reserve(xchg_, (u64)owners * 2, false);
-    CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, (u64)owners * 2 * sizeof(u64), stream_));
-    CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));
-    const u64 n = std::min(h_counters_[CTR_CLAIMED], pending_.claim_cap);
-    pending_.n_claimed = n;
-    if (n) {
-        const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
-        if (wide_) wide_export_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
-        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, (uint32_t)owners, xchg_.ptr, nullptr, nullptr, nullptr);
+    set_sharding(world, rank);
+    pending_ = PendingLevel{};
+    PendingLevel &pl = pending_;
+    pl.lv.base = total_;
+    pl.exhaustive = exhaustive;
+    pl.cost = cost;
+    pl.routed = true;
+    for (int o = 0; o < world; ++o) send_counts[o] = send_offsets[o] = 0;
+    *rows_dev = *ords_dev = nullptr;
+    *sep_ord_out = VAL_EMPTY;
+    *n_seps_out = 0;
+    if (deadline >= 0 && monotonic_s() > deadline) {  // engine.py:416-417, before the first chunk
+        prune_ok_ = false;
+        levels_.push_back(pl.lv);
+        return LTLB200_TIME_BUDGET;
+    }
+    if (!exhaustive && store_has_separator_)
+        throw std::invalid_argument("a non-exhaustive level over a store that holds a separating CM follows the reference's chunk "
+                                    "truncation: build it with ltlb200_expand_level on every rank");
+    if (prune_mask_ == 0) prune_mask_ = op_mask;
+    else if (prune_mask_ != op_mask) prune_ok_ = false;
+    u64 n_tiles = 0;
+    plan_level(cost, op_mask, pl.lv, pl.constructed, n_tiles);
+    pl.active = true;
+    if (pl.constructed == 0) return LTLB200_OK;
+    const LevelMeta &lv = pl.lv;
+    const u64 constructed = pl.constructed;
+    std::vector<u64> counts((size_t)world, 0);
+    try {
+        if (table_dirty_) rebuild_table(table_slots());
+        CUDA_CHECK(cudaMemcpyAsync(d_blocks_, lv.blocks.data(), lv.blocks.size() * sizeof(BlockDesc), cudaMemcpyHostToDevice, stream_));
+        st_.h2d_bytes += lv.blocks.size() * sizeof(BlockDesc);
+        dead_n_ = 0;
+        reserve(xchg_, 16, false);
+        // a rank builds ~1/world of the candidates and a uniform hash sends ~1/world of those to each owner; a
+        // region that overflows is only counted, and the level is routed again with the exact sizes
+        u64 cap = (u64)((double)(constructed / (u64)world + 1) / (double)world * 1.25) + (1ull << 16);
+        cap = std::min(cap, constructed + 64);
+        for (int attempt = 0;; ++attempt) {
+            if (exhaustive) reserve(sep_list_, std::max<u64>(std::max<u64>(1ull << 20, constructed / 16), sep_want_), false);
+            reserve(xs_rows_, (u64)world * cap * nvec_, false);
+            reserve(xs_ords_, (u64)world * cap, false);
+            level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+            CUDA_CHECK(cudaGetLastError());
+            CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, 16 * sizeof(u64), stream_));
+            pl.claim_cap = 0;
+            CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+            if (wide_) {
+                WideParams P = wide_params(exhaustive);
+                P.shard_stride = (u64)world;
+                P.shard_offset = (u64)rank;
+                P.route_rows = xs_rows_.ptr;
+                P.route_ords = xs_ords_.ptr;
+                P.route_cap = cap;
+                P.route_counts = xchg_.ptr;
+                P.route_world = (uint32_t)world;
+                P.route_sep_any = store_has_separator_ ? 0 : 1;
+                launch_enumerate_wide(P, lv);
+            } else {
+                NarrowParams P = narrow_params(exhaustive);
+                P.shard_stride = (u64)world;
+                P.shard_offset = (u64)rank;
+                P.route_rows = xs_rows_.ptr;
+                P.route_ords = xs_ords_.ptr;
+                P.route_cap = cap;
+                P.route_counts = xchg_.ptr;
+                P.route_world = (uint32_t)world;
+                P.route_sep_any = store_has_separator_ ? 0 : 1;
+                launch_enumerate(P, lv);
+            }
+            CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+            CUDA_CHECK(cudaMemcpyAsync(h_counters_ + CTR_COUNT, xchg_.ptr, (u64)world * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+            read_counters();
+            st_.d2h_bytes += (u64)world * sizeof(u64);
+            float ms = 0;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+            st_.enumerate_ms += ms;
+            st_.enumerate_candidates += constructed / (u64)world;
+            u64 need = 0;
+            for (int o = 0; o < world; ++o) {
+                counts[o] = h_counters_[CTR_COUNT + o];
+                need = std::max(need, counts[o]);
+            }
+            if (attempt > 4) throw CudaError("route regions keep overflowing");
+            if (need > cap) {
+                cap = need + 1024;
+                continue;
+            }
+            if (exhaustive && h_counters_[CTR_SEPCOUNT] > sep_list_.cap) {
+                sep_want_ = h_counters_[CTR_SEPCOUNT] + 1024;
+                continue;
+            }
+            break;
+        }
+        pl.region_cap = cap;
+    } catch (const MemoryBudget &e) {
+        g_last_error = e.what();
+        pl.active = false;
+        prune_ok_ = false;
+        levels_.push_back(LevelMeta{0, total_, {}});
+        return LTLB200_MEMORY_BUDGET;
+    }
+    pl.sep_ord = h_counters_[CTR_SEP];
+    pl.n_seps = h_counters_[CTR_SEPCOUNT];
+    for (int o = 0; o < world; ++o) {
+        send_counts[o] = counts[o];
+        send_offsets[o] = (u64)o * pl.region_cap;
+    }
+    *rows_dev = xs_rows_.ptr;
+    *ords_dev = xs_ords_.ptr;
+    *sep_ord_out = pl.sep_ord;
+    *n_seps_out = pl.n_seps;
+    return LTLB200_OK;
+}
+
+// receive buffers of the next exchange (records of the route phase, then the winners of the other owners)
+void Engine::exchange_recv(u64 n_records, void **rows_dev, void **ords_dev) {
+    if (!pending_.active || !pending_.routed) throw std::invalid_argument("exchange_recv outside a routed level");
+    CUDA_CHECK(cudaSetDevice(device_));
+    reserve(xr_rows_, std::max<u64>(n_records, 1) * nvec_, false);
+    reserve(xr_ords_, std::max<u64>(n_records, 1), false);
+    *rows_dev = xr_rows_.ptr;
+    *ords_dev = xr_ords_.ptr;
+}
+
+// Phase B: the first `n_records` records of the receive buffers are folded into the owned part of the set; then
+// the ordinals of this owner's winners are marked in the level's bitmap (one bit per candidate of the WHOLE level,
+// so that the bitmaps of all owners add up to the level's winners).
+int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u64 *bitmap_words) {
+    PendingLevel &pl = pending_;
+    if (!pl.active || !pl.routed) throw std::invalid_argument("owner_reduce outside a routed level");
+    CUDA_CHECK(cudaSetDevice(device_));
+    *n_claimed_out = 0;
+    *bitmap_dev = nullptr;
+    *bitmap_words = 0;
+    try {
+    const u64 constructed = pl.constructed;
+    const u64 n_words = (constructed + 31) / 32, n_sb = (n_words + 31) / 32;
+    pl.n_received = n_records;
+    const u64 kExact = 1ull << 22, kSlack = 1ull << 21;
+    u64 est = n_records;
+    if (n_records > kExact) {
+        double u = 1.0;
+        if (levels_.size() >= 2 && last_constructed_ > 0) u = std::min(1.0, 1.5 * (double)levels_.back().n / (double)last_constructed_ + 0.02);
+        est = std::min(n_records, std::max(kExact, (u64)(u * (double)n_records)));
+    }
+    const u64 owned = total_ / (u64)owner_world_ + total_ / (u64)(8 * owner_world_) + 1024;  // this rank's share of the stored CMs
+    for (int attempt = 0;; ++attempt) {
+        const u64 slack = wide_ ? (u64)sm_count_ * 8 * (u64)(CTA_THREADS >> log2g_) * WIDE_CHUNK + 1024
+                                : (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 2 + 1024;
+        const u64 claim_cap = est + slack;
+        const u64 want_slots = next_pow2(2 * (owned + est));
+        if (want_slots > table_slots()) rebuild_table(grown_size(want_slots));
+        else if (table_dirty_) rebuild_table(table_slots());
+        level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+        CUDA_CHECK(cudaGetLastError());
+        pl.claim_cap = claim_cap;
+        CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+        if (wide_) {
+            reserve(stage_rows_, claim_cap * nvec_, false);
+            reserve(stage_ord_, claim_cap, false);
+            reserve(stage_slot_, claim_cap, false);
+            CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+            if (n_records) {
+                WideParams P = wide_params(pl.exhaustive);
+                P.sep_list = nullptr;
+                P.sep_list_cap = 0;
+                const u64 groups = (u64)(CTA_THREADS >> log2g_);
+                const int grid = (int)std::max<u64>(1, std::min<u64>((n_records + groups - 1) / groups, (u64)sm_count_ * 8));
+                wide_import_kernel<<<grid, CTA_THREADS, 0, stream_>>>(P, xr_rows_.ptr, xr_ords_.ptr, n_records);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches++;
+            }
+        } else {
+            reserve(claim_key_, claim_cap, false);
+            reserve(claim_ord_, claim_cap, false);
+            CUDA_CHECK(cudaMemsetAsync(claim_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+            if (n_records) {
+                NarrowParams P = narrow_params(pl.exhaustive);
+                P.sep_list = nullptr;  // separating candidates were recorded where they were built
+                P.sep_list_cap = 0;
+                P.prune_after_sep = 0;
+                const u64 steps = (n_records + 32 * PROBE_BATCH - 1) / (32 * PROBE_BATCH);
+                const int grid = (int)std::max<u64>(1, std::min<u64>((steps + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * occupancy_));
+                switch (lw_) {
+                    case 8: narrow_probe_8(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
+                    case 16: narrow_probe_16(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
+                    case 32: narrow_probe_32(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
+                    default: narrow_probe_64(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
+                }
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches++;
+            }
+        }
+        CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+        read_counters();
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+        st_.enumerate_ms += ms;
+        if (h_counters_[CTR_OVERFLOW] == 0) break;
+        // the records are still in the receive buffers: regrow locally and fold them in again, no new exchange
+        if (attempt > 8 || est >= n_records) throw CudaError("hash set overflow while folding in received records");
+        est = std::min(n_records, est * 4);
+        rebuild_table(next_pow2(2 * (owned + est + kSlack)));
+    }
+    const u64 n_claimed = std::min(h_counters_[CTR_CLAIMED], pl.claim_cap);
+    pl.n_claimed = n_claimed;
+    pl.reduced = true;
+    reserve(bitmap_, n_words + 1, false);
+    reserve(sb_rank_, n_sb + 1, false);
+    CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+    if (n_claimed) {
+        const int fgrid = (int)std::max<u64>(1, std::min<u64>((n_claimed + 255) / 256, (u64)sm_count_ * 16));
+        if (wide_) {
+            WideFinalize W{};
+            W.stage_ord = stage_ord_.ptr;
+            W.n_staged = n_claimed;
+            W.bitmap = bitmap_.ptr;
+            W.ord_limit = VAL_EMPTY - 1;
+            wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
+        } else {
+            FinalizeParams F{};
+            F.claim_ord = claim_ord_.ptr;
+            F.n_claimed = n_claimed;
+            F.bitmap = bitmap_.ptr;
+            F.ord_limit = VAL_EMPTY - 1;
+            narrow_mark_kernel<<<fgrid, 256, 0, stream_>>>(F);
+        }
         CUDA_CHECK(cudaGetLastError());
         st_.kernel_launches++;
     }
-    CUDA_CHECK(cudaMemcpyAsync(counts, xchg_.ptr, (u64)owners * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
-    CUDA_CHECK(cudaStreamSynchronize(stream_));
-    pending_.owner_counts.assign(counts, counts + owners);
+    CUDA_CHECK(cudaStreamSynchronize(stream_));  // the caller's collective may run on another stream
+    *n_claimed_out = n_claimed;
+    *bitmap_dev = bitmap_.ptr;
+    *bitmap_words = n_words + 1;
+    } catch (const MemoryBudget &e) {  // the device is full: the level ends empty here; the caller tells the other ranks
+        g_last_error = e.what();
+        level_abort();
+        return LTLB200_MEMORY_BUDGET;
+    }
+    return LTLB200_OK;
 }
 
-// writes the local claims grouped by owner (owner 0 first) to device buffers sized by claims_count
-void Engine::claims_pack(int owners, void *rows_dev, void *ords_dev) {
-    if (!pending_.active || (int)pending_.owner_counts.size() != owners) throw std::invalid_argument("claims_pack needs claims_count first");
+// Ends the pending level empty (another rank ran out of budget; every rank stops or none does).
+void Engine::level_abort() {
+    if (!pending_.active) return;
+    pending_.active = false;
+    table_dirty_ = true;
+    prune_ok_ = false;
+    levels_.push_back(LevelMeta{0, total_, {}});
+}
+
+// this owner's winners with an ordinal <= the level's separator (all of them in an exhaustive run), dense
+void Engine::winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void **ords_dev) {
+    PendingLevel &pl = pending_;
+    if (!pl.active || !pl.reduced) throw std::invalid_argument("winners_export needs owner_reduce first");
     CUDA_CHECK(cudaSetDevice(device_));
-    std::vector<u64> cursors((size_t)owners);
-    u64 acc = 0;
-    for (int o = 0; o < owners; ++o) {
-        cursors[o] = acc;
-        acc += pending_.owner_counts[o];
-    }
-    CUDA_CHECK(cudaMemcpyAsync(xchg_.ptr + owners, cursors.data(), (u64)owners * sizeof(u64), cudaMemcpyHostToDevice, stream_));
-    const u64 n = pending_.n_claimed;
+    const bool cut = !pl.exhaustive && sep_ord != VAL_EMPTY;
+    const u64 limit = cut ? sep_ord : VAL_EMPTY - 1;
+    const u64 n = pl.n_claimed;
+    reserve(xs_rows_, std::max<u64>(n, 1) * nvec_, false);
+    reserve(xs_ords_, std::max<u64>(n, 1), false);
+    CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, sizeof(u64), stream_));
     if (n) {
         const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
-        if (wide_) wide_export_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
-        else narrow_export_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, (uint32_t)owners, nullptr, xchg_.ptr + owners, (uint4 *)rows_dev, (u64 *)ords_dev);
+        if (wide_) wide_winners_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
+        else narrow_winners_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
         CUDA_CHECK(cudaGetLastError());
         st_.kernel_launches++;
     }
-    CUDA_CHECK(cudaStreamSynchronize(stream_));  // `cursors` leaves scope; the caller hands the buffers to NCCL next
+    u64 count = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&count, xchg_.ptr, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += sizeof(u64);
+    pl.n_winners = count;
+    *n_winners = count;
+    *rows_dev = xs_rows_.ptr;
+    *ords_dev = xs_ords_.ptr;
 }
 
-// insert-or-min `n` records (device buffers) into the local set
-void Engine::claims_import(const void *rows_dev, const void *ords_dev, u64 n) {
-    if (!pending_.active) throw std::invalid_argument("claims_import outside a level");
-    if (!n) return;
-    CUDA_CHECK(cudaSetDevice(device_));
-    pending_.imported = true;
-    if (wide_) {
-        WideParams P = wide_params(pending_.exhaustive);
-        P.sep_list = nullptr;
-        const u64 groups = (u64)(CTA_THREADS >> log2g_);
-        const int grid = (int)std::max<u64>(1, std::min<u64>((n + groups - 1) / groups, (u64)sm_count_ * 8));
-        wide_import_kernel<<<grid, CTA_THREADS, 0, stream_>>>(P, (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
-    } else {
-        const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
-        narrow_import_kernel<<<grid, 256, 0, stream_>>>(narrow_params(pending_.exhaustive), (const uint4 *)rows_dev, (const u64 *)ords_dev, n);
-    }
-    CUDA_CHECK(cudaGetLastError());
-    st_.kernel_launches++;
+int Engine::level_commit(u64 sep_ord, const u64 *seps, u64 n_seps, u64 n_received, int64_t batch, u64 mem_budget, int64_t *n_new,
+                         int64_t *sep_gid, int64_t *constructed_delta) {
+    PendingLevel &pl = pending_;
+    if (!pl.active || !pl.routed) throw std::invalid_argument("level_commit outside a routed level");
+    if (pl.constructed && !pl.reduced) throw std::invalid_argument("level_commit needs owner_reduce and winners_export first");
+    // (counters as owner_reduce left them: CTR_CLAIMED = this owner's claims)
+    return finalize_level(sep_ord, seps, n_seps, batch, mem_budget, n_new, sep_gid, constructed_delta, true, n_received);
 }
 
 // every separating ordinal this handle recorded in the pending level (exhaustive runs)
@@ -1920,49 +2204,64 @@ int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int3
     });
 }
 
-int ltlb200_level_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, double deadline_s,
-                        int32_t shard_index, int32_t shard_count, uint64_t *n_claimed, uint64_t *sep_ord, uint64_t *n_seps) {
-    if (!e || !n_claimed || !sep_ord || !n_seps) return LTLB200_ERR_ARGUMENT;
+int ltlb200_route_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32_t exhaustive, double deadline_s, int32_t rank,
+                        int32_t world, uint64_t *send_counts, uint64_t *send_offsets, void **rows_dev, void **ords_dev,
+                        uint64_t *sep_ord, uint64_t *n_seps) {
+    if (!e || !send_counts || !send_offsets || !rows_dev || !ords_dev || !sep_ord || !n_seps) return LTLB200_ERR_ARGUMENT;
     return guarded([&] {
-        ltlb200::u64 a = 0, b = 0, c = 0;
-        int rc = e->impl->level_begin(cost, op_mask, exhaustive != 0, deadline_s, shard_index, shard_count, &a, &b, &c);
-        *n_claimed = a;
-        *sep_ord = b;
-        *n_seps = c;
+        ltlb200::u64 sep = 0, ns = 0;
+        int rc = e->impl->route_begin(cost, op_mask, exhaustive != 0, deadline_s, rank, world, (ltlb200::u64 *)send_counts,
+                                      (ltlb200::u64 *)send_offsets, rows_dev, ords_dev, &sep, &ns);
+        *sep_ord = sep;
+        *n_seps = ns;
         return rc;
     });
 }
 
-int ltlb200_level_end(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, int64_t batch_size,
-                      uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
-    if (!e || !n_new || !sep_gid || !constructed_delta) return LTLB200_ERR_ARGUMENT;
+int ltlb200_exchange_recv(ltlb200_engine *e, uint64_t n_records, void **rows_dev, void **ords_dev) {
+    if (!e || !rows_dev || !ords_dev) return LTLB200_ERR_ARGUMENT;
     return guarded([&] {
-        return e->impl->level_end(sep_ord, (const ltlb200::u64 *)seps, n_seps, batch_size, memory_budget_bytes, n_new, sep_gid,
-                                  constructed_delta);
-    });
-}
-
-int ltlb200_claims_count(ltlb200_engine *e, int32_t owners, uint64_t *counts) {
-    if (!e || !counts || owners < 1) return LTLB200_ERR_ARGUMENT;
-    return guarded([&] {
-        e->impl->claims_count(owners, (ltlb200::u64 *)counts);
+        e->impl->exchange_recv(n_records, rows_dev, ords_dev);
         return LTLB200_OK;
     });
 }
 
-int ltlb200_claims_pack(ltlb200_engine *e, int32_t owners, void *rows_dev, void *ords_dev) {
-    if (!e || owners < 1) return LTLB200_ERR_ARGUMENT;
+int ltlb200_owner_reduce(ltlb200_engine *e, uint64_t n_records, uint64_t *n_claimed, void **bitmap_dev, uint64_t *bitmap_words) {
+    if (!e || !n_claimed || !bitmap_dev || !bitmap_words) return LTLB200_ERR_ARGUMENT;
     return guarded([&] {
-        e->impl->claims_pack(owners, rows_dev, ords_dev);
-        return LTLB200_OK;
+        ltlb200::u64 nc = 0, words = 0;
+        const int rc = e->impl->owner_reduce(n_records, &nc, bitmap_dev, &words);
+        *n_claimed = nc;
+        *bitmap_words = words;
+        return rc;
     });
 }
 
-int ltlb200_claims_import(ltlb200_engine *e, const void *rows_dev, const void *ords_dev, uint64_t n) {
+int ltlb200_level_abort(ltlb200_engine *e) {
     if (!e) return LTLB200_ERR_ARGUMENT;
     return guarded([&] {
-        e->impl->claims_import(rows_dev, ords_dev, n);
+        e->impl->level_abort();
         return LTLB200_OK;
+    });
+}
+
+int ltlb200_winners_export(ltlb200_engine *e, uint64_t sep_ord, uint64_t *n_winners, void **rows_dev, void **ords_dev) {
+    if (!e || !n_winners || !rows_dev || !ords_dev) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        ltlb200::u64 n = 0;
+        e->impl->winners_export(sep_ord, &n, rows_dev, ords_dev);
+        *n_winners = n;
+        return LTLB200_OK;
+    });
+}
+
+int ltlb200_level_commit(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, uint64_t n_received,
+                         int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
+                         int64_t *constructed_delta) {
+    if (!e || !n_new || !sep_gid || !constructed_delta) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        return e->impl->level_commit(sep_ord, (const ltlb200::u64 *)seps, n_seps, n_received, batch_size, memory_budget_bytes,
+                                     n_new, sep_gid, constructed_delta);
     });
 }
 

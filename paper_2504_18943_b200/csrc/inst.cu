@@ -34,6 +34,18 @@ void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const Narrow
         narrow_guarded_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
         return;
     }
+    if (kind == LK_ROUTE) {
+        switch (op) {
+            case OP_ATOM: narrow_route_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_NOT: narrow_route_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_NEXT: narrow_route_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_FUTURE: narrow_route_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_AND: narrow_route_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_UNTIL: narrow_route_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            default: narrow_route_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        }
+        return;
+    }
     switch (op) {
         case OP_ATOM: narrow_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
         case OP_NOT: narrow_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
@@ -43,6 +55,11 @@ void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const Narrow
         case OP_UNTIL: narrow_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
         default: narrow_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
     }
+}
+
+void LTLB200_CAT(narrow_probe_, LTLB200_INST_LW)(const NarrowParams &P, const void *rows, const void *ords, unsigned long long n,
+                                                 int grid, cudaStream_t st) {
+    narrow_probe_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P, (const uint4 *)rows, (const u64 *)ords, n);
 }
 
 int LTLB200_CAT(narrow_occupancy_, LTLB200_INST_LW)() {
@@ -77,6 +94,14 @@ static void launch_operator(const WideParams &P, int grid, size_t smem, int devi
     wide2_level_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
 }
 
+template <int OP>
+static void launch_route(const WideParams &P, int grid, size_t smem, int device, cudaStream_t st) {
+    static unsigned long long seen = 0;
+    static std::mutex mu;
+    opt_in(wide2_route_kernel<LW, OP>, device, seen, mu);
+    wide2_route_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
+}
+
 void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WideParams &P, int grid, size_t smem, int device,
                                                  cudaStream_t st) {
     if (kind == LK_SMALL) {
@@ -91,6 +116,18 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
         static std::mutex mu;
         opt_in(wide2_guarded_level_kernel<LW>, device, seen, mu);
         wide2_guarded_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
+        return;
+    }
+    if (kind == LK_ROUTE) {
+        switch (op) {
+            case OP_ATOM: launch_route<OP_ATOM>(P, grid, smem, device, st); break;
+            case OP_NOT: launch_route<OP_NOT>(P, grid, smem, device, st); break;
+            case OP_NEXT: launch_route<OP_NEXT>(P, grid, smem, device, st); break;
+            case OP_FUTURE: launch_route<OP_FUTURE>(P, grid, smem, device, st); break;
+            case OP_AND: launch_route<OP_AND>(P, grid, smem, device, st); break;
+            case OP_UNTIL: launch_route<OP_UNTIL>(P, grid, smem, device, st); break;
+            default: launch_route<OP_OR>(P, grid, smem, device, st); break;
+        }
         return;
     }
     switch (op) {

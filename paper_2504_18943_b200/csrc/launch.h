@@ -15,12 +15,15 @@ struct NarrowParams;
 struct WideParams;
 
 // which kernel of a (lane width) set: one launch per operator (big levels), one launch for every
-// operator (levels up to kSmallLevel candidates), the guarded kernel (scan pass / dead ranges)
-enum : int { LK_OPERATOR = 0, LK_SMALL = 1, LK_GUARDED = 2 };
+// operator (levels up to kSmallLevel candidates), the guarded kernel (scan pass / dead ranges), and -- one search
+// sharded over several GPUs -- the kernel that routes candidates to their hash owners instead of probing them
+enum : int { LK_OPERATOR = 0, LK_SMALL = 1, LK_GUARDED = 2, LK_ROUTE = 3 };
 
 #define LTLB200_DECLARE_LW(LW)                                                                                     \
     void narrow_launch_##LW(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st);                    \
     int narrow_occupancy_##LW();                                                                                    \
+    void narrow_probe_##LW(const NarrowParams &P, const void *rows, const void *ords, unsigned long long n, int grid, \
+                           cudaStream_t st);                                                                         \
     void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \
     int wide2_occupancy_##LW(int nvec, int device);
 

@@ -112,6 +112,14 @@ struct NarrowParams {
     const u64 *dead;
     uint32_t dead_n;
     int scan_only;  // the pass that finds those chunks: only record the ordinal of every separating candidate
+    // One search sharded over several GPUs (narrow_route_kernel): candidates are not probed here but appended as
+    // records {CM, ordinal} to the region of their hash owner, route_world regions of route_cap records each.
+    uint4 *route_rows;
+    u64 *route_ords;
+    u64 route_cap;
+    u64 *route_counts;     // records appended per owner; keeps counting past route_cap (the exact need of a redo)
+    uint32_t route_world;
+    int route_sep_any;     // the store holds no separating CM: every separating candidate is fresh w.r.t. earlier levels
 };
 
 // [1] claim indices reserved, [2] separator ordinal (min), [3] special-key val (persists across levels),
@@ -152,6 +160,11 @@ __device__ __forceinline__ void ld_slot(const Slot16 *p, uint4 &key, u64 &val) {
     (void)pad0;
     (void)pad1;
     val = (u64)v1 << 32 | v0;
+}
+
+// hash owner of a CM in a sharded search: independent of the slot hash
+__device__ __forceinline__ uint32_t key_owner(uint4 key, uint32_t owners) {
+    return hash_vec(key, 0x5BD1E995u) % owners;
 }
 
 // ---- per-warp state -------------------------------------------------------------------
@@ -727,6 +740,144 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) narrow_guarded_level_kernel(co
             default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
         }
         if (stop) break;
+    }
+    if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+        while (st.qfill > 0u) drain_round(P, ws.queue, st);
+}
+
+// ---- one search sharded over several GPUs: route instead of probe ----------------------------------------------
+// The hash set of a sharded search is OWNER-SHARDED: rank r holds exactly the CMs with key_owner(CM) == r, of
+// every level.  A rank therefore cannot decide locally whether a candidate is new; it builds its share of the
+// level's pair space and appends every candidate that is not a duplicate by construction as a record
+// {CM, ordinal} to the send region of the CM's owner (phase A, narrow_route_kernel).  After the all-to-all the
+// owner folds what it received into its part of the set (phase B, narrow_probe_kernel = insert_batch over
+// records).  Per rank and level that is C/N candidates built, (K+8)*C/N bytes streamed out and in, and C/N
+// random probes into a set of 1/N of the keys: every term shrinks with the number of GPUs.
+//
+// Records are staged per owner in the warp's shared memory and flushed 32 at a time (one atomicAdd per 32 records
+// and owner; 512 + 256 contiguous bytes per flush), so the regions are dense: no holes, exact send sizes.
+constexpr int ROUTE_MAX_WORLD = 8;
+
+struct __align__(16) WarpSharedRoute {
+    uint4 skey[ROUTE_MAX_WORLD][32];
+    u64 sord[ROUTE_MAX_WORLD][32];
+    uint4 rows[TILE_S];
+    u64 term[TILE_S];
+    BlockDesc block;
+    u64 ticket, sep_now;
+    uint32_t fill[ROUTE_MAX_WORLD];
+};
+
+__device__ __forceinline__ void route_flush(const NarrowParams &P, WarpSharedRoute &ws, uint32_t w, uint32_t cnt) {
+    const int lane = threadIdx.x & 31;
+    u64 base = 0;
+    if (lane == 0) base = atomicAdd(&P.route_counts[w], (u64)cnt);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (base + cnt <= P.route_cap && (uint32_t)lane < cnt) {  // (past the region: only counted; the host redoes the level)
+        const u64 at = (u64)w * P.route_cap + base + lane;
+        P.route_rows[at] = ws.skey[w][lane];
+        P.route_ords[at] = ws.sord[w][lane];
+    }
+}
+
+struct RouteSink {
+    const NarrowParams &P;
+    WarpSharedRoute &ws;
+    template <int LW, typename OrdOf>
+    __device__ __forceinline__ void emit(const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                         const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
+        const int lane = threadIdx.x & 31;
+        const uint32_t lt = lanemask_lt();
+#pragma unroll
+        for (int r = 0; r < PROBE_BATCH; ++r) {
+            if (live[r] && cm_sep_diff<LW>(cand[r], P.target) == 0u) {
+                const u64 o = ord_of(r);
+                if (P.route_sep_any) atomicMin(&P.counters[CTR_SEP], o);
+                if (P.sep_list) {  // exhaustive runs keep every separating ordinal (chunk-exact separator id)
+                    const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+                    if (pos < P.sep_list_cap) P.sep_list[pos] = o;
+                }
+            }
+            const bool send = live[r] && !known[r];
+            const uint32_t owner = send ? key_owner(cand[r], P.route_world) : 0xFFFFFFFFu;
+            uint32_t pending = __ballot_sync(0xFFFFFFFFu, send);
+            while (pending) {  // one round per owner present in this batch row
+                const uint32_t w = __shfl_sync(0xFFFFFFFFu, owner, __ffs(pending) - 1);
+                const bool mine = owner == w;
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+                pending &= ~m;
+                const uint32_t n = __popc(m), fill = ws.fill[w];
+                const uint32_t pos = fill + __popc(m & lt);
+                if (mine && pos < 32u) {
+                    ws.skey[w][pos] = cand[r];
+                    ws.sord[w][pos] = ord_of(r);
+                }
+                uint32_t fill_after = fill + n;
+                __syncwarp();
+                if (fill_after >= 32u) {
+                    route_flush(P, ws, w, 32u);
+                    __syncwarp();
+                    if (mine && pos >= 32u) {
+                        ws.skey[w][pos - 32u] = cand[r];
+                        ws.sord[w][pos - 32u] = ord_of(r);
+                    }
+                    fill_after -= 32u;
+                }
+                if (lane == 0) ws.fill[w] = fill_after;
+                __syncwarp();
+            }
+        }
+    }
+};
+
+template <int LW, int OP>
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_route_kernel(const NarrowParams P) {
+    __shared__ WarpSharedRoute s_warp[WARPS_PER_CTA];
+    WarpSharedRoute &ws = s_warp[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    if (lane < ROUTE_MAX_WORLD) ws.fill[lane] = 0u;
+    __syncwarp();
+    RouteSink sink{P, ws};
+    TileFetch next = fetch_tile(P, nullptr);
+    for (;;) {
+        const TileFetch cur = next;
+        if (!open_tile(P, ws, cur)) break;
+        next = fetch_tile(P, nullptr);
+        if (run_tile<LW, OP>(P, ws, sink)) break;
+    }
+    __syncwarp();
+    for (uint32_t w = 0; w < P.route_world; ++w) {
+        const uint32_t fill = ws.fill[w];
+        if (fill) route_flush(P, ws, w, fill);
+    }
+}
+
+// Phase B on the owner: insert-or-min of `n` received records, PROBE_BATCH coalesced records per lane and step
+// through the same insert_batch / drain_round as the single-GPU kernel.
+template <int LW>
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_probe_kernel(const NarrowParams P, const uint4 *rows,
+                                                                                    const u64 *ords, u64 n) {
+    __shared__ WarpShared s_warp[WARPS_PER_CTA];
+    WarpShared &ws = s_warp[threadIdx.x >> 5];
+    WarpState st;
+    const int lane = threadIdx.x & 31;
+    const u64 warp = (u64)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5), n_warps = (u64)gridDim.x * WARPS_PER_CTA;
+    constexpr u64 STEP = 32ull * PROBE_BATCH;
+#pragma unroll 1
+    for (u64 base = warp * STEP; base < n; base += n_warps * STEP) {
+        if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] != 0ull) break;
+        uint4 cand[PROBE_BATCH];
+        u64 o[PROBE_BATCH];
+        bool live[PROBE_BATCH], known[PROBE_BATCH];
+#pragma unroll
+        for (int r = 0; r < PROBE_BATCH; ++r) {
+            const u64 i = base + (u64)r * 32 + lane;
+            live[r] = i < n;
+            known[r] = false;
+            cand[r] = live[r] ? __ldcs(rows + i) : make_uint4(0, 0, 0, 0);
+            o[r] = live[r] ? __ldcs(ords + i) : 0ull;
+        }
+        insert_batch<LW>(P, ws.queue, st, cand, live, known, [&](int r) { return o[r]; });
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
         while (st.qfill > 0u) drain_round(P, ws.queue, st);

@@ -135,12 +135,14 @@ __global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kerne
 }
 
 // re-insert finalised rows [first, first+count) into a fresh table (regrow / rollback)
+// (owners > 1: an owner-sharded set holds only the CMs whose hash owner is `rank`)
 __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 slot_mask, const uint4 *store,
-                                                             u64 first, u64 count, u64 *counters) {
+                                                             u64 first, u64 count, u64 *counters, uint32_t owners, uint32_t rank) {
     const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (u64)gridDim.x * blockDim.x) {
         const u64 gid = first + t;
         const uint4 key = store[gid];
+        if (owners > 1u && key_owner(key, owners) != rank) continue;
         if (key_is_empty(key)) {
             counters[CTR_SPECIAL] = gid;
             continue;
@@ -157,85 +159,41 @@ __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 
     }
 }
 
-// ---- exchange of a level's claims between ranks (one search sharded over several GPUs) ----
-// A record is {key (uint4), ordinal (u64)}.  owner(key) = a hash independent of the slot hash.
+// ---- sharded search: what an owner publishes, and what every rank appends to its cache ----------------------
 
-__device__ __forceinline__ uint32_t key_owner(uint4 key, uint32_t owners) {
-    return hash_vec(key, 0x5BD1E995u) % owners;
-}
-
-// counts[o] += claims of this level owned by rank o; with `cursors`, also writes the records
-// grouped by owner (cursors[o] = next free position of owner o's range)
-__global__ void __launch_bounds__(256) narrow_export_kernel(const uint4 *claim_key, const u64 *claim_ord, u64 n_claimed,
-                                                            uint32_t owners, u64 *counts, u64 *cursors, uint4 *keys_out,
-                                                            u64 *ords_out) {
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_claimed; t += (u64)gridDim.x * blockDim.x) {
-        const u64 ord = claim_ord[t];
-        if (ord == VAL_EMPTY) continue;  // reserved but never used
-        const uint4 key = claim_key[t];
-        const uint32_t o = key_owner(key, owners);
-        if (cursors) {
-            const u64 pos = atomicAdd(&cursors[o], 1ull);
-            keys_out[pos] = key;
+// Compacts this owner's winners (claims whose smallest ordinal is <= ord_limit) into dense record arrays;
+// cursor[0] = how many.  The order is irrelevant: the receiver places every record by the rank of its ordinal.
+__global__ void __launch_bounds__(256) narrow_winners_kernel(const uint4 *claim_key, const u64 *claim_ord, u64 n_claimed,
+                                                             u64 ord_limit, u64 *cursor, uint4 *rows_out, u64 *ords_out) {
+    const int lane = threadIdx.x & 31;
+    const u64 n_round = (n_claimed + 31) & ~31ull;  // whole warps stay in the loop for the ballot
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_round; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = t < n_claimed ? claim_ord[t] : VAL_EMPTY;
+        const bool keep = ord != VAL_EMPTY && ord <= ord_limit;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
+        if (m == 0u) continue;
+        u64 base = 0;
+        if (lane == 0) base = atomicAdd(cursor, (u64)__popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (keep) {
+            const u64 pos = base + __popc(m & ((1u << lane) - 1u));
+            rows_out[pos] = claim_key[t];
             ords_out[pos] = ord;
-        } else {
-            atomicAdd(&counts[o], 1ull);
         }
     }
 }
 
-// insert-or-min received records into the local set; new CMs get a claim index of their own
-__global__ void __launch_bounds__(256) narrow_import_kernel(const NarrowParams P, const uint4 *keys, const u64 *ords, u64 n) {
-    const uint4 empty = make_uint4(~0u, ~0u, ~0u, ~0u);
+// Appends records published by OTHER owners to the cache: position = rank of the ordinal in the level's global
+// winners bitmap (the all-reduced union of every owner's marks), exactly as narrow_scatter_kernel places this
+// owner's own claims.
+__global__ void __launch_bounds__(256) narrow_scatter_records_kernel(const uint4 *rows, const u64 *ords, u64 n,
+                                                                     const uint32_t *bitmap, const uint32_t *sb_rank,
+                                                                     uint4 *store, u64 *store_ords, u64 base) {
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (u64)gridDim.x * blockDim.x) {
-        const uint4 key = keys[t];
         const u64 ord = ords[t];
-        u64 *val_at = nullptr;
-        bool claimed = false, overflow = false;
-        u64 my_idx = 0;
-        if (key_is_empty(key)) {  // the all-ones CM has a register instead of a slot
-            val_at = &P.counters[CTR_SPECIAL];
-            if (*(volatile u64 *)val_at == VAL_EMPTY) {
-                my_idx = atomicAdd(&P.counters[CTR_CLAIMED], 1ull);
-                if (my_idx >= P.claim_cap) overflow = true;
-                else claimed = atomicCAS(val_at, VAL_EMPTY, P.epoch | my_idx) == VAL_EMPTY;
-            }
-        } else {
-            u64 slot = hash_vec(key, 0u) & P.slot_mask;
-            for (;;) {
-                uint4 k = ld_cg_u4(&P.slots[slot].key);
-                if (key_is_empty(k)) {
-                    my_idx = atomicAdd(&P.counters[CTR_CLAIMED], 1ull);  // stays unused if the CAS below loses
-                    if (my_idx >= P.claim_cap) {
-                        overflow = true;
-                        break;
-                    }
-                    k = cas128(&P.slots[slot].key, empty, key);
-                    if (key_is_empty(k)) {
-                        claimed = true;
-                        __stcg(&P.slots[slot].val, P.epoch | my_idx);
-                        k = key;
-                    }
-                }
-                if (v_eq(k, key)) {
-                    val_at = &P.slots[slot].val;
-                    break;
-                }
-                slot = (slot + 1) & P.slot_mask;
-            }
-        }
-        if (overflow) {
-            atomicExch(&P.counters[CTR_OVERFLOW], 1ull);
-            continue;
-        }
-        if (claimed) {
-            P.claim_key[my_idx] = key;
-            atomicMin(&P.claim_ord[my_idx], ord);
-        } else {
-            u64 v;
-            while ((v = *(volatile u64 *)val_at) == VAL_EMPTY) {}  // a claimer publishes right after its CAS
-            if (v >= P.epoch) atomicMin(&P.claim_ord[v & CLAIM_IDX_MASK], ord);
-        }
+        const u64 gid = base + ordinal_rank(bitmap, sb_rank, ord);
+        store[gid] = rows[t];
+        store_ords[gid] = ord;
     }
 }
 

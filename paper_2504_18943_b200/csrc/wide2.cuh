@@ -36,6 +36,7 @@ constexpr int W2_BATCH = 2;        // candidates a lane carries through the pass
 constexpr int W2_PREFETCH = LTLB200_W2_PREFETCH;  // vectors of a stored row fetched ahead of the full-row compare
 constexpr int W2_SC_VECS = 512;    // uint4 vectors of scalar-operand rows staged per warp (8 KiB)
 constexpr int W2_TERMS = 128;      // max scalar rows per tile
+enum : int { W2_PLAIN = 0, W2_GUARD = 1, W2_ROUTE = 2 };  // what a tile does with its candidates (wide2_batch / wide2_route_batch)
 
 struct __align__(16) Wide2Fixed {  // per-warp shared state behind the row areas
     u64 term[W2_TERMS];
@@ -247,7 +248,84 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
     }
 }
 
-template <int LW, int OP, bool GUARD>
+// One search sharded over several GPUs (see narrow.cuh: "route instead of probe"): the candidate is not probed
+// here; its row goes to the send region of its hash owner.  Pass 1 yields the owner hash, the separation flag and
+// the equals-an-operand flags; the lanes of one owner take consecutive records (one atomicAdd per owner present in
+// the batch row); pass 2 writes the row -- nvec consecutive vectors per lane, whole 32-byte sectors.
+template <int LW, int OP, class Gen>
+__device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wide2Warp &W, Gen gen,
+                                                  const bool (&live)[W2_BATCH], const u64 (&ords)[W2_BATCH]) {
+    const int nvec = P.nvec;
+    uint32_t ho[W2_BATCH], sepacc[W2_BATCH], da[W2_BATCH], db[W2_BATCH];
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) ho[r] = sepacc[r] = da[r] = db[r] = 0u;
+#pragma unroll 1
+    for (int p = 0; p < nvec; ++p) {
+        const uint4 valid = W.consts[p], target = W.consts[nvec + p];
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            uint4 a, b;
+            gen(r, p, a, b);
+            const uint4 c = cm_apply<LW, OP>(a, b, valid);
+            ho[r] ^= hash_vec(c, 0x5BD1E995u * (uint32_t)(p + 1));
+            sepacc[r] |= cm_sep_diff<LW>(c, target);
+            da[r] |= v_diff(c, a);
+            db[r] |= v_diff(c, b);
+        }
+    }
+    u64 at[W2_BATCH];
+    bool send[W2_BATCH];
+    const uint32_t lt = lanemask_lt();
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) {
+        if (live[r] && sepacc[r] == 0u) {
+            if (P.route_sep_any) atomicMin(&P.counters[CTR_SEP], ords[r]);
+            if (P.sep_list) {
+                const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
+                if (pos < P.sep_list_cap) P.sep_list[pos] = ords[r];
+            }
+        }
+        const bool known = OP != OP_ATOM && (da[r] == 0u || db[r] == 0u);  // equals an operand: already in the cache
+        send[r] = live[r] && !known;
+        const uint32_t owner = send[r] ? row_owner_mix(ho[r]) % P.route_world : 0xFFFFFFFFu;
+        at[r] = ~0ull;
+        uint32_t pending = __ballot_sync(0xFFFFFFFFu, send[r]);
+        while (pending) {
+            const uint32_t w = __shfl_sync(0xFFFFFFFFu, owner, __ffs(pending) - 1);
+            const bool mine = owner == w;
+            const uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+            pending &= ~m;
+            u64 base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(&P.route_counts[w], (u64)__popc(m));
+            base = __shfl_sync(0xFFFFFFFFu, base, __ffs(m) - 1);
+            if (mine) {
+                const u64 pos = base + __popc(m & lt);
+                if (pos < P.route_cap) {  // (past the region: only counted; the host redoes the level)
+                    at[r] = (u64)w * P.route_cap + pos;
+                    P.route_ords[at[r]] = ords[r];
+                }
+            }
+        }
+    }
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < W2_BATCH; ++r) any = any || at[r] != ~0ull;
+    if (!any) return;
+#pragma unroll 1
+    for (int p = 0; p < nvec; ++p) {
+        const uint4 valid = W.consts[p];
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) {
+            if (at[r] == ~0ull) continue;
+            uint4 a, b;
+            gen(r, p, a, b);
+            P.route_rows[at[r] * nvec + p] = cm_apply<LW, OP>(a, b, valid);
+        }
+    }
+}
+
+template <int LW, int OP, int MODE>
 __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
                                                  u64 sep_now) {
     const BlockDesc &B = W.fx->block;
@@ -275,11 +353,12 @@ __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide
             a = __ldg(rows[r] + p);
             b = a;
         };
-        wide2_batch<LW, OP, GUARD>(P, W, st, gen, live, ords);
+        if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW, OP>(P, W, gen, live, ords);
+        else wide2_batch<LW, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
     }
 }
 
-template <int LW, int OP, bool VEC_B, bool GUARD>
+template <int LW, int OP, bool VEC_B, int MODE>
 __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
                                                   u64 sep_now) {
     const BlockDesc &B = W.fx->block;
@@ -340,7 +419,8 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
                 a = VEC_B ? xs : xv;
                 b = VEC_B ? xv : xs;
             };
-            wide2_batch<LW, OP, GUARD>(P, W, st, gen, live, ords);
+            if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW, OP>(P, W, gen, live, ords);
+        else wide2_batch<LW, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
         }
     }
 }
@@ -380,16 +460,16 @@ __device__ __forceinline__ bool wide2_next_tile(const WideParams &P, const Wide2
     return W.fx->ticket < P.tile_end;
 }
 
-template <int LW, int OP, bool GUARD = false>
+template <int LW, int OP, int MODE = W2_PLAIN>
 __device__ __forceinline__ void wide2_run_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st) {
     const u64 sep_now = W.fx->sep_now;
     if (W.fx->block.ord0 > sep_now) return;
     const u64 tile_local = W.fx->ticket - W.fx->block.tile0;
     if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
-        if (W.fx->block.vec_is_b) wide2_binary_tile<LW, OP, true, GUARD>(P, W, st, tile_local, sep_now);
-        else wide2_binary_tile<LW, OP, false, GUARD>(P, W, st, tile_local, sep_now);
+        if (W.fx->block.vec_is_b) wide2_binary_tile<LW, OP, true, MODE>(P, W, st, tile_local, sep_now);
+        else wide2_binary_tile<LW, OP, false, MODE>(P, W, st, tile_local, sep_now);
     } else {
-        wide2_unary_tile<LW, OP, GUARD>(P, W, st, tile_local, sep_now);
+        wide2_unary_tile<LW, OP, MODE>(P, W, st, tile_local, sep_now);
     }
 }
 
@@ -428,15 +508,24 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_guarded_level_kernel(con
     Wide2State st;
     while (wide2_next_tile(P, W)) {
         switch (W.fx->block.op) {
-            case OP_ATOM: wide2_run_tile<LW, OP_ATOM, true>(P, W, st); break;
-            case OP_NOT: wide2_run_tile<LW, OP_NOT, true>(P, W, st); break;
-            case OP_NEXT: wide2_run_tile<LW, OP_NEXT, true>(P, W, st); break;
-            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE, true>(P, W, st); break;
-            case OP_AND: wide2_run_tile<LW, OP_AND, true>(P, W, st); break;
-            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL, true>(P, W, st); break;
-            default: wide2_run_tile<LW, OP_OR, true>(P, W, st); break;
+            case OP_ATOM: wide2_run_tile<LW, OP_ATOM, W2_GUARD>(P, W, st); break;
+            case OP_NOT: wide2_run_tile<LW, OP_NOT, W2_GUARD>(P, W, st); break;
+            case OP_NEXT: wide2_run_tile<LW, OP_NEXT, W2_GUARD>(P, W, st); break;
+            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE, W2_GUARD>(P, W, st); break;
+            case OP_AND: wide2_run_tile<LW, OP_AND, W2_GUARD>(P, W, st); break;
+            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL, W2_GUARD>(P, W, st); break;
+            default: wide2_run_tile<LW, OP_OR, W2_GUARD>(P, W, st); break;
         }
     }
+}
+
+// sharded search, phase A: one launch per operator like wide2_level_kernel, candidates routed to their owners
+template <int LW, int OP>
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_WIDE2_MIN_CTAS) wide2_route_kernel(const __grid_constant__ WideParams P) {
+    extern __shared__ __align__(16) uint4 s_w2[];
+    const Wide2Warp W = wide2_carve(P, s_w2);
+    Wide2State st;
+    while (wide2_next_tile(P, W)) wide2_run_tile<LW, OP, W2_ROUTE>(P, W, st);
 }
 
 }  // namespace ltlb200

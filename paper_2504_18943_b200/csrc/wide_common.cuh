@@ -53,7 +53,27 @@ struct WideParams {
     const u64 *dead;
     uint32_t dead_n;
     int scan_only;
+    // sharded search (wide2_route_kernel; see NarrowParams): rows go to the region of their hash owner
+    uint4 *route_rows;  // route_world regions of route_cap rows of nvec vectors
+    u64 *route_ords;
+    u64 route_cap;
+    u64 *route_counts;
+    uint32_t route_world;
+    int route_sep_any;
 };
+
+// hash owner of a row in a sharded search (independent of the slot hash and of the fingerprint)
+__device__ __forceinline__ uint32_t row_owner_mix(uint32_t h) {
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 13;
+    return h;
+}
+__device__ __forceinline__ uint32_t row_owner(const uint4 *row, int nvec, uint32_t owners) {
+    uint32_t h = 0;
+    for (int p = 0; p < nvec; ++p) h ^= hash_vec(row[p], 0x5BD1E995u * (uint32_t)(p + 1));
+    return row_owner_mix(h) % owners;
+}
 
 // per-group registers (uniform inside a group)
 struct GroupState {

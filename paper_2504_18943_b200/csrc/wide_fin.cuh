@@ -84,9 +84,11 @@ __global__ void __launch_bounds__(256) wide_copy_kernel(const WideFinalize F) {
 
 // re-insert finalised rows [0, count) into a fresh table: rows of the cache are pairwise
 // distinct, so claiming the first empty slot of the probe sequence is enough
+// (owners > 1: an owner-sharded set holds only the rows whose hash owner is `rank`)
 __global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_mask, const uint4 *store, u64 count,
-                                                           int nvec, int log2g) {
+                                                           int nvec, int log2g, uint32_t owners, uint32_t rank) {
     for (u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x; gid < count; gid += (u64)gridDim.x * blockDim.x) {
+        if (owners > 1u && row_owner(store + gid * nvec, nvec, owners) != rank) continue;
         uint32_t a = 0, b = 0;
         for (int p = 0; p < nvec; ++p) {
             const uint4 part = store[gid * nvec + p];
@@ -105,32 +107,43 @@ __global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_
     }
 }
 
-// ---- exchange of a level's claims between ranks (wide rows) ----------------------------------
+// ---- sharded search: what an owner publishes, what every rank appends, what an owner folds in ---------------
 
-__device__ __forceinline__ uint32_t row_owner(const uint4 *row, int nvec, uint32_t owners) {
-    uint32_t h = 0;
-    for (int p = 0; p < nvec; ++p) h ^= hash_vec(row[p], 0x5BD1E995u * (uint32_t)(p + 1));
-    h ^= h >> 15;
-    h *= 0x2C1B3C6Du;
-    h ^= h >> 13;
-    return h % owners;
-}
-
-// one thread per staging entry: count per owner, or (with cursors) copy the records out grouped by owner
-__global__ void __launch_bounds__(256) wide_export_kernel(const uint4 *stage_rows, const u64 *stage_ord, u64 n_staged, int nvec,
-                                                          uint32_t owners, u64 *counts, u64 *cursors, uint4 *rows_out,
-                                                          u64 *ords_out) {
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_staged; t += (u64)gridDim.x * blockDim.x) {
-        const u64 ord = stage_ord[t];
-        if (ord == VAL_EMPTY) continue;  // reserved but never published
-        const uint32_t o = row_owner(stage_rows + t * nvec, nvec, owners);
-        if (cursors) {
-            const u64 pos = atomicAdd(&cursors[o], 1ull);
+// Compacts this owner's winners (staging entries whose smallest ordinal is <= ord_limit) into dense record
+// arrays; cursor[0] = how many.  One warp per 32 entries: positions by ballot, rows copied vector by vector.
+__global__ void __launch_bounds__(256) wide_winners_kernel(const uint4 *stage_rows, const u64 *stage_ord, u64 n_staged, int nvec,
+                                                           u64 ord_limit, u64 *cursor, uint4 *rows_out, u64 *ords_out) {
+    const int lane = threadIdx.x & 31;
+    const u64 n_round = (n_staged + 31) & ~31ull;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_round; t += (u64)gridDim.x * blockDim.x) {
+        const u64 ord = t < n_staged ? stage_ord[t] : VAL_EMPTY;
+        const bool keep = ord != VAL_EMPTY && ord <= ord_limit;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
+        if (m == 0u) continue;
+        u64 base = 0;
+        if (lane == 0) base = atomicAdd(cursor, (u64)__popc(m));
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (keep) {
+            const u64 pos = base + __popc(m & ((1u << lane) - 1u));
             for (int p = 0; p < nvec; ++p) rows_out[pos * nvec + p] = stage_rows[t * nvec + p];
             ords_out[pos] = ord;
-        } else {
-            atomicAdd(&counts[o], 1ull);
         }
+    }
+}
+
+// Appends records published by OTHER owners to the cache (see narrow_scatter_records_kernel): one thread per
+// (record, vector), the rank of a record's ordinal recomputed per vector from the L2-resident bitmap prefix.
+__global__ void __launch_bounds__(256) wide_scatter_records_kernel(const uint4 *rows, const u64 *ords, u64 n, int nvec,
+                                                                   const uint32_t *bitmap, const uint32_t *sb_rank,
+                                                                   uint4 *store, u64 *store_ords, u64 base) {
+    const u64 total = n * (u64)nvec;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+        const u64 k = t / nvec;
+        const int p = (int)(t - k * nvec);
+        const u64 ord = ords[k];
+        const u64 gid = base + ordinal_rank(bitmap, sb_rank, ord);
+        store[gid * nvec + p] = rows[t];
+        if (p == 0) store_ords[gid] = ord;
     }
 }
 

@@ -1,24 +1,30 @@
 """One search sharded over several GPUs: the per-level exchange protocol.
 
-Every rank holds the complete language cache of the finished levels (replicated).  For a
-new level each rank enumerates a tile-strided shard of the level's pair space into its
-local hash set, then the ranks agree on the level's contents with one exchange:
+The language cache (rows and winning ordinals of every finished level) is replicated on every rank, because any
+rank reads any operand.  The dedup set is **owner-sharded**: rank ``r`` holds exactly the CMs whose hash owner is
+``r``, of every level, so the set of an N-GPU search has N times the capacity of one GPU's and every rank probes
+1/N of a level's candidates.  One level:
 
-1. **route**   every rank sends its local claims ``{CM row, min ordinal}`` to the row's hash
-               owner (``all_to_all``: counts, then rows and ordinals);
-2. **reduce**  the owner folds what it received into its own set (insert-or-min on the device),
-               so that for the CMs it owns it now knows the smallest ordinal over all ranks;
-3. **publish** every owner ``all_gather``\\ s its winners; every rank folds all of them into its
-               set.  Now every set holds exactly the level's new CMs with their global minimum
-               ordinals, so the finalisation (rank by ordinal, append, assign ids) produces the
-               same level -- bytes, provenance, ids -- on every rank and on one GPU;
-4. **separator** ``all_reduce(min)`` of the smallest fresh separating ordinal (plus an
-               ``all_gather`` of all separating ordinals in exhaustive runs, for the
-               reference's chunk-exact separator id).
+1. **route**    every rank builds its tile-strided share of the level's pair space; every candidate that is not a
+                duplicate by construction goes, as a record ``{CM row, ordinal}``, to the send region of its
+                hash owner (on the device, inside the construction kernel); one grouped send/recv of exact sizes
+                moves the regions (``all_to_all``);
+2. **reduce**   the owner folds what it received into its part of the set (insert-or-min on the device): it now
+                knows, for the CMs it owns, whether they are new and the smallest ordinal that built them; it marks
+                its winners in a bitmap with one bit per candidate ordinal of the level;
+3. **rank**     ``all_reduce(SUM)`` of the bitmaps -- the owners' bits are disjoint, so the sum is the union --
+                gives every rank the level's winners bitmap: the id of a winner is the number of set bits before
+                its ordinal; the separator is the ``min`` of the ranks' smallest separating ordinals;
+4. **publish**  every owner sends its winners up to the separator to every other rank (``all_gather`` of exact
+                sizes); every rank appends its own and the received rows to its cache at their ids.
 
-The protocol is written against a small shard-engine interface so that the same code runs
-over NCCL with the CUDA engine (``CandidateStore``) and, in the CPU test suite, over gloo with
-a numpy stand-in.  Collectives move torch tensors that live wherever the engine lives.
+Per rank and level: C/N candidates built, (K+8)·C/N bytes out and in over NVLink, C/N random probes into a set of
+1/N of the keys, and the u·C new rows that every replica of the cache stores anyway (sequential appends, no set
+insert).  Metadata travels in two small ``all_gather``s; the host reads three counts per level.
+
+The protocol is written against a small shard-engine interface so that the same code runs over NCCL with the CUDA
+engine (``CandidateStore``) and, in the CPU test suite, over gloo with a numpy stand-in.  Collectives move torch
+tensors that alias the engine's own buffers.
 """
 
 from __future__ import annotations
@@ -46,6 +52,7 @@ from .engine import (
 from .traces import validate_feasible
 
 NO_SEPARATOR = (1 << 64) - 1
+_I64_MAX = (1 << 63) - 1
 
 # Levels with fewer candidates than this are built REDUNDANTLY on every rank instead of being sharded: the
 # cache is replicated and the engine is deterministic, so every rank gets the same level without a single
@@ -59,73 +66,68 @@ class ShardEngine(Protocol):
 
     key_bytes: int
 
-    def level_begin(self, cost: int, op_mask: int, exhaustive: bool, deadline, shard_index: int, shard_count: int):
-        """-> (status, n_claimed, sep_ord or NO_SEPARATOR, n_seps)"""
+    def route_begin(self, cost: int, op_mask: int, exhaustive: bool, deadline, rank: int, world: int):
+        """-> (status, parts, sep_ord or NO_SEPARATOR, n_seps); parts[o] = (rows uint8 [n_o, key_bytes],
+        ords int64 [n_o]): the records this rank built whose hash owner is o"""
 
-    def claims_count(self, owners: int) -> list[int]: ...
+    def exchange_recv(self, n_records: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """-> (rows uint8 [n, key_bytes], ords int64 [n]) to receive into"""
 
-    def claims_pack(self, owners: int, total: int) -> tuple[torch.Tensor, torch.Tensor]:
-        """-> rows uint8 [total, key_bytes], ords int64 [total], grouped by owner (owner 0 first)"""
+    def owner_reduce(self, n_records: int) -> tuple[int, torch.Tensor]:
+        """folds the first n_records received records into the owned part of the set
+        -> (status, bitmap int32 [words]: this owner's winners, one bit per ordinal of the level)"""
 
-    def claims_import(self, rows: torch.Tensor, ords: torch.Tensor) -> None: ...
+    def level_abort(self) -> None:
+        """ends the pending level empty (some rank ran out of budget)"""
+
+    def winners_export(self, sep_ord: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """-> (rows, ords) of this owner's winners with ordinal <= sep_ord"""
 
     def separating_ordinals(self) -> torch.Tensor:
-        """int64 tensor of every separating ordinal recorded in the pending level"""
+        """int64 tensor of every separating ordinal this rank recorded in the pending level"""
 
-    def level_end(self, sep_ord: int, seps, batch_size: int, memory_budget_bytes: int):
-        """-> (status, n_new, sep_gid or None, constructed_delta)"""
+    def level_commit(self, sep_ord: int, seps, n_received: int, batch_size: int, memory_budget_bytes: int):
+        """-> (status, n_new, sep_gid or None, constructed_delta); the global bitmap is in owner_reduce's tensor,
+        the first n_received records of the receive buffers are the winners of the other owners"""
 
-    # optional: without these two every level is sharded
+    # optional: without these two every level goes through the exchange
     def level_candidates(self, cost: int, op_mask: int) -> int: ...
 
     def expand_local(self, cost: int, op_mask: int, exhaustive: bool, batch_size: int, memory_budget_bytes: int, deadline):
         """-> (status, n_new, sep_gid or None, constructed_delta): the whole level on this rank"""
 
 
-def _all_to_all_v(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group) -> torch.Tensor:
-    """Variable-size all-to-all along dim 0."""
-    out = send.new_empty((sum(recv_counts),) + tuple(send.shape[1:]))
-    if dist.get_backend(group) == "gloo":
-        # gloo has no all_to_all_single for uneven splits everywhere: use pairwise isend/irecv
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-        s_off = [0]
-        r_off = [0]
-        for c in send_counts:
-            s_off.append(s_off[-1] + c)
-        for c in recv_counts:
-            r_off.append(r_off[-1] + c)
-        out[r_off[rank]:r_off[rank + 1]] = send[s_off[rank]:s_off[rank + 1]]
-        reqs = []
-        for peer in range(world):
-            if peer == rank:
-                continue
-            if send_counts[peer]:
-                reqs.append(dist.isend(send[s_off[peer]:s_off[peer + 1]].contiguous(), dist.get_global_rank(group, peer) if group else peer, group=group))
-            if recv_counts[peer]:
-                buf = out[r_off[peer]:r_off[peer + 1]]
-                reqs.append(dist.irecv(buf, dist.get_global_rank(group, peer) if group else peer, group=group))
-        for r in reqs:
-            r.wait()
-        return out
-    dist.all_to_all_single(out, send.contiguous(), recv_counts, send_counts, group=group)
-    return out
-
-
-def _all_gather_v(local: torch.Tensor, group) -> torch.Tensor:
-    """Concatenation over ranks (rank order) of tensors whose dim 0 differs per rank."""
+def _gather_ints(values: list[int], device, group) -> list[list[int]]:
+    """all_gather of a short int64 vector: result[r] = the vector of rank r."""
     world = dist.get_world_size(group)
-    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
-    counts = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(counts, n, group=group)
-    sizes = [int(c.item()) for c in counts]
-    biggest = max(sizes) if sizes else 0
-    if biggest == 0:
-        return local.new_empty((0,) + tuple(local.shape[1:]))
-    padded = local.new_zeros((biggest,) + tuple(local.shape[1:]))
-    padded[: local.shape[0]] = local
-    parts = [torch.empty_like(padded) for _ in range(world)]
-    dist.all_gather(parts, padded, group=group)
-    return torch.cat([p[:k] for p, k in zip(parts, sizes)], dim=0)
+    mine = torch.tensor(values, dtype=torch.int64, device=device)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    return [[int(v) for v in p.tolist()] for p in parts]
+
+
+def _exchange(send_parts, recv_bufs, recv_counts, group, include_self: bool):
+    """One grouped exchange of exact sizes.  send_parts[peer] = tuple of tensors (same leading size) that goes to
+    `peer`; what `src` sends lands in the tensors of recv_bufs at the offset of src (source-major, dense).  With
+    include_self the rank's own part is copied in place; otherwise recv_counts[rank] must be 0."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    offsets = [0]
+    for c in recv_counts:
+        offsets.append(offsets[-1] + c)
+    if include_self and recv_counts[rank]:
+        for buf, part in zip(recv_bufs, send_parts[rank]):
+            buf[offsets[rank]:offsets[rank + 1]].copy_(part)
+    ops = []
+    peer_of = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    for shift in range(1, world):  # every rank posts its sends and receives in the same relative order
+        dst, src = (rank + shift) % world, (rank - shift) % world
+        if send_parts[dst][0].shape[0]:
+            ops += [dist.P2POp(dist.isend, part, peer_of(dst), group) for part in send_parts[dst]]
+        if recv_counts[src]:
+            ops += [dist.P2POp(dist.irecv, buf[offsets[src]:offsets[src + 1]], peer_of(src), group) for buf in recv_bufs]
+    if ops:
+        for work in dist.batch_isend_irecv(ops):  # NCCL: one ncclGroup of sends and receives
+            work.wait()
 
 
 def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfig, stats: RunStats | None = None,
@@ -137,9 +139,10 @@ def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfi
     stats = stats if stats is not None else RunStats()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     mask = operator_mask(ops)
-    # ... and so is a NON-exhaustive level over a store that already holds a separating CM, whatever its size: the
-    # reference then truncates every chunk at its first separating candidate (engine.py:334-335), which the
-    # single-handle expand_level reproduces and the claim exchange (minimum ordinal per CM) cannot
+    device = _device_of(store)
+    # A NON-exhaustive level over a store that already holds a separating CM is built by every rank on its own,
+    # whatever its size: the reference then truncates every chunk at its first separating candidate
+    # (engine.py:334-335), which the single-handle expand_level reproduces and "minimum ordinal per CM" cannot.
     truncating = (not config.exhaustive) and getattr(store, "holds_separator", lambda: False)()
     if hasattr(store, "level_candidates") and hasattr(store, "expand_local") \
             and (truncating or store.level_candidates(cost, mask) < REPLICATE_BELOW):
@@ -147,64 +150,59 @@ def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfi
         # because the time budget is read from each rank's own clock
         status, n_new, sep_gid, delta = store.expand_local(cost, mask, config.exhaustive, config.batch_size,
                                                            config.memory_budget_mb << 20, deadline)
-        flag = torch.tensor([status], dtype=torch.int64, device=_device_of(store))
+        flag = torch.tensor([status], dtype=torch.int64, device=device)
         dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
         stats.constructed += delta
         stats.unique = store.total
         if int(flag.item()) in _FAILURE_TEXT:
             raise _BudgetExceeded(_FAILURE_TEXT[int(flag.item())])
         return n_new, sep_gid
-    status, _, sep_local, _ = store.level_begin(cost, mask, config.exhaustive, deadline, rank, world)
 
-    # a budget stop must be collective: every rank stops or none does
-    flag = torch.tensor([status], dtype=torch.int64, device=_device_of(store))
-    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
-    if int(flag.item()) != 0:
-        code = int(flag.item())
-        if status == 0:  # this rank began the level: close it empty
-            store.level_end(NO_SEPARATOR, None, config.batch_size, 0)
-        raise _BudgetExceeded(_FAILURE_TEXT.get(code, "budget exhausted"))
-
-    # 1. route local claims to their hash owners
-    send_counts = store.claims_count(world)
-    rows, ords = store.claims_pack(world, sum(send_counts))
-    counts_t = torch.tensor(send_counts, dtype=torch.int64, device=rows.device)
-    recv_t = torch.empty_like(counts_t)
-    dist.all_to_all_single(recv_t, counts_t, group=group) if dist.get_backend(group) != "gloo" else _gloo_counts(recv_t, counts_t, group)
-    recv_counts = [int(c) for c in recv_t.tolist()]
-    got_rows = _all_to_all_v(rows, send_counts, recv_counts, group)
-    got_ords = _all_to_all_v(ords, send_counts, recv_counts, group)
-    # 2. the owner reduces: min ordinal over all ranks for the CMs it owns
-    store.claims_import(got_rows, got_ords)
-    # 3. owners publish their winners, everybody folds them in
-    own_counts = store.claims_count(world)
-    all_rows, all_ords = store.claims_pack(world, sum(own_counts))
-    lo = sum(own_counts[:rank])
-    mine_rows, mine_ords = all_rows[lo:lo + own_counts[rank]], all_ords[lo:lo + own_counts[rank]]
-    store.claims_import(_all_gather_v(mine_rows, group), _all_gather_v(mine_ords, group))
-    # 4. separator
-    sep_t = torch.tensor([min(sep_local, (1 << 63) - 1)], dtype=torch.int64, device=rows.device)
-    dist.all_reduce(sep_t, op=dist.ReduceOp.MIN, group=group)
-    sep_ord = int(sep_t.item())
-    sep_ord = NO_SEPARATOR if sep_ord == (1 << 63) - 1 else sep_ord
+    # 1. route: candidates to their hash owners
+    status, parts, sep_local, n_seps = store.route_begin(cost, mask, config.exhaustive, deadline, rank, world)
+    meta = _gather_ints([status, min(sep_local, _I64_MAX), n_seps] + [p[1].shape[0] for p in parts], device, group)
+    worst = max(m[0] for m in meta)
+    if worst != 0:  # a budget stop must be collective: every rank stops or none does
+        store.level_abort()
+        raise _BudgetExceeded(_FAILURE_TEXT.get(worst, "budget exhausted"))
+    recv_counts = [m[3 + rank] for m in meta]
+    n_records = sum(recv_counts)
+    recv_rows, recv_ords = store.exchange_recv(n_records)
+    _exchange(parts, (recv_rows, recv_ords), recv_counts, group, include_self=True)
+    # 2. reduce on the owner; its winners up to the separator (the min of the ranks' smallest separating ordinals)
+    sep_ord = min(m[1] for m in meta)
+    sep_ord = NO_SEPARATOR if sep_ord == _I64_MAX else sep_ord
+    status, bitmap = store.owner_reduce(n_records)
+    win_rows = win_ords = None
+    if status == 0:
+        win_rows, win_ords = store.winners_export(sep_ord)
+    counts = _gather_ints([status, 0 if win_ords is None else win_ords.shape[0]], device, group)
+    worst = max(c[0] for c in counts)
+    if worst != 0:  # an owner ran out of device memory
+        store.level_abort()
+        raise _BudgetExceeded(_FAILURE_TEXT.get(worst, "budget exhausted"))
+    # 3. rank: the union of the owners' winners bitmaps (disjoint bits: a sum)
+    dist.all_reduce(bitmap, op=dist.ReduceOp.SUM, group=group)
+    # 4. publish: every owner's winners to every other rank
+    seps_mine = store.separating_ordinals() if config.exhaustive else None
+    win_counts = [0 if r == rank else counts[r][1] for r in range(world)]
+    n_received = sum(win_counts)
+    recv_rows, recv_ords = store.exchange_recv(n_received)
+    _exchange([(win_rows, win_ords)] * world, (recv_rows, recv_ords), win_counts, group, include_self=False)
     seps = None
-    if config.exhaustive:
-        seps = _all_gather_v(store.separating_ordinals(), group)
-    status, n_new, sep_gid, delta = store.level_end(sep_ord, seps, config.batch_size, config.memory_budget_mb << 20)
+    if config.exhaustive:  # every separating ordinal of the level, for the reference's chunk-exact separator id
+        sep_counts = [m[2] for m in meta]
+        seps = torch.empty((sum(sep_counts),), dtype=torch.int64, device=device)
+        _exchange([(seps_mine,)] * world, (seps,), sep_counts, group, include_self=True)
+    status, n_new, sep_gid, delta = store.level_commit(sep_ord, seps, n_received, config.batch_size,
+                                                       config.memory_budget_mb << 20)
+    flag = torch.tensor([status], dtype=torch.int64, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)  # (a rank whose device filled up while appending)
     stats.constructed += delta
     stats.unique = store.total
-    if status in _FAILURE_TEXT:
-        raise _BudgetExceeded(_FAILURE_TEXT[status])
+    if int(flag.item()) in _FAILURE_TEXT:
+        raise _BudgetExceeded(_FAILURE_TEXT[int(flag.item())])
     return n_new, sep_gid
-
-
-def _gloo_counts(recv_t, counts_t, group):
-    world = dist.get_world_size(group)
-    parts = [torch.empty_like(counts_t) for _ in range(world)]
-    dist.all_gather(parts, counts_t, group=group)
-    rank = dist.get_rank(group)
-    for peer in range(world):
-        recv_t[peer] = parts[peer][rank]
 
 
 def _device_of(store) -> torch.device:
@@ -219,7 +217,11 @@ def synthesize_sharded(spec, config: EngineConfig = EngineConfig(), group=None, 
     validate_feasible(spec)
     ops = normalize_operators(config.operators)
     t0 = time.perf_counter()
-    store = store_factory(spec) if store_factory else CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb)
+    if store_factory:
+        store = store_factory(spec)
+    else:  # on torch's current stream: the collectives and the engine's kernels are then ordered without host waits
+        store = CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb,
+                               stream=torch.cuda.current_stream(torch.device("cuda", config.device)).cuda_stream)
     try:
         stats = RunStats()
         deadline = t0 + config.time_budget_s
@@ -236,13 +238,15 @@ def synthesize_sharded(spec, config: EngineConfig = EngineConfig(), group=None, 
                 if not config.exhaustive:
                     break
         stats.elapsed_s = time.perf_counter() - t0
+        device_stats = store.device_stats() if hasattr(store, "device_stats") else None
         if found is None:
-            return SynthesisResult(None, None, False, OUTCOME_EXHAUSTED, stats, failure)
+            return SynthesisResult(None, None, False, OUTCOME_EXHAUSTED, stats, failure, device_stats)
         formula = reconstruct(store, found[0])
+        device_stats = store.device_stats() if hasattr(store, "device_stats") else None
     finally:
         close = getattr(store, "close", None)
         if close:
             close()
     if not semantics.separates_by_sat(spec, formula):
         raise RuntimeError("internal error: synthesized formula fails the reference semantics")
-    return SynthesisResult(formula, found[1], True, OUTCOME_FOUND, stats)
+    return SynthesisResult(formula, found[1], True, OUTCOME_FOUND, stats, None, device_stats)

@@ -110,6 +110,9 @@ class SynthesisResult:
     outcome: str
     stats: RunStats
     failure: str | None = None
+    # beyond the reference's fields: counters of the device handle that ran the search (ltlb200_stats: bytes copied
+    # host<->device, kernel launches, device time of the construction kernels, ...)
+    device_stats: dict | None = None
 
 
 class _Level:
@@ -130,6 +133,13 @@ class _Level:
     right = property(lambda self: self._fetch()[3])
 
 
+class _DeviceMemory:
+    """``__cuda_array_interface__`` face of a device buffer the engine owns (for ``torch.as_tensor``)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr), False), "version": 2}
+
+
 class CandidateStore:
     """Cost-indexed cache of unique CMs with provenance, resident on the GPU."""
 
@@ -142,6 +152,7 @@ class CandidateStore:
         self.key_words = -(-(self.trace_count * self.dtype.itemsize) // 8)
         self.levels: list[_Level] = []
         self._device = int(device)
+        self._stream = int(stream or 0)
         lib = _native.load()
         if lib.ltlb200_device_count() < 1:
             raise _native.NativeEngineError("no usable B200: " + _native.last_error())
@@ -239,51 +250,89 @@ class CandidateStore:
 
         return torch.device("cuda", self._device)
 
-    def level_begin(self, cost, op_mask, exhaustive, deadline, shard_index, shard_count):
-        """Enumerate this rank's shard of level ``cost``; ``deadline`` is on ``time.perf_counter()``."""
-        n_claimed, sep_ord, n_seps = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    # routed level of a sharded search (dist.sharded_expand_level; protocol in include/ltlsynth_b200.h)
+    def _tensor(self, ptr: int, shape, dtype):
+        """torch view of device memory the engine owns (zero copy; valid until the engine reuses the buffer)."""
+        import torch
+
+        count = 1
+        for d in shape:
+            count *= d
+        if count == 0 or not ptr:
+            return torch.empty(shape, dtype=dtype, device=self.torch_device)
+        typestr = {torch.uint8: "|u1", torch.int64: "<i8", torch.int32: "<i4"}[dtype]
+        return torch.as_tensor(_DeviceMemory(ptr, tuple(shape), typestr), device=self.torch_device)
+
+    def _wait_for_torch(self):
+        """The collectives ran on torch's current stream; unless that is the engine's stream, wait for them."""
+        import torch
+
+        stream = torch.cuda.current_stream(self.torch_device)
+        if stream.cuda_stream != (self._stream or -1):
+            stream.synchronize()
+
+    def route_begin(self, cost, op_mask, exhaustive, deadline, rank, world):
+        """Build this rank's share of level ``cost`` and route its candidates to their hash owners;
+        ``deadline`` is on ``time.perf_counter()``.  -> (status, parts, sep_ord, n_seps)."""
+        import torch
+
+        counts, offsets = (ctypes.c_uint64 * world)(), (ctypes.c_uint64 * world)()
+        rows_ptr, ords_ptr = ctypes.c_void_p(), ctypes.c_void_p()
+        sep_ord, n_seps = ctypes.c_uint64(), ctypes.c_uint64()
         native_deadline = -1.0 if deadline is None else _monotonic() + (deadline - time.perf_counter())
         status = _native.check(
-            _native.load().ltlb200_level_begin(self._handle, cost, op_mask, int(exhaustive), native_deadline,
-                                               shard_index, shard_count, ctypes.byref(n_claimed),
+            _native.load().ltlb200_route_begin(self._handle, cost, op_mask, int(exhaustive), native_deadline, rank, world,
+                                               counts, offsets, ctypes.byref(rows_ptr), ctypes.byref(ords_ptr),
                                                ctypes.byref(sep_ord), ctypes.byref(n_seps)),
-            f"level_begin({cost})",
+            f"route_begin({cost})",
         )
         self._pending_seps = n_seps.value
+        kb = self.key_bytes
+        parts = []
+        for o in range(world):
+            n, off = int(counts[o]), int(offsets[o])
+            parts.append((self._tensor((rows_ptr.value or 0) + off * kb, (n, kb), torch.uint8),
+                          self._tensor((ords_ptr.value or 0) + off * 8, (n,), torch.int64)))
         if status != _native.OK:  # the level was closed (empty) by the engine
             self.levels.append(_Level(self, cost, 0, self.total))
-        return status, n_claimed.value, sep_ord.value, n_seps.value
+        return status, parts, sep_ord.value, n_seps.value
 
-    def claims_count(self, owners: int) -> list[int]:
-        counts = (ctypes.c_uint64 * owners)()
-        _native.check(_native.load().ltlb200_claims_count(self._handle, owners, counts), "claims_count")
-        return [int(c) for c in counts]
-
-    def claims_pack(self, owners: int, total: int):
+    def exchange_recv(self, n_records: int):
         import torch
 
-        rows = torch.empty((total, self.key_bytes), dtype=torch.uint8, device=self.torch_device)
-        ords = torch.empty((total,), dtype=torch.int64, device=self.torch_device)
-        _native.check(
-            _native.load().ltlb200_claims_pack(self._handle, owners, ctypes.c_void_p(rows.data_ptr()),
-                                               ctypes.c_void_p(ords.data_ptr())),
-            "claims_pack",
-        )
-        return rows, ords
+        rows_ptr, ords_ptr = ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(_native.load().ltlb200_exchange_recv(self._handle, int(n_records), ctypes.byref(rows_ptr),
+                                                           ctypes.byref(ords_ptr)), "exchange_recv")
+        return (self._tensor(rows_ptr.value, (n_records, self.key_bytes), torch.uint8),
+                self._tensor(ords_ptr.value, (n_records,), torch.int64))
 
-    def claims_import(self, rows, ords) -> None:
+    def owner_reduce(self, n_records: int):
         import torch
 
-        n = int(ords.shape[0])
-        if n == 0:
-            return
-        rows, ords = rows.contiguous(), ords.contiguous()
-        torch.cuda.current_stream(self.torch_device).synchronize()  # NCCL wrote these on torch's stream
-        _native.check(
-            _native.load().ltlb200_claims_import(self._handle, ctypes.c_void_p(rows.data_ptr()),
-                                                 ctypes.c_void_p(ords.data_ptr()), n),
-            "claims_import",
-        )
+        self._wait_for_torch()
+        n_claimed, words, bitmap_ptr = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_void_p()
+        status = _native.check(
+            _native.load().ltlb200_owner_reduce(self._handle, int(n_records), ctypes.byref(n_claimed),
+                                                ctypes.byref(bitmap_ptr), ctypes.byref(words)), "owner_reduce")
+        if status != _native.OK:
+            self.levels.append(_Level(self, len(self.levels) + 1, 0, self.total))
+            return status, None
+        return status, self._tensor(bitmap_ptr.value, (int(words.value),), torch.int32)
+
+    def winners_export(self, sep_ord: int):
+        import torch
+
+        n, rows_ptr, ords_ptr = ctypes.c_uint64(), ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(_native.load().ltlb200_winners_export(self._handle, int(sep_ord), ctypes.byref(n),
+                                                            ctypes.byref(rows_ptr), ctypes.byref(ords_ptr)), "winners_export")
+        return (self._tensor(rows_ptr.value, (int(n.value), self.key_bytes), torch.uint8),
+                self._tensor(ords_ptr.value, (int(n.value),), torch.int64))
+
+    def level_abort(self) -> None:
+        had = _native.load().ltlb200_num_levels(self._handle)
+        _native.check(_native.load().ltlb200_level_abort(self._handle), "level_abort")
+        if _native.load().ltlb200_num_levels(self._handle) > had:
+            self.levels.append(_Level(self, len(self.levels) + 1, 0, self.total))
 
     def separating_ordinals(self):
         import torch
@@ -294,17 +343,18 @@ class CandidateStore:
         _native.check(int(got), "seps_copy")
         return torch.from_numpy(host[: int(got)].astype(np.int64)).to(self.torch_device)
 
-    def level_end(self, sep_ord, seps, batch_size, memory_budget_bytes):
+    def level_commit(self, sep_ord, seps, n_received, batch_size, memory_budget_bytes):
+        self._wait_for_torch()
         n_new, sep, delta = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         seps_ptr, n_seps = None, 0
         if seps is not None:
             host = np.ascontiguousarray(seps.detach().cpu().numpy().astype(np.uint64))
             seps_ptr, n_seps = host.ctypes.data, len(host)
         status = _native.check(
-            _native.load().ltlb200_level_end(self._handle, int(sep_ord), seps_ptr, n_seps, int(batch_size),
-                                             int(memory_budget_bytes), ctypes.byref(n_new), ctypes.byref(sep),
-                                             ctypes.byref(delta)),
-            "level_end",
+            _native.load().ltlb200_level_commit(self._handle, int(sep_ord), seps_ptr, n_seps, int(n_received),
+                                                int(batch_size), int(memory_budget_bytes), ctypes.byref(n_new),
+                                                ctypes.byref(sep), ctypes.byref(delta)),
+            "level_commit",
         )
         self.levels.append(_Level(self, len(self.levels) + 1, n_new.value, self.total))
         return status, n_new.value, (None if sep.value < 0 else sep.value), delta.value
@@ -387,10 +437,11 @@ def synthesize(spec: Specification, config: EngineConfig = EngineConfig()) -> Sy
                     break
         stats.elapsed_s = time.perf_counter() - t0
         if found is None:
-            return SynthesisResult(None, None, False, OUTCOME_EXHAUSTED, stats, failure)
+            return SynthesisResult(None, None, False, OUTCOME_EXHAUSTED, stats, failure, store.device_stats())
         formula = reconstruct(store, found[0])
+        device_stats = store.device_stats()
     finally:
         store.close()
     if not semantics.separates_by_sat(spec, formula):
         raise RuntimeError("internal error: synthesized formula fails the reference semantics")
-    return SynthesisResult(formula, found[1], True, OUTCOME_FOUND, stats)
+    return SynthesisResult(formula, found[1], True, OUTCOME_FOUND, stats, None, device_stats)

@@ -41,6 +41,7 @@ class CpuShardEngine:
         self.key_bytes = -(-self.row_bytes // 16) * 16
         self.levels: list[_Level] = []
         self.seen: set[bytes] = set()
+        self.has_separator = False
         self.torch_device = torch.device("cpu")
         self._pending = None
 
@@ -153,15 +154,12 @@ class CpuShardEngine:
     def _key(self, row) -> bytes:
         return row.tobytes().ljust(self.key_bytes, b"\0")
 
-    # ---- shard-engine interface --------------------------------------------------------------
-    def level_begin(self, cost, op_mask, exhaustive, deadline, shard_index, shard_count):
+    # ---- shard-engine interface (paper_2504_18943_b200.dist.ShardEngine) -------------------------------------
+    def _enumerate(self, cost, op_mask, shard_index, shard_count):
+        """(blocks, constructed, candidate rows, ordinals) of this shard: ordinals strided over the ranks."""
         blocks, constructed = self._blocks(cost, op_mask)
-        claims: dict[bytes, int] = {}
-        sep_local, seps = NO_SEPARATOR, []
-        target = self.layout.target
+        rows, ords = [], []
         for b in blocks:
-            local = np.arange(shard_index, b["size"], shard_count, dtype=np.int64)
-            # keep the global ordinal stride aligned: shard by (ord0 + local) % shard_count
             local = np.arange(b["size"], dtype=np.int64)
             local = local[(b["ord0"] + local) % shard_count == shard_index]
             if not len(local):
@@ -173,63 +171,88 @@ class CpuShardEngine:
             else:
                 lb = b["la"] if b["kind"] == "tri" else b["lb"]
                 cand = self._apply(b["op"], b["la"].cms[i], lb.cms[j])
-            sep_flags = ((cand & self.dtype.type(1)) == target).all(axis=1)
-            for k in range(len(local)):
-                ordinal = int(b["ord0"] + local[k])
-                key = self._key(cand[k])
-                fresh = key not in self.seen
-                if fresh and ordinal < claims.get(key, NO_SEPARATOR):
-                    claims[key] = ordinal
-                if sep_flags[k]:
-                    seps.append(ordinal)
-                    if fresh:
-                        sep_local = min(sep_local, ordinal)
-        self._pending = dict(cost=cost, blocks=blocks, constructed=constructed, claims=claims, seps=seps,
-                             exhaustive=exhaustive)
-        return 0, len(claims), sep_local, len(seps)
-
-    def level_candidates(self, cost, op_mask):
-        return self._blocks(cost, op_mask)[1]
-
-    def expand_local(self, cost, op_mask, exhaustive, batch_size, memory_budget_bytes, deadline):
-        """The whole level on this rank: what dist.py does for levels below REPLICATE_BELOW."""
-        _, _, sep_local, _ = self.level_begin(cost, op_mask, exhaustive, deadline, 0, 1)
-        seps = torch.tensor(self._pending["seps"], dtype=torch.int64) if exhaustive else None
-        return self.level_end(sep_local, seps, batch_size, memory_budget_bytes)
+            rows.append(cand)
+            ords.append(b["ord0"] + local)
+        if rows:
+            return blocks, constructed, np.concatenate(rows), np.concatenate(ords)
+        return blocks, constructed, np.empty((0, self.T), dtype=self.dtype), np.empty(0, dtype=np.int64)
 
     def _owner(self, key: bytes, owners: int) -> int:
         return zlib.crc32(key) % owners
 
-    def claims_count(self, owners):
-        counts = [0] * owners
-        for key in self._pending["claims"]:
-            counts[self._owner(key, owners)] += 1
-        return counts
-
-    def claims_pack(self, owners, total):
-        items = sorted(self._pending["claims"].items(), key=lambda kv: (self._owner(kv[0], owners), kv[0]))
+    def _records(self, items):
+        """(rows uint8 [n, key_bytes], ords int64 [n]) tensors of (key, ordinal) pairs."""
         rows = np.frombuffer(b"".join(k for k, _ in items), dtype=np.uint8).reshape(len(items), self.key_bytes).copy() \
             if items else np.empty((0, self.key_bytes), dtype=np.uint8)
-        ords = np.array([v for _, v in items], dtype=np.int64)
-        assert len(items) == total
-        return torch.from_numpy(rows), torch.from_numpy(ords)
+        return torch.from_numpy(rows), torch.from_numpy(np.array([o for _, o in items], dtype=np.int64))
 
-    def claims_import(self, rows, ords):
-        claims = self._pending["claims"]
-        raw = rows.numpy()
+    def route_begin(self, cost, op_mask, exhaustive, deadline, rank, world):
+        blocks, constructed, cand, ords = self._enumerate(cost, op_mask, rank, world)
+        sep_flags = ((cand & self.dtype.type(1)) == self.layout.target).all(axis=1) if len(cand) else np.zeros(0, bool)
+        seps = [int(o) for o in ords[sep_flags]]
+        # while the store holds no separating CM, a separating candidate cannot repeat an older CM
+        sep_local = min(seps) if seps and not self.has_separator else NO_SEPARATOR
+        per_owner = [[] for _ in range(world)]
         for k in range(len(ords)):
-            key = raw[k].tobytes()
-            o = int(ords[k])
-            if o < claims.get(key, NO_SEPARATOR):
+            key = self._key(cand[k])
+            per_owner[self._owner(key, world)].append((key, int(ords[k])))
+        self._pending = dict(cost=cost, blocks=blocks, constructed=constructed, seps=seps, exhaustive=exhaustive,
+                             rank=rank, world=world, claims={}, recv=None, bitmap=None)
+        return 0, [self._records(items) for items in per_owner], sep_local, len(seps)
+
+    def exchange_recv(self, n_records):
+        rows = torch.empty((n_records, self.key_bytes), dtype=torch.uint8)
+        ords = torch.empty((n_records,), dtype=torch.int64)
+        self._pending["recv"] = (rows, ords)
+        return rows, ords
+
+    def owner_reduce(self, n_records):
+        p = self._pending
+        rows, ords = p["recv"]
+        raw, claims = rows.numpy(), p["claims"]
+        for k in range(n_records):
+            key, o = raw[k].tobytes(), int(ords[k])
+            assert self._owner(key, p["world"]) == p["rank"], "a record reached a rank that does not own it"
+            if key not in self.seen and o < claims.get(key, NO_SEPARATOR):
                 claims[key] = o
+        words = np.zeros((p["constructed"] + 31) // 32 + 1, dtype=np.uint32)
+        for o in claims.values():
+            words[o >> 5] |= np.uint32(1 << (o & 31))
+        p["bitmap"] = torch.from_numpy(words.view(np.int32))
+        return 0, p["bitmap"]
+
+    def winners_export(self, sep_ord):
+        p = self._pending
+        cut = (not p["exhaustive"]) and sep_ord != NO_SEPARATOR
+        p["winners"] = [(k, o) for k, o in p["claims"].items() if not cut or o <= sep_ord]
+        return self._records(p["winners"])
+
+    def level_abort(self):
+        if self._pending is not None:
+            self.levels.append(_Level(np.empty((0, self.T), dtype=self.dtype), np.empty(0, np.uint8), np.empty(0, np.int64),
+                                      np.empty(0, np.int64), self.total))
+            self._pending = None
 
     def separating_ordinals(self):
         return torch.tensor(self._pending["seps"], dtype=torch.int64)
 
-    def level_end(self, sep_ord, seps, batch_size, memory_budget_bytes):
+    def level_commit(self, sep_ord, seps, n_received, batch_size, memory_budget_bytes):
         p = self._pending
+        rows, ords = p["recv"] if n_received else (None, None)
+        items = [(o, k) for k, o in p["winners"]]
+        for k in range(n_received):
+            items.append((int(ords[k]), rows[k].numpy().tobytes()))
+        items.sort()
+        # the all-reduced bitmap is the level's winners: one bit per entry, at its ordinal
+        bits = p["bitmap"].numpy().view(np.uint32)
         cut = (not p["exhaustive"]) and sep_ord != NO_SEPARATOR
-        items = sorted((o, k) for k, o in p["claims"].items() if not cut or o <= sep_ord)
+        marked = [o for o in np.flatnonzero(np.unpackbits(bits.view(np.uint8), bitorder="little")) if not cut or o <= sep_ord]
+        assert marked == [o for o, _ in items], "winners bitmap and published winners disagree"
+        if sep_ord != NO_SEPARATOR or (seps is not None and len(seps)):
+            self.has_separator = True
+        return self._append(p, items, sep_ord)
+
+    def _append(self, p, items, sep_ord):
         ords = np.array([o for o, _ in items], dtype=np.int64)
         base = self.total
         if items:
@@ -248,3 +271,25 @@ class CpuShardEngine:
                 sep_gid = base + pos
         self._pending = None
         return 0, len(items), sep_gid, p["constructed"]
+
+    def level_candidates(self, cost, op_mask):
+        return self._blocks(cost, op_mask)[1]
+
+    def expand_local(self, cost, op_mask, exhaustive, batch_size, memory_budget_bytes, deadline):
+        """The whole level on this rank: what dist.py does for levels below REPLICATE_BELOW."""
+        blocks, constructed, cand, ords = self._enumerate(cost, op_mask, 0, 1)
+        claims: dict[bytes, int] = {}
+        sep_flags = ((cand & self.dtype.type(1)) == self.layout.target).all(axis=1) if len(cand) else np.zeros(0, bool)
+        sep_ord = NO_SEPARATOR
+        for k in range(len(ords)):
+            key, o = self._key(cand[k]), int(ords[k])
+            fresh = key not in self.seen
+            if fresh and o < claims.get(key, NO_SEPARATOR):
+                claims[key] = o
+            if sep_flags[k]:
+                self.has_separator = True
+                if fresh:
+                    sep_ord = min(sep_ord, o)
+        cut = (not exhaustive) and sep_ord != NO_SEPARATOR
+        items = sorted((o, k) for k, o in claims.items() if not cut or o <= sep_ord)
+        return self._append(dict(blocks=blocks, constructed=constructed), items, sep_ord)

@@ -1,4 +1,4 @@
-"""GPU tests of the sharded-search primitives of the C ABI (level_begin / claims_* / level_end).
+"""GPU tests of the sharded-search primitives of the C ABI (route_begin / owner_reduce / winners_export / level_commit).
 
 Only one GPU is available to the test run, so two stores on the same device play two ranks
 and the test moves the exchange records between them by hand, step for step as
@@ -21,38 +21,46 @@ NO_SEP = (1 << 64) - 1
 
 
 def _exchange_level(stores, cost, cfg):
+    """dist.sharded_expand_level with the collectives done by hand between stores on one device."""
     world = len(stores)
     mask = engine.operator_mask(cfg.operators)
-    begun = [s.level_begin(cost, mask, cfg.exhaustive, None, r, world) for r, s in enumerate(stores)]
+    # 1. route
+    begun = [s.route_begin(cost, mask, cfg.exhaustive, None, r, world) for r, s in enumerate(stores)]
     assert all(b[0] == 0 for b in begun)
-    # 1. route to owners
-    packed = []
-    for s in stores:
-        counts = s.claims_count(world)
-        rows, ords = s.claims_pack(world, sum(counts))
-        packed.append((counts, rows, ords))
-    for owner, s in enumerate(stores):
-        rows_in, ords_in = [], []
-        for counts, rows, ords in packed:
-            lo = sum(counts[:owner])
-            rows_in.append(rows[lo:lo + counts[owner]])
-            ords_in.append(ords[lo:lo + counts[owner]])
-        s.claims_import(torch.cat(rows_in), torch.cat(ords_in))  # 2. owner reduces
-    # 3. owners publish
-    winners_rows, winners_ords = [], []
-    for owner, s in enumerate(stores):
-        counts = s.claims_count(world)
-        rows, ords = s.claims_pack(world, sum(counts))
-        lo = sum(counts[:owner])
-        winners_rows.append(rows[lo:lo + counts[owner]])
-        winners_ords.append(ords[lo:lo + counts[owner]])
-    all_rows, all_ords = torch.cat(winners_rows), torch.cat(winners_ords)
-    for s in stores:
-        s.claims_import(all_rows, all_ords)
-    # 4. separator
+    for owner, s in enumerate(stores):  # "all-to-all": what every rank built for this owner, source-major
+        counts = [begun[src][1][owner][1].shape[0] for src in range(world)]
+        rows, ords = s.exchange_recv(sum(counts))
+        at = 0
+        for src in range(world):
+            part_rows, part_ords = begun[src][1][owner]
+            rows[at:at + counts[src]].copy_(part_rows)
+            ords[at:at + counts[src]].copy_(part_ords)
+            at += counts[src]
+    torch.cuda.synchronize()
     sep = min(b[2] for b in begun)
+    # 2. reduce, 3. rank ("all-reduce": sum of the owners' bitmaps)
+    reduced = [s.owner_reduce(sum(begun[src][1][owner][1].shape[0] for src in range(world))) for owner, s in enumerate(stores)]
+    assert all(r[0] == 0 for r in reduced)
+    winners = [s.winners_export(sep) for s in stores]
+    total = sum(r[1] for r in reduced)
+    for _, bitmap in reduced:
+        bitmap.copy_(total)
+    # 4. publish ("all-gather": the winners of the other owners)
+    received = []
+    for r, s in enumerate(stores):
+        others = [winners[o] for o in range(world) if o != r]
+        n = sum(w[1].shape[0] for w in others)
+        rows, ords = s.exchange_recv(n)
+        at = 0
+        for w_rows, w_ords in others:
+            k = w_ords.shape[0]
+            rows[at:at + k].copy_(w_rows)
+            ords[at:at + k].copy_(w_ords)
+            at += k
+        received.append(n)
+    torch.cuda.synchronize()
     seps = torch.cat([s.separating_ordinals() for s in stores]) if cfg.exhaustive else None
-    return [s.level_end(sep, seps, cfg.batch_size, 0) for s in stores]
+    return [s.level_commit(sep, seps, received[r], cfg.batch_size, 0) for r, s in enumerate(stores)]
 
 
 @pytest.mark.parametrize("workload,seed,max_cost,exhaustive,world", [
@@ -62,6 +70,10 @@ def _exchange_level(stores, cost, cfg):
     ("c5", 0, 7, True, 2),       # 128-byte rows
     ("c3wide", 0, 7, True, 2),   # 80-byte rows (5 vectors in groups of 8 lanes)
     ("c1", 1, 14, False, 2),
+    ("c3", 1, 11, True, 8),      # the most ranks a route kernel stages for
+    ("w64n", 0, 9, True, 4),     # 64-bit lanes
+    ("c3", 0, 13, True, 2),      # 12 M candidates in the last level: big route regions, probe kernel at scale
+    ("spec2", 0, 14, False, 3),  # non-exhaustive, no separator up to here
 ])
 def test_shards_on_one_gpu_agree_with_oracle(workload, seed, max_cost, exhaustive, world):
     spec = workloads.named_workload(workload, seed)

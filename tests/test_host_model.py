@@ -183,3 +183,35 @@ def test_fast_witness_check_agrees_with_the_quantifier_semantics():
         tr = Trace(tuple(frozenset(p for p in range(3) if rng.random() < 0.5) for _ in range(length)))
         f = formula(rng.randint(1, 5))
         assert semantics._truth_table_fast(tr, f) == semantics._truth_table(tr, f), (tr, f)
+
+
+def test_bench_gpus_flag_starts_that_many_ranks():
+    """`bench.py --gpus 2` outside torchrun must START two processes (it silently measured one).  No GPU
+    here, so the launch path is exercised with --selftest-cpu: gloo + the numpy shard engine run the sharded protocol."""
+    import json
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parent.parent
+    proc = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--selftest-cpu"], capture_output=True,
+                          text=True, timeout=300)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-2000:]
+    line = json.loads([ln for ln in proc.stdout.splitlines() if ln.startswith("{")][-1])
+    assert (line["n_gpus"], line["processes"], line["witness"], line["unique_per_step"]) == (2, 2, "!(b U a)", 33)
+
+
+def test_bench_reference_arm_runs_the_cpu_enumerator_on_the_gpu_arms_config():
+    import json
+    import pathlib
+    import subprocess
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parent.parent
+    proc = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--workload", "spec1", "--steps", "1",
+                           "--warmup", "0"], capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    line = json.loads(proc.stdout.splitlines()[-1])
+    assert line["impl"] == "reference" and line["config"]["max_cost"] == 10 and line["config"]["workload"] == "spec1"
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    assert "233 unique" in line["cpu_baseline"]["sample"]
