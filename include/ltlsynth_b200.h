@@ -207,6 +207,13 @@ int32_t ltlb200_num_levels(const ltlb200_engine *e);
 int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t count, uint8_t *cms,
                        uint8_t *op, int64_t *left, int64_t *right);
 
+/*
+ * _Level.cms where it lives: DEVICE pointers to the level's rows (ltlb200_key_bytes bytes each: the numpy row image
+ * zero padded to 16-byte vectors) and to the ordinal each entry won with, for consumers that stay on the GPU.
+ * Valid until the next level is built or the handle is reset / destroyed; NULL for an empty level.
+ */
+int ltlb200_level_device(ltlb200_engine *e, int32_t cost, void **rows_dev, void **ords_dev);
+
 /* CandidateStore.entry (engine.py:140-145): provenance of one global id. */
 int ltlb200_entry(ltlb200_engine *e, int64_t gid, int32_t *op, int64_t *left, int64_t *right);
 

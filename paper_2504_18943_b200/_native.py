@@ -43,6 +43,7 @@ EXPORTED_SYMBOLS = (
     "ltlb200_holds_separator",
     "ltlb200_num_levels",
     "ltlb200_level_copy",
+    "ltlb200_level_device",
     "ltlb200_entry",
     "ltlb200_approx_bytes",
     "ltlb200_get_stats",
@@ -140,6 +141,8 @@ def load():
     L.ltlb200_num_levels.argtypes = [p]
     L.ltlb200_level_copy.restype = ctypes.c_int
     L.ltlb200_level_copy.argtypes = [p, i32, i64, i64, p, p, p, p]
+    L.ltlb200_level_device.restype = ctypes.c_int
+    L.ltlb200_level_device.argtypes = [p, i32, pp, pp]
     L.ltlb200_entry.restype = ctypes.c_int
     L.ltlb200_entry.argtypes = [p, i64, ctypes.POINTER(i32), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.ltlb200_approx_bytes.restype = u64

@@ -328,6 +328,7 @@ public:
     int level_info(int cost, int64_t *n, int64_t *base) const;
     int64_t level_candidates(int cost, uint32_t op_mask);
     int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
+    int level_device(int cost, void **rows_dev, void **ords_dev);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
     void reset();
@@ -1208,7 +1209,12 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         if (constructed > kExact) {
             double u = 1.0;
             if (levels_.size() >= 2 && last_constructed_ > 0) u = std::min(1.0, 1.5 * (double)levels_.back().n / (double)last_constructed_ + 0.02);
-            est = std::min(constructed, std::max(kExact, (u64)(u * (double)constructed)));
+            // LTLB200_EST_SCALE (tests): scales the guess so that the overflow -> regrow -> redo path runs
+            static const double scale = [] {
+                const char *e = getenv("LTLB200_EST_SCALE");
+                return e ? atof(e) : 1.0;
+            }();
+            est = std::min(constructed, std::max(kExact, (u64)(scale * u * (double)constructed)));
         }
         for (int attempt = 0;; ++attempt) {
             const bool exact = est >= constructed;
@@ -2089,6 +2095,17 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
     return LTLB200_OK;
 }
 
+// the level where it lives: rows of key_bytes() bytes and winning ordinals, valid until the next level is built
+int Engine::level_device(int cost, void **rows_dev, void **ords_dev) {
+    if (cost < 1 || cost > (int)levels_.size()) return LTLB200_ERR_ARGUMENT;
+    CUDA_CHECK(cudaSetDevice(device_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    const LevelMeta &lv = levels_[cost - 1];
+    *rows_dev = lv.n ? (void *)(store_.ptr + lv.base * nvec_) : nullptr;
+    *ords_dev = lv.n ? (void *)(ords_.ptr + lv.base) : nullptr;
+    return LTLB200_OK;
+}
+
 int Engine::entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
     if (gid < 0 || (u64)gid >= total_) return LTLB200_ERR_ARGUMENT;
     size_t li = 0;
@@ -2300,6 +2317,11 @@ int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t c
                        int64_t *left, int64_t *right) {
     if (!e) return LTLB200_ERR_ARGUMENT;
     return guarded([&] { return e->impl->level_copy(cost, first, count, cms, op, left, right); });
+}
+
+int ltlb200_level_device(ltlb200_engine *e, int32_t cost, void **rows_dev, void **ords_dev) {
+    if (!e || !rows_dev || !ords_dev) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] { return e->impl->level_device(cost, rows_dev, ords_dev); });
 }
 
 int ltlb200_entry(ltlb200_engine *e, int64_t gid, int32_t *op, int64_t *left, int64_t *right) {

@@ -359,6 +359,25 @@ class CandidateStore:
         self.levels.append(_Level(self, len(self.levels) + 1, n_new.value, self.total))
         return status, n_new.value, (None if sep.value < 0 else sep.value), delta.value
 
+    def level_device(self, cost: int):
+        """Zero-copy torch views of level ``cost`` on the device: rows uint8 [n, key_bytes] (the numpy row image, zero
+        padded to 16-byte vectors) and the winning ordinals int64 [n].  Valid until the next level is built."""
+        import torch
+
+        rows_ptr, ords_ptr = ctypes.c_void_p(), ctypes.c_void_p()
+        _native.check(_native.load().ltlb200_level_device(self._handle, cost, ctypes.byref(rows_ptr), ctypes.byref(ords_ptr)),
+                      f"level_device({cost})")
+        n = self.level(cost).n
+        return (self._tensor(rows_ptr.value, (n, self.key_bytes), torch.uint8), self._tensor(ords_ptr.value, (n,), torch.int64))
+
+    def _copy_provenance(self, cost: int, n: int):
+        """(op, left, right) of a level without its CMs (full-size tests read the rows on the device)."""
+        op, left, right = np.empty(n, dtype=np.uint8), np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int64)
+        if n:
+            _native.check(_native.load().ltlb200_level_copy(self._handle, cost, 0, n, None, op.ctypes.data, left.ctypes.data,
+                                                            right.ctypes.data), f"level_copy({cost})")
+        return op, left, right
+
     def _copy_level(self, cost: int, n: int):
         cms = np.empty((n, self.trace_count), dtype=self.dtype)
         op = np.empty(n, dtype=np.uint8)

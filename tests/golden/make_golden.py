@@ -81,6 +81,8 @@ SLOW_CASES = [
     dict(name="spec2_found", workload="spec2", max_cost=16, exhaustive=False),
     dict(name="c3_s0_exh12", workload="c3", seed=0, max_cost=12, exhaustive=True),
     dict(name="c5_s0_exh10", workload="c5", seed=0, max_cost=10, exhaustive=True),
+    dict(name="c5_s0_exh11", workload="c5", seed=0, max_cost=11, exhaustive=True),          # 19.0 M CMs of 128 bytes
+    dict(name="c4-1024_s0_exh10", workload="c4-1024", seed=0, max_cost=10, exhaustive=True),  # 0.98 M CMs of 128 bytes
 ]
 
 
