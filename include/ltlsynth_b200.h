@@ -38,7 +38,10 @@ enum {
     LTLB200_OP_FUTURE = 3,
     LTLB200_OP_AND = 4,
     LTLB200_OP_UNTIL = 5,
-    LTLB200_OP_OR = 6
+    LTLB200_OP_OR = 6,
+    /* EXTENSION, not a reference tag: G ("globally"; SPEC.md:211 lists it as a non-goal).  Enabled only when bit 7
+     * of op_mask is set, which the Python face does only for EngineConfig(extended_grammar=True). */
+    LTLB200_OP_GLOBALLY = 7
 };
 
 /* status of ltlb200_expand_level; 1 and 2 are the reference's two _BudgetExceeded
@@ -73,6 +76,10 @@ typedef struct ltlb200_stats {
     double alloc_ms;             /* host time spent in device allocations */
     double rebuild_host_ms;      /* host time spent issuing hash-set regrows */
     double create_ms;            /* host time of ltlb200_create */
+    double route_ms;             /* sharded search: device time of the route kernels (phase A; also in enumerate_ms) */
+    double probe_ms;             /* sharded search: device time of the owner-side insert-or-min (phase B; also in enumerate_ms) */
+    uint64_t routed_records;     /* records this handle sent to hash owners */
+    uint64_t received_records;   /* records this handle folded into its part of the set */
 } ltlb200_stats;
 
 /* ABI version of the loaded library (== LTLB200_ABI_VERSION it was built with). */
@@ -97,6 +104,14 @@ int ltlb200_device_count(void);
 ltlb200_engine *ltlb200_create(int32_t trace_count, int32_t lane_bits, const uint64_t *masks,
                                const uint64_t *target, const uint64_t *atoms, int32_t n_atoms,
                                int32_t device, uint64_t hbm_budget_bytes, void *cuda_stream);
+
+/*
+ * EXTENSION (no reference counterpart: formulas.py:65-71 counts every node as 1; SPEC.md:315 calls the weights
+ * "config-extensible" without implementing them).  weights[k] = cost of one node of operator tag k (weights[0] = an
+ * atom), each in 1..64; cost level c then holds the formulas whose node weights add up to c.  Before the first
+ * level only.  All ones (the default) is the reference's cost.
+ */
+int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights);
 
 /* Frees every device allocation of the handle. */
 void ltlb200_destroy(ltlb200_engine *e);

@@ -38,7 +38,9 @@ _HERE = pathlib.Path(__file__).resolve().parent
 _LIB_PATH = _HERE / "_build" / "libltl_oracle.so"
 
 OP_ATOM, OP_NOT, OP_NEXT, OP_FUTURE, OP_AND, OP_UNTIL, OP_OR = range(7)
-_OP_BIT = {"not": OP_NOT, "next": OP_NEXT, "future": OP_FUTURE, "and": OP_AND, "until": OP_UNTIL, "or": OP_OR}
+OP_GLOBALLY = 7  # extension (see ltl_oracle.c's header): not in the reference
+_OP_BIT = {"not": OP_NOT, "next": OP_NEXT, "future": OP_FUTURE, "and": OP_AND, "until": OP_UNTIL, "or": OP_OR,
+           "globally": OP_GLOBALLY, "atom": OP_ATOM}
 _STATUS_FAILURE = {1: "time budget exhausted", 2: "memory budget exhausted"}
 
 
@@ -62,6 +64,8 @@ def lib():
         L.orc_create.restype = p
         L.orc_create.argtypes = [ctypes.c_int, ctypes.c_int, p, p, p, ctypes.c_int]
         L.orc_destroy.argtypes = [p]
+        L.orc_set_weights.restype = ctypes.c_int
+        L.orc_set_weights.argtypes = [p, p]
         L.orc_expand_level.restype = ctypes.c_int
         L.orc_expand_level.argtypes = [p, ctypes.c_int, ctypes.c_uint, ctypes.c_int, i64, i64, ctypes.c_double,
                                        ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
@@ -77,7 +81,7 @@ def lib():
 
 
 def op_mask(operators) -> int:
-    return sum(1 << _OP_BIT[name] for name in F.OPERATOR_NAMES if name in set(operators))
+    return sum(1 << _OP_BIT[name] for name in F.EXTENDED_OPERATOR_NAMES if name in set(operators))
 
 
 @dataclass
@@ -96,7 +100,7 @@ class OracleLevel:
 class OracleStore:
     """Reference-shaped candidate store backed by the C oracle."""
 
-    def __init__(self, spec: Specification, dtype=None):
+    def __init__(self, spec: Specification, dtype=None, operator_weights: dict | None = None):
         self.spec = spec
         self.dtype = np.dtype(dtype) if dtype is not None else smallest_lane_dtype(spec.max_length)
         self.layout = Layout.from_specification(spec, self.dtype)
@@ -110,6 +114,12 @@ class OracleStore:
                                    target.ctypes.data, atoms.ctypes.data, spec.alphabet.n)
         if not self._h:
             raise RuntimeError("orc_create failed")
+        if operator_weights:  # extension
+            vec = [1] * 8
+            for name, value in operator_weights.items():
+                vec[_OP_BIT[name]] = int(value)
+            if lib().orc_set_weights(self._h, (ctypes.c_int * 8)(*vec)) != 0:
+                raise ValueError("bad operator weights")
         self.n_levels = 0
         self._cache: dict[int, OracleLevel] = {}
 
@@ -172,8 +182,8 @@ def reconstruct(store, gid: int) -> F.Formula:
     tag, left, right = store.entry(gid)
     if tag == OP_ATOM:
         return F.Atom(left)
-    if tag in (OP_NOT, OP_NEXT, OP_FUTURE):
-        return {OP_NOT: F.Not, OP_NEXT: F.Next, OP_FUTURE: F.Future}[tag](reconstruct(store, left))
+    if tag in (OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY):
+        return {OP_NOT: F.Not, OP_NEXT: F.Next, OP_FUTURE: F.Future, OP_GLOBALLY: F.Globally}[tag](reconstruct(store, left))
     node = {OP_AND: F.And, OP_UNTIL: F.Until, OP_OR: F.Or}[tag]
     return node(reconstruct(store, left), reconstruct(store, right))
 
@@ -193,13 +203,13 @@ class OracleResult:
 
 
 def synthesize(spec: Specification, operators=F.DEFAULT_OPERATORS, max_cost=20, time_budget_s=300.0,
-               memory_budget_mb=8192, batch_size=1 << 16, exhaustive=False) -> OracleResult:
+               memory_budget_mb=8192, batch_size=1 << 16, exhaustive=False, operator_weights: dict | None = None) -> OracleResult:
     """Level loop of the reference's ``synthesize`` (engine.py:454-506) over the C oracle."""
     validate_feasible(spec)
-    unknown = set(operators) - set(F.OPERATOR_NAMES)
+    unknown = set(operators) - set(F.EXTENDED_OPERATOR_NAMES)
     if unknown:
         raise ValueError(f"unknown operators: {sorted(unknown)}")
-    store = OracleStore(spec)
+    store = OracleStore(spec, operator_weights=operator_weights)
     t0 = time.perf_counter()
     deadline = lib().orc_now() + time_budget_s
     constructed, reached, found_gid, found_cost, failure = 0, 0, None, None, None
@@ -228,27 +238,29 @@ def synthesize(spec: Specification, operators=F.DEFAULT_OPERATORS, max_cost=20, 
 # ---- dedup-free brute force (reference oracle.py:67-109), for minimality checks on tiny specs
 
 
-def enumerate_formulas(n_atoms: int, operators=F.DEFAULT_OPERATORS, max_cost: int = 6):
+def enumerate_formulas(n_atoms: int, operators=F.DEFAULT_OPERATORS, max_cost: int = 6, operator_weights: dict | None = None):
+    """Every formula tree by ascending cost, no dedup (reference oracle.py:67-93).  ``operator_weights`` / the operator
+    ``globally`` are the extension: a node of operator ``name`` costs ``operator_weights.get(name, 1)``."""
     enabled = set(operators)
+    w = lambda name: int((operator_weights or {}).get(name, 1))
     by_cost: list[list] = [[]]
     for c in range(1, max_cost + 1):
         here = []
-        if c == 1:
+        if c == w("atom"):
             here = [F.Atom(i) for i in range(n_atoms)]
-        else:
-            for name, node in (("not", F.Not), ("next", F.Next), ("future", F.Future)):
-                if name in enabled:
-                    here += [node(g) for g in by_cost[c - 1]]
-            for name, node in (("and", F.And), ("until", F.Until), ("or", F.Or)):
-                if name in enabled:
-                    for c1 in range(1, c - 1):
-                        here += [node(a, b) for a, b in product(by_cost[c1], by_cost[c - 1 - c1])]
+        for name, node in (("not", F.Not), ("next", F.Next), ("future", F.Future), ("globally", F.Globally)):
+            if name in enabled and c - w(name) >= 1:
+                here += [node(g) for g in by_cost[c - w(name)]]
+        for name, node in (("and", F.And), ("until", F.Until), ("or", F.Or)):
+            if name in enabled:
+                for c1 in range(1, c - w(name)):
+                    here += [node(a, b) for a, b in product(by_cost[c1], by_cost[c - w(name) - c1])]
         yield from ((c, g) for g in here)
         by_cost.append(here)
 
 
-def min_cost_bruteforce(spec: Specification, operators=F.DEFAULT_OPERATORS, max_cost: int = 8):
-    for c, g in enumerate_formulas(spec.alphabet.n, operators, max_cost):
+def min_cost_bruteforce(spec: Specification, operators=F.DEFAULT_OPERATORS, max_cost: int = 8, operator_weights: dict | None = None):
+    for c, g in enumerate_formulas(spec.alphabet.n, operators, max_cost, operator_weights):
         if semantics.separates_by_sat(spec, g):
             return c, g
     return None

@@ -23,13 +23,20 @@
  * sort-dedup + seen-set computes.
  *
  * Each function cites the reference lines it follows.
+ *
+ * EXTENSION, not in the reference (SPEC.md:211 lists G as a non-goal, SPEC.md:315 calls the
+ * operator weights "config-extensible" without implementing them): OP_GLOBALLY and per-operator cost weights
+ * (orc_set_weights).  With the default weights (all 1) and G disabled every code path below is the restatement of
+ * the reference; with them the level structure generalises as "operator of weight w over operands whose costs add
+ * up to cost - w".  PARITY UNPINNED for the extension: no reference output exists; tests pin it to the semantic
+ * identity G x = !F!x and to a brute-force search over weighted formula trees.
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
 
-enum { OP_ATOM = 0, OP_NOT, OP_NEXT, OP_FUTURE, OP_AND, OP_UNTIL, OP_OR }; /* engine.py:42 */
+enum { OP_ATOM = 0, OP_NOT, OP_NEXT, OP_FUTURE, OP_AND, OP_UNTIL, OP_OR, OP_GLOBALLY /* extension */ }; /* engine.py:42 */
 enum { ST_OK = 0, ST_TIME = 1, ST_MEMORY = 2, ST_BAD = -1 };
 
 typedef struct {
@@ -59,6 +66,7 @@ typedef struct {
     /* scratch */
     uint64_t *la, *lb, *lc;
     uint8_t *packed;
+    int weights[8]; /* extension: cost of one node of every operator tag ([0] = an atom); all 1 = the reference */
 } oracle_t;
 
 static double now_s(void) {
@@ -106,6 +114,15 @@ static void k_future(const oracle_t *o, const uint64_t *x, uint64_t *r) {
         uint64_t v = x[t];
         for (int k = 0; k < ns; k++) v |= v >> sh[k];
         r[t] = v;
+    }
+}
+/* extension (not in the reference): G x = "x at every position from here to the end" = !F!x */
+static void k_globally(const oracle_t *o, const uint64_t *x, uint64_t *r) {
+    int sh[8], ns = shift_schedule(o->w, sh);
+    for (int t = 0; t < o->T; t++) {
+        uint64_t v = lane_trunc(o, ~x[t]) & o->masks[t];
+        for (int k = 0; k < ns; k++) v |= v >> sh[k];
+        r[t] = lane_trunc(o, ~v) & o->masks[t];
     }
 }
 /* kernels.py:60-73 */
@@ -200,7 +217,18 @@ oracle_t *orc_create(int T, int lane_bits, const uint64_t *masks, const uint64_t
     o->lb = (uint64_t *)malloc(sizeof(uint64_t) * T);
     o->lc = (uint64_t *)malloc(sizeof(uint64_t) * T);
     o->packed = (uint8_t *)malloc((size_t)o->row_bytes);
+    for (int k = 0; k < 8; k++) o->weights[k] = 1;
     return o;
+}
+
+/* extension: cost of one node per operator tag (weights[0] = an atom), before the first level */
+int orc_set_weights(oracle_t *o, const int *weights) {
+    if (!o || o->n_levels) return ST_BAD;
+    for (int k = 0; k < 8; k++) {
+        if (weights[k] < 1) return ST_BAD;
+        o->weights[k] = weights[k];
+    }
+    return ST_OK;
 }
 
 void orc_destroy(oracle_t *o) {
@@ -301,6 +329,7 @@ static void do_chunk(run_t *r, const chunk_t *c) {
             load_row(o, left, o->la);
             if (c->tag == OP_NOT) k_not(o, o->la, o->lc);
             else if (c->tag == OP_NEXT) k_next(o, o->la, o->lc);
+            else if (c->tag == OP_GLOBALLY) k_globally(o, o->la, o->lc);
             else k_future(o, o->la, o->lc);
             break;
         case 2: { /* engine.py:292-307 */
@@ -395,18 +424,21 @@ int orc_expand_level(oracle_t *o, int cost, unsigned op_mask, int exhaustive, in
     chunk_t c;
     memset(&c, 0, sizeof(c));
 
-    if (cost == 1) { /* engine.py:221-223 */
+    const int *w = o->weights; /* all 1 in the reference: cost - w - ... below is then engine.py's cost - 1 - ... */
+    if (cost == w[OP_ATOM]) { /* engine.py:221-223 */
         c.kind = 0;
         c.tag = OP_ATOM;
         c.i1 = o->n_atoms;
         do_chunk(&r, &c);
-    } else {
-        const level_t *prev = &o->levels[cost - 2];
-        static const int unary_tags[3] = {OP_NOT, OP_NEXT, OP_FUTURE};   /* engine.py:44 */
-        static const int binary_tags[3] = {OP_AND, OP_UNTIL, OP_OR};     /* engine.py:45 */
-        for (int u = 0; u < 3 && !r.stop; u++) { /* engine.py:225-229 */
+    }
+    if (cost > 1) {
+        static const int unary_tags[4] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY}; /* engine.py:44 (+ extension) */
+        static const int binary_tags[3] = {OP_AND, OP_UNTIL, OP_OR};                /* engine.py:45 */
+        for (int u = 0; u < 4 && !r.stop; u++) { /* engine.py:225-229 */
             int tag = unary_tags[u];
-            if (!(op_mask >> tag & 1) || prev->n == 0) continue;
+            if (!(op_mask >> tag & 1) || cost - w[tag] < 1) continue;
+            const level_t *prev = &o->levels[cost - w[tag] - 1];
+            if (prev->n == 0) continue;
             for (int64_t i0 = 0; i0 < prev->n && !r.stop; i0 += batch) {
                 c.kind = 1;
                 c.tag = tag;
@@ -420,8 +452,8 @@ int orc_expand_level(oracle_t *o, int cost, unsigned op_mask, int exhaustive, in
             int tag = binary_tags[b];
             if (!(op_mask >> tag & 1)) continue;
             int commutative = (tag == OP_AND || tag == OP_OR); /* engine.py:46 */
-            for (int c1 = 1; c1 < cost - 1 && !r.stop; c1++) {
-                int c2 = cost - 1 - c1;
+            for (int c1 = 1; c1 < cost - w[tag] && !r.stop; c1++) {
+                int c2 = cost - w[tag] - c1;
                 if (commutative && c1 > c2) break;
                 const level_t *la = &o->levels[c1 - 1], *lb = &o->levels[c2 - 1];
                 int64_t na = la->n, nb = lb->n;

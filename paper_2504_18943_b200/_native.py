@@ -25,6 +25,7 @@ EXPORTED_SYMBOLS = (
     "ltlb200_last_error",
     "ltlb200_device_count",
     "ltlb200_create",
+    "ltlb200_set_weights",
     "ltlb200_destroy",
     "ltlb200_reset",
     "ltlb200_trim",
@@ -73,6 +74,10 @@ class Stats(ctypes.Structure):
         ("alloc_ms", ctypes.c_double),
         ("rebuild_host_ms", ctypes.c_double),
         ("create_ms", ctypes.c_double),
+        ("route_ms", ctypes.c_double),
+        ("probe_ms", ctypes.c_double),
+        ("routed_records", ctypes.c_uint64),
+        ("received_records", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:
@@ -103,6 +108,8 @@ def load():
     L.ltlb200_device_count.restype = ctypes.c_int
     L.ltlb200_create.restype = p
     L.ltlb200_create.argtypes = [i32, i32, p, p, p, i32, i32, u64, p]
+    L.ltlb200_set_weights.restype = ctypes.c_int
+    L.ltlb200_set_weights.argtypes = [p, p]
     L.ltlb200_destroy.argtypes = [p]
     L.ltlb200_destroy.restype = None
     L.ltlb200_trim.restype = None

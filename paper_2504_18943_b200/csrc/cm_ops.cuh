@@ -89,7 +89,14 @@ __device__ __forceinline__ uint32_t cm_sep_diff(uint4 x, uint4 target) {
     }
 }
 
-enum : int { OP_ATOM = 0, OP_NOT = 1, OP_NEXT = 2, OP_FUTURE = 3, OP_AND = 4, OP_UNTIL = 5, OP_OR = 6 };
+// OP_GLOBALLY is an EXTENSION beyond the reference's tags (engine.py:42 ends at OP_OR; SPEC.md:211 lists G as a
+// non-goal): G x = x at every position from here to the end of the trace = !F!x, one more masked cascade.
+enum : int { OP_ATOM = 0, OP_NOT = 1, OP_NEXT = 2, OP_FUTURE = 3, OP_AND = 4, OP_UNTIL = 5, OP_OR = 6, OP_GLOBALLY = 7 };
+
+template <int LW>
+__device__ __forceinline__ uint4 cm_globally(uint4 x, uint4 valid) {
+    return v_andnot(valid, cm_future<LW>(v_andnot(valid, x)));
+}
 
 template <int LW, int OP>
 __device__ __forceinline__ uint4 cm_apply(uint4 a, uint4 b, uint4 valid) {
@@ -99,6 +106,7 @@ __device__ __forceinline__ uint4 cm_apply(uint4 a, uint4 b, uint4 valid) {
     else if constexpr (OP == OP_FUTURE) return cm_future<LW>(a);
     else if constexpr (OP == OP_AND) return v_and(a, b);
     else if constexpr (OP == OP_OR) return v_or(a, b);
+    else if constexpr (OP == OP_GLOBALLY) return cm_globally<LW>(a, valid);
     else return cm_until<LW>(a, b, valid);
 }
 

@@ -329,6 +329,7 @@ public:
     int64_t level_candidates(int cost, uint32_t op_mask);
     int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
     int level_device(int cost, void **rows_dev, void **ords_dev);
+    void set_weights(const int32_t *weights);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
     void reset();
@@ -400,6 +401,10 @@ private:
     // all levels were built with one operator set; the first cut level or change of operators ends it.
     bool prune_ok_ = true;
     uint32_t prune_mask_ = 0;  // operator set of the levels built so far (0 = none yet)
+    // EXTENSION (not in the reference: "config-extensible", unimplemented): cost of one node per operator
+    // tag, [0] = an atom.  All 1 = the reference's node count.
+    int weights_[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+    bool unit_weights_ = true;
     // Non-exhaustive level over a store that already holds a separating CM (narrow path, one GPU): the chunks
     // the reference truncates at a separating candidate are found by a scan pass and their tails excluded
     // from the enumeration (NarrowParams::dead).  batch_size is known to expand_level only.
@@ -747,7 +752,7 @@ void Engine::reset() {
     approx_bytes_ = 0;
     last_constructed_ = 0;
     store_has_separator_ = false;
-    prune_ok_ = true;
+    prune_ok_ = unit_weights_;
     prune_mask_ = 0;
     entry_cache_total_ = 0;
     rebuild_table(kMinSlots);  // small levels probe an L2-resident set again; it regrows with the search
@@ -804,7 +809,10 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         n_tiles += b.tiles_v * b.tiles_s;
         lv.blocks.push_back(b);
     };
-    if (cost == 1) {
+    // weights_[tag] = cost of one node of that operator ([0] = an atom); all 1 in the reference, where the lines
+    // below read "atoms at cost 1, unary over level cost - 1, binary over c1 + c2 = cost - 1" (engine.py:219-266)
+    const int *w = weights_;
+    if (cost == w[OP_ATOM]) {
         BlockDesc b{};
         b.op = OP_ATOM;
         b.kind = BK_UNARY;
@@ -812,13 +820,13 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.na = (u64)n_atoms_;
         b.size = b.na;
         push(b);
-        return;
     }
-    const LevelMeta &prev = levels_[cost - 2];
-    static const int unary_tags[3] = {OP_NOT, OP_NEXT, OP_FUTURE};
+    static const int unary_tags[4] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY};
     static const int binary_tags[3] = {OP_AND, OP_UNTIL, OP_OR};
     for (int tag : unary_tags) {
-        if (!(op_mask >> tag & 1u) || prev.n == 0) continue;
+        if (!(op_mask >> tag & 1u) || cost - w[tag] < 1) continue;
+        const LevelMeta &prev = levels_[cost - w[tag] - 1];
+        if (prev.n == 0) continue;
         BlockDesc b{};
         b.op = (uint32_t)tag;
         b.kind = BK_UNARY;
@@ -830,8 +838,8 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
     for (int tag : binary_tags) {
         if (!(op_mask >> tag & 1u)) continue;
         const bool commutative = tag == OP_AND || tag == OP_OR;
-        for (int c1 = 1; c1 < cost - 1; ++c1) {
-            const int c2 = cost - 1 - c1;
+        for (int c1 = 1; c1 < cost - w[tag]; ++c1) {
+            const int c2 = cost - w[tag] - c1;
             if (commutative && c1 > c2) break;
             const LevelMeta &la = levels_[c1 - 1], &lb = levels_[c2 - 1];
             if (la.n == 0 || lb.n == 0) continue;
@@ -1826,6 +1834,7 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             float ms = 0;
             CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
             st_.enumerate_ms += ms;
+            st_.route_ms += ms;
             st_.enumerate_candidates += constructed / (u64)world;
             u64 need = 0;
             for (int o = 0; o < world; ++o) {
@@ -1854,6 +1863,7 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     pl.sep_ord = h_counters_[CTR_SEP];
     pl.n_seps = h_counters_[CTR_SEPCOUNT];
     for (int o = 0; o < world; ++o) {
+        st_.routed_records += counts[o];
         send_counts[o] = counts[o];
         send_offsets[o] = (u64)o * pl.region_cap;
     }
@@ -1888,6 +1898,7 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
     const u64 constructed = pl.constructed;
     const u64 n_words = (constructed + 31) / 32, n_sb = (n_words + 31) / 32;
     pl.n_received = n_records;
+    st_.received_records += n_records;
     const u64 kExact = 1ull << 22, kSlack = 1ull << 21;
     u64 est = n_records;
     if (n_records > kExact) {
@@ -1906,12 +1917,12 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
         level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
         CUDA_CHECK(cudaGetLastError());
         pl.claim_cap = claim_cap;
-        CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
         if (wide_) {
             reserve(stage_rows_, claim_cap * nvec_, false);
             reserve(stage_ord_, claim_cap, false);
             reserve(stage_slot_, claim_cap, false);
             CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+            CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
             if (n_records) {
                 WideParams P = wide_params(pl.exhaustive);
                 P.sep_list = nullptr;
@@ -1926,6 +1937,7 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
             reserve(claim_key_, claim_cap, false);
             reserve(claim_ord_, claim_cap, false);
             CUDA_CHECK(cudaMemsetAsync(claim_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+            CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
             if (n_records) {
                 NarrowParams P = narrow_params(pl.exhaustive);
                 P.sep_list = nullptr;  // separating candidates were recorded where they were built
@@ -1948,6 +1960,7 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
         float ms = 0;
         CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
         st_.enumerate_ms += ms;
+        st_.probe_ms += ms;
         if (h_counters_[CTR_OVERFLOW] == 0) break;
         // the records are still in the receive buffers: regrow locally and fold them in again, no new exchange
         if (attempt > 8 || est >= n_records) throw CudaError("hash set overflow while folding in received records");
@@ -2093,6 +2106,18 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
         }
     }
     return LTLB200_OK;
+}
+
+void Engine::set_weights(const int32_t *weights) {
+    if (!levels_.empty()) throw std::invalid_argument("operator weights must be set before the first level");
+    unit_weights_ = true;
+    for (int k = 0; k < 8; ++k) {
+        if (weights[k] < 1 || weights[k] > 64) throw std::invalid_argument("operator weights must be in 1..64");
+        weights_[k] = weights[k];
+        unit_weights_ = unit_weights_ && weights[k] == 1;
+    }
+    // the argument behind the associativity pruning of AND blocks was made for the reference's node-count cost
+    if (!unit_weights_) prune_ok_ = false;
 }
 
 // the level where it lives: rows of key_bytes() bytes and winning ordinals, valid until the next level is built
@@ -2317,6 +2342,14 @@ int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t c
                        int64_t *left, int64_t *right) {
     if (!e) return LTLB200_ERR_ARGUMENT;
     return guarded([&] { return e->impl->level_copy(cost, first, count, cms, op, left, right); });
+}
+
+int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights) {
+    if (!e || !weights) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        e->impl->set_weights(weights);
+        return LTLB200_OK;
+    });
 }
 
 int ltlb200_level_device(ltlb200_engine *e, int32_t cost, void **rows_dev, void **ords_dev) {

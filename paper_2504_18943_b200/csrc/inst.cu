@@ -42,6 +42,7 @@ void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const Narrow
             case OP_FUTURE: narrow_route_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
             case OP_AND: narrow_route_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
             case OP_UNTIL: narrow_route_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_GLOBALLY: narrow_route_kernel<LW, OP_GLOBALLY><<<grid, CTA_THREADS, 0, st>>>(P); break;
             default: narrow_route_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
         }
         return;
@@ -53,6 +54,7 @@ void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const Narrow
         case OP_FUTURE: narrow_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
         case OP_AND: narrow_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
         case OP_UNTIL: narrow_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
+        case OP_GLOBALLY: narrow_level_kernel<LW, OP_GLOBALLY><<<grid, CTA_THREADS, 0, st>>>(P); break;
         default: narrow_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
     }
 }
@@ -126,6 +128,7 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
             case OP_FUTURE: launch_route<OP_FUTURE>(P, grid, smem, device, st); break;
             case OP_AND: launch_route<OP_AND>(P, grid, smem, device, st); break;
             case OP_UNTIL: launch_route<OP_UNTIL>(P, grid, smem, device, st); break;
+            case OP_GLOBALLY: launch_route<OP_GLOBALLY>(P, grid, smem, device, st); break;
             default: launch_route<OP_OR>(P, grid, smem, device, st); break;
         }
         return;
@@ -137,6 +140,7 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
         case OP_FUTURE: launch_operator<OP_FUTURE>(P, grid, smem, device, st); break;
         case OP_AND: launch_operator<OP_AND>(P, grid, smem, device, st); break;
         case OP_UNTIL: launch_operator<OP_UNTIL>(P, grid, smem, device, st); break;
+        case OP_GLOBALLY: launch_operator<OP_GLOBALLY>(P, grid, smem, device, st); break;
         default: launch_operator<OP_OR>(P, grid, smem, device, st); break;
     }
 }

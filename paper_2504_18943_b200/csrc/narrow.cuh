@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) narrow_small_level_kernel(cons
             case OP_FUTURE: stop = run_tile<LW, OP_FUTURE>(P, ws, sink); break;
             case OP_AND: stop = run_tile<LW, OP_AND>(P, ws, sink); break;
             case OP_UNTIL: stop = run_tile<LW, OP_UNTIL>(P, ws, sink); break;
+            case OP_GLOBALLY: stop = run_tile<LW, OP_GLOBALLY>(P, ws, sink); break;
             default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
         }
         if (stop) break;
@@ -737,6 +738,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) narrow_guarded_level_kernel(co
             case OP_FUTURE: stop = run_tile<LW, OP_FUTURE>(P, ws, sink); break;
             case OP_AND: stop = run_tile<LW, OP_AND>(P, ws, sink); break;
             case OP_UNTIL: stop = run_tile<LW, OP_UNTIL>(P, ws, sink); break;
+            case OP_GLOBALLY: stop = run_tile<LW, OP_GLOBALLY>(P, ws, sink); break;
             default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
         }
         if (stop) break;

@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_small_level_kernel(const
             case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE>(P, W, st); break;
             case OP_AND: wide2_run_tile<LW, OP_AND>(P, W, st); break;
             case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL>(P, W, st); break;
+            case OP_GLOBALLY: wide2_run_tile<LW, OP_GLOBALLY>(P, W, st); break;
             default: wide2_run_tile<LW, OP_OR>(P, W, st); break;
         }
     }
@@ -514,6 +515,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_guarded_level_kernel(con
             case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE, W2_GUARD>(P, W, st); break;
             case OP_AND: wide2_run_tile<LW, OP_AND, W2_GUARD>(P, W, st); break;
             case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL, W2_GUARD>(P, W, st); break;
+            case OP_GLOBALLY: wide2_run_tile<LW, OP_GLOBALLY, W2_GUARD>(P, W, st); break;
             default: wide2_run_tile<LW, OP_OR, W2_GUARD>(P, W, st); break;
         }
     }

@@ -215,12 +215,12 @@ def synthesize_sharded(spec, config: EngineConfig = EngineConfig(), group=None, 
     from .engine import CandidateStore
 
     validate_feasible(spec)
-    ops = normalize_operators(config.operators)
+    ops = normalize_operators(config.operators, config.extended_grammar)
     t0 = time.perf_counter()
     if store_factory:
         store = store_factory(spec)
     else:  # on torch's current stream: the collectives and the engine's kernels are then ordered without host waits
-        store = CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb,
+        store = CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb, operator_weights=config.weights,
                                stream=torch.cuda.current_stream(torch.device("cuda", config.device)).cuda_stream)
     try:
         stats = RunStats()

@@ -35,11 +35,14 @@ import numpy as np
 from . import _native, semantics
 from .formulas import (
     DEFAULT_OPERATORS,
+    EXTENDED_OPERATOR_NAMES,
     OPERATOR_NAMES,
+    WEIGHT_NAMES,
     And,
     Atom,
     Formula,
     Future,
+    Globally,
     Next,
     Not,
     Or,
@@ -48,8 +51,10 @@ from .formulas import (
 from .traces import Layout, Specification, atom_bitvectors, smallest_lane_dtype, validate_feasible
 
 OP_ATOM, OP_NOT, OP_NEXT, OP_FUTURE, OP_AND, OP_UNTIL, OP_OR = range(7)
-_TAG_OF = {"not": OP_NOT, "next": OP_NEXT, "future": OP_FUTURE, "and": OP_AND, "until": OP_UNTIL, "or": OP_OR}
-_UNARY_NODE = {OP_NOT: Not, OP_NEXT: Next, OP_FUTURE: Future}
+OP_GLOBALLY = 7  # EXTENSION: not a reference tag (engine.py:42 ends at OP_OR); only with EngineConfig.extended_grammar
+_TAG_OF = {"not": OP_NOT, "next": OP_NEXT, "future": OP_FUTURE, "and": OP_AND, "until": OP_UNTIL, "or": OP_OR,
+           "globally": OP_GLOBALLY, "atom": OP_ATOM}
+_UNARY_NODE = {OP_NOT: Not, OP_NEXT: Next, OP_FUTURE: Future, OP_GLOBALLY: Globally}
 _BINARY_NODE = {OP_AND: And, OP_UNTIL: Until, OP_OR: Or}
 
 OUTCOME_FOUND = "found"
@@ -57,17 +62,32 @@ OUTCOME_EXHAUSTED = "exhausted"
 _FAILURE_TEXT = {_native.TIME_BUDGET: "time budget exhausted", _native.MEMORY_BUDGET: "memory budget exhausted"}
 
 
-def normalize_operators(operators) -> tuple[str, ...]:
+def normalize_operators(operators, extended: bool = False) -> tuple[str, ...]:
+    """Canonical operator order (reference engine.py:52-58).  ``extended`` also admits ``globally`` (an extension the
+    reference rejects like any unknown name)."""
+    names = EXTENDED_OPERATOR_NAMES if extended else OPERATOR_NAMES
     wanted = set(operators)
-    bad = wanted.difference(OPERATOR_NAMES)
+    bad = wanted.difference(names)
     if bad:
         raise ValueError(f"unknown operators: {sorted(bad)}")
-    return tuple(name for name in OPERATOR_NAMES if name in wanted)
+    return tuple(name for name in names if name in wanted)
 
 
 def operator_mask(operators) -> int:
     """Bit k set <=> operator tag k enabled (``op_mask`` of the C ABI)."""
-    return sum(1 << _TAG_OF[name] for name in normalize_operators(operators))
+    return sum(1 << _TAG_OF[name] for name in normalize_operators(operators, extended=True))
+
+
+def weight_vector(weights: dict | None) -> list[int]:
+    """Cost of one node per operator tag (index 0 = an atom) for ``ltlb200_set_weights``; all 1 = the reference."""
+    vec = [1] * 8
+    for name, value in (weights or {}).items():
+        if name not in WEIGHT_NAMES:
+            raise ValueError(f"unknown operator in operator_weights: {name!r}")
+        if int(value) != value or int(value) < 1:
+            raise ValueError("operator weights must be integers >= 1")
+        vec[_TAG_OF[name]] = int(value)
+    return vec
 
 
 @dataclass(frozen=True)
@@ -82,6 +102,12 @@ class EngineConfig:
     dnc_threshold: int = 8
     device: int = 0  # extension: CUDA device ordinal
     hbm_budget_mb: int = 0  # extension: cap on device memory (0 = 90% of free HBM)
+    # EXTENSIONS beyond the reference grammar and cost, off by default so that every reference
+    # call behaves as the reference does: `extended_grammar` admits the operator "globally" (G; SPEC.md:211 lists it as a
+    # non-goal), `operator_weights` gives one node of an operator a cost other than 1 ("config-extensible",
+    # unimplemented in the reference): {"atom" | "not" | "next" | "future" | "globally" | "and" | "until" | "or": int >= 1}
+    extended_grammar: bool = False
+    operator_weights: tuple | None = None  # ((name, weight), ...): hashable form of the dict
 
     def __post_init__(self):
         if self.max_cost < 1:
@@ -92,6 +118,18 @@ class EngineConfig:
             raise ValueError("batch_size must be >= 1")
         if self.threads is not None and self.threads < 1:
             raise ValueError("threads must be >= 1")
+        if self.operator_weights is not None:
+            if isinstance(self.operator_weights, dict):
+                object.__setattr__(self, "operator_weights", tuple(sorted(self.operator_weights.items())))
+            if not self.extended_grammar:
+                raise ValueError("operator_weights is an extension: set extended_grammar=True")
+            weight_vector(dict(self.operator_weights))
+        if "globally" in self.operators and not self.extended_grammar:
+            raise ValueError("unknown operators: ['globally']")
+
+    @property
+    def weights(self) -> dict:
+        return dict(self.operator_weights or ())
 
 
 @dataclass
@@ -143,7 +181,8 @@ class _DeviceMemory:
 class CandidateStore:
     """Cost-indexed cache of unique CMs with provenance, resident on the GPU."""
 
-    def __init__(self, spec: Specification, dtype=None, device: int = 0, hbm_budget_mb: int = 0, stream=None):
+    def __init__(self, spec: Specification, dtype=None, device: int = 0, hbm_budget_mb: int = 0, stream=None,
+                 operator_weights: dict | None = None):
         self.spec = spec
         self.dtype = np.dtype(dtype) if dtype is not None else smallest_lane_dtype(spec.max_length)
         self.layout = Layout.from_specification(spec, self.dtype)
@@ -164,6 +203,9 @@ class CandidateStore:
         )
         if not self._handle:
             raise _native.NativeEngineError("ltlb200_create failed: " + _native.last_error())
+        if operator_weights:  # extension: per-operator node costs
+            vec = (ctypes.c_int32 * 8)(*weight_vector(operator_weights))
+            _native.check(lib.ltlb200_set_weights(self._handle, vec), "set_weights")
 
     def close(self):
         handle, self._handle = getattr(self, "_handle", None), None
@@ -436,9 +478,9 @@ def expand_level(store: CandidateStore, cost: int, ops=DEFAULT_OPERATORS, config
 def synthesize(spec: Specification, config: EngineConfig = EngineConfig()) -> SynthesisResult:
     """Minimum-cost separating formula by level-wise enumeration on the GPU."""
     validate_feasible(spec)
-    ops = normalize_operators(config.operators)
+    ops = normalize_operators(config.operators, config.extended_grammar)
     t0 = time.perf_counter()
-    store = CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb)
+    store = CandidateStore(spec, device=config.device, hbm_budget_mb=config.hbm_budget_mb, operator_weights=config.weights)
     try:
         stats = RunStats()
         deadline = t0 + config.time_budget_s

@@ -41,6 +41,13 @@ class Future(Formula):
 
 
 @dataclass(frozen=True)
+class Globally(Formula):
+    """EXTENSION (not in the reference grammar): G child = child at every position to the end."""
+
+    child: Formula
+
+
+@dataclass(frozen=True)
 class And(Formula):
     left: Formula
     right: Formula
@@ -60,8 +67,12 @@ class Until(Formula):
 
 OPERATOR_NAMES = ("not", "next", "future", "and", "until", "or")
 DEFAULT_OPERATORS = ("not", "next", "future", "and", "until")
+# EXTENSION: operators beyond the reference grammar, accepted only by an EngineConfig with
+# extended_grammar=True, and the names a cost-weight table may use ("atom" = one atomic proposition)
+EXTENDED_OPERATOR_NAMES = ("not", "next", "future", "globally", "and", "until", "or")
+WEIGHT_NAMES = ("atom",) + EXTENDED_OPERATOR_NAMES
 
-_UNARY_PREFIX = {Not: "!", Next: "X ", Future: "F "}
+_UNARY_PREFIX = {Not: "!", Next: "X ", Future: "F ", Globally: "G "}
 # binary node -> (symbol, own level, level required of left child, of right child)
 _BINARY_SHAPE = {
     Until: (" U ", 3, 4, 3),  # right-associative
@@ -88,6 +99,23 @@ def cost(f: Formula) -> int:
     return total
 
 
+_WEIGHT_KEY = {Atom: "atom", Not: "not", Next: "next", Future: "future", Globally: "globally", And: "and", Until: "until", Or: "or"}
+
+
+def weighted_cost(f: Formula, weights: dict | None = None) -> int:
+    """EXTENSION: sum of the node weights (``weights[name]``, default 1 each); ``cost`` when no weights are given."""
+    weights = weights or {}
+    total, todo = 0, [f]
+    while todo:
+        g = todo.pop()
+        total += int(weights.get(_WEIGHT_KEY[type(g)], 1))
+        if type(g) in _UNARY_PREFIX:
+            todo.append(g.child)
+        elif type(g) in _BINARY_SHAPE:
+            todo.extend((g.left, g.right))
+    return total
+
+
 def to_text(f: Formula, alphabet: Alphabet) -> str:
     def show(g: Formula, need: int) -> str:
         if isinstance(g, Atom):
@@ -111,7 +139,7 @@ class FormulaSyntaxError(ValueError):
 
 
 _LEX = re.compile(r"\s*(?:(?P<sym>[!&|()])|(?P<word>[A-Za-z_][A-Za-z0-9_]*))")
-_KEYWORDS = {"X": Next, "F": Future}
+_KEYWORDS = {"X": Next, "F": Future, "G": Globally}  # (G: extension; an alphabet with an atom named G keeps the reference reading)
 
 
 def _lex(text: str):
@@ -142,7 +170,7 @@ def parse_formula(text: str, alphabet: Alphabet) -> Formula:
         if tok == "!":
             pos += 1
             return Not(unary())
-        if tok in _KEYWORDS:
+        if tok in _KEYWORDS and not (tok == "G" and "G" in alphabet.names):
             pos += 1
             return _KEYWORDS[tok](unary())
         if tok == "(":

@@ -15,7 +15,7 @@ agree on random formulas and traces.  Neither is ever part of enumeration.
 
 from __future__ import annotations
 
-from .formulas import And, Atom, Formula, Future, Next, Not, Or, Until
+from .formulas import And, Atom, Formula, Future, Globally, Next, Not, Or, Until
 from .traces import Specification, Trace
 
 
@@ -32,6 +32,9 @@ def _truth_table(trace: Trace, f: Formula) -> list[bool]:
     if isinstance(f, Future):
         inner = _truth_table(trace, f.child)
         return [any(inner[i:]) for i in range(n)]
+    if isinstance(f, Globally):  # extension
+        inner = _truth_table(trace, f.child)
+        return [all(inner[i:]) for i in range(n)]
     if isinstance(f, (And, Or, Until)):
         lhs, rhs = _truth_table(trace, f.left), _truth_table(trace, f.right)
         if isinstance(f, And):
@@ -56,6 +59,11 @@ def _truth_table_fast(trace: Trace, f: Formula) -> list[bool]:
         out = _truth_table_fast(trace, f.child)
         for i in range(n - 2, -1, -1):
             out[i] = out[i] or out[i + 1]
+        return out
+    if isinstance(f, Globally):  # extension: G p = p & X G p, with G p = p at the last position
+        out = _truth_table_fast(trace, f.child)
+        for i in range(n - 2, -1, -1):
+            out[i] = out[i] and out[i + 1]
         return out
     if isinstance(f, (And, Or, Until)):
         lhs, rhs = _truth_table_fast(trace, f.left), _truth_table_fast(trace, f.right)
