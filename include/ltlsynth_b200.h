@@ -113,6 +113,25 @@ ltlb200_engine *ltlb200_create(int32_t trace_count, int32_t lane_bits, const uin
  */
 int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights);
 
+/*
+ * REGEX FRONT-END, first slice.  Not in the reference (SPEC.md:11 scopes regular-expression
+ * synthesis out; PAPER.md:81-113 only motivates it): no reference interface to cite, PARITY UNPINNED; the CPU
+ * oracle is oracle/regex_oracle.py (membership pinned to Python's re.fullmatch).
+ *
+ * The same engine enumerates regular expressions when its rows are characteristic sequences (CS: one bit per infix
+ * of the example strings, infixes sorted by (length, text), bit 0 = the empty word).  Create the handle with the CS
+ * bitsets as byte rows -- ltlb200_create(trace_count = ceil(n_bits / 8), lane_bits = 8, masks = the bits of all
+ * example strings, target = the bits of the positive ones, atoms = the CSs of the empty word and of the letters) --
+ * then, before the first level, hand over the infix-split guide table: the splits w = u v of infix w are entries
+ * offsets[w] .. offsets[w + 1] - 1, each (index of u) | (index of v) << 16.  Levels are then built with
+ *   op_mask bits  LTLB200_OP_RE_QUESTION  r?      LTLB200_OP_RE_STAR  r*
+ *                 LTLB200_OP_RE_CONCAT    r s     LTLB200_OP_OR       r | s  (union)
+ * and the five cost parameters (literal, ?, *, concatenation, union) are ltlb200_set_weights on the tags
+ * 0, 8, 9, 10, 6.  This slice takes CSs of up to 128 bits (the narrow kernels).
+ */
+enum { LTLB200_OP_RE_QUESTION = 8, LTLB200_OP_RE_STAR = 9, LTLB200_OP_RE_CONCAT = 10 };
+int ltlb200_set_regex(ltlb200_engine *e, int32_t n_bits, const uint32_t *offsets, const uint32_t *entries, uint64_t n_entries);
+
 /* Frees every device allocation of the handle. */
 void ltlb200_destroy(ltlb200_engine *e);
 

@@ -26,6 +26,7 @@ EXPORTED_SYMBOLS = (
     "ltlb200_device_count",
     "ltlb200_create",
     "ltlb200_set_weights",
+    "ltlb200_set_regex",
     "ltlb200_destroy",
     "ltlb200_reset",
     "ltlb200_trim",
@@ -110,6 +111,8 @@ def load():
     L.ltlb200_create.argtypes = [i32, i32, p, p, p, i32, i32, u64, p]
     L.ltlb200_set_weights.restype = ctypes.c_int
     L.ltlb200_set_weights.argtypes = [p, p]
+    L.ltlb200_set_regex.restype = ctypes.c_int
+    L.ltlb200_set_regex.argtypes = [p, i32, p, p, u64]
     L.ltlb200_destroy.argtypes = [p]
     L.ltlb200_destroy.restype = None
     L.ltlb200_trim.restype = None

@@ -78,10 +78,14 @@ __device__ __forceinline__ uint4 cm_until(uint4 a, uint4 b, uint4 valid) {
     return v_and(r, valid);
 }
 
-// word-wise "position-0 bit of every lane differs from the target" (0 when this vector agrees)
+// word-wise "position-0 bit of every lane differs from the target" (0 when this vector agrees).
+// LW == 1 is the regex front-end's bitset (regex_ops.cuh): `valid` = the bits of the example strings (positives and
+// negatives), `target` = the bits of the positives; a CS separates when it agrees with the target on those bits.
 template <int LW>
-__device__ __forceinline__ uint32_t cm_sep_diff(uint4 x, uint4 target) {
-    if constexpr (LW == 64) {
+__device__ __forceinline__ uint32_t cm_sep_diff(uint4 x, uint4 target, uint4 valid) {
+    if constexpr (LW == 1) {
+        return ((x.x & valid.x) ^ target.x) | ((x.y & valid.y) ^ target.y) | ((x.z & valid.z) ^ target.z) | ((x.w & valid.w) ^ target.w);
+    } else if constexpr (LW == 64) {
         return ((x.x & 1u) ^ target.x) | target.y | ((x.z & 1u) ^ target.z) | target.w;
     } else {
         const uint32_t b = lane_bit0_32<LW>();

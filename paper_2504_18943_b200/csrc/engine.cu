@@ -329,7 +329,8 @@ public:
     int64_t level_candidates(int cost, uint32_t op_mask);
     int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
     int level_device(int cost, void **rows_dev, void **ords_dev);
-    void set_weights(const int32_t *weights);
+    void set_weights(const int32_t *weights, int count);
+    void set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
     void reset();
@@ -403,8 +404,11 @@ private:
     uint32_t prune_mask_ = 0;  // operator set of the levels built so far (0 = none yet)
     // EXTENSION (not in the reference: "config-extensible", unimplemented): cost of one node per operator
     // tag, [0] = an atom.  All 1 = the reference's node count.
-    int weights_[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+    int weights_[16] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
     bool unit_weights_ = true;
+    // regex front-end (regex_ops.cuh): the infix-split guide table on the device; n_bits_ > 0 = regex grammar
+    DeviceArray<uint32_t> guide_;
+    int n_bits_ = 0;
     // Non-exhaustive level over a store that already holds a separating CM (narrow path, one GPU): the chunks
     // the reference truncates at a separating candidate are found by a scan pass and their tails excluded
     // from the enumeration (NarrowParams::dead).  batch_size is known to expand_level only.
@@ -662,6 +666,7 @@ Engine::~Engine() {
     release(scan_tmp_);
     release(sep_list_);
     release(misc_);
+    release(guide_);
     release(xchg_);
     release(xs_rows_);
     release(xr_rows_);
@@ -821,8 +826,10 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
         b.size = b.na;
         push(b);
     }
-    static const int unary_tags[4] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY};
-    static const int binary_tags[3] = {OP_AND, OP_UNTIL, OP_OR};
+    // (the regex operators -- question, star unary; concatenation, non-commutative, before union = OP_OR -- are only
+    // ever enabled on a handle with the regex grammar, where none of the LTL tags is)
+    static const int unary_tags[6] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY, OP_RE_QUESTION, OP_RE_STAR};
+    static const int binary_tags[4] = {OP_AND, OP_UNTIL, OP_RE_CONCAT, OP_OR};
     for (int tag : unary_tags) {
         if (!(op_mask >> tag & 1u) || cost - w[tag] < 1) continue;
         const LevelMeta &prev = levels_[cost - w[tag] - 1];
@@ -1048,6 +1055,7 @@ void Engine::fan_end() {
 
 void Engine::launch_narrow(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st) {
     switch (lw_) {
+        case LW_REGEX: narrow_launch_1(kind, op, P, grid, st); break;
         case 8: narrow_launch_8(kind, op, P, grid, st); break;
         case 16: narrow_launch_16(kind, op, P, grid, st); break;
         case 32: narrow_launch_32(kind, op, P, grid, st); break;
@@ -1336,6 +1344,8 @@ NarrowParams Engine::narrow_params(bool exhaustive) const {
     P.dead = dead_n_ ? dead_.ptr : nullptr;
     P.dead_n = (uint32_t)dead_n_;
     P.scan_only = 0;
+    P.guide = guide_.ptr;
+    P.n_bits = n_bits_;
     return P;
 }
 
@@ -1946,6 +1956,7 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
                 const u64 steps = (n_records + 32 * PROBE_BATCH - 1) / (32 * PROBE_BATCH);
                 const int grid = (int)std::max<u64>(1, std::min<u64>((steps + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * occupancy_));
                 switch (lw_) {
+                    case LW_REGEX: narrow_probe_1(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 8: narrow_probe_8(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 16: narrow_probe_16(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 32: narrow_probe_32(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
@@ -2108,10 +2119,35 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
     return LTLB200_OK;
 }
 
-void Engine::set_weights(const int32_t *weights) {
+// The regex front-end (first slice): the handle was created with the CS bitsets as byte rows
+// (masks = the bits of all example strings, target = the bits of the positives, atoms = the CSs of the empty word
+// and of the letters); this switches its kernels to the regex operators and uploads the infix-split guide table.
+void Engine::set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries) {
+    if (!levels_.empty()) throw std::invalid_argument("the grammar must be set before the first level");
+    if (n_bits < 1 || n_bits > 128 || wide_ || lw_ != 8 || (n_bits + 7) / 8 != row_bytes_)
+        throw std::invalid_argument("regex front-end: this slice takes characteristic sequences of up to 128 bits, created as "
+                                    "ceil(bits / 8) lanes of 8 bits");
+    CUDA_CHECK(cudaSetDevice(device_));
+    std::vector<uint32_t> h((size_t)n_bits + 1 + n_entries);
+    memcpy(h.data(), offsets, ((size_t)n_bits + 1) * sizeof(uint32_t));
+    memcpy(h.data() + n_bits + 1, entries, n_entries * sizeof(uint32_t));
+    if (h[n_bits] != n_entries) throw std::invalid_argument("regex guide table: offsets do not end at the entry count");
+    reserve(guide_, h.size(), false);
+    CUDA_CHECK(cudaMemcpyAsync(guide_.ptr, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.h2d_bytes += h.size() * sizeof(uint32_t);
+    n_bits_ = n_bits;
+    lw_ = LW_REGEX;
+    special_possible_ = n_bits == 128;  // only a 128-bit CS can be all ones (the empty-slot marker)
+    prune_ok_ = false;                  // (the associativity pruning is an argument about LTL's AND)
+    occupancy_ = narrow_occupancy_1();
+}
+
+void Engine::set_weights(const int32_t *weights, int count) {
     if (!levels_.empty()) throw std::invalid_argument("operator weights must be set before the first level");
+    if (count < 1 || count > 16) throw std::invalid_argument("operator weights: 1..16 entries");
     unit_weights_ = true;
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < count; ++k) {
         if (weights[k] < 1 || weights[k] > 64) throw std::invalid_argument("operator weights must be in 1..64");
         weights_[k] = weights[k];
         unit_weights_ = unit_weights_ && weights[k] == 1;
@@ -2347,7 +2383,15 @@ int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t c
 int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights) {
     if (!e || !weights) return LTLB200_ERR_ARGUMENT;
     return guarded([&] {
-        e->impl->set_weights(weights);
+        e->impl->set_weights(weights, 16);
+        return LTLB200_OK;
+    });
+}
+
+int ltlb200_set_regex(ltlb200_engine *e, int32_t n_bits, const uint32_t *offsets, const uint32_t *entries, uint64_t n_entries) {
+    if (!e || !offsets || (!entries && n_entries)) return LTLB200_ERR_ARGUMENT;
+    return guarded([&] {
+        e->impl->set_regex(n_bits, offsets, entries, n_entries);
         return LTLB200_OK;
     });
 }

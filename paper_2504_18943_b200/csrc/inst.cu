@@ -25,38 +25,42 @@ constexpr int LW = LTLB200_INST_LW;
 
 #if !LTLB200_INST_WIDE
 
-void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st) {
-    if (kind == LK_SMALL) {
-        narrow_small_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
-        return;
-    }
-    if (kind == LK_GUARDED) {
-        narrow_guarded_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
-        return;
-    }
-    if (kind == LK_ROUTE) {
+// one launch per operator: the fused construct + probe kernel, or (ROUTE) the kernel that routes to hash owners
+template <bool ROUTE, int OP>
+static void launch_one(const NarrowParams &P, int grid, cudaStream_t st) {
+    if constexpr (ROUTE) narrow_route_kernel<LW, OP><<<grid, CTA_THREADS, 0, st>>>(P);
+    else narrow_level_kernel<LW, OP><<<grid, CTA_THREADS, 0, st>>>(P);
+}
+
+template <bool ROUTE>
+static void launch_by_operator(int op, const NarrowParams &P, int grid, cudaStream_t st) {
+    if constexpr (LW == LW_REGEX) {  // the regex front-end's operators (regex_ops.cuh)
         switch (op) {
-            case OP_ATOM: narrow_route_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            case OP_NOT: narrow_route_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            case OP_NEXT: narrow_route_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            case OP_FUTURE: narrow_route_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            case OP_AND: narrow_route_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            case OP_UNTIL: narrow_route_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            case OP_GLOBALLY: narrow_route_kernel<LW, OP_GLOBALLY><<<grid, CTA_THREADS, 0, st>>>(P); break;
-            default: narrow_route_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
+            case OP_ATOM: launch_one<ROUTE, OP_ATOM>(P, grid, st); break;
+            case OP_RE_QUESTION: launch_one<ROUTE, OP_RE_QUESTION>(P, grid, st); break;
+            case OP_RE_STAR: launch_one<ROUTE, OP_RE_STAR>(P, grid, st); break;
+            case OP_RE_CONCAT: launch_one<ROUTE, OP_RE_CONCAT>(P, grid, st); break;
+            default: launch_one<ROUTE, OP_OR>(P, grid, st); break;
         }
-        return;
+    } else {
+        switch (op) {
+            case OP_ATOM: launch_one<ROUTE, OP_ATOM>(P, grid, st); break;
+            case OP_NOT: launch_one<ROUTE, OP_NOT>(P, grid, st); break;
+            case OP_NEXT: launch_one<ROUTE, OP_NEXT>(P, grid, st); break;
+            case OP_FUTURE: launch_one<ROUTE, OP_FUTURE>(P, grid, st); break;
+            case OP_GLOBALLY: launch_one<ROUTE, OP_GLOBALLY>(P, grid, st); break;
+            case OP_AND: launch_one<ROUTE, OP_AND>(P, grid, st); break;
+            case OP_UNTIL: launch_one<ROUTE, OP_UNTIL>(P, grid, st); break;
+            default: launch_one<ROUTE, OP_OR>(P, grid, st); break;
+        }
     }
-    switch (op) {
-        case OP_ATOM: narrow_level_kernel<LW, OP_ATOM><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_NOT: narrow_level_kernel<LW, OP_NOT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_NEXT: narrow_level_kernel<LW, OP_NEXT><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_FUTURE: narrow_level_kernel<LW, OP_FUTURE><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_AND: narrow_level_kernel<LW, OP_AND><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_UNTIL: narrow_level_kernel<LW, OP_UNTIL><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        case OP_GLOBALLY: narrow_level_kernel<LW, OP_GLOBALLY><<<grid, CTA_THREADS, 0, st>>>(P); break;
-        default: narrow_level_kernel<LW, OP_OR><<<grid, CTA_THREADS, 0, st>>>(P); break;
-    }
+}
+
+void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st) {
+    if (kind == LK_SMALL) narrow_small_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
+    else if (kind == LK_GUARDED) narrow_guarded_level_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P);
+    else if (kind == LK_ROUTE) launch_by_operator<true>(op, P, grid, st);
+    else launch_by_operator<false>(op, P, grid, st);
 }
 
 void LTLB200_CAT(narrow_probe_, LTLB200_INST_LW)(const NarrowParams &P, const void *rows, const void *ords, unsigned long long n,
@@ -66,7 +70,8 @@ void LTLB200_CAT(narrow_probe_, LTLB200_INST_LW)(const NarrowParams &P, const vo
 
 int LTLB200_CAT(narrow_occupancy_, LTLB200_INST_LW)() {
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, OP_UNTIL>, CTA_THREADS, 0) != cudaSuccess) {
+    constexpr int kHeaviest = LW == LW_REGEX ? (int)OP_RE_CONCAT : (int)OP_UNTIL;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, kHeaviest>, CTA_THREADS, 0) != cudaSuccess) {
         cudaGetLastError();
         occ = 1;
     }

@@ -27,6 +27,7 @@ enum : int { LK_OPERATOR = 0, LK_SMALL = 1, LK_GUARDED = 2, LK_ROUTE = 3 };
     void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \
     int wide2_occupancy_##LW(int nvec, int device);
 
+LTLB200_DECLARE_LW(1)  // the regex front-end's bitset CS (regex_ops.cuh; narrow kernels only)
 LTLB200_DECLARE_LW(8)
 LTLB200_DECLARE_LW(16)
 LTLB200_DECLARE_LW(32)

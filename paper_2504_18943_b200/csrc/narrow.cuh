@@ -27,6 +27,7 @@
 // positions come from warp ballots, not from shared-memory atomics.
 #pragma once
 #include "cm_ops.cuh"
+#include "regex_ops.cuh"
 
 namespace ltlb200 {
 
@@ -114,6 +115,9 @@ struct NarrowParams {
     int scan_only;  // the pass that finds those chunks: only record the ordinal of every separating candidate
     // One search sharded over several GPUs (narrow_route_kernel): candidates are not probed here but appended as
     // records {CM, ordinal} to the region of their hash owner, route_world regions of route_cap records each.
+    // regex front-end (regex_ops.cuh; LW == LW_REGEX instantiation only): the infix-split guide table
+    const uint32_t *guide;
+    int n_bits;
     uint4 *route_rows;
     u64 *route_ords;
     u64 route_cap;
@@ -333,7 +337,7 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queu
     }
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        const bool sep = cm_sep_diff<LW>(cand[r], P.target) == 0u;
+        const bool sep = cm_sep_diff<LW>(cand[r], P.target, P.valid) == 0u;
         flags[r] = sep ? PK_SEP : 0u;
         act[r] = ACT_NONE;
         if (!live[r]) continue;
@@ -413,6 +417,13 @@ static __device__ __noinline__ bool ordinal_is_dead(const u64 *dead, uint32_t n,
     return a > 0 && ord < dead[2 * (a - 1) + 1];
 }
 
+// one connective on one-vector CMs: the LTL connectives of cm_ops.cuh, or -- LW == LW_REGEX -- the regex operators
+template <int LW, int OP>
+__device__ __forceinline__ uint4 apply_op(const NarrowParams &P, uint4 a, uint4 b) {
+    if constexpr (LW == LW_REGEX) return re_apply<OP>(P.guide, P.n_bits, a, b);
+    else return cm_apply<LW, OP>(a, b, P.valid);
+}
+
 // The tile runners are generic over where candidates go: `sink.emit<LW>(cand, live, known, ord_of)`
 // is the direct insert (DirectSink -> insert_batch) or the bucket scatter of the partitioned
 // path (narrow_part.cuh); WS is the warp's shared state (rows / term / block).
@@ -444,7 +455,7 @@ __device__ __forceinline__ bool run_unary_tile(const NarrowParams &P, WS &ws, Si
         }
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
-            cand[r] = cm_apply<LW, OP>(x[r], x[r], P.valid);
+            cand[r] = apply_op<LW, OP>(P, x[r], x[r]);
             known[r] = OP != OP_ATOM && v_eq(cand[r], x[r]);
         }
         if (sink_is_guarded<Sink>::value && P.dead_n) {
@@ -542,7 +553,7 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
             for (int r = 0; r < PROBE_BATCH; ++r) {
                 const uint4 xs = ws.rows[min(g + r, s_cnt - 1)];
                 live[r] = g + r < s_live;
-                cand[r] = VEC_B ? cm_apply<LW, OP>(xs, xv, P.valid) : cm_apply<LW, OP>(xv, xs, P.valid);
+                cand[r] = VEC_B ? apply_op<LW, OP>(P, xs, xv) : apply_op<LW, OP>(P, xv, xs);
                 known[r] = v_eq(cand[r], xs) || v_eq(cand[r], xv);
                 if (prune) known[r] = known[r] || skip_v || (ws.term[min(g + r, s_cnt - 1)] & SKIP_BIT) != 0ull;
             }
@@ -563,7 +574,7 @@ __device__ __noinline__ void scan_batch(const NarrowParams &P, const uint4 (&can
                                         OrdOf ord_of) {
 #pragma unroll
     for (int r = 0; r < PROBE_BATCH; ++r) {
-        if (!live[r] || cm_sep_diff<LW>(cand[r], P.target) != 0u) continue;
+        if (!live[r] || cm_sep_diff<LW>(cand[r], P.target, P.valid) != 0u) continue;
         const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
         if (pos < P.sep_list_cap) P.sep_list[pos] = ord_of(r);
     }
@@ -655,12 +666,37 @@ __device__ __forceinline__ bool run_tile(const NarrowParams &P, WS &ws, Sink &si
     const u64 sep_now = ws.sep_now;
     if (ws.block.ord0 > sep_now) return true;  // the whole block, and every later one, is ordered after the separator
     const u64 tile_local = ws.ticket - ws.block.tile0;
-    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
+    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL || OP == OP_RE_CONCAT) {
         // which operand sits in the lanes changes only how the ordinal is formed, not the result
         if (ws.block.vec_is_b) return run_binary_tile<LW, OP, true>(P, ws, sink, tile_local, sep_now);
         return run_binary_tile<LW, OP, false>(P, ws, sink, tile_local, sep_now);
     } else {
         return run_unary_tile<LW, OP>(P, ws, sink, tile_local, sep_now);
+    }
+}
+
+// run-time operator dispatch of the one-launch kernels: the LTL connectives, or (LW_REGEX) the regex operators
+template <int LW, class WS, class Sink>
+__device__ __forceinline__ bool run_tile_any(const NarrowParams &P, WS &ws, Sink &sink) {
+    if constexpr (LW == LW_REGEX) {
+        switch (ws.block.op) {
+            case OP_ATOM: return run_tile<LW, OP_ATOM>(P, ws, sink);
+            case OP_RE_QUESTION: return run_tile<LW, OP_RE_QUESTION>(P, ws, sink);
+            case OP_RE_STAR: return run_tile<LW, OP_RE_STAR>(P, ws, sink);
+            case OP_RE_CONCAT: return run_tile<LW, OP_RE_CONCAT>(P, ws, sink);
+            default: return run_tile<LW, OP_OR>(P, ws, sink);
+        }
+    } else {
+        switch (ws.block.op) {
+            case OP_ATOM: return run_tile<LW, OP_ATOM>(P, ws, sink);
+            case OP_NOT: return run_tile<LW, OP_NOT>(P, ws, sink);
+            case OP_NEXT: return run_tile<LW, OP_NEXT>(P, ws, sink);
+            case OP_FUTURE: return run_tile<LW, OP_FUTURE>(P, ws, sink);
+            case OP_GLOBALLY: return run_tile<LW, OP_GLOBALLY>(P, ws, sink);
+            case OP_AND: return run_tile<LW, OP_AND>(P, ws, sink);
+            case OP_UNTIL: return run_tile<LW, OP_UNTIL>(P, ws, sink);
+            default: return run_tile<LW, OP_OR>(P, ws, sink);
+        }
     }
 }
 
@@ -700,18 +736,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) narrow_small_level_kernel(cons
         const TileFetch cur = next;
         if (!open_tile(P, ws, cur)) break;
         next = fetch_tile(P, nullptr);
-        bool stop;
-        switch (ws.block.op) {
-            case OP_ATOM: stop = run_tile<LW, OP_ATOM>(P, ws, sink); break;
-            case OP_NOT: stop = run_tile<LW, OP_NOT>(P, ws, sink); break;
-            case OP_NEXT: stop = run_tile<LW, OP_NEXT>(P, ws, sink); break;
-            case OP_FUTURE: stop = run_tile<LW, OP_FUTURE>(P, ws, sink); break;
-            case OP_AND: stop = run_tile<LW, OP_AND>(P, ws, sink); break;
-            case OP_UNTIL: stop = run_tile<LW, OP_UNTIL>(P, ws, sink); break;
-            case OP_GLOBALLY: stop = run_tile<LW, OP_GLOBALLY>(P, ws, sink); break;
-            default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
-        }
-        if (stop) break;
+        if (run_tile_any<LW>(P, ws, sink)) break;
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
         while (st.qfill > 0u) drain_round(P, ws.queue, st);
@@ -730,18 +755,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) narrow_guarded_level_kernel(co
         const TileFetch cur = next;
         if (!open_tile(P, ws, cur)) break;
         next = fetch_tile(P, nullptr);
-        bool stop;
-        switch (ws.block.op) {
-            case OP_ATOM: stop = run_tile<LW, OP_ATOM>(P, ws, sink); break;
-            case OP_NOT: stop = run_tile<LW, OP_NOT>(P, ws, sink); break;
-            case OP_NEXT: stop = run_tile<LW, OP_NEXT>(P, ws, sink); break;
-            case OP_FUTURE: stop = run_tile<LW, OP_FUTURE>(P, ws, sink); break;
-            case OP_AND: stop = run_tile<LW, OP_AND>(P, ws, sink); break;
-            case OP_UNTIL: stop = run_tile<LW, OP_UNTIL>(P, ws, sink); break;
-            case OP_GLOBALLY: stop = run_tile<LW, OP_GLOBALLY>(P, ws, sink); break;
-            default: stop = run_tile<LW, OP_OR>(P, ws, sink); break;
-        }
-        if (stop) break;
+        if (run_tile_any<LW>(P, ws, sink)) break;
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
         while (st.qfill > 0u) drain_round(P, ws.queue, st);
@@ -792,7 +806,7 @@ struct RouteSink {
         const uint32_t lt = lanemask_lt();
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
-            if (live[r] && cm_sep_diff<LW>(cand[r], P.target) == 0u) {
+            if (live[r] && cm_sep_diff<LW>(cand[r], P.target, P.valid) == 0u) {
                 const u64 o = ord_of(r);
                 if (P.route_sep_any) atomicMin(&P.counters[CTR_SEP], o);
                 if (P.sep_list) {  // exhaustive runs keep every separating ordinal (chunk-exact separator id)

@@ -115,7 +115,7 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
             const uint4 c = cm_apply<LW, OP>(a, b, valid);
             ha[r] ^= hash_vec(c, seed_a);
             hb[r] ^= hash_vec(c, seed_b);
-            sepacc[r] |= cm_sep_diff<LW>(c, target);
+            sepacc[r] |= cm_sep_diff<LW>(c, target, valid);
             da[r] |= v_diff(c, a);
             db[r] |= v_diff(c, b);
         }
@@ -268,7 +268,7 @@ __device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wid
             gen(r, p, a, b);
             const uint4 c = cm_apply<LW, OP>(a, b, valid);
             ho[r] ^= hash_vec(c, 0x5BD1E995u * (uint32_t)(p + 1));
-            sepacc[r] |= cm_sep_diff<LW>(c, target);
+            sepacc[r] |= cm_sep_diff<LW>(c, target, valid);
             da[r] |= v_diff(c, a);
             db[r] |= v_diff(c, b);
         }

@@ -80,7 +80,7 @@ def operator_mask(operators) -> int:
 
 def weight_vector(weights: dict | None) -> list[int]:
     """Cost of one node per operator tag (index 0 = an atom) for ``ltlb200_set_weights``; all 1 = the reference."""
-    vec = [1] * 8
+    vec = [1] * 16
     for name, value in (weights or {}).items():
         if name not in WEIGHT_NAMES:
             raise ValueError(f"unknown operator in operator_weights: {name!r}")
@@ -204,7 +204,7 @@ class CandidateStore:
         if not self._handle:
             raise _native.NativeEngineError("ltlb200_create failed: " + _native.last_error())
         if operator_weights:  # extension: per-operator node costs
-            vec = (ctypes.c_int32 * 8)(*weight_vector(operator_weights))
+            vec = (ctypes.c_int32 * 16)(*weight_vector(operator_weights))
             _native.check(lib.ltlb200_set_weights(self._handle, vec), "set_weights")
 
     def close(self):

@@ -1,0 +1,80 @@
+"""Regex front-end on the CUDA engine (first slice: characteristic sequences of up to 128 bits) against the CPU oracle
+(oracle/regex_oracle.py, pinned to Python's `re` by tests/test_regex_oracle.py).  PARITY UNPINNED with respect to the
+reference, which has no regex synthesiser."""
+
+import random
+import re
+
+import numpy as np
+import pytest
+
+from oracle import regex_oracle as ro
+from paper_2504_18943_b200 import _native
+from paper_2504_18943_b200 import regex as rx
+from test_regex_oracle import EMAIL_N, EMAIL_P, random_binary_spec
+
+pytestmark = pytest.mark.gpu
+
+
+def _assert_level_equal(store, oracle_store, cost, where):
+    a, b = store.level(cost), oracle_store.level(cost)
+    assert (a.n, a.base) == (b.n, b.base), where
+    want = np.frombuffer(b"".join(store.ix.row_bytes(cs) for cs in b.cs), dtype=np.uint8).reshape(b.n, store.ix.n_bytes) \
+        if b.n else np.empty((0, store.ix.n_bytes), dtype=np.uint8)
+    assert np.array_equal(a.cms, want), where + ": characteristic sequences differ"
+    assert list(a.op) == b.op and list(a.left) == b.left and list(a.right) == b.right, where + ": provenance differs"
+
+
+@pytest.mark.parametrize("seed,cost,max_cost", [
+    (0, rx.CostFunction(), 7), (1, rx.CostFunction(), 7), (2, rx.CostFunction(), 6),
+    (3, rx.CostFunction(literal=1, question=2, star=2, concat=1, union=3), 8),
+    (4, rx.CostFunction(literal=2, star=1, concat=2), 9),
+])
+def test_levels_equal_the_oracle_on_baseline_config_0(seed, cost, max_cost):
+    """BASELINE configs[0]: alphabet {0,1}, 4 positive / 4 negative strings of length <= 5; exhaustive levels."""
+    spec = random_binary_spec(random.Random(seed))
+    store, ref = rx.RegexStore(spec, cost), ro.RegexOracle(spec, cost)
+    try:
+        for c in range(1, max_cost + 1):
+            status, n_new, sep, constructed = store.expand(c, exhaustive=True)
+            o_new, o_sep, o_constructed = ref.expand_level(c, exhaustive=True)
+            assert (status, n_new, constructed) == (0, o_new, o_constructed), f"seed {seed} cost {c}"
+            _assert_level_equal(store, ref, c, f"seed {seed} cost {c}")
+        for lv_cost in (2, max_cost):  # every stored expression means what re says it means
+            lv = store.level(lv_cost)
+            for k in range(0, lv.n, max(1, lv.n // 50)):
+                pattern = rx.to_pattern(store.regex_of(lv.base + k))
+                assert store.ix.row_bytes(store.ix.cs_of_pattern(pattern)) == lv.cms[k].tobytes(), pattern
+    finally:
+        store.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_synthesize_regex_returns_the_oracles_expression(seed):
+    spec = random_binary_spec(random.Random(100 + seed))
+    res = rx.synthesize_regex(spec, rx.RegexConfig(max_cost=9))
+    want = ro.synthesize(spec, max_cost=9)
+    assert (res.pattern, res.cost, res.stats.unique, res.stats.constructed) == (want.pattern, want.cost, want.unique, want.constructed)
+    if res.pattern is not None:
+        assert all(re.fullmatch(res.pattern, w) for w in spec.positives) and not any(re.fullmatch(res.pattern, w) for w in spec.negatives)
+
+
+def test_three_letter_alphabet_and_wider_sequences():
+    words = ['aacca', 'acacbcab', 'bbccba', 'bcaaaaac', 'bcaabbca', 'bcacbbac', 'cbcbba', 'ccaaca']
+    spec = rx.RegexSpecification(tuple(words[:4]), tuple(words[4:]))
+    ix = rx.InfixIndex(spec)
+    assert ix.n_bits == 111  # all four words of the uint4 in use
+    store, ref = rx.RegexStore(spec), ro.RegexOracle(spec)
+    try:
+        for c in range(1, 6):
+            _, n_new, _, constructed = store.expand(c, exhaustive=True)
+            o_new, _, o_constructed = ref.expand_level(c, exhaustive=True)
+            assert (n_new, constructed) == (o_new, o_constructed)
+            _assert_level_equal(store, ref, c, f"abc cost {c}")
+    finally:
+        store.close()
+
+
+def test_email_example_is_refused_on_the_gpu_in_this_slice():
+    with pytest.raises(_native.NativeEngineError, match="128 bits"):
+        rx.RegexStore(rx.RegexSpecification(EMAIL_P, EMAIL_N))
