@@ -244,7 +244,9 @@ int ltlb200_level_copy(ltlb200_engine *e, int32_t cost, int64_t first, int64_t c
 /*
  * _Level.cms where it lives: DEVICE pointers to the level's rows (ltlb200_key_bytes bytes each: the numpy row image
  * zero padded to 16-byte vectors) and to the ordinal each entry won with, for consumers that stay on the GPU.
- * Valid until the next level is built or the handle is reset / destroyed; NULL for an empty level.
+ * Valid until the next level is built or the handle is reset / destroyed; NULL for an empty level.  (Multi-vector
+ * CMs live in claim order on the device -- finalising a level does not move them -- so for those the rows pointer
+ * is the level's range of an id-ordered image gathered on demand.)
  */
 int ltlb200_level_device(ltlb200_engine *e, int32_t cost, void **rows_dev, void **ords_dev);
 

@@ -329,6 +329,7 @@ public:
     int64_t level_candidates(int cost, uint32_t op_mask);
     int level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uint8_t *op, int64_t *left, int64_t *right);
     int level_device(int cost, void **rows_dev, void **ords_dev);
+    const uint4 *rows_in_id_order(u64 first, u64 count);
     void set_weights(const int32_t *weights, int count);
     void set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
@@ -379,10 +380,12 @@ private:
     DeviceArray<uint4> claim_key_;   // narrow path: this level's new CMs by claim index
     DeviceArray<u64> claim_ord_;
     DeviceArray<u64> wslots_;          // wide path: slot words
-    DeviceArray<uint4> stage_rows_;    // wide path: this level's new rows
+    // wide path: store_ is the ROW LOG (rows in the order they were staged, a level's new rows at its tail);
+    // loc_[id] = log index of entry id; log_tail_ = log entries in use (finalised levels incl. their unused entries)
+    DeviceArray<u64> loc_;
+    DeviceArray<uint4> gather_;  // level_copy / level_device: rows of a level gathered into id order
+    u64 log_tail_ = 0;
     DeviceArray<u64> stage_ord_;
-    DeviceArray<uint32_t> stage_slot_;
-    DeviceArray<u64> stage_gid_;
     DeviceArray<uint32_t> bitmap_;
     DeviceArray<uint32_t> sb_rank_;
     DeviceArray<uint32_t> scan_tmp_;
@@ -657,10 +660,9 @@ Engine::~Engine() {
     release(claim_key_);
     release(claim_ord_);
     release(wslots_);
-    release(stage_rows_);
+    release(loc_);
+    release(gather_);
     release(stage_ord_);
-    release(stage_slot_);
-    release(stage_gid_);
     release(bitmap_);
     release(sb_rank_);
     release(scan_tmp_);
@@ -715,7 +717,7 @@ void Engine::rebuild_table(u64 slots) {
         CUDA_CHECK(cudaMemsetAsync(wslots_.ptr, 0, wslots_.cap * sizeof(u64), stream_));
         if (total_) {
             int grid = (int)std::min<u64>((total_ + 255) / 256, (u64)sm_count_ * 16);
-            wide_rebuild_kernel<<<grid, 256, 0, stream_>>>(wslots_.ptr, wslots_.cap - 1, store_.ptr, total_, nvec_, log2g_, (uint32_t)owner_world_, (uint32_t)owner_rank_);
+            wide_rebuild_kernel<<<grid, 256, 0, stream_>>>(wslots_.ptr, wslots_.cap - 1, store_.ptr, loc_.ptr, total_, nvec_, log2g_, (uint32_t)owner_world_, (uint32_t)owner_rank_);
             CUDA_CHECK(cudaGetLastError());
             st_.kernel_launches++;
         }
@@ -754,6 +756,7 @@ void Engine::reset() {
     CUDA_CHECK(cudaSetDevice(device_));
     levels_.clear();
     total_ = 0;
+    log_tail_ = 0;
     approx_bytes_ = 0;
     last_constructed_ = 0;
     store_has_separator_ = false;
@@ -1255,9 +1258,8 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             CUDA_CHECK(cudaGetLastError());
             pl.claim_cap = claim_cap;
             if (wide_) {
-                reserve(stage_rows_, claim_cap * nvec_, false);
+                reserve(store_, (log_tail_ + claim_cap) * nvec_, true, log_tail_ * nvec_);  // new rows are staged at the log's tail
                 reserve(stage_ord_, claim_cap, false);
-                reserve(stage_slot_, claim_cap, false);
                 CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
                 WideParams P = wide_params(exhaustive);
                 CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
@@ -1355,11 +1357,11 @@ WideParams Engine::wide_params(bool exhaustive) const {
     P.atoms = d_atoms_;
     P.slots = wslots_.ptr;
     P.slot_mask = wslots_.cap - 1;
-    P.stage_rows = stage_rows_.ptr;
+    P.loc = loc_.ptr;
+    P.stage_rows = store_.ptr + log_tail_ * nvec_;
     P.stage_ord = stage_ord_.ptr;
-    P.stage_slot = stage_slot_.ptr;
     P.stage_cap = pending_.claim_cap;
-    P.total_before = total_;
+    P.total_before = log_tail_;
     P.counters = d_counters_;
     P.blocks = d_blocks_;
     P.valid = d_valid_;
@@ -1416,7 +1418,12 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
         reserve(bitmap_, n_words + 1, false);
         reserve(sb_rank_, n_sb + 1, false);
-        reserve(store_, (total_ + n_claimed + n_received) * nvec_, true, total_ * nvec_);
+        if (wide_) {  // the staged rows stay where they are; received rows are appended behind them
+            reserve(store_, (log_tail_ + n_claimed + n_received) * nvec_, true, (log_tail_ + n_claimed) * nvec_);
+            reserve(loc_, total_ + n_claimed + n_received, true, total_);
+        } else {
+            reserve(store_, (total_ + n_claimed + n_received) * nvec_, true, total_ * nvec_);
+        }
         reserve(ords_, total_ + n_claimed + n_received, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
         if (!global_bitmap) CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
@@ -1426,20 +1433,15 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
         WideFinalize W{};
         const int fgrid = (int)std::max<u64>(1, std::min<u64>((n_claimed + 255) / 256, (u64)sm_count_ * 16));
         if (wide_) {
-            W.slots = wslots_.ptr;
-            W.stage_rows = stage_rows_.ptr;
             W.stage_ord = stage_ord_.ptr;
-            W.stage_slot = stage_slot_.ptr;
-            reserve(stage_gid_, std::max<u64>(1, std::min(n_claimed, pl.claim_cap)), false);
-            W.stage_gid = stage_gid_.ptr;
             W.n_staged = std::min(n_claimed, pl.claim_cap);
             W.bitmap = bitmap_.ptr;
             W.sb_rank = sb_rank_.ptr;
             W.ord_limit = ord_limit;
-            W.store = store_.ptr;
+            W.loc = loc_.ptr;
             W.ords = ords_.ptr;
             W.base = total_;
-            W.nvec = nvec_;
+            W.log_base = log_tail_;
             if (!global_bitmap) wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
         } else {
             F.claim_key = claim_key_.ptr;
@@ -1471,10 +1473,6 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
         level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
         if (wide_) {
             wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
-            const u64 work = W.n_staged * (u64)nvec_;
-            const int wgrid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
-            wide_copy_kernel<<<wgrid, 256, 0, stream_>>>(W);
-            st_.kernel_launches++;
         } else {
             narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
         }
@@ -1482,7 +1480,7 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
         if (n_received) {  // what the other owners published
             const u64 work = n_received * (u64)(wide_ ? nvec_ : 1);
             const int rgrid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
-            if (wide_) wide_scatter_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, nvec_, bitmap_.ptr, sb_rank_.ptr, store_.ptr, ords_.ptr, total_);
+            if (wide_) wide_append_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, nvec_, bitmap_.ptr, sb_rank_.ptr, store_.ptr, log_tail_ + n_claimed, loc_.ptr, ords_.ptr, total_);
             else narrow_scatter_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, bitmap_.ptr, sb_rank_.ptr, store_.ptr, ords_.ptr, total_);
             CUDA_CHECK(cudaGetLastError());
             st_.kernel_launches++;
@@ -1500,6 +1498,7 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
         if (global_bitmap && lv.n != pl.n_winners + n_received)
             throw CudaError("sharded level: the winners bitmap holds " + std::to_string(lv.n) + " entries, the owners published " +
                             std::to_string(pl.n_winners + n_received));
+        if (wide_) log_tail_ += n_claimed + n_received;  // (unused and cut-off staging entries stay behind as dead log entries)
         sep_ord = h_counters_[CTR_SEP];
         if (sep_ord != VAL_EMPTY) *sep_gid = (int64_t)(total_ + h_counters_[CTR_SEPRANK]);
         if (cut) table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
@@ -1569,7 +1568,8 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
             reserve(bitmap_, n_sb * 32 + 1, false);
             reserve(sb_rank_, n_sb + 1, false);
         }
-        reserve(store_, (total_ + pl.claim_cap) * nvec_, true, total_ * nvec_);
+        if (wide_) reserve(loc_, total_ + pl.claim_cap, true, total_);  // (the rows are in the log already)
+        else reserve(store_, (total_ + pl.claim_cap) * nvec_, true, total_ * nvec_);
         reserve(ords_, total_ + pl.claim_cap, true, total_);
         CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
         // the grids are sized by what the level can have claimed at most (its candidates, or the claim arrays)
@@ -1577,18 +1577,13 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
         if (wide_) {
             WideFinalize W{};
-            W.slots = wslots_.ptr;
-            W.stage_rows = stage_rows_.ptr;
             W.stage_ord = stage_ord_.ptr;
-            W.stage_slot = stage_slot_.ptr;
             W.bitmap = bitmap_.ptr;
             W.sb_rank = sb_rank_.ptr;
-            W.store = store_.ptr;
+            W.loc = loc_.ptr;
             W.ords = ords_.ptr;
             W.base = total_;
-            W.nvec = nvec_;
-            reserve(stage_gid_, std::max<u64>(1, pl.claim_cap), false);
-            W.stage_gid = stage_gid_.ptr;
+            W.log_base = log_tail_;
             W.live = d_counters_;
             W.stage_cap = pl.claim_cap;
             W.cut_allowed = exhaustive ? 0 : 1;
@@ -1598,10 +1593,8 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
             launch_rank_scan(n_words, n_sb);
             level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
             wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
-            const int wgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound * (u64)nvec_ + 255) / 256, (u64)sm_count_ * 16));
-            wide_copy_kernel<<<wgrid, 256, 0, stream_>>>(W);
             CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches += 4;
+            st_.kernel_launches += 3;
         } else {
             FinalizeParams F{};
             F.claim_key = claim_key_.ptr;
@@ -1661,6 +1654,7 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
             return kRetryLevel;
         }
         lv.n = h_counters_[CTR_WINNERS];
+        if (wide_) log_tail_ += std::min(h_counters_[CTR_CLAIMED], pl.claim_cap);
         sep_ord = h_counters_[CTR_SEP];
         if (sep_ord != VAL_EMPTY || h_counters_[CTR_SEPCOUNT]) store_has_separator_ = true;
         if (exhaustive && h_counters_[CTR_SEPCOUNT]) {
@@ -1928,9 +1922,8 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
         CUDA_CHECK(cudaGetLastError());
         pl.claim_cap = claim_cap;
         if (wide_) {
-            reserve(stage_rows_, claim_cap * nvec_, false);
+            reserve(store_, (log_tail_ + claim_cap) * nvec_, true, log_tail_ * nvec_);
             reserve(stage_ord_, claim_cap, false);
-            reserve(stage_slot_, claim_cap, false);
             CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
             CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
             if (n_records) {
@@ -2038,7 +2031,7 @@ void Engine::winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void *
     CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, sizeof(u64), stream_));
     if (n) {
         const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
-        if (wide_) wide_winners_kernel<<<grid, 256, 0, stream_>>>(stage_rows_.ptr, stage_ord_.ptr, n, nvec_, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
+        if (wide_) wide_winners_kernel<<<grid, 256, 0, stream_>>>(store_.ptr + log_tail_ * nvec_, stage_ord_.ptr, n, nvec_, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
         else narrow_winners_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
         CUDA_CHECK(cudaGetLastError());
         st_.kernel_launches++;
@@ -2097,7 +2090,7 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
     const u64 g0 = lv.base + (u64)first;
     if (cms) {
         std::vector<uint4> rows((size_t)count * nvec_);
-        CUDA_CHECK(cudaMemcpyAsync(rows.data(), store_.ptr + g0 * nvec_, rows.size() * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
+        CUDA_CHECK(cudaMemcpyAsync(rows.data(), rows_in_id_order(g0, (u64)count), rows.size() * sizeof(uint4), cudaMemcpyDeviceToHost, stream_));
         CUDA_CHECK(cudaStreamSynchronize(stream_));
         st_.d2h_bytes += rows.size() * sizeof(uint4);
         for (int64_t k = 0; k < count; ++k) memcpy(cms + (size_t)k * row_bytes_, &rows[(size_t)k * nvec_], (size_t)row_bytes_);
@@ -2156,13 +2149,28 @@ void Engine::set_weights(const int32_t *weights, int count) {
     if (!unit_weights_) prune_ok_ = false;
 }
 
+// device pointer to `count` rows from id `first` on, in id order: the cache itself on the narrow path; on the wide
+// path, where rows live in claim order, their place in a gathered image of the whole cache (filled on demand, range
+// by range; valid until the next level is built)
+const uint4 *Engine::rows_in_id_order(u64 first, u64 count) {
+    if (!wide_) return store_.ptr + first;
+    reserve(gather_, std::max<u64>(total_, 1) * nvec_, false);
+    const u64 work = count * (u64)nvec_;
+    const int grid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
+    wide_gather_kernel<<<grid, 256, 0, stream_>>>(store_.ptr, loc_.ptr, first, count, nvec_, gather_.ptr + first * nvec_);
+    CUDA_CHECK(cudaGetLastError());
+    st_.kernel_launches++;
+    return gather_.ptr + first * nvec_;
+}
+
 // the level where it lives: rows of key_bytes() bytes and winning ordinals, valid until the next level is built
 int Engine::level_device(int cost, void **rows_dev, void **ords_dev) {
     if (cost < 1 || cost > (int)levels_.size()) return LTLB200_ERR_ARGUMENT;
     CUDA_CHECK(cudaSetDevice(device_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     const LevelMeta &lv = levels_[cost - 1];
-    *rows_dev = lv.n ? (void *)(store_.ptr + lv.base * nvec_) : nullptr;
+    *rows_dev = lv.n ? (void *)rows_in_id_order(lv.base, lv.n) : nullptr;
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
     *ords_dev = lv.n ? (void *)(ords_.ptr + lv.base) : nullptr;
     return LTLB200_OK;
 }

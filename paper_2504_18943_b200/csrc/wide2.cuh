@@ -29,7 +29,10 @@ namespace ltlb200 {
 #ifndef LTLB200_WIDE2_MIN_CTAS
 #define LTLB200_WIDE2_MIN_CTAS 3
 #endif
-constexpr int W2_BATCH = 2;        // candidates a lane carries through the passes together
+#ifndef LTLB200_W2_BATCH
+#define LTLB200_W2_BATCH 2
+#endif
+constexpr int W2_BATCH = LTLB200_W2_BATCH;  // candidates a lane carries through the passes together
 #ifndef LTLB200_W2_PREFETCH
 #define LTLB200_W2_PREFETCH 4
 #endif
@@ -181,7 +184,10 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
             row[r] = match[r] ? (staged_row[r] ? P.stage_rows + (idx - P.total_before) * nvec : P.store + idx * nvec) : nullptr;
             diff[r] = 0u;
         }
-        const bool any_claim = __any_sync(0xFFFFFFFFu, claim[0] || claim[W2_BATCH - 1]);
+        bool claims_here = false;
+#pragma unroll
+        for (int r = 0; r < W2_BATCH; ++r) claims_here = claims_here || claim[r];
+        const bool any_claim = __any_sync(0xFFFFFFFFu, claims_here);
         // The stored rows of the fingerprint matches are fetched W2_PREFETCH vectors ahead of the compare: taken one
         // at a time (load, compare, next vector) a 128-byte CM costs eight dependent trips to the L2 / DRAM, and
         // the first ncu capture had a third of this kernel's stall samples on exactly that compare.
@@ -216,7 +222,6 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
                 const u64 old = atomicCAS(&P.slots[slot[r]], 0ull, slot_word(fp[r], P.total_before + entry[r]));
                 if (old == 0ull) {
                     atomicMin(&P.stage_ord[entry[r]], ords[r]);
-                    P.stage_slot[entry[r]] = slot[r];
                     fresh[r] = true;
                     active[r] = false;
                 } else {
@@ -331,7 +336,6 @@ __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide
     const BlockDesc &B = W.fx->block;
     const int lane = threadIdx.x & 31;
     const int nvec = P.nvec;
-    const uint4 *src = B.from_atoms ? P.atoms : P.store + B.a_off * nvec;
     const u64 per_tile = (u64)32 * B.tile_s;
     const u64 first = tile_local * per_tile + lane;
     const u64 ord0 = B.ord0, n = B.na;
@@ -347,7 +351,8 @@ __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide
             const u64 i = first + (u64)(k + r) * 32;
             live[r] = k + r < n_steps && i < n;
             ords[r] = ord0 + i;
-            rows[r] = src + (live[r] ? i : 0) * nvec;
+            // a finalised row lives where it was staged (claim order): loc[id] is its place in the row log
+            rows[r] = B.from_atoms ? P.atoms + (live[r] ? i : 0) * nvec : P.store + __ldg(P.loc + B.a_off + (live[r] ? i : 0)) * nvec;
         }
         auto gen = [&](int r, int p, uint4 &a, uint4 &b) {
             a = __ldg(rows[r] + p);
@@ -377,11 +382,15 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
     const u64 ord0 = B.ord0, na = B.na, nb = B.nb;
     const u64 tile_min = ord0 + (VEC_B ? (tri ? s0 * na - (s0 ? (s0 * (s0 - 1)) / 2 : 0) : s0 * nb + v0) : v0 * nb + s0);
     if (tile_min > sep_now) return;
-    const uint4 *vec_rows = P.store + (VEC_B ? B.b_off : B.a_off) * nvec;
-    const uint4 *sc_rows = P.store + (VEC_B ? B.a_off : B.b_off) * nvec;
+    // operand rows by id: a finalised row lives where it was staged (claim order), loc[id] = its place in the row log
+    const u64 *vec_loc = P.loc + (VEC_B ? B.b_off : B.a_off);
+    const u64 *sc_loc = P.loc + (VEC_B ? B.a_off : B.b_off);
     __syncwarp();
-    // stage the scalar rows (contiguous in the cache: one coalesced copy) and their ordinal terms
-    for (int t = lane; t < s_cnt * nvec; t += 32) W.sc[t] = __ldg(sc_rows + s0 * nvec + t);
+    // stage the scalar rows (whole rows of nvec consecutive vectors) and their ordinal terms
+    for (int t = lane; t < s_cnt * nvec; t += 32) {
+        const int rrow = t / nvec, p = t - rrow * nvec;
+        W.sc[t] = __ldg(P.store + __ldg(sc_loc + s0 + rrow) * nvec + p);
+    }
     for (int k = lane; k < s_cnt; k += 32) {
         const u64 s = s0 + k;
         W.fx->term[k] = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
@@ -395,7 +404,7 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
         const int rows_here = (int)min((u64)32, n_vec - vbase);
         for (int t = lane; t < rows_here * nvec; t += 32) {
             const int rrow = t / nvec, p = t - rrow * nvec;
-            W.vec[p * 32 + rrow] = __ldg(vec_rows + vbase * nvec + t);
+            W.vec[p * 32 + rrow] = __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p);
         }
         __syncwarp();
         const u64 v = vbase + lane;

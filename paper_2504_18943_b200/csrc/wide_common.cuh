@@ -5,9 +5,11 @@
 // compare-and-swap:
 //
 //   * a CM is `nvec` uint4 vectors;
-//   * the hash set holds 8-byte words  [fingerprint:24 | row index + 1 : 40]  (0 = empty).
-//     The row index points either into the language cache (a CM finalised at an earlier
-//     level: index < total_before) or into this level's STAGING pool of new rows;
+//   * rows live in a ROW LOG in the order they were staged; the hash set holds 8-byte words
+//     [fingerprint:24 | log index + 1 : 40]  (0 = empty).  An index below total_before is a row of an
+//     earlier level, anything beyond is one of this level's new rows, staged at the tail of the log;
+//     finalising a level leaves the rows where they are and records loc[id] = log index (no copy,
+//     no slot rewrite);
 //   * to claim a slot the row is first written to a private staging entry and only then
 //     published with one 64-bit CAS on the slot word.  A reader that finds a matching
 //     fingerprint therefore always finds a complete row behind it -- no waiting, no locks --
@@ -27,15 +29,18 @@ constexpr u64 SLOT_IDX_MASK = (1ull << 40) - 1;
 constexpr int MAX_NVEC = 32;
 
 struct WideParams {
-    const uint4 *store;  // finalised rows by global id, nvec vectors each
+    // The ROW LOG: every row the search ever staged, in claim order, nvec vectors each.  A level's new rows are staged
+    // at its tail and STAY there when the level is finalised (no copy into id order): `loc[id]` = the log index of
+    // entry `id`, and a slot word's row index is a log index.
+    const uint4 *store;
+    const u64 *loc;      // log index of every finalised entry by global id
     const uint4 *atoms;  // atom rows, nvec vectors each
     u64 *slots;
     u64 slot_mask;
-    uint4 *stage_rows;  // this level's new rows, nvec vectors each
+    uint4 *stage_rows;  // this level's new rows = the tail of the log (store + total_before * nvec)
     u64 *stage_ord;     // min ordinal per staging entry (all ones = unused)
-    uint32_t *stage_slot;
     u64 stage_cap;
-    u64 total_before;  // rows finalised before this level
+    u64 total_before;  // log entries before this level: a slot word pointing at or beyond it is one of this level's rows
     u64 *counters;     // CTR_*; CTR_CLAIMED counts reserved staging entries
     const BlockDesc *blocks;
     int block_begin, block_end;
@@ -159,10 +164,7 @@ static __device__ __noinline__ bool wide_insert(const WideParams &P, GroupGeom g
             if (lane == g.leader) old = atomicCAS(&P.slots[s], 0ull, slot_word(fp, P.total_before + gs.spare));
             old = __shfl_sync(g.mask, old, g.leader);
             if (old == 0ull) {
-                if (lane == g.leader) {
-                    atomicMin(&P.stage_ord[gs.spare], ord);
-                    P.stage_slot[gs.spare] = s;
-                }
+                if (lane == g.leader) atomicMin(&P.stage_ord[gs.spare], ord);
                 gs.spare = ~0ull;
                 return true;
             }

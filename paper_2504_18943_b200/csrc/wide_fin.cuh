@@ -8,20 +8,16 @@ namespace ltlb200 {
 // ---- finalisation (wide) -------------------------------------------------------------------
 
 struct WideFinalize {
-    u64 *slots;
-    const uint4 *stage_rows;
     const u64 *stage_ord;
-    const uint32_t *stage_slot;
     u64 n_staged;  // staging entries reserved (some unused: ord = all ones)
     uint32_t *bitmap;
     const uint32_t *sb_rank;
     u64 ord_limit;
-    uint4 *store;
+    u64 *loc;      // log index per global id (written here)
     u64 *ords;
-    u64 base;
-    int nvec;
-    u64 *stage_gid;  // final id per staging entry (written by wide_rank_kernel)
-    // deferred mode (see FinalizeParams in narrow.cuh): bounds resolved on the device
+    u64 base;      // global id of the level's first entry
+    u64 log_base;  // log index of staging entry 0
+    // deferred mode (see FinalizeParams in narrow_fin.cuh): bounds resolved on the device
     const u64 *live;
     u64 stage_cap;
     int cut_allowed;
@@ -47,51 +43,34 @@ __global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
     }
 }
 
-// Scatter in two steps, so that the rank of an entry is computed once, not once per vector:
-//   wide_rank_kernel   one thread per staging entry: final id = base + rank(ordinal); records the
-//                      ordinal, re-points the entry's slot word at the final id, leaves the id in
-//                      stage_gid (all ones = entry unused or ordered after the separator);
-//   wide_copy_kernel   one thread per (staging entry, vector): coalesced copy of the row to its
-//                      place in the cache.
+// One thread per staging entry: final id = base + rank(ordinal).  The row stays where it was staged -- the slot
+// word that published it already points there -- so finalising an entry is two 8-byte stores: its place in the
+// row log and the ordinal it won with.  (Round 1 copied every row into id order and rewrote every slot word:
+// wide_copy_kernel + the slot read-modify-write were 12 of the 41 ms of a c5 search to cost 12.)
 __global__ void __launch_bounds__(256) wide_rank_kernel(const WideFinalize F) {
     u64 n_staged, ord_limit;
     if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
     for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < n_staged; k += (u64)gridDim.x * blockDim.x) {
         const u64 ord = F.stage_ord[k];
-        if (ord > ord_limit) {
-            F.stage_gid[k] = ~0ull;
-            continue;
-        }
+        if (ord > ord_limit) continue;  // unused entry, or ordered after the separator
         const u64 gid = F.base + ordinal_rank(F.bitmap, F.sb_rank, ord);
-        F.stage_gid[k] = gid;
+        F.loc[gid] = F.log_base + k;
         F.ords[gid] = ord;
-        u64 *slot = &F.slots[F.stage_slot[k]];
-        *slot = (*slot & ~SLOT_IDX_MASK) | (gid + 1);  // same fingerprint, final row id
     }
 }
 
-__global__ void __launch_bounds__(256) wide_copy_kernel(const WideFinalize F) {
-    u64 n_staged, ord_limit;
-    if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
-    const u64 total = n_staged * (u64)F.nvec;
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
-        const u64 k = t / F.nvec;
-        const u64 gid = F.stage_gid[k];
-        if (gid == ~0ull) continue;
-        F.store[gid * F.nvec + (t - k * F.nvec)] = F.stage_rows[t];
-    }
-}
-
-// re-insert finalised rows [0, count) into a fresh table: rows of the cache are pairwise
-// distinct, so claiming the first empty slot of the probe sequence is enough
+// re-insert finalised rows into a fresh table: rows of the cache are pairwise distinct, so claiming the first
+// empty slot of the probe sequence is enough.  Entries are visited by id, their rows found through loc[]
 // (owners > 1: an owner-sharded set holds only the rows whose hash owner is `rank`)
-__global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_mask, const uint4 *store, u64 count,
+__global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_mask, const uint4 *store, const u64 *loc, u64 count,
                                                            int nvec, int log2g, uint32_t owners, uint32_t rank) {
     for (u64 gid = (u64)blockIdx.x * blockDim.x + threadIdx.x; gid < count; gid += (u64)gridDim.x * blockDim.x) {
-        if (owners > 1u && row_owner(store + gid * nvec, nvec, owners) != rank) continue;
+        const u64 at = loc[gid];
+        const uint4 *row = store + at * nvec;
+        if (owners > 1u && row_owner(row, nvec, owners) != rank) continue;
         uint32_t a = 0, b = 0;
         for (int p = 0; p < nvec; ++p) {
-            const uint4 part = store[gid * nvec + p];
+            const uint4 part = row[p];
             a ^= hash_vec(part, 0x9E3779B9u * (uint32_t)(p + 1));
             b ^= hash_vec(part, 0x7F4A7C15u * (uint32_t)(p + 1) + 0x632BE5ABu);
         }
@@ -102,8 +81,17 @@ __global__ void __launch_bounds__(256) wide_rebuild_kernel(u64 *slots, u64 slot_
         b *= 0xC2B2AE35u;
         b ^= b >> 16;
         u64 s = a & slot_mask;
-        const u64 word = slot_word(b >> 8, gid);
+        const u64 word = slot_word(b >> 8, at);
         while (atomicCAS(&slots[s], 0ull, word) != 0ull) s = (s + 1) & slot_mask;
+    }
+}
+
+// rows [first, first + count) of the cache in id order, gathered from the row log (level_copy / level_device)
+__global__ void __launch_bounds__(256) wide_gather_kernel(const uint4 *store, const u64 *loc, u64 first, u64 count, int nvec, uint4 *out) {
+    const u64 total = count * (u64)nvec;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+        const u64 k = t / nvec;
+        out[t] = store[loc[first + k] * nvec + (t - k * nvec)];
     }
 }
 
@@ -131,19 +119,21 @@ __global__ void __launch_bounds__(256) wide_winners_kernel(const uint4 *stage_ro
     }
 }
 
-// Appends records published by OTHER owners to the cache (see narrow_scatter_records_kernel): one thread per
-// (record, vector), the rank of a record's ordinal recomputed per vector from the L2-resident bitmap prefix.
-__global__ void __launch_bounds__(256) wide_scatter_records_kernel(const uint4 *rows, const u64 *ords, u64 n, int nvec,
-                                                                   const uint32_t *bitmap, const uint32_t *sb_rank,
-                                                                   uint4 *store, u64 *store_ords, u64 base) {
+// Appends records published by OTHER owners to the cache: the rows go to the tail of the row log in the order they
+// arrived (a coalesced copy), and loc[] / ords[] of the id the ordinal ranks at point there.
+__global__ void __launch_bounds__(256) wide_append_records_kernel(const uint4 *rows, const u64 *ords, u64 n, int nvec,
+                                                                  const uint32_t *bitmap, const uint32_t *sb_rank, uint4 *store,
+                                                                  u64 log_at, u64 *loc, u64 *store_ords, u64 base) {
     const u64 total = n * (u64)nvec;
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
+        store[log_at * nvec + t] = rows[t];
         const u64 k = t / nvec;
-        const int p = (int)(t - k * nvec);
-        const u64 ord = ords[k];
-        const u64 gid = base + ordinal_rank(bitmap, sb_rank, ord);
-        store[gid * nvec + p] = rows[t];
-        if (p == 0) store_ords[gid] = ord;
+        if (t - k * nvec == 0) {
+            const u64 ord = ords[k];
+            const u64 gid = base + ordinal_rank(bitmap, sb_rank, ord);
+            loc[gid] = log_at + k;
+            store_ords[gid] = ord;
+        }
     }
 }
 
