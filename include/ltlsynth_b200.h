@@ -151,7 +151,10 @@ int ltlb200_reset(ltlb200_engine *e);
  *                     level that holds the separator depends on it
  *   memory_budget_bytes  EngineConfig.memory_budget_mb << 20, applied to the reference's own
  *                     estimate (rows + n*(key_words*8+80), :442-444); 0 = unlimited
- *   deadline_s        absolute CLOCK_MONOTONIC seconds (see ltlb200_now), < 0 = none (:416)
+ *   deadline_s        absolute CLOCK_MONOTONIC seconds (see ltlb200_now), < 0 = none.  The reference polls it
+ *                     before every chunk (:416-417); the device polls it with every tile of candidates a warp
+ *                     starts, so a level stops within a tile of the deadline, keeps what it built until then
+ *                     (the reference's partial level) and the call returns LTLB200_TIME_BUDGET
  * Outputs: *n_new entries appended, *sep_gid id of the level's first fresh separating
  * entry or -1, *constructed_delta the reference's `stats.constructed` increment.
  * A level is appended on every status >= 0 (the reference's `finally: flush()`).

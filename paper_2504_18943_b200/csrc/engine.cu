@@ -283,9 +283,12 @@ __global__ void __launch_bounds__(1024) sb_add_kernel(uint32_t *out, u64 n, cons
     if (i < n) out[i] += block_prefix[blockIdx.x];
 }
 
-__global__ void level_init_kernel(u64 *counters) {
+// counters of a level start at zero (CTR_SEP at "none"); the special-key register persists across levels;
+// `time_left_ns` (all ones = no deadline) anchors the level's deadline on the device's own timer
+__global__ void level_init_kernel(u64 *counters, u64 time_left_ns) {
     const int i = threadIdx.x;
     if (i < CTR_COUNT && i != CTR_SPECIAL) counters[i] = i == CTR_SEP ? VAL_EMPTY : 0ull;
+    if (i == CTR_STOPAT) counters[i] = time_left_ns == VAL_EMPTY ? VAL_EMPTY : global_timer_ns() + time_left_ns;
 }
 
 // number of winners and rank of the separator's ordinal (the separator is counters[CTR_SEP])
@@ -331,6 +334,12 @@ public:
     int level_device(int cost, void **rows_dev, void **ords_dev);
     const uint4 *rows_in_id_order(u64 first, u64 count);
     void set_weights(const int32_t *weights, int count);
+    double deadline_ = -1.0;  // CLOCK_MONOTONIC deadline of the level being built (< 0: none)
+    u64 time_left_ns() const {
+        if (deadline_ < 0) return VAL_EMPTY;
+        const double left = deadline_ - monotonic_s();
+        return left <= 0 ? 1ull : (u64)(left * 1e9);
+    }
     void set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries);
     int entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right);
     void get_stats(ltlb200_stats *out);
@@ -1131,7 +1140,7 @@ void Engine::collect_dead_ranges(const LevelMeta &lv, u64 constructed, u64 batch
     u64 want = std::max<u64>(1ull << 20, constructed / 16), n = 0;
     for (;;) {
         reserve(sep_list_, want, false);
-        level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+        level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_, time_left_ns());
         CUDA_CHECK(cudaGetLastError());
         if (wide_) {
             WideParams Q = wide_params(false);
@@ -1184,6 +1193,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
     CUDA_CHECK(cudaSetDevice(device_));
     set_sharding(1, 0);  // a level built by one handle needs the whole set
+    deadline_ = deadline;
     pending_ = PendingLevel{};
     PendingLevel &pl = pending_;
     pl.lv.base = total_;
@@ -1254,7 +1264,7 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             if (want_slots > table_slots()) rebuild_table(grown_size(want_slots));
             if (exhaustive) reserve(sep_list_, std::max<u64>(std::max<u64>(1ull << 20, constructed / 16), sep_want_), false);
             // counters start at zero (CTR_SEP at "none"); the special-key register persists across levels
-            level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+            level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_, time_left_ns());
             CUDA_CHECK(cudaGetLastError());
             pl.claim_cap = claim_cap;
             if (wide_) {
@@ -1520,6 +1530,10 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
     approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
     levels_.push_back(std::move(lv));
     PHASE(7, "end: bookkeeping", tp);
+    if (h_counters_[CTR_TIMEOUT]) {  // the deadline passed while the level was being built: it holds what was built
+        prune_ok_ = false;           // until then (the reference's partial level, engine.py:416-417 + 447-449)
+        return LTLB200_TIME_BUDGET;
+    }
     if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
     return LTLB200_OK;
 }
@@ -1701,6 +1715,10 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
     approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
     levels_.push_back(std::move(lv));
     PHASE(7, "end: bookkeeping", tp);
+    if (h_counters_[CTR_TIMEOUT]) {  // the deadline passed while the level was being built: it holds what was built
+        prune_ok_ = false;           // until then (the reference's partial level, engine.py:416-417 + 447-449)
+        return LTLB200_TIME_BUDGET;
+    }
     if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
     return LTLB200_OK;
 }
@@ -1762,6 +1780,7 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     if (world < 1 || world > ROUTE_MAX_WORLD || rank < 0 || rank >= world) throw std::invalid_argument("bad shard (at most 8 ranks)");
     CUDA_CHECK(cudaSetDevice(device_));
     set_sharding(world, rank);
+    deadline_ = deadline;
     pending_ = PendingLevel{};
     PendingLevel &pl = pending_;
     pl.lv.base = total_;
@@ -1803,7 +1822,7 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             if (exhaustive) reserve(sep_list_, std::max<u64>(std::max<u64>(1ull << 20, constructed / 16), sep_want_), false);
             reserve(xs_rows_, (u64)world * cap * nvec_, false);
             reserve(xs_ords_, (u64)world * cap, false);
-            level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+            level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_, time_left_ns());
             CUDA_CHECK(cudaGetLastError());
             CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, 16 * sizeof(u64), stream_));
             pl.claim_cap = 0;
@@ -1857,6 +1876,10 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
             break;
         }
         pl.region_cap = cap;
+        if (h_counters_[CTR_TIMEOUT]) {  // the deadline passed while this rank was building its share: the level ends
+            level_abort();               // empty here, and the caller tells the other ranks
+            return LTLB200_TIME_BUDGET;
+        }
     } catch (const MemoryBudget &e) {
         g_last_error = e.what();
         pl.active = false;
@@ -1918,7 +1941,7 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
         const u64 want_slots = next_pow2(2 * (owned + est));
         if (want_slots > table_slots()) rebuild_table(grown_size(want_slots));
         else if (table_dirty_) rebuild_table(table_slots());
-        level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_);
+        level_init_kernel<<<1, 32, 0, stream_>>>(d_counters_, time_left_ns());
         CUDA_CHECK(cudaGetLastError());
         pl.claim_cap = claim_cap;
         if (wide_) {

@@ -126,10 +126,27 @@ struct NarrowParams {
     int route_sep_any;     // the store holds no separating CM: every separating candidate is fresh w.r.t. earlier levels
 };
 
-// [1] claim indices reserved, [2] separator ordinal (min), [3] special-key val (persists across levels),
+// [0] set when the level's deadline passed while it was being built, [15] that deadline on the device's
+// nanosecond timer (all ones = none), [1] claim indices reserved, [2] separator ordinal (min), [3] special-key val (persists across levels),
 // [4] overflow flag, [5] winners (summary), [6] rank of the separator (summary),
 // [7] separating candidates recorded, [8..14] one tile ticket per operator launch
-enum : int { CTR_UNUSED = 0, CTR_CLAIMED = 1, CTR_SEP = 2, CTR_SPECIAL = 3, CTR_OVERFLOW = 4, CTR_WINNERS = 5, CTR_SEPRANK = 6, CTR_SEPCOUNT = 7, CTR_TICKET0 = 8, CTR_COUNT = 16 };
+enum : int { CTR_TIMEOUT = 0, CTR_CLAIMED = 1, CTR_SEP = 2, CTR_SPECIAL = 3, CTR_OVERFLOW = 4, CTR_WINNERS = 5, CTR_SEPRANK = 6, CTR_SEPCOUNT = 7, CTR_TICKET0 = 8, CTR_STOPAT = 15, CTR_COUNT = 16 };
+
+__device__ __forceinline__ u64 global_timer_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// The reference polls its deadline before every chunk of a level (engine.py:416-417); here every warp polls it
+// as it draws tile tickets: past the deadline no further tile is started, what was built so far is kept
+// (the reference's partial level) and the host reports "time budget exhausted".
+__device__ __forceinline__ bool deadline_passed(u64 *counters) {
+    const u64 stop_at = __ldcg(&counters[CTR_STOPAT]);
+    if (stop_at == ~0ull || global_timer_ns() <= stop_at) return false;
+    atomicExch(&counters[CTR_TIMEOUT], 1ull);
+    return true;
+}
 
 __device__ __forceinline__ uint4 ld_cg_u4(const uint4 *p) { return __ldcg(p); }
 
@@ -638,7 +655,11 @@ template <class WS>
 __device__ __forceinline__ bool open_tile(const NarrowParams &P, WS &ws, const TileFetch &f) {
     const int lane = threadIdx.x & 31;
     const u64 ticket = __shfl_sync(0xFFFFFFFFu, f.t, 0);
-    const u64 ovf = __shfl_sync(0xFFFFFFFFu, f.ovf, 0);
+    u64 ovf = f.ovf;
+    // the level's deadline, polled with every 16th ticket a warp draws (a look at it with EVERY ticket cost 4 % of
+    // the kernel: one more word kept alive across the tile in a kernel at its register limit)
+    if (lane == 0 && (f.t & 15ull) == 0ull && deadline_passed(P.counters)) ovf = 1ull;  // start no further tile; the claims stay valid
+    ovf = __shfl_sync(0xFFFFFFFFu, ovf, 0);
     const u64 sep = __shfl_sync(0xFFFFFFFFu, f.sep, 0);
     const u64 t = ovf ? P.tile_end : P.tile_begin + P.shard_offset + ticket * P.shard_stride;
     if (t >= P.tile_end) return false;

@@ -455,7 +455,7 @@ __device__ __forceinline__ bool wide2_next_tile(const WideParams &P, const Wide2
     __syncwarp();
     if (lane == 0) {
         u64 t = P.tile_end;
-        if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
+        if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull && !deadline_passed(P.counters))
             t = P.tile_begin + P.shard_offset + atomicAdd(&P.counters[P.ticket], 1ull) * P.shard_stride;
         W.fx->ticket = t;
         W.fx->sep_now = P.prune_after_sep ? *(volatile u64 *)&P.counters[CTR_SEP] : (u64)~0ull;

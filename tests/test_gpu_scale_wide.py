@@ -220,3 +220,36 @@ def test_device_memory_exhaustion_ends_with_the_reference_outcome():
         assert store.total == stats.unique >= sum(g["n"] for g in gold["levels"])
     finally:
         store.close()
+
+
+def test_deadline_is_polled_inside_a_level():
+    """The reference checks its deadline before every chunk (engine.py:416-417); the device checks it with every tile a
+    warp starts: a level that would run for tens of milliseconds stops a few milliseconds after its deadline, keeps
+    the partial level and reports the reference's failure text."""
+    import time
+
+    spec = workloads.named_workload("c5", 0)
+    cfg = engine.EngineConfig(exhaustive=True, max_cost=12, memory_budget_mb=1 << 22)
+    full = None
+    for budget_s in (None, 0.004):
+        store = engine.CandidateStore(spec)
+        try:
+            stats = engine.RunStats()
+            for cost in range(1, 12):
+                engine.expand_level(store, cost, cfg.operators, config=cfg, stats=stats)
+            t0 = time.perf_counter()
+            if budget_s is None:
+                engine.expand_level(store, 12, cfg.operators, config=cfg, stats=stats)  # also allocates the buffers of level 12
+                full = (store.level(12).n, time.perf_counter() - t0)
+            else:
+                with pytest.raises(engine._BudgetExceeded, match="time budget exhausted"):
+                    engine.expand_level(store, 12, cfg.operators, config=cfg, stats=stats, deadline=t0 + budget_s)
+                elapsed = time.perf_counter() - t0
+                assert 0 < store.level(12).n < full[0], "the partial level was not kept"
+                assert elapsed < 0.020, f"the level ran {1e3 * elapsed:.1f} ms past a {1e3 * budget_s:.0f} ms deadline"
+                rows, _ = store.level_device(12)  # what was stored is still a set of distinct rows
+                h1, h2 = _row_hashes(rows)
+                order = __import__("torch").argsort(h1)
+                assert not bool(((h1[order][1:] == h1[order][:-1]) & (h2[order][1:] == h2[order][:-1])).any())
+        finally:
+            store.close()
