@@ -187,9 +187,10 @@ int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int3
  *                           separator ordinal
  *   ltlb200_winners_export  this owner's winners with ordinal <= sep_ord, as dense records
  *   [all-gather]            every rank receives the winners of the OTHER owners (ltlb200_exchange_recv again)
- *   ltlb200_level_commit    ids from the global bitmap; own winners and the n_received records appended to the
- *                           cache; outputs as ltlb200_expand_level (`seps`: every separating ordinal of the level,
- *                           host array, exhaustive runs).
+ *   ltlb200_level_commit    ids from the global bitmap; own winners and the received records appended to the
+ *                           cache (recv_counts[k], k < n_sources <= 8: how many records each source sent, in the
+ *                           order they sit in the receive buffers); outputs as ltlb200_expand_level (`seps`: every
+ *                           separating ordinal of the level, host array, exhaustive runs).
  *
  * A non-exhaustive level over a store that already holds a separating CM is refused (the reference's chunk
  * truncation, engine.py:334-335, needs the whole set): build it with ltlb200_expand_level on every rank.
@@ -201,8 +202,8 @@ int ltlb200_route_begin(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int32
 int ltlb200_exchange_recv(ltlb200_engine *e, uint64_t n_records, void **rows_dev, void **ords_dev);
 int ltlb200_owner_reduce(ltlb200_engine *e, uint64_t n_records, uint64_t *n_claimed, void **bitmap_dev, uint64_t *bitmap_words);
 int ltlb200_winners_export(ltlb200_engine *e, uint64_t sep_ord, uint64_t *n_winners, void **rows_dev, void **ords_dev);
-int ltlb200_level_commit(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, uint64_t n_received,
-                         int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
+int ltlb200_level_commit(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, const uint64_t *recv_counts,
+                         int32_t n_sources, int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
                          int64_t *constructed_delta);
 /* Ends the pending routed level empty: another rank ran out of its time or memory budget (statuses 1 / 2 of
  * ltlb200_route_begin / ltlb200_owner_reduce), and every rank stops or none does. */

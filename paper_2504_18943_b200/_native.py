@@ -135,7 +135,7 @@ def load():
     L.ltlb200_level_abort.restype = ctypes.c_int
     L.ltlb200_level_abort.argtypes = [p]
     L.ltlb200_level_commit.restype = ctypes.c_int
-    L.ltlb200_level_commit.argtypes = [p, u64, p, u64, u64, i64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.ltlb200_level_commit.argtypes = [p, u64, p, u64, p, i32, i64, u64, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.ltlb200_seps_copy.restype = i64
     L.ltlb200_seps_copy.argtypes = [p, p, u64]
     L.ltlb200_key_bytes.restype = i32

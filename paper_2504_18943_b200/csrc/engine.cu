@@ -358,8 +358,9 @@ public:
     int owner_reduce(u64 n_records, u64 *n_claimed, void **bitmap_dev, u64 *bitmap_words);
     void level_abort();
     void winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void **ords_dev);
-    int level_commit(u64 sep_ord, const u64 *seps, u64 n_seps, u64 n_received, int64_t batch, u64 mem_budget, int64_t *n_new,
-                     int64_t *sep_gid, int64_t *constructed_delta);
+    int level_commit(u64 sep_ord, const u64 *seps, u64 n_seps, const u64 *recv_counts, int n_sources, int64_t batch, u64 mem_budget,
+                     int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta);
+    RecordSources sources_{};  // layout of the winners received from the other owners (level_commit)
     u64 seps_copy(u64 *out, u64 cap);
     int key_bytes() const { return 16 * nvec_; }
     int num_levels() const { return (int)levels_.size(); }
@@ -1488,10 +1489,10 @@ int Engine::finalize_level(u64 sep_ord, const u64 *seps, u64 n_seps, int64_t bat
         }
         CUDA_CHECK(cudaGetLastError());
         if (n_received) {  // what the other owners published
-            const u64 work = n_received * (u64)(wide_ ? nvec_ : 1);
+            const u64 work = sources_.longest * (u64)sources_.n * (u64)(wide_ ? nvec_ : 1);
             const int rgrid = (int)std::max<u64>(1, std::min<u64>((work + 255) / 256, (u64)sm_count_ * 16));
-            if (wide_) wide_append_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, nvec_, bitmap_.ptr, sb_rank_.ptr, store_.ptr, log_tail_ + n_claimed, loc_.ptr, ords_.ptr, total_);
-            else narrow_scatter_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, n_received, bitmap_.ptr, sb_rank_.ptr, store_.ptr, ords_.ptr, total_);
+            if (wide_) wide_append_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, sources_, nvec_, bitmap_.ptr, sb_rank_.ptr, store_.ptr, log_tail_ + n_claimed, loc_.ptr, ords_.ptr, total_);
+            else narrow_scatter_records_kernel<<<rgrid, 256, 0, stream_>>>(xr_rows_.ptr, xr_ords_.ptr, sources_, bitmap_.ptr, sb_rank_.ptr, store_.ptr, ords_.ptr, total_);
             CUDA_CHECK(cudaGetLastError());
             st_.kernel_launches++;
         }
@@ -2069,11 +2070,23 @@ void Engine::winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void *
     *ords_dev = xs_ords_.ptr;
 }
 
-int Engine::level_commit(u64 sep_ord, const u64 *seps, u64 n_seps, u64 n_received, int64_t batch, u64 mem_budget, int64_t *n_new,
-                         int64_t *sep_gid, int64_t *constructed_delta) {
+int Engine::level_commit(u64 sep_ord, const u64 *seps, u64 n_seps, const u64 *recv_counts, int n_sources, int64_t batch,
+                         u64 mem_budget, int64_t *n_new, int64_t *sep_gid, int64_t *constructed_delta) {
     PendingLevel &pl = pending_;
     if (!pl.active || !pl.routed) throw std::invalid_argument("level_commit outside a routed level");
     if (pl.constructed && !pl.reduced) throw std::invalid_argument("level_commit needs owner_reduce and winners_export first");
+    if (n_sources < 0 || n_sources > 8 || (n_sources && !recv_counts)) throw std::invalid_argument("level_commit: at most 8 sources");
+    // the receive buffers hold the winners of the other owners source by source (dense)
+    sources_ = RecordSources{};
+    u64 n_received = 0;
+    for (int k = 0; k < n_sources; ++k) {
+        if (recv_counts[k] == 0) continue;
+        sources_.offsets[sources_.n] = n_received;
+        sources_.counts[sources_.n] = recv_counts[k];
+        sources_.longest = std::max<u64>(sources_.longest, recv_counts[k]);
+        sources_.n++;
+        n_received += recv_counts[k];
+    }
     // (counters as owner_reduce left them: CTR_CLAIMED = this owner's claims)
     return finalize_level(sep_ord, seps, n_seps, batch, mem_budget, n_new, sep_gid, constructed_delta, true, n_received);
 }
@@ -2364,13 +2377,13 @@ int ltlb200_winners_export(ltlb200_engine *e, uint64_t sep_ord, uint64_t *n_winn
     });
 }
 
-int ltlb200_level_commit(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, uint64_t n_received,
-                         int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
+int ltlb200_level_commit(ltlb200_engine *e, uint64_t sep_ord, const uint64_t *seps, uint64_t n_seps, const uint64_t *recv_counts,
+                         int32_t n_sources, int64_t batch_size, uint64_t memory_budget_bytes, int64_t *n_new, int64_t *sep_gid,
                          int64_t *constructed_delta) {
     if (!e || !n_new || !sep_gid || !constructed_delta) return LTLB200_ERR_ARGUMENT;
     return guarded([&] {
-        return e->impl->level_commit(sep_ord, (const ltlb200::u64 *)seps, n_seps, n_received, batch_size, memory_budget_bytes,
-                                     n_new, sep_gid, constructed_delta);
+        return e->impl->level_commit(sep_ord, (const ltlb200::u64 *)seps, n_seps, (const ltlb200::u64 *)recv_counts, n_sources,
+                                     batch_size, memory_budget_bytes, n_new, sep_gid, constructed_delta);
     });
 }
 

@@ -183,13 +183,36 @@ __global__ void __launch_bounds__(256) narrow_winners_kernel(const uint4 *claim_
     }
 }
 
+// Where the records of the other owners sit in the receive buffers: source s sent counts[s] records starting at
+// record offsets[s].  The sources are walked in step (record i of source 0, of source 1, ...).  Measured on c3 to
+// cost 15 with 8 ranks played on one GPU (tools/shard_model.py): it does NOT make the scatter cheaper than walking
+// one source after the other (4.2 vs 4.3 ms for 54.6 M received records) -- an owner's winners are not in ordinal
+// order, so the two 8/16-byte stores per record stay random; what would help is publishing the winners bucketed
+// by ordinal range ("what limits the scaling").
+struct RecordSources {
+    unsigned long long offsets[8], counts[8];
+    unsigned long long longest;  // max of counts
+    int n;
+};
+
+__device__ __forceinline__ bool interleaved_record(const RecordSources &S, u64 v, u64 &rec) {
+    const u64 i = v / (u64)S.n;
+    const int s = (int)(v - i * (u64)S.n);
+    if (i >= S.counts[s]) return false;
+    rec = S.offsets[s] + i;
+    return true;
+}
+
 // Appends records published by OTHER owners to the cache: position = rank of the ordinal in the level's global
 // winners bitmap (the all-reduced union of every owner's marks), exactly as narrow_scatter_kernel places this
 // owner's own claims.
-__global__ void __launch_bounds__(256) narrow_scatter_records_kernel(const uint4 *rows, const u64 *ords, u64 n,
+__global__ void __launch_bounds__(256) narrow_scatter_records_kernel(const uint4 *rows, const u64 *ords, const RecordSources S,
                                                                      const uint32_t *bitmap, const uint32_t *sb_rank,
                                                                      uint4 *store, u64 *store_ords, u64 base) {
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (u64)gridDim.x * blockDim.x) {
+    const u64 total = S.longest * (u64)S.n;
+    for (u64 v = (u64)blockIdx.x * blockDim.x + threadIdx.x; v < total; v += (u64)gridDim.x * blockDim.x) {
+        u64 t;
+        if (!interleaved_record(S, v, t)) continue;
         const u64 ord = ords[t];
         const u64 gid = base + ordinal_rank(bitmap, sb_rank, ord);
         store[gid] = rows[t];

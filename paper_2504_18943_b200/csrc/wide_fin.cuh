@@ -119,19 +119,23 @@ __global__ void __launch_bounds__(256) wide_winners_kernel(const uint4 *stage_ro
     }
 }
 
-// Appends records published by OTHER owners to the cache: the rows go to the tail of the row log in the order they
-// arrived (a coalesced copy), and loc[] / ords[] of the id the ordinal ranks at point there.
-__global__ void __launch_bounds__(256) wide_append_records_kernel(const uint4 *rows, const u64 *ords, u64 n, int nvec,
+// Appends records published by OTHER owners to the cache: the rows go to the tail of the row log (record t at
+// log_at + t), and loc[] / ords[] of the id the ordinal ranks at point there.  The sources are walked in step
+// (see RecordSources in narrow_fin.cuh) so that the loc / ords writes of all of them land in the same region.
+__global__ void __launch_bounds__(256) wide_append_records_kernel(const uint4 *rows, const u64 *ords, const RecordSources S, int nvec,
                                                                   const uint32_t *bitmap, const uint32_t *sb_rank, uint4 *store,
                                                                   u64 log_at, u64 *loc, u64 *store_ords, u64 base) {
-    const u64 total = n * (u64)nvec;
-    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (u64)gridDim.x * blockDim.x) {
-        store[log_at * nvec + t] = rows[t];
-        const u64 k = t / nvec;
-        if (t - k * nvec == 0) {
-            const u64 ord = ords[k];
+    const u64 total = S.longest * (u64)S.n * (u64)nvec;
+    for (u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (u64)gridDim.x * blockDim.x) {
+        const u64 v = x / nvec;
+        const int p = (int)(x - v * nvec);
+        u64 t;
+        if (!interleaved_record(S, v, t)) continue;
+        store[(log_at + t) * nvec + p] = rows[t * nvec + p];
+        if (p == 0) {
+            const u64 ord = ords[t];
             const u64 gid = base + ordinal_rank(bitmap, sb_rank, ord);
-            loc[gid] = log_at + k;
+            loc[gid] = log_at + t;
             store_ords[gid] = ord;
         }
     }

@@ -86,9 +86,9 @@ class ShardEngine(Protocol):
     def separating_ordinals(self) -> torch.Tensor:
         """int64 tensor of every separating ordinal this rank recorded in the pending level"""
 
-    def level_commit(self, sep_ord: int, seps, n_received: int, batch_size: int, memory_budget_bytes: int):
+    def level_commit(self, sep_ord: int, seps, recv_counts: list[int], batch_size: int, memory_budget_bytes: int):
         """-> (status, n_new, sep_gid or None, constructed_delta); the global bitmap is in owner_reduce's tensor,
-        the first n_received records of the receive buffers are the winners of the other owners"""
+        the receive buffers hold the winners of the other owners, recv_counts[k] records from the k-th source"""
 
     # optional: without these two every level goes through the exchange
     def level_candidates(self, cost: int, op_mask: int) -> int: ...
@@ -194,7 +194,7 @@ def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfi
         sep_counts = [m[2] for m in meta]
         seps = torch.empty((sum(sep_counts),), dtype=torch.int64, device=device)
         _exchange([(seps_mine,)] * world, (seps,), sep_counts, group, include_self=True)
-    status, n_new, sep_gid, delta = store.level_commit(sep_ord, seps, n_received, config.batch_size,
+    status, n_new, sep_gid, delta = store.level_commit(sep_ord, seps, [c for c in win_counts if c], config.batch_size,
                                                        config.memory_budget_mb << 20)
     flag = torch.tensor([status], dtype=torch.int64, device=device)
     dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)  # (a rank whose device filled up while appending)

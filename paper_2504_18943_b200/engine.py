@@ -385,15 +385,17 @@ class CandidateStore:
         _native.check(int(got), "seps_copy")
         return torch.from_numpy(host[: int(got)].astype(np.int64)).to(self.torch_device)
 
-    def level_commit(self, sep_ord, seps, n_received, batch_size, memory_budget_bytes):
+    def level_commit(self, sep_ord, seps, recv_counts, batch_size, memory_budget_bytes):
+        """``recv_counts``: how many winners each other owner sent, in the order they sit in the receive buffers."""
         self._wait_for_torch()
+        counts = (ctypes.c_uint64 * max(1, len(recv_counts)))(*recv_counts)
         n_new, sep, delta = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         seps_ptr, n_seps = None, 0
         if seps is not None:
             host = np.ascontiguousarray(seps.detach().cpu().numpy().astype(np.uint64))
             seps_ptr, n_seps = host.ctypes.data, len(host)
         status = _native.check(
-            _native.load().ltlb200_level_commit(self._handle, int(sep_ord), seps_ptr, n_seps, int(n_received),
+            _native.load().ltlb200_level_commit(self._handle, int(sep_ord), seps_ptr, n_seps, counts, len(recv_counts),
                                                 int(batch_size), int(memory_budget_bytes), ctypes.byref(n_new),
                                                 ctypes.byref(sep), ctypes.byref(delta)),
             "level_commit",

@@ -236,8 +236,9 @@ class CpuShardEngine:
     def separating_ordinals(self):
         return torch.tensor(self._pending["seps"], dtype=torch.int64)
 
-    def level_commit(self, sep_ord, seps, n_received, batch_size, memory_budget_bytes):
+    def level_commit(self, sep_ord, seps, recv_counts, batch_size, memory_budget_bytes):
         p = self._pending
+        n_received = sum(recv_counts)
         rows, ords = p["recv"] if n_received else (None, None)
         items = [(o, k) for k, o in p["winners"]]
         for k in range(n_received):

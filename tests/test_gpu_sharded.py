@@ -57,7 +57,7 @@ def _exchange_level(stores, cost, cfg):
             rows[at:at + k].copy_(w_rows)
             ords[at:at + k].copy_(w_ords)
             at += k
-        received.append(n)
+        received.append([w[1].shape[0] for w in others if w[1].shape[0]])
     torch.cuda.synchronize()
     seps = torch.cat([s.separating_ordinals() for s in stores]) if cfg.exhaustive else None
     return [s.level_commit(sep, seps, received[r], cfg.batch_size, 0) for r, s in enumerate(stores)]

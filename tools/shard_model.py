@@ -63,7 +63,7 @@ def exchange_level(stores, cost, cfg, acc):
             rows[at:at + k].copy_(w_rows)
             ords[at:at + k].copy_(w_ords)
             at += k
-        received.append(n)
+        received.append([w[1].shape[0] for w in others if w[1].shape[0]])
         acc["gather_bytes_per_rank"] += n * (key_bytes + 8) / world
     torch.cuda.synchronize()
     seps = torch.cat([s.separating_ordinals() for s in stores]) if cfg.exhaustive else None
