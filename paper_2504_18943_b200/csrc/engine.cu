@@ -29,8 +29,11 @@
 #include <vector>
 
 #include "../../include/ltlsynth_b200.h"
+#include <deque>
+
 #include "launch.h"
 #include "narrow_fin.cuh"
+#include "narrow_tiny.cuh"
 #include "wide2.cuh"
 #include "wide_fin.cuh"
 
@@ -334,6 +337,23 @@ public:
     int level_device(int cost, void **rows_dev, void **ords_dev);
     const uint4 *rows_in_id_order(u64 first, u64 count);
     void set_weights(const int32_t *weights, int count);
+    // Tiny levels built ahead of the caller by ONE launch (narrow_tiny.cuh) and handed out one expand_level call
+    // at a time: the rows, ordinals and set entries of these levels are on the device already; levels_ / total_
+    // learn about a level when it is handed out.
+    struct Lookahead {
+        int cost;
+        u64 n_new, sep_ord, sep_rank;
+    };
+    std::deque<Lookahead> lookahead_;
+    uint32_t la_mask_ = 0;
+    bool la_exhaustive_ = false;
+    bool tiny_off_ = false;  // an exhaustive level held a separating candidate: so will the following ones (until reset)
+    DeviceArray<u64> tiny_tab_, tiny_results_;
+    bool tiny_eligible(int cost, uint32_t op_mask, bool exhaustive);
+    void tiny_run(int cost, uint32_t op_mask, bool exhaustive);
+    int tiny_reveal(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline, int64_t *n_new,
+                    int64_t *sep_gid, int64_t *constructed_delta);
+    void discard_lookahead();
     double deadline_ = -1.0;  // CLOCK_MONOTONIC deadline of the level being built (< 0: none)
     u64 time_left_ns() const {
         if (deadline_ < 0) return VAL_EMPTY;
@@ -678,6 +698,8 @@ Engine::~Engine() {
     release(scan_tmp_);
     release(sep_list_);
     release(misc_);
+    release(tiny_tab_);
+    release(tiny_results_);
     release(guide_);
     release(xchg_);
     release(xs_rows_);
@@ -764,6 +786,8 @@ void Engine::rebuild_table(u64 slots) {
 // Forget every level but keep the device buffers (and the hash set's capacity) for the next search.
 void Engine::reset() {
     CUDA_CHECK(cudaSetDevice(device_));
+    lookahead_.clear();
+    tiny_off_ = false;
     levels_.clear();
     total_ = 0;
     log_tail_ = 0;
@@ -1730,6 +1754,10 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     *n_new = 0;
     *sep_gid = -1;
     *constructed_delta = 0;
+    // levels the tiny-levels kernel built ahead (same operators, same mode), or a new run of it
+    if (!lookahead_.empty() && (lookahead_.front().cost != cost || la_mask_ != op_mask || la_exhaustive_ != exhaustive)) discard_lookahead();
+    if (lookahead_.empty() && tiny_eligible(cost, op_mask, exhaustive)) tiny_run(cost, op_mask, exhaustive);
+    if (!lookahead_.empty()) return tiny_reveal(cost, op_mask, exhaustive, batch, mem_budget, deadline, n_new, sep_gid, constructed_delta);
     u64 n_claimed = 0, sep_ord = VAL_EMPTY, n_seps = 0;
     static const bool defer = getenv("LTLB200_NO_DEFER") == nullptr;
     mode_batch_ = batch;  // (collect_dead_ranges needs the reference's chunk schedule)
@@ -1746,6 +1774,161 @@ int Engine::expand_level(int cost, uint32_t op_mask, bool exhaustive, int64_t ba
     mode_batch_ = 0;
     if (rc != LTLB200_OK) return rc;
     return level_end(sep_ord, nullptr, 0, batch, mem_budget, n_new, sep_gid, constructed_delta);
+}
+
+// ---- tiny levels: several levels per launch (narrow_tiny.cuh) --------------------------------------------------
+
+// LTLB200_TINY=0: every level through its own expand_level launches
+static bool tiny_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LTLB200_TINY");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool Engine::tiny_eligible(int cost, uint32_t op_mask, bool exhaustive) {
+    if (!tiny_enabled() || tiny_off_ || wide_ || pending_.active || cost != (int)levels_.size() + 1 || cost > 60) return false;
+    if (!exhaustive && store_has_separator_) return false;  // the chunk-truncation regime (collect_dead_ranges)
+    LevelMeta lv;
+    u64 constructed = 0, n_tiles = 0;
+    plan_level(cost, op_mask, lv, constructed, n_tiles);
+    const u64 slots = std::max<u64>(table_slots(), kMinSlots);
+    return constructed <= TINY_MAX_CANDIDATES && (int)lv.blocks.size() <= TINY_MAX_BLOCKS && 2 * (total_ + constructed) <= slots;
+}
+
+// Builds level `cost` and as many following levels as stay tiny, in one launch; queues their sizes.
+void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
+    CUDA_CHECK(cudaSetDevice(device_));
+    set_sharding(1, 0);
+    try {
+        if (table_dirty_) rebuild_table(table_slots());
+        const u64 claim_cap = (u64)TINY_MAX_CANDIDATES + (u64)TINY_WARPS * CLAIM_CHUNK + 1024;
+        const u64 growth = (u64)TINY_MAX_LEVELS * TINY_MAX_CANDIDATES;  // at most what the levels of one launch can store
+        reserve(claim_key_, claim_cap, false);
+        reserve(claim_ord_, claim_cap, false);
+        reserve(store_, total_ + growth, true, total_);
+        reserve(ords_, total_ + growth, true, total_);
+        reserve(tiny_tab_, 2 * 128, false);
+        reserve(tiny_results_, 5 * (TINY_MAX_LEVELS + 1), false);
+    } catch (const MemoryBudget &) {
+        return;  // (the usual path reports the memory budget)
+    }
+    const u64 claim_cap = (u64)TINY_MAX_CANDIDATES + (u64)TINY_WARPS * CLAIM_CHUNK + 1024;
+    std::vector<u64> tab(2 * 128, 0);
+    for (size_t c = 1; c <= levels_.size(); ++c) {
+        tab[2 * c] = levels_[c - 1].n;
+        tab[2 * c + 1] = levels_[c - 1].base;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(tiny_tab_.ptr, tab.data(), tab.size() * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaMemsetAsync(tiny_results_.ptr, 0, 5 * (TINY_MAX_LEVELS + 1) * sizeof(u64), stream_));
+    CUDA_CHECK(cudaMemsetAsync(claim_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+    st_.h2d_bytes += tab.size() * sizeof(u64);
+    pending_ = PendingLevel{};
+    pending_.claim_cap = claim_cap;
+    pending_.cost = cost;
+    TinyParams T{};
+    T.P = narrow_params(exhaustive);
+    T.P.ords = nullptr;  // (no associativity pruning here: it needs the block lists of the stored levels)
+    T.P.sep_list = exhaustive ? d_counters_ : nullptr;  // capacity 0: separating candidates are only counted
+    T.P.sep_list_cap = 0;
+    T.store = store_.ptr;
+    T.store_ords = ords_.ptr;
+    T.level_tab = tiny_tab_.ptr;
+    T.results = reinterpret_cast<TinyLevelResult *>(tiny_results_.ptr);
+    T.total = total_;
+    T.table_slots = table_slots();
+    T.op_mask = op_mask;
+    T.n_atoms = n_atoms_;
+    T.cost_first = cost;
+    T.cost_last = std::min(cost + TINY_MAX_LEVELS - 1, 62);
+    T.exhaustive = exhaustive ? 1 : 0;
+    for (int k = 0; k < 16; ++k) T.weights[k] = weights_[k];
+    CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+    switch (lw_) {
+        case LW_REGEX: narrow_tiny_1(T, device_, stream_); break;
+        case 8: narrow_tiny_8(T, device_, stream_); break;
+        case 16: narrow_tiny_16(T, device_, stream_); break;
+        case 32: narrow_tiny_32(T, device_, stream_); break;
+        default: narrow_tiny_64(T, device_, stream_); break;
+    }
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+    std::vector<u64> res(5 * (TINY_MAX_LEVELS + 1));
+    CUDA_CHECK(cudaMemcpyAsync(res.data(), tiny_results_.ptr, res.size() * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += res.size() * sizeof(u64);
+    st_.kernel_launches++;
+    st_.enumerate_launches++;
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+    st_.enumerate_ms += ms;
+    recycle_retired(false);
+    const int asked = T.cost_last - T.cost_first + 1;
+    int built = 0;
+    while (built < asked && res[5 * built] == TINY_BUILT) {
+        lookahead_.push_back(Lookahead{cost + built, res[5 * built + 1], res[5 * built + 2], res[5 * built + 3]});
+        DBG("tiny level %d: %llu new, %.1f us", cost + built, (unsigned long long)res[5 * built + 1], 1e-3 * (double)res[5 * built + 4]);
+        ++built;
+    }
+    la_mask_ = op_mask;
+    la_exhaustive_ = exhaustive;
+    // a level the kernel started but left to the host (set / claim arrays too small, an exhaustive level with a
+    // separating candidate) has its claims in the set: rebuild it from the cache before the next level
+    const u64 why = res[5 * TINY_MAX_LEVELS];
+    if (built < asked && why != TINY_END_BIG) table_dirty_ = true;
+    // once an exhaustive search holds a separating CM, (nearly) every later level contains a separating candidate,
+    // and each of them would be built here only to be handed to the host: stop trying on this store
+    if (why == TINY_END_SEPARATOR) tiny_off_ = true;
+    DBG("tiny levels: asked %d from cost %d, built %d (end reason %llu)", asked, cost, built, (unsigned long long)why);
+}
+
+// Hands out the first queued level: the bookkeeping of level_end, with the block list replayed on the host.
+int Engine::tiny_reveal(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline, int64_t *n_new,
+                        int64_t *sep_gid, int64_t *constructed_delta) {
+    if (deadline >= 0 && monotonic_s() > deadline) {  // engine.py:416-417, before the first chunk
+        discard_lookahead();
+        prune_ok_ = false;
+        levels_.push_back(LevelMeta{0, total_, {}});
+        return LTLB200_TIME_BUDGET;
+    }
+    const Lookahead la = lookahead_.front();
+    lookahead_.pop_front();
+    if (prune_mask_ == 0) prune_mask_ = op_mask;
+    else if (prune_mask_ != op_mask) prune_ok_ = false;
+    LevelMeta lv;
+    lv.base = total_;
+    u64 constructed = 0, n_tiles = 0;
+    plan_level(cost, op_mask, lv, constructed, n_tiles);
+    lv.n = la.n_new;
+    const bool found_cut = !exhaustive && la.sep_ord != VAL_EMPTY;
+    if (la.sep_ord != VAL_EMPTY) {
+        store_has_separator_ = true;
+        *sep_gid = (int64_t)(total_ + la.sep_rank);
+    }
+    if (found_cut) {
+        prune_ok_ = false;    // the level keeps only what precedes its separator: no longer complete
+        table_dirty_ = true;  // claims ordered after the separator stay flagged in the set
+    }
+    *constructed_delta = (int64_t)(found_cut ? constructed_through(lv, la.sep_ord, (u64)batch) : constructed);
+    st_.enumerate_candidates += constructed;
+    last_constructed_ = constructed;
+    *n_new = (int64_t)lv.n;
+    total_ += lv.n;
+    st_.constructed += (u64)*constructed_delta;
+    st_.unique = total_;
+    approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442
+    levels_.push_back(std::move(lv));
+    if (mem_budget && approx_bytes_ > mem_budget) return LTLB200_MEMORY_BUDGET;  // engine.py:443-444
+    return LTLB200_OK;
+}
+
+// Levels built ahead that the caller does not want after all (other operators, another mode, a sharded level):
+// their rows lie beyond total_ and are simply overwritten; their set entries go with a rebuild.
+void Engine::discard_lookahead() {
+    if (lookahead_.empty()) return;
+    lookahead_.clear();
+    table_dirty_ = true;
 }
 
 // ---- one search sharded over several GPUs ----------------------------------------------------------------------
@@ -1780,6 +1963,7 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
     if (world < 1 || world > ROUTE_MAX_WORLD || rank < 0 || rank >= world) throw std::invalid_argument("bad shard (at most 8 ranks)");
     CUDA_CHECK(cudaSetDevice(device_));
+    discard_lookahead();
     set_sharding(world, rank);
     deadline_ = deadline;
     pending_ = PendingLevel{};

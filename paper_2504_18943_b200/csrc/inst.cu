@@ -9,7 +9,7 @@
 #if LTLB200_INST_WIDE
 #include "wide2.cuh"
 #else
-#include "narrow.cuh"
+#include "narrow_tiny.cuh"
 #endif
 
 #ifndef LTLB200_INST_LW
@@ -66,6 +66,20 @@ void LTLB200_CAT(narrow_launch_, LTLB200_INST_LW)(int kind, int op, const Narrow
 void LTLB200_CAT(narrow_probe_, LTLB200_INST_LW)(const NarrowParams &P, const void *rows, const void *ords, unsigned long long n,
                                                  int grid, cudaStream_t st) {
     narrow_probe_kernel<LW><<<grid, CTA_THREADS, 0, st>>>(P, (const uint4 *)rows, (const u64 *)ords, n);
+}
+
+void LTLB200_CAT(narrow_tiny_, LTLB200_INST_LW)(const TinyParams &T, int device, cudaStream_t st) {
+    constexpr size_t smem = sizeof(WarpSharedTiny) * TINY_WARPS;
+    {   // opt in to > 48 KB of dynamic shared memory: a per-device attribute of the kernel
+        static std::mutex mu;
+        static unsigned long long seen = 0;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!(seen >> (device & 63) & 1ull)) {
+            cudaFuncSetAttribute(narrow_tiny_levels_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            seen |= 1ull << (device & 63);
+        }
+    }
+    narrow_tiny_levels_kernel<LW><<<1, TINY_THREADS, smem, st>>>(T);
 }
 
 int LTLB200_CAT(narrow_occupancy_, LTLB200_INST_LW)() {

@@ -13,6 +13,7 @@ namespace ltlb200 {
 
 struct NarrowParams;
 struct WideParams;
+struct TinyParams;
 
 // which kernel of a (lane width) set: one launch per operator (big levels), one launch for every
 // operator (levels up to kSmallLevel candidates), the guarded kernel (scan pass / dead ranges), and -- one search
@@ -22,6 +23,7 @@ enum : int { LK_OPERATOR = 0, LK_SMALL = 1, LK_GUARDED = 2, LK_ROUTE = 3 };
 #define LTLB200_DECLARE_LW(LW)                                                                                     \
     void narrow_launch_##LW(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st);                    \
     int narrow_occupancy_##LW();                                                                                    \
+    void narrow_tiny_##LW(const TinyParams &T, int device, cudaStream_t st); /* several tiny levels in one launch */ \
     void narrow_probe_##LW(const NarrowParams &P, const void *rows, const void *ords, unsigned long long n, int grid, \
                            cudaStream_t st);                                                                         \
     void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \

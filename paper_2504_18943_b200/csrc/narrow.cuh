@@ -142,7 +142,7 @@ __device__ __forceinline__ u64 global_timer_ns() {
 // as it draws tile tickets: past the deadline no further tile is started, what was built so far is kept
 // (the reference's partial level) and the host reports "time budget exhausted".
 __device__ __forceinline__ bool deadline_passed(u64 *counters) {
-    const u64 stop_at = __ldcg(&counters[CTR_STOPAT]);
+    const u64 stop_at = *(volatile const u64 *)&counters[CTR_STOPAT];  // (generic: the tiny-levels kernel keeps its counters in shared memory)
     if (stop_at == ~0ull || global_timer_ns() <= stop_at) return false;
     atomicExch(&counters[CTR_TIMEOUT], 1ull);
     return true;
@@ -418,6 +418,26 @@ __device__ __forceinline__ void insert_batch(const NarrowParams &P, Parked *queu
     while (st.qfill >= 32u) drain_round(P, queue, st);
 }
 
+// rank of an ordinal among the level's winners: bits set before it in the winners bitmap (one bit per ordinal,
+// exclusive popcount prefixes per 1024-bit superblock)
+__device__ __forceinline__ u64 ordinal_rank(const uint32_t *bitmap, const uint32_t *sb_rank, u64 ord) {
+    const u64 word = ord >> 5, sb = word >> 5;
+    u64 rank = sb_rank[sb];
+    for (u64 w = sb << 5; w < word; ++w) rank += __popc(bitmap[w]);
+    return rank + __popc(bitmap[word] & ((1u << (ord & 31)) - 1u));
+}
+
+// operand rows come through the read-only path, except in a kernel that writes rows itself (narrow_tiny.cuh)
+template <class S, class = void>
+struct sink_coherent_rows : std::false_type {};
+template <class S>
+struct sink_coherent_rows<S, std::void_t<decltype(S::kCoherentRows)>> : std::bool_constant<S::kCoherentRows> {};
+template <class Sink>
+__device__ __forceinline__ uint4 ld_row(const uint4 *p) {
+    if constexpr (sink_coherent_rows<Sink>::value) return __ldcg(p);
+    else return __ldg(p);
+}
+
 template <class S, class = void>
 struct sink_is_guarded : std::false_type {};
 template <class S>
@@ -468,7 +488,7 @@ __device__ __forceinline__ bool run_unary_tile(const NarrowParams &P, WS &ws, Si
         for (int r = 0; r < PROBE_BATCH; ++r) {
             const u64 i = first + (u64)(g + r) * TILE_V;
             live[r] = g + r < n_groups && i < n;
-            x[r] = live[r] ? __ldg(src + i) : make_uint4(0, 0, 0, 0);
+            x[r] = live[r] ? ld_row<Sink>(src + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
@@ -533,7 +553,7 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
     __syncwarp();
     for (int k = lane; k < s_cnt; k += 32) {
         const u64 s = s0 + k;
-        ws.rows[k] = __ldg(sc_rows + s);
+        ws.rows[k] = ld_row<Sink>(sc_rows + s);
         // scalar-row part of the ordinal; the lane part is j (VEC_B) or ord0 + i*nb (!VEC_B)
         u64 term = !VEC_B ? s : ord0 + (tri ? s * na - (s ? (s * (s - 1)) / 2 : 0) - s : s * nb);
         if (prune && sc_hi > sc_lo) {
@@ -544,14 +564,14 @@ __device__ __forceinline__ bool run_binary_tile(const NarrowParams &P, WS &ws, S
     }
     __syncwarp();
     // the vector row of the NEXT group is loaded while this group is processed
-    uint4 xv_next = v0 + lane < n_vec ? __ldg(vec_rows + v0 + lane) : make_uint4(0, 0, 0, 0);
+    uint4 xv_next = v0 + lane < n_vec ? ld_row<Sink>(vec_rows + v0 + lane) : make_uint4(0, 0, 0, 0);
 #pragma unroll 1
     for (uint32_t vg = 0; vg < vg_n; ++vg) {
         const u64 v = v0 + (u64)vg * TILE_V + lane;
         if (v0 + (u64)vg * TILE_V >= n_vec) break;
         const bool v_ok = v < n_vec;
         const uint4 xv = xv_next;
-        if (vg + 1 < vg_n && v + TILE_V < n_vec) xv_next = __ldg(vec_rows + v + TILE_V);
+        if (vg + 1 < vg_n && v + TILE_V < n_vec) xv_next = ld_row<Sink>(vec_rows + v + TILE_V);
         bool skip_v = false;
         if (prune && vec_hi > vec_lo && v_ok) {
             const u64 o = __ldg(vec_ords + v);

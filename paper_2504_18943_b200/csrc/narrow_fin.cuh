@@ -49,13 +49,6 @@ __global__ void __launch_bounds__(256) narrow_mark_kernel(const FinalizeParams F
     }
 }
 
-__device__ __forceinline__ u64 ordinal_rank(const uint32_t *bitmap, const uint32_t *sb_rank, u64 ord) {
-    const u64 word = ord >> 5, sb = word >> 5;
-    u64 rank = sb_rank[sb];
-    for (u64 w = sb << 5; w < word; ++w) rank += __popc(bitmap[w]);
-    return rank + __popc(bitmap[word] & ((1u << (ord & 31)) - 1u));
-}
-
 __global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParams F) {
     u64 n_claimed, ord_limit;
     if (!finalize_bounds(F, n_claimed, ord_limit)) return;

@@ -1,0 +1,336 @@
+// narrow_tiny.cuh -- the tiny levels of a search, SEVERAL LEVELS IN ONE LAUNCH.
+//
+// The first levels of every search hold tens to thousands of candidates.  Built one expand_level call at a time
+// each of them costs ~75 us of launches and one host synchronisation around ~10 us of work: 1 ms of the 6.3 ms of
+// the paper's 7+7 example, and nearly all of a small search (a divide-and-conquer leaf, BASELINE configs[0]).
+// The host needs nothing from a level but its size to plan the next one -- and the device can do that planning
+// itself.  This kernel is ONE CTA that, level after level,
+//
+//   plans      the canonical block list of the level from the sizes of the stored levels (the same blocks, in
+//              the same order, with the same ordinals as Engine::plan_level on the host, which replays the
+//              planning afterwards from the sizes reported here; reference _tasks_for_level, engine.py:219-266),
+//   enumerates it with the tile runners and insert_batch of the big kernels, its warps drawing tiles,
+//   finalises  it in shared memory (winners bitmap -> ranks -> rows and ordinals appended to the cache),
+//
+// until a level would exceed TINY_MAX_CANDIDATES candidates, finds a separator, or needs the host (hash set or claim
+// arrays too small; an exhaustive level that holds a separating candidate, whose reported separator depends on the
+// reference's chunk schedule).  The host hands the levels out one expand_level call at a time (Engine::tiny_*),
+// so callers see no difference -- results are bit-identical, which every parity test checks, since every search
+// starts here.
+#pragma once
+#include "narrow.cuh"
+
+namespace ltlb200 {
+
+constexpr int TINY_WARPS = 16;  // measured on spec2 level 8 (13.9 K candidates): 8 warps 172 us, 16 warps 125 us, 32 warps 153 us (64 registers)
+constexpr int TINY_TILE_S = 32;  // scalar rows per tile here (the big kernels stage up to TILE_S = 128)
+constexpr int TINY_THREADS = 32 * TINY_WARPS;
+constexpr uint32_t TINY_MAX_CANDIDATES = 1u << 15;  // winners bitmap of a level: 4 KiB of shared memory
+constexpr int TINY_MAX_BLOCKS = 64;
+constexpr int TINY_MAX_LEVELS = 24;
+
+// status of one level: not built (the host builds it the usual way) / built
+enum : unsigned long long { TINY_NOT_BUILT = 0ull, TINY_BUILT = 1ull };
+// why the launch ended before cost_last (results[TINY_MAX_LEVELS].status): the next level is too big for one CTA or
+// for the set as it is; the claim arrays / the set overflowed; an exhaustive level holds a separating candidate
+enum : unsigned long long { TINY_END_NONE = 0ull, TINY_END_BIG = 1ull, TINY_END_OVERFLOW = 2ull, TINY_END_SEPARATOR = 3ull };
+
+struct TinyLevelResult {
+    u64 status, n_new, sep_ord, sep_rank;
+    u64 ns;  // device time of the level (LTLB200_DEBUG prints it)
+};
+
+struct TinyParams {
+    NarrowParams P;      // ords = nullptr (no pruning); blocks is replaced by the kernel's shared-memory block list
+    uint4 *store;        // writable alias of P.store
+    u64 *store_ords;     // winning ordinal of every entry of the cache
+    const u64 *level_tab;  // [2c] = n(c), [2c + 1] = base(c) by cost c >= 1: the stored levels (cost < cost_first)
+    TinyLevelResult *results;  // [cost - cost_first]
+    u64 total;           // entries of the cache before cost_first
+    u64 table_slots;
+    uint32_t op_mask;
+    int n_atoms, cost_first, cost_last, exhaustive;
+    int weights[16];
+};
+
+// per-warp shared state with the row area of a tiny tile: 6 KB instead of 8.3 KB, so that 32 warps fit one SM
+struct __align__(16) WarpSharedTiny {
+    Parked queue[QUEUE_CAP];
+    uint4 rows[TINY_TILE_S];
+    u64 term[TINY_TILE_S];
+    BlockDesc block;
+    u64 ticket, sep_now;
+};
+
+// tile runners instantiated with this sink read operand rows with ld.cg: the rows of a level are written by this
+// very kernel, which rules out the read-only path
+struct TinySink {
+    static constexpr bool kCoherentRows = true;
+    const NarrowParams &P;
+    WarpSharedTiny &ws;
+    WarpState &st;
+    template <int LW, typename OrdOf>
+    __device__ __forceinline__ void emit(const uint4 (&cand)[PROBE_BATCH], const bool (&live)[PROBE_BATCH],
+                                         const bool (&known)[PROBE_BATCH], OrdOf ord_of) {
+        insert_batch<LW>(P, ws.queue, st, cand, live, known, ord_of);
+    }
+};
+
+// one block of the level's canonical order; tiles are small so that sixteen warps share even a tiny block
+__device__ __forceinline__ void tiny_push(BlockDesc *blocks, int &n_blocks, u64 &constructed, u64 &n_tiles, BlockDesc b) {
+    if (b.size == 0) return;
+    if (n_blocks >= TINY_MAX_BLOCKS) {
+        constructed = ~0ull;  // too many blocks: the host builds this level
+        return;
+    }
+    if (b.kind == BK_UNARY) {
+        b.tile_s = 4;
+        b.vg = 1;
+        b.tiles_v = (b.na + (u64)TILE_V * 4 - 1) / ((u64)TILE_V * 4);
+        b.tiles_s = 1;
+    } else {
+        const u64 n_vec = b.vec_is_b ? b.nb : b.na, n_sc = b.vec_is_b ? b.na : b.nb;
+        b.tile_s = (uint32_t)(n_sc < TINY_TILE_S ? n_sc : TINY_TILE_S);
+        b.tiles_s = (n_sc + b.tile_s - 1) / b.tile_s;
+        b.vg = 1;
+        b.tiles_v = (n_vec + TILE_V - 1) / TILE_V;
+    }
+    b.ord0 = constructed;
+    b.tile0 = n_tiles;
+    constructed += b.size;
+    n_tiles += b.tiles_v * b.tiles_s;
+    blocks[n_blocks++] = b;
+}
+
+// Engine::plan_level on the device (same blocks, same order, same ordinals; tile geometry is private to a launch)
+__device__ inline void tiny_plan(const TinyParams &T, BlockDesc *blocks, int cost, const u64 *level_tab, int &n_blocks, u64 &constructed,
+                                 u64 &n_tiles) {
+    n_blocks = 0;
+    constructed = 0;
+    n_tiles = 0;
+    const int *w = T.weights;
+    auto n_of = [&](int c) { return level_tab[2 * c]; };
+    auto base_of = [&](int c) { return level_tab[2 * c + 1]; };
+    if (cost == w[OP_ATOM]) {
+        BlockDesc b{};
+        b.op = OP_ATOM;
+        b.kind = BK_UNARY;
+        b.from_atoms = 1;
+        b.na = (u64)T.n_atoms;
+        b.size = b.na;
+        tiny_push(blocks, n_blocks, constructed, n_tiles, b);
+    }
+    const int unary_tags[6] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY, OP_RE_QUESTION, OP_RE_STAR};
+    const int binary_tags[4] = {OP_AND, OP_UNTIL, OP_RE_CONCAT, OP_OR};
+    for (int k = 0; k < 6; ++k) {
+        const int tag = unary_tags[k];
+        if (!(T.op_mask >> tag & 1u) || cost - w[tag] < 1) continue;
+        const int src = cost - w[tag];
+        if (n_of(src) == 0) continue;
+        BlockDesc b{};
+        b.op = (uint32_t)tag;
+        b.kind = BK_UNARY;
+        b.a_off = base_of(src);
+        b.na = n_of(src);
+        b.size = b.na;
+        tiny_push(blocks, n_blocks, constructed, n_tiles, b);
+        if (constructed == ~0ull) return;
+    }
+    for (int k = 0; k < 4; ++k) {
+        const int tag = binary_tags[k];
+        if (!(T.op_mask >> tag & 1u)) continue;
+        const bool commutative = tag == OP_AND || tag == OP_OR;
+        for (int c1 = 1; c1 < cost - w[tag]; ++c1) {
+            const int c2 = cost - w[tag] - c1;
+            if (commutative && c1 > c2) break;
+            const u64 na = n_of(c1), nb = n_of(c2);
+            if (na == 0 || nb == 0) continue;
+            BlockDesc b{};
+            b.op = (uint32_t)tag;
+            b.a_off = base_of(c1);
+            b.na = na;
+            b.b_off = base_of(c2);
+            b.nb = nb;
+            if (commutative && c1 == c2) {
+                b.kind = BK_TRI;
+                b.vec_is_b = 1;
+                b.size = na * (na + 1) / 2;
+            } else {
+                b.kind = BK_RECT;
+                b.vec_is_b = nb >= na;
+                b.size = na * nb;
+            }
+            b.c_left = (uint32_t)c1;
+            tiny_push(blocks, n_blocks, constructed, n_tiles, b);
+            if (constructed == ~0ull) return;
+        }
+    }
+}
+
+// fetch_tile for counters that live in shared memory (volatile generic loads instead of ld.global.cg)
+__device__ __forceinline__ TileFetch tiny_fetch_tile(const NarrowParams &P) {
+    TileFetch f;
+    if ((threadIdx.x & 31) == 0) {
+        f.ovf = *(volatile u64 *)&P.counters[CTR_OVERFLOW];
+        f.t = atomicAdd(&P.counters[P.ticket], 1ull);
+        if (P.prune_after_sep) f.sep = *(volatile u64 *)&P.counters[CTR_SEP];
+    }
+    return f;
+}
+
+struct TinyControl {  // CTA-wide decisions of thread 0
+    int go;           // build this level
+    int n_blocks;
+    u64 constructed, n_tiles, base;
+    u64 n_claimed, ord_limit, sep_ord;
+    int stop_after;
+    u64 t0;
+};
+
+template <int LW>
+__global__ void __launch_bounds__(TINY_THREADS, 1) narrow_tiny_levels_kernel(const TinyParams T) {
+    extern __shared__ __align__(16) unsigned char s_tiny_raw[];
+    WarpSharedTiny *s_warp = reinterpret_cast<WarpSharedTiny *>(s_tiny_raw);
+    __shared__ NarrowParams sQ;
+    __shared__ TinyControl ctl;
+    __shared__ BlockDesc s_blocks[TINY_MAX_BLOCKS];  // the level's block list (planned here, read by open_tile)
+    __shared__ u64 s_tab[2 * 64];                    // n(c), base(c) of every level so far
+    __shared__ uint32_t s_bitmap[TINY_MAX_CANDIDATES / 32];
+    __shared__ uint32_t s_sbrank[TINY_MAX_CANDIDATES / 1024 + 1];
+    __shared__ u64 s_counters[CTR_COUNT];  // the level's counters live in shared memory here: every claim-index chunk, tile
+                                           // ticket and separator update is a shared-memory atomic, not a trip to the L2
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    WarpSharedTiny &ws = s_warp[warp];
+    u64 *counters = s_counters;
+    if (tid == 0) {
+        sQ = T.P;
+        sQ.blocks = s_blocks;
+        sQ.counters = s_counters;
+        s_counters[CTR_SPECIAL] = T.P.counters[CTR_SPECIAL];  // the all-ones key's register persists across levels and launches
+        ctl.base = T.total;
+    }
+    for (int k = tid; k < 2 * 64; k += TINY_THREADS) s_tab[k] = k < 2 * T.cost_first ? T.level_tab[k] : 0ull;
+    __syncthreads();
+    for (int cost = T.cost_first; cost <= T.cost_last; ++cost) {
+        // ---- plan (thread 0) and reset the level's counters
+        if (tid == 0) {
+            int n_blocks;
+            u64 constructed, n_tiles;
+            ctl.t0 = global_timer_ns();
+            tiny_plan(T, s_blocks, cost, s_tab, n_blocks, constructed, n_tiles);
+            ctl.go = 1;
+            // the host builds levels that are too big for one CTA, or for the set / the claim arrays as they are
+            if (constructed == ~0ull || constructed > TINY_MAX_CANDIDATES || 2 * (ctl.base + constructed) > T.table_slots ||
+                constructed + (u64)TINY_WARPS * CLAIM_CHUNK > T.P.claim_cap) {
+                ctl.go = 0;
+                T.results[TINY_MAX_LEVELS].status = TINY_END_BIG;
+            }
+            ctl.n_blocks = n_blocks;
+            ctl.constructed = constructed;
+            ctl.n_tiles = n_tiles;
+            for (int i = 0; i < CTR_COUNT; ++i)
+                if (i != CTR_SPECIAL) counters[i] = (i == CTR_SEP || i == CTR_STOPAT) ? VAL_EMPTY : 0ull;
+            sQ.block_begin = 0;
+            sQ.block_end = n_blocks;
+            sQ.tile_begin = 0;
+            sQ.tile_end = n_tiles;
+            sQ.ticket = CTR_TICKET0;
+            sQ.epoch = (u64)cost << EPOCH_SHIFT;
+        }
+        __syncthreads();
+        if (!ctl.go) break;
+        if (ctl.constructed == 0) {  // an empty level (e.g. below the atoms' weight)
+            if (tid == 0) {
+                s_tab[2 * cost] = 0;
+                s_tab[2 * cost + 1] = ctl.base;
+                T.results[cost - T.cost_first] = TinyLevelResult{TINY_BUILT, 0, VAL_EMPTY, VAL_EMPTY, 0};
+            }
+            __syncthreads();
+            continue;
+        }
+        // ---- enumerate: the warps draw the level's tiles
+        {
+            WarpState st;
+            TinySink sink{sQ, ws, st};
+            TileFetch next = tiny_fetch_tile(sQ);
+            for (;;) {
+                const TileFetch cur = next;
+                if (!open_tile(sQ, ws, cur)) break;
+                next = tiny_fetch_tile(sQ);
+                if (run_tile_any<LW>(sQ, ws, sink)) break;
+            }
+            if (*(volatile u64 *)&counters[CTR_OVERFLOW] == 0ull)
+                while (st.qfill > 0u) drain_round(sQ, ws.queue, st);
+        }
+        __threadfence();
+        __syncthreads();
+        // ---- does the host have to take over?
+        if (tid == 0) {
+            const u64 sep = counters[CTR_SEP];
+            ctl.n_claimed = counters[CTR_CLAIMED];
+            ctl.sep_ord = sep;
+            ctl.go = 1;
+            if (counters[CTR_OVERFLOW] || ctl.n_claimed > T.P.claim_cap) {
+                ctl.go = 0;
+                T.results[TINY_MAX_LEVELS].status = TINY_END_OVERFLOW;
+            }
+            // an exhaustive level with a separating candidate reports "the first chunk whose first separating
+            // candidate is fresh" (engine.py:331,425-433): chunk schedule and batch size are the host's business
+            if (T.exhaustive && counters[CTR_SEPCOUNT]) {
+                ctl.go = 0;
+                T.results[TINY_MAX_LEVELS].status = TINY_END_SEPARATOR;
+            }
+            ctl.ord_limit = (!T.exhaustive && sep != VAL_EMPTY) ? sep : VAL_EMPTY - 1;
+            ctl.stop_after = (!T.exhaustive && sep != VAL_EMPTY) ? 1 : 0;
+        }
+        __syncthreads();
+        if (!ctl.go) break;  // (the host rebuilds the set: this level's claims are in it)
+        // ---- finalise in shared memory: winners bitmap -> ranks -> append
+        const u64 n_bits = ctl.constructed, n_words = (n_bits + 31) >> 5, n_sb = (n_words + 31) >> 5;
+        const u64 n_claimed = ctl.n_claimed, ord_limit = ctl.ord_limit, base = ctl.base;
+        for (u64 w = tid; w < n_sb * 32; w += TINY_THREADS) s_bitmap[w] = 0u;
+        __syncthreads();
+        for (u64 t = tid; t < n_claimed; t += TINY_THREADS) {
+            const u64 ord = __ldcg(&T.P.claim_ord[t]);
+            if (ord <= ord_limit) atomicOr(&s_bitmap[ord >> 5], 1u << (ord & 31));
+        }
+        __syncthreads();
+        if (warp == 0) {  // exclusive popcount prefix per 1024-bit superblock (at most 32 of them)
+            uint32_t v = 0;
+            if ((u64)lane < n_sb)
+                for (int k = 0; k < 32; ++k) v += __popc(s_bitmap[lane * 32 + k]);
+            uint32_t incl = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= d) incl += t;
+            }
+            s_sbrank[lane] = incl - v;
+        }
+        __syncthreads();
+        for (u64 t = tid; t < n_claimed; t += TINY_THREADS) {
+            const u64 ord = __ldcg(&T.P.claim_ord[t]);
+            if (ord > ord_limit) continue;  // unused index, or ordered after the separator
+            const u64 gid = base + ordinal_rank(s_bitmap, s_sbrank, ord);
+            T.store[gid] = __ldcg(&T.P.claim_key[t]);
+            T.store_ords[gid] = ord;
+        }
+        for (u64 t = tid; t < n_claimed; t += TINY_THREADS) T.P.claim_ord[t] = VAL_EMPTY;  // clean for the next level
+        if (tid == 0) {
+            const u64 winners = ordinal_rank(s_bitmap, s_sbrank, n_bits - 1) + ((s_bitmap[(n_bits - 1) >> 5] >> ((n_bits - 1) & 31)) & 1u);
+            const u64 sep = ctl.sep_ord;
+            s_tab[2 * cost] = winners;
+            s_tab[2 * cost + 1] = base;
+            T.results[cost - T.cost_first] =
+                TinyLevelResult{TINY_BUILT, winners, sep, sep < n_bits ? ordinal_rank(s_bitmap, s_sbrank, sep) : VAL_EMPTY,
+                                global_timer_ns() - ctl.t0};
+            ctl.base = base + winners;
+        }
+        __threadfence();
+        __syncthreads();
+        if (ctl.stop_after) break;
+    }
+    if (tid == 0) T.P.counters[CTR_SPECIAL] = s_counters[CTR_SPECIAL];
+}
+
+}  // namespace ltlb200

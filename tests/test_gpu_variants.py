@@ -6,6 +6,8 @@ cases in a child process:
   LTLB200_NO_DEFER=1    two synchronisations per level (finalisation launched after the counters
                         were read) instead of the deferred, device-bounded finalisation
   LTLB200_PRUNE=0       no associativity pruning: every AND candidate is probed
+  LTLB200_TINY=0        every level through its own launches, instead of the tiny levels of a search built several
+                        per launch by narrow_tiny_levels_kernel (the default, which every other test therefore runs)
   LTLB200_OPSTREAMS=0   every operator launch of a level on the engine's own stream, one after the
                         other, instead of fanned out over side streams (the default)
 
@@ -38,7 +40,8 @@ print("variant ok")
 
 @pytest.mark.parametrize("switch,value,cases", [("LTLB200_NO_DEFER", "1", CASES + WIDE_CASES),
                                                  ("LTLB200_OPSTREAMS", "0", CASES + WIDE_CASES),
-                                                 ("LTLB200_PRUNE", "0", CASES)])
+                                                 ("LTLB200_PRUNE", "0", CASES),
+                                                 ("LTLB200_TINY", "0", CASES + ["spec1_found_b1", "spec1_or_found", "c1_s0", "c1_s3", "w32n_s2_found", "w64n_s3_found"])])
 def test_variant_matches_reference(switch, value, cases):
     env = dict(os.environ)
     env[switch] = value
