@@ -290,6 +290,7 @@ def kernel_numbers(arm, steps) -> dict:
     peak, peak_src = measured_peaks()
     achieved = alg / (enum_ms * 1e-3) / 1e9 if enum_ms > 0 else 0.0
     return dict(enum_ms=enum_ms, fin_ms=(after["finalize_ms"] - before["finalize_ms"]) / steps,
+                tiny_ms=(after.get("tiny_ms", 0.0) - before.get("tiny_ms", 0.0)) / steps,
                 enum_launches=(after["enumerate_launches"] - before["enumerate_launches"]) // steps,
                 launches=(after["kernel_launches"] - before["kernel_launches"]) // steps,
                 alg_bytes=alg, achieved=achieved, peak=peak, peak_src=peak_src, frac=achieved / peak)
@@ -406,7 +407,8 @@ def main() -> int:
                            "unique_per_step": a["stats"].unique, "constructed_per_step": a["stats"].constructed,
                            "max_cost_reached": a["stats"].max_cost_reached, "cm_bytes": a["after"]["row_bytes"],
                            "device_bytes": a["after"]["device_bytes"], "kernel_ms_per_step": kk["enum_ms"],
-                           "finalize_ms_per_step": kk["fin_ms"], "roofline_frac": kk["frac"], "steps": 2, "warmup": 1}
+                           "finalize_ms_per_step": kk["fin_ms"], "tiny_levels_ms_per_step": kk["tiny_ms"],
+                           "roofline_frac": kk["frac"], "steps": 2, "warmup": 1}
         _native.load().ltlb200_trim(local_rank)
 
     if rank != 0:
@@ -485,6 +487,7 @@ def main() -> int:
             "bound": "hbm", "achieved": k["achieved"], "peak": k["peak"], "unit": "GB/s", "frac": k["frac"],
             "traffic": traffic, "kernel": kernel_name,
             "launches_per_step": int(k["enum_launches"]), "kernel_ms_per_step": k["enum_ms"], "finalize_ms_per_step": k["fin_ms"],
+            "tiny_levels_ms_per_step": k["tiny_ms"],
             "algorithmic_bytes_per_step": k["alg_bytes"], "peak_source": k["peak_src"],
             "traffic_source": traffic_src,
             "random_probe": probe,

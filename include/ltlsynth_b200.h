@@ -80,6 +80,8 @@ typedef struct ltlb200_stats {
     double probe_ms;             /* sharded search: device time of the owner-side insert-or-min (phase B; also in enumerate_ms) */
     uint64_t routed_records;     /* records this handle sent to hash owners */
     uint64_t received_records;   /* records this handle folded into its part of the set */
+    double tiny_ms;              /* device time of the launches that build several tiny levels each (plan + enumerate +
+                                    finalise; not part of enumerate_ms / finalize_ms) */
 } ltlb200_stats;
 
 /* ABI version of the loaded library (== LTLB200_ABI_VERSION it was built with). */

@@ -79,6 +79,7 @@ class Stats(ctypes.Structure):
         ("probe_ms", ctypes.c_double),
         ("routed_records", ctypes.c_uint64),
         ("received_records", ctypes.c_uint64),
+        ("tiny_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -1859,10 +1859,9 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     st_.d2h_bytes += res.size() * sizeof(u64);
     st_.kernel_launches++;
-    st_.enumerate_launches++;
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
-    st_.enumerate_ms += ms;
+    st_.tiny_ms += ms;
     recycle_retired(false);
     const int asked = T.cost_last - T.cost_first + 1;
     int built = 0;
