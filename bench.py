@@ -28,7 +28,8 @@ Numbers on the line:
                     installed there by ``__graft_entry__.build()``; else the C port ``oracle/ltl_oracle.c``) timed on
                     this host on a bounded sample of the same workload;
 * ``workloads``     (N = 1) BASELINE configs[2], [3], [4] in short device-resident runs: ``c3-fill`` (<= 128-bit CMs
-                    until the set cannot grow), ``c4-1024`` (1024-bit CMs), ``c5-12`` (LTL, 128-byte CMs, cost 12).
+                    until the set cannot grow), ``c4-1024`` (1024-bit CMs), ``c5-12`` (LTL, 128-byte CMs, cost 12) and
+                    ``c5-fill`` (the same until the device is full: cost 13, 536 M CMs).
 
 ``--impl reference`` times the reference's CPU implementation alone (rank 0; the other ranks exit).
 Only that leg and ``cpu_baseline`` touch ``oracle/``; the measured product path never does.
@@ -65,13 +66,16 @@ WORKLOADS = {
     "spec1": dict(max_cost=10, exhaustive=True, sample_cost=10),
     "c5": dict(max_cost=10, exhaustive=True, sample_cost=9),
     "c5-12": dict(max_cost=12, exhaustive=True, sample_cost=9, base="c5"),
+    # BASELINE configs[4] until the device is full: cost 13 stores 536.5 M CMs of 128 bytes (68.7 GB of rows, 114 GB in
+    # all); cost 14 would need a hash set beyond 2^32 slots and ends the run with "memory budget exhausted"
+    "c5-fill": dict(max_cost=14, exhaustive=True, sample_cost=9, base="c5"),
     "c4-512": dict(max_cost=10, exhaustive=True, sample_cost=9),
     "c4-1024": dict(max_cost=10, exhaustive=True, sample_cost=9),
     "c4-1024-11": dict(max_cost=11, exhaustive=True, sample_cost=9, base="c4-1024"),
 }
 DEFAULT_WORKLOAD = {1: "spec2"}
 DEFAULT_SHARDED_WORKLOAD = "c3-16"
-EXTRA_WORKLOADS = ("c3-fill", "c4-1024-11", "c5-12")
+EXTRA_WORKLOADS = ("c3-fill", "c4-1024-11", "c5-12", "c5-fill")
 OPERATORS = "not,next,future,and,until"
 
 
@@ -228,12 +232,14 @@ def search_loop(store, cfg, expand):
 
     store.reset()
     stats, found = engine.RunStats(), None
+    stats.levels_built = 0  # (levels whose candidates were constructed: a level that ran out of memory is not one)
     for cost in range(1, cfg.max_cost + 1):
         stats.max_cost_reached = cost
         try:
             _, sep = expand(store, cost, cfg, stats)
         except engine._BudgetExceeded:  # the cache filled the device: the search ends here (outcome "exhausted")
             break
+        stats.levels_built = cost
         if sep is not None and found is None:
             found = (sep, cost)
             if not cfg.exhaustive:
@@ -270,7 +276,7 @@ def device_arm(name, seed, device, stream, steps, warmup, expand, sync, clocks_i
             sampler.__exit__()
         after = store.device_stats()
         out = dict(spec=spec, cfg=cfg, stats=stats, found=found, device_ms=start.elapsed_time(stop), before=before, after=after,
-                   clocks=sampler.summary() if sampler else None, levels=[store.level(c).n for c in range(1, len(store.levels) + 1)])
+                   clocks=sampler.summary() if sampler else None, levels=[store.level(c).n for c in range(1, stats.levels_built + 1)])
         out["witness"] = None
         if found:
             from paper_2504_18943_b200 import to_text

@@ -725,7 +725,7 @@ u64 Engine::grown_size(u64 want_slots) const {
     const u64 slot_bytes = wide_ ? sizeof(u64) : sizeof(Slot16);
     const u64 want_bytes = want_slots * slot_bytes;
     u64 grown = want_slots * (want_bytes >= (1ull << 30) ? 2 : want_bytes >= (256ull << 20) ? 4 : 8);
-    while (grown > want_slots && grown * slot_bytes > budget_ / 4) grown /= 2;
+    while (grown > want_slots && (grown * slot_bytes > budget_ / 4 || grown > (1ull << 32) - 2)) grown /= 2;  // (slot indices are 32-bit)
     return grown;
 }
 
@@ -1262,7 +1262,10 @@ int Engine::level_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
         u64 est = constructed;
         if (constructed > kExact) {
             double u = 1.0;
-            if (levels_.size() >= 2 && last_constructed_ > 0) u = std::min(1.0, 1.5 * (double)levels_.back().n / (double)last_constructed_ + 0.02);
+            // (head-room x1.5 over the previous level's uniqueness; x1.2 for levels of more than 2^28 candidates, whose
+            // staging is tens of GB -- uniqueness moves by a few per cent from level to level, and a wrong guess is redone)
+            const double head = constructed > (1ull << 28) ? 1.2 : 1.5;
+            if (levels_.size() >= 2 && last_constructed_ > 0) u = std::min(1.0, head * (double)levels_.back().n / (double)last_constructed_ + 0.02);
             // LTLB200_EST_SCALE (tests): scales the guess so that the overflow -> regrow -> redo path runs
             static const double scale = [] {
                 const char *e = getenv("LTLB200_EST_SCALE");
