@@ -442,6 +442,8 @@ private:
     // regex front-end (regex_ops.cuh): the infix-split guide table on the device; n_bits_ > 0 = regex grammar
     DeviceArray<uint32_t> guide_;
     int n_bits_ = 0;
+    uint32_t guide_smem_words_ = 0;  // wide kernels: the tables are staged in the CTA's shared memory (LTLB200_GUIDE_SMEM=1)
+    uint32_t guide_entries_ = 0, guide_rounds_ = 0;
     // Non-exhaustive level over a store that already holds a separating CM (narrow path, one GPU): the chunks
     // the reference truncates at a separating candidate are found by a scan pass and their tails excluded
     // from the enumeration (NarrowParams::dead).  batch_size is known to expand_level only.
@@ -668,8 +670,8 @@ Engine::Engine(int T, int lane_bits, const uint64_t *masks, const uint64_t *targ
         auto it = cache.find({device_, lw_, nvec_});
         if (it == cache.end()) {
             int occ;
-            if (wide_) occ = lw_ == 8 ? wide2_occupancy_8(nvec_, device_) : lw_ == 16 ? wide2_occupancy_16(nvec_, device_)
-                             : lw_ == 32 ? wide2_occupancy_32(nvec_, device_) : wide2_occupancy_64(nvec_, device_);
+            if (wide_) occ = lw_ == 8 ? wide2_occupancy_8(nvec_, device_, 0) : lw_ == 16 ? wide2_occupancy_16(nvec_, device_, 0)
+                             : lw_ == 32 ? wide2_occupancy_32(nvec_, device_, 0) : wide2_occupancy_64(nvec_, device_, 0);
             else occ = lw_ == 8 ? narrow_occupancy_8() : lw_ == 16 ? narrow_occupancy_16() : lw_ == 32 ? narrow_occupancy_32() : narrow_occupancy_64();
             it = cache.emplace(std::make_tuple(device_, lw_, nvec_), occ).first;
         }
@@ -814,7 +816,7 @@ void Engine::plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &construc
     n_tiles = 0;
     // tile geometry: narrow = one lane per vector row; wide = one group of G lanes per vector row
     const u64 tile_v = (u64)TILE_V;
-    const u64 tile_s_max = wide_ ? (u64)wide2_tile_s(nvec_) : (u64)TILE_S;
+    const u64 tile_s_max = wide_ ? (u64)wide2_tile_s(nvec_, lw_ == LW_REGEX) : (u64)TILE_S;
     const u64 tile_max = (u64)TILE_V * TILE_S;  // candidates of a full-size tile
     // A block is cut into at least ~4 tiles per resident warp so that small levels still
     // spread over the whole GPU instead of a few warps grinding through full-size tiles.
@@ -1104,8 +1106,9 @@ void Engine::launch_narrow(int kind, int op, const NarrowParams &P, int grid, cu
 }
 
 void Engine::launch_wide(int kind, int op, const WideParams &P, int grid, cudaStream_t st) {
-    const size_t smem = wide2_warp_vecs(nvec_) * sizeof(uint4) * WARPS_PER_CTA;
+    const size_t smem = wide2_warp_vecs(nvec_, lw_ == LW_REGEX) * sizeof(uint4) * WARPS_PER_CTA + (size_t)guide_smem_words_ * sizeof(uint32_t);
     switch (lw_) {
+        case LW_REGEX: wide2_launch_1(kind, op, P, grid, smem, device_, st); break;
         case 8: wide2_launch_8(kind, op, P, grid, smem, device_, st); break;
         case 16: wide2_launch_16(kind, op, P, grid, smem, device_, st); break;
         case 32: wide2_launch_32(kind, op, P, grid, smem, device_, st); break;
@@ -1414,6 +1417,11 @@ WideParams Engine::wide_params(bool exhaustive) const {
     P.dead = dead_n_ ? dead_.ptr : nullptr;
     P.dead_n = (uint32_t)dead_n_;
     P.scan_only = 0;
+    P.guide = guide_.ptr;
+    P.n_bits = n_bits_;
+    P.guide_smem_words = guide_smem_words_;
+    P.guide_entries = guide_entries_;
+    P.guide_rounds = guide_rounds_;
     return P;
 }
 
@@ -1964,6 +1972,7 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     if (pending_.active) throw std::invalid_argument("route_begin: the previous level was not ended");
     if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
     if (world < 1 || world > ROUTE_MAX_WORLD || rank < 0 || rank >= world) throw std::invalid_argument("bad shard (at most 8 ranks)");
+    if (wide_ && lw_ == LW_REGEX) throw std::invalid_argument("regex front-end: sequences wider than 128 bits are not sharded over GPUs");
     CUDA_CHECK(cudaSetDevice(device_));
     discard_lookahead();
     set_sharding(world, rank);
@@ -2339,23 +2348,80 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
 // and of the letters); this switches its kernels to the regex operators and uploads the infix-split guide table.
 void Engine::set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries) {
     if (!levels_.empty()) throw std::invalid_argument("the grammar must be set before the first level");
-    if (n_bits < 1 || n_bits > 128 || wide_ || lw_ != 8 || (n_bits + 7) / 8 != row_bytes_)
-        throw std::invalid_argument("regex front-end: this slice takes characteristic sequences of up to 128 bits, created as "
-                                    "ceil(bits / 8) lanes of 8 bits");
+    // (wide2_regex.cuh keeps three row areas of 32 rows per warp in shared memory: 16 vectors = 2048 bits)
+    if (n_bits < 1 || n_bits > 2048 || lw_ != 8 || (n_bits + 7) / 8 != row_bytes_)
+        throw std::invalid_argument("regex front-end: characteristic sequences of up to 2048 bits, created as ceil(bits / 8) "
+                                    "lanes of 8 bits");
     CUDA_CHECK(cudaSetDevice(device_));
-    std::vector<uint32_t> h((size_t)n_bits + 1 + n_entries);
-    memcpy(h.data(), offsets, ((size_t)n_bits + 1) * sizeof(uint32_t));
-    memcpy(h.data() + n_bits + 1, entries, n_entries * sizeof(uint32_t));
-    if (h[n_bits] != n_entries) throw std::invalid_argument("regex guide table: offsets do not end at the entry count");
+    // device layout (wide2_regex.cuh: RegexGuide): the table as given (offsets | entries u | v << 16, sorted by the
+    // result infix w) | w of every entry | the entries grouped by their LEFT part u (offsets | v | w << 16) | grouped
+    // by their RIGHT part v (offsets | u | w << 16) | the entry offsets of the star's rounds.  A round holds the
+    // infixes of one split depth: depth(w) = 1 + max depth(v) over the splits w = u v with u non-empty, which is the
+    // length of w; the star of 32 rows at a time settles one round after the other.
+    if (n_entries > 0xFFFFFFFFull / 8) throw std::invalid_argument("regex guide table: too many entries");
+    const size_t nb1 = (size_t)n_bits + 1, E = (size_t)n_entries;
+    if (offsets[0] != 0 || offsets[n_bits] != n_entries) throw std::invalid_argument("regex guide table: offsets do not span the entries");
+    std::vector<uint32_t> w_of(E), depth(n_bits, 0), left_n(nb1, 0), right_n(nb1, 0);
+    for (int w = 0; w < n_bits; ++w) {
+        if (offsets[w] > offsets[w + 1]) throw std::invalid_argument("regex guide table: offsets are not ascending");
+        for (uint32_t e = offsets[w]; e < offsets[w + 1]; ++e) {
+            const uint32_t u = entries[e] & 0xFFFFu, v = entries[e] >> 16;
+            if (u >= (uint32_t)n_bits || v >= (uint32_t)n_bits) throw std::invalid_argument("regex guide table: infix index out of range");
+            w_of[e] = (uint32_t)w;
+            left_n[u + 1]++;
+            right_n[v + 1]++;
+            if (u != 0u) {
+                if (v >= (uint32_t)w) throw std::invalid_argument("regex guide table: infixes must be sorted by length (a split's right part after the whole)");
+                depth[w] = std::max(depth[w], depth[v] + 1);
+            }
+        }
+        if (w > 0 && depth[w] < depth[w - 1]) throw std::invalid_argument("regex guide table: infixes must be sorted by length");
+    }
+    std::vector<uint32_t> rounds;  // rounds[d] = first entry of the infixes of depth d
+    for (int w = 0; w < n_bits; ++w)
+        while (rounds.size() <= depth[w]) rounds.push_back(offsets[w]);
+    const uint32_t n_rounds = (uint32_t)rounds.size();
+    rounds.push_back((uint32_t)E);
+    std::vector<uint32_t> h;
+    h.reserve(3 * nb1 + 4 * E + rounds.size());
+    h.insert(h.end(), offsets, offsets + nb1);
+    h.insert(h.end(), entries, entries + E);
+    h.insert(h.end(), w_of.begin(), w_of.end());
+    for (int side = 0; side < 2; ++side) {
+        std::vector<uint32_t> &cnt = side == 0 ? left_n : right_n;
+        for (size_t k = 1; k < nb1; ++k) cnt[k] += cnt[k - 1];  // exclusive offsets
+        std::vector<uint32_t> ent(E), at(cnt.begin(), cnt.end() - 1);
+        for (size_t e = 0; e < E; ++e) {
+            const uint32_t u = entries[e] & 0xFFFFu, v = entries[e] >> 16;
+            ent[at[side == 0 ? u : v]++] = (side == 0 ? v : u) | (w_of[e] << 16);
+        }
+        h.insert(h.end(), cnt.begin(), cnt.end());
+        h.insert(h.end(), ent.begin(), ent.end());
+    }
+    h.insert(h.end(), rounds.begin(), rounds.end());
+    guide_entries_ = (uint32_t)E;
+    guide_rounds_ = n_rounds;
     reserve(guide_, h.size(), false);
     CUDA_CHECK(cudaMemcpyAsync(guide_.ptr, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     st_.h2d_bytes += h.size() * sizeof(uint32_t);
     n_bits_ = n_bits;
     lw_ = LW_REGEX;
-    special_possible_ = n_bits == 128;  // only a 128-bit CS can be all ones (the empty-slot marker)
+    special_possible_ = n_bits == 128;  // only a 128-bit CS can be all ones (the empty-slot marker of the narrow set)
     prune_ok_ = false;                  // (the associativity pruning is an argument about LTL's AND)
-    occupancy_ = narrow_occupancy_1();
+    if (wide_) {
+        // LTLB200_GUIDE_SMEM=1: stage the tables in shared memory behind the warps' areas.  Off by default: measured on
+        // the e-mail example (57 KB of tables) the staged copy costs two of the four resident CTAs per SM and the
+        // search to cost 12 gets slower, while the tables read through L1 hit at 95 %
+        const size_t warps = wide2_warp_vecs(nvec_, true) * sizeof(uint4) * WARPS_PER_CTA, table = h.size() * sizeof(uint32_t);
+        const char *env = getenv("LTLB200_GUIDE_SMEM");
+        const bool want = env && atoi(env) != 0;
+        guide_smem_words_ = want && warps + table <= kMaxDynamicSmem ? (uint32_t)h.size() : 0u;
+        if (warps > kMaxDynamicSmem) throw std::invalid_argument("regex front-end: sequences too wide for the shared-memory areas of the wide kernels");
+        occupancy_ = wide2_occupancy_1(nvec_, device_, (int)guide_smem_words_);
+    } else {
+        occupancy_ = narrow_occupancy_1();
+    }
 }
 
 void Engine::set_weights(const int32_t *weights, int count) {

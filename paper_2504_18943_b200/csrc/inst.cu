@@ -94,7 +94,7 @@ int LTLB200_CAT(narrow_occupancy_, LTLB200_INST_LW)() {
 
 #else  // wide
 
-static size_t max_smem() { return wide2_warp_vecs(MAX_NVEC) * sizeof(uint4) * WARPS_PER_CTA; }
+static size_t max_smem() { return LW == LW_REGEX ? kMaxDynamicSmem : wide2_warp_vecs(MAX_NVEC) * sizeof(uint4) * WARPS_PER_CTA; }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a per-DEVICE attribute of a kernel: a process that drives
 // several GPUs (synthesize_dnc(devices=[0, 1]), one store per device) must opt in on each of them.
@@ -115,6 +115,7 @@ static void launch_operator(const WideParams &P, int grid, size_t smem, int devi
     wide2_level_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
 }
 
+#if LTLB200_INST_LW != 1
 template <int OP>
 static void launch_route(const WideParams &P, int grid, size_t smem, int device, cudaStream_t st) {
     static unsigned long long seen = 0;
@@ -122,6 +123,7 @@ static void launch_route(const WideParams &P, int grid, size_t smem, int device,
     opt_in(wide2_route_kernel<LW, OP>, device, seen, mu);
     wide2_route_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
 }
+#endif
 
 void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WideParams &P, int grid, size_t smem, int device,
                                                  cudaStream_t st) {
@@ -139,6 +141,16 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
         wide2_guarded_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
         return;
     }
+#if LTLB200_INST_LW == 1  // the regex front-end's operators (regex_ops.cuh); no sharded search in this slice
+    if (kind == LK_ROUTE) return;
+    switch (op) {
+        case OP_ATOM: launch_operator<OP_ATOM>(P, grid, smem, device, st); break;
+        case OP_RE_QUESTION: launch_operator<OP_RE_QUESTION>(P, grid, smem, device, st); break;
+        case OP_RE_STAR: launch_operator<OP_RE_STAR>(P, grid, smem, device, st); break;
+        case OP_RE_CONCAT: launch_operator<OP_RE_CONCAT>(P, grid, smem, device, st); break;
+        default: launch_operator<OP_OR>(P, grid, smem, device, st); break;
+    }
+#else
     if (kind == LK_ROUTE) {
         switch (op) {
             case OP_ATOM: launch_route<OP_ATOM>(P, grid, smem, device, st); break;
@@ -150,27 +162,29 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
             case OP_GLOBALLY: launch_route<OP_GLOBALLY>(P, grid, smem, device, st); break;
             default: launch_route<OP_OR>(P, grid, smem, device, st); break;
         }
-        return;
+    } else {
+        switch (op) {
+            case OP_ATOM: launch_operator<OP_ATOM>(P, grid, smem, device, st); break;
+            case OP_NOT: launch_operator<OP_NOT>(P, grid, smem, device, st); break;
+            case OP_NEXT: launch_operator<OP_NEXT>(P, grid, smem, device, st); break;
+            case OP_FUTURE: launch_operator<OP_FUTURE>(P, grid, smem, device, st); break;
+            case OP_AND: launch_operator<OP_AND>(P, grid, smem, device, st); break;
+            case OP_UNTIL: launch_operator<OP_UNTIL>(P, grid, smem, device, st); break;
+            case OP_GLOBALLY: launch_operator<OP_GLOBALLY>(P, grid, smem, device, st); break;
+            default: launch_operator<OP_OR>(P, grid, smem, device, st); break;
+        }
     }
-    switch (op) {
-        case OP_ATOM: launch_operator<OP_ATOM>(P, grid, smem, device, st); break;
-        case OP_NOT: launch_operator<OP_NOT>(P, grid, smem, device, st); break;
-        case OP_NEXT: launch_operator<OP_NEXT>(P, grid, smem, device, st); break;
-        case OP_FUTURE: launch_operator<OP_FUTURE>(P, grid, smem, device, st); break;
-        case OP_AND: launch_operator<OP_AND>(P, grid, smem, device, st); break;
-        case OP_UNTIL: launch_operator<OP_UNTIL>(P, grid, smem, device, st); break;
-        case OP_GLOBALLY: launch_operator<OP_GLOBALLY>(P, grid, smem, device, st); break;
-        default: launch_operator<OP_OR>(P, grid, smem, device, st); break;
-    }
+#endif
 }
 
-int LTLB200_CAT(wide2_occupancy_, LTLB200_INST_LW)(int nvec, int device) {
+int LTLB200_CAT(wide2_occupancy_, LTLB200_INST_LW)(int nvec, int device, int guide_smem_words) {
     static unsigned long long seen = 0;
     static std::mutex mu;
-    opt_in(wide2_level_kernel<LW, OP_UNTIL>, device, seen, mu);
+    constexpr int kHeaviest = LW == LW_REGEX ? (int)OP_RE_CONCAT : (int)OP_UNTIL;
+    opt_in(wide2_level_kernel<LW, kHeaviest>, device, seen, mu);
     int occ = 0;
-    const size_t smem = wide2_warp_vecs(nvec) * sizeof(uint4) * WARPS_PER_CTA;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_level_kernel<LW, OP_UNTIL>, CTA_THREADS, smem) != cudaSuccess) {
+    const size_t smem = wide2_warp_vecs(nvec, LW == LW_REGEX) * sizeof(uint4) * WARPS_PER_CTA + (size_t)guide_smem_words * sizeof(uint32_t);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide2_level_kernel<LW, kHeaviest>, CTA_THREADS, smem) != cudaSuccess) {
         cudaGetLastError();
         occ = 1;
     }

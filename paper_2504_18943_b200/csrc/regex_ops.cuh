@@ -12,8 +12,9 @@
 //   star         r*      : bit 0, and bit w = OR over the splits w = u v, u non-empty, of  CS(r)[u] & CS(r*)[v]
 //                          (v is shorter than w and infixes are sorted by length: one pass in index order)
 // The splits come from the GUIDE TABLE the host precomputes: offsets[w] .. offsets[w+1] index entries (u | v << 16)
-// of infix indices.  This slice handles CSs of up to 128 bits (one uint4, the narrow kernels); the table is read
-// through the read-only cache (a few KB, shared by every candidate).
+// of infix indices.  CSs of up to 128 bits are one uint4 and take the operators below (narrow kernels; the table is
+// read through the read-only cache, a few KB shared by every candidate); wider ones (up to 2048 bits) are handled 32
+// candidates at a time on bit-sliced rows (wide2_regex.cuh) with the same table regrouped by Engine::set_regex.
 #pragma once
 #include "cm_ops.cuh"
 
@@ -77,6 +78,7 @@ __device__ __forceinline__ uint4 re_star(const uint32_t *guide, int n_bits, uint
     }
     return out;
 }
+
 
 template <int OP>
 __device__ __forceinline__ uint4 re_apply(const uint32_t *guide, int n_bits, uint4 a, uint4 b) {

@@ -20,6 +20,7 @@
 //     finalisation are wide.cuh's, unchanged: both kernels can run against the same set (the
 //     sharded import and the regrow still use wide.cuh's code), and the results are identical.
 #pragma once
+#include "regex_ops.cuh"
 #include "wide_common.cuh"
 
 namespace ltlb200 {
@@ -47,17 +48,30 @@ struct __align__(16) Wide2Fixed {  // per-warp shared state behind the row areas
     u64 ticket, sep_now;
 };
 
-// per-warp shared memory in uint4 units: vec rows | scalar rows | valid + target | fixed part
-__host__ __device__ inline size_t wide2_warp_vecs(int nvec) {
-    return (size_t)nvec * 32 + W2_SC_VECS + 2 * (size_t)nvec + (sizeof(Wide2Fixed) + 15) / 16;
+// Regex grammar (LW_REGEX, wide2_regex.cuh): fewer scalar rows per tile, and two more areas per warp, each the size of
+// the vector-row area -- the 32 vector rows BIT-SLICED (word x = bit x of every row) and the 32 result rows.
+constexpr int W2_RE_SC_VECS = 128;
+
+// per-warp shared memory in uint4 units: vec rows | scalar rows | valid + target | fixed part [| bit-sliced rows | result rows]
+__host__ __device__ inline size_t wide2_warp_vecs(int nvec, bool regex = false) {
+    const size_t fixed = 2 * (size_t)nvec + (sizeof(Wide2Fixed) + 15) / 16;
+    if (regex) return (size_t)nvec * 32 + W2_RE_SC_VECS + fixed + 2 * (size_t)nvec * 32;
+    return (size_t)nvec * 32 + W2_SC_VECS + fixed;
 }
-__host__ __device__ inline int wide2_tile_s(int nvec) { return W2_SC_VECS / nvec < W2_TERMS ? W2_SC_VECS / nvec : W2_TERMS; }
+__host__ __device__ inline int wide2_tile_s(int nvec, bool regex = false) {
+    const int rows = (regex ? W2_RE_SC_VECS : W2_SC_VECS) / nvec;
+    return rows < W2_TERMS ? rows : W2_TERMS;
+}
 
 struct Wide2Warp {
     uint4 *vec;     // [nvec][32] transposed vector-operand rows
     uint4 *sc;      // [tile_s][nvec] scalar-operand rows
     uint4 *consts;  // [0, nvec) valid masks, [nvec, 2 nvec) targets
     Wide2Fixed *fx;
+    // regex grammar: the guide tables (regex_ops.cuh; staged in the CTA's shared memory on request), the vector rows
+    // bit-sliced, and the result rows ([word][lane] once finished)
+    const uint32_t *guide;
+    uint32_t *sliced, *out;
 };
 
 struct Wide2State {  // warp-uniform registers
@@ -96,34 +110,35 @@ __device__ __forceinline__ u64 cas64_release(u64 *addr, u64 expect, u64 desired)
 
 __device__ __forceinline__ uint32_t v_diff(uint4 a, uint4 b) { return (a.x ^ b.x) | (a.y ^ b.y) | (a.z ^ b.z) | (a.w ^ b.w); }
 
-// Carries W2_BATCH candidates of one lane through hash -> probe -> claim / compare.
-// `gen(r, p, a, b)` yields the operands of candidate r's vector p in formula order.
+// Carries NB candidates of one lane (W2_BATCH; 1 in the regex tiles) through hash -> probe -> claim / compare.
+// `gen(r, p, a, b, c)` yields the operands of candidate r's vector p in formula order and the vector itself (for the
+// LTL operators c = cm_apply(a, b): a vector depends on the same vector of its operands; the regex concatenation
+// and star read bits all over their operands, see the regex tiles below).
 // GUARD (wide2_guarded_level_kernel): candidates whose ordinal lies in a dead range do not exist, and in the scan
 // pass only the ordinal of every separating candidate is recorded (NarrowParams::dead / scan_only).
-template <int LW, int OP, bool GUARD, class Gen>
+template <int LW, int OP, bool GUARD, int NB, class Gen>
 __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp &W, Wide2State &st, Gen gen,
-                                            const bool (&live_in)[W2_BATCH], const u64 (&ords)[W2_BATCH]) {
+                                            const bool (&live_in)[NB], const u64 (&ords)[NB]) {
     const int nvec = P.nvec;
     const uint32_t mask32 = (uint32_t)P.slot_mask;
-    bool live[W2_BATCH];
+    bool live[NB];
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) {
+    for (int r = 0; r < NB; ++r) {
         live[r] = live_in[r];
         if (GUARD && P.dead_n && live[r] && ordinal_is_dead(P.dead, P.dead_n, ords[r])) live[r] = false;
     }
     // ---- pass 1: hashes, separation flag, duplicate-by-construction flags
-    uint32_t ha[W2_BATCH], hb[W2_BATCH], sepacc[W2_BATCH], da[W2_BATCH], db[W2_BATCH];
+    uint32_t ha[NB], hb[NB], sepacc[NB], da[NB], db[NB];
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) ha[r] = hb[r] = sepacc[r] = da[r] = db[r] = 0u;
+    for (int r = 0; r < NB; ++r) ha[r] = hb[r] = sepacc[r] = da[r] = db[r] = 0u;
 #pragma unroll 1
     for (int p = 0; p < nvec; ++p) {
         const uint4 valid = W.consts[p], target = W.consts[nvec + p];
         const uint32_t seed_a = 0x9E3779B9u * (uint32_t)(p + 1), seed_b = 0x7F4A7C15u * (uint32_t)(p + 1) + 0x632BE5ABu;
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
-            uint4 a, b;
-            gen(r, p, a, b);
-            const uint4 c = cm_apply<LW, OP>(a, b, valid);
+        for (int r = 0; r < NB; ++r) {
+            uint4 a, b, c;
+            gen(r, p, a, b, c);
             ha[r] ^= hash_vec(c, seed_a);
             hb[r] ^= hash_vec(c, seed_b);
             sepacc[r] |= cm_sep_diff<LW>(c, target, valid);
@@ -133,18 +148,18 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
     }
     if (GUARD && P.scan_only) {
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
+        for (int r = 0; r < NB; ++r) {
             if (!live[r] || sepacc[r] != 0u) continue;
             const u64 pos = atomicAdd(&P.counters[CTR_SEPCOUNT], 1ull);
             if (pos < P.sep_list_cap) P.sep_list[pos] = ords[r];
         }
         return;
     }
-    uint32_t slot[W2_BATCH], fp[W2_BATCH];
-    u64 w[W2_BATCH], entry[W2_BATCH];
-    bool active[W2_BATCH], fresh[W2_BATCH];
+    uint32_t slot[NB], fp[NB];
+    u64 w[NB], entry[NB];
+    bool active[NB], fresh[NB];
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) {  // final mix of wide.cuh's row_hash
+    for (int r = 0; r < NB; ++r) {  // final mix of wide.cuh's row_hash
         uint32_t a = ha[r], b = hb[r];
         a ^= a >> 16;
         a *= 0x85EBCA6Bu;
@@ -162,10 +177,10 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
     }
     // ---- resolve: every round, claims write their row and matches compare theirs in ONE pass over the vectors
     for (;;) {
-        bool claim[W2_BATCH], match[W2_BATCH];
+        bool claim[NB], match[NB];
         bool any = false;
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
+        for (int r = 0; r < NB; ++r) {
             claim[r] = active[r] && w[r] == 0ull;
             match[r] = active[r] && !claim[r] && (uint32_t)(w[r] >> 40) == fp[r];
             if (active[r] && !claim[r] && !match[r]) {  // another CM lives there: linear probing
@@ -175,11 +190,11 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
             any = any || active[r];
         }
         if (!__any_sync(0xFFFFFFFFu, any)) break;
-        bool staged_row[W2_BATCH];
-        const uint4 *row[W2_BATCH];
-        uint32_t diff[W2_BATCH];
+        bool staged_row[NB];
+        const uint4 *row[NB];
+        uint32_t diff[NB];
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
+        for (int r = 0; r < NB; ++r) {
             const bool want = claim[r] && entry[r] == ~0ull;  // (a lost race left this candidate its entry)
             const u64 got = wide2_reserve(P, st, want);
             if (want) entry[r] = got;
@@ -197,9 +212,9 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
         // the first ncu capture had a third of this kernel's stall samples on exactly that compare.
 #pragma unroll 1
         for (int p0 = 0; p0 < nvec; p0 += W2_PREFETCH) {
-            uint4 stored[W2_BATCH][W2_PREFETCH];
+            uint4 stored[NB][W2_PREFETCH];
 #pragma unroll
-            for (int r = 0; r < W2_BATCH; ++r)
+            for (int r = 0; r < NB; ++r)
 #pragma unroll
                 for (int q = 0; q < W2_PREFETCH; ++q)
                     if (match[r] && p0 + q < nvec) stored[r][q] = __ldcg(row[r] + p0 + q);
@@ -207,20 +222,18 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
             for (int q = 0; q < W2_PREFETCH; ++q) {
                 const int p = p0 + q;
                 if (p >= nvec) break;
-                const uint4 valid = W.consts[p];
 #pragma unroll
-                for (int r = 0; r < W2_BATCH; ++r) {
+                for (int r = 0; r < NB; ++r) {
                     if (!claim[r] && !match[r]) continue;
-                    uint4 a, b;
-                    gen(r, p, a, b);
-                    const uint4 c = cm_apply<LW, OP>(a, b, valid);
+                    uint4 a, b, c;
+                    gen(r, p, a, b, c);
                     if (claim[r]) P.stage_rows[entry[r] * nvec + p] = c;
                     else diff[r] |= v_diff(c, stored[r][q]);
                 }
             }
         }
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
+        for (int r = 0; r < NB; ++r) {
             if (claim[r]) {
                 // release-ordered publish: the row this lane wrote above is visible to whoever reads the word (a warp-wide
                 // __threadfence() before a relaxed CAS was 5-7 % of this kernel's stall samples; c5 to cost 12: 26.2 -> 25.6 ms)
@@ -247,7 +260,7 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
         }
     }
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) {
+    for (int r = 0; r < NB; ++r) {
         if (live[r] && sepacc[r] == 0u) {
             if (fresh[r]) atomicMin(&P.counters[CTR_SEP], ords[r]);
             if (P.sep_list) {
@@ -274,9 +287,8 @@ __device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wid
         const uint4 valid = W.consts[p], target = W.consts[nvec + p];
 #pragma unroll
         for (int r = 0; r < W2_BATCH; ++r) {
-            uint4 a, b;
-            gen(r, p, a, b);
-            const uint4 c = cm_apply<LW, OP>(a, b, valid);
+            uint4 a, b, c;
+            gen(r, p, a, b, c);
             ho[r] ^= hash_vec(c, 0x5BD1E995u * (uint32_t)(p + 1));
             sepacc[r] |= cm_sep_diff<LW>(c, target, valid);
             da[r] |= v_diff(c, a);
@@ -324,13 +336,12 @@ __device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wid
     if (!any) return;
 #pragma unroll 1
     for (int p = 0; p < nvec; ++p) {
-        const uint4 valid = W.consts[p];
 #pragma unroll
         for (int r = 0; r < W2_BATCH; ++r) {
             if (at[r] == ~0ull) continue;
-            uint4 a, b;
-            gen(r, p, a, b);
-            P.route_rows[at[r] * nvec + p] = cm_apply<LW, OP>(a, b, valid);
+            uint4 a, b, c;
+            gen(r, p, a, b, c);
+            P.route_rows[at[r] * nvec + p] = c;
         }
     }
 }
@@ -359,9 +370,10 @@ __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide
             // a finalised row lives where it was staged (claim order): loc[id] is its place in the row log
             rows[r] = B.from_atoms ? P.atoms + (live[r] ? i : 0) * nvec : P.store + __ldg(P.loc + B.a_off + (live[r] ? i : 0)) * nvec;
         }
-        auto gen = [&](int r, int p, uint4 &a, uint4 &b) {
+        auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
             a = __ldg(rows[r] + p);
             b = a;
+            c = cm_apply<LW, OP>(a, b, W.consts[p]);
         };
         if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW, OP>(P, W, gen, live, ords);
         else wide2_batch<LW, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
@@ -409,7 +421,16 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
         const int rows_here = (int)min((u64)32, n_vec - vbase);
         for (int t = lane; t < rows_here * nvec; t += 32) {
             const int rrow = t / nvec, p = t - rrow * nvec;
-            W.vec[p * 32 + rrow] = __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p);
+            const uint4 x = __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p);
+            if constexpr (LW == LW_REGEX) {  // word q of row i at [q][i]: the concatenation tests single bits of a lane's row
+                uint32_t *vw = reinterpret_cast<uint32_t *>(W.vec) + rrow;
+                vw[(p * 4) * 32] = x.x;
+                vw[(p * 4 + 1) * 32] = x.y;
+                vw[(p * 4 + 2) * 32] = x.z;
+                vw[(p * 4 + 3) * 32] = x.w;
+            } else {
+                W.vec[p * 32 + rrow] = x;
+            }
         }
         __syncwarp();
         const u64 v = vbase + lane;
@@ -428,24 +449,50 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
                 live[r] = k + r < s_live;
                 ords[r] = W.fx->term[srow[r]] + lane_term;
             }
-            auto gen = [&](int r, int p, uint4 &a, uint4 &b) {
-                const uint4 xv = W.vec[p * 32 + lane], xs = W.sc[srow[r] * nvec + p];
-                a = VEC_B ? xs : xv;
-                b = VEC_B ? xv : xs;
+            auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
+                if constexpr (LW == LW_REGEX) {  // vector rows staged word by word (see above)
+                    const uint32_t *vw = reinterpret_cast<const uint32_t *>(W.vec) + lane;
+                    const uint4 xv = make_uint4(vw[(p * 4) * 32], vw[(p * 4 + 1) * 32], vw[(p * 4 + 2) * 32], vw[(p * 4 + 3) * 32]);
+                    const uint4 xs = W.sc[srow[r] * nvec + p];
+                    a = VEC_B ? xs : xv;
+                    b = VEC_B ? xv : xs;
+                    c = v_or(a, b);  // union (the concatenation has its own tile, wide2_regex_concat_tile)
+                } else {
+                    const uint4 xv = W.vec[p * 32 + lane], xs = W.sc[srow[r] * nvec + p];
+                    a = VEC_B ? xs : xv;
+                    b = VEC_B ? xv : xs;
+                    c = cm_apply<LW, OP>(a, b, W.consts[p]);
+                }
             };
             if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW, OP>(P, W, gen, live, ords);
-        else wide2_batch<LW, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
+            else wide2_batch<LW, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
         }
     }
 }
 
+#include "wide2_regex.cuh"
+
+template <int LW>
 __device__ __forceinline__ Wide2Warp wide2_carve(const WideParams &P, uint4 *base) {
+    constexpr bool kRegex = LW == LW_REGEX;
     Wide2Warp W;
-    uint4 *mine = base + (threadIdx.x >> 5) * wide2_warp_vecs(P.nvec);
+    uint4 *mine = base + (threadIdx.x >> 5) * wide2_warp_vecs(P.nvec, kRegex);
     W.vec = mine;
     W.sc = W.vec + (size_t)P.nvec * 32;
-    W.consts = W.sc + W2_SC_VECS;
+    W.consts = W.sc + (kRegex ? W2_RE_SC_VECS : W2_SC_VECS);
     W.fx = reinterpret_cast<Wide2Fixed *>(W.consts + 2 * (size_t)P.nvec);
+    W.guide = P.guide;
+    W.sliced = W.out = nullptr;
+    if constexpr (kRegex) {
+        W.sliced = reinterpret_cast<uint32_t *>(mine + (size_t)P.nvec * 32 + W2_RE_SC_VECS + 2 * (size_t)P.nvec + (sizeof(Wide2Fixed) + 15) / 16);
+        W.out = W.sliced + (size_t)P.nvec * 128;
+        if (P.guide_smem_words) {  // the guide table behind the warps' areas: one copy per CTA
+            uint32_t *g = reinterpret_cast<uint32_t *>(base + (size_t)WARPS_PER_CTA * wide2_warp_vecs(P.nvec, true));
+            for (uint32_t k = threadIdx.x; k < P.guide_smem_words; k += blockDim.x) g[k] = __ldg(P.guide + k);
+            W.guide = g;
+            __syncthreads();
+        }
+    }
     const int lane = threadIdx.x & 31;
     for (int p = lane; p < P.nvec; p += 32) {
         W.consts[p] = P.valid[p];
@@ -479,18 +526,48 @@ __device__ __forceinline__ void wide2_run_tile(const WideParams &P, const Wide2W
     const u64 sep_now = W.fx->sep_now;
     if (W.fx->block.ord0 > sep_now) return;
     const u64 tile_local = W.fx->ticket - W.fx->block.tile0;
-    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
+    if constexpr (OP == OP_RE_CONCAT) {
+        if (W.fx->block.vec_is_b) wide2_regex_concat_tile<true, MODE>(P, W, st, tile_local, sep_now);
+        else wide2_regex_concat_tile<false, MODE>(P, W, st, tile_local, sep_now);
+    } else if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
         if (W.fx->block.vec_is_b) wide2_binary_tile<LW, OP, true, MODE>(P, W, st, tile_local, sep_now);
         else wide2_binary_tile<LW, OP, false, MODE>(P, W, st, tile_local, sep_now);
+    } else if constexpr (LW == LW_REGEX) {
+        wide2_regex_unary_tile<OP, MODE>(P, W, st, tile_local, sep_now);
     } else {
         wide2_unary_tile<LW, OP, MODE>(P, W, st, tile_local, sep_now);
     }
 }
 
+// the tile's operator read from its block (kernels that serve every operator in one launch)
+template <int LW, int MODE>
+__device__ __forceinline__ void wide2_run_tile_any(const WideParams &P, const Wide2Warp &W, Wide2State &st) {
+    if constexpr (LW == LW_REGEX) {
+        switch (W.fx->block.op) {
+            case OP_ATOM: wide2_run_tile<LW, OP_ATOM, MODE>(P, W, st); break;
+            case OP_RE_QUESTION: wide2_run_tile<LW, OP_RE_QUESTION, MODE>(P, W, st); break;
+            case OP_RE_STAR: wide2_run_tile<LW, OP_RE_STAR, MODE>(P, W, st); break;
+            case OP_RE_CONCAT: wide2_run_tile<LW, OP_RE_CONCAT, MODE>(P, W, st); break;
+            default: wide2_run_tile<LW, OP_OR, MODE>(P, W, st); break;
+        }
+    } else {
+        switch (W.fx->block.op) {
+            case OP_ATOM: wide2_run_tile<LW, OP_ATOM, MODE>(P, W, st); break;
+            case OP_NOT: wide2_run_tile<LW, OP_NOT, MODE>(P, W, st); break;
+            case OP_NEXT: wide2_run_tile<LW, OP_NEXT, MODE>(P, W, st); break;
+            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE, MODE>(P, W, st); break;
+            case OP_AND: wide2_run_tile<LW, OP_AND, MODE>(P, W, st); break;
+            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL, MODE>(P, W, st); break;
+            case OP_GLOBALLY: wide2_run_tile<LW, OP_GLOBALLY, MODE>(P, W, st); break;
+            default: wide2_run_tile<LW, OP_OR, MODE>(P, W, st); break;
+        }
+    }
+}
+
 template <int LW, int OP>
-__global__ void __launch_bounds__(CTA_THREADS, LTLB200_WIDE2_MIN_CTAS) wide2_level_kernel(const __grid_constant__ WideParams P) {
+__global__ void __launch_bounds__(CTA_THREADS, LW == LW_REGEX ? 4 : LTLB200_WIDE2_MIN_CTAS) wide2_level_kernel(const __grid_constant__ WideParams P) {
     extern __shared__ __align__(16) uint4 s_w2[];
-    const Wide2Warp W = wide2_carve(P, s_w2);
+    const Wide2Warp W = wide2_carve<LW>(P, s_w2);
     Wide2State st;
     while (wide2_next_tile(P, W)) wide2_run_tile<LW, OP>(P, W, st);
 }
@@ -499,19 +576,10 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_WIDE2_MIN_CTAS) wide2_lev
 template <int LW>
 __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_small_level_kernel(const __grid_constant__ WideParams P) {
     extern __shared__ __align__(16) uint4 s_w2[];
-    const Wide2Warp W = wide2_carve(P, s_w2);
+    const Wide2Warp W = wide2_carve<LW>(P, s_w2);
     Wide2State st;
     while (wide2_next_tile(P, W)) {
-        switch (W.fx->block.op) {
-            case OP_ATOM: wide2_run_tile<LW, OP_ATOM>(P, W, st); break;
-            case OP_NOT: wide2_run_tile<LW, OP_NOT>(P, W, st); break;
-            case OP_NEXT: wide2_run_tile<LW, OP_NEXT>(P, W, st); break;
-            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE>(P, W, st); break;
-            case OP_AND: wide2_run_tile<LW, OP_AND>(P, W, st); break;
-            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL>(P, W, st); break;
-            case OP_GLOBALLY: wide2_run_tile<LW, OP_GLOBALLY>(P, W, st); break;
-            default: wide2_run_tile<LW, OP_OR>(P, W, st); break;
-        }
+        wide2_run_tile_any<LW, W2_PLAIN>(P, W, st);
     }
 }
 
@@ -519,19 +587,10 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_small_level_kernel(const
 template <int LW>
 __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_guarded_level_kernel(const __grid_constant__ WideParams P) {
     extern __shared__ __align__(16) uint4 s_w2[];
-    const Wide2Warp W = wide2_carve(P, s_w2);
+    const Wide2Warp W = wide2_carve<LW>(P, s_w2);
     Wide2State st;
     while (wide2_next_tile(P, W)) {
-        switch (W.fx->block.op) {
-            case OP_ATOM: wide2_run_tile<LW, OP_ATOM, W2_GUARD>(P, W, st); break;
-            case OP_NOT: wide2_run_tile<LW, OP_NOT, W2_GUARD>(P, W, st); break;
-            case OP_NEXT: wide2_run_tile<LW, OP_NEXT, W2_GUARD>(P, W, st); break;
-            case OP_FUTURE: wide2_run_tile<LW, OP_FUTURE, W2_GUARD>(P, W, st); break;
-            case OP_AND: wide2_run_tile<LW, OP_AND, W2_GUARD>(P, W, st); break;
-            case OP_UNTIL: wide2_run_tile<LW, OP_UNTIL, W2_GUARD>(P, W, st); break;
-            case OP_GLOBALLY: wide2_run_tile<LW, OP_GLOBALLY, W2_GUARD>(P, W, st); break;
-            default: wide2_run_tile<LW, OP_OR, W2_GUARD>(P, W, st); break;
-        }
+        wide2_run_tile_any<LW, W2_GUARD>(P, W, st);
     }
 }
 
@@ -539,7 +598,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) wide2_guarded_level_kernel(con
 template <int LW, int OP>
 __global__ void __launch_bounds__(CTA_THREADS, LTLB200_WIDE2_MIN_CTAS) wide2_route_kernel(const __grid_constant__ WideParams P) {
     extern __shared__ __align__(16) uint4 s_w2[];
-    const Wide2Warp W = wide2_carve(P, s_w2);
+    const Wide2Warp W = wide2_carve<LW>(P, s_w2);
     Wide2State st;
     while (wide2_next_tile(P, W)) wide2_run_tile<LW, OP, W2_ROUTE>(P, W, st);
 }

@@ -1,0 +1,207 @@
+// wide2_regex.cuh -- the regex grammar's tiles of the wide kernels (LW_REGEX; included by wide2.cuh).
+//
+// NOT in the reference; see regex_ops.cuh for the operators and the guide tables.  A warp's tile is, as
+// for LTL, 32 "vector" rows (one per lane) combined with one "scalar" row at a time, but concatenation and star do
+// not map vector p of the operands to vector p of the result: bit w of  r s  is the OR over the splits w = u v of
+// r[u] & s[v].  Walking the splits per candidate (what regex_ops.cuh does for one-vector CSs) costs thousands of
+// dependent shared-memory reads per candidate on sequences of several hundred bits.  Here the 32 vector rows are
+// BIT-SLICED instead: word x of the sliced area holds bit x of all 32 rows, so one 32-bit AND / OR acts on the 32
+// candidates of the tile at once, the lanes work on 32 guide entries in parallel, and nothing branches on data:
+//
+//   concatenation  for every infix u in the scalar row (a warp-uniform walk over its set bits), for every entry
+//                  (x, w) of u's group in the guide table grouped by that side:   out[w] |= sliced[x]
+//                  (within a group the w are distinct: plain read-modify-write, one __syncwarp per group);
+//   star           out[empty] = all ones; rounds by split depth (= infix length): for every entry (u, v) -> w of
+//                  the round, u non-empty:   out[w] |= sliced[u] & out[v]   (shared-memory atomicOr: several
+//                  entries of a round share their w);
+//
+// then 32 x 32 bit transposes (five shuffle rounds per 32 infixes) turn `out` back into one row per lane, in place,
+// which the hashing / probe / claim / compare passes of wide2_batch read from shared memory (a row is built once;
+// the LTL vectors are cheap enough to be rebuilt in pass 2 instead).
+#pragma once
+// (included by wide2.cuh inside namespace ltlb200, between the batch passes and the tile dispatch)
+
+// lane r holds row r of a 32 x 32 bit matrix (bit c = column c); returns column `lane` (bit r = row r)
+__device__ __forceinline__ uint32_t transpose32(uint32_t x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
+        x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y & m) << s));
+    }
+    return x;
+}
+
+// rows [word][lane] -> bit-sliced [infix] (and back: the transpose is its own inverse), 32 infixes per step
+__device__ __forceinline__ void regex_slice(const uint32_t *rows, uint32_t *sliced, int n_words) {
+    const int lane = threadIdx.x & 31;
+    for (int q = 0; q < n_words; ++q) sliced[q * 32 + lane] = transpose32(rows[q * 32 + lane]);
+}
+
+struct RegexGuide {  // the tables of Engine::set_regex (global memory or the CTA's staged copy)
+    const uint32_t *off, *uv, *w_of;          // sorted by result infix: offsets, entries u | v << 16, result infix per entry
+    const uint32_t *left_off, *left_ent;      // grouped by the LEFT part u:  entries v | w << 16
+    const uint32_t *right_off, *right_ent;    // grouped by the RIGHT part v: entries u | w << 16
+    const uint32_t *rounds;                   // entry offsets of the star's rounds (split depth), n_rounds + 1 values
+};
+
+__device__ __forceinline__ RegexGuide regex_guide(const WideParams &P, const uint32_t *base) {
+    RegexGuide G;
+    const uint32_t n = (uint32_t)P.n_bits, E = P.guide_entries;
+    G.off = base;
+    G.uv = base + n + 1;
+    G.w_of = G.uv + E;
+    G.left_off = G.w_of + E;
+    G.left_ent = G.left_off + n + 1;
+    G.right_off = G.left_ent + E;
+    G.right_ent = G.right_off + n + 1;
+    G.rounds = G.right_ent + E;
+    return G;
+}
+
+// literal, question, star
+template <int OP, int MODE>
+__device__ __forceinline__ void wide2_regex_unary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
+                                                       u64 sep_now) {
+    const BlockDesc &B = W.fx->block;
+    const int lane = threadIdx.x & 31;
+    const int nvec = P.nvec, n_words = nvec * 4;
+    const u64 per_tile = (u64)32 * B.tile_s;
+    const u64 first = tile_local * per_tile + lane;
+    const u64 ord0 = B.ord0, n = B.na;
+    if (ord0 + tile_local * per_tile > sep_now) return;
+    const int n_steps = (int)min((u64)B.tile_s, (n - tile_local * per_tile + 31) / 32);
+    const RegexGuide G = regex_guide(P, W.guide);
+    uint32_t *vw = reinterpret_cast<uint32_t *>(W.vec) + lane, *ow = W.out + lane;
+#pragma unroll 1
+    for (int k = 0; k < n_steps; ++k) {
+        const u64 i = first + (u64)k * 32;
+        const bool live[1] = {i < n};
+        const u64 ords[1] = {ord0 + i};
+        const uint4 *row = B.from_atoms ? P.atoms + (live[0] ? i : 0) * nvec : P.store + __ldg(P.loc + B.a_off + (live[0] ? i : 0)) * nvec;
+        __syncwarp();
+        for (int p = 0; p < nvec; ++p) {  // every lane its own row, word by word into its own bank
+            const uint4 x = __ldg(row + p);
+            vw[(p * 4) * 32] = x.x;
+            vw[(p * 4 + 1) * 32] = x.y;
+            vw[(p * 4 + 2) * 32] = x.z;
+            vw[(p * 4 + 3) * 32] = x.w;
+        }
+        if constexpr (OP == OP_RE_STAR) {
+            __syncwarp();
+            regex_slice(reinterpret_cast<const uint32_t *>(W.vec), W.sliced, n_words);
+            for (int q = 0; q < n_words; ++q) W.out[q * 32 + lane] = 0u;
+            __syncwarp();
+            if (lane == 0) W.out[0] = 0xFFFFFFFFu;  // the empty word, in every row
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t r = 1; r < P.guide_rounds; ++r) {
+                const uint32_t e_hi = G.rounds[r + 1];
+                for (uint32_t e = G.rounds[r] + lane; e < e_hi; e += 32) {
+                    const uint32_t uv = G.uv[e];
+                    const uint32_t u = uv & 0xFFFFu;
+                    if (u == 0u) continue;
+                    const uint32_t val = W.sliced[u] & W.out[uv >> 16];
+                    if (val) atomicOr(&W.out[G.w_of[e]], val);
+                }
+                __syncwarp();
+            }
+            regex_slice(W.out, W.out, n_words);  // back to one row per lane, in place
+        }
+        __syncwarp();
+        auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
+            a = make_uint4(vw[(p * 4) * 32], vw[(p * 4 + 1) * 32], vw[(p * 4 + 2) * 32], vw[(p * 4 + 3) * 32]);
+            b = a;
+            if constexpr (OP == OP_RE_STAR) c = make_uint4(ow[(p * 4) * 32], ow[(p * 4 + 1) * 32], ow[(p * 4 + 2) * 32], ow[(p * 4 + 3) * 32]);
+            else if constexpr (OP == OP_RE_QUESTION) c = make_uint4(a.x | (p == 0 ? 1u : 0u), a.y, a.z, a.w);
+            else c = a;
+        };
+        wide2_batch<LW_REGEX, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
+    }
+}
+
+// concatenation  left . right;  VEC_B: the lanes' rows are the RIGHT operands, the scalar row is the left one
+template <bool VEC_B, int MODE>
+__device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
+                                                        u64 sep_now) {
+    const BlockDesc &B = W.fx->block;
+    const int lane = threadIdx.x & 31;
+    const int nvec = P.nvec, n_words = nvec * 4;
+    const int tile_s = (int)B.tile_s;
+    const uint32_t vg_n = B.vg;
+    u64 tv, ts;
+    if (VEC_B) { ts = tile_local / B.tiles_v; tv = tile_local % B.tiles_v; }
+    else { tv = tile_local / B.tiles_s; ts = tile_local % B.tiles_s; }
+    const u64 n_vec = VEC_B ? B.nb : B.na, n_sc = VEC_B ? B.na : B.nb;
+    const u64 v0 = tv * (u64)(32 * vg_n), s0 = ts * (u64)tile_s;
+    const int s_cnt = (int)min((u64)tile_s, n_sc - s0);
+    const u64 ord0 = B.ord0, nb = B.nb;
+    if (ord0 + (VEC_B ? s0 * nb + v0 : v0 * nb + s0) > sep_now) return;
+    const u64 *vec_loc = P.loc + (VEC_B ? B.b_off : B.a_off);
+    const u64 *sc_loc = P.loc + (VEC_B ? B.a_off : B.b_off);
+    const RegexGuide G = regex_guide(P, W.guide);
+    // the table grouped by the scalar row's side: its entries name the bit of the lanes' rows and the result bit
+    const uint32_t *g_off = VEC_B ? G.left_off : G.right_off, *g_ent = VEC_B ? G.left_ent : G.right_ent;
+    const int sc_words = (P.n_bits + 31) >> 5;
+    uint32_t *vw = reinterpret_cast<uint32_t *>(W.vec) + lane, *ow = W.out + lane;
+    __syncwarp();
+    for (int t = lane; t < s_cnt * nvec; t += 32) {
+        const int rrow = t / nvec, p = t - rrow * nvec;
+        W.sc[t] = __ldg(P.store + __ldg(sc_loc + s0 + rrow) * nvec + p);
+    }
+#pragma unroll 1
+    for (uint32_t vg = 0; vg < vg_n; ++vg) {
+        const u64 vbase = v0 + (u64)vg * 32;
+        if (vbase >= n_vec) break;
+        __syncwarp();
+        const int rows_here = (int)min((u64)32, n_vec - vbase);
+        for (int t = lane; t < 32 * nvec; t += 32) {  // (rows past the end of the level: zero)
+            const int rrow = t / nvec, p = t - rrow * nvec;
+            const uint4 x = rrow < rows_here ? __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p) : make_uint4(0, 0, 0, 0);
+            uint32_t *col = reinterpret_cast<uint32_t *>(W.vec) + rrow;
+            col[(p * 4) * 32] = x.x;
+            col[(p * 4 + 1) * 32] = x.y;
+            col[(p * 4 + 2) * 32] = x.z;
+            col[(p * 4 + 3) * 32] = x.w;
+        }
+        __syncwarp();
+        regex_slice(reinterpret_cast<const uint32_t *>(W.vec), W.sliced, n_words);
+        const u64 v = vbase + lane;
+        const bool v_ok = v < n_vec;
+#pragma unroll 1
+        for (int k = 0; k < s_cnt; ++k) {
+            const uint32_t *sw = reinterpret_cast<const uint32_t *>(W.sc + k * nvec);
+            __syncwarp();
+            for (int q = 0; q < n_words; ++q) W.out[q * 32 + lane] = 0u;
+            __syncwarp();
+#pragma unroll 1
+            for (int q = 0; q < sc_words; ++q) {
+                uint32_t word = sw[q];  // the same for every lane
+                while (word) {
+                    const uint32_t s = (uint32_t)q * 32u + (uint32_t)(__ffs(word) - 1);
+                    word &= word - 1u;
+                    const uint32_t e_hi = g_off[s + 1];
+                    for (uint32_t e = g_off[s] + lane; e < e_hi; e += 32) {
+                        const uint32_t ent = g_ent[e];
+                        W.out[ent >> 16] |= W.sliced[ent & 0xFFFFu];
+                    }
+                    __syncwarp();
+                }
+            }
+            regex_slice(W.out, W.out, n_words);  // one row per lane, in place
+            __syncwarp();
+            const bool live[1] = {v_ok};
+            const u64 ords[1] = {ord0 + (VEC_B ? (s0 + k) * nb + v : v * nb + (s0 + k))};
+            auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
+                const uint4 xv = make_uint4(vw[(p * 4) * 32], vw[(p * 4 + 1) * 32], vw[(p * 4 + 2) * 32], vw[(p * 4 + 3) * 32]);
+                const uint4 xs = W.sc[k * nvec + p];
+                a = VEC_B ? xs : xv;
+                b = VEC_B ? xv : xs;
+                c = make_uint4(ow[(p * 4) * 32], ow[(p * 4 + 1) * 32], ow[(p * 4 + 2) * 32], ow[(p * 4 + 3) * 32]);
+            };
+            wide2_batch<LW_REGEX, OP_RE_CONCAT, MODE == W2_GUARD>(P, W, st, gen, live, ords);
+        }
+    }
+}
+

@@ -65,6 +65,12 @@ struct WideParams {
     u64 *route_counts;
     uint32_t route_world;
     int route_sep_any;
+    // regex grammar (LW_REGEX instantiation of wide2.cuh; wide2_regex.cuh): the guide tables laid out by
+    // Engine::set_regex, bits per characteristic sequence, entries of the table, rounds of the star
+    const uint32_t *guide;
+    int n_bits;
+    uint32_t guide_entries, guide_rounds;
+    uint32_t guide_smem_words;  // > 0: the kernels stage the tables in the CTA's shared memory
 };
 
 // hash owner of a row in a sharded search (independent of the slot hash and of the fingerprint)

@@ -18,9 +18,11 @@ The idea is the paper's "enumerate semantics, not syntax" applied to regular exp
   (``csrc/engine.cu: plan_level`` with the regex operator tags); the **cost function has five parameters** --
   literal, ``?``, ``*``, concatenation, union -- which are the engine's per-operator weights.
 
-This slice: CSs of up to 128 bits (``InfixIndex.n_bits <= 128``: BASELINE configs[0]-sized example sets) run on the
-GPU through the narrow kernels (``csrc/regex_ops.cuh``); wider example sets (the e-mail example has 528 infixes) are
-handled by the host model and the CPU oracle only and raise ``NativeEngineError`` on the GPU path.
+CSs of up to 128 bits (``InfixIndex.n_bits <= 128``: BASELINE configs[0]-sized example sets) run through the narrow
+kernels (one ``uint4`` per CS, ``csrc/regex_ops.cuh``), CSs of up to 2048 bits (the e-mail example has 528 infixes)
+through the wide kernels (``csrc/wide2.cuh``: row log, 8-byte slot words, the concatenation testing single bits of its
+operands in shared memory); wider example sets are handled by the host model and the CPU oracle only and raise
+``NativeEngineError`` on the GPU path.
 """
 
 from __future__ import annotations
@@ -38,6 +40,7 @@ from .traces import InfeasibleSpecificationError
 
 OP_LITERAL, OP_UNION, OP_QUESTION, OP_STAR, OP_CONCAT = 0, 6, 8, 9, 10  # operator tags of include/ltlsynth_b200.h
 _OP_MASK = (1 << OP_UNION) | (1 << OP_QUESTION) | (1 << OP_STAR) | (1 << OP_CONCAT)
+MAX_GPU_BITS = 2048  # csrc/engine.cu: Engine::set_regex
 
 
 # ---- expressions ------------------------------------------------------------------------------------------------
@@ -219,9 +222,9 @@ class RegexStore(CandidateStore):
         lib = _native.load()
         if lib.ltlb200_device_count() < 1:
             raise _native.NativeEngineError("no usable B200: " + _native.last_error())
-        if self.ix.n_bits > 128:
+        if self.ix.n_bits > MAX_GPU_BITS:
             raise _native.NativeEngineError(
-                f"regex front-end, first slice: the GPU path takes characteristic sequences of up to 128 bits; these examples "
+                f"regex front-end: the GPU path takes characteristic sequences of up to {MAX_GPU_BITS} bits; these examples "
                 f"have {self.ix.n_bits} infixes (the host model and oracle/regex_oracle.py handle any width)")
         lanes = lambda cs: np.frombuffer(self.ix.row_bytes(cs), dtype=np.uint8).astype(np.uint64)
         masks, target = lanes(self.ix.example_bits), lanes(self.ix.positive_bits)

@@ -1,4 +1,4 @@
-"""Regex front-end on the CUDA engine (first slice: characteristic sequences of up to 128 bits) against the CPU oracle
+"""Regex front-end on the CUDA engine (characteristic sequences of up to 2048 bits) against the CPU oracle
 (oracle/regex_oracle.py, pinned to Python's `re` by tests/test_regex_oracle.py).  PARITY UNPINNED with respect to the
 reference, which has no regex synthesiser."""
 
@@ -75,6 +75,94 @@ def test_three_letter_alphabet_and_wider_sequences():
         store.close()
 
 
-def test_email_example_is_refused_on_the_gpu_in_this_slice():
-    with pytest.raises(_native.NativeEngineError, match="128 bits"):
-        rx.RegexStore(rx.RegexSpecification(EMAIL_P, EMAIL_N))
+def _wide_words(seed, n_words=8, length=(9, 13), letters="abc"):
+    rng = random.Random(seed)
+    words = set()
+    while len(words) < n_words:
+        words.add("".join(rng.choice(letters) for _ in range(rng.randint(*length))))
+    return sorted(words)
+
+
+@pytest.mark.parametrize("seed,cost,max_cost", [
+    (0, rx.CostFunction(), 5), (1, rx.CostFunction(literal=1, question=2, star=1, concat=1, union=2), 6),
+])
+def test_sequences_wider_than_128_bits_equal_the_oracle(seed, cost, max_cost):
+    """CSs of several uint4 vectors: the wide kernels (row log, word-wise concatenation and star)."""
+    words = _wide_words(seed)
+    spec = rx.RegexSpecification(tuple(words[:4]), tuple(words[4:]))
+    store, ref = rx.RegexStore(spec, cost), ro.RegexOracle(spec, cost)
+    assert 128 < store.ix.n_bits <= 1024
+    try:
+        for c in range(1, max_cost + 1):
+            status, n_new, sep, constructed = store.expand(c, exhaustive=True)
+            o_new, o_sep, o_constructed = ref.expand_level(c, exhaustive=True)
+            assert (status, n_new, constructed) == (0, o_new, o_constructed), f"seed {seed} cost {c}"
+            _assert_level_equal(store, ref, c, f"wide seed {seed} cost {c}")
+    finally:
+        store.close()
+
+
+def _build_levels(store, max_cost):
+    for c in range(1, max_cost + 1):
+        status, n_new, sep, constructed = store.expand(c, exhaustive=True)
+        assert status == 0
+    return [store.level(c) for c in range(1, max_cost + 1)]
+
+
+def test_email_example_on_the_gpu():
+    """528 infixes (five uint4 vectors per CS), 4103 guide entries, 20 literals.  Levels 1-6 against the
+    oracle; levels 7-8 (10^5..10^6 candidates: the per-operator kernels, the estimate-and-redo path) against `re` on a
+    sample, pairwise distinct over the whole store, and identical on a second run."""
+    spec = rx.RegexSpecification(EMAIL_P, EMAIL_N)
+    store, ref = rx.RegexStore(spec), ro.RegexOracle(spec)
+    assert (store.ix.n_bits, len(store.ix.splits)) == (528, 4103)
+    try:
+        for c in range(1, 7):
+            status, n_new, sep, constructed = store.expand(c, exhaustive=True)
+            o_new, o_sep, o_constructed = ref.expand_level(c, exhaustive=True)
+            assert (status, n_new, constructed) == (0, o_new, o_constructed), f"cost {c}"
+            _assert_level_equal(store, ref, c, f"e-mail cost {c}")
+        seen = set()
+        for c in range(1, 9):
+            if c > 6:
+                status, n_new, sep, constructed = store.expand(c, exhaustive=True)
+                assert status == 0 and sep is None
+            lv = store.level(c)
+            rows = {lv.cms[k].tobytes() for k in range(lv.n)}
+            assert len(rows) == lv.n and not (rows & seen), f"cost {c}: a sequence is stored twice"
+            seen |= rows
+            for k in range(0, lv.n, max(1, lv.n // 25)):
+                pattern = rx.to_pattern(store.regex_of(lv.base + k))
+                assert store.ix.row_bytes(store.ix.cs_of_pattern(pattern)) == lv.cms[k].tobytes(), pattern
+        assert store.level(8).n > 50_000
+        again = rx.RegexStore(spec)
+        try:
+            for lv, lv2 in zip([store.level(c) for c in (7, 8)], _build_levels(again, 8)[6:]):
+                assert np.array_equal(lv.cms, lv2.cms) and np.array_equal(lv.op, lv2.op)
+                assert np.array_equal(lv.left, lv2.left) and np.array_equal(lv.right, lv2.right)
+        finally:
+            again.close()
+    finally:
+        store.close()
+
+
+def test_synthesize_regex_on_wide_sequences():
+    """Searches that end with a separator cut on sequences of two / three vectors: same expression, cost and counters as
+    the oracle."""
+    cases = [
+        (("abcabcabcabc", "abcabc", "abc"), ("cacbaccbabacab", "bccabbabcbbaca", "cbabcaacbcabbb", "abcab", "bca", "acb"), 9),
+        (("abaabaaba", "abab", "ab", "abaab"), ("aabbaaaabbabbaababba", "babbbbbabbaababbabbb", "abaaaaabbbbbabbabaab", "a", "bb", "aab"), 10),
+    ]
+    for pos, neg, max_cost in cases:
+        spec = rx.RegexSpecification(pos, neg)
+        assert rx.InfixIndex(spec).n_bits > 128
+        res = rx.synthesize_regex(spec, rx.RegexConfig(max_cost=max_cost))
+        want = ro.synthesize(spec, max_cost=max_cost)
+        assert want.pattern is not None
+        assert (res.pattern, res.cost, res.stats.unique, res.stats.constructed) == (want.pattern, want.cost, want.unique, want.constructed)
+
+
+def test_sequences_beyond_2048_bits_are_refused():
+    words = _wide_words(7, n_words=12, length=(28, 30), letters="abcdefgh")
+    with pytest.raises(_native.NativeEngineError, match="2048 bits"):
+        rx.RegexStore(rx.RegexSpecification(tuple(words[:6]), tuple(words[6:])))
