@@ -2348,9 +2348,9 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
 // and of the letters); this switches its kernels to the regex operators and uploads the infix-split guide table.
 void Engine::set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries) {
     if (!levels_.empty()) throw std::invalid_argument("the grammar must be set before the first level");
-    // (wide2_regex.cuh keeps three row areas of 32 rows per warp in shared memory: 16 vectors = 2048 bits)
-    if (n_bits < 1 || n_bits > 2048 || lw_ != 8 || (n_bits + 7) / 8 != row_bytes_)
-        throw std::invalid_argument("regex front-end: characteristic sequences of up to 2048 bits, created as ceil(bits / 8) "
+    // (wide2_regex.cuh keeps three row areas of 32 rows per warp in shared memory: 32 vectors = 4096 bits, 214 KB per CTA)
+    if (n_bits < 1 || n_bits > 4096 || lw_ != 8 || (n_bits + 7) / 8 != row_bytes_)
+        throw std::invalid_argument("regex front-end: characteristic sequences of up to 4096 bits, created as ceil(bits / 8) "
                                     "lanes of 8 bits");
     CUDA_CHECK(cudaSetDevice(device_));
     // device layout (wide2_regex.cuh: RegexGuide): the table as given (offsets | entries u | v << 16, sorted by the

@@ -13,7 +13,7 @@
 //                          (v is shorter than w and infixes are sorted by length: one pass in index order)
 // The splits come from the GUIDE TABLE the host precomputes: offsets[w] .. offsets[w+1] index entries (u | v << 16)
 // of infix indices.  CSs of up to 128 bits are one uint4 and take the operators below (narrow kernels; the table is
-// read through the read-only cache, a few KB shared by every candidate); wider ones (up to 2048 bits) are handled 32
+// read through the read-only cache, a few KB shared by every candidate); wider ones (up to 4096 bits) are handled 32
 // candidates at a time on bit-sliced rows (wide2_regex.cuh) with the same table regrouped by Engine::set_regex.
 #pragma once
 #include "cm_ops.cuh"

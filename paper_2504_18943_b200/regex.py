@@ -19,7 +19,7 @@ The idea is the paper's "enumerate semantics, not syntax" applied to regular exp
   literal, ``?``, ``*``, concatenation, union -- which are the engine's per-operator weights.
 
 CSs of up to 128 bits (``InfixIndex.n_bits <= 128``: BASELINE configs[0]-sized example sets) run through the narrow
-kernels (one ``uint4`` per CS, ``csrc/regex_ops.cuh``), CSs of up to 2048 bits (the e-mail example has 528 infixes)
+kernels (one ``uint4`` per CS, ``csrc/regex_ops.cuh``), CSs of up to 4096 bits (the e-mail example has 528 infixes)
 through the wide kernels (``csrc/wide2.cuh``: row log, 8-byte slot words, the concatenation testing single bits of its
 operands in shared memory); wider example sets are handled by the host model and the CPU oracle only and raise
 ``NativeEngineError`` on the GPU path.
@@ -40,7 +40,7 @@ from .traces import InfeasibleSpecificationError
 
 OP_LITERAL, OP_UNION, OP_QUESTION, OP_STAR, OP_CONCAT = 0, 6, 8, 9, 10  # operator tags of include/ltlsynth_b200.h
 _OP_MASK = (1 << OP_UNION) | (1 << OP_QUESTION) | (1 << OP_STAR) | (1 << OP_CONCAT)
-MAX_GPU_BITS = 2048  # csrc/engine.cu: Engine::set_regex
+MAX_GPU_BITS = 4096  # csrc/engine.cu: Engine::set_regex
 
 
 # ---- expressions ------------------------------------------------------------------------------------------------

@@ -97,3 +97,36 @@ def named_workload(name: str, seed: int = 0) -> Specification:
 
 def workload_names() -> tuple[str, ...]:
     return ("spec1", "spec2") + tuple(_SYNTHETIC)
+
+
+# ---- regular-expression example sets (regex front-end; BASELINE.json configs[0]-[3] as literally worded) ----------
+
+EMAIL_POSITIVES = ("geon@ex.io", "test@gmail.com", "mail@test.org", "mail@testing.com")  # reference PAPER.md:83-94
+EMAIL_NEGATIVES = ("hello@", "@test", "email@gmail", "t@test@gmail.com", "mail with@space.com")
+
+# name -> (letters, strings per side, maximum length)
+_REGEX_SYNTHETIC = {
+    "re-c0": ("01", 4, 5),      # configs[0]: a few dozen infixes, one uint4 per characteristic sequence
+    "re-c2": ("01", 20, 10),    # configs[2]: ~200 infixes
+    "re-c3": ("abc", 64, 16),   # configs[3]: ~2700 infixes (22 uint4 per sequence)
+}
+
+
+def regex_workload(name: str, seed: int = 0):
+    """Example strings of a regex workload as a ``RegexSpecification``: distinct random strings of length
+    1..maximum over the letters, drawn from ``random.Random(seed)``, the first half positive."""
+    from .regex import RegexSpecification
+
+    key = name.lower()
+    if key in ("re-email", "re-c1"):
+        return RegexSpecification(EMAIL_POSITIVES, EMAIL_NEGATIVES)
+    if key not in _REGEX_SYNTHETIC:
+        raise KeyError(f"unknown regex workload {name!r}; known: re-email, {', '.join(_REGEX_SYNTHETIC)}")
+    letters, per_side, longest = _REGEX_SYNTHETIC[key]
+    rng = random.Random(seed)
+    words: set[str] = set()
+    while len(words) < 2 * per_side:
+        words.add("".join(rng.choice(letters) for _ in range(rng.randint(1, longest))))
+    drawn = sorted(words)
+    rng.shuffle(drawn)
+    return RegexSpecification(tuple(drawn[:per_side]), tuple(drawn[per_side:]))

@@ -1,4 +1,4 @@
-"""Regex front-end on the CUDA engine (characteristic sequences of up to 2048 bits) against the CPU oracle
+"""Regex front-end on the CUDA engine (characteristic sequences of up to 4096 bits) against the CPU oracle
 (oracle/regex_oracle.py, pinned to Python's `re` by tests/test_regex_oracle.py).  PARITY UNPINNED with respect to the
 reference, which has no regex synthesiser."""
 
@@ -162,7 +162,26 @@ def test_synthesize_regex_on_wide_sequences():
         assert (res.pattern, res.cost, res.stats.unique, res.stats.constructed) == (want.pattern, want.cost, want.unique, want.constructed)
 
 
-def test_sequences_beyond_2048_bits_are_refused():
+@pytest.mark.parametrize("name,max_cost,bits", [("re-c2", 10, 207), ("re-c3", 7, 2709)])
+def test_baseline_shaped_example_sets_equal_the_oracle(name, max_cost, bits):
+    """BASELINE configs[2] / configs[3] as literally worded (binary alphabet 20 + 20 strings of length <= 10; three
+    letters, 64 + 64 strings of length <= 16: 22 uint4 per sequence, 24912 guide entries)."""
+    from paper_2504_18943_b200.workloads import regex_workload
+
+    spec = regex_workload(name)
+    store, ref = rx.RegexStore(spec), ro.RegexOracle(spec)
+    assert store.ix.n_bits == bits
+    try:
+        for c in range(1, max_cost + 1):
+            status, n_new, sep, constructed = store.expand(c, exhaustive=True)
+            o_new, o_sep, o_constructed = ref.expand_level(c, exhaustive=True)
+            assert (status, n_new, constructed) == (0, o_new, o_constructed), f"{name} cost {c}"
+            _assert_level_equal(store, ref, c, f"{name} cost {c}")
+    finally:
+        store.close()
+
+
+def test_sequences_beyond_4096_bits_are_refused():
     words = _wide_words(7, n_words=12, length=(28, 30), letters="abcdefgh")
-    with pytest.raises(_native.NativeEngineError, match="2048 bits"):
+    with pytest.raises(_native.NativeEngineError, match="4096 bits"):
         rx.RegexStore(rx.RegexSpecification(tuple(words[:6]), tuple(words[6:])))
