@@ -76,7 +76,46 @@ WORKLOADS = {
 DEFAULT_WORKLOAD = {1: "spec2"}
 DEFAULT_SHARDED_WORKLOAD = "c3-16"
 EXTRA_WORKLOADS = ("c3-fill", "c4-1024-11", "c5-12", "c5-fill")
+# regex front-end (BASELINE configs[1]-[3] as literally worded): name -> exhaustive levels built
+REGEX_WORKLOADS = {"re-email": 13, "re-c2": 19, "re-c3": 13}
 OPERATORS = "not,next,future,and,until"
+
+
+def regex_arm(name: str, max_cost: int, seed: int, device: int, steps: int, warmup: int) -> dict:
+    """One regex workload of the `workloads` table: exhaustive levels 1..max_cost through the regex front-end's store
+    (paper_2504_18943_b200.regex.RegexStore), host wall clock around the level loop (every level ends with a
+    device-to-host read of its counters)."""
+    import torch
+
+    from paper_2504_18943_b200 import regex as rx
+    from paper_2504_18943_b200.workloads import regex_workload
+
+    spec = regex_workload(name, seed)
+    times, unique, constructed, stats = [], 0, 0, None
+    for it in range(warmup + steps):
+        store = rx.RegexStore(spec, device=device)
+        try:
+            torch.cuda.synchronize(device)
+            t0 = time.perf_counter()
+            unique = constructed = reached = 0
+            for c in range(1, max_cost + 1):
+                status, n_new, _, built = store.expand(c, exhaustive=True)
+                unique, constructed = unique + n_new, constructed + built
+                if status != 0:
+                    break
+                reached = c
+            torch.cuda.synchronize(device)
+            if it >= warmup:
+                times.append(time.perf_counter() - t0)
+            stats, n_bits, entries = store.device_stats(), store.ix.n_bits, len(store.ix.splits)
+        finally:
+            store.close()
+    ms = 1e3 * sum(times) / len(times)
+    return {"ms_per_step": ms, "unique_per_s": unique / (ms * 1e-3), "constructed_per_s": constructed / (ms * 1e-3),
+            "unique_per_step": unique, "constructed_per_step": constructed, "max_cost_reached": reached,
+            "cs_bits": n_bits, "guide_entries": entries, "cm_bytes": stats["row_bytes"], "device_bytes": stats["device_bytes"],
+            "kernel_ms_per_step": stats["enumerate_ms"], "finalize_ms_per_step": stats["finalize_ms"], "steps": steps, "warmup": warmup,
+            "grammar": "regex (literal, ?, *, concatenation, union; unit costs); parity unpinned: the reference has no regex synthesiser"}
 
 
 def measured_peaks() -> tuple[float, str]:
@@ -415,6 +454,12 @@ def main() -> int:
                            "device_bytes": a["after"]["device_bytes"], "kernel_ms_per_step": kk["enum_ms"],
                            "finalize_ms_per_step": kk["fin_ms"], "tiny_levels_ms_per_step": kk["tiny_ms"],
                            "roofline_frac": kk["frac"], "steps": 2, "warmup": 1}
+        for name, max_cost in REGEX_WORKLOADS.items():
+            _native.load().ltlb200_trim(local_rank)
+            try:
+                extra[name] = regex_arm(name, max_cost, args.seed, local_rank, 2, 1)
+            except Exception as err:  # noqa: BLE001
+                extra[name] = {"error": str(err)[:200]}
         _native.load().ltlb200_trim(local_rank)
 
     if rank != 0:

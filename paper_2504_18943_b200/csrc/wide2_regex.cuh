@@ -21,14 +21,19 @@
 #pragma once
 // (included by wide2.cuh inside namespace ltlb200, between the batch passes and the tile dispatch)
 
-// lane r holds row r of a 32 x 32 bit matrix (bit c = column c); returns column `lane` (bit r = row r)
+// lane r holds row r of a 32 x 32 bit matrix (bit c = column c); returns column `lane` (bit r = row r).
+// Five butterfly rounds, s = 16, 8, 4, 2, 1: a lane keeps the half of its word that stays and takes the other half from
+// lane ^ s, shifted by s towards it.  The sender rotates (left by s if its bit s is set, right otherwise: the bits that
+// wrap around land where the receiver's mask drops them), so a round is one funnel shift, one shuffle and one LOP3.
 __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) {
         const uint32_t m = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
-        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-        x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y & m) << s));
+        const bool up = (lane & s) != 0;
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, __funnelshift_l(x, x, up ? s : 32 - s), s);
+        const uint32_t keep = up ? ~m : m;
+        x = (x & keep) | (y & ~keep);
     }
     return x;
 }
@@ -36,6 +41,7 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
 // rows [word][lane] -> bit-sliced [infix] (and back: the transpose is its own inverse), 32 infixes per step
 __device__ __forceinline__ void regex_slice(const uint32_t *rows, uint32_t *sliced, int n_words) {
     const int lane = threadIdx.x & 31;
+#pragma unroll 2
     for (int q = 0; q < n_words; ++q) sliced[q * 32 + lane] = transpose32(rows[q * 32 + lane]);
 }
 
@@ -166,7 +172,7 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
             col[(p * 4 + 3) * 32] = x.w;
         }
         __syncwarp();
-        regex_slice(reinterpret_cast<const uint32_t *>(W.vec), W.sliced, n_words);
+        regex_slice(reinterpret_cast<const uint32_t *>(W.vec), W.sliced, sc_words);
         const u64 v = vbase + lane;
         const bool v_ok = v < n_vec;
 #pragma unroll 1
@@ -189,7 +195,7 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
                     __syncwarp();
                 }
             }
-            regex_slice(W.out, W.out, n_words);  // one row per lane, in place
+            regex_slice(W.out, W.out, sc_words);  // one row per lane, in place (the words past the last infix stay zero)
             __syncwarp();
             const bool live[1] = {v_ok};
             const u64 ords[1] = {ord0 + (VEC_B ? (s0 + k) * nb + v : v * nb + (s0 + k))};

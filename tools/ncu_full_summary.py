@@ -16,6 +16,9 @@ KEEP = [
     r"^lts__t_sectors_srcunit_tex_op_read\.sum$", r"^lts__t_sectors_srcunit_tex_op_read_lookup_hit\.sum$",
     r"^smsp__thread_inst_executed_per_inst_executed\.ratio$", r"^l1tex__data_bank_conflicts_pipe_lsu_mem_shared\.sum$",
     r"^smsp__average_warps_issue_stalled_.*_per_issue_active\.ratio$",
+    r"^sm__inst_executed_pipe_(alu|fma|lsu|xu|adu|cbu|uniform)\.avg\.pct_of_peak_sustained_active$",
+    r"^l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate\.pct$", r"^l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum\.pct_of_peak_sustained_elapsed$",
+    r"^sm__throughput\.avg\.pct_of_peak_sustained_elapsed$",
 ]
 
 
