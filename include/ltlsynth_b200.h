@@ -116,7 +116,7 @@ ltlb200_engine *ltlb200_create(int32_t trace_count, int32_t lane_bits, const uin
 int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights);
 
 /*
- * REGEX FRONT-END, first slice.  Not in the reference (SPEC.md:11 scopes regular-expression
+ * REGEX FRONT-END.  Not in the reference (SPEC.md:11 scopes regular-expression
  * synthesis out; PAPER.md:81-113 only motivates it): no reference interface to cite, PARITY UNPINNED; the CPU
  * oracle is oracle/regex_oracle.py (membership pinned to Python's re.fullmatch).
  *
@@ -129,7 +129,9 @@ int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights);
  *   op_mask bits  LTLB200_OP_RE_QUESTION  r?      LTLB200_OP_RE_STAR  r*
  *                 LTLB200_OP_RE_CONCAT    r s     LTLB200_OP_OR       r | s  (union)
  * and the five cost parameters (literal, ?, *, concatenation, union) are ltlb200_set_weights on the tags
- * 0, 8, 9, 10, 6.  This slice takes CSs of up to 128 bits (the narrow kernels).
+ * 0, 8, 9, 10, 6.  CSs of up to 128 bits take the narrow kernels, up to 4096 bits the wide ones (infixes must be
+ * sorted by length: the right part of a split comes before the whole); a sharded search (ltlb200_route_begin) is
+ * refused for the wide ones.
  */
 enum { LTLB200_OP_RE_QUESTION = 8, LTLB200_OP_RE_STAR = 9, LTLB200_OP_RE_CONCAT = 10 };
 int ltlb200_set_regex(ltlb200_engine *e, int32_t n_bits, const uint32_t *offsets, const uint32_t *entries, uint64_t n_entries);
