@@ -245,6 +245,29 @@ class CandidateStore:
             return np.empty((0, self.trace_count), dtype=self.dtype)
         return np.concatenate(parts, axis=0)
 
+    # -- the reference's key helpers (engine.py:130, 151-167).  The dedup set itself lives on the device; these are
+    # host-side views for callers that inspect a store the way the reference's tests could.
+    def pack_rows(self, rows: np.ndarray) -> np.ndarray:
+        """CM rows as (n, key_words) uint64 keys: the row's bytes, zero-padded to a multiple of eight."""
+        rows = np.ascontiguousarray(rows, dtype=self.dtype)
+        n, row_bytes = len(rows), self.trace_count * self.dtype.itemsize
+        padded = np.zeros((n, self.key_words * 8), dtype=np.uint8)
+        padded[:, :row_bytes] = rows.reshape(n, -1).view(np.uint8)
+        return padded.view(np.uint64)
+
+    def keys_of(self, packed: np.ndarray) -> list:
+        """Hashable keys of packed rows: ints for one-word keys, bytes otherwise (as the reference's)."""
+        packed = np.ascontiguousarray(packed, dtype=np.uint64)
+        if self.key_words == 1:
+            return [int(k) for k in packed[:, 0]]
+        stride, raw = self.key_words * 8, packed.tobytes()
+        return [raw[k:k + stride] for k in range(0, len(raw), stride)]
+
+    @property
+    def seen(self) -> set:
+        """Keys of every stored CM, rebuilt from the levels on each access (the live set is the device hash set)."""
+        return set(self.keys_of(self.pack_rows(self.all_cms()))) if self.levels else set()
+
     def device_stats(self) -> dict:
         st = _native.Stats()
         _native.check(_native.load().ltlb200_get_stats(self._handle, ctypes.byref(st)), "get_stats")

@@ -63,3 +63,26 @@ def test_engine_solves_paper_example_like_reference():
     # the 7+7 example to its cost-16 witness: 142,066,187 candidates, 16,258,320 unique CMs
     # (golden digests of all 16 levels; the oracle replay would take minutes, so golden only)
     _run_case("spec2_found", compare_oracle=False)
+
+
+@pytest.mark.parametrize("workload,max_cost", [("c1", 7), ("c3", 6), ("c3wide", 5)])
+def test_key_helpers_of_the_reference_store(workload, max_cost):
+    """`pack_rows`, `keys_of`, `seen` (reference engine.py:130, 151-167): one key per stored CM, zero-padded row bytes
+    (8-byte rows -> int keys, 16 / 80-byte rows -> bytes keys)."""
+    import numpy as np
+
+    spec = workloads.named_workload(workload, 0)
+    store = engine.CandidateStore(spec)
+    try:
+        for cost in range(1, max_cost + 1):
+            engine.expand_level(store, cost, config=engine.EngineConfig(exhaustive=True))
+        rows = store.all_cms()
+        packed = store.pack_rows(rows)
+        row_bytes = store.trace_count * store.dtype.itemsize
+        assert packed.dtype == np.uint64 and packed.shape == (store.total, -(-row_bytes // 8))
+        assert packed.view(np.uint8).reshape(store.total, -1)[:, :row_bytes].tobytes() == rows.tobytes()
+        keys = store.keys_of(packed)
+        assert all(isinstance(k, int if store.key_words == 1 else bytes) for k in keys[:4])
+        assert len(set(keys)) == len(keys) == store.total and store.seen == set(keys)
+    finally:
+        store.close()
