@@ -130,8 +130,8 @@ int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights);
  *                 LTLB200_OP_RE_CONCAT    r s     LTLB200_OP_OR       r | s  (union)
  * and the five cost parameters (literal, ?, *, concatenation, union) are ltlb200_set_weights on the tags
  * 0, 8, 9, 10, 6.  CSs of up to 128 bits take the narrow kernels, up to 4096 bits the wide ones (infixes must be
- * sorted by length: the right part of a split comes before the whole); a sharded search (ltlb200_route_begin) is
- * refused for the wide ones.
+ * sorted by length: the right part of a split comes before the whole).  A sharded search (ltlb200_route_begin ...)
+ * works for both.
  */
 enum { LTLB200_OP_RE_QUESTION = 8, LTLB200_OP_RE_STAR = 9, LTLB200_OP_RE_CONCAT = 10 };
 int ltlb200_set_regex(ltlb200_engine *e, int32_t n_bits, const uint32_t *offsets, const uint32_t *entries, uint64_t n_entries);

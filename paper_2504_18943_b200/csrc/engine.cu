@@ -1975,7 +1975,6 @@ int Engine::route_begin(int cost, uint32_t op_mask, bool exhaustive, double dead
     if (pending_.active) throw std::invalid_argument("route_begin: the previous level was not ended");
     if (cost != (int)levels_.size() + 1) throw std::invalid_argument("cost must be the next unbuilt level");
     if (world < 1 || world > ROUTE_MAX_WORLD || rank < 0 || rank >= world) throw std::invalid_argument("bad shard (at most 8 ranks)");
-    if (wide_ && lw_ == LW_REGEX) throw std::invalid_argument("regex front-end: sequences wider than 128 bits are not sharded over GPUs");
     CUDA_CHECK(cudaSetDevice(device_));
     discard_lookahead();
     set_sharding(world, rank);

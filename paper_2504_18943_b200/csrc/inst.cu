@@ -115,7 +115,6 @@ static void launch_operator(const WideParams &P, int grid, size_t smem, int devi
     wide2_level_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
 }
 
-#if LTLB200_INST_LW != 1
 template <int OP>
 static void launch_route(const WideParams &P, int grid, size_t smem, int device, cudaStream_t st) {
     static unsigned long long seen = 0;
@@ -123,7 +122,6 @@ static void launch_route(const WideParams &P, int grid, size_t smem, int device,
     opt_in(wide2_route_kernel<LW, OP>, device, seen, mu);
     wide2_route_kernel<LW, OP><<<grid, CTA_THREADS, smem, st>>>(P);
 }
-#endif
 
 void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WideParams &P, int grid, size_t smem, int device,
                                                  cudaStream_t st) {
@@ -141,8 +139,17 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
         wide2_guarded_level_kernel<LW><<<grid, CTA_THREADS, smem, st>>>(P);
         return;
     }
-#if LTLB200_INST_LW == 1  // the regex front-end's operators (regex_ops.cuh); no sharded search in this slice
-    if (kind == LK_ROUTE) return;
+#if LTLB200_INST_LW == 1  // the regex front-end's operators (regex_ops.cuh, wide2_regex.cuh)
+    if (kind == LK_ROUTE) {
+        switch (op) {
+            case OP_ATOM: launch_route<OP_ATOM>(P, grid, smem, device, st); break;
+            case OP_RE_QUESTION: launch_route<OP_RE_QUESTION>(P, grid, smem, device, st); break;
+            case OP_RE_STAR: launch_route<OP_RE_STAR>(P, grid, smem, device, st); break;
+            case OP_RE_CONCAT: launch_route<OP_RE_CONCAT>(P, grid, smem, device, st); break;
+            default: launch_route<OP_OR>(P, grid, smem, device, st); break;
+        }
+        return;
+    }
     switch (op) {
         case OP_ATOM: launch_operator<OP_ATOM>(P, grid, smem, device, st); break;
         case OP_RE_QUESTION: launch_operator<OP_RE_QUESTION>(P, grid, smem, device, st); break;

@@ -275,18 +275,18 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
 // here; its row goes to the send region of its hash owner.  Pass 1 yields the owner hash, the separation flag and
 // the equals-an-operand flags; the lanes of one owner take consecutive records (one atomicAdd per owner present in
 // the batch row); pass 2 writes the row -- nvec consecutive vectors per lane, whole 32-byte sectors.
-template <int LW, int OP, class Gen>
+template <int LW, int OP, int NB, class Gen>
 __device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wide2Warp &W, Gen gen,
-                                                  const bool (&live)[W2_BATCH], const u64 (&ords)[W2_BATCH]) {
+                                                  const bool (&live)[NB], const u64 (&ords)[NB]) {
     const int nvec = P.nvec;
-    uint32_t ho[W2_BATCH], sepacc[W2_BATCH], da[W2_BATCH], db[W2_BATCH];
+    uint32_t ho[NB], sepacc[NB], da[NB], db[NB];
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) ho[r] = sepacc[r] = da[r] = db[r] = 0u;
+    for (int r = 0; r < NB; ++r) ho[r] = sepacc[r] = da[r] = db[r] = 0u;
 #pragma unroll 1
     for (int p = 0; p < nvec; ++p) {
         const uint4 valid = W.consts[p], target = W.consts[nvec + p];
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
+        for (int r = 0; r < NB; ++r) {
             uint4 a, b, c;
             gen(r, p, a, b, c);
             ho[r] ^= hash_vec(c, 0x5BD1E995u * (uint32_t)(p + 1));
@@ -295,12 +295,12 @@ __device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wid
             db[r] |= v_diff(c, b);
         }
     }
-    u64 at[W2_BATCH];
-    bool send[W2_BATCH];
+    u64 at[NB];
+    bool send[NB];
     const uint32_t lt = lanemask_lt();
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) {
+    for (int r = 0; r < NB; ++r) {
         if (live[r] && sepacc[r] == 0u) {
             if (P.route_sep_any) atomicMin(&P.counters[CTR_SEP], ords[r]);
             if (P.sep_list) {
@@ -332,12 +332,12 @@ __device__ __forceinline__ void wide2_route_batch(const WideParams &P, const Wid
     }
     bool any = false;
 #pragma unroll
-    for (int r = 0; r < W2_BATCH; ++r) any = any || at[r] != ~0ull;
+    for (int r = 0; r < NB; ++r) any = any || at[r] != ~0ull;
     if (!any) return;
 #pragma unroll 1
     for (int p = 0; p < nvec; ++p) {
 #pragma unroll
-        for (int r = 0; r < W2_BATCH; ++r) {
+        for (int r = 0; r < NB; ++r) {
             if (at[r] == ~0ull) continue;
             uint4 a, b, c;
             gen(r, p, a, b, c);

@@ -123,7 +123,8 @@ __device__ __forceinline__ void wide2_regex_unary_tile(const WideParams &P, cons
             else if constexpr (OP == OP_RE_QUESTION) c = make_uint4(a.x | (p == 0 ? 1u : 0u), a.y, a.z, a.w);
             else c = a;
         };
-        wide2_batch<LW_REGEX, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
+        if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW_REGEX, OP>(P, W, gen, live, ords);
+        else wide2_batch<LW_REGEX, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
     }
 }
 
@@ -206,7 +207,8 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
                 b = VEC_B ? xv : xs;
                 c = make_uint4(ow[(p * 4) * 32], ow[(p * 4 + 1) * 32], ow[(p * 4 + 2) * 32], ow[(p * 4 + 3) * 32]);
             };
-            wide2_batch<LW_REGEX, OP_RE_CONCAT, MODE == W2_GUARD>(P, W, st, gen, live, ords);
+            if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW_REGEX, OP_RE_CONCAT>(P, W, gen, live, ords);
+            else wide2_batch<LW_REGEX, OP_RE_CONCAT, MODE == W2_GUARD>(P, W, st, gen, live, ords);
         }
     }
 }

@@ -138,7 +138,7 @@ def sharded_expand_level(store: ShardEngine, cost: int, ops, config: EngineConfi
     the single-GPU ``expand_level``."""
     stats = stats if stats is not None else RunStats()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    mask = operator_mask(ops)
+    mask = ops if isinstance(ops, int) else operator_mask(ops)  # (an operator mask as it is: the regex front-end's tags)
     device = _device_of(store)
     # A NON-exhaustive level over a store that already holds a separating CM is built by every rank on its own,
     # whatever its size: the reference then truncates every chunk at its first separating candidate

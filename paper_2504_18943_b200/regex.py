@@ -275,9 +275,14 @@ class RegexResult:
     failure: str | None = None
 
 
-def synthesize_regex(spec: RegexSpecification, config: RegexConfig = RegexConfig()) -> RegexResult:
+def synthesize_regex(spec: RegexSpecification, config: RegexConfig = RegexConfig(), group=None) -> RegexResult:
     """Minimum-cost regular expression that accepts every positive and rejects every negative example, by level-wise
-    enumeration of characteristic sequences on the GPU.  The result is re-checked with ``re.fullmatch``."""
+    enumeration of characteristic sequences on the GPU.  The result is re-checked with ``re.fullmatch``.
+
+    ``group``: a ``torch.distributed`` process group (one rank per GPU, every rank calls this with the same
+    arguments and ``config.device`` = its own GPU): the search is sharded over the ranks with the LTL engine's protocol
+    (``dist.sharded_expand_level``: candidates routed to their hash owners, winners published to every rank) and every
+    rank returns the same result as a single-GPU run."""
     t0 = time.perf_counter()
     store = RegexStore(spec, config.cost, device=config.device, hbm_budget_mb=config.hbm_budget_mb)
     try:
@@ -285,9 +290,22 @@ def synthesize_regex(spec: RegexSpecification, config: RegexConfig = RegexConfig
         deadline = _monotonic() + config.time_budget_s
         for cost in range(1, config.max_cost + 1):
             stats.max_cost_reached = cost
-            status, _, sep_gid, delta = store.expand(cost, config.exhaustive, deadline)
-            stats.constructed += delta
-            stats.unique = store.total
+            if group is not None:
+                from . import dist as _dist
+                from .engine import EngineConfig
+
+                try:
+                    _, sep_gid = _dist.sharded_expand_level(
+                        store, cost, _OP_MASK, EngineConfig(exhaustive=config.exhaustive, batch_size=1, memory_budget_mb=1 << 30),
+                        stats, deadline, group)
+                except _BudgetExceeded as stop:
+                    failure = str(stop)
+                    break
+                status = 0
+            else:
+                status, _, sep_gid, delta = store.expand(cost, config.exhaustive, deadline)
+                stats.constructed += delta
+                stats.unique = store.total
             if status in _FAILURE_TEXT:
                 failure = _FAILURE_TEXT[status]
                 break

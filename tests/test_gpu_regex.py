@@ -181,6 +181,61 @@ def test_baseline_shaped_example_sets_equal_the_oracle(name, max_cost, bits):
         store.close()
 
 
+@pytest.mark.parametrize("name,seed,max_cost,world", [("re-c0", 0, 8, 2), ("re-c0", 3, 7, 3), ("re-c2", 0, 11, 2), ("re-email", 0, 6, 3)])
+def test_sharded_search_of_regex_stores(name, seed, max_cost, world):
+    """One regex search over several ranks (stores on one GPU play them, the exchange done by hand as in
+    tests/test_gpu_sharded.py): candidates routed to their hash owners -- one-vector sequences through the narrow route
+    kernel, wider ones through the bit-sliced tiles in route mode -- and every rank ends every level equal to the oracle."""
+    from paper_2504_18943_b200 import engine
+    from paper_2504_18943_b200.workloads import regex_workload
+    from test_gpu_sharded import _exchange_level
+
+    spec = regex_workload(name, seed)
+    stores, ref = [rx.RegexStore(spec) for _ in range(world)], ro.RegexOracle(spec)
+    cfg = engine.EngineConfig(exhaustive=True, batch_size=1)
+    try:
+        for c in range(1, max_cost + 1):
+            results = _exchange_level(stores, c, cfg, mask=rx._OP_MASK)
+            o_new, o_sep, o_constructed = ref.expand_level(c, exhaustive=True)
+            for r, (status, n_new, sep, delta) in enumerate(results):
+                assert (status, n_new, delta) == (0, o_new, o_constructed), f"{name} cost {c} rank {r}"
+                _assert_level_equal(stores[r], ref, c, f"{name} cost {c} rank {r}")
+    finally:
+        for s in stores:
+            s.close()
+
+
+def test_synthesize_regex_over_a_process_group():
+    """The real protocol code (dist.sharded_expand_level over NCCL) with one rank: every level through the exchange,
+    small levels built locally, and the default threshold; same expression and counters as the oracle."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_18943_b200 import dist as pdist
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    default_threshold = pdist.REPLICATE_BELOW
+    try:
+        cases = [(rx.RegexSpecification(("abcabcabcabc", "abcabc", "abc"), ("cacbaccbabacab", "bccabbabcbbaca", "cbabcaacbcabbb", "abcab", "bca", "acb")), 9),
+                 (random_binary_spec(random.Random(101)), 9)]
+        for spec, max_cost in cases:
+            want = ro.synthesize(spec, max_cost=max_cost)
+            for replicate_below in (0, 500, default_threshold):
+                pdist.REPLICATE_BELOW = replicate_below
+                res = rx.synthesize_regex(spec, rx.RegexConfig(max_cost=max_cost), group=dist.group.WORLD)
+                assert (res.pattern, res.cost, res.stats.unique, res.stats.constructed) == (want.pattern, want.cost, want.unique, want.constructed)
+    finally:
+        pdist.REPLICATE_BELOW = default_threshold
+        dist.destroy_process_group()
+
+
 def test_sequences_beyond_4096_bits_are_refused():
     words = _wide_words(7, n_words=12, length=(28, 30), letters="abcdefgh")
     with pytest.raises(_native.NativeEngineError, match="4096 bits"):

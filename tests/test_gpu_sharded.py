@@ -20,10 +20,10 @@ pytestmark = pytest.mark.gpu
 NO_SEP = (1 << 64) - 1
 
 
-def _exchange_level(stores, cost, cfg):
+def _exchange_level(stores, cost, cfg, mask=None):
     """dist.sharded_expand_level with the collectives done by hand between stores on one device."""
     world = len(stores)
-    mask = engine.operator_mask(cfg.operators)
+    mask = engine.operator_mask(cfg.operators) if mask is None else mask
     # 1. route
     begun = [s.route_begin(cost, mask, cfg.exhaustive, None, r, world) for r, s in enumerate(stores)]
     assert all(b[0] == 0 for b in begun)
