@@ -7,7 +7,13 @@ that scripts written against the reference run unchanged:
 
 synth exit codes: 0 separator found, 2 budget exhausted, 1 input error (``cli.py:1-5``).
 check exit codes: 0 formula separates, 2 it does not, 1 input error.
-Extensions (absent from the reference, default to its behaviour): ``--device``, ``--gpus``.
+Extensions (absent from the reference, default to its behaviour): ``--device``, ``--gpus``, and the ``regex``
+command of the regex front-end (no reference counterpart):
+
+    python -m paper_2504_18943_b200 regex --input examples.txt [--cost 1,1,1,1,1] [--max-cost 12] [--format json]
+
+where the file holds one example string per line, the positives, a line ``---``, the negatives (a line ``<eps>`` is
+the empty string).  Exit codes as for synth.
 ``--threads`` is accepted and ignored: the device schedules its own parallelism, and the
 reference guarantees that the thread count changes nothing (its tests/test_cli.py:130-140).
 """
@@ -50,6 +56,13 @@ def make_parser() -> argparse.ArgumentParser:
     check = commands.add_parser("check", help="check a formula against a specification")
     check.add_argument("--input", required=True, help="trace specification file")
     check.add_argument("--formula", required=True, help="formula text, e.g. '!(b U a)'")
+    regex = commands.add_parser("regex", help="synthesize a minimum-cost regular expression (extension)")
+    regex.add_argument("--input", required=True, help="example strings: positives, a line '---', negatives")
+    regex.add_argument("--cost", default="1,1,1,1,1", help="cost of a literal, ?, *, concatenation, union")
+    regex.add_argument("--max-cost", type=int, default=12)
+    regex.add_argument("--time-budget-s", type=float, default=300.0)
+    regex.add_argument("--format", choices=("text", "json"), default="text")
+    regex.add_argument("--device", type=int, default=0)
     return parser
 
 
@@ -116,9 +129,55 @@ def run_check(args) -> int:
     return 0 if all_good else 2
 
 
+def parse_examples(text: str):
+    """Example strings of the regex command: one per line, positives / ``---`` / negatives; ``<eps>`` = the empty string."""
+    sides, current = [[], []], 0
+    for number, line in enumerate(text.splitlines(), 1):
+        line = line.rstrip("\r\n")
+        if line.strip() == "---":
+            if current == 1:
+                raise ValueError(f"line {number}: a second '---'")
+            current = 1
+        elif line.strip() == "<eps>":
+            sides[current].append("")
+        elif line:
+            sides[current].append(line)
+    if current == 0:
+        raise ValueError("no '---' line between the positive and the negative examples")
+    return tuple(sides[0]), tuple(sides[1])
+
+
+def run_regex(args) -> int:
+    from .regex import CostFunction, RegexConfig, RegexSpecification, synthesize_regex  # (needs the CUDA engine)
+    from .traces import InfeasibleSpecificationError
+
+    try:
+        with open(args.input, "r", encoding="utf-8") as handle:
+            positives, negatives = parse_examples(handle.read())
+        parts = [int(x) for x in args.cost.split(",")]
+        if len(parts) != 5:
+            raise ValueError("--cost takes five integers: literal, ?, *, concatenation, union")
+        spec = RegexSpecification(positives, negatives)
+        config = RegexConfig(cost=CostFunction(*parts), max_cost=args.max_cost, time_budget_s=args.time_budget_s, device=args.device)
+    except (OSError, ValueError, InfeasibleSpecificationError) as problem:
+        print(f"error: {problem}", file=sys.stderr)
+        return 1
+    result = synthesize_regex(spec, config)
+    report = {"regex": result.pattern, "cost": result.cost, "constructed": result.stats.constructed, "unique": result.stats.unique,
+              "elapsed_ms": round(1000.0 * result.stats.elapsed_s, 3), "cost_function": parts,
+              "budgets": {"max_cost": args.max_cost, "time_budget_s": args.time_budget_s}, "outcome": result.outcome}
+    if args.format == "json":
+        print(json.dumps(report))
+    else:
+        print(f"regex: {result.pattern}\ncost: {result.cost}" if result.pattern is not None
+              else f"no expression found ({result.failure or 'budget exhausted'})")
+        print(f"constructed: {report['constructed']}  unique: {report['unique']}  elapsed_ms: {report['elapsed_ms']}")
+    return 0 if result.outcome == OUTCOME_FOUND else 2
+
+
 def main(argv=None) -> int:
     args = make_parser().parse_args(argv)
-    return run_synth(args) if args.command == "synth" else run_check(args)
+    return {"synth": run_synth, "check": run_check, "regex": run_regex}[args.command](args)
 
 
 def entry_point() -> None:

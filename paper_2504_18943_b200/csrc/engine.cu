@@ -6,7 +6,8 @@
 //
 //   plan      canonical block list of the level (reference _tasks_for_level,
 //             engine.py:219-266, minus its batch chunking) -> ordinal offsets, tiles
-//   enumerate one persistent launch of the construction+dedup kernel (narrow.cuh / wide.cuh)
+//   enumerate persistent launches of the construction+dedup kernels (narrow.cuh / wide2.cuh), one per operator on
+//             big levels, one for all on small ones, one for several tiny levels (narrow_tiny.cuh)
 //   finalise  bitmap-rank compaction: winners ordered by ordinal, appended to the cache
 //   account   `constructed` as the reference counts it, including its chunk rounding on
 //             the level that holds the separator (engine.py:418,445-446)

@@ -462,8 +462,8 @@ __device__ __forceinline__ uint4 apply_op(const NarrowParams &P, uint4 a, uint4 
 }
 
 // The tile runners are generic over where candidates go: `sink.emit<LW>(cand, live, known, ord_of)`
-// is the direct insert (DirectSink -> insert_batch) or the bucket scatter of the partitioned
-// path (narrow_part.cuh); WS is the warp's shared state (rows / term / block).
+// is the direct insert (DirectSink -> insert_batch), the routing to hash owners of a sharded search (RouteSink) or
+// the tiny-levels kernel's sink (narrow_tiny.cuh); WS is the warp's shared state (rows / term / block).
 // Both return true when this tile AND every later tile of the launch are ordered after the
 // separator (tiles follow the canonical order of their outer index), so the warp can stop
 // drawing tickets instead of fetching and skipping them one by one.

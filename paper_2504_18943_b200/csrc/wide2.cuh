@@ -1,9 +1,9 @@
 // wide2.cuh -- construction + dedup kernel for multi-vector CMs, one LANE per candidate.
 //
-// wide.cuh gives a candidate to a group of G lanes (one uint4 each).  Its ncu capture on the
-// LTL configuration of BASELINE.json (c5: 128-byte CMs) shows why that is slow: 96 warp
+// Round 1's first wide kernel gave a candidate to a group of G lanes (one uint4 each).  Its ncu capture on the
+// LTL configuration of BASELINE.json (c5: 128-byte CMs) showed why that is slow: 96 warp
 // instructions per candidate, because everything that is scalar per candidate -- hashing,
-// the slot probe, the claim, the CAS -- runs with 1/G of the lanes, and every step is a
+// the slot probe, the claim, the CAS -- ran with 1/G of the lanes, and every step was a
 // group-wide ballot or shuffle.  Here a lane owns a whole candidate, like in the narrow path:
 //
 //   * a tile = 32 vector-operand rows (one per lane) x up to tile_s scalar-operand rows; both are
@@ -16,9 +16,11 @@
 //     need it, pass 2 streams over the vectors again: a CLAIM writes them to its staging entry,
 //     a fingerprint MATCH compares them with the stored row.  Rebuilding a vector costs a few
 //     dozen integer instructions; keeping 32 rows x nvec vectors in registers is impossible;
-//   * the hash set, the staging pool, the publish protocol (row -> fence -> 64-bit CAS) and the
-//     finalisation are wide.cuh's, unchanged: both kernels can run against the same set (the
-//     sharded import and the regrow still use wide.cuh's code), and the results are identical.
+//   * the hash set, the row log and the publish protocol (row -> release-ordered 64-bit CAS on the slot word)
+//     are wide_common.cuh's; the group-collective insert there serves the import of exchanged records and
+//     the regrow, against the same set;
+//   * the regex grammar (LW_REGEX) has its own tiles for the operators that are not vector-local
+//     (wide2_regex.cuh) and shares the passes below.
 #pragma once
 #include "regex_ops.cuh"
 #include "wide_common.cuh"
@@ -159,7 +161,7 @@ __device__ __forceinline__ void wide2_batch(const WideParams &P, const Wide2Warp
     u64 w[NB], entry[NB];
     bool active[NB], fresh[NB];
 #pragma unroll
-    for (int r = 0; r < NB; ++r) {  // final mix of wide.cuh's row_hash
+    for (int r = 0; r < NB; ++r) {  // final mix of wide_common.cuh's row_hash
         uint32_t a = ha[r], b = hb[r];
         a ^= a >> 16;
         a *= 0x85EBCA6Bu;

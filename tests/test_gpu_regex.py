@@ -236,6 +236,25 @@ def test_synthesize_regex_over_a_process_group():
         dist.destroy_process_group()
 
 
+def test_regex_command_line(tmp_path, capsys):
+    import json
+
+    from paper_2504_18943_b200 import cli
+
+    path = tmp_path / "examples.txt"
+    path.write_text("abcabcabcabc\nabcabc\nabc\n<eps>\n---\nabcab\nbca\nacb\nab\n")
+    assert cli.main(["regex", "--input", str(path), "--format", "json"]) == 0
+    report = json.loads(capsys.readouterr().out)
+    want = ro.synthesize(rx.RegexSpecification(("abcabcabcabc", "abcabc", "abc", ""), ("abcab", "bca", "acb", "ab")), max_cost=12)
+    assert (report["regex"], report["cost"], report["constructed"], report["unique"], report["outcome"]) == \
+        (want.pattern, want.cost, want.constructed, want.unique, "found")
+    assert cli.main(["regex", "--input", str(path), "--max-cost", "3"]) == 2     # budget exhausted
+    assert "no expression found" in capsys.readouterr().out
+    path.write_text("ab\n---\nab\n")
+    assert cli.main(["regex", "--input", str(path)]) == 1                         # infeasible
+    assert "error:" in capsys.readouterr().err
+
+
 def test_sequences_beyond_4096_bits_are_refused():
     words = _wide_words(7, n_words=12, length=(28, 30), letters="abcdefgh")
     with pytest.raises(_native.NativeEngineError, match="4096 bits"):

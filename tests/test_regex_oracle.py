@@ -90,3 +90,14 @@ def test_minimality_against_bruteforce(cost):
         assert res.cost == brute[0] == rx.regex_cost(res.regex, cost), (rx.to_pattern(brute[1]), res.pattern)
         assert all(re.fullmatch(res.pattern, w) for w in spec.positives) and not any(re.fullmatch(res.pattern, w) for w in spec.negatives)
     assert solved >= 4
+
+
+def test_example_file_of_the_regex_command():
+    from paper_2504_18943_b200 import cli
+
+    assert cli.parse_examples("ab\n<eps>\n\n---\nb\r\na b\n") == (("ab", ""), ("b", "a b"))
+    for bad in ("ab\n", "a\n---\nb\n---\nc\n"):
+        with pytest.raises(ValueError):
+            cli.parse_examples(bad)
+    args = cli.make_parser().parse_args(["regex", "--input", "x.txt", "--cost", "1,2,2,1,3"])
+    assert (args.command, args.cost, args.max_cost, args.format) == ("regex", "1,2,2,1,3", 12, "text")
