@@ -32,6 +32,9 @@ namespace ltlb200 {
 #ifndef LTLB200_WIDE2_MIN_CTAS
 #define LTLB200_WIDE2_MIN_CTAS 3
 #endif
+#ifndef LTLB200_RE_MIN_CTAS
+#define LTLB200_RE_MIN_CTAS 5  // regex tiles: one candidate per lane in the passes; 96 registers (4 and 5 CTAs measure the same on the e-mail example, 5 is 9 % faster on re-c2, 6 spills)
+#endif
 #ifndef LTLB200_W2_BATCH
 #define LTLB200_W2_BATCH 2
 #endif
@@ -50,14 +53,15 @@ struct __align__(16) Wide2Fixed {  // per-warp shared state behind the row areas
     u64 ticket, sep_now;
 };
 
-// Regex grammar (LW_REGEX, wide2_regex.cuh): fewer scalar rows per tile, and two more areas per warp, each the size of
-// the vector-row area -- the 32 vector rows BIT-SLICED (word x = bit x of every row) and the 32 result rows.
+// Regex grammar (LW_REGEX, wide2_regex.cuh): fewer scalar rows per tile, and one more area per warp the size of the
+// vector-row area -- the 32 vector rows BIT-SLICED (word x = bit x of every row); the vector-row area itself also
+// takes the 32 result rows of the concatenation and star tiles.
 constexpr int W2_RE_SC_VECS = 128;
 
-// per-warp shared memory in uint4 units: vec rows | scalar rows | valid + target | fixed part [| bit-sliced rows | result rows]
+// per-warp shared memory in uint4 units: vec rows | scalar rows | valid + target | fixed part [| bit-sliced rows]
 __host__ __device__ inline size_t wide2_warp_vecs(int nvec, bool regex = false) {
     const size_t fixed = 2 * (size_t)nvec + (sizeof(Wide2Fixed) + 15) / 16;
-    if (regex) return (size_t)nvec * 32 + W2_RE_SC_VECS + fixed + 2 * (size_t)nvec * 32;
+    if (regex) return (size_t)nvec * 32 + W2_RE_SC_VECS + fixed + (size_t)nvec * 32;
     return (size_t)nvec * 32 + W2_SC_VECS + fixed;
 }
 __host__ __device__ inline int wide2_tile_s(int nvec, bool regex = false) {
@@ -487,7 +491,7 @@ __device__ __forceinline__ Wide2Warp wide2_carve(const WideParams &P, uint4 *bas
     W.sliced = W.out = nullptr;
     if constexpr (kRegex) {
         W.sliced = reinterpret_cast<uint32_t *>(mine + (size_t)P.nvec * 32 + W2_RE_SC_VECS + 2 * (size_t)P.nvec + (sizeof(Wide2Fixed) + 15) / 16);
-        W.out = W.sliced + (size_t)P.nvec * 128;
+        W.out = reinterpret_cast<uint32_t *>(W.vec);  // (the union tile stages its vector rows there, wide2_binary_tile)
         if (P.guide_smem_words) {  // the guide table behind the warps' areas: one copy per CTA
             uint32_t *g = reinterpret_cast<uint32_t *>(base + (size_t)WARPS_PER_CTA * wide2_warp_vecs(P.nvec, true));
             for (uint32_t k = threadIdx.x; k < P.guide_smem_words; k += blockDim.x) g[k] = __ldg(P.guide + k);
@@ -567,7 +571,7 @@ __device__ __forceinline__ void wide2_run_tile_any(const WideParams &P, const Wi
 }
 
 template <int LW, int OP>
-__global__ void __launch_bounds__(CTA_THREADS, LW == LW_REGEX ? 4 : LTLB200_WIDE2_MIN_CTAS) wide2_level_kernel(const __grid_constant__ WideParams P) {
+__global__ void __launch_bounds__(CTA_THREADS, LW == LW_REGEX ? LTLB200_RE_MIN_CTAS : LTLB200_WIDE2_MIN_CTAS) wide2_level_kernel(const __grid_constant__ WideParams P) {
     extern __shared__ __align__(16) uint4 s_w2[];
     const Wide2Warp W = wide2_carve<LW>(P, s_w2);
     Wide2State st;

@@ -66,7 +66,20 @@ __device__ __forceinline__ RegexGuide regex_guide(const WideParams &P, const uin
     return G;
 }
 
-// literal, question, star
+// bit j of the result = rows `x` and `y` (both bit-sliced) differ in candidate j somewhere in the first n_bits infixes
+__device__ __forceinline__ uint32_t sliced_diff(const uint32_t *x, const uint32_t *y, int n_bits) {
+    uint32_t d = 0;
+    for (int k = threadIdx.x & 31; k < n_bits; k += 32) d |= x[k] ^ y[k];
+    return __reduce_or_sync(0xFFFFFFFFu, d);
+}
+
+// wide2_batch takes "the operands" of a candidate only to spot one that equals an operand (such a CM is in the cache
+// already).  The regex tiles decide that on the bit-sliced rows, 32 candidates at a time, and hand the verdict over
+// as operands that do / do not equal the result.
+__device__ __forceinline__ uint4 regex_operand_stub(uint4 c, bool equals) { return equals ? c : make_uint4(~c.x, ~c.y, ~c.z, ~c.w); }
+
+// literal, question, star.  The lanes' rows are staged word by word ([word][lane]) in the row area, which is also
+// where the finished rows end up; the star works on their bit-sliced copy.
 template <int OP, int MODE>
 __device__ __forceinline__ void wide2_regex_unary_tile(const WideParams &P, const Wide2Warp &W, Wide2State &st, u64 tile_local,
                                                        u64 sep_now) {
@@ -79,7 +92,7 @@ __device__ __forceinline__ void wide2_regex_unary_tile(const WideParams &P, cons
     if (ord0 + tile_local * per_tile > sep_now) return;
     const int n_steps = (int)min((u64)B.tile_s, (n - tile_local * per_tile + 31) / 32);
     const RegexGuide G = regex_guide(P, W.guide);
-    uint32_t *vw = reinterpret_cast<uint32_t *>(W.vec) + lane, *ow = W.out + lane;
+    uint32_t *ow = W.out + lane;
 #pragma unroll 1
     for (int k = 0; k < n_steps; ++k) {
         const u64 i = first + (u64)k * 32;
@@ -89,39 +102,55 @@ __device__ __forceinline__ void wide2_regex_unary_tile(const WideParams &P, cons
         __syncwarp();
         for (int p = 0; p < nvec; ++p) {  // every lane its own row, word by word into its own bank
             const uint4 x = __ldg(row + p);
-            vw[(p * 4) * 32] = x.x;
-            vw[(p * 4 + 1) * 32] = x.y;
-            vw[(p * 4 + 2) * 32] = x.z;
-            vw[(p * 4 + 3) * 32] = x.w;
+            ow[(p * 4) * 32] = x.x;
+            ow[(p * 4 + 1) * 32] = x.y;
+            ow[(p * 4 + 2) * 32] = x.z;
+            ow[(p * 4 + 3) * 32] = x.w;
+        }
+        bool same = false;  // the result equals the operand
+        if constexpr (OP == OP_RE_QUESTION) {
+            same = (ow[0] & 1u) != 0u;
+            ow[0] |= 1u;
         }
         if constexpr (OP == OP_RE_STAR) {
             __syncwarp();
-            regex_slice(reinterpret_cast<const uint32_t *>(W.vec), W.sliced, n_words);
+            regex_slice(W.out, W.sliced, n_words);
+            __syncwarp();
             for (int q = 0; q < n_words; ++q) W.out[q * 32 + lane] = 0u;
             __syncwarp();
             if (lane == 0) W.out[0] = 0xFFFFFFFFu;  // the empty word, in every row
             __syncwarp();
+            uint32_t e_lo = G.rounds[1];
 #pragma unroll 1
             for (uint32_t r = 1; r < P.guide_rounds; ++r) {
                 const uint32_t e_hi = G.rounds[r + 1];
-                for (uint32_t e = G.rounds[r] + lane; e < e_hi; e += 32) {
-                    const uint32_t uv = G.uv[e];
-                    const uint32_t u = uv & 0xFFFFu;
-                    if (u == 0u) continue;
-                    const uint32_t val = W.sliced[u] & W.out[uv >> 16];
-                    if (val) atomicOr(&W.out[G.w_of[e]], val);
+                // four entries per lane and step, their table words loaded together: with sequences of thousands of
+                // bits few warps fit an SM and nothing else hides the latency of the loads
+                for (uint32_t e0 = e_lo; e0 < e_hi; e0 += 128) {
+                    uint32_t uv[4], w[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint32_t e = e0 + (uint32_t)t * 32u + lane;
+                        uv[t] = e < e_hi ? G.uv[e] : 0u;  // (u = 0: skipped below)
+                        w[t] = e < e_hi ? G.w_of[e] : 0u;
+                    }
+                    uint32_t val[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) val[t] = (uv[t] & 0xFFFFu) ? (W.sliced[uv[t] & 0xFFFFu] & W.out[uv[t] >> 16]) : 0u;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (val[t]) atomicOr(&W.out[w[t]], val[t]);
                 }
+                e_lo = e_hi;
                 __syncwarp();
             }
+            same = ((sliced_diff(W.out, W.sliced, P.n_bits) >> lane) & 1u) == 0u;
             regex_slice(W.out, W.out, n_words);  // back to one row per lane, in place
         }
         __syncwarp();
         auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
-            a = make_uint4(vw[(p * 4) * 32], vw[(p * 4 + 1) * 32], vw[(p * 4 + 2) * 32], vw[(p * 4 + 3) * 32]);
-            b = a;
-            if constexpr (OP == OP_RE_STAR) c = make_uint4(ow[(p * 4) * 32], ow[(p * 4 + 1) * 32], ow[(p * 4 + 2) * 32], ow[(p * 4 + 3) * 32]);
-            else if constexpr (OP == OP_RE_QUESTION) c = make_uint4(a.x | (p == 0 ? 1u : 0u), a.y, a.z, a.w);
-            else c = a;
+            c = make_uint4(ow[(p * 4) * 32], ow[(p * 4 + 1) * 32], ow[(p * 4 + 2) * 32], ow[(p * 4 + 3) * 32]);
+            a = b = regex_operand_stub(c, same);
         };
         if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW_REGEX, OP>(P, W, gen, live, ords);
         else wide2_batch<LW_REGEX, OP, MODE == W2_GUARD>(P, W, st, gen, live, ords);
@@ -151,7 +180,7 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
     // the table grouped by the scalar row's side: its entries name the bit of the lanes' rows and the result bit
     const uint32_t *g_off = VEC_B ? G.left_off : G.right_off, *g_ent = VEC_B ? G.left_ent : G.right_ent;
     const int sc_words = (P.n_bits + 31) >> 5;
-    uint32_t *vw = reinterpret_cast<uint32_t *>(W.vec) + lane, *ow = W.out + lane;
+    uint32_t *ow = W.out + lane;
     __syncwarp();
     for (int t = lane; t < s_cnt * nvec; t += 32) {
         const int rrow = t / nvec, p = t - rrow * nvec;
@@ -162,18 +191,19 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
         const u64 vbase = v0 + (u64)vg * 32;
         if (vbase >= n_vec) break;
         __syncwarp();
+        // the 32 vector rows: staged [word][row] in the row area, bit-sliced from there (the row area then takes the results)
         const int rows_here = (int)min((u64)32, n_vec - vbase);
         for (int t = lane; t < 32 * nvec; t += 32) {  // (rows past the end of the level: zero)
             const int rrow = t / nvec, p = t - rrow * nvec;
             const uint4 x = rrow < rows_here ? __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p) : make_uint4(0, 0, 0, 0);
-            uint32_t *col = reinterpret_cast<uint32_t *>(W.vec) + rrow;
+            uint32_t *col = W.out + rrow;
             col[(p * 4) * 32] = x.x;
             col[(p * 4 + 1) * 32] = x.y;
             col[(p * 4 + 2) * 32] = x.z;
             col[(p * 4 + 3) * 32] = x.w;
         }
         __syncwarp();
-        regex_slice(reinterpret_cast<const uint32_t *>(W.vec), W.sliced, sc_words);
+        regex_slice(W.out, W.sliced, n_words);
         const u64 v = vbase + lane;
         const bool v_ok = v < n_vec;
 #pragma unroll 1
@@ -182,34 +212,64 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
             __syncwarp();
             for (int q = 0; q < n_words; ++q) W.out[q * 32 + lane] = 0u;
             __syncwarp();
-#pragma unroll 1
-            for (int q = 0; q < sc_words; ++q) {
-                uint32_t word = sw[q];  // the same for every lane
-                while (word) {
-                    const uint32_t s = (uint32_t)q * 32u + (uint32_t)(__ffs(word) - 1);
-                    word &= word - 1u;
-                    const uint32_t e_hi = g_off[s + 1];
-                    for (uint32_t e = g_off[s] + lane; e < e_hi; e += 32) {
-                        const uint32_t ent = g_ent[e];
-                        W.out[ent >> 16] |= W.sliced[ent & 0xFFFFu];
-                    }
-                    __syncwarp();
+            // (the offsets and the first 32 entries of the NEXT infix's group are fetched while this one is applied)
+            int q = 0;
+            uint32_t word = 0;
+            auto next_infix = [&]() -> uint32_t {  // the same for every lane; ~0u = the row is done
+                while (word == 0u) {
+                    if (q >= sc_words) return ~0u;
+                    word = sw[q++];
                 }
+                const uint32_t s = (uint32_t)(q - 1) * 32u + (uint32_t)(__ffs(word) - 1);
+                word &= word - 1u;
+                return s;
+            };
+            uint32_t s = next_infix();
+            uint32_t lo = 0, hi = 0, ent0 = 0;
+            if (s != ~0u) {
+                lo = g_off[s];
+                hi = g_off[s + 1];
+                ent0 = lo + lane < hi ? g_ent[lo + lane] : 0u;
             }
+            while (s != ~0u) {
+                const uint32_t s_next = next_infix();
+                uint32_t lo_n = 0, hi_n = 0, ent_n = 0;
+                if (s_next != ~0u) {
+                    lo_n = g_off[s_next];
+                    hi_n = g_off[s_next + 1];
+                    ent_n = lo_n + lane < hi_n ? g_ent[lo_n + lane] : 0u;
+                }
+                if (lo + lane < hi) W.out[ent0 >> 16] |= W.sliced[ent0 & 0xFFFFu];
+                for (uint32_t e = lo + 32 + lane; e < hi; e += 32) {
+                    const uint32_t ent = g_ent[e];
+                    W.out[ent >> 16] |= W.sliced[ent & 0xFFFFu];
+                }
+                __syncwarp();
+                s = s_next;
+                lo = lo_n;
+                hi = hi_n;
+                ent0 = ent_n;
+            }
+            // a candidate that equals one of its operands is in the cache already: decided here, on the sliced rows
+            uint32_t differs_vec = 0, differs_sc = 0;
+            for (int x = lane; x < P.n_bits; x += 32) {
+                const uint32_t o = W.out[x];
+                differs_vec |= o ^ W.sliced[x];
+                differs_sc |= o ^ (((sw[x >> 5] >> (x & 31)) & 1u) ? 0xFFFFFFFFu : 0u);
+            }
+            const uint32_t differs = __reduce_or_sync(0xFFFFFFFFu, differs_vec) & __reduce_or_sync(0xFFFFFFFFu, differs_sc);
+            const bool same = ((differs >> lane) & 1u) == 0u;
+            __syncwarp();
             regex_slice(W.out, W.out, sc_words);  // one row per lane, in place (the words past the last infix stay zero)
             __syncwarp();
             const bool live[1] = {v_ok};
             const u64 ords[1] = {ord0 + (VEC_B ? (s0 + k) * nb + v : v * nb + (s0 + k))};
             auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
-                const uint4 xv = make_uint4(vw[(p * 4) * 32], vw[(p * 4 + 1) * 32], vw[(p * 4 + 2) * 32], vw[(p * 4 + 3) * 32]);
-                const uint4 xs = W.sc[k * nvec + p];
-                a = VEC_B ? xs : xv;
-                b = VEC_B ? xv : xs;
                 c = make_uint4(ow[(p * 4) * 32], ow[(p * 4 + 1) * 32], ow[(p * 4 + 2) * 32], ow[(p * 4 + 3) * 32]);
+                a = b = regex_operand_stub(c, same);
             };
             if constexpr (MODE == W2_ROUTE) wide2_route_batch<LW_REGEX, OP_RE_CONCAT>(P, W, gen, live, ords);
             else wide2_batch<LW_REGEX, OP_RE_CONCAT, MODE == W2_GUARD>(P, W, st, gen, live, ords);
         }
     }
 }
-
