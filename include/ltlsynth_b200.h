@@ -122,16 +122,16 @@ int ltlb200_set_weights(ltlb200_engine *e, const int32_t *weights);
  *
  * The same engine enumerates regular expressions when its rows are characteristic sequences (CS: one bit per infix
  * of the example strings, infixes sorted by (length, text), bit 0 = the empty word).  Create the handle with the CS
- * bitsets as byte rows -- ltlb200_create(trace_count = ceil(n_bits / 8), lane_bits = 8, masks = the bits of all
+ * bitsets as byte rows -- ltlb200_create(trace_count = max(17, ceil(n_bits / 8)), lane_bits = 8, masks = the bits of all
  * example strings, target = the bits of the positive ones, atoms = the CSs of the empty word and of the letters) --
  * then, before the first level, hand over the infix-split guide table: the splits w = u v of infix w are entries
  * offsets[w] .. offsets[w + 1] - 1, each (index of u) | (index of v) << 16.  Levels are then built with
  *   op_mask bits  LTLB200_OP_RE_QUESTION  r?      LTLB200_OP_RE_STAR  r*
  *                 LTLB200_OP_RE_CONCAT    r s     LTLB200_OP_OR       r | s  (union)
  * and the five cost parameters (literal, ?, *, concatenation, union) are ltlb200_set_weights on the tags
- * 0, 8, 9, 10, 6.  CSs of up to 128 bits take the narrow kernels, up to 4096 bits the wide ones (infixes must be
- * sorted by length: the right part of a split comes before the whole).  A sharded search (ltlb200_route_begin ...)
- * works for both.
+ * 0, 8, 9, 10, 6.  CSs of up to 4096 bits; the rows must be wider than 16 bytes (the regex operators exist in the
+ * multi-vector kernels only: pad short sequences with zero lanes) and the infixes sorted by length (the right part of
+ * a split comes before the whole).  A sharded search (ltlb200_route_begin ...) works as for LTL.
  */
 enum { LTLB200_OP_RE_QUESTION = 8, LTLB200_OP_RE_STAR = 9, LTLB200_OP_RE_CONCAT = 10 };
 int ltlb200_set_regex(ltlb200_engine *e, int32_t n_bits, const uint32_t *offsets, const uint32_t *entries, uint64_t n_entries);

@@ -34,8 +34,7 @@ def _units() -> list[tuple[str, str, list[str]]]:
     for lw in LANE_WIDTHS:
         units.append((f"narrow_lw{lw}", "inst.cu", [f"-DLTLB200_INST_LW={lw}", "-DLTLB200_INST_WIDE=0"]))
         units.append((f"wide_lw{lw}", "inst.cu", [f"-DLTLB200_INST_LW={lw}", "-DLTLB200_INST_WIDE=1"]))
-    units.append(("narrow_regex", "inst.cu", ["-DLTLB200_INST_LW=1", "-DLTLB200_INST_WIDE=0"]))  # regex front-end (regex_ops.cuh)
-    units.append(("wide_regex", "inst.cu", ["-DLTLB200_INST_LW=1", "-DLTLB200_INST_WIDE=1"]))
+    units.append(("wide_regex", "inst.cu", ["-DLTLB200_INST_LW=1", "-DLTLB200_INST_WIDE=1"]))  # regex grammar (wide2_regex.cuh)
     return units
 
 

@@ -1098,7 +1098,6 @@ void Engine::fan_end() {
 
 void Engine::launch_narrow(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st) {
     switch (lw_) {
-        case LW_REGEX: narrow_launch_1(kind, op, P, grid, st); break;
         case 8: narrow_launch_8(kind, op, P, grid, st); break;
         case 16: narrow_launch_16(kind, op, P, grid, st); break;
         case 32: narrow_launch_32(kind, op, P, grid, st); break;
@@ -1391,8 +1390,6 @@ NarrowParams Engine::narrow_params(bool exhaustive) const {
     P.dead = dead_n_ ? dead_.ptr : nullptr;
     P.dead_n = (uint32_t)dead_n_;
     P.scan_only = 0;
-    P.guide = guide_.ptr;
-    P.n_bits = n_bits_;
     return P;
 }
 
@@ -1861,7 +1858,6 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     for (int k = 0; k < 16; ++k) T.weights[k] = weights_[k];
     CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
     switch (lw_) {
-        case LW_REGEX: narrow_tiny_1(T, device_, stream_); break;
         case 8: narrow_tiny_8(T, device_, stream_); break;
         case 16: narrow_tiny_16(T, device_, stream_); break;
         case 32: narrow_tiny_32(T, device_, stream_); break;
@@ -2171,7 +2167,6 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
                 const u64 steps = (n_records + 32 * PROBE_BATCH - 1) / (32 * PROBE_BATCH);
                 const int grid = (int)std::max<u64>(1, std::min<u64>((steps + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * occupancy_));
                 switch (lw_) {
-                    case LW_REGEX: narrow_probe_1(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 8: narrow_probe_8(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 16: narrow_probe_16(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 32: narrow_probe_32(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
@@ -2351,9 +2346,12 @@ int Engine::level_copy(int cost, int64_t first, int64_t count, uint8_t *cms, uin
 // and of the letters); this switches its kernels to the regex operators and uploads the infix-split guide table.
 void Engine::set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entries, u64 n_entries) {
     if (!levels_.empty()) throw std::invalid_argument("the grammar must be set before the first level");
-    // (wide2_regex.cuh keeps three row areas of 32 rows per warp in shared memory: 32 vectors = 4096 bits, 214 KB per CTA)
-    if (n_bits < 1 || n_bits > 4096 || lw_ != 8 || (n_bits + 7) / 8 != row_bytes_)
-        throw std::invalid_argument("regex front-end: characteristic sequences of up to 4096 bits, created as ceil(bits / 8) "
+    // The regex operators live in the multi-vector kernels only (wide2_regex.cuh: two row areas of 32 rows per warp in
+    // shared memory, 32 vectors = 4096 bits), so the rows must be wider than one uint4: short sequences are created
+    // with zero lanes up to 17 bytes.  (A one-vector instantiation that walked the table per candidate existed; the
+    // bit-sliced tiles are faster at every width: 111-bit sequences to cost 10, 3.8 -> 1.1 ms.)
+    if (n_bits < 1 || n_bits > 4096 || lw_ != 8 || (n_bits + 7) / 8 > row_bytes_ || !wide_)
+        throw std::invalid_argument("regex front-end: characteristic sequences of up to 4096 bits, created as max(17, ceil(bits / 8)) "
                                     "lanes of 8 bits");
     CUDA_CHECK(cudaSetDevice(device_));
     // device layout (wide2_regex.cuh: RegexGuide): the table as given (offsets | entries u | v << 16, sorted by the
@@ -2410,9 +2408,8 @@ void Engine::set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entr
     st_.h2d_bytes += h.size() * sizeof(uint32_t);
     n_bits_ = n_bits;
     lw_ = LW_REGEX;
-    special_possible_ = n_bits == 128;  // only a 128-bit CS can be all ones (the empty-slot marker of the narrow set)
-    prune_ok_ = false;                  // (the associativity pruning is an argument about LTL's AND)
-    if (wide_) {
+    prune_ok_ = false;  // (the associativity pruning is an argument about LTL's AND)
+    {
         // LTLB200_GUIDE_SMEM=1: stage the tables in shared memory behind the warps' areas.  Off by default: measured on
         // the e-mail example (57 KB of tables) the staged copy costs two of the four resident CTAs per SM and the
         // search to cost 12 gets slower, while the tables read through L1 hit at 95 %
@@ -2422,8 +2419,6 @@ void Engine::set_regex(int n_bits, const uint32_t *offsets, const uint32_t *entr
         guide_smem_words_ = want && warps + table <= kMaxDynamicSmem ? (uint32_t)h.size() : 0u;
         if (warps > kMaxDynamicSmem) throw std::invalid_argument("regex front-end: sequences too wide for the shared-memory areas of the wide kernels");
         occupancy_ = wide2_occupancy_1(nvec_, device_, (int)guide_smem_words_);
-    } else {
-        occupancy_ = narrow_occupancy_1();
     }
 }
 

@@ -1,6 +1,6 @@
 // inst.cu -- instantiates the enumeration kernels of ONE lane width (see launch.h).
 //
-//   nvcc -DLTLB200_INST_LW=8|16|32|64 -DLTLB200_INST_WIDE=0|1 -c inst.cu
+//   nvcc -DLTLB200_INST_LW=8|16|32|64 -DLTLB200_INST_WIDE=0|1 -c inst.cu     (LW=1, WIDE=1: the regex grammar)
 //
 // INST_WIDE=0: narrow.cuh (CMs of one uint4), INST_WIDE=1: wide2.cuh (multi-vector CMs).
 #include <mutex>
@@ -34,25 +34,15 @@ static void launch_one(const NarrowParams &P, int grid, cudaStream_t st) {
 
 template <bool ROUTE>
 static void launch_by_operator(int op, const NarrowParams &P, int grid, cudaStream_t st) {
-    if constexpr (LW == LW_REGEX) {  // the regex front-end's operators (regex_ops.cuh)
-        switch (op) {
-            case OP_ATOM: launch_one<ROUTE, OP_ATOM>(P, grid, st); break;
-            case OP_RE_QUESTION: launch_one<ROUTE, OP_RE_QUESTION>(P, grid, st); break;
-            case OP_RE_STAR: launch_one<ROUTE, OP_RE_STAR>(P, grid, st); break;
-            case OP_RE_CONCAT: launch_one<ROUTE, OP_RE_CONCAT>(P, grid, st); break;
-            default: launch_one<ROUTE, OP_OR>(P, grid, st); break;
-        }
-    } else {
-        switch (op) {
-            case OP_ATOM: launch_one<ROUTE, OP_ATOM>(P, grid, st); break;
-            case OP_NOT: launch_one<ROUTE, OP_NOT>(P, grid, st); break;
-            case OP_NEXT: launch_one<ROUTE, OP_NEXT>(P, grid, st); break;
-            case OP_FUTURE: launch_one<ROUTE, OP_FUTURE>(P, grid, st); break;
-            case OP_GLOBALLY: launch_one<ROUTE, OP_GLOBALLY>(P, grid, st); break;
-            case OP_AND: launch_one<ROUTE, OP_AND>(P, grid, st); break;
-            case OP_UNTIL: launch_one<ROUTE, OP_UNTIL>(P, grid, st); break;
-            default: launch_one<ROUTE, OP_OR>(P, grid, st); break;
-        }
+    switch (op) {
+        case OP_ATOM: launch_one<ROUTE, OP_ATOM>(P, grid, st); break;
+        case OP_NOT: launch_one<ROUTE, OP_NOT>(P, grid, st); break;
+        case OP_NEXT: launch_one<ROUTE, OP_NEXT>(P, grid, st); break;
+        case OP_FUTURE: launch_one<ROUTE, OP_FUTURE>(P, grid, st); break;
+        case OP_GLOBALLY: launch_one<ROUTE, OP_GLOBALLY>(P, grid, st); break;
+        case OP_AND: launch_one<ROUTE, OP_AND>(P, grid, st); break;
+        case OP_UNTIL: launch_one<ROUTE, OP_UNTIL>(P, grid, st); break;
+        default: launch_one<ROUTE, OP_OR>(P, grid, st); break;
     }
 }
 
@@ -84,8 +74,7 @@ void LTLB200_CAT(narrow_tiny_, LTLB200_INST_LW)(const TinyParams &T, int device,
 
 int LTLB200_CAT(narrow_occupancy_, LTLB200_INST_LW)() {
     int occ = 0;
-    constexpr int kHeaviest = LW == LW_REGEX ? (int)OP_RE_CONCAT : (int)OP_UNTIL;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, kHeaviest>, CTA_THREADS, 0) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, narrow_level_kernel<LW, OP_UNTIL>, CTA_THREADS, 0) != cudaSuccess) {
         cudaGetLastError();
         occ = 1;
     }

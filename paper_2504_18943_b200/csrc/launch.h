@@ -21,20 +21,23 @@ struct TinyParams;
 enum : int { LK_OPERATOR = 0, LK_SMALL = 1, LK_GUARDED = 2, LK_ROUTE = 3 };
 constexpr size_t kMaxDynamicSmem = 227 * 1024;  // per CTA on sm_100
 
+#define LTLB200_DECLARE_WIDE(LW)                                                                                   \
+    void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \
+    int wide2_occupancy_##LW(int nvec, int device, int guide_smem_words);
 #define LTLB200_DECLARE_LW(LW)                                                                                     \
     void narrow_launch_##LW(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st);                    \
     int narrow_occupancy_##LW();                                                                                    \
     void narrow_tiny_##LW(const TinyParams &T, int device, cudaStream_t st); /* several tiny levels in one launch */ \
     void narrow_probe_##LW(const NarrowParams &P, const void *rows, const void *ords, unsigned long long n, int grid, \
                            cudaStream_t st);                                                                         \
-    void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \
-    int wide2_occupancy_##LW(int nvec, int device, int guide_smem_words);
+    LTLB200_DECLARE_WIDE(LW)
 
-LTLB200_DECLARE_LW(1)  // the regex front-end's bitset CS (regex_ops.cuh)
+LTLB200_DECLARE_WIDE(1)  // the regex grammar's bitset CS (wide2_regex.cuh): the multi-vector kernels only
 LTLB200_DECLARE_LW(8)
 LTLB200_DECLARE_LW(16)
 LTLB200_DECLARE_LW(32)
 LTLB200_DECLARE_LW(64)
+#undef LTLB200_DECLARE_WIDE
 #undef LTLB200_DECLARE_LW
 
 }  // namespace ltlb200

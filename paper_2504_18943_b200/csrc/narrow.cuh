@@ -115,9 +115,6 @@ struct NarrowParams {
     int scan_only;  // the pass that finds those chunks: only record the ordinal of every separating candidate
     // One search sharded over several GPUs (narrow_route_kernel): candidates are not probed here but appended as
     // records {CM, ordinal} to the region of their hash owner, route_world regions of route_cap records each.
-    // regex front-end (regex_ops.cuh; LW == LW_REGEX instantiation only): the infix-split guide table
-    const uint32_t *guide;
-    int n_bits;
     uint4 *route_rows;
     u64 *route_ords;
     u64 route_cap;
@@ -454,11 +451,10 @@ static __device__ __noinline__ bool ordinal_is_dead(const u64 *dead, uint32_t n,
     return a > 0 && ord < dead[2 * (a - 1) + 1];
 }
 
-// one connective on one-vector CMs: the LTL connectives of cm_ops.cuh, or -- LW == LW_REGEX -- the regex operators
+// one connective on one-vector CMs (cm_ops.cuh)
 template <int LW, int OP>
 __device__ __forceinline__ uint4 apply_op(const NarrowParams &P, uint4 a, uint4 b) {
-    if constexpr (LW == LW_REGEX) return re_apply<OP>(P.guide, P.n_bits, a, b);
-    else return cm_apply<LW, OP>(a, b, P.valid);
+    return cm_apply<LW, OP>(a, b, P.valid);
 }
 
 // The tile runners are generic over where candidates go: `sink.emit<LW>(cand, live, known, ord_of)`
@@ -707,7 +703,7 @@ __device__ __forceinline__ bool run_tile(const NarrowParams &P, WS &ws, Sink &si
     const u64 sep_now = ws.sep_now;
     if (ws.block.ord0 > sep_now) return true;  // the whole block, and every later one, is ordered after the separator
     const u64 tile_local = ws.ticket - ws.block.tile0;
-    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL || OP == OP_RE_CONCAT) {
+    if constexpr (OP == OP_AND || OP == OP_OR || OP == OP_UNTIL) {
         // which operand sits in the lanes changes only how the ordinal is formed, not the result
         if (ws.block.vec_is_b) return run_binary_tile<LW, OP, true>(P, ws, sink, tile_local, sep_now);
         return run_binary_tile<LW, OP, false>(P, ws, sink, tile_local, sep_now);
@@ -716,28 +712,18 @@ __device__ __forceinline__ bool run_tile(const NarrowParams &P, WS &ws, Sink &si
     }
 }
 
-// run-time operator dispatch of the one-launch kernels: the LTL connectives, or (LW_REGEX) the regex operators
+// run-time operator dispatch of the one-launch kernels
 template <int LW, class WS, class Sink>
 __device__ __forceinline__ bool run_tile_any(const NarrowParams &P, WS &ws, Sink &sink) {
-    if constexpr (LW == LW_REGEX) {
-        switch (ws.block.op) {
-            case OP_ATOM: return run_tile<LW, OP_ATOM>(P, ws, sink);
-            case OP_RE_QUESTION: return run_tile<LW, OP_RE_QUESTION>(P, ws, sink);
-            case OP_RE_STAR: return run_tile<LW, OP_RE_STAR>(P, ws, sink);
-            case OP_RE_CONCAT: return run_tile<LW, OP_RE_CONCAT>(P, ws, sink);
-            default: return run_tile<LW, OP_OR>(P, ws, sink);
-        }
-    } else {
-        switch (ws.block.op) {
-            case OP_ATOM: return run_tile<LW, OP_ATOM>(P, ws, sink);
-            case OP_NOT: return run_tile<LW, OP_NOT>(P, ws, sink);
-            case OP_NEXT: return run_tile<LW, OP_NEXT>(P, ws, sink);
-            case OP_FUTURE: return run_tile<LW, OP_FUTURE>(P, ws, sink);
-            case OP_GLOBALLY: return run_tile<LW, OP_GLOBALLY>(P, ws, sink);
-            case OP_AND: return run_tile<LW, OP_AND>(P, ws, sink);
-            case OP_UNTIL: return run_tile<LW, OP_UNTIL>(P, ws, sink);
-            default: return run_tile<LW, OP_OR>(P, ws, sink);
-        }
+    switch (ws.block.op) {
+        case OP_ATOM: return run_tile<LW, OP_ATOM>(P, ws, sink);
+        case OP_NOT: return run_tile<LW, OP_NOT>(P, ws, sink);
+        case OP_NEXT: return run_tile<LW, OP_NEXT>(P, ws, sink);
+        case OP_FUTURE: return run_tile<LW, OP_FUTURE>(P, ws, sink);
+        case OP_GLOBALLY: return run_tile<LW, OP_GLOBALLY>(P, ws, sink);
+        case OP_AND: return run_tile<LW, OP_AND>(P, ws, sink);
+        case OP_UNTIL: return run_tile<LW, OP_UNTIL>(P, ws, sink);
+        default: return run_tile<LW, OP_OR>(P, ws, sink);
     }
 }
 

@@ -120,9 +120,9 @@ __device__ inline void tiny_plan(const TinyParams &T, BlockDesc *blocks, int cos
         b.size = b.na;
         tiny_push(blocks, n_blocks, constructed, n_tiles, b);
     }
-    const int unary_tags[6] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY, OP_RE_QUESTION, OP_RE_STAR};
-    const int binary_tags[4] = {OP_AND, OP_UNTIL, OP_RE_CONCAT, OP_OR};
-    for (int k = 0; k < 6; ++k) {
+    const int unary_tags[4] = {OP_NOT, OP_NEXT, OP_FUTURE, OP_GLOBALLY};
+    const int binary_tags[3] = {OP_AND, OP_UNTIL, OP_OR};
+    for (int k = 0; k < 4; ++k) {
         const int tag = unary_tags[k];
         if (!(T.op_mask >> tag & 1u) || cost - w[tag] < 1) continue;
         const int src = cost - w[tag];
@@ -136,7 +136,7 @@ __device__ inline void tiny_plan(const TinyParams &T, BlockDesc *blocks, int cos
         tiny_push(blocks, n_blocks, constructed, n_tiles, b);
         if (constructed == ~0ull) return;
     }
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 3; ++k) {
         const int tag = binary_tags[k];
         if (!(T.op_mask >> tag & 1u)) continue;
         const bool commutative = tag == OP_AND || tag == OP_OR;

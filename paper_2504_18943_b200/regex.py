@@ -18,11 +18,10 @@ The idea is the paper's "enumerate semantics, not syntax" applied to regular exp
   (``csrc/engine.cu: plan_level`` with the regex operator tags); the **cost function has five parameters** --
   literal, ``?``, ``*``, concatenation, union -- which are the engine's per-operator weights.
 
-CSs of up to 128 bits (``InfixIndex.n_bits <= 128``: BASELINE configs[0]-sized example sets) run through the narrow
-kernels (one ``uint4`` per CS, ``csrc/regex_ops.cuh``), CSs of up to 4096 bits (the e-mail example has 528 infixes)
-through the wide kernels (``csrc/wide2.cuh``: row log, 8-byte slot words, the concatenation testing single bits of its
-operands in shared memory); wider example sets are handled by the host model and the CPU oracle only and raise
-``NativeEngineError`` on the GPU path.
+CSs of up to 4096 bits (BASELINE configs[0]-sized example sets have a few dozen infixes, the e-mail example 528)
+run through the multi-vector kernels (``csrc/wide2.cuh`` with the tiles of ``csrc/wide2_regex.cuh``: row log, 8-byte
+slot words, concatenation and star on bit-sliced rows, 32 candidates per word operation); wider example sets are
+handled by the host model and the CPU oracle only and raise ``NativeEngineError`` on the GPU path.
 """
 
 from __future__ import annotations
@@ -41,6 +40,7 @@ from .traces import InfeasibleSpecificationError
 OP_LITERAL, OP_UNION, OP_QUESTION, OP_STAR, OP_CONCAT = 0, 6, 8, 9, 10  # operator tags of include/ltlsynth_b200.h
 _OP_MASK = (1 << OP_UNION) | (1 << OP_QUESTION) | (1 << OP_STAR) | (1 << OP_CONCAT)
 MAX_GPU_BITS = 4096  # csrc/engine.cu: Engine::set_regex
+MIN_ROW_BYTES = 17
 
 
 # ---- expressions ------------------------------------------------------------------------------------------------
@@ -177,7 +177,8 @@ class InfixIndex:
         self.infixes = infix_closure(spec.positives + spec.negatives)
         self.index = {w: k for k, w in enumerate(self.infixes)}
         self.n_bits = len(self.infixes)
-        self.n_bytes = -(-self.n_bits // 8)
+        # (rows wider than one uint4 select the engine's multi-vector kernels, where the regex operators live)
+        self.n_bytes = max(MIN_ROW_BYTES, -(-self.n_bits // 8))
         # guide table: splits of infix w are entries offsets[w] .. offsets[w+1]-1, each (u, v) with w = u v
         self.offsets, self.splits = [0], []
         for w in self.infixes:

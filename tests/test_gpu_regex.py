@@ -63,7 +63,7 @@ def test_three_letter_alphabet_and_wider_sequences():
     words = ['aacca', 'acacbcab', 'bbccba', 'bcaaaaac', 'bcaabbca', 'bcacbbac', 'cbcbba', 'ccaaca']
     spec = rx.RegexSpecification(tuple(words[:4]), tuple(words[4:]))
     ix = rx.InfixIndex(spec)
-    assert ix.n_bits == 111  # all four words of the uint4 in use
+    assert ix.n_bits == 111
     store, ref = rx.RegexStore(spec), ro.RegexOracle(spec)
     try:
         for c in range(1, 6):
@@ -87,7 +87,7 @@ def _wide_words(seed, n_words=8, length=(9, 13), letters="abc"):
     (0, rx.CostFunction(), 5), (1, rx.CostFunction(literal=1, question=2, star=1, concat=1, union=2), 6),
 ])
 def test_sequences_wider_than_128_bits_equal_the_oracle(seed, cost, max_cost):
-    """CSs of several uint4 vectors: the wide kernels (row log, word-wise concatenation and star)."""
+    """CSs of three vectors."""
     words = _wide_words(seed)
     spec = rx.RegexSpecification(tuple(words[:4]), tuple(words[4:]))
     store, ref = rx.RegexStore(spec, cost), ro.RegexOracle(spec, cost)
@@ -184,8 +184,7 @@ def test_baseline_shaped_example_sets_equal_the_oracle(name, max_cost, bits):
 @pytest.mark.parametrize("name,seed,max_cost,world", [("re-c0", 0, 8, 2), ("re-c0", 3, 7, 3), ("re-c2", 0, 11, 2), ("re-email", 0, 6, 3)])
 def test_sharded_search_of_regex_stores(name, seed, max_cost, world):
     """One regex search over several ranks (stores on one GPU play them, the exchange done by hand as in
-    tests/test_gpu_sharded.py): candidates routed to their hash owners -- one-vector sequences through the narrow route
-    kernel, wider ones through the bit-sliced tiles in route mode -- and every rank ends every level equal to the oracle."""
+    tests/test_gpu_sharded.py): candidates routed to their hash owners by the bit-sliced tiles in route mode, and every rank ends every level equal to the oracle."""
     from paper_2504_18943_b200 import engine
     from paper_2504_18943_b200.workloads import regex_workload
     from test_gpu_sharded import _exchange_level
