@@ -254,6 +254,24 @@ def test_regex_command_line(tmp_path, capsys):
     assert "error:" in capsys.readouterr().err
 
 
+@pytest.mark.parametrize("seed", [207, 210])
+def test_cut_levels_on_top_of_a_store_that_holds_a_solution(seed):
+    """Exhaustive levels up to and including the first solution, then non-exhaustive ones: the guarded kernel with the
+    regex tiles (the LTL engine's chunk truncation at batch size 1)."""
+    spec = random_binary_spec(random.Random(seed))
+    first = ro.synthesize(spec, max_cost=10).cost
+    assert first == 8
+    store, ref = rx.RegexStore(spec), ro.RegexOracle(spec)
+    try:
+        for c in range(1, first + 3):
+            exhaustive = c <= first
+            status, n_new, sep, constructed = store.expand(c, exhaustive=exhaustive)
+            assert (status, n_new, sep, constructed) == (0,) + tuple(ref.expand_level(c, exhaustive=exhaustive)), f"seed {seed} cost {c}"
+            _assert_level_equal(store, ref, c, f"seed {seed} cost {c}")
+    finally:
+        store.close()
+
+
 def test_sequences_beyond_4096_bits_are_refused():
     words = _wide_words(7, n_words=12, length=(28, 30), letters="abcdefgh")
     with pytest.raises(_native.NativeEngineError, match="4096 bits"):
