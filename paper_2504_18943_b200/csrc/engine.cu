@@ -1614,7 +1614,7 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
     try {
         const u64 n_bits = constructed;
         const u64 n_words = (n_bits + 31) / 32, n_sb = (n_words + 31) / 32;
-        const bool small = !wide_ && n_bits <= SMALL_FIN_MAX_BITS;  // bitmap in shared memory, one launch
+        const bool small = n_bits <= SMALL_FIN_MAX_BITS;  // bitmap in shared memory, one launch
         if (!small || exhaustive) {
             reserve(bitmap_, n_sb * 32 + 1, false);
             reserve(sb_rank_, n_sb + 1, false);
@@ -1638,14 +1638,21 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
             W.live = d_counters_;
             W.stage_cap = pl.claim_cap;
             W.cut_allowed = exhaustive ? 0 : 1;
-            CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
-            wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
-            CUDA_CHECK(cudaGetLastError());
-            launch_rank_scan(n_words, n_sb);
-            level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
-            wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
-            CUDA_CHECK(cudaGetLastError());
-            st_.kernel_launches += 3;
+            if (small) {
+                const size_t smem = (size_t)n_sb * 32 * sizeof(uint32_t) + (size_t)n_sb * sizeof(uint32_t);
+                small_finalize_kernel<WideFinalize><<<1, SMALL_FIN_THREADS, smem, stream_>>>(W, n_bits, d_counters_, exhaustive ? 1 : 0);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches++;
+            } else {
+                CUDA_CHECK(cudaMemsetAsync(bitmap_.ptr, 0, (n_words + 1) * sizeof(uint32_t), stream_));
+                wide_mark_kernel<<<fgrid, 256, 0, stream_>>>(W);
+                CUDA_CHECK(cudaGetLastError());
+                launch_rank_scan(n_words, n_sb);
+                level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+                wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
+                CUDA_CHECK(cudaGetLastError());
+                st_.kernel_launches += 3;
+            }
         } else {
             FinalizeParams F{};
             F.claim_key = claim_key_.ptr;
@@ -1659,18 +1666,8 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
             F.claim_cap = pl.claim_cap;
             F.cut_allowed = exhaustive ? 0 : 1;
             if (small) {
-                {   // opt in to > 48 KB of dynamic shared memory: a per-device attribute of the kernel
-                    static std::mutex mu;
-                    static unsigned long long seen = 0;
-                    std::lock_guard<std::mutex> lock(mu);
-                    if (!(seen >> (device_ & 63) & 1ull)) {
-                        cudaFuncSetAttribute(narrow_small_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)((SMALL_FIN_MAX_BITS / 8) + 512 * sizeof(uint32_t) + 256));
-                        seen |= 1ull << (device_ & 63);
-                    }
-                }
                 const size_t smem = (size_t)n_sb * 32 * sizeof(uint32_t) + (size_t)n_sb * sizeof(uint32_t);
-                narrow_small_finalize_kernel<<<1, SMALL_FIN_THREADS, smem, stream_>>>(F, n_bits, d_counters_, exhaustive ? 1 : 0);
+                small_finalize_kernel<FinalizeParams><<<1, SMALL_FIN_THREADS, smem, stream_>>>(F, n_bits, d_counters_, exhaustive ? 1 : 0);
                 CUDA_CHECK(cudaGetLastError());
                 st_.kernel_launches++;
             } else {

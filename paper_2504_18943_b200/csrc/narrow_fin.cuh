@@ -61,30 +61,38 @@ __global__ void __launch_bounds__(256) narrow_scatter_kernel(const FinalizeParam
     }
 }
 
-// Small levels: the whole finalisation in ONE CTA.  The winners bitmap of a level of up to 2^19
-// candidates is 64 KiB and lives in shared memory, so mark -> superblock ranks -> summary ->
+// Small levels: the whole finalisation in ONE CTA.  The winners bitmap of a level of up to 2^15
+// candidates is 4 KiB and lives in shared memory, so mark -> superblock ranks -> summary ->
 // scatter need no global bitmap, no scan launches and no separate summary launch: such a level
-// is launch latency, and this is one launch instead of five.
+// is launch latency, and this is one launch instead of five.  One kernel for both key widths: what differs is where
+// the ordinals come from and what placing an entry means (fin_* overloads here and in wide_fin.cuh).
 constexpr int SMALL_FIN_THREADS = 1024;
 constexpr u64 SMALL_FIN_MAX_BITS = 1ull << 15;
 
-__global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kernel(const FinalizeParams F, u64 n_bits, u64 *counters,
-                                                                                  int export_bitmap) {
+__device__ __forceinline__ bool fin_bounds(const FinalizeParams &F, u64 &n, u64 &ord_limit) { return finalize_bounds(F, n, ord_limit); }
+__device__ __forceinline__ u64 fin_ord(const FinalizeParams &F, u64 t) { return F.claim_ord[t]; }
+__device__ __forceinline__ void fin_place(const FinalizeParams &F, u64 t, u64 gid, u64 ord) {
+    F.store[gid] = F.claim_key[t];
+    F.ords[gid] = ord;
+}
+
+template <class Fin>
+__global__ void __launch_bounds__(SMALL_FIN_THREADS) small_finalize_kernel(const Fin F, u64 n_bits, u64 *counters, int export_bitmap) {
     extern __shared__ uint32_t s_fin[];
-    const u64 n_words = (n_bits + 31) >> 5, n_sb = (n_words + 31) >> 5;  // <= 16384 words, <= 512 superblocks
+    const u64 n_words = (n_bits + 31) >> 5, n_sb = (n_words + 31) >> 5;  // <= 1024 words, <= 32 superblocks
     uint32_t *bitmap = s_fin, *sb_rank = s_fin + n_sb * 32;              // bitmap padded to whole superblocks
     __shared__ uint32_t warp_tot[32];
     u64 n_claimed, ord_limit;
-    if (!finalize_bounds(F, n_claimed, ord_limit)) return;  // uniform: the level overflowed and is redone
+    if (!fin_bounds(F, n_claimed, ord_limit)) return;  // uniform: the level overflowed and is redone
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (u64 w = tid; w < n_sb * 32; w += SMALL_FIN_THREADS) bitmap[w] = 0u;
     __syncthreads();
     for (u64 t = tid; t < n_claimed; t += SMALL_FIN_THREADS) {
-        const u64 ord = F.claim_ord[t];
+        const u64 ord = fin_ord(F, t);
         if (ord <= ord_limit) atomicOr(&bitmap[ord >> 5], 1u << (ord & 31));
     }
     __syncthreads();
-    // exclusive popcount prefix per superblock (n_sb <= 512 <= threads)
+    // exclusive popcount prefix per superblock (n_sb <= threads)
     uint32_t v = 0;
     if ((u64)tid < n_sb)
         for (int k = 0; k < 32; ++k) v += __popc(bitmap[tid * 32 + k]);
@@ -119,11 +127,9 @@ __global__ void __launch_bounds__(SMALL_FIN_THREADS) narrow_small_finalize_kerne
         counters[CTR_SEPRANK] = sep_ord < n_bits ? ordinal_rank(bitmap, sb_rank, sep_ord) : ~0ull;
     }
     for (u64 t = tid; t < n_claimed; t += SMALL_FIN_THREADS) {
-        const u64 ord = F.claim_ord[t];
+        const u64 ord = fin_ord(F, t);
         if (ord > ord_limit) continue;
-        const u64 gid = F.base + ordinal_rank(bitmap, sb_rank, ord);
-        F.store[gid] = F.claim_key[t];
-        F.ords[gid] = ord;
+        fin_place(F, t, F.base + ordinal_rank(bitmap, sb_rank, ord), ord);
     }
 }
 

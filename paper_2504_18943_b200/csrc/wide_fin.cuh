@@ -34,6 +34,14 @@ __device__ __forceinline__ bool wide_finalize_bounds(const WideFinalize &F, u64 
     return true;
 }
 
+// small levels: narrow_fin.cuh's one-CTA finalisation (small_finalize_kernel<WideFinalize>)
+__device__ __forceinline__ bool fin_bounds(const WideFinalize &F, u64 &n, u64 &ord_limit) { return wide_finalize_bounds(F, n, ord_limit); }
+__device__ __forceinline__ u64 fin_ord(const WideFinalize &F, u64 t) { return F.stage_ord[t]; }
+__device__ __forceinline__ void fin_place(const WideFinalize &F, u64 t, u64 gid, u64 ord) {
+    F.loc[gid] = F.log_base + t;
+    F.ords[gid] = ord;
+}
+
 __global__ void __launch_bounds__(256) wide_mark_kernel(const WideFinalize F) {
     u64 n_staged, ord_limit;
     if (!wide_finalize_bounds(F, n_staged, ord_limit)) return;
