@@ -276,3 +276,54 @@ def test_sequences_beyond_4096_bits_are_refused():
     words = _wide_words(7, n_words=12, length=(28, 30), letters="abcdefgh")
     with pytest.raises(_native.NativeEngineError, match="4096 bits"):
         rx.RegexStore(rx.RegexSpecification(tuple(words[:6]), tuple(words[6:])))
+
+
+def test_email_example_at_scale():
+    """The e-mail example to cost 10 (16.1 M candidates, 992 K stored sequences of 528 bits; levels 8-10 take the
+    per-operator launches and the estimate-and-redo path): pairwise distinct over the whole store, every sampled entry
+    is the operator of its provenance applied to its children (oracle operators on Python integers), the closed-form
+    candidate counts, and a second run gives the same arrays."""
+    spec = rx.RegexSpecification(EMAIL_P, EMAIL_N)
+    store = rx.RegexStore(spec)
+    ix = store.ix
+    try:
+        sizes, constructed = [], []
+        for c in range(1, 11):
+            status, n_new, sep, built = store.expand(c, exhaustive=True)
+            assert status == 0 and sep is None
+            sizes.append(n_new)
+            constructed.append(built)
+        n = lambda c: sizes[c - 1] if c >= 1 else 0
+        for c in range(2, 11):  # unit costs: ? and * over level c-1, concatenation over all splits of c-1, union over c1 <= c2
+            want = 2 * n(c - 1) + sum(n(a) * n(c - 1 - a) for a in range(1, c - 1))
+            want += sum(n(a) * n(c - 1 - a) if a < c - 1 - a else n(a) * (n(a) + 1) // 2 for a in range(1, c - 1) if a <= c - 1 - a)
+            assert constructed[c - 1] == want, f"cost {c}"
+        assert store.total == sum(sizes) == 992_008 and sum(constructed) == 16_139_866
+        rows = store.all_cms()
+        keys = {rows[k].tobytes() for k in range(len(rows))}
+        assert len(keys) == store.total
+        as_int = lambda k: int.from_bytes(rows[k].tobytes(), "little")
+        rng = random.Random(5)
+        lv10 = store.level(10)
+        for k in [rng.randrange(lv10.n) for _ in range(1500)] + list(range(40)) + list(range(lv10.n - 40, lv10.n)):
+            tag, left, right = int(lv10.op[k]), int(lv10.left[k]), int(lv10.right[k])
+            if tag == rx.OP_QUESTION:
+                want = ro.cs_question(ix, as_int(left))
+            elif tag == rx.OP_STAR:
+                want = ro.cs_star(ix, as_int(left))
+            elif tag == rx.OP_CONCAT:
+                want = ro.cs_concat(ix, as_int(left), as_int(right))
+            else:
+                want = ro.cs_union(ix, as_int(left), as_int(right))
+            assert as_int(lv10.base + k) == want, (k, tag, left, right)
+        again = rx.RegexStore(spec)
+        try:
+            for c in range(1, 11):
+                again.expand(c, exhaustive=True)
+            lv = again.level(10)
+            assert np.array_equal(lv.cms, lv10.cms) and np.array_equal(lv.op, lv10.op)
+            assert np.array_equal(lv.left, lv10.left) and np.array_equal(lv.right, lv10.right)
+        finally:
+            again.close()
+    finally:
+        store.close()
