@@ -48,3 +48,25 @@ def test_variant_matches_reference(switch, value, cases):
     code = CHILD.format(root=str(ROOT), tests=str(ROOT / "tests"), cases=cases)
     proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert proc.returncode == 0 and "variant ok" in proc.stdout, proc.stdout[-2000:] + proc.stderr[-4000:]
+
+
+REGEX_CHILD = """
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import test_gpu_regex as t
+t.test_sequences_wider_than_128_bits_equal_the_oracle(0, t.rx.CostFunction(), 5)
+t.test_baseline_shaped_example_sets_equal_the_oracle("re-c2", 10, 207)
+t.test_cut_levels_on_top_of_a_store_that_holds_a_solution(207)
+print("variant ok")
+"""
+
+
+@pytest.mark.parametrize("switch,value", [("LTLB200_GUIDE_SMEM", "1"), ("LTLB200_NO_DEFER", "1"), ("LTLB200_OPSTREAMS", "0")])
+def test_regex_variant_matches_the_oracle(switch, value):
+    """LTLB200_GUIDE_SMEM=1: the regex guide tables staged in the CTA's shared memory (off by default: it costs
+    occupancy); and the regex tiles under the two scheduling switches above."""
+    env = dict(os.environ)
+    env[switch] = value
+    code = REGEX_CHILD.format(root=str(ROOT), tests=str(ROOT / "tests"))
+    proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert proc.returncode == 0 and "variant ok" in proc.stdout, proc.stdout[-2000:] + proc.stderr[-4000:]
