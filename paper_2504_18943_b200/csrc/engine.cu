@@ -35,7 +35,7 @@
 #include "launch.h"
 #include "narrow_fin.cuh"
 #include "narrow_tiny.cuh"
-#include "wide2.cuh"
+#include "wide2_tiny.cuh"
 #include "wide_fin.cuh"
 
 namespace ltlb200 {
@@ -344,6 +344,7 @@ public:
     struct Lookahead {
         int cost;
         u64 n_new, sep_ord, sep_rank;
+        u64 n_staged;  // wide: log entries the level takes
     };
     std::deque<Lookahead> lookahead_;
     uint32_t la_mask_ = 0;
@@ -352,6 +353,7 @@ public:
     DeviceArray<u64> tiny_tab_, tiny_results_;
     bool tiny_eligible(int cost, uint32_t op_mask, bool exhaustive);
     void tiny_run(int cost, uint32_t op_mask, bool exhaustive);
+    void tiny_run_wide(int cost, uint32_t op_mask, bool exhaustive);
     int tiny_reveal(int cost, uint32_t op_mask, bool exhaustive, int64_t batch, u64 mem_budget, double deadline, int64_t *n_new,
                     int64_t *sep_gid, int64_t *constructed_delta);
     void discard_lookahead();
@@ -1796,20 +1798,31 @@ static bool tiny_enabled() {
     return on;
 }
 
+// multi-vector CMs: one CTA of eight warps beats the per-level launches only while a level is a few thousand candidates
+static u64 wide_tiny_max_candidates() {
+    static const u64 n = [] {
+        const char *e = getenv("LTLB200_WIDE_TINY_MAX");
+        return e ? (u64)atoll(e) : 4096ull;
+    }();
+    return std::min<u64>(n, TINY_MAX_CANDIDATES);
+}
+
 bool Engine::tiny_eligible(int cost, uint32_t op_mask, bool exhaustive) {
-    if (!tiny_enabled() || tiny_off_ || wide_ || pending_.active || cost != (int)levels_.size() + 1 || cost > 60) return false;
+    if (!tiny_enabled() || tiny_off_ || pending_.active || cost != (int)levels_.size() + 1 || cost > 60) return false;
     if (!exhaustive && store_has_separator_) return false;  // the chunk-truncation regime (collect_dead_ranges)
     LevelMeta lv;
     u64 constructed = 0, n_tiles = 0;
     plan_level(cost, op_mask, lv, constructed, n_tiles);
     const u64 slots = std::max<u64>(table_slots(), kMinSlots);
-    return constructed <= TINY_MAX_CANDIDATES && (int)lv.blocks.size() <= TINY_MAX_BLOCKS && 2 * (total_ + constructed) <= slots;
+    return constructed <= (wide_ ? wide_tiny_max_candidates() : (u64)TINY_MAX_CANDIDATES) && (int)lv.blocks.size() <= TINY_MAX_BLOCKS &&
+           2 * (total_ + constructed) <= slots;
 }
 
 // Builds level `cost` and as many following levels as stay tiny, in one launch; queues their sizes.
 void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     CUDA_CHECK(cudaSetDevice(device_));
     set_sharding(1, 0);
+    if (wide_) return tiny_run_wide(cost, op_mask, exhaustive);
     try {
         if (table_dirty_) rebuild_table(table_slots());
         const u64 claim_cap = (u64)TINY_MAX_CANDIDATES + (u64)TINY_WARPS * CLAIM_CHUNK + 1024;
@@ -1874,7 +1887,7 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     const int asked = T.cost_last - T.cost_first + 1;
     int built = 0;
     while (built < asked && res[5 * built] == TINY_BUILT) {
-        lookahead_.push_back(Lookahead{cost + built, res[5 * built + 1], res[5 * built + 2], res[5 * built + 3]});
+        lookahead_.push_back(Lookahead{cost + built, res[5 * built + 1], res[5 * built + 2], res[5 * built + 3], 0});
         DBG("tiny level %d: %llu new, %.1f us", cost + built, (unsigned long long)res[5 * built + 1], 1e-3 * (double)res[5 * built + 4]);
         ++built;
     }
@@ -1888,6 +1901,98 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     // and each of them would be built here only to be handed to the host: stop trying on this store
     if (why == TINY_END_SEPARATOR) tiny_off_ = true;
     DBG("tiny levels: asked %d from cost %d, built %d (end reason %llu)", asked, cost, built, (unsigned long long)why);
+}
+
+// The same for multi-vector CMs (wide2_tiny.cuh): the levels' rows are staged at the tail of the row log, which the
+// kernel moves on level by level; the host learns how far when it hands a level out.
+void Engine::tiny_run_wide(int cost, uint32_t op_mask, bool exhaustive) {
+    const bool regex = lw_ == LW_REGEX;
+    // as many warps as fit the CTA's shared memory beside the kernel's static part
+    const size_t per_warp = wide2_warp_vecs(nvec_, regex) * sizeof(uint4);
+    const int warps = (int)std::min<size_t>(W2_TINY_MAX_WARPS, (kMaxDynamicSmem - 16 * 1024) / per_warp);
+    if (warps < 2) return;
+    const u64 claim_cap = (u64)TINY_MAX_CANDIDATES + (u64)warps * CLAIM_CHUNK + 1024;
+    const u64 growth = 1ull << 17;  // log entries (and cache entries) one launch may add; the kernel stops before
+    try {
+        if (table_dirty_) rebuild_table(table_slots());
+        reserve(stage_ord_, claim_cap, false);
+        reserve(store_, (log_tail_ + growth) * nvec_, true, log_tail_ * nvec_);
+        reserve(loc_, total_ + growth, true, total_);
+        reserve(ords_, total_ + growth, true, total_);
+        reserve(tiny_tab_, 2 * 128, false);
+        reserve(tiny_results_, 6 * (TINY_MAX_LEVELS + 1), false);
+    } catch (const MemoryBudget &) {
+        return;  // (the usual path reports the memory budget)
+    }
+    std::vector<u64> tab(2 * 128, 0);
+    for (size_t c = 1; c <= levels_.size(); ++c) {
+        tab[2 * c] = levels_[c - 1].n;
+        tab[2 * c + 1] = levels_[c - 1].base;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(tiny_tab_.ptr, tab.data(), tab.size() * sizeof(u64), cudaMemcpyHostToDevice, stream_));
+    CUDA_CHECK(cudaMemsetAsync(tiny_results_.ptr, 0, 6 * (TINY_MAX_LEVELS + 1) * sizeof(u64), stream_));
+    CUDA_CHECK(cudaMemsetAsync(stage_ord_.ptr, 0xFF, claim_cap * sizeof(u64), stream_));
+    st_.h2d_bytes += tab.size() * sizeof(u64);
+    pending_ = PendingLevel{};
+    pending_.claim_cap = claim_cap;
+    pending_.cost = cost;
+    WideTinyParams T{};
+    T.P = wide_params(exhaustive);
+    T.P.stage_cap = claim_cap;
+    T.P.sep_list = exhaustive ? d_counters_ : nullptr;  // capacity 0: separating candidates are only counted
+    T.P.sep_list_cap = 0;
+    T.P.dead = nullptr;
+    T.P.dead_n = 0;
+    T.store = store_.ptr;
+    T.loc = loc_.ptr;
+    T.ords = ords_.ptr;
+    T.level_tab = tiny_tab_.ptr;
+    T.results = reinterpret_cast<WideTinyLevelResult *>(tiny_results_.ptr);
+    T.total = total_;
+    T.log_tail = log_tail_;
+    T.log_cap = log_tail_ + growth;
+    T.table_slots = table_slots();
+    T.max_candidates = wide_tiny_max_candidates();
+    T.op_mask = op_mask;
+    T.n_atoms = n_atoms_;
+    T.cost_first = cost;
+    T.cost_last = std::min(cost + TINY_MAX_LEVELS - 1, 62);
+    T.exhaustive = exhaustive ? 1 : 0;
+    for (int k = 0; k < 16; ++k) T.weights[k] = weights_[k];
+    const size_t smem = per_warp * (size_t)warps;
+    CUDA_CHECK(cudaEventRecord(ev_[0], stream_));
+    switch (lw_) {
+        case LW_REGEX: wide2_tiny_1(T, warps, smem, device_, stream_); break;
+        case 8: wide2_tiny_8(T, warps, smem, device_, stream_); break;
+        case 16: wide2_tiny_16(T, warps, smem, device_, stream_); break;
+        case 32: wide2_tiny_32(T, warps, smem, device_, stream_); break;
+        default: wide2_tiny_64(T, warps, smem, device_, stream_); break;
+    }
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaEventRecord(ev_[1], stream_));
+    std::vector<u64> res(6 * (TINY_MAX_LEVELS + 1));
+    CUDA_CHECK(cudaMemcpyAsync(res.data(), tiny_results_.ptr, res.size() * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
+    CUDA_CHECK(cudaStreamSynchronize(stream_));
+    st_.d2h_bytes += res.size() * sizeof(u64);
+    st_.kernel_launches++;
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+    st_.tiny_ms += ms;
+    recycle_retired(false);
+    const int asked = T.cost_last - T.cost_first + 1;
+    int built = 0;
+    while (built < asked && res[6 * built] == TINY_BUILT) {
+        lookahead_.push_back(Lookahead{cost + built, res[6 * built + 1], res[6 * built + 2], res[6 * built + 3], res[6 * built + 5]});
+        DBG("tiny level %d: %llu new, %llu staged, %.1f us", cost + built, (unsigned long long)res[6 * built + 1],
+            (unsigned long long)res[6 * built + 5], 1e-3 * (double)res[6 * built + 4]);
+        ++built;
+    }
+    la_mask_ = op_mask;
+    la_exhaustive_ = exhaustive;
+    const u64 why = res[6 * TINY_MAX_LEVELS];
+    if (built < asked && why != TINY_END_BIG) table_dirty_ = true;  // (see tiny_run)
+    if (why == TINY_END_SEPARATOR) tiny_off_ = true;
+    DBG("tiny levels (wide): asked %d from cost %d, built %d (end reason %llu)", asked, cost, built, (unsigned long long)why);
 }
 
 // Hands out the first queued level: the bookkeeping of level_end, with the block list replayed on the host.
@@ -1922,6 +2027,7 @@ int Engine::tiny_reveal(int cost, uint32_t op_mask, bool exhaustive, int64_t bat
     last_constructed_ = constructed;
     *n_new = (int64_t)lv.n;
     total_ += lv.n;
+    log_tail_ += la.n_staged;  // (wide: unused and cut-off staging entries stay behind as dead log entries)
     st_.constructed += (u64)*constructed_delta;
     st_.unique = total_;
     approx_bytes_ += lv.n * ((u64)row_bytes_ + (u64)key_words_ * 8 + 80);  // engine.py:442

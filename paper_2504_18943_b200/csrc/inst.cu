@@ -7,7 +7,7 @@
 
 #include "launch.h"
 #if LTLB200_INST_WIDE
-#include "wide2.cuh"
+#include "wide2_tiny.cuh"
 #else
 #include "narrow_tiny.cuh"
 #endif
@@ -171,6 +171,20 @@ void LTLB200_CAT(wide2_launch_, LTLB200_INST_LW)(int kind, int op, const WidePar
         }
     }
 #endif
+}
+
+void LTLB200_CAT(wide2_tiny_, LTLB200_INST_LW)(const WideTinyParams &T, int warps, size_t smem, int device, cudaStream_t st) {
+    static unsigned long long seen = 0;
+    static std::mutex mu;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        const unsigned long long bit = 1ull << (device & 63);
+        if (!(seen & bit)) {  // (less than the 227 KB of a CTA: the kernel has ~14 KB of static shared memory)
+            cudaFuncSetAttribute(wide2_tiny_levels_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kMaxDynamicSmem - 16 * 1024));
+            seen |= bit;
+        }
+    }
+    wide2_tiny_levels_kernel<LW><<<1, 32 * warps, smem, st>>>(T);
 }
 
 int LTLB200_CAT(wide2_occupancy_, LTLB200_INST_LW)(int nvec, int device, int guide_smem_words) {

@@ -14,6 +14,7 @@ namespace ltlb200 {
 struct NarrowParams;
 struct WideParams;
 struct TinyParams;
+struct WideTinyParams;
 
 // which kernel of a (lane width) set: one launch per operator (big levels), one launch for every
 // operator (levels up to kSmallLevel candidates), the guarded kernel (scan pass / dead ranges), and -- one search
@@ -23,7 +24,8 @@ constexpr size_t kMaxDynamicSmem = 227 * 1024;  // per CTA on sm_100
 
 #define LTLB200_DECLARE_WIDE(LW)                                                                                   \
     void wide2_launch_##LW(int kind, int op, const WideParams &P, int grid, size_t smem, int device, cudaStream_t st); \
-    int wide2_occupancy_##LW(int nvec, int device, int guide_smem_words);
+    int wide2_occupancy_##LW(int nvec, int device, int guide_smem_words);                                             \
+    void wide2_tiny_##LW(const WideTinyParams &T, int warps, size_t smem, int device, cudaStream_t st); /* several tiny levels in one launch */
 #define LTLB200_DECLARE_LW(LW)                                                                                     \
     void narrow_launch_##LW(int kind, int op, const NarrowParams &P, int grid, cudaStream_t st);                    \
     int narrow_occupancy_##LW();                                                                                    \

@@ -45,7 +45,16 @@ constexpr int W2_BATCH = LTLB200_W2_BATCH;  // candidates a lane carries through
 constexpr int W2_PREFETCH = LTLB200_W2_PREFETCH;  // vectors of a stored row fetched ahead of the full-row compare
 constexpr int W2_SC_VECS = 512;    // uint4 vectors of scalar-operand rows staged per warp (8 KiB)
 constexpr int W2_TERMS = 128;      // max scalar rows per tile
-enum : int { W2_PLAIN = 0, W2_GUARD = 1, W2_ROUTE = 2 };  // what a tile does with its candidates (wide2_batch / wide2_route_batch)
+// what a tile does with its candidates (wide2_batch / wide2_route_batch); W2_TINY = W2_PLAIN inside the kernel that
+// builds several levels per launch (wide2_tiny.cuh): the rows and the row directory it reads were written by that
+// very kernel, which rules out the read-only path
+enum : int { W2_PLAIN = 0, W2_GUARD = 1, W2_ROUTE = 2, W2_TINY = 3 };
+
+template <int MODE, typename T>
+__device__ __forceinline__ T w2_ld(const T *p) {
+    if constexpr (MODE == W2_TINY) return __ldcg(p);
+    else return __ldg(p);
+}
 
 struct __align__(16) Wide2Fixed {  // per-warp shared state behind the row areas
     u64 term[W2_TERMS];
@@ -374,10 +383,10 @@ __device__ __forceinline__ void wide2_unary_tile(const WideParams &P, const Wide
             live[r] = k + r < n_steps && i < n;
             ords[r] = ord0 + i;
             // a finalised row lives where it was staged (claim order): loc[id] is its place in the row log
-            rows[r] = B.from_atoms ? P.atoms + (live[r] ? i : 0) * nvec : P.store + __ldg(P.loc + B.a_off + (live[r] ? i : 0)) * nvec;
+            rows[r] = B.from_atoms ? P.atoms + (live[r] ? i : 0) * nvec : P.store + w2_ld<MODE>(P.loc + B.a_off + (live[r] ? i : 0)) * nvec;
         }
         auto gen = [&](int r, int p, uint4 &a, uint4 &b, uint4 &c) {
-            a = __ldg(rows[r] + p);
+            a = w2_ld<MODE>(rows[r] + p);
             b = a;
             c = cm_apply<LW, OP>(a, b, W.consts[p]);
         };
@@ -412,7 +421,7 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
     // stage the scalar rows (whole rows of nvec consecutive vectors) and their ordinal terms
     for (int t = lane; t < s_cnt * nvec; t += 32) {
         const int rrow = t / nvec, p = t - rrow * nvec;
-        W.sc[t] = __ldg(P.store + __ldg(sc_loc + s0 + rrow) * nvec + p);
+        W.sc[t] = w2_ld<MODE>(P.store + w2_ld<MODE>(sc_loc + s0 + rrow) * nvec + p);
     }
     for (int k = lane; k < s_cnt; k += 32) {
         const u64 s = s0 + k;
@@ -427,7 +436,7 @@ __device__ __forceinline__ void wide2_binary_tile(const WideParams &P, const Wid
         const int rows_here = (int)min((u64)32, n_vec - vbase);
         for (int t = lane; t < rows_here * nvec; t += 32) {
             const int rrow = t / nvec, p = t - rrow * nvec;
-            const uint4 x = __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p);
+            const uint4 x = w2_ld<MODE>(P.store + w2_ld<MODE>(vec_loc + vbase + rrow) * nvec + p);
             if constexpr (LW == LW_REGEX) {  // word q of row i at [q][i]: the concatenation tests single bits of a lane's row
                 uint32_t *vw = reinterpret_cast<uint32_t *>(W.vec) + rrow;
                 vw[(p * 4) * 32] = x.x;

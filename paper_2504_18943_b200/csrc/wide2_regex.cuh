@@ -98,10 +98,10 @@ __device__ __forceinline__ void wide2_regex_unary_tile(const WideParams &P, cons
         const u64 i = first + (u64)k * 32;
         const bool live[1] = {i < n};
         const u64 ords[1] = {ord0 + i};
-        const uint4 *row = B.from_atoms ? P.atoms + (live[0] ? i : 0) * nvec : P.store + __ldg(P.loc + B.a_off + (live[0] ? i : 0)) * nvec;
+        const uint4 *row = B.from_atoms ? P.atoms + (live[0] ? i : 0) * nvec : P.store + w2_ld<MODE>(P.loc + B.a_off + (live[0] ? i : 0)) * nvec;
         __syncwarp();
         for (int p = 0; p < nvec; ++p) {  // every lane its own row, word by word into its own bank
-            const uint4 x = __ldg(row + p);
+            const uint4 x = w2_ld<MODE>(row + p);
             ow[(p * 4) * 32] = x.x;
             ow[(p * 4 + 1) * 32] = x.y;
             ow[(p * 4 + 2) * 32] = x.z;
@@ -184,7 +184,7 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
     __syncwarp();
     for (int t = lane; t < s_cnt * nvec; t += 32) {
         const int rrow = t / nvec, p = t - rrow * nvec;
-        W.sc[t] = __ldg(P.store + __ldg(sc_loc + s0 + rrow) * nvec + p);
+        W.sc[t] = w2_ld<MODE>(P.store + w2_ld<MODE>(sc_loc + s0 + rrow) * nvec + p);
     }
 #pragma unroll 1
     for (uint32_t vg = 0; vg < vg_n; ++vg) {
@@ -195,7 +195,7 @@ __device__ __forceinline__ void wide2_regex_concat_tile(const WideParams &P, con
         const int rows_here = (int)min((u64)32, n_vec - vbase);
         for (int t = lane; t < 32 * nvec; t += 32) {  // (rows past the end of the level: zero)
             const int rrow = t / nvec, p = t - rrow * nvec;
-            const uint4 x = rrow < rows_here ? __ldg(P.store + __ldg(vec_loc + vbase + rrow) * nvec + p) : make_uint4(0, 0, 0, 0);
+            const uint4 x = rrow < rows_here ? w2_ld<MODE>(P.store + w2_ld<MODE>(vec_loc + vbase + rrow) * nvec + p) : make_uint4(0, 0, 0, 0);
             uint32_t *col = W.out + rrow;
             col[(p * 4) * 32] = x.x;
             col[(p * 4 + 1) * 32] = x.y;

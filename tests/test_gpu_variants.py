@@ -7,7 +7,9 @@ cases in a child process:
                         were read) instead of the deferred, device-bounded finalisation
   LTLB200_PRUNE=0       no associativity pruning: every AND candidate is probed
   LTLB200_TINY=0        every level through its own launches, instead of the tiny levels of a search built several
-                        per launch by narrow_tiny_levels_kernel (the default, which every other test therefore runs)
+                        per launch by narrow_tiny_levels_kernel / wide2_tiny_levels_kernel (the default, which every
+                        other test therefore runs)
+  LTLB200_WIDE_TINY_MAX=32768  multi-vector CMs: levels of up to 2^15 candidates (default 4096) in the one-CTA kernel
   LTLB200_OPSTREAMS=0   every operator launch of a level on the engine's own stream, one after the
                         other, instead of fanned out over side streams (the default)
 
@@ -41,7 +43,8 @@ print("variant ok")
 @pytest.mark.parametrize("switch,value,cases", [("LTLB200_NO_DEFER", "1", CASES + WIDE_CASES),
                                                  ("LTLB200_OPSTREAMS", "0", CASES + WIDE_CASES),
                                                  ("LTLB200_PRUNE", "0", CASES),
-                                                 ("LTLB200_TINY", "0", CASES + ["spec1_found_b1", "spec1_or_found", "c1_s0", "c1_s3", "w32n_s2_found", "w64n_s3_found"])])
+                                                 ("LTLB200_TINY", "0", CASES + WIDE_CASES + ["spec1_found_b1", "spec1_or_found", "c1_s0", "c1_s3", "w32n_s2_found", "w64n_s3_found"]),
+                                                 ("LTLB200_WIDE_TINY_MAX", "32768", WIDE_CASES)])
 def test_variant_matches_reference(switch, value, cases):
     env = dict(os.environ)
     env[switch] = value
@@ -61,7 +64,8 @@ print("variant ok")
 """
 
 
-@pytest.mark.parametrize("switch,value", [("LTLB200_GUIDE_SMEM", "1"), ("LTLB200_NO_DEFER", "1"), ("LTLB200_OPSTREAMS", "0")])
+@pytest.mark.parametrize("switch,value", [("LTLB200_GUIDE_SMEM", "1"), ("LTLB200_NO_DEFER", "1"), ("LTLB200_OPSTREAMS", "0"),
+                                          ("LTLB200_TINY", "0"), ("LTLB200_WIDE_TINY_MAX", "32768")])
 def test_regex_variant_matches_the_oracle(switch, value):
     """LTLB200_GUIDE_SMEM=1: the regex guide tables staged in the CTA's shared memory (off by default: it costs
     occupancy); and the regex tiles under the two scheduling switches above."""
