@@ -1798,7 +1798,20 @@ static bool tiny_enabled() {
     return on;
 }
 
-// multi-vector CMs: one CTA of eight warps beats the per-level launches only while a level is a few thousand candidates
+// One CTA beats the per-level launches only while a level is a few thousand candidates.  One-vector CMs: measured on
+// spec2 / c3 with 1024 / 2048 / 4096 / 8192 / 32768 candidates -- 6.03 / 6.03 / 6.03 / 6.03 / 6.12 ms and 2.33 / 2.28 /
+// 2.26 / 2.26 / 2.39 ms.  (A thread-block cluster of eight CTAs sharing CTA 0's counters and bitmap through distributed
+// shared memory was built for the levels in between, 4 K - 64 K candidates: parity green, level 8 of spec2 125 -> 58 us,
+// and still slower than handing those levels to the whole device -- spec2 6.09 ms, c3 2.54 ms; removed.)
+static u64 narrow_tiny_max_candidates() {
+    static const u64 n = [] {
+        const char *e = getenv("LTLB200_TINY_MAX");
+        return e ? (u64)atoll(e) : 4096ull;
+    }();
+    return std::min<u64>(n, TINY_MAX_CANDIDATES);
+}
+
+// multi-vector CMs: eight warps (LTLB200_WIDE_TINY_MAX)
 static u64 wide_tiny_max_candidates() {
     static const u64 n = [] {
         const char *e = getenv("LTLB200_WIDE_TINY_MAX");
@@ -1814,7 +1827,7 @@ bool Engine::tiny_eligible(int cost, uint32_t op_mask, bool exhaustive) {
     u64 constructed = 0, n_tiles = 0;
     plan_level(cost, op_mask, lv, constructed, n_tiles);
     const u64 slots = std::max<u64>(table_slots(), kMinSlots);
-    return constructed <= (wide_ ? wide_tiny_max_candidates() : (u64)TINY_MAX_CANDIDATES) && (int)lv.blocks.size() <= TINY_MAX_BLOCKS &&
+    return constructed <= (wide_ ? wide_tiny_max_candidates() : narrow_tiny_max_candidates()) && (int)lv.blocks.size() <= TINY_MAX_BLOCKS &&
            2 * (total_ + constructed) <= slots;
 }
 
@@ -1823,10 +1836,11 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     CUDA_CHECK(cudaSetDevice(device_));
     set_sharding(1, 0);
     if (wide_) return tiny_run_wide(cost, op_mask, exhaustive);
+    const u64 max_candidates = narrow_tiny_max_candidates();
+    const u64 claim_cap = max_candidates + (u64)TINY_WARPS * CLAIM_CHUNK + 1024;
+    const u64 growth = 4 * max_candidates;  // what one launch may add to the cache (the kernel stops before)
     try {
         if (table_dirty_) rebuild_table(table_slots());
-        const u64 claim_cap = (u64)TINY_MAX_CANDIDATES + (u64)TINY_WARPS * CLAIM_CHUNK + 1024;
-        const u64 growth = (u64)TINY_MAX_LEVELS * TINY_MAX_CANDIDATES;  // at most what the levels of one launch can store
         reserve(claim_key_, claim_cap, false);
         reserve(claim_ord_, claim_cap, false);
         reserve(store_, total_ + growth, true, total_);
@@ -1836,7 +1850,6 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     } catch (const MemoryBudget &) {
         return;  // (the usual path reports the memory budget)
     }
-    const u64 claim_cap = (u64)TINY_MAX_CANDIDATES + (u64)TINY_WARPS * CLAIM_CHUNK + 1024;
     std::vector<u64> tab(2 * 128, 0);
     for (size_t c = 1; c <= levels_.size(); ++c) {
         tab[2 * c] = levels_[c - 1].n;
@@ -1860,6 +1873,8 @@ void Engine::tiny_run(int cost, uint32_t op_mask, bool exhaustive) {
     T.results = reinterpret_cast<TinyLevelResult *>(tiny_results_.ptr);
     T.total = total_;
     T.table_slots = table_slots();
+    T.max_candidates = max_candidates;
+    T.store_cap = total_ + growth;
     T.op_mask = op_mask;
     T.n_atoms = n_atoms_;
     T.cost_first = cost;

@@ -34,6 +34,8 @@ struct TinyParams {
     TinyLevelResult *results;  // [cost - cost_first]
     u64 total;           // entries of the cache before cost_first
     u64 table_slots;
+    u64 max_candidates;  // a level beyond this is left to the launches that spread over the whole device
+    u64 store_cap;       // entries the cache arrays have room for
     uint32_t op_mask;
     int n_atoms, cost_first, cost_last, exhaustive;
     int weights[16];
@@ -115,8 +117,8 @@ __global__ void __launch_bounds__(TINY_THREADS, 1) narrow_tiny_levels_kernel(con
             tiny_plan(T.op_mask, T.n_atoms, T.weights, TINY_TILE_S, s_blocks, cost, s_tab, n_blocks, constructed, n_tiles);
             ctl.go = 1;
             // the host builds levels that are too big for one CTA, or for the set / the claim arrays as they are
-            if (constructed == ~0ull || constructed > TINY_MAX_CANDIDATES || 2 * (ctl.base + constructed) > T.table_slots ||
-                constructed + (u64)TINY_WARPS * CLAIM_CHUNK > T.P.claim_cap) {
+            if (constructed == ~0ull || constructed > T.max_candidates || 2 * (ctl.base + constructed) > T.table_slots ||
+                constructed + (u64)TINY_WARPS * CLAIM_CHUNK > T.P.claim_cap || ctl.base + constructed > T.store_cap) {
                 ctl.go = 0;
                 T.results[TINY_MAX_LEVELS].status = TINY_END_BIG;
             }
