@@ -452,7 +452,7 @@ def main() -> int:
         for name in EXTRA_WORKLOADS:
             _native.load().ltlb200_trim(local_rank)
             try:
-                a = device_arm(name, args.seed, local_rank, stream, 2, 1, single, torch.cuda.synchronize)
+                a = device_arm(name, args.seed, local_rank, stream, 2, 2, single, torch.cuda.synchronize)
             except Exception as err:  # noqa: BLE001  (a workload that does not fit this device is reported, not fatal)
                 extra[name] = {"error": str(err)[:200]}
                 continue
@@ -463,11 +463,11 @@ def main() -> int:
                            "max_cost_reached": a["stats"].max_cost_reached, "cm_bytes": a["after"]["row_bytes"],
                            "device_bytes": a["after"]["device_bytes"], "kernel_ms_per_step": kk["enum_ms"],
                            "finalize_ms_per_step": kk["fin_ms"], "tiny_levels_ms_per_step": kk["tiny_ms"],
-                           "roofline_frac": kk["frac"], "steps": 2, "warmup": 1}
+                           "roofline_frac": kk["frac"], "steps": 2, "warmup": 2}
         for name, max_cost in REGEX_WORKLOADS.items():
             _native.load().ltlb200_trim(local_rank)
             try:
-                extra[name] = regex_arm(name, max_cost, args.seed, local_rank, 2, 1)
+                extra[name] = regex_arm(name, max_cost, args.seed, local_rank, 2, 2)
             except Exception as err:  # noqa: BLE001
                 extra[name] = {"error": str(err)[:200]}
         _native.load().ltlb200_trim(local_rank)
