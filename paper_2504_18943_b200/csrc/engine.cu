@@ -212,6 +212,9 @@ struct StreamBundle {
     cudaEvent_t ev[4] = {};      // timing: enumerate begin/end, finalise begin/end
     cudaStream_t side[4] = {};   // operator fan-out (Engine::fan_*)
     cudaEvent_t fork = nullptr, join[4] = {};
+    cudaStream_t copy = nullptr;     // reads the level's counters while the last finalisation kernel still runs
+    cudaEvent_t summary = nullptr;   // the counters are final
+    cudaEvent_t fin[4] = {};         // finalisation begin / end, double-buffered (read one level late)
 };
 static std::mutex g_bundle_mu;
 static std::map<int, std::vector<StreamBundle>> g_bundles;
@@ -232,6 +235,9 @@ static StreamBundle bundle_get(int dev) {
     for (auto &st : b.side) CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CUDA_CHECK(cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming));
     for (auto &e : b.join) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&b.copy, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&b.summary, cudaEventDisableTiming));
+    for (auto &e : b.fin) CUDA_CHECK(cudaEventCreate(&e));
     return b;
 }
 
@@ -502,6 +508,10 @@ private:
     void plan_level(int cost, uint32_t op_mask, LevelMeta &lv, u64 &constructed, u64 &n_tiles);
     void rebuild_table(u64 slots);
     void read_counters();
+    void read_counters_early();
+    void collect_finalize_time(int slot, bool wait);
+    int fin_slot_ = 0;
+    bool fin_pending_[2] = {false, false};
     void decode(const LevelMeta &lv, u64 ord, int32_t *op, int64_t *left, int64_t *right) const;
     u64 constructed_through(const LevelMeta &lv, u64 sep_ord, u64 batch) const;
     void launch_enumerate(NarrowParams P, const LevelMeta &lv);
@@ -814,6 +824,31 @@ void Engine::read_counters() {
     CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     st_.d2h_bytes += CTR_COUNT * sizeof(u64);
+}
+
+// The counters of a level are final once level_summary_kernel has run; the kernel behind it (the scatter of the
+// winners' rows, or the row directory of the wide path) changes none of them.  Reading them from a second stream
+// that waits for the summary only lets the host plan and launch the next level while that kernel runs: the device
+// then goes from one level to the next without waiting for the host's turn-around (~30 us a level).  Everything the
+// host does to the cache afterwards is queued on stream_ and so stays ordered behind the scatter.
+void Engine::read_counters_early() {
+    CUDA_CHECK(cudaStreamWaitEvent(res_.copy, res_.summary, 0));
+    CUDA_CHECK(cudaMemcpyAsync(h_counters_, d_counters_, CTR_COUNT * sizeof(u64), cudaMemcpyDeviceToHost, res_.copy));
+    CUDA_CHECK(cudaStreamSynchronize(res_.copy));
+    st_.d2h_bytes += CTR_COUNT * sizeof(u64);
+}
+
+// finalisation time of a level whose last kernel was still running when the host moved on
+void Engine::collect_finalize_time(int slot, bool wait) {
+    if (!fin_pending_[slot]) return;
+    if (wait) CUDA_CHECK(cudaEventSynchronize(res_.fin[2 * slot + 1]));
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, res_.fin[2 * slot], res_.fin[2 * slot + 1]) == cudaSuccess) {
+        st_.finalize_ms += ms;
+        fin_pending_[slot] = false;
+    } else {
+        cudaGetLastError();
+    }
 }
 
 // Canonical block order of one level (reference engine.py:219-266 without the chunking).
@@ -1624,7 +1659,14 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
         if (wide_) reserve(loc_, total_ + pl.claim_cap, true, total_);  // (the rows are in the log already)
         else reserve(store_, (total_ + pl.claim_cap) * nvec_, true, total_ * nvec_);
         reserve(ords_, total_ + pl.claim_cap, true, total_);
-        CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
+        static const bool early_on = [] {  // LTLB200_EARLY_COUNTERS=0: one full synchronisation per level
+            const char *e = getenv("LTLB200_EARLY_COUNTERS");
+            return !(e && e[0] == '0');
+        }();
+        const bool early = early_on && !small;  // (a small level is one kernel: nothing to overlap)
+        const int slot = fin_slot_;
+        if (early) collect_finalize_time(slot, true);  // (two levels back: long finished)
+        CUDA_CHECK(cudaEventRecord(early ? res_.fin[2 * slot] : ev_[2], stream_));
         // the grids are sized by what the level can have claimed at most (its candidates, or the claim arrays)
         const u64 claim_bound = std::min(constructed + (u64)sm_count_ * occupancy_ * WARPS_PER_CTA * CLAIM_CHUNK * 8, pl.claim_cap);
         const int fgrid = (int)std::max<u64>(1, std::min<u64>((claim_bound + 255) / 256, (u64)sm_count_ * 16));
@@ -1651,6 +1693,7 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
                 CUDA_CHECK(cudaGetLastError());
                 launch_rank_scan(n_words, n_sb);
                 level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+                if (early) CUDA_CHECK(cudaEventRecord(res_.summary, stream_));
                 wide_rank_kernel<<<fgrid, 256, 0, stream_>>>(W);
                 CUDA_CHECK(cudaGetLastError());
                 st_.kernel_launches += 3;
@@ -1678,20 +1721,29 @@ int Engine::level_end_deferred(int64_t batch, u64 mem_budget, int64_t *n_new, in
                 CUDA_CHECK(cudaGetLastError());
                 launch_rank_scan(n_words, n_sb);
                 level_summary_kernel<<<1, 1, 0, stream_>>>(bitmap_.ptr, sb_rank_.ptr, n_bits, d_counters_);
+                if (early) CUDA_CHECK(cudaEventRecord(res_.summary, stream_));
                 narrow_scatter_kernel<<<fgrid, 256, 0, stream_>>>(F);
                 CUDA_CHECK(cudaGetLastError());
                 st_.kernel_launches += 3;
             }
         }
-        CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
+        CUDA_CHECK(cudaEventRecord(early ? res_.fin[2 * slot + 1] : ev_[3], stream_));
         PHASE(5, "end: reserve + launches", tp);
-        read_counters();
+        if (early) read_counters_early();
+        else read_counters();
         PHASE(6, "end: sync + read counters", tp);
         float ms = 0;
         CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
         st_.enumerate_ms += ms;
-        CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
-        st_.finalize_ms += ms;
+        if (early) {
+            fin_pending_[slot] = true;
+            collect_finalize_time(slot ^ 1, false);  // the previous level's: its last kernel ran before this level's first
+            fin_slot_ ^= 1;
+        } else {
+            CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+            st_.finalize_ms += ms;
+        }
+        // (blocks retired during this level were last touched by work queued before the summary kernel)
         recycle_retired(false);
         pl.active = false;
         if (h_counters_[CTR_OVERFLOW]) {  // the guess of new CMs was too small: nothing was finalised
@@ -2609,6 +2661,11 @@ int Engine::entry(int64_t gid, int32_t *op, int64_t *left, int64_t *right) {
 }
 
 void Engine::get_stats(ltlb200_stats *out) {
+    if (fin_pending_[0] || fin_pending_[1]) {
+        CUDA_CHECK(cudaSetDevice(device_));
+        collect_finalize_time(0, true);
+        collect_finalize_time(1, true);
+    }
     st_.table_slots = table_slots();
     st_.device_bytes = held_;
     *out = st_;

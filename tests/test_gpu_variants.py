@@ -10,6 +10,8 @@ cases in a child process:
                         per launch by narrow_tiny_levels_kernel / wide2_tiny_levels_kernel (the default, which every
                         other test therefore runs)
   LTLB200_TINY_MAX=32768 / LTLB200_WIDE_TINY_MAX=32768  levels of up to 2^15 candidates (default 4096) in the one-CTA kernels
+  LTLB200_EARLY_COUNTERS=0  the host waits for the whole finalisation of a level before it reads its counters (default:
+                        it reads them behind the summary kernel, while the scatter still runs)
   LTLB200_OPSTREAMS=0   every operator launch of a level on the engine's own stream, one after the
                         other, instead of fanned out over side streams (the default)
 
@@ -45,7 +47,8 @@ print("variant ok")
                                                  ("LTLB200_PRUNE", "0", CASES),
                                                  ("LTLB200_TINY", "0", CASES + WIDE_CASES + ["spec1_found_b1", "spec1_or_found", "c1_s0", "c1_s3", "w32n_s2_found", "w64n_s3_found"]),
                                                  ("LTLB200_WIDE_TINY_MAX", "32768", WIDE_CASES),
-                                                 ("LTLB200_TINY_MAX", "32768", CASES)])
+                                                 ("LTLB200_TINY_MAX", "32768", CASES),
+                                                 ("LTLB200_EARLY_COUNTERS", "0", CASES + WIDE_CASES)])
 def test_variant_matches_reference(switch, value, cases):
     env = dict(os.environ)
     env[switch] = value
