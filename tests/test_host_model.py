@@ -156,11 +156,12 @@ def test_naive_semantics_fixtures():
 
 
 def test_fast_witness_check_agrees_with_the_quantifier_semantics():
-    """semantics._truth_table_fast (expansion laws, one backward pass per node) == semantics._truth_table
-    (quantifiers of F and U written out) on random formulas over random traces."""
+    """semantics._truth_table_fast (expansion laws, one backward pass per node) and semantics._truth_mask (the same on
+    integer bit masks, doubling shifts) == semantics._truth_table (quantifiers of F and U written out) on random formulas
+    over random traces."""
     import random
 
-    from paper_2504_18943_b200.formulas import And, Future, Next, Not, Or, Until
+    from paper_2504_18943_b200.formulas import And, Future, Globally, Next, Not, Or, Until
     from paper_2504_18943_b200.traces import Trace
 
     rng = random.Random(0xF457)
@@ -168,21 +169,26 @@ def test_fast_witness_check_agrees_with_the_quantifier_semantics():
     def formula(depth):
         if depth == 0 or rng.random() < 0.2:
             return Atom(rng.randrange(3))
-        kind = rng.choice(("not", "next", "future", "and", "or", "until"))
+        kind = rng.choice(("not", "next", "future", "globally", "and", "or", "until"))
         if kind == "not":
             return Not(formula(depth - 1))
         if kind == "next":
             return Next(formula(depth - 1))
         if kind == "future":
             return Future(formula(depth - 1))
+        if kind == "globally":
+            return Globally(formula(depth - 1))
         node = {"and": And, "or": Or, "until": Until}[kind]
         return node(formula(depth - 1), formula(depth - 1))
 
-    for _ in range(300):
-        length = rng.randint(1, 9)
+    for _ in range(400):
+        length = rng.randint(1, 19)
         tr = Trace(tuple(frozenset(p for p in range(3) if rng.random() < 0.5) for _ in range(length)))
         f = formula(rng.randint(1, 5))
-        assert semantics._truth_table_fast(tr, f) == semantics._truth_table(tr, f), (tr, f)
+        want = semantics._truth_table(tr, f)
+        assert semantics._truth_table_fast(tr, f) == want, (tr, f)
+        mask = semantics._truth_mask(tr, f, {})  # the integer tables separates_by_sat evaluates
+        assert [bool(mask >> i & 1) for i in range(length)] == want and mask >> length == 0, (tr, f)
 
 
 def test_bench_gpus_flag_starts_that_many_ranks():
