@@ -738,7 +738,9 @@ Engine::~Engine() {
 // memset queues behind the persistent enumerate CTAs.  Launched two or three levels early -- the size of the next
 // set is predictable: grown_size of twice the current one -- it does run in the background and the regrows of
 // `spec2` drop from 0.68 to 0.31 ms, but the search does not get faster (6.06 -> 6.09 ms): the device is busy 92 % of
-// the time, so the 2.5 GB of stores only move into the enumerate launches they overlap.)
+// the time, so the 2.5 GB of stores only move into the enumerate launches they overlap.  Cleared by copy-engine
+// copies of a pattern instead of a memset kernel it overlaps too, and costs more than it hides: 5.91 -> 6.19 ms, the
+// random probes and the scatter slow down beside 4 GB of streaming traffic.)
 u64 Engine::grown_size(u64 want_slots) const {
     const u64 slot_bytes = wide_ ? sizeof(u64) : sizeof(Slot16);
     const u64 want_bytes = want_slots * slot_bytes;
