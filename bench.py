@@ -266,6 +266,13 @@ def free_port() -> int:
 
 def respawn_under_torchrun(args) -> int:
     """`bench.py --gpus N` outside torchrun: start the N ranks here (one process per GPU) and pass their output on."""
+    if not getattr(args, "selftest_cpu", False):
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:  # say so in the line's own format instead of N tracebacks from the ranks
+            print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error": f"--gpus {args.gpus} needs {args.gpus} CUDA devices, this box has {have}"}))
+            return 1
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(ROOT / "bench.py"), *sys.argv[1:]]
     env = dict(os.environ)
