@@ -2418,17 +2418,26 @@ void Engine::winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void *
     reserve(xs_rows_, std::max<u64>(n, 1) * nvec_, false);
     reserve(xs_ords_, std::max<u64>(n, 1), false);
     CUDA_CHECK(cudaMemsetAsync(xchg_.ptr, 0, sizeof(u64), stream_));
+    CUDA_CHECK(cudaEventRecord(ev_[2], stream_));
     if (n) {
+        // the winners leave in ordinal order: their places are the ranks of their ordinals among this owner's own marks
+        // (the bitmap is still the owner's: the ranks all-reduce it after this call, and level_commit ranks it again)
+        const u64 n_words = (pl.constructed + 31) / 32, n_sb = (n_words + 31) / 32;
+        launch_rank_scan(n_words, n_sb);
         const int grid = (int)std::max<u64>(1, std::min<u64>((n + 255) / 256, (u64)sm_count_ * 8));
-        if (wide_) wide_winners_kernel<<<grid, 256, 0, stream_>>>(store_.ptr + log_tail_ * nvec_, stage_ord_.ptr, n, nvec_, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
-        else narrow_winners_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, limit, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
+        if (wide_) wide_winners_kernel<<<grid, 256, 0, stream_>>>(store_.ptr + log_tail_ * nvec_, stage_ord_.ptr, n, nvec_, limit, bitmap_.ptr, sb_rank_.ptr, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
+        else narrow_winners_kernel<<<grid, 256, 0, stream_>>>(claim_key_.ptr, claim_ord_.ptr, n, limit, bitmap_.ptr, sb_rank_.ptr, xchg_.ptr, xs_rows_.ptr, xs_ords_.ptr);
         CUDA_CHECK(cudaGetLastError());
         st_.kernel_launches++;
     }
+    CUDA_CHECK(cudaEventRecord(ev_[3], stream_));
     u64 count = 0;
     CUDA_CHECK(cudaMemcpyAsync(&count, xchg_.ptr, sizeof(u64), cudaMemcpyDeviceToHost, stream_));
     CUDA_CHECK(cudaStreamSynchronize(stream_));
     st_.d2h_bytes += sizeof(u64);
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+    st_.finalize_ms += ms;  // (publishing the winners is part of finalising a sharded level)
     pl.n_winners = count;
     *n_winners = count;
     *rows_dev = xs_rows_.ptr;

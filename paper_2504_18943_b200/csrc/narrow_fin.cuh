@@ -160,10 +160,15 @@ __global__ void __launch_bounds__(256) narrow_rebuild_kernel(Slot16 *slots, u64 
 
 // ---- sharded search: what an owner publishes, and what every rank appends to its cache ----------------------
 
-// Compacts this owner's winners (claims whose smallest ordinal is <= ord_limit) into dense record arrays;
-// cursor[0] = how many.  The order is irrelevant: the receiver places every record by the rank of its ordinal.
+// This owner's winners (claims whose smallest ordinal is <= ord_limit) as dense record arrays IN ORDINAL ORDER;
+// cursor[0] = how many.  `bitmap` / `sb_rank` are the owner's OWN marks, ranked (before the ranks all-reduce the
+// bitmap): the rank of a winner's ordinal among them is its place in the export -- the winners up to a separator are
+// a prefix of that order, so the places are dense.  Sorting here costs the owner one random store per winner it
+// publishes (u C / N of them); it saves every receiver the random placement of everything it receives: records
+// that arrive in ordinal order go to ascending ids (narrow_scatter_records_kernel).
 __global__ void __launch_bounds__(256) narrow_winners_kernel(const uint4 *claim_key, const u64 *claim_ord, u64 n_claimed,
-                                                             u64 ord_limit, u64 *cursor, uint4 *rows_out, u64 *ords_out) {
+                                                             u64 ord_limit, const uint32_t *bitmap, const uint32_t *sb_rank,
+                                                             u64 *cursor, uint4 *rows_out, u64 *ords_out) {
     const int lane = threadIdx.x & 31;
     const u64 n_round = (n_claimed + 31) & ~31ull;  // whole warps stay in the loop for the ballot
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_round; t += (u64)gridDim.x * blockDim.x) {
@@ -171,11 +176,9 @@ __global__ void __launch_bounds__(256) narrow_winners_kernel(const uint4 *claim_
         const bool keep = ord != VAL_EMPTY && ord <= ord_limit;
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
         if (m == 0u) continue;
-        u64 base = 0;
-        if (lane == 0) base = atomicAdd(cursor, (u64)__popc(m));
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (lane == 0) atomicAdd(cursor, (u64)__popc(m));
         if (keep) {
-            const u64 pos = base + __popc(m & ((1u << lane) - 1u));
+            const u64 pos = ordinal_rank(bitmap, sb_rank, ord);
             rows_out[pos] = claim_key[t];
             ords_out[pos] = ord;
         }
@@ -183,11 +186,10 @@ __global__ void __launch_bounds__(256) narrow_winners_kernel(const uint4 *claim_
 }
 
 // Where the records of the other owners sit in the receive buffers: source s sent counts[s] records starting at
-// record offsets[s].  The sources are walked in step (record i of source 0, of source 1, ...).  Measured on c3 to
-// cost 15 with 8 ranks played on one GPU (tools/shard_model.py): it does NOT make the scatter cheaper than walking
-// one source after the other (4.2 vs 4.3 ms for 54.6 M received records) -- an owner's winners are not in ordinal
-// order, so the two 8/16-byte stores per record stay random; what would help is publishing the winners bucketed
-// by ordinal range ("what limits the scaling").
+// record offsets[s], each source's in ordinal order.  The sources are walked in step (record i of source 0, of source
+// 1, ...): the i-th winners of all owners have neighbouring ordinals (owners are hash classes), so a warp's stores go
+// to one neighbourhood of ids.  (With unordered records -- the first version -- the walk order made no difference:
+// 4.2 vs 4.3 ms for the 54.6 M records a rank of eight receives on c3 to cost 15; tools/shard_model.py.)
 struct RecordSources {
     unsigned long long offsets[8], counts[8];
     unsigned long long longest;  // max of counts

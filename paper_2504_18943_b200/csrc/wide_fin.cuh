@@ -105,10 +105,12 @@ __global__ void __launch_bounds__(256) wide_gather_kernel(const uint4 *store, co
 
 // ---- sharded search: what an owner publishes, what every rank appends, what an owner folds in ---------------
 
-// Compacts this owner's winners (staging entries whose smallest ordinal is <= ord_limit) into dense record
-// arrays; cursor[0] = how many.  One warp per 32 entries: positions by ballot, rows copied vector by vector.
+// This owner's winners (staging entries whose smallest ordinal is <= ord_limit) as dense record arrays in ordinal
+// order (see narrow_winners_kernel: the place of a winner is the rank of its ordinal among the owner's own marks);
+// cursor[0] = how many.  Rows copied vector by vector.
 __global__ void __launch_bounds__(256) wide_winners_kernel(const uint4 *stage_rows, const u64 *stage_ord, u64 n_staged, int nvec,
-                                                           u64 ord_limit, u64 *cursor, uint4 *rows_out, u64 *ords_out) {
+                                                           u64 ord_limit, const uint32_t *bitmap, const uint32_t *sb_rank, u64 *cursor,
+                                                           uint4 *rows_out, u64 *ords_out) {
     const int lane = threadIdx.x & 31;
     const u64 n_round = (n_staged + 31) & ~31ull;
     for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n_round; t += (u64)gridDim.x * blockDim.x) {
@@ -116,11 +118,9 @@ __global__ void __launch_bounds__(256) wide_winners_kernel(const uint4 *stage_ro
         const bool keep = ord != VAL_EMPTY && ord <= ord_limit;
         const uint32_t m = __ballot_sync(0xFFFFFFFFu, keep);
         if (m == 0u) continue;
-        u64 base = 0;
-        if (lane == 0) base = atomicAdd(cursor, (u64)__popc(m));
-        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        if (lane == 0) atomicAdd(cursor, (u64)__popc(m));
         if (keep) {
-            const u64 pos = base + __popc(m & ((1u << lane) - 1u));
+            const u64 pos = ordinal_rank(bitmap, sb_rank, ord);
             for (int p = 0; p < nvec; ++p) rows_out[pos * nvec + p] = stage_rows[t * nvec + p];
             ords_out[pos] = ord;
         }
