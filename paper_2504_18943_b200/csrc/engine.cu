@@ -2337,7 +2337,7 @@ int Engine::owner_reduce(u64 n_records, u64 *n_claimed_out, void **bitmap_dev, u
                 P.sep_list_cap = 0;
                 P.prune_after_sep = 0;
                 const u64 steps = (n_records + 32 * PROBE_BATCH - 1) / (32 * PROBE_BATCH);
-                const int grid = (int)std::max<u64>(1, std::min<u64>((steps + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * occupancy_));
+                const int grid = (int)std::max<u64>(1, std::min<u64>((steps + WARPS_PER_CTA - 1) / WARPS_PER_CTA, (u64)sm_count_ * LTLB200_PROBE_CTAS));
                 switch (lw_) {
                     case 8: narrow_probe_8(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;
                     case 16: narrow_probe_16(P, xr_rows_.ptr, xr_ords_.ptr, n_records, grid, stream_); break;

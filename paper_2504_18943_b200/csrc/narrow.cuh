@@ -895,10 +895,13 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_route_ke
     }
 }
 
+#ifndef LTLB200_PROBE_CTAS
+#define LTLB200_PROBE_CTAS 3  // (3 / 4 / 5 CTAs per SM: 4.83 / 5.13 / 5.82 ms on c3 to cost 15 with two ranks)
+#endif
 // Phase B on the owner: insert-or-min of `n` received records, PROBE_BATCH coalesced records per lane and step
 // through the same insert_batch / drain_round as the single-GPU kernel.
 template <int LW>
-__global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_probe_kernel(const NarrowParams P, const uint4 *rows,
+__global__ void __launch_bounds__(CTA_THREADS, LTLB200_PROBE_CTAS) narrow_probe_kernel(const NarrowParams P, const uint4 *rows,
                                                                                     const u64 *ords, u64 n) {
     __shared__ WarpShared s_warp[WARPS_PER_CTA];
     WarpShared &ws = s_warp[threadIdx.x >> 5];
@@ -906,21 +909,36 @@ __global__ void __launch_bounds__(CTA_THREADS, LTLB200_MIN_CTAS) narrow_probe_ke
     const int lane = threadIdx.x & 31;
     const u64 warp = (u64)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5), n_warps = (u64)gridDim.x * WARPS_PER_CTA;
     constexpr u64 STEP = 32ull * PROBE_BATCH;
-#pragma unroll 1
-    for (u64 base = warp * STEP; base < n; base += n_warps * STEP) {
-        if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] != 0ull) break;
-        uint4 cand[PROBE_BATCH];
-        u64 o[PROBE_BATCH];
-        bool live[PROBE_BATCH], known[PROBE_BATCH];
+    // the records of the next step are fetched before the current ones are probed (a step is two dependent trips to
+    // memory otherwise: the records, then their slots), and the overflow flag is looked at every eighth step
+    uint4 cand[PROBE_BATCH];
+    u64 o[PROBE_BATCH];
+    auto fetch = [&](u64 base) {
 #pragma unroll
         for (int r = 0; r < PROBE_BATCH; ++r) {
             const u64 i = base + (u64)r * 32 + lane;
-            live[r] = i < n;
-            known[r] = false;
-            cand[r] = live[r] ? __ldcs(rows + i) : make_uint4(0, 0, 0, 0);
-            o[r] = live[r] ? __ldcs(ords + i) : 0ull;
+            cand[r] = i < n ? __ldcs(rows + i) : make_uint4(0, 0, 0, 0);
+            o[r] = i < n ? __ldcs(ords + i) : 0ull;
         }
-        insert_batch<LW>(P, ws.queue, st, cand, live, known, [&](int r) { return o[r]; });
+    };
+    u64 base = warp * STEP;
+    if (base < n) fetch(base);
+    uint32_t step = 0;
+#pragma unroll 1
+    for (; base < n; base += n_warps * STEP, ++step) {
+        if ((step & 7u) == 0u && *(volatile u64 *)&P.counters[CTR_OVERFLOW] != 0ull) break;
+        uint4 cur[PROBE_BATCH];
+        u64 cur_o[PROBE_BATCH];
+        bool live[PROBE_BATCH], known[PROBE_BATCH];
+#pragma unroll
+        for (int r = 0; r < PROBE_BATCH; ++r) {
+            cur[r] = cand[r];
+            cur_o[r] = o[r];
+            live[r] = base + (u64)r * 32 + lane < n;
+            known[r] = false;
+        }
+        if (base + n_warps * STEP < n) fetch(base + n_warps * STEP);
+        insert_batch<LW>(P, ws.queue, st, cur, live, known, [&](int r) { return cur_o[r]; });
     }
     if (*(volatile u64 *)&P.counters[CTR_OVERFLOW] == 0ull)
         while (st.qfill > 0u) drain_round(P, ws.queue, st);
