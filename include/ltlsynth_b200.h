@@ -189,7 +189,7 @@ int ltlb200_expand_level(ltlb200_engine *e, int32_t cost, uint32_t op_mask, int3
  *                           whole level; *bitmap_words 32-bit words at *bitmap_dev)
  *   [all-reduce SUM]        of the bitmaps (the owners' bits are disjoint, so the sum is the union); min of the
  *                           separator ordinal
- *   ltlb200_winners_export  this owner's winners with ordinal <= sep_ord, as dense records
+ *   ltlb200_winners_export  this owner's winners with ordinal <= sep_ord, as dense records in ordinal order
  *   [all-gather]            every rank receives the winners of the OTHER owners (ltlb200_exchange_recv again)
  *   ltlb200_level_commit    ids from the global bitmap; own winners and the received records appended to the
  *                           cache (recv_counts[k], k < n_sources <= 8: how many records each source sent, in the

@@ -2125,7 +2125,8 @@ void Engine::discard_lookahead() {
 //   owner_reduce   insert-or-min of the received records into the owned part of the set (phase B); marks the
 //                  ordinals of this owner's winners in the level's bitmap
 //   [all-reduce]   the caller sums the bitmaps (disjoint bits: a sum is the union); min of the separator
-//   winners_export this owner's winners up to the separator as dense records
+//   winners_export this owner's winners up to the separator as dense records, in ordinal order (so that what the
+//                  other ranks receive goes to ascending ids)
 //   [all-gather]   every rank receives the winners of the others (exchange_recv again)
 //   level_commit   ranks of the global bitmap -> ids; own winners and received records appended to the cache
 //
@@ -2407,7 +2408,7 @@ void Engine::level_abort() {
     levels_.push_back(LevelMeta{0, total_, {}});
 }
 
-// this owner's winners with an ordinal <= the level's separator (all of them in an exhaustive run), dense
+// this owner's winners with an ordinal <= the level's separator (all of them in an exhaustive run), dense, in ordinal order
 void Engine::winners_export(u64 sep_ord, u64 *n_winners, void **rows_dev, void **ords_dev) {
     PendingLevel &pl = pending_;
     if (!pl.active || !pl.reduced) throw std::invalid_argument("winners_export needs owner_reduce first");
